@@ -1,0 +1,123 @@
+"""Calibration (PCA basis) — oracle (test infrastructure).
+
+Paper: "we forward all sequences ... collect their KV caches. For
+each sequence, cache entries are concatenated along the time dimension to form
+a global pool of positions. We then sample n token positions from this pool,
+excluding attention sinks.  For each sampled position, we take the
+corresponding keys (and, equivalently, values) from l layers and h heads, undo
+positional rotations, and concatenate them ... C in R^{n x p} with p = l h
+d_head ... Let mu be the per-feature mean of C. We compute the SVD of the
+centered matrix C - mu = U Sigma V^T with singular values ... sorted in
+descending order (equivalently, PCA of C)."  V is truncated to r < p
+(cap 10K) and "stored in 16bit precision".
+
+Oracle algorithm: the sample positions are an INPUT (random numbers the method
+draws are passed in); rows are gathered in (layer, head, dim) feature order,
+keys through R1 (oracle.rope.unrope_r1); mu = column mean; Sigma =
+(C-mu)^T (C-mu) in fp64; eigh (the symmetric eigendecomposition equals the
+right singular vectors of C - mu); descending order; canonical sign (Q13: the
+largest-|entry| component of each column is positive); r = min(cap, n-1, p).
+The artifact master is fp32 (mu, V); the GEMM operands are RNE copies of the
+master: V_c = bf16(V) for compression (X is bf16), V_d = fp16(V) for
+decompression (R2, R6).
+
+Pins (tests/test_oracle_pca.py): V^T V = I; eigenvalues == squared singular
+values from np.linalg.svd (library routine); planted rank-k data gives exactly
+k non-zero sigma; full-rank project -> reconstruct is the identity;
+truncation error == sum of discarded squared coefficients.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .numerics import bf16, f16, f32
+from .rope import unrope_r1
+
+
+@dataclass
+class Basis:
+    mu: np.ndarray        # [p]   fp32 master (held in fp64)
+    V: np.ndarray         # [p, r] fp32 master
+    sigma: np.ndarray     # [r]
+    n: int
+
+    @property
+    def p(self) -> int:
+        return self.V.shape[0]
+
+    @property
+    def r(self) -> int:
+        return self.V.shape[1]
+
+    @property
+    def Vc(self) -> np.ndarray:
+        """bf16 compress operand (R2)."""
+        return bf16(self.V)
+
+    @property
+    def Vd(self) -> np.ndarray:
+        """fp16 decompress operand (R6)."""
+        return f16(self.V)
+
+
+def flatten_rows(kv) -> np.ndarray:
+    """[l, t, h, d] -> [t, l*h*d] with features in (layer, head, dim) order."""
+    kv = np.asarray(kv, dtype=np.float64)
+    l, t, h, d = kv.shape
+    return np.transpose(kv, (1, 0, 2, 3)).reshape(t, l * h * d)
+
+
+def gather(caches, samples, is_keys: bool, invf=None, pairing: int = 0) -> np.ndarray:
+    """Calibration matrix C [n, p].
+
+    caches: list of (kv [l, t, h, d] bf16 values as fp64, pos0); samples: int
+    array [n, 2] of (sequence index, token index).  Keys are un-RoPE'd at their
+    absolute positions through R1."""
+    rows = []
+    for seq, tok in np.asarray(samples, dtype=np.int64):
+        kv, pos0 = caches[int(seq)]
+        x = np.asarray(kv, dtype=np.float64)[:, int(tok):int(tok) + 1]   # [l, 1, h, d]
+        if is_keys:
+            x = unrope_r1(x, [pos0 + int(tok)], invf, pairing)
+        rows.append(flatten_rows(x)[0])
+    return np.stack(rows, axis=0)
+
+
+def fit(C, rank_cap: int) -> Basis:
+    C = np.asarray(C, dtype=np.float64)
+    n, p = C.shape
+    mu = C.mean(axis=0)
+    Xc = C - mu
+    S = Xc.T @ Xc
+    w, V = np.linalg.eigh(S)
+    order = np.argsort(-w, kind="stable")
+    w = w[order]
+    V = V[:, order]
+    r = min(rank_cap, max(n - 1, 1), p)
+    w = w[:r]
+    V = V[:, :r]
+    idx = np.argmax(np.abs(V), axis=0)
+    sgn = np.sign(V[idx, np.arange(r)])
+    sgn[sgn == 0] = 1.0
+    V = V * sgn
+    return Basis(mu=f32(mu), V=f32(V), sigma=np.sqrt(np.maximum(w, 0.0)), n=n)
+
+
+def project(basis: Basis, X, cols=None) -> np.ndarray:
+    """D = X V_c - mu V_c in fp64 (= (X - mu) V_c, R2)."""
+    Vc = basis.Vc if cols is None else basis.Vc[:, cols]
+    X = np.asarray(X, dtype=np.float64)
+    return X @ Vc - (basis.mu @ Vc)[None, :]
+
+
+def reconstruct(basis: Basis, Dh, cols=None) -> np.ndarray:
+    """X^ = D^ V_d^T + mu in fp64 (R6)."""
+    Vd = basis.Vd if cols is None else basis.Vd[:, cols]
+    return np.asarray(Dh, dtype=np.float64) @ Vd.T + basis.mu[None, :]
+
+
+def dp_coefficients(basis: Basis, C, row_cap: int = 32768) -> np.ndarray:
+    """P for the DP: (C_dp - mu) V_c on the first <= 32K rows (Q8)."""
+    return project(basis, np.asarray(C)[:row_cap])
