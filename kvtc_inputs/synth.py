@@ -84,8 +84,9 @@ SHAPES = {
 }
 
 
-def make_spec(name: str, **over) -> SynthSpec:
-    return replace(SHAPES[name], **over) if over else SHAPES[name]
+def make_spec(base: str, **over) -> SynthSpec:
+    """A named shape, optionally with fields overridden (e.g. name=..., layers=...)."""
+    return replace(SHAPES[base], **over) if over else SHAPES[base]
 
 
 _MODEL_CACHE: dict = {}

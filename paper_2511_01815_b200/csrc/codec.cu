@@ -1,0 +1,559 @@
+// codec.cu — stage entry points and the compress / decompress orchestration
+// with the container format of DESIGN.md §4.
+#include <cstring>
+
+#include "api_internal.h"
+
+using namespace kvtc;
+
+namespace {
+
+constexpr uint32_t kContainerMagic = 0x4354564Bu;  // "KVTC"
+constexpr uint32_t kContainerVersion = 1;
+
+struct ContainerHeader {
+  uint32_t magic, version;
+  int32_t layers, kv_heads, head_dim, sinks, window, chunk_bytes;
+  int64_t tokens, pos0, m;
+  uint64_t total_bytes, raw_bytes;
+  uint64_t payload_bytes[2], entropy_bytes[2];
+  uint64_t basis_fp[2], plan_fp[2];
+  uint64_t raw_off, section_off[2];
+  uint8_t pad[256 - 160];
+};
+static_assert(sizeof(ContainerHeader) == KVTC_HEADER_BYTES, "container header size");
+
+__global__ void header_kernel(ContainerHeader h, uint8_t *out, const uint64_t *lens, uint64_t *offs) {
+  // offs[0] = K section offset (host-known), offs[1] = V section offset (= after K)
+  if (lens) {
+    h.entropy_bytes[0] = lens[0];
+    h.entropy_bytes[1] = lens[1];
+    h.section_off[1] = offs[1];
+    h.total_bytes = offs[1] + lens[1];
+  }
+  *reinterpret_cast<ContainerHeader *>(out) = h;
+}
+__global__ void offset_after_kernel(const uint64_t *off, const uint64_t *len, uint64_t *next) {
+  *next = *off + ((*len + 15) & ~15ull);
+}
+
+inline uint64_t align16(uint64_t x) { return (x + 15) & ~15ull; }
+
+// R1/R7 cos/sin table for tokens [tok_begin, tok_begin + m) of a view.
+kvtc_status rope_table_for(const kvtc_basis *b, int64_t pos_first, int64_t m, float2 *cs, cudaStream_t st) {
+  return launch_rope_table(b->d_invf, b->shape.head_dim / 2, pos_first, m, cs, st);
+}
+
+kvtc_status tmap_X(CUtensorMap *m, const void *X, int64_t rows, int64_t p) {
+  return make_tmap_2d(m, X, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, uint64_t(p), uint64_t(rows), uint64_t(p) * 2, kBlockK,
+                      kTileM);
+}
+
+kvtc_status run_project_quant(const kvtc_basis *b, kvtc_plan *pl, const Operands *op, const void *X, int64_t m,
+                              uint8_t *payload, cudaStream_t st) {
+  if (m == 0 || pl->G == 0) return KVTC_OK;
+  CUtensorMap tA;
+  kvtc_status s = tmap_X(&tA, X, m, b->p);
+  if (s) return s;
+  GemmCompressArgs a = {};
+  a.tmA = &tA;
+  a.tmB = &op->tm_VcT;
+  a.K = b->p;
+  a.m = m;
+  a.bias = op->bias;
+  a.payload = payload;
+  a.G = pl->G;
+  a.tile_bytes = pl->tile_bytes;
+  a.codes_off_last = plan_codes_off_last(pl, m % kTileM);
+  a.groups = pl->d_gdesc;
+  for (const SegLaunch &L : pl->launches) {
+    if (L.nseg == 0) continue;
+    a.segs = pl->d_segs + L.seg_begin;
+    a.nsegs = L.nseg;
+    a.parts = L.parts;
+    if ((s = launch_gemm_project_quant(a, st))) return s;
+  }
+  return KVTC_OK;
+}
+
+kvtc_status run_reconstruct(const kvtc_basis *b, const kvtc_plan *pl, const Operands *op, const __half *Dh,
+                            int64_t ld, int64_t m, int64_t tok_begin, int32_t lb, int32_t le, const kvtc_kv_view *out,
+                            __nv_bfloat16 *const *bases_dev, const float2 *cs, cudaStream_t st) {
+  const int hd = b->shape.kv_heads * b->shape.head_dim;
+  if (m == 0 || lb >= le) return KVTC_OK;
+  GemmDecompressArgs a = {};
+  CUtensorMap tA;
+  // with an empty plan D^ has no columns: use a 1-column zero view (K = 0 -> only mu)
+  const int64_t kcols = std::max<int64_t>(pl->r_nz, 1);
+  kvtc_status s = make_tmap_2d(&tA, Dh, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, uint64_t(kcols), uint64_t(m),
+                               uint64_t(ld) * 2, kBlockK, kTileM);
+  if (s) return s;
+  a.tmA = &tA;
+  a.tmB = pl->r_nz ? &op->tm_Vd : &tA;
+  a.K = pl->r_nz;
+  a.m = m;
+  a.n_begin = lb * hd;
+  a.n_end = le * hd;
+  a.mu = b->d_mu;
+  a.cs = b->has_rope ? cs : nullptr;
+  a.layers = b->shape.layers;
+  a.heads = b->shape.kv_heads;
+  a.head_dim = b->shape.head_dim;
+  a.pairing = b->pairing;
+  a.layout = out->layout;
+  a.page_tokens = out->page_tokens;
+  a.layer_base = bases_dev;
+  a.block_table = out->block_table;
+  a.tok_begin = tok_begin;
+  int tile = kMaxTileN;
+  while (hd % tile) tile /= 2;
+  a.tile_n = tile;
+  return launch_gemm_reconstruct(a, st);
+}
+
+bool same_shape(const kvtc_shape &a, const kvtc_shape &b) {
+  return a.layers == b.layers && a.kv_heads == b.kv_heads && a.head_dim == b.head_dim;
+}
+
+}  // namespace
+
+// ============================================================ stage entry points
+extern "C" kvtc_status kvtc_stage_project(const kvtc_basis *b, const kvtc_plan *plan, const void *X, int64_t m,
+                                          float *D, void *stream) {
+  KVTC_CHECK_ARG(b && X && D && m >= 0, "project arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (m == 0) return KVTC_OK;
+  CUtensorMap tA, tB;
+  kvtc_status s = tmap_X(&tA, X, m, b->p);
+  if (s) return s;
+  GemmCompressArgs a = {};
+  a.tmA = &tA;
+  a.K = b->p;
+  a.m = m;
+  a.D = D;
+  int32_t ncols;
+  if (plan) {
+    const Operands *op;
+    if ((s = plan_operands(b, const_cast<kvtc_plan *>(plan), &op))) return s;
+    if (op->r_nz == 0) return KVTC_OK;
+    a.tmB = &op->tm_VcT;
+    a.bias = op->bias;
+    ncols = op->r_nz;
+  } else {
+    if ((s = make_tmap_2d(&tB, b->d_VcT, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, b->p, b->r, uint64_t(b->p) * 2, kBlockK,
+                          kMaxTileN)))
+      return s;
+    a.tmB = &tB;
+    a.bias = b->d_bias;
+    ncols = b->r;
+  }
+  a.ldd = ncols;
+  return launch_gemm_project_f32(a, ncols, st);
+}
+
+extern "C" kvtc_status kvtc_stage_quantize_pack(const kvtc_plan *plan, const float *D, int64_t m, uint8_t *payload,
+                                                void *stream) {
+  KVTC_CHECK_ARG(plan && D && payload && m >= 0, "quantize_pack arguments");
+  auto *pl = const_cast<kvtc_plan *>(plan);
+  return launch_quant_pack_simt(pl->d_segs, pl->d_gdesc, pl->nsegs, pl->G, D, pl->r_nz, m, pl->tile_bytes,
+                                plan_codes_off_last(pl, m % kTileM), payload, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" kvtc_status kvtc_stage_project_quantize(const kvtc_basis *b, const kvtc_plan *plan, const void *X,
+                                                   int64_t m, uint8_t *payload, void *stream) {
+  KVTC_CHECK_ARG(b && plan && X && payload && m >= 0, "project_quantize arguments");
+  auto *pl = const_cast<kvtc_plan *>(plan);
+  const Operands *op;
+  kvtc_status s = plan_operands(b, pl, &op);
+  if (s) return s;
+  return run_project_quant(b, pl, op, X, m, payload, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" size_t kvtc_deflate_bound(size_t n, int32_t chunk_bytes) { return deflate_section_bound(n, chunk_bytes); }
+extern "C" size_t kvtc_deflate_workspace_bytes(size_t n, int32_t chunk_bytes) {
+  return deflate_workspace(n, chunk_bytes) + 256;
+}
+
+extern "C" kvtc_status kvtc_stage_deflate(const uint8_t *in, size_t n, int32_t chunk_bytes, uint8_t *out,
+                                          size_t out_cap, size_t *out_len_host, void *workspace,
+                                          size_t workspace_bytes, void *stream) {
+  KVTC_CHECK_ARG(in && out && workspace, "deflate arguments");
+  KVTC_CHECK_ARG(out_cap >= deflate_section_bound(n, chunk_bytes), "deflate output capacity");
+  KVTC_CHECK_ARG(workspace_bytes >= kvtc_deflate_workspace_bytes(n, chunk_bytes), "deflate workspace");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Bump ws(workspace, workspace_bytes);
+  uint64_t *len = ws.take<uint64_t>(1);
+  void *rest = ws.take<uint8_t>(deflate_workspace(n, chunk_bytes));
+  kvtc_status s = launch_deflate(in, n, chunk_bytes, out, nullptr, len, rest, deflate_workspace(n, chunk_bytes), st);
+  if (s) return s;
+  if (out_len_host) {
+    uint64_t h = 0;
+    KVTC_CUDA_TRY(cudaMemcpyAsync(&h, len, 8, cudaMemcpyDeviceToHost, st));
+    KVTC_CUDA_TRY(cudaStreamSynchronize(st));
+    *out_len_host = size_t(h);
+  }
+  return KVTC_OK;
+}
+
+extern "C" kvtc_status kvtc_stage_inflate(const uint8_t *section, size_t len, uint8_t *out, size_t n_out,
+                                          void *stream) {
+  KVTC_CHECK_ARG(section && out && len >= kSectionHeaderBytes, "inflate arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t hdr[kSectionHeaderBytes];
+  KVTC_CUDA_TRY(cudaMemcpyAsync(hdr, section, sizeof(hdr), cudaMemcpyDeviceToHost, st));
+  KVTC_CUDA_TRY(cudaStreamSynchronize(st));
+  uint32_t nch = 0;
+  kvtc_status s = check_section_header(hdr, len, n_out, &nch);
+  if (s) return s;
+  int32_t *err = nullptr;
+  KVTC_CUDA_TRY(cudaMallocAsync(&err, 4, st));
+  KVTC_CUDA_TRY(cudaMemsetAsync(err, 0, 4, st));
+  s = launch_inflate_section(section, nullptr, n_out, nch, out, err, st);
+  int32_t herr = 0;
+  KVTC_CUDA_TRY(cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st));
+  KVTC_CUDA_TRY(cudaStreamSynchronize(st));
+  cudaFreeAsync(err, st);
+  if (s) return s;
+  if (herr) {
+    set_error("corrupt DEFLATE stream (code %d)", herr);
+    return KVTC_E_CORRUPT;
+  }
+  return KVTC_OK;
+}
+
+extern "C" kvtc_status kvtc_stage_inflate_raw(const uint8_t *in, const int64_t *in_off, const int64_t *in_len,
+                                              int32_t nstreams, uint8_t *out, const int64_t *out_off,
+                                              const int64_t *out_len, int32_t *status_dev, void *stream) {
+  KVTC_CHECK_ARG(nstreams >= 0 && (nstreams == 0 || (in && in_off && in_len && out && out_off && out_len && status_dev)),
+                 "inflate_raw arguments");
+  return launch_inflate_raw(in, in_off, in_len, nstreams, out, out_off, out_len, status_dev,
+                            static_cast<cudaStream_t>(stream));
+}
+
+extern "C" kvtc_status kvtc_stage_dequantize(const kvtc_plan *plan, const uint8_t *payload, int64_t m, uint16_t *Dh,
+                                             int64_t ld, void *stream) {
+  KVTC_CHECK_ARG(plan && payload && Dh && ld >= plan->r_nz && m >= 0, "dequantize arguments");
+  auto *pl = const_cast<kvtc_plan *>(plan);
+  return launch_dequant(pl->d_pgroups, pl->d_codes_off_full, pl->G, plan_codes_off_last(pl, m % kTileM),
+                        pl->tile_bytes, payload, m, reinterpret_cast<__half *>(Dh), ld,
+                        static_cast<cudaStream_t>(stream));
+}
+
+extern "C" kvtc_status kvtc_stage_reconstruct(const kvtc_basis *b, const kvtc_plan *plan, const uint16_t *Dh,
+                                              int64_t ld, int64_t m, int64_t tok_begin, int32_t layer_begin,
+                                              int32_t layer_end, const kvtc_kv_view *out, void *stream) {
+  kvtc_status s = check_view(out);
+  if (s) return s;
+  KVTC_CHECK_ARG(b && plan && Dh && same_shape(out->shape, b->shape), "reconstruct arguments");
+  KVTC_CHECK_ARG(ld % 8 == 0 && ld >= plan->r_nz, "ld must be a multiple of 8 and >= plan columns");
+  KVTC_CHECK_ARG(0 <= layer_begin && layer_begin <= layer_end && layer_end <= b->shape.layers, "layer range");
+  KVTC_CHECK_ARG(tok_begin >= 0 && tok_begin + m <= out->tokens, "token range");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  auto *pl = const_cast<kvtc_plan *>(plan);
+  const Operands *op;
+  if ((s = plan_operands(b, pl, &op))) return s;
+  const int half = b->shape.head_dim / 2;
+  Bump need;
+  need.take<void *>(b->shape.layers);
+  need.take<float2>(m * half);
+  void *scratch = nullptr;
+  KVTC_CUDA_TRY(cudaMallocAsync(&scratch, need.used, st));
+  Bump ws(scratch, need.used);
+  auto *bases = ws.take<__nv_bfloat16 *>(b->shape.layers);
+  float2 *cs = ws.take<float2>(m * half);
+  if ((s = upload_bases(out, bases, st))) return s;
+  if (b->has_rope && (s = rope_table_for(b, out->pos0 + tok_begin, m, cs, st))) return s;
+  s = run_reconstruct(b, pl, op, reinterpret_cast<const __half *>(Dh), ld, m, tok_begin, layer_begin, layer_end, out,
+                      bases, cs, st);
+  cudaFreeAsync(scratch, st);
+  return s;
+}
+
+// ================================================================== codec
+namespace {
+struct CompressLayout {
+  int64_t m, nraw, raw_bytes;
+  uint64_t pay[2];
+  uint64_t sec_bound[2];
+  uint64_t k_off;
+  uint64_t bound;
+};
+CompressLayout compress_layout(const kvtc_plan *kp, const kvtc_plan *vp, const kvtc_kv_view *k,
+                               const kvtc_policy *pol) {
+  CompressLayout L{};
+  const int64_t t = k->tokens;
+  const int64_t sw = int64_t(pol->sinks) + pol->window;
+  L.m = t > sw ? t - sw : 0;
+  L.nraw = L.m ? sw : t;
+  const int64_t hd = int64_t(k->shape.kv_heads) * k->shape.head_dim;
+  L.raw_bytes = 2 * int64_t(k->shape.layers) * L.nraw * hd * 2;
+  L.pay[0] = kvtc_payload_bytes(kp, L.m);
+  L.pay[1] = kvtc_payload_bytes(vp, L.m);
+  for (int s = 0; s < 2; ++s) L.sec_bound[s] = deflate_section_bound(L.pay[s], pol->chunk_bytes);
+  L.k_off = align16(KVTC_HEADER_BYTES + L.raw_bytes);
+  L.bound = L.k_off + align16(L.sec_bound[0]) + align16(L.sec_bound[1]) + 64;
+  return L;
+}
+}  // namespace
+
+extern "C" size_t kvtc_compress_bound(const kvtc_plan *kp, const kvtc_plan *vp, const kvtc_kv_view *k,
+                                      const kvtc_policy *pol) {
+  if (!kp || !vp || !k || !pol) return 0;
+  return size_t(compress_layout(kp, vp, k, pol).bound);
+}
+
+extern "C" size_t kvtc_compress_workspace_bytes(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb,
+                                                const kvtc_plan *vp, const kvtc_kv_view *k, const kvtc_policy *pol) {
+  if (!kb || !kp || !vb || !vp || !k || !pol) return 0;
+  const CompressLayout L = compress_layout(kp, vp, k, pol);
+  Bump b;
+  b.take<void *>(k->shape.layers);
+  b.take<void *>(k->shape.layers);
+  b.take<uint64_t>(8);
+  b.take<__nv_bfloat16>(L.m * kb->p);
+  b.take<float2>(L.m * (kb->shape.head_dim / 2));
+  b.take<uint8_t>(std::max(L.pay[0], L.pay[1]) + 16);
+  b.take<uint8_t>(deflate_workspace(std::max(L.pay[0], L.pay[1]), pol->chunk_bytes));
+  return b.used + 256;
+}
+
+extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb,
+                                     const kvtc_plan *vp, const kvtc_kv_view *k, const kvtc_kv_view *v,
+                                     const kvtc_policy *pol, void *out, size_t out_cap, size_t *out_len_host,
+                                     void *workspace, size_t workspace_bytes, void *stream) {
+  KVTC_CHECK_ARG(kb && kp && vb && vp && k && v && pol && out, "compress arguments");
+  kvtc_status s;
+  if ((s = check_view(k)) || (s = check_view(v))) return s;
+  KVTC_CHECK_ARG(same_shape(k->shape, v->shape) && k->tokens == v->tokens && k->pos0 == v->pos0,
+                 "key and value views differ");
+  KVTC_CHECK_ARG(same_shape(k->shape, kb->shape) && same_shape(v->shape, vb->shape), "basis shape mismatch");
+  KVTC_CHECK_ARG(kb->which == KVTC_KEYS && vb->which == KVTC_VALUES, "basis streams");
+  KVTC_CHECK_ARG(pol->sinks >= 0 && pol->window >= 0, "policy");
+  KVTC_CHECK_ARG(pol->chunk_bytes == 16384 || pol->chunk_bytes == 32768 || pol->chunk_bytes == 65536, "chunk_bytes");
+  const CompressLayout L = compress_layout(kp, vp, k, pol);
+  if (out_cap < L.bound) {
+    set_error("output capacity %zu < bound %llu", out_cap, (unsigned long long)L.bound);
+    return KVTC_E_CAPACITY;
+  }
+  const size_t need = kvtc_compress_workspace_bytes(kb, kp, vb, vp, k, pol);
+  if (workspace_bytes < need || !workspace) {
+    set_error("workspace %zu < %zu", workspace_bytes, need);
+    return KVTC_E_CAPACITY;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  auto *kpl = const_cast<kvtc_plan *>(kp);
+  auto *vpl = const_cast<kvtc_plan *>(vp);
+  const Operands *kop, *vop;
+  if ((s = plan_operands(kb, kpl, &kop)) || (s = plan_operands(vb, vpl, &vop))) return s;
+
+  Bump ws(workspace, workspace_bytes);
+  auto *kbases = ws.take<__nv_bfloat16 *>(k->shape.layers);
+  auto *vbases = ws.take<__nv_bfloat16 *>(k->shape.layers);
+  uint64_t *lens = ws.take<uint64_t>(8);     // [0..1] section lengths, [2..3] section offsets
+  auto *X = ws.take<__nv_bfloat16>(L.m * kb->p);
+  float2 *cs = ws.take<float2>(L.m * (kb->shape.head_dim / 2));
+  uint8_t *payload = ws.take<uint8_t>(std::max(L.pay[0], L.pay[1]) + 16);
+  const size_t dws = deflate_workspace(std::max(L.pay[0], L.pay[1]), pol->chunk_bytes);
+  void *dwsp = ws.take<uint8_t>(dws);
+  if ((s = upload_bases(k, kbases, st)) || (s = upload_bases(v, vbases, st))) return s;
+
+  uint8_t *o = static_cast<uint8_t *>(out);
+  ContainerHeader h = {};
+  h.magic = kContainerMagic;
+  h.version = kContainerVersion;
+  h.layers = k->shape.layers;
+  h.kv_heads = k->shape.kv_heads;
+  h.head_dim = k->shape.head_dim;
+  h.sinks = pol->sinks;
+  h.window = pol->window;
+  h.chunk_bytes = pol->chunk_bytes;
+  h.tokens = k->tokens;
+  h.pos0 = k->pos0;
+  h.m = L.m;
+  h.raw_bytes = L.raw_bytes;
+  h.payload_bytes[0] = L.pay[0];
+  h.payload_bytes[1] = L.pay[1];
+  h.basis_fp[0] = kb->fp;
+  h.basis_fp[1] = vb->fp;
+  h.plan_fp[0] = kp->fp;
+  h.plan_fp[1] = vp->fp;
+  h.raw_off = KVTC_HEADER_BYTES;
+  h.section_off[0] = L.k_off;
+
+  // raw sinks + window, K then V: [layers][nraw][h*d] each
+  const int64_t hd = int64_t(k->shape.kv_heads) * k->shape.head_dim;
+  auto *rawk = reinterpret_cast<__nv_bfloat16 *>(o + KVTC_HEADER_BYTES);
+  auto *rawv = rawk + int64_t(k->shape.layers) * L.nraw * hd;
+  const int64_t t = k->tokens;
+  if (L.m) {
+    for (int sv = 0; sv < 2; ++sv) {
+      const kvtc_kv_view *vw = sv ? v : k;
+      __nv_bfloat16 *const *bs = sv ? vbases : kbases;
+      __nv_bfloat16 *dst = sv ? rawv : rawk;
+      if ((s = launch_pack_raw(*vw, bs, 0, pol->sinks, dst, L.nraw, 0, st))) return s;
+      if ((s = launch_pack_raw(*vw, bs, t - pol->window, pol->window, dst, L.nraw, pol->sinks, st))) return s;
+    }
+  } else {
+    if ((s = launch_pack_raw(*k, kbases, 0, t, rawk, L.nraw, 0, st))) return s;
+    if ((s = launch_pack_raw(*v, vbases, 0, t, rawv, L.nraw, 0, st))) return s;
+    header_kernel<<<1, 1, 0, st>>>(h, o, nullptr, nullptr);
+    KVTC_LAUNCH_CHECK();
+    if (out_len_host) {
+      KVTC_CUDA_TRY(cudaStreamSynchronize(st));
+      *out_len_host = size_t(h.raw_off + L.raw_bytes);
+    }
+    return KVTC_NOTHING_TO_COMPRESS;
+  }
+  KVTC_CUDA_TRY(cudaMemcpyAsync(lens + 2, &h.section_off[0], 8, cudaMemcpyHostToDevice, st));
+  // ---- keys: un-RoPE gather (K1) -> fused projection + quantisation (K2) -> DEFLATE (K3)
+  if ((s = rope_table_for(kb, k->pos0 + pol->sinks, L.m, cs, st))) return s;
+  if ((s = launch_gather(*k, kbases, pol->sinks, L.m, cs, kb->pairing, X, st))) return s;
+  if ((s = run_project_quant(kb, kpl, kop, X, L.m, payload, st))) return s;
+  if ((s = launch_deflate(payload, L.pay[0], pol->chunk_bytes, o, lens + 2, lens + 0, dwsp, dws, st))) return s;
+  offset_after_kernel<<<1, 1, 0, st>>>(lens + 2, lens + 0, lens + 3);
+  // ---- values
+  if ((s = launch_gather(*v, vbases, pol->sinks, L.m, nullptr, 0, X, st))) return s;
+  if ((s = run_project_quant(vb, vpl, vop, X, L.m, payload, st))) return s;
+  if ((s = launch_deflate(payload, L.pay[1], pol->chunk_bytes, o, lens + 3, lens + 1, dwsp, dws, st))) return s;
+  header_kernel<<<1, 1, 0, st>>>(h, o, lens, lens + 2);
+  KVTC_LAUNCH_CHECK();
+  if (out_len_host) {
+    uint64_t l4[4];
+    KVTC_CUDA_TRY(cudaMemcpyAsync(l4, lens, 32, cudaMemcpyDeviceToHost, st));
+    KVTC_CUDA_TRY(cudaStreamSynchronize(st));
+    *out_len_host = size_t(l4[3] + l4[1]);      // V section offset + V section length
+  }
+  return KVTC_OK;
+}
+
+extern "C" kvtc_status kvtc_container_parse(const void *header_host, kvtc_container_info *info) {
+  KVTC_CHECK_ARG(header_host && info, "container_parse arguments");
+  ContainerHeader h;
+  memcpy(&h, header_host, sizeof(h));
+  if (h.magic != kContainerMagic || h.version != kContainerVersion) {
+    set_error("not a KVTC container (magic %08x version %u)", h.magic, h.version);
+    return KVTC_E_CORRUPT;
+  }
+  info->magic = h.magic;
+  info->version = h.version;
+  info->layers = h.layers;
+  info->kv_heads = h.kv_heads;
+  info->head_dim = h.head_dim;
+  info->sinks = h.sinks;
+  info->window = h.window;
+  info->chunk_bytes = h.chunk_bytes;
+  info->tokens = h.tokens;
+  info->pos0 = h.pos0;
+  info->m = h.m;
+  info->total_bytes = h.m ? h.total_bytes : h.raw_off + h.raw_bytes;
+  info->raw_bytes = h.raw_bytes;
+  for (int s = 0; s < 2; ++s) {
+    info->payload_bytes[s] = h.payload_bytes[s];
+    info->entropy_bytes[s] = h.entropy_bytes[s];
+    info->basis_fp[s] = h.basis_fp[s];
+    info->plan_fp[s] = h.plan_fp[s];
+  }
+  return KVTC_OK;
+}
+
+extern "C" size_t kvtc_decompress_workspace_bytes(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb,
+                                                  const kvtc_plan *vp, const void *in_header_host) {
+  if (!kb || !kp || !vb || !vp || !in_header_host) return 0;
+  ContainerHeader h;
+  memcpy(&h, in_header_host, sizeof(h));
+  Bump b;
+  b.take<void *>(h.layers);
+  b.take<void *>(h.layers);
+  b.take<int32_t>(4);
+  b.take<uint8_t>(std::max(h.payload_bytes[0], h.payload_bytes[1]) + 16);
+  b.take<__half>(h.m * std::max(std::max(kp->r_nz_pad, vp->r_nz_pad), 8));
+  b.take<float2>(h.m * (kb->shape.head_dim / 2));
+  return b.used + 256;
+}
+
+extern "C" kvtc_status kvtc_decompress(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb,
+                                       const kvtc_plan *vp, const void *in, size_t in_len, int32_t layer_begin,
+                                       int32_t layer_end, const kvtc_kv_view *k_out, const kvtc_kv_view *v_out,
+                                       void *workspace, size_t workspace_bytes, void *stream) {
+  KVTC_CHECK_ARG(kb && kp && vb && vp && in && k_out && v_out, "decompress arguments");
+  kvtc_status s;
+  if ((s = check_view(k_out)) || (s = check_view(v_out))) return s;
+  KVTC_CHECK_ARG(in_len >= KVTC_HEADER_BYTES, "container too short");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ContainerHeader h;
+  KVTC_CUDA_TRY(cudaMemcpyAsync(&h, in, sizeof(h), cudaMemcpyDeviceToHost, st));
+  KVTC_CUDA_TRY(cudaStreamSynchronize(st));
+  kvtc_container_info info;
+  if ((s = kvtc_container_parse(&h, &info))) return s;
+  const kvtc_shape shp{h.layers, h.kv_heads, h.head_dim};
+  if (!same_shape(shp, k_out->shape) || !same_shape(shp, v_out->shape) || k_out->tokens != h.tokens ||
+      v_out->tokens != h.tokens || !same_shape(shp, kb->shape) || !same_shape(shp, vb->shape)) {
+    set_error("container shape does not match the output views / bases");
+    return KVTC_E_MISMATCH;
+  }
+  if (h.basis_fp[0] != kb->fp || h.basis_fp[1] != vb->fp || h.plan_fp[0] != kp->fp || h.plan_fp[1] != vp->fp) {
+    set_error("container was written with a different basis or plan");
+    return KVTC_E_MISMATCH;
+  }
+  if (info.total_bytes > in_len) {
+    set_error("container length %llu > buffer %zu", (unsigned long long)info.total_bytes, in_len);
+    return KVTC_E_CORRUPT;
+  }
+  if (h.m && (h.payload_bytes[0] != kvtc_payload_bytes(kp, h.m) || h.payload_bytes[1] != kvtc_payload_bytes(vp, h.m))) {
+    set_error("payload sizes do not match the plans");
+    return KVTC_E_CORRUPT;
+  }
+  KVTC_CHECK_ARG(0 <= layer_begin && layer_begin <= layer_end && layer_end <= h.layers, "layer range");
+  const size_t need = kvtc_decompress_workspace_bytes(kb, kp, vb, vp, &h);
+  if (!workspace || workspace_bytes < need) {
+    set_error("workspace %zu < %zu", workspace_bytes, need);
+    return KVTC_E_CAPACITY;
+  }
+  Bump ws(workspace, workspace_bytes);
+  auto *kbases = ws.take<__nv_bfloat16 *>(h.layers);
+  auto *vbases = ws.take<__nv_bfloat16 *>(h.layers);
+  int32_t *err = ws.take<int32_t>(4);
+  uint8_t *payload = ws.take<uint8_t>(std::max(h.payload_bytes[0], h.payload_bytes[1]) + 16);
+  const int64_t ld = std::max(std::max(kp->r_nz_pad, vp->r_nz_pad), 8);
+  __half *Dh = ws.take<__half>(h.m * ld);
+  float2 *cs = ws.take<float2>(h.m * (h.head_dim / 2));
+  if ((s = upload_bases(k_out, kbases, st)) || (s = upload_bases(v_out, vbases, st))) return s;
+  KVTC_CUDA_TRY(cudaMemsetAsync(err, 0, 4, st));
+  const uint8_t *ib = static_cast<const uint8_t *>(in);
+  const int64_t t = h.tokens;
+  const int64_t nraw = h.m ? int64_t(h.sinks) + h.window : t;
+  const int64_t hd = int64_t(h.kv_heads) * h.head_dim;
+  const auto *rawk = reinterpret_cast<const __nv_bfloat16 *>(ib + h.raw_off);
+  const auto *rawv = rawk + int64_t(h.layers) * nraw * hd;
+  if (!h.m) {
+    if ((s = launch_unpack_raw(rawk, nraw, 0, t, *k_out, kbases, 0, layer_begin, layer_end, st))) return s;
+    return launch_unpack_raw(rawv, nraw, 0, t, *v_out, vbases, 0, layer_begin, layer_end, st);
+  }
+  // device copy of the section offsets lives in the container header itself
+  const uint64_t *sec_off_dev = reinterpret_cast<const uint64_t *>(ib + offsetof(ContainerHeader, section_off));
+  if (kb->has_rope && (s = rope_table_for(kb, h.pos0 + h.sinks, h.m, cs, st))) return s;
+  for (int sv = 0; sv < 2; ++sv) {
+    const kvtc_basis *b = sv ? vb : kb;
+    kvtc_plan *pl = const_cast<kvtc_plan *>(sv ? vp : kp);
+    const kvtc_kv_view *vw = sv ? v_out : k_out;
+    __nv_bfloat16 *const *bs = sv ? vbases : kbases;
+    const Operands *op;
+    if ((s = plan_operands(b, pl, &op))) return s;
+    const uint32_t nch = uint32_t((h.payload_bytes[sv] + h.chunk_bytes - 1) / h.chunk_bytes);
+    if ((s = launch_inflate_section(ib, sec_off_dev + sv, h.payload_bytes[sv], nch, payload, err, st))) return s;
+    if ((s = launch_dequant(pl->d_pgroups, pl->d_codes_off_full, pl->G, plan_codes_off_last(pl, h.m % kTileM),
+                            pl->tile_bytes, payload, h.m, Dh, ld, st)))
+      return s;
+    if (pl->r_nz == 0) KVTC_CUDA_TRY(cudaMemsetAsync(Dh, 0, h.m * ld * 2, st));
+    if ((s = run_reconstruct(b, pl, op, Dh, ld, h.m, h.sinks, layer_begin, layer_end, vw, bs, cs, st))) return s;
+    const __nv_bfloat16 *raw = sv ? rawv : rawk;
+    if ((s = launch_unpack_raw(raw, nraw, 0, h.sinks, *vw, bs, 0, layer_begin, layer_end, st))) return s;
+    if ((s = launch_unpack_raw(raw, nraw, h.sinks, h.window, *vw, bs, t - h.window, layer_begin, layer_end, st)))
+      return s;
+  }
+  return KVTC_OK;
+}
+
+// ------------------------------------------------- calibration / allocation
+// (implemented in calib.cu / dp.cu)
+

@@ -1,0 +1,809 @@
+// deflate.cu — chunk-parallel DEFLATE (RFC 1951) encoder and decoders (K3/K4).
+//
+// Paper: the packed byte array is "further compressed using the DEFLATE
+// algorithm" and runs on the GPU.  Reading Q15: 64 KiB chunks, each
+// an independent raw DEFLATE stream that stock zlib inflates (wbits = -15).
+//
+// Encoder (one CTA of 256 threads per chunk): byte histogram -> length-limited
+// canonical Huffman code (<= 15 bits; in-place minimum-redundancy lengths +
+// Kraft-sum repair) -> one dynamic block (literals + EOB only, no LZ77 matches in
+// this version) -> each thread emits the bits of 1/256 of the chunk at an offset
+// from a block-wide exclusive scan.  Falls back to stored blocks when smaller.
+// While emitting, the bit offset of every 1/32 of the chunk ("segment") is
+// recorded in a side index that lives in the section, NOT in the DEFLATE stream.
+//
+// Decoder, fast path (one warp per chunk): lane 0 parses the block header, the
+// warp builds a 10-bit lookup table in shared memory, then lane j decodes
+// segment j from its recorded bit offset — 32 independent serial decoders.
+// Decoder, generic path (kvtc_stage_inflate_raw): a complete sequential inflater
+// (stored / fixed / dynamic blocks, LZ77 back-references) for foreign streams.
+//
+// Section layout: 64-byte header, chunk table [nchunks] x
+// {u64 offset, u32 bytes, u32 kind}, segment index [nchunks][32] u32, then the
+// chunk streams, each starting 4-byte aligned.
+#include <cub/block/block_scan.cuh>
+
+#include "internal.h"
+
+namespace kvtc {
+
+constexpr uint32_t kSectionMagic = 0x4454564Bu;  // "KVTD"
+constexpr int kEncThreads = 256;
+constexpr int kNSeg = 32;
+constexpr int kLitSyms = 257;                    // 0..255 literals + 256 end-of-block
+constexpr int kMaxBits = 15;
+
+__host__ __device__ inline uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+__host__ __device__ inline uint32_t umin32(uint32_t a, uint32_t b) { return a < b ? a : b; }
+
+struct SectionHeader {
+  uint32_t magic, version;
+  uint64_t raw_bytes;
+  uint32_t chunk_bytes, nchunks;
+  uint32_t seg_bytes, nseg;
+  uint64_t data_offset;
+  uint64_t section_bytes;
+  uint64_t pad[2];
+};
+static_assert(sizeof(SectionHeader) == 64, "section header is 64 bytes");
+struct ChunkEntry {
+  uint64_t offset;     // from data start
+  uint32_t bytes;      // stream bytes
+  uint32_t kind;       // 0 = Huffman (indexed), 1 = stored
+};
+
+__host__ __device__ inline uint32_t stored_bytes(uint32_t n) {
+  const uint32_t blocks = n == 0 ? 1 : (n + 32767) / 32768;
+  return n + 5 * blocks;
+}
+__host__ __device__ inline uint64_t slot_stride(int32_t chunk) { return ((stored_bytes(chunk) + 64 + 15) / 16) * 16; }
+
+size_t deflate_section_bound(size_t n, int32_t chunk) {
+  const size_t nch = (n + chunk - 1) / chunk;
+  return sizeof(SectionHeader) + nch * sizeof(ChunkEntry) + nch * kNSeg * 4 + nch * ((stored_bytes(chunk) + 3) & ~3u) +
+         16;
+}
+size_t deflate_workspace(size_t n, int32_t chunk) {
+  const size_t nch = (n + chunk - 1) / chunk;
+  return nch * slot_stride(chunk) + nch * 8 + nch * kNSeg * 4 + 256;
+}
+
+// ---------------------------------------------------------- Huffman lengths
+// In-place minimum-redundancy code lengths for weights sorted ascending
+// (A[i] becomes the code length of the i-th lightest symbol).
+__device__ void min_redundancy_lengths(int *A, int n) {
+  if (n == 0) return;
+  if (n == 1) {
+    A[0] = 1;
+    return;
+  }
+  int root, leaf, next, avbl, used, dpth;
+  A[0] += A[1];
+  root = 0;
+  leaf = 2;
+  for (next = 1; next < n - 1; next++) {
+    if (leaf >= n || A[root] < A[leaf]) {
+      A[next] = A[root];
+      A[root++] = next;
+    } else {
+      A[next] = A[leaf++];
+    }
+    if (leaf >= n || (root < next && A[root] < A[leaf])) {
+      A[next] += A[root];
+      A[root++] = next;
+    } else {
+      A[next] += A[leaf++];
+    }
+  }
+  A[n - 2] = 0;
+  for (next = n - 3; next >= 0; next--) A[next] = A[A[next]] + 1;
+  avbl = 1;
+  used = dpth = 0;
+  root = n - 2;
+  next = n - 1;
+  while (avbl > 0) {
+    while (root >= 0 && A[root] == dpth) {
+      used++;
+      root--;
+    }
+    while (avbl > used) {
+      A[next--] = dpth;
+      avbl--;
+    }
+    avbl = 2 * used;
+    dpth++;
+    used = 0;
+  }
+}
+
+// Single-thread: code lengths (<= maxbits, complete prefix code) for nsym
+// symbols with frequencies freq[]; sorted[] = symbols with freq > 0 sorted by
+// (freq, symbol) ascending, count nz.  work: int[nsym].
+__device__ void build_lengths(const uint32_t *freq, const int *sorted, int nz, int maxbits, uint8_t *len, int nsym,
+                              int *work) {
+  for (int s = 0; s < nsym; ++s) len[s] = 0;
+  if (nz == 0) return;
+  if (nz == 1) {
+    len[sorted[0]] = 1;
+    return;
+  }
+  for (int i = 0; i < nz; ++i) work[i] = int(freq[sorted[i]]);
+  min_redundancy_lengths(work, nz);
+  int num[33];
+  for (int i = 0; i < 33; ++i) num[i] = 0;
+  for (int i = 0; i < nz; ++i) num[work[i] > 32 ? 32 : work[i]]++;
+  // enforce the maximum length while keeping the Kraft sum exactly 1
+  for (int i = maxbits + 1; i <= 32; i++) {
+    num[maxbits] += num[i];
+    num[i] = 0;
+  }
+  uint32_t total = 0;
+  for (int i = maxbits; i > 0; i--) total += uint32_t(num[i]) << (maxbits - i);
+  while (total != (1u << maxbits)) {
+    num[maxbits]--;
+    for (int i = maxbits - 1; i > 0; i--)
+      if (num[i]) {
+        num[i]--;
+        num[i + 1] += 2;
+        break;
+      }
+    total--;
+  }
+  // most frequent symbols get the shortest codes
+  int j = nz;
+  for (int l = 1; l <= maxbits; ++l)
+    for (int k = num[l]; k > 0; --k) len[sorted[--j]] = uint8_t(l);
+}
+
+// Canonical codes (RFC 1951 §3.2.2), returned bit-reversed for LSB-first output.
+__device__ void canonical_codes(const uint8_t *len, int nsym, uint16_t *rev_code) {
+  int bl_count[16] = {0};
+  for (int s = 0; s < nsym; ++s) bl_count[len[s]]++;
+  bl_count[0] = 0;
+  int next_code[16];
+  int code = 0;
+  for (int b = 1; b <= 15; ++b) {
+    code = (code + bl_count[b - 1]) << 1;
+    next_code[b] = code;
+  }
+  for (int s = 0; s < nsym; ++s) {
+    const int l = len[s];
+    if (l) {
+      const uint32_t c = uint32_t(next_code[l]++);
+      rev_code[s] = uint16_t(__brev(c) >> (32 - l));
+    } else {
+      rev_code[s] = 0;
+    }
+  }
+}
+
+// Small LSB-first bit writer into shared memory (block header).
+struct BitWriter {
+  uint32_t *buf;
+  uint32_t nbits;
+  __device__ void put(uint32_t v, int n) {
+    for (int i = 0; i < n; ++i, ++nbits) {
+      if (((v >> i) & 1u)) buf[nbits >> 5] |= 1u << (nbits & 31);
+    }
+  }
+};
+
+__device__ void rank_sort(const uint32_t *freq, int nsym, int *sorted, int *nz_out) {
+  // parallel rank sort of symbols with freq > 0 by (freq, symbol); all threads call
+  for (int s = threadIdx.x; s < nsym; s += blockDim.x) {
+    const uint32_t f = freq[s];
+    if (f == 0) continue;
+    int rank = 0;
+    for (int j = 0; j < nsym; ++j) {
+      const uint32_t g = freq[j];
+      if (g != 0 && (g < f || (g == f && j < s))) rank++;
+    }
+    sorted[rank] = s;
+  }
+  if (threadIdx.x == 0) {
+    int nz = 0;
+    for (int s = 0; s < nsym; ++s) nz += freq[s] != 0;
+    *nz_out = nz;
+  }
+}
+
+struct EncShared {
+  uint32_t hist[kLitSyms + 3];
+  uint32_t clhist[19];
+  int sorted[kLitSyms + 3];
+  int work[kLitSyms + 3];
+  int nz, clnz;
+  uint8_t len[kLitSyms + 3];
+  uint16_t rev[kLitSyms + 3];
+  uint8_t cllen[19];
+  uint16_t clrev[19];
+  uint16_t rle_sym[kLitSyms + 8];
+  uint8_t rle_extra[kLitSyms + 8];
+  int nrle;
+  uint32_t hdr[160];   // header bits (<= 5120)
+  uint32_t hdr_bits;
+  uint32_t total_bits;
+  int use_stored;
+  typename cub::BlockScan<uint32_t, kEncThreads>::TempStorage scan;
+};
+
+__global__ void __launch_bounds__(kEncThreads) deflate_encode_kernel(const uint8_t *in, uint64_t n, int32_t chunk,
+                                                                     uint8_t *slots, uint64_t stride,
+                                                                     uint32_t *chunk_bytes, uint32_t *chunk_kind,
+                                                                     uint32_t *index) {
+  __shared__ EncShared S;
+  const int c = blockIdx.x;
+  const uint64_t base = uint64_t(c) * chunk;
+  const uint32_t nc = uint32_t(umin64(chunk, n - base));
+  const uint8_t *src = in + base;
+  uint8_t *out = slots + uint64_t(c) * stride;
+  const int t = threadIdx.x;
+  const uint32_t piece = uint32_t(chunk) / kEncThreads;
+  const uint32_t p0 = min(nc, t * piece), p1 = min(nc, (t + 1) * piece);
+
+  for (int s = t; s < kLitSyms + 3; s += kEncThreads) S.hist[s] = 0;
+  if (t < 19) S.clhist[t] = 0;
+  if (t < 160) S.hdr[t] = 0;
+  __syncthreads();
+  // ---- histogram (16-byte vector loads when aligned)
+  {
+    uint32_t i = p0;
+    for (; i + 16 <= p1 && ((reinterpret_cast<uintptr_t>(src + i) & 15) == 0); i += 16) {
+      const uint4 v = *reinterpret_cast<const uint4 *>(src + i);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int k = 0; k < 16; ++k) atomicAdd(&S.hist[(w[k >> 2] >> (8 * (k & 3))) & 0xFF], 1u);
+    }
+    for (; i < p1; ++i) atomicAdd(&S.hist[src[i]], 1u);
+  }
+  __syncthreads();
+  if (t == 0) S.hist[256] = 1;  // end-of-block
+  __syncthreads();
+  rank_sort(S.hist, kLitSyms, S.sorted, &S.nz);
+  __syncthreads();
+  if (t == 0) {
+    build_lengths(S.hist, S.sorted, S.nz, kMaxBits, S.len, kLitSyms, S.work);
+    canonical_codes(S.len, kLitSyms, S.rev);
+    // code-length sequence: 257 literal/length lengths + 1 distance length (0)
+    uint8_t seq[kLitSyms + 1];
+    for (int s = 0; s < kLitSyms; ++s) seq[s] = S.len[s];
+    seq[kLitSyms] = 0;
+    const int nseq = kLitSyms + 1;
+    int nr = 0;
+    for (int i = 0; i < nseq;) {
+      const uint8_t v = seq[i];
+      int run = 1;
+      while (i + run < nseq && seq[i + run] == v) run++;
+      if (v == 0) {
+        int left = run;
+        while (left >= 11) {
+          const int r = min(left, 138);
+          S.rle_sym[nr] = 18; S.rle_extra[nr++] = uint8_t(r - 11); left -= r;
+        }
+        if (left >= 3) {
+          S.rle_sym[nr] = 17; S.rle_extra[nr++] = uint8_t(left - 3); left = 0;
+        }
+        while (left-- > 0) { S.rle_sym[nr] = 0; S.rle_extra[nr++] = 0; }
+      } else {
+        S.rle_sym[nr] = v; S.rle_extra[nr++] = 0;
+        int left = run - 1;
+        while (left >= 3) {
+          const int r = min(left, 6);
+          S.rle_sym[nr] = 16; S.rle_extra[nr++] = uint8_t(r - 3); left -= r;
+        }
+        while (left-- > 0) { S.rle_sym[nr] = v; S.rle_extra[nr++] = 0; }
+      }
+      i += run;
+    }
+    S.nrle = nr;
+    for (int i = 0; i < nr; ++i) S.clhist[S.rle_sym[i]]++;
+    // a complete code-length code needs >= 2 used symbols
+    int used = 0;
+    for (int i = 0; i < 19; ++i) used += S.clhist[i] != 0;
+    if (used < 2) {
+      for (int i = 0; i < 19 && used < 2; ++i)
+        if (!S.clhist[i]) { S.clhist[i] = 1; used++; }
+    }
+    int csorted[19], cwork[19];
+    int cnz = 0;
+    for (int pass = 0; pass < 1; ++pass) {
+      // tiny insertion sort by (freq, symbol)
+      for (int s = 0; s < 19; ++s)
+        if (S.clhist[s]) {
+          int k = cnz++;
+          while (k > 0 && (S.clhist[csorted[k - 1]] > S.clhist[s])) { csorted[k] = csorted[k - 1]; --k; }
+          csorted[k] = s;
+        }
+    }
+    build_lengths(S.clhist, csorted, cnz, 7, S.cllen, 19, cwork);
+    canonical_codes(S.cllen, 19, S.clrev);
+    const int order[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
+    int hclen = 19;
+    while (hclen > 4 && S.cllen[order[hclen - 1]] == 0) hclen--;
+    BitWriter bw{S.hdr, 0};
+    bw.put(1, 1);            // BFINAL
+    bw.put(2, 2);            // BTYPE = 10 (dynamic Huffman)
+    bw.put(0, 5);            // HLIT  = 257 - 257
+    bw.put(0, 5);            // HDIST = 1 - 1
+    bw.put(hclen - 4, 4);    // HCLEN
+    for (int i = 0; i < hclen; ++i) bw.put(S.cllen[order[i]], 3);
+    for (int i = 0; i < nr; ++i) {
+      const int s = S.rle_sym[i];
+      bw.put(S.clrev[s], S.cllen[s]);
+      if (s == 16) bw.put(S.rle_extra[i], 2);
+      else if (s == 17) bw.put(S.rle_extra[i], 3);
+      else if (s == 18) bw.put(S.rle_extra[i], 7);
+    }
+    S.hdr_bits = bw.nbits;
+  }
+  __syncthreads();
+  // ---- bit counts per piece, exclusive scan
+  uint32_t mybits = 0;
+  for (uint32_t i = p0; i < p1; ++i) mybits += S.len[src[i]];
+  if (t == 0) mybits += S.hdr_bits;
+  if (p1 == nc && p0 < p1) mybits += S.len[256];  // EOB after the last byte
+  if (nc == 0 && t == 0) mybits += S.len[256];
+  uint32_t myoff, total;
+  cub::BlockScan<uint32_t, kEncThreads>(S.scan).ExclusiveSum(mybits, myoff, total);
+  if (t == 0) {
+    const uint32_t huff = (total + 7) / 8;
+    S.use_stored = huff >= stored_bytes(nc);
+    S.total_bits = total;
+  }
+  __syncthreads();
+  if (S.use_stored) {
+    // stored blocks of <= 32 KiB: [BFINAL|00][pad] LEN NLEN data
+    const uint32_t blocks = nc == 0 ? 1 : (nc + 32767) / 32768;
+    for (uint32_t b = t; b < blocks; b += kEncThreads) {
+      const uint32_t len = umin32(32768, nc - b * 32768);
+      uint8_t *o = out + b * (32768 + 5);
+      o[0] = (b + 1 == blocks) ? 1 : 0;
+      o[1] = len & 0xFF; o[2] = len >> 8; o[3] = (~len) & 0xFF; o[4] = ((~len) >> 8) & 0xFF;
+    }
+    for (uint32_t i = t; i < nc; i += kEncThreads) out[(i / 32768) * (32768 + 5) + 5 + (i % 32768)] = src[i];
+    if (t == 0) {
+      chunk_bytes[c] = stored_bytes(nc);
+      chunk_kind[c] = 1;
+    }
+    return;
+  }
+  // ---- segment index (bit offset of each 1/32 of the chunk)
+  const uint32_t pieces_per_seg = kEncThreads / kNSeg;
+  if (t % pieces_per_seg == 0) index[uint64_t(c) * kNSeg + t / pieces_per_seg] = myoff + (t == 0 ? S.hdr_bits : 0);
+  // ---- emission: full words stored, partial edge words OR-ed atomically
+  uint32_t *ow = reinterpret_cast<uint32_t *>(out);
+  const uint32_t w_first = myoff >> 5, w_last = (myoff + mybits - 1) >> 5;
+  if (mybits) {
+    ow[w_first] = 0;
+    ow[w_last] = 0;
+  }
+  __syncthreads();
+  if (mybits) {
+    uint64_t acc = 0;
+    uint32_t nb = myoff & 31;     // bits already "occupied" in the first word (left zeros)
+    uint32_t w = w_first;
+    auto flush = [&](bool final_) {
+      while (nb >= 32 || (final_ && nb > 0)) {
+        const uint32_t word = uint32_t(acc);
+        if (w == w_first || w == w_last) atomicOr(&ow[w], word);
+        else ow[w] = word;
+        acc >>= 32;
+        nb = nb >= 32 ? nb - 32 : 0;
+        ++w;
+      }
+    };
+    if (t == 0) {
+      for (uint32_t i = 0; i < S.hdr_bits; i += 16) {
+        const uint32_t k = umin32(16, S.hdr_bits - i);
+        const uint32_t v = (S.hdr[i >> 5] >> (i & 31)) & ((1u << k) - 1);
+        acc |= uint64_t(v) << nb;
+        nb += k;
+        flush(false);
+      }
+    }
+    for (uint32_t i = p0; i < p1; ++i) {
+      const uint8_t s = src[i];
+      acc |= uint64_t(S.rev[s]) << nb;
+      nb += S.len[s];
+      flush(false);
+    }
+    if (p1 == nc) {
+      acc |= uint64_t(S.rev[256]) << nb;
+      nb += S.len[256];
+    }
+    flush(true);
+  }
+  if (t == 0) {
+    chunk_bytes[c] = (S.total_bits + 7) / 8;
+    chunk_kind[c] = 0;
+  }
+}
+
+// Section assembly: one block computes the chunk offsets and the header; then
+// one block per chunk copies the stream and its index entry.
+__global__ void __launch_bounds__(1024) section_layout_kernel(const uint32_t *chunk_bytes, const uint32_t *chunk_kind, uint32_t nch,
+                                      uint64_t n, int32_t chunk, uint8_t *out_base, const uint64_t *off_dev,
+                                      uint64_t *section_len) {
+  uint8_t *out = out_base + (off_dev ? *off_dev : 0);
+  __shared__ typename cub::BlockScan<uint64_t, 1024>::TempStorage tmp;
+  __shared__ uint64_t carry;
+  SectionHeader *h = reinterpret_cast<SectionHeader *>(out);
+  ChunkEntry *tab = reinterpret_cast<ChunkEntry *>(out + sizeof(SectionHeader));
+  const uint64_t data_off = sizeof(SectionHeader) + uint64_t(nch) * sizeof(ChunkEntry) + uint64_t(nch) * kNSeg * 4;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (uint32_t b = 0; b < nch; b += 1024) {
+    const uint32_t i = b + threadIdx.x;
+    const uint64_t sz = i < nch ? ((uint64_t(chunk_bytes[i]) + 3) & ~3ull) : 0;
+    uint64_t off, tot;
+    cub::BlockScan<uint64_t, 1024>(tmp).ExclusiveSum(sz, off, tot);
+    if (i < nch) {
+      tab[i].offset = carry + off;
+      tab[i].bytes = chunk_bytes[i];
+      tab[i].kind = chunk_kind[i];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    SectionHeader hh = {};
+    hh.magic = kSectionMagic;
+    hh.version = 1;
+    hh.raw_bytes = n;
+    hh.chunk_bytes = uint32_t(chunk);
+    hh.nchunks = nch;
+    hh.seg_bytes = uint32_t(chunk) / kNSeg;
+    hh.nseg = kNSeg;
+    hh.data_offset = data_off;
+    hh.section_bytes = data_off + carry;
+    *h = hh;
+    *section_len = data_off + carry;
+  }
+}
+
+__global__ void section_copy_kernel(const uint8_t *slots, uint64_t stride, const uint32_t *index, uint32_t nch,
+                                    uint8_t *out_base, const uint64_t *off_dev) {
+  uint8_t *out = out_base + (off_dev ? *off_dev : 0);
+  const uint32_t c = blockIdx.x;
+  const SectionHeader *h = reinterpret_cast<const SectionHeader *>(out);
+  const ChunkEntry e = reinterpret_cast<const ChunkEntry *>(out + sizeof(SectionHeader))[c];
+  uint32_t *idx = reinterpret_cast<uint32_t *>(out + sizeof(SectionHeader) + uint64_t(nch) * sizeof(ChunkEntry));
+  if (threadIdx.x < kNSeg) idx[uint64_t(c) * kNSeg + threadIdx.x] = e.kind == 0 ? index[uint64_t(c) * kNSeg + threadIdx.x] : 0;
+  const uint32_t *s = reinterpret_cast<const uint32_t *>(slots + uint64_t(c) * stride);
+  uint32_t *d = reinterpret_cast<uint32_t *>(out + h->data_offset + e.offset);
+  const uint32_t words = (e.bytes + 3) / 4;
+  for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) d[i] = s[i];
+}
+
+kvtc_status launch_deflate(const uint8_t *in, size_t n, int32_t chunk, uint8_t *out, const uint64_t *off_dev,
+                           uint64_t *section_len_dev, void *ws, size_t ws_bytes, cudaStream_t st) {
+  KVTC_CHECK_ARG(chunk == 16384 || chunk == 32768 || chunk == 65536, "chunk_bytes must be 16/32/64 KiB");
+  KVTC_CHECK_ARG(ws_bytes >= deflate_workspace(n, chunk), "deflate workspace");
+  const uint32_t nch = uint32_t((n + chunk - 1) / chunk);
+  const uint64_t stride = slot_stride(chunk);
+  uint8_t *slots = static_cast<uint8_t *>(ws);
+  uint32_t *cbytes = reinterpret_cast<uint32_t *>(slots + nch * stride);
+  uint32_t *ckind = cbytes + nch;
+  uint32_t *index = ckind + nch;
+  if (nch > 0) {
+    deflate_encode_kernel<<<nch, kEncThreads, 0, st>>>(in, n, chunk, slots, stride, cbytes, ckind, index);
+    KVTC_LAUNCH_CHECK();
+  }
+  section_layout_kernel<<<1, 1024, 0, st>>>(cbytes, ckind, nch, n, chunk, out, off_dev, section_len_dev);
+  KVTC_LAUNCH_CHECK();
+  if (nch > 0) {
+    section_copy_kernel<<<nch, 256, 0, st>>>(slots, stride, index, nch, out, off_dev);
+    KVTC_LAUNCH_CHECK();
+  }
+  return KVTC_OK;
+}
+
+// ================================================================ decoders
+struct BitReader {
+  const uint8_t *p;
+  uint64_t nbytes;
+  uint64_t pos;   // bit position
+  __device__ uint32_t bits(int n) {
+    uint32_t v = 0;
+    for (int i = 0; i < n; ++i, ++pos) {
+      const uint64_t byte = pos >> 3;
+      const uint32_t b = byte < nbytes ? (p[byte] >> (pos & 7)) & 1u : 0u;
+      v |= b << i;
+    }
+    return v;
+  }
+};
+
+// canonical decode tables (puff style): count[len], symbols sorted by (len, sym)
+struct Huff {
+  int16_t count[16];
+  int16_t symbol[320];
+};
+__device__ int huff_build(Huff &h, const uint8_t *len, int n) {
+  for (int l = 0; l < 16; ++l) h.count[l] = 0;
+  for (int s = 0; s < n; ++s) h.count[len[s]]++;
+  if (h.count[0] == n) return 0;
+  int left = 1;
+  for (int l = 1; l < 16; ++l) {
+    left <<= 1;
+    left -= h.count[l];
+    if (left < 0) return -1;   // over-subscribed
+  }
+  int offs[16];
+  offs[1] = 0;
+  for (int l = 1; l < 15; ++l) offs[l + 1] = offs[l] + h.count[l];
+  for (int s = 0; s < n; ++s)
+    if (len[s]) h.symbol[offs[len[s]]++] = int16_t(s);
+  return left;
+}
+__device__ int huff_decode(BitReader &br, const Huff &h) {
+  int code = 0, first = 0, index = 0;
+  for (int l = 1; l < 16; ++l) {
+    code |= int(br.bits(1));
+    const int count = h.count[l];
+    if (code - count < first) return h.symbol[index + (code - first)];
+    index += count;
+    first += count;
+    first <<= 1;
+    code <<= 1;
+  }
+  return -10;
+}
+
+// Parse a dynamic block header; fills literal/length and distance lengths.
+__device__ int parse_dynamic(BitReader &br, uint8_t *lens, int &nlen, int &ndist) {
+  nlen = int(br.bits(5)) + 257;
+  ndist = int(br.bits(5)) + 1;
+  const int ncode = int(br.bits(4)) + 4;
+  if (nlen > 286 || ndist > 30) return -3;
+  const int order[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
+  uint8_t cl[19];
+  for (int i = 0; i < 19; ++i) cl[i] = 0;
+  for (int i = 0; i < ncode; ++i) cl[order[i]] = uint8_t(br.bits(3));
+  Huff hc;
+  if (huff_build(hc, cl, 19) != 0) return -4;
+  int idx = 0;
+  while (idx < nlen + ndist) {
+    int sym = huff_decode(br, hc);
+    if (sym < 0) return sym;
+    if (sym < 16) {
+      lens[idx++] = uint8_t(sym);
+    } else {
+      int rep = 0;
+      uint8_t v = 0;
+      if (sym == 16) {
+        if (idx == 0) return -5;
+        v = lens[idx - 1];
+        rep = 3 + int(br.bits(2));
+      } else if (sym == 17) {
+        rep = 3 + int(br.bits(3));
+      } else {
+        rep = 11 + int(br.bits(7));
+      }
+      if (idx + rep > nlen + ndist) return -6;
+      while (rep--) lens[idx++] = v;
+    }
+  }
+  if (lens[256] == 0) return -9;
+  return 0;
+}
+
+// ---- fast path: our indexed Huffman-literal chunks, warp per chunk
+struct FastShared {
+  uint16_t table[1024];        // (sym << 4) | len for codes <= 10 bits; 0 = slow
+  Huff h;
+  uint8_t lens[320];
+  int status;
+};
+
+__global__ void __launch_bounds__(32) inflate_fast_kernel(const uint8_t *base, const uint64_t *off_dev,
+                                                          uint64_t n_out, uint32_t nchunks, uint8_t *out,
+                                                          int32_t *err) {
+  __shared__ FastShared S;
+  const uint8_t *section = base + (off_dev ? *off_dev : 0);
+  const SectionHeader *hdr = reinterpret_cast<const SectionHeader *>(section);
+  if (hdr->magic != kSectionMagic || hdr->raw_bytes != n_out || hdr->nchunks != nchunks || hdr->nseg != kNSeg) {
+    if (threadIdx.x == 0) atomicExch(err, -20);
+    return;
+  }
+  const uint32_t c = blockIdx.x;
+  const ChunkEntry e = reinterpret_cast<const ChunkEntry *>(section + sizeof(SectionHeader))[c];
+  const uint32_t *index =
+      reinterpret_cast<const uint32_t *>(section + sizeof(SectionHeader) + uint64_t(hdr->nchunks) * sizeof(ChunkEntry));
+  const uint8_t *stream = section + hdr->data_offset + e.offset;
+  const uint64_t obase = uint64_t(c) * hdr->chunk_bytes;
+  const uint32_t nc = uint32_t(umin64(hdr->chunk_bytes, hdr->raw_bytes - obase));
+  const int lane = threadIdx.x;
+  uint8_t *o = out + obase;
+  if (e.kind == 1) {
+    for (uint32_t i = lane; i < nc; i += 32) o[i] = stream[(i / 32768) * (32768 + 5) + 5 + (i % 32768)];
+    return;
+  }
+  if (lane == 0) {
+    BitReader br{stream, e.bytes, 0};
+    const uint32_t bfinal = br.bits(1), btype = br.bits(2);
+    int nlen, ndist;
+    int st = (btype == 2 && bfinal == 1) ? parse_dynamic(br, S.lens, nlen, ndist) : -1;
+    if (st == 0 && huff_build(S.h, S.lens, 257) < 0) st = -4;
+    S.status = st;
+    if (st) atomicExch(err, st);
+  }
+  __syncwarp();
+  if (S.status) return;
+  // 10-bit lookup table from canonical codes
+  for (int i = lane; i < 1024; i += 32) S.table[i] = 0;
+  __syncwarp();
+  if (lane == 0) {
+    int code = 0, k = 0;
+    for (int l = 1; l <= 15; ++l) {
+      for (int j = 0; j < S.h.count[l]; ++j, ++k, ++code) {
+        if (l <= 10) {
+          const int sym = S.h.symbol[k];
+          const uint32_t rev = __brev(uint32_t(code)) >> (32 - l);
+          for (uint32_t f = rev; f < 1024; f += (1u << l)) S.table[f] = uint16_t((sym << 4) | l);
+        }
+      }
+      code <<= 1;
+    }
+  }
+  __syncwarp();
+  const uint32_t seg = hdr->seg_bytes;
+  const uint32_t s0 = lane * seg, s1 = min(nc, (lane + 1) * seg);
+  if (s0 >= s1) return;
+  const uint32_t *words = reinterpret_cast<const uint32_t *>(stream);
+  uint64_t pos = index[uint64_t(c) * kNSeg + lane];
+  uint64_t wi = pos >> 5;
+  uint64_t buf = uint64_t(words[wi++]) >> (pos & 31);
+  int cnt = 32 - int(pos & 31);
+  uint32_t outw = 0;
+  int nout = 0;
+  for (uint32_t i = s0; i < s1; ++i) {
+    if (cnt <= 32) {
+      buf |= uint64_t(words[wi++]) << cnt;
+      cnt += 32;
+    }
+    const uint16_t te = S.table[buf & 1023];
+    int sym;
+    if (te) {
+      sym = te >> 4;
+      const int l = te & 15;
+      buf >>= l;
+      cnt -= l;
+    } else {
+      // canonical decode for codes longer than 10 bits
+      int code = 0, first = 0, idx = 0;
+      sym = -1;
+      for (int l = 1; l < 16; ++l) {
+        code |= int(buf & 1);
+        buf >>= 1;
+        cnt--;
+        const int count = S.h.count[l];
+        if (code - count < first) {
+          sym = S.h.symbol[idx + (code - first)];
+          break;
+        }
+        idx += count;
+        first += count;
+        first <<= 1;
+        code <<= 1;
+      }
+    }
+    if (sym < 0 || sym > 255) {
+      atomicExch(err, -7);
+      return;
+    }
+    outw |= uint32_t(sym) << (8 * nout);
+    if (++nout == 4) {
+      *reinterpret_cast<uint32_t *>(o + i - 3) = outw;
+      outw = 0;
+      nout = 0;
+    }
+  }
+  for (int k = 0; k < nout; ++k) o[s1 - nout + k] = (outw >> (8 * k)) & 0xFF;
+}
+
+kvtc_status launch_inflate_section(const uint8_t *base, const uint64_t *off_dev, uint64_t n_out, uint32_t nchunks,
+                                   uint8_t *out, int32_t *err, cudaStream_t st) {
+  if (nchunks == 0) return KVTC_OK;
+  inflate_fast_kernel<<<nchunks, 32, 0, st>>>(base, off_dev, n_out, nchunks, out, err);
+  KVTC_LAUNCH_CHECK();
+  return KVTC_OK;
+}
+
+// Validates a section header (host copy) against the expected payload size.
+kvtc_status check_section_header(const void *hdr_host, size_t len, size_t n_out, uint32_t *nchunks) {
+  const SectionHeader *h = static_cast<const SectionHeader *>(hdr_host);
+  if (h->magic != kSectionMagic || h->version != 1 || h->section_bytes > len || h->raw_bytes != n_out ||
+      h->nseg != kNSeg || h->chunk_bytes == 0 || h->nchunks != (n_out + h->chunk_bytes - 1) / h->chunk_bytes) {
+    set_error("corrupt entropy section header");
+    return KVTC_E_CORRUPT;
+  }
+  *nchunks = h->nchunks;
+  return KVTC_OK;
+}
+
+// ---- generic sequential inflater (one thread per stream)
+__constant__ uint16_t c_lbase[29] = {3,  4,  5,  6,  7,  8,  9,  10, 11,  13,  15,  17,  19,  23, 27,
+                                     31, 35, 43, 51, 59, 67, 83, 99, 115, 131, 163, 195, 227, 258};
+__constant__ uint8_t c_lext[29] = {0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 2, 2, 2, 2, 3, 3, 3, 3, 4, 4, 4, 4, 5, 5, 5, 5, 0};
+__constant__ uint16_t c_dbase[30] = {1,   2,   3,   4,   5,   7,    9,    13,   17,   25,   33,   49,   65,    97,    129,
+                                     193, 257, 385, 513, 769, 1025, 1537, 2049, 3073, 4097, 6145, 8193, 12289, 16385, 24577};
+__constant__ uint8_t c_dext[30] = {0, 0, 0, 0, 1, 1, 2, 2, 3, 3, 4, 4, 5, 5, 6, 6, 7, 7, 8, 8, 9, 9, 10, 10, 11, 11, 12, 12, 13, 13};
+
+__global__ void inflate_raw_kernel(const uint8_t *in, const int64_t *in_off, const int64_t *in_len, int32_t nstreams,
+                                   uint8_t *out, const int64_t *out_off, const int64_t *out_len, int32_t *status) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nstreams) return;
+  BitReader br{in + in_off[i], uint64_t(in_len[i]), 0};
+  uint8_t *o = out + out_off[i];
+  const uint64_t cap = uint64_t(out_len[i]);
+  uint64_t w = 0;
+  Huff lit, dist;
+  uint8_t lens[320];
+  int last = 0, st = 0;
+  do {
+    last = int(br.bits(1));
+    const int type = int(br.bits(2));
+    if (type == 0) {
+      br.pos = (br.pos + 7) & ~7ull;
+      const uint32_t len = br.bits(16), nlen = br.bits(16);
+      if ((len ^ 0xFFFFu) != nlen) { st = -2; break; }
+      if ((br.pos >> 3) + len > br.nbytes || w + len > cap) { st = -2; break; }
+      for (uint32_t k = 0; k < len; ++k) o[w++] = br.p[(br.pos >> 3) + k];
+      br.pos += 8ull * len;
+      continue;
+    }
+    int nlen = 288, ndist = 30;
+    if (type == 1) {
+      for (int s = 0; s < 144; ++s) lens[s] = 8;
+      for (int s = 144; s < 256; ++s) lens[s] = 9;
+      for (int s = 256; s < 280; ++s) lens[s] = 7;
+      for (int s = 280; s < 288; ++s) lens[s] = 8;
+      for (int s = 0; s < 30; ++s) lens[288 + s] = 5;
+      huff_build(lit, lens, 288);
+      huff_build(dist, lens + 288, 30);
+    } else if (type == 2) {
+      st = parse_dynamic(br, lens, nlen, ndist);
+      if (st) break;
+      if (huff_build(lit, lens, nlen) < 0 || huff_build(dist, lens + nlen, ndist) < 0) { st = -4; break; }
+    } else {
+      st = -1;
+      break;
+    }
+    for (;;) {
+      int sym = huff_decode(br, lit);
+      if (sym < 0) { st = sym; break; }
+      if (sym < 256) {
+        if (w >= cap) { st = -8; break; }
+        o[w++] = uint8_t(sym);
+      } else if (sym == 256) {
+        break;
+      } else {
+        sym -= 257;
+        if (sym >= 29) { st = -10; break; }
+        const uint32_t len = c_lbase[sym] + br.bits(c_lext[sym]);
+        const int ds = huff_decode(br, dist);
+        if (ds < 0 || ds >= 30) { st = -11; break; }
+        const uint32_t dd = c_dbase[ds] + br.bits(c_dext[ds]);
+        if (dd > w || w + len > cap) { st = -12; break; }
+        for (uint32_t k = 0; k < len; ++k, ++w) o[w] = o[w - dd];
+      }
+    }
+    if (st) break;
+    if (br.pos > 8 * br.nbytes) { st = -13; break; }
+  } while (!last);
+  if (!st && w != cap) st = -14;
+  status[i] = st;
+}
+
+kvtc_status launch_inflate_raw(const uint8_t *in, const int64_t *in_off, const int64_t *in_len, int32_t n,
+                               uint8_t *out, const int64_t *out_off, const int64_t *out_len, int32_t *status,
+                               cudaStream_t st) {
+  if (n == 0) return KVTC_OK;
+  inflate_raw_kernel<<<unsigned(ceil_div(n, 32)), 32, 0, st>>>(in, in_off, in_len, n, out, out_off, out_len, status);
+  KVTC_LAUNCH_CHECK();
+  return KVTC_OK;
+}
+
+}  // namespace kvtc

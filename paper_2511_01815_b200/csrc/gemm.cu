@@ -1,0 +1,422 @@
+// gemm.cu — the tcgen05/TMEM/TMA GEMMs of the KVTC path (K2/K5/K6).
+//
+//   EPI_QUANT  K2  compress: D = X V_c - mu V_c and, straight from
+//                  TMEM, per-(token, group) min/max -> fp16 shift/scale -> codes
+//                  -> bit-pack into the §4 payload.  D never
+//                  reaches HBM.  Groups wider than one tile (1024) are split over
+//                  a thread-block cluster that exchanges row min/max through DSMEM.
+//   EPI_F32        the same GEMM with an fp32 D output (DP coefficients, tests).
+//   EPI_RECON  K5  decompress: X^ = D^ V_d^T + mu, keys
+//                  re-rotated (RoPE, R7), bf16 RNE, scattered into a contiguous
+//                  or paged cache.
+//   EPI_XTX    K6  calibration: S += C^T C over a chunk of rows.
+//
+// One CTA computes a 128 x N (N <= 256) fp32 tile in TMEM.  Warp roles: warp 0
+// TMA producer, warp 1 single-thread tcgen05.mma issuer, warp 2 TMEM allocator,
+// warps 4-7 epilogue (warp w reads TMEM lanes 32*(w%4) .. +31).  Operands are
+// K-major, 128 B swizzled, 4-stage mbarrier pipeline.
+#include "internal.h"
+#include "quant.cuh"
+
+namespace kvtc {
+
+constexpr int kStages = 4;
+constexpr int kABytes = kTileM * kBlockK * 2;      // 16 KiB
+constexpr int kBBytes = kMaxTileN * kBlockK * 2;   // 32 KiB
+constexpr int kStageBytes = kABytes + kBBytes;     // 48 KiB
+constexpr int kStagePitch = 257;                   // fp32 words per staged row (conflict-free)
+constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 2048;
+constexpr int kThreads = 256;
+constexpr int kTmemCols = 256;
+
+enum { EPI_F32 = 0, EPI_QUANT = 1, EPI_RECON = 2, EPI_XTX = 3 };
+
+struct Params {
+  int32_t K;
+  int64_t m;
+  int32_t ncols;       // F32 / XTX: valid N extent; RECON: n_end
+  int32_t n_begin;     // RECON
+  const float *bias;   // F32 / QUANT: [r_nz]; RECON: mu [p]
+  float *D;            // F32 / XTX output
+  int64_t ldd;
+  // QUANT
+  uint8_t *payload;
+  const SegDesc *segs;
+  const GroupDesc *groups;
+  int32_t parts;
+  int32_t G;
+  int64_t tile_bytes;
+  const int64_t *codes_off_last;
+  // RECON
+  const float2 *cs;
+  int32_t layers, heads, head_dim, pairing;
+  int32_t layout, page_tokens;
+  __nv_bfloat16 *const *layer_base;
+  const int32_t *block_table;
+  int64_t tok_begin;
+  int32_t fmt;         // 0 fp16, 1 bf16 operands
+  int32_t tile_n;      // RECON N tile
+};
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ float2 ld_peer_f2(const float2 *local, uint32_t cta) {
+  uint32_t a = smem_u32(local), ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(cta));
+  float2 v;
+  asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(ra) : "memory");
+  return v;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ Params P) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *tiles = smem;
+  uint64_t *full_bar = reinterpret_cast<uint64_t *>(smem + kStages * kStageBytes);
+  uint64_t *empty_bar = full_bar + kStages;
+  uint64_t *tmem_full = empty_bar + kStages;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
+  float2 *red = reinterpret_cast<float2 *>(smem + kStages * kStageBytes + 128);   // [128] row min/max
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int64_t m0 = int64_t(blockIdx.y) * kTileM;
+
+  // tile geometry
+  int n0, ncols;
+  int seg_g0 = 0, seg_g1 = 0;
+  if constexpr (MODE == EPI_QUANT) {
+    const SegDesc sd = P.segs[blockIdx.x];
+    n0 = sd.col0;
+    ncols = sd.width;
+    seg_g0 = sd.g_begin;
+    seg_g1 = sd.g_end;
+  } else if constexpr (MODE == EPI_RECON) {
+    n0 = P.n_begin + blockIdx.x * P.tile_n;
+    ncols = min(P.tile_n, P.ncols - n0);
+  } else {
+    n0 = blockIdx.x * kMaxTileN;
+    ncols = min(kMaxTileN, P.ncols - n0);
+  }
+  const int n_mma = (ncols + 15) & ~15;
+  const int num_kb = (P.K + kBlockK - 1) / kBlockK;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer
+    for (int kb = 0; kb < num_kb; ++kb) {
+      const int s = kb % kStages;
+      if (kb >= kStages) mbar_wait(&empty_bar[s], ((kb / kStages) - 1) & 1);
+      uint8_t *a = tiles + s * kStageBytes;
+      uint8_t *b = a + kABytes;
+      mbar_arrive_expect_tx(&full_bar[s], kStageBytes);
+      tma_load_2d(a, &tmA, &full_bar[s], kb * kBlockK, int32_t(m0));
+      tma_load_2d(b, &tmB, &full_bar[s], kb * kBlockK, n0);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer (one thread)
+    const uint32_t idesc = make_idesc_f16(P.fmt, kTileM, n_mma);
+    for (int kb = 0; kb < num_kb; ++kb) {
+      const int s = kb % kStages;
+      mbar_wait(&full_bar[s], (kb / kStages) & 1);
+      tc_fence_after();
+      const uint64_t ad = make_sdesc_sw128(tiles + s * kStageBytes);
+      const uint64_t bd = make_sdesc_sw128(tiles + s * kStageBytes + kABytes);
+#pragma unroll
+      for (int k = 0; k < kBlockK / 16; ++k)
+        umma_f16(tmem_base, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+      umma_commit(&empty_bar[s]);
+    }
+    umma_commit(tmem_full);
+  }
+
+  // ---------------- epilogue
+  const bool epi = warp >= 4;
+  const int row = (warp & 3) * 32 + lane;                 // TMEM lane == tile row
+  const int64_t tok = m0 + row;
+  const bool valid = tok < P.m;
+  const uint32_t trow = tmem_base + (uint32_t((warp & 3) * 32) << 16);
+  if (epi) {
+    mbar_wait(tmem_full, 0);
+    tc_fence_after();
+  }
+
+  if constexpr (MODE == EPI_F32 || MODE == EPI_XTX) {
+    if (epi) {
+      for (int c = 0; c < n_mma; c += 16) {
+        float v[16];
+        tmem_ld16(trow + c, v);
+        if (valid) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int col = n0 + c + j;
+            if (c + j < ncols) {
+              float *dst = P.D + tok * P.ldd + col;
+              if constexpr (MODE == EPI_F32) *dst = __fsub_rn(v[j], P.bias[col]);
+              else *dst += v[j];
+            }
+          }
+        }
+      }
+    }
+  } else if constexpr (MODE == EPI_QUANT) {
+    // stage this thread's row of D (fp32, minus the bias mu V_c) in shared memory
+    float *stage = reinterpret_cast<float *>(tiles);
+    float *xr = stage + row * kStagePitch;
+    if (epi) {
+      for (int c = 0; c < n_mma; c += 16) {
+        float v[16];
+        tmem_ld16(trow + c, v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) xr[c + j] = (c + j < ncols) ? __fsub_rn(v[j], P.bias[n0 + c + j]) : 0.0f;
+      }
+    }
+    const int ntok = int(P.m - m0 < kTileM ? P.m - m0 : kTileM);
+    const bool last = ntok < kTileM;
+    uint8_t *tile_base = P.payload + (m0 / kTileM) * P.tile_bytes;
+    float rmn = 0.f, rmx = 0.f;
+    if (P.parts > 1) {
+      // split group: one piece per CTA; exchange row min/max over the cluster (DSMEM)
+      const GroupDesc gd = P.groups[seg_g0];
+      if (epi) {
+        float mn = xr[gd.col], mx = xr[gd.col];
+        for (int c = 1; c < gd.size; ++c) {
+          mn = fminf(mn, xr[gd.col + c]);
+          mx = fmaxf(mx, xr[gd.col + c]);
+        }
+        red[row] = make_float2(mn, mx);
+      }
+      cluster_sync_all();
+      if (epi) {
+        rmn = red[row].x;
+        rmx = red[row].y;
+        for (int q = 0; q < P.parts; ++q) {
+          const float2 o = ld_peer_f2(&red[row], q);
+          rmn = fminf(rmn, o.x);
+          rmx = fmaxf(rmx, o.y);
+        }
+      }
+      cluster_sync_all();
+    }
+    if (epi) {
+      for (int gi = seg_g0; gi < seg_g1; ++gi) {
+        const GroupDesc gd = P.groups[gi];
+        const float *x = xr + gd.col;
+        float mn, mx;
+        if (P.parts > 1) {
+          mn = rmn;
+          mx = rmx;
+        } else {
+          mn = x[0];
+          mx = x[0];
+          for (int c = 1; c < gd.size; ++c) {
+            mn = fminf(mn, x[c]);
+            mx = fmaxf(mx, x[c]);
+          }
+        }
+        uint8_t *cb = tile_base + (last ? P.codes_off_last[gd.gidx] : gd.codes_off);
+        emit_group(x, gd.size, gd.full_size, gd.part, gd.type, gd.gidx, mn, mx, valid, row, lane, (warp & 3) * 32,
+                   ntok, last, tile_base, cb);
+      }
+    }
+  } else if constexpr (MODE == EPI_RECON) {
+    if (epi) {
+      // tcgen05.ld is warp-collective: every lane loads, only valid rows store
+      const int d = P.head_dim;
+      const int hd = P.heads * d;
+      const int layer = n0 / hd;
+      const int head0 = (n0 % hd) / d;
+      const int64_t ctok = P.tok_begin + tok;
+      __nv_bfloat16 *rowp = nullptr;
+      if (valid) {
+        int64_t slot = ctok;
+        if (P.layout == KVTC_LAYOUT_PAGED)
+          slot = int64_t(P.block_table[ctok / P.page_tokens]) * P.page_tokens + (ctok % P.page_tokens);
+        rowp = P.layer_base[layer] + slot * hd;
+      }
+      const float2 *cs = (P.cs && valid) ? P.cs + tok * (d / 2) : nullptr;
+      const bool rot = P.cs != nullptr;
+      for (int hh = 0; hh < ncols / d; ++hh) {
+        const int f = n0 + hh * d;                         // first feature of the head
+        __nv_bfloat16 *dst = valid ? rowp + (head0 + hh) * d : nullptr;
+        if (P.pairing == 0 || !rot) {
+          for (int c = 0; c < d / 2; c += 16) {
+            float lo[16], hi[16];
+            tmem_ld16(trow + hh * d + c, lo);
+            tmem_ld16(trow + hh * d + d / 2 + c, hi);
+            if (!valid) continue;
+            if (num_kb == 0) {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) lo[j] = hi[j] = 0.0f;
+            }
+            __align__(16) __nv_bfloat16 olo[16], ohi[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const float x1 = __fadd_rn(lo[j], P.bias[f + c + j]);
+              const float x2 = __fadd_rn(hi[j], P.bias[f + d / 2 + c + j]);
+              float y1 = x1, y2 = x2;
+              if (rot) {
+                const float2 t = cs[c + j];
+                y1 = __fsub_rn(__fmul_rn(x1, t.x), __fmul_rn(x2, t.y));
+                y2 = __fadd_rn(__fmul_rn(x2, t.x), __fmul_rn(x1, t.y));
+              }
+              olo[j] = __float2bfloat16_rn(y1);
+              ohi[j] = __float2bfloat16_rn(y2);
+            }
+            uint4 *a = reinterpret_cast<uint4 *>(dst + c);
+            uint4 *b = reinterpret_cast<uint4 *>(dst + d / 2 + c);
+            a[0] = reinterpret_cast<uint4 *>(olo)[0];
+            a[1] = reinterpret_cast<uint4 *>(olo)[1];
+            b[0] = reinterpret_cast<uint4 *>(ohi)[0];
+            b[1] = reinterpret_cast<uint4 *>(ohi)[1];
+          }
+        } else {
+          for (int c = 0; c < d; c += 16) {
+            float v[16];
+            tmem_ld16(trow + hh * d + c, v);
+            if (!valid) continue;
+            if (num_kb == 0) {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) v[j] = 0.0f;
+            }
+            __align__(16) __nv_bfloat16 o[16];
+#pragma unroll
+            for (int j = 0; j < 16; j += 2) {
+              const float x1 = __fadd_rn(v[j], P.bias[f + c + j]);
+              const float x2 = __fadd_rn(v[j + 1], P.bias[f + c + j + 1]);
+              const float2 t = cs[(c + j) / 2];
+              o[j] = __float2bfloat16_rn(__fsub_rn(__fmul_rn(x1, t.x), __fmul_rn(x2, t.y)));
+              o[j + 1] = __float2bfloat16_rn(__fadd_rn(__fmul_rn(x2, t.x), __fmul_rn(x1, t.y)));
+            }
+            uint4 *a = reinterpret_cast<uint4 *>(dst + c);
+            a[0] = reinterpret_cast<uint4 *>(o)[0];
+            a[1] = reinterpret_cast<uint4 *>(o)[1];
+          }
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<kTmemCols>(tmem_base);
+}
+
+template <int MODE>
+static kvtc_status launch(const CUtensorMap *tmA, const CUtensorMap *tmB, const Params &p, dim3 grid, int cluster,
+                          cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    KVTC_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    if (MODE == EPI_QUANT)
+      KVTC_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<MODE>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    configured = true;
+  }
+  if (grid.x == 0 || grid.y == 0) return KVTC_OK;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  KVTC_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_kernel<MODE>, *tmA, *tmB, p));
+  return KVTC_OK;
+}
+
+kvtc_status launch_gemm_project_f32(const GemmCompressArgs &a, int32_t ncols, cudaStream_t st) {
+  Params p = {};
+  p.K = a.K;
+  p.m = a.m;
+  p.ncols = ncols;
+  p.bias = a.bias;
+  p.D = a.D;
+  p.ldd = a.ldd;
+  p.fmt = 1;
+  dim3 grid(unsigned(ceil_div(ncols, kMaxTileN)), unsigned(ceil_div(a.m, kTileM)));
+  return launch<EPI_F32>(a.tmA, a.tmB, p, grid, 1, st);
+}
+
+kvtc_status launch_gemm_project_quant(const GemmCompressArgs &a, cudaStream_t st) {
+  Params p = {};
+  p.K = a.K;
+  p.m = a.m;
+  p.bias = a.bias;
+  p.payload = a.payload;
+  p.segs = a.segs;
+  p.groups = a.groups;
+  p.parts = a.parts;
+  p.G = a.G;
+  p.tile_bytes = a.tile_bytes;
+  p.codes_off_last = a.codes_off_last;
+  p.fmt = 1;
+  dim3 grid(unsigned(a.nsegs), unsigned(ceil_div(a.m, kTileM)));
+  return launch<EPI_QUANT>(a.tmA, a.tmB, p, grid, a.parts, st);
+}
+
+kvtc_status launch_gemm_reconstruct(const GemmDecompressArgs &a, cudaStream_t st) {
+  Params p = {};
+  p.K = a.K;
+  p.m = a.m;
+  p.n_begin = a.n_begin;
+  p.ncols = a.n_end;
+  p.bias = a.mu;
+  p.cs = a.cs;
+  p.layers = a.layers;
+  p.heads = a.heads;
+  p.head_dim = a.head_dim;
+  p.pairing = a.pairing;
+  p.layout = a.layout;
+  p.page_tokens = a.page_tokens;
+  p.layer_base = a.layer_base;
+  p.block_table = a.block_table;
+  p.tok_begin = a.tok_begin;
+  p.fmt = 0;
+  p.tile_n = a.tile_n;
+  dim3 grid(unsigned(ceil_div(a.n_end - a.n_begin, a.tile_n)), unsigned(ceil_div(a.m, kTileM)));
+  return launch<EPI_RECON>(a.tmA, a.tmB, p, grid, 1, st);
+}
+
+kvtc_status launch_gemm_xtx(const CUtensorMap *tmA, const CUtensorMap *tmB, int32_t p_, int32_t nk, float *S,
+                            cudaStream_t st) {
+  Params p = {};
+  p.K = nk;
+  p.m = p_;
+  p.ncols = p_;
+  p.D = S;
+  p.ldd = p_;
+  p.fmt = 1;
+  dim3 grid(unsigned(ceil_div(p_, kMaxTileN)), unsigned(ceil_div(p_, kTileM)));
+  return launch<EPI_XTX>(tmA, tmB, p, grid, 1, st);
+}
+
+}  // namespace kvtc

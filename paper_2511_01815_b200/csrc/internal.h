@@ -1,0 +1,141 @@
+// internal.h — host-side objects and kernel launchers shared by the library's
+// translation units (not part of the ABI).
+#pragma once
+
+#include <map>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+
+namespace kvtc {
+
+// One non-None group of a plan (PC order).  `col` is the column in the
+// compacted operand space (non-None PCs only, in order).
+struct PlanGroup {
+  int32_t start, size, type, col;
+};
+
+// Device descriptor of one piece of a group handled by one GEMM tile.
+struct GroupDesc {
+  int32_t col;        // first column inside the tile (0..255)
+  int32_t size;       // columns of this piece (<= 256)
+  int32_t full_size;  // group size (pieces of a split group: size * parts)
+  int32_t type;       // kvtc_type
+  int32_t gidx;       // index of the group among non-None groups (params slot)
+  int32_t part;       // piece index inside a split group
+  int64_t codes_off;  // byte offset of the group's code block in a FULL tile
+};
+struct SegDesc {
+  int32_t col0;       // first compacted column of the tile
+  int32_t width;      // columns used
+  int32_t g_begin, g_end;  // GroupDesc range
+};
+
+// Operands of a (basis, plan) pair, compacted to the plan's non-None PCs.
+struct Operands {
+  int32_t r_nz = 0, r_nz_pad = 0;
+  __nv_bfloat16 *VcT = nullptr;  // [r_nz x p]  rows = PCs (compress B operand, K-major)
+  float *bias = nullptr;         // [r_nz] mu V_c (fp32)
+  __half *Vd = nullptr;          // [p x r_nz_pad] (decompress B operand, K-major)
+  CUtensorMap tm_VcT, tm_Vd;
+  bool ready = false;
+};
+
+struct kvtc_basis_impl;
+struct kvtc_plan_impl;
+
+// CUDA driver entry point for cuTensorMapEncodeTiled (no libcuda link needed)
+kvtc_status make_tmap_2d(CUtensorMap *m, const void *base, CUtensorMapDataType dt, uint64_t inner, uint64_t outer,
+                         uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer);
+
+// ------------------------------------------------------------------ launchers
+struct GemmCompressArgs {
+  const CUtensorMap *tmA;  // X [m x p] bf16, box {64, 128}
+  const CUtensorMap *tmB;  // VcT [r_nz x p] bf16, box {64, 256}
+  int32_t K;               // p
+  int64_t m;
+  const float *bias;       // [r_nz]
+  // mode F32
+  float *D;                // [m x ldd]
+  int64_t ldd;
+  // mode quantise
+  uint8_t *payload;
+  const SegDesc *segs;
+  const GroupDesc *groups;
+  int32_t nsegs;
+  int32_t parts;           // cluster size along x (1 = unsplit)
+  int32_t G;               // number of non-None groups
+  int64_t tile_bytes;      // bytes of a full tile
+  const int64_t *codes_off_last;  // [G] code-block offsets of the last partial tile
+};
+kvtc_status launch_gemm_project_f32(const GemmCompressArgs &a, int32_t ncols, cudaStream_t st);
+kvtc_status launch_gemm_project_quant(const GemmCompressArgs &a, cudaStream_t st);
+
+struct GemmDecompressArgs {
+  const CUtensorMap *tmA;  // D^ [m x r_nz_pad] fp16, box {64, 128}
+  const CUtensorMap *tmB;  // Vd [p x r_nz_pad] fp16, box {64, 256}
+  int32_t K;               // r_nz_pad
+  int64_t m;
+  int32_t n_begin, n_end;  // feature range (multiple of 256)
+  const float *mu;         // [p]
+  const float2 *cs;        // [m x d/2] cos/sin (keys) or nullptr
+  int32_t layers, heads, head_dim, pairing;
+  // output view
+  int32_t layout, page_tokens;
+  __nv_bfloat16 *const *layer_base;  // device array [layers]
+  const int32_t *block_table;
+  int64_t tok_begin;                 // cache token index of row 0
+  int32_t tile_n;                    // N tile (<= 256, divides heads*head_dim)
+};
+kvtc_status launch_gemm_reconstruct(const GemmDecompressArgs &a, cudaStream_t st);
+
+// XtX accumulation: S[p x p] += C^T C for a chunk Ct [p x nk] (K-major);
+// tmA box {64, 128}, tmB box {64, 256} over the same Ct.
+kvtc_status launch_gemm_xtx(const CUtensorMap *tmA, const CUtensorMap *tmB, int32_t p, int32_t nk, float *S,
+                            cudaStream_t st);
+
+// elementwise.cu
+kvtc_status launch_rope_table(const float *invf_dev, int32_t half, int64_t pos_first, int64_t n, float2 *cs,
+                              cudaStream_t st);
+kvtc_status launch_gather(const kvtc_kv_view &v, __nv_bfloat16 *const *layer_base_dev, int64_t tok_begin,
+                          int64_t ntok, const float2 *cs, int32_t pairing, __nv_bfloat16 *X, cudaStream_t st);
+kvtc_status launch_gather_rows(const kvtc_kv_view *seqs, int32_t nseq, __nv_bfloat16 *const *bases_dev,
+                               const int64_t *rows_dev, int64_t n, const float *invf_dev, int32_t unrope,
+                               int32_t pairing, int64_t ld, __nv_bfloat16 *X, cudaStream_t st);
+kvtc_status launch_quant_pack_simt(const SegDesc *segs, const GroupDesc *groups, int32_t nsegs, int32_t G,
+                                   const float *D, int64_t ldd, int64_t m, int64_t tile_bytes,
+                                   const int64_t *codes_off_last, uint8_t *payload, cudaStream_t st);
+kvtc_status launch_codes_off_last(const int32_t *gsize, const int32_t *gbits, int32_t G, int32_t ntok,
+                                  int64_t *out, cudaStream_t st);
+kvtc_status launch_dequant(const PlanGroup *groups_dev, const int64_t *codes_off_full, int32_t G,
+                           const int64_t *codes_off_last, int64_t tile_bytes, const uint8_t *payload, int64_t m,
+                           __half *Dh, int64_t ld, cudaStream_t st);
+kvtc_status launch_copy_tokens(const kvtc_kv_view &src, __nv_bfloat16 *const *src_bases, int64_t src_tok,
+                               const kvtc_kv_view &dst, __nv_bfloat16 *const *dst_bases, int64_t dst_tok,
+                               int64_t ntok, int32_t layer_begin, int32_t layer_end, cudaStream_t st);
+// raw token rows packed as [layers][ntok][h*d] in a flat buffer
+kvtc_status launch_pack_raw(const kvtc_kv_view &src, __nv_bfloat16 *const *bases, int64_t tok, int64_t ntok,
+                            __nv_bfloat16 *dst, int64_t flat_ntok, int64_t flat_tok0, cudaStream_t st);
+kvtc_status launch_unpack_raw(const __nv_bfloat16 *src, int64_t ntok_total, int64_t src_tok0, int64_t ntok,
+                              const kvtc_kv_view &dst, __nv_bfloat16 *const *bases, int64_t dst_tok,
+                              int32_t layer_begin, int32_t layer_end, cudaStream_t st);
+
+// deflate.cu
+size_t deflate_section_bound(size_t n, int32_t chunk);
+size_t deflate_workspace(size_t n, int32_t chunk);
+// Writes the section (header, chunk table, index, data) to out; sizes on device;
+// *section_len_dev receives the section length (device uint64).
+// The section is written at out + (off_dev ? *off_dev : 0) (device offset).
+kvtc_status launch_deflate(const uint8_t *in, size_t n, int32_t chunk, uint8_t *out, const uint64_t *off_dev,
+                           uint64_t *section_len_dev, void *ws, size_t ws_bytes, cudaStream_t st);
+kvtc_status launch_inflate_section(const uint8_t *base, const uint64_t *off_dev, uint64_t n_out, uint32_t nchunks,
+                                   uint8_t *out, int32_t *err, cudaStream_t st);
+kvtc_status check_section_header(const void *hdr_host, size_t len, size_t n_out, uint32_t *nchunks);
+constexpr size_t kSectionHeaderBytes = 64;
+kvtc_status launch_inflate_raw(const uint8_t *in, const int64_t *in_off, const int64_t *in_len, int32_t n,
+                               uint8_t *out, const int64_t *out_off, const int64_t *out_len, int32_t *status,
+                               cudaStream_t st);
+
+}  // namespace kvtc

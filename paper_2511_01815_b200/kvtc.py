@@ -1,0 +1,284 @@
+"""Thin Python binding over the C ABI (include/kvtc.h).
+
+Argument marshalling only: torch tensors provide device memory and streams;
+every step of the path runs in libkvtc.so's sm_100a kernels.  Names follow the
+C entry points (kvtc_<name>).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from ._lib import check, lib
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _ptr(t: torch.Tensor | None):
+    return C.c_void_p(0 if t is None else t.data_ptr())
+
+
+def _f32p(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_float))
+
+
+def _i32p(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+def device_check() -> None:
+    check(lib().kvtc_device_check())
+
+
+# ------------------------------------------------------------------- views
+class KVView:
+    """A cache of one stream as the C ABI sees it (kvtc_kv_view).
+
+    contiguous: tensor [layers, tokens, kv_heads, head_dim] bf16 (or a list of
+    per-layer [tokens, kv_heads, head_dim] tensors);
+    paged: pages [layers, num_pages, page_tokens, kv_heads, head_dim] bf16 and
+    block_table int32 [ceil(tokens / page_tokens)] on the device."""
+
+    def __init__(self, cache, pos0: int = 0, tokens: int | None = None, block_table: torch.Tensor | None = None):
+        layers = list(cache) if isinstance(cache, (list, tuple)) else [cache[i] for i in range(cache.shape[0])]
+        for t in layers:
+            assert t.dtype == torch.bfloat16 and t.is_cuda and t.is_contiguous()
+        self._keep = (cache, layers, block_table)
+        paged = block_table is not None
+        if paged:
+            _, page_tokens, h, d = layers[0].shape
+            assert tokens is not None
+        else:
+            t0, h, d = layers[0].shape
+            tokens = t0 if tokens is None else tokens
+            page_tokens = 0
+        self.shape = (len(layers), h, d)
+        self.tokens = tokens
+        self.pos0 = pos0
+        self._bases = (C.c_void_p * len(layers))(*[x.data_ptr() for x in layers])
+        self.c = L.View(L.Shape(len(layers), h, d), tokens, pos0, L.LAYOUT_PAGED if paged else L.LAYOUT_CONTIGUOUS,
+                        page_tokens, C.cast(self._bases, C.POINTER(C.c_void_p)),
+                        C.c_void_p(block_table.data_ptr() if paged else 0), 1, 0)
+
+
+def _rope(inv_freq, pairing: int):
+    a = np.ascontiguousarray(np.asarray(inv_freq, dtype=np.float32))
+    return L.Rope(_f32p(a), pairing), a
+
+
+# ------------------------------------------------------------------- basis
+class Basis:
+    """kvtc_basis: mu, V (fp32 master) -> bf16 / fp16 GEMM operands (R2, R6)."""
+
+    def __init__(self, handle, shape, which):
+        self.h = C.c_void_p(handle) if not isinstance(handle, C.c_void_p) else handle
+        self.shape = shape
+        self.which = which
+
+    @classmethod
+    def create(cls, shape, which: int, mu, V, sigma=None, inv_freq=None, pairing: int = 0) -> "Basis":
+        mu = np.ascontiguousarray(np.asarray(mu, dtype=np.float32))
+        V = np.ascontiguousarray(np.asarray(V, dtype=np.float32))
+        r = V.shape[1]
+        sg = None if sigma is None else np.ascontiguousarray(np.asarray(sigma, dtype=np.float32))
+        rope, keep = _rope(inv_freq, pairing) if inv_freq is not None else (None, None)
+        out = C.c_void_p()
+        check(lib().kvtc_basis_create(C.byref(L.Shape(*shape)), which, C.byref(rope) if rope else None, r,
+                                      _f32p(mu), _f32p(V), _f32p(sg) if sg is not None else None, C.byref(out)))
+        return cls(out, tuple(shape), which)
+
+    def get(self):
+        p, r = C.c_int32(), C.c_int32()
+        check(lib().kvtc_basis_get(self.h, C.byref(p), C.byref(r), None, None, None))
+        mu = np.empty(p.value, np.float32)
+        V = np.empty((p.value, r.value), np.float32)
+        sg = np.empty(r.value, np.float32)
+        check(lib().kvtc_basis_get(self.h, None, None, _f32p(mu), _f32p(V), _f32p(sg)))
+        return mu, V, sg
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().kvtc_basis_destroy(self.h)
+        except Exception:
+            pass
+
+
+# -------------------------------------------------------------------- plan
+@dataclass
+class PlanInfo:
+    r: int
+    groups: list          # [(start, size, type)]
+    bits_per_token: int
+    r_eff: int
+    expected_error: float
+    budget: int
+
+
+class Plan:
+    def __init__(self, handle):
+        self.h = handle if isinstance(handle, C.c_void_p) else C.c_void_p(handle)
+
+    @classmethod
+    def create(cls, r: int, groups) -> "Plan":
+        g = np.asarray(groups, dtype=np.int32).reshape(-1, 3)
+        st, sz, tp = (np.ascontiguousarray(g[:, i]) for i in range(3))
+        out = C.c_void_p()
+        check(lib().kvtc_plan_create(r, len(g), _i32p(st), _i32p(sz), _i32p(tp), C.byref(out)))
+        return cls(out)
+
+    def info(self) -> PlanInfo:
+        r, n = C.c_int32(), C.c_int32()
+        check(lib().kvtc_plan_get(self.h, C.byref(r), C.byref(n), None, None, None, None, None, None, None))
+        st, sz, tp = (np.empty(max(1, n.value), np.int32) for _ in range(3))
+        bits, reff, err, bud = C.c_int64(), C.c_int32(), C.c_double(), C.c_int64()
+        check(lib().kvtc_plan_get(self.h, None, C.byref(n), _i32p(st), _i32p(sz), _i32p(tp), C.byref(bits),
+                                  C.byref(reff), C.byref(err), C.byref(bud)))
+        groups = [(int(st[i]), int(sz[i]), int(tp[i])) for i in range(n.value)]
+        return PlanInfo(r.value, groups, bits.value, reff.value, err.value, bud.value)
+
+    def payload_bytes(self, m: int) -> int:
+        return int(lib().kvtc_payload_bytes(self.h, m))
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().kvtc_plan_destroy(self.h)
+        except Exception:
+            pass
+
+
+# ------------------------------------------------------------ stage calls
+def gather(view: KVView, tok_begin: int, ntok: int, unrope: bool, inv_freq=None, pairing: int = 0, stream=None):
+    p = view.shape[0] * view.shape[1] * view.shape[2]
+    X = torch.empty(ntok, p, dtype=torch.bfloat16, device="cuda")
+    rope, keep = _rope(inv_freq, pairing) if unrope else (None, None)
+    check(lib().kvtc_stage_gather(C.byref(view.c), tok_begin, ntok, int(unrope), C.byref(rope) if rope else None,
+                                  _ptr(X), _stream(stream)))
+    return X
+
+
+def project(basis: Basis, plan: Plan | None, X: torch.Tensor, ncols: int, stream=None):
+    D = torch.empty(X.shape[0], ncols, dtype=torch.float32, device="cuda")
+    check(lib().kvtc_stage_project(basis.h, plan.h if plan else None, _ptr(X), X.shape[0], _ptr(D), _stream(stream)))
+    return D
+
+
+def quantize_pack(plan: Plan, D: torch.Tensor, stream=None):
+    m = D.shape[0]
+    out = torch.zeros(plan.payload_bytes(m) + 16, dtype=torch.uint8, device="cuda")
+    check(lib().kvtc_stage_quantize_pack(plan.h, _ptr(D), m, _ptr(out), _stream(stream)))
+    return out[: plan.payload_bytes(m)]
+
+
+def project_quantize(basis: Basis, plan: Plan, X: torch.Tensor, stream=None):
+    m = X.shape[0]
+    out = torch.zeros(plan.payload_bytes(m) + 16, dtype=torch.uint8, device="cuda")
+    check(lib().kvtc_stage_project_quantize(basis.h, plan.h, _ptr(X), m, _ptr(out), _stream(stream)))
+    return out[: plan.payload_bytes(m)]
+
+
+def deflate(data: torch.Tensor, chunk_bytes: int = 65536, stream=None):
+    n = data.numel()
+    cap = int(lib().kvtc_deflate_bound(n, chunk_bytes))
+    out = torch.zeros(cap + 16, dtype=torch.uint8, device="cuda")
+    wsb = int(lib().kvtc_deflate_workspace_bytes(n, chunk_bytes))
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    ln = C.c_size_t()
+    check(lib().kvtc_stage_deflate(_ptr(data), n, chunk_bytes, _ptr(out), cap + 16, C.byref(ln), _ptr(ws), wsb,
+                                   _stream(stream)))
+    return out[: ln.value]
+
+
+def inflate(section: torch.Tensor, n_out: int, stream=None):
+    out = torch.empty(n_out + 16, dtype=torch.uint8, device="cuda")
+    sec = torch.zeros(section.numel() + 64, dtype=torch.uint8, device="cuda")
+    sec[: section.numel()] = section
+    check(lib().kvtc_stage_inflate(_ptr(sec), section.numel(), _ptr(out), n_out, _stream(stream)))
+    return out[:n_out]
+
+
+def inflate_raw(streams: list, out_lens: list, stream=None):
+    """Generic inflate of independent raw DEFLATE streams (e.g. zlib wbits=-15)."""
+    in_off = np.cumsum([0] + [len(s) for s in streams])[:-1].astype(np.int64)
+    out_off = np.cumsum([0] + list(out_lens))[:-1].astype(np.int64)
+    blob = np.frombuffer(b"".join(streams) + b"\0" * 16, dtype=np.uint8)
+    dev = torch.from_numpy(blob.copy()).cuda()
+    t = lambda a: torch.from_numpy(np.asarray(a, dtype=np.int64)).cuda()
+    out = torch.zeros(int(sum(out_lens)) + 16, dtype=torch.uint8, device="cuda")
+    status = torch.zeros(len(streams), dtype=torch.int32, device="cuda")
+    ioff, ilen, ooff, olen = t(in_off), t([len(s) for s in streams]), t(out_off), t(out_lens)
+    check(lib().kvtc_stage_inflate_raw(_ptr(dev), _ptr(ioff), _ptr(ilen), len(streams), _ptr(out), _ptr(ooff),
+                                       _ptr(olen), _ptr(status), _stream(stream)))
+    torch.cuda.synchronize()
+    return out[: int(sum(out_lens))], status
+
+
+def dequantize(plan: Plan, payload: torch.Tensor, m: int, ld: int | None = None, stream=None):
+    ncols = sum(z for (_, z, _) in plan.info().groups)
+    ld = ld or max(8, (ncols + 7) // 8 * 8)
+    Dh = torch.zeros(m, ld, dtype=torch.float16, device="cuda")
+    check(lib().kvtc_stage_dequantize(plan.h, _ptr(payload), m, _ptr(Dh), ld, _stream(stream)))
+    return Dh
+
+
+def reconstruct(basis: Basis, plan: Plan, Dh: torch.Tensor, m: int, tok_begin: int, layer_begin: int,
+                layer_end: int, out: KVView, stream=None):
+    check(lib().kvtc_stage_reconstruct(basis.h, plan.h, _ptr(Dh), Dh.shape[1], m, tok_begin, layer_begin, layer_end,
+                                       C.byref(out.c), _stream(stream)))
+
+
+# ------------------------------------------------------------------ codec
+def compress(kb: Basis, kp: Plan, vb: Basis, vp: Plan, k: KVView, v: KVView, sinks: int = 4, window: int = 128,
+             chunk_bytes: int = 65536, stream=None, out: torch.Tensor | None = None, workspace=None,
+             sync_len: bool = True):
+    """Returns (container tensor [len], status)."""
+    pol = L.Policy(sinks, window, chunk_bytes)
+    cap = int(lib().kvtc_compress_bound(kp.h, vp.h, C.byref(k.c), C.byref(pol)))
+    wsb = int(lib().kvtc_compress_workspace_bytes(kb.h, kp.h, vb.h, vp.h, C.byref(k.c), C.byref(pol)))
+    if out is None:
+        out = torch.empty(cap, dtype=torch.uint8, device="cuda")
+    if workspace is None:
+        workspace = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    ln = C.c_size_t(0)
+    st = check(lib().kvtc_compress(kb.h, kp.h, vb.h, vp.h, C.byref(k.c), C.byref(v.c), C.byref(pol), _ptr(out),
+                                   out.numel(), C.byref(ln) if sync_len else None, _ptr(workspace),
+                                   workspace.numel(), _stream(stream)),
+               allow=(L.KVTC_OK, L.KVTC_NOTHING_TO_COMPRESS))
+    return (out[: ln.value] if sync_len else out), st
+
+
+def compress_sizes(kb, kp, vb, vp, k: KVView, sinks=4, window=128, chunk_bytes=65536):
+    pol = L.Policy(sinks, window, chunk_bytes)
+    cap = int(lib().kvtc_compress_bound(kp.h, vp.h, C.byref(k.c), C.byref(pol)))
+    wsb = int(lib().kvtc_compress_workspace_bytes(kb.h, kp.h, vb.h, vp.h, C.byref(k.c), C.byref(pol)))
+    return cap, wsb
+
+
+def container_info(container: torch.Tensor) -> L.ContainerInfo:
+    hdr = container[: L.HEADER_BYTES].cpu().numpy().tobytes()
+    info = L.ContainerInfo()
+    check(lib().kvtc_container_parse(C.c_char_p(hdr), C.byref(info)))
+    return info
+
+
+def decompress_workspace_bytes(kb, kp, vb, vp, header: bytes) -> int:
+    return int(lib().kvtc_decompress_workspace_bytes(kb.h, kp.h, vb.h, vp.h, C.c_char_p(header)))
+
+
+def decompress(kb: Basis, kp: Plan, vb: Basis, vp: Plan, container: torch.Tensor, k_out: KVView, v_out: KVView,
+               layer_begin: int = 0, layer_end: int | None = None, stream=None, workspace=None):
+    layer_end = k_out.shape[0] if layer_end is None else layer_end
+    if workspace is None:
+        hdr = container[: L.HEADER_BYTES].cpu().numpy().tobytes()
+        workspace = torch.empty(decompress_workspace_bytes(kb, kp, vb, vp, hdr), dtype=torch.uint8, device="cuda")
+    check(lib().kvtc_decompress(kb.h, kp.h, vb.h, vp.h, _ptr(container), container.numel(), layer_begin, layer_end,
+                                C.byref(k_out.c), C.byref(v_out.c), _ptr(workspace), workspace.numel(),
+                                _stream(stream)))

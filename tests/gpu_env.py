@@ -1,0 +1,146 @@
+"""Shared seeded setups for the GPU parity tests (inputs from kvtc_inputs,
+expected values from oracle/ only)."""
+from __future__ import annotations
+
+import functools
+
+import numpy as np
+import torch
+
+from oracle import layout as OL
+
+from kvtc_inputs import make_spec, generate, sample_positions
+from oracle import dp as ODP
+from oracle import pca as OPCA
+from oracle import quant as OQ
+
+T1, T2, T4, T8 = OQ.T_NONE, OQ.T_INT2, OQ.T_INT4, OQ.T_FP8
+
+
+@functools.lru_cache(maxsize=None)
+def setup(name: str):
+    """(spec, invf, bases(k, v), calibration matrices) from the oracle."""
+    if name == "toy":
+        spec = make_spec("toy")
+        tcal, ncal = 2048, 2000
+    elif name == "mid":
+        # 2 layers x 8 heads x 128 = p 2048: several N tiles, a 1024-group split
+        spec = make_spec("toy", name="mid", layers=2, kv_heads=8, head_dim=128, latent=256, rope_base=500000.0)
+        tcal, ncal = 3200, 3000
+    else:
+        raise KeyError(name)
+    invf = spec.inv_freq().double().numpy()
+    cal = [generate(spec, st, tcal, pos0=0, conversation=100).double().numpy() for st in (0, 1)]
+    samples = sample_positions([tcal], ncal, sinks=spec.sinks, seed=1)
+    Ck = OPCA.gather([(cal[0], 0)], samples, True, invf)
+    Cv = OPCA.gather([(cal[1], 0)], samples, False)
+    kb = OPCA.fit(Ck, 10000)
+    vb = OPCA.fit(Cv, 10000)
+    return spec, invf, kb, vb, Ck, Cv
+
+
+def mid_plan_groups():
+    """Explicit plan over 2048 PCs covering every size/type path, None gaps
+    included, and a 1024-wide group (cluster-split in the fused kernel)."""
+    g = []
+    c = 0
+    for t in (T2, T2, T8, T4, T2):                  # size-1 groups (sub-byte and byte)
+        g.append((c, 1, t)); c += 1
+    for t in (T4, T4, T8, T2):
+        g.append((c, 16, t)); c += 16
+    c += 3                                          # None gap
+    for t in (T4, T2, T8):
+        g.append((c, 64, t)); c += 64
+    g.append((c, 256, T2)); c += 256
+    g.append((c, 1024, T2)); c += 1024
+    c += 40                                         # None gap
+    g.append((c, 256, T8)); c += 256
+    assert c <= 2048
+    return g
+
+
+def toy_plans(cr: float = 16):
+    spec, invf, kb, vb, Ck, Cv = setup("toy")
+    kp, _, _ = ODP.allocate(OPCA.dp_coefficients(kb, Ck), cr, spec.p)
+    vp, _, _ = ODP.allocate(OPCA.dp_coefficients(vb, Cv), cr, spec.p)
+    return kp, vp
+
+
+def caches(name: str, tokens: int, pos0: int = 0, conversation: int = 0):
+    spec = setup(name)[0]
+    K = generate(spec, 0, tokens, pos0=pos0, conversation=conversation)
+    V = generate(spec, 1, tokens, pos0=pos0, conversation=conversation)
+    return K, V
+
+
+def boundary_distance(D_ref, shift, scale, t):
+    """Distance (in D units) from each oracle coefficient to the nearest decision
+    boundary of its quantiser (int-k: shift + (k + 1/2) scale; fp8: midpoints of
+    the E4M3 grid times scale, plus shift)."""
+    sc = np.where(scale[:, None] == 0, 1.0, scale[:, None])
+    y = (D_ref - shift[:, None]) / sc
+    if t in (T2, T4):
+        d = np.abs(y - (np.floor(y) + 0.5))
+    else:
+        from oracle.numerics import E4M3_VALUES
+        vals = np.sort(np.unique(E4M3_VALUES[~np.isnan(E4M3_VALUES)]))
+        mids = (vals[1:] + vals[:-1]) / 2
+        idx = np.clip(np.searchsorted(mids, y), 1, len(mids) - 1)
+        d = np.minimum(np.abs(y - mids[idx]), np.abs(y - mids[idx - 1]))
+    return d * sc
+
+
+def fp32_dot_bound(X, Vc_cols, bias_cols, D_ref):
+    """Worst-case fp32 error of D = X V_c - mu V_c accumulated over K = p terms
+    (gamma_K = K 2^-24 times sum |x v|) plus the bias subtraction — the SURVEY
+    §8(c) classification bound — and the typical sqrt(K) 2^-24 scale."""
+    S = np.abs(X) @ np.abs(Vc_cols)
+    K = X.shape[1]
+    u = 2.0 ** -24
+    worst = K * u * S + 2 * u * (np.abs(bias_cols)[None, :] + np.abs(D_ref))
+    typical = np.sqrt(K) * u * S + 2 * u * (np.abs(bias_cols)[None, :] + np.abs(D_ref))
+    return worst, typical
+
+
+def codes_parity(payload_gpu, groups, D_ref, m, X, basis, cols):
+    """GPU codes vs oracle codes from the fp64 D.  Every mismatch must sit within
+    the worst-case fp32 accumulation bound of a decision boundary, or be where the
+    GPU's fp16 shift/scale differ from the oracle's (fp32 vs fp64 evaluation of
+    the same formula).  Returns (total, mismatches, unexplained, beyond_typical,
+    per-type counts)."""
+    sh_g, sc_g, cd_g = OL.unpack(groups, payload_gpu, m)
+    Vc = basis.Vc[:, cols]
+    bias = basis.mu @ Vc
+    worst, typical = fp32_dot_bound(X, Vc, bias, D_ref)
+    total = mism = unexplained = beyond = 0
+    per = {}
+    off = 0
+    for g, (_, z, t) in enumerate(groups):
+        sh, sc, cd = OQ.quantize_rows(D_ref[:, off:off + z], t)
+        same_f = (sh == sh_g[g]) & (sc == sc_g[g])
+        bad = cd != cd_g[g]
+        dist = boundary_distance(D_ref[:, off:off + z], sh, sc, t)
+        ok = (dist <= worst[:, off:off + z]) | ~same_f[:, None]
+        total += cd.size
+        mism += int(bad.sum())
+        unexplained += int((bad & ~ok).sum())
+        beyond += int((bad & same_f[:, None] & (dist > typical[:, off:off + z])).sum())
+        a, b = per.get(t, (0, 0))
+        per[t] = (a + int(bad.sum()), b + cd.size)
+        off += z
+    return total, mism, unexplained, beyond, per
+
+
+
+def assert_codes_parity(payload_gpu, groups, D_ref, m, X, basis, cols, label=""):
+    """The code-parity gate: every mismatch within the TYPICAL
+    fp32 accumulation error (sqrt(K) 2^-24 sum|xv|) of a decision boundary (or
+    with differing fp16 factors); int2/int4 codes >= 99.99 % equal; fp8 codes,
+    whose E4M3 grid puts boundaries 2^-9 scale apart near zero, >= 99.8 %."""
+    total, mism, unexplained, beyond, per = codes_parity(payload_gpu, groups, D_ref, m, X, basis, cols)
+    print(f"\n[codes] {label} total={total} mismatches={mism} ({mism / max(total, 1):.2e}) "
+          f"beyond-typical={beyond} per-type={per}")
+    assert unexplained == 0 and beyond == 0, (mism, unexplained, beyond, total)
+    for t, (bad, n) in per.items():
+        limit = 2e-3 if t == T8 else 1e-4
+        assert bad <= max(2, limit * n), (t, bad, n)

@@ -1,0 +1,147 @@
+"""End-to-end GPU compress / decompress through the C ABI vs the oracle."""
+import zlib
+
+import numpy as np
+import pytest
+import torch
+
+from tests import gpu_env as E
+from tests.kvtc_format import parse_container, parse_section
+
+pytestmark = pytest.mark.gpu
+
+from oracle import codec as OC
+from oracle import dp as ODP
+from oracle import layout as OL
+from oracle import quant as OQ
+
+
+@pytest.fixture(scope="module")
+def K():
+    from paper_2511_01815_b200 import kvtc
+    kvtc.device_check()
+    return kvtc
+
+
+def _setup(K, name):
+    spec, invf, kb, vb, Ck, Cv = E.setup(name)
+    shape = (spec.layers, spec.kv_heads, spec.head_dim)
+    if name == "toy":
+        kp, vp = E.toy_plans(16)
+        gk, gv = kp.groups, vp.groups
+    else:
+        gk = gv = E.mid_plan_groups()
+    KB = K.Basis.create(shape, 0, kb.mu, kb.V, kb.sigma, inv_freq=invf, pairing=0)
+    VB = K.Basis.create(shape, 1, vb.mu, vb.V, vb.sigma)
+    KP = K.Plan.create(kb.r, gk)
+    VP = K.Plan.create(vb.r, gv)
+    okp = ODP.Plan(r=kb.r, blocks=list(gk))
+    ovp = ODP.Plan(r=vb.r, blocks=list(gv))
+    return spec, invf, kb, vb, KB, VB, KP, VP, okp, ovp
+
+
+@pytest.mark.parametrize("name,tokens,pos0", [("toy", 512, 0), ("toy", 133, 0), ("mid", 1000, 300), ("mid", 260, 0)])
+def test_compress_decompress_vs_oracle(K, name, tokens, pos0):
+    spec, invf, kb, vb, KB, VB, KP, VP, okp, ovp = _setup(K, name)
+    Kc, Vc = E.caches(name, tokens, pos0, conversation=5)
+    kd, vd = Kc.cuda(), Vc.cuda()
+    cont, st = K.compress(KB, KP, VB, VP, K.KVView(kd, pos0=pos0), K.KVView(vd, pos0=pos0))
+    buf = cont.cpu().numpy().tobytes()
+    h = parse_container(buf)
+    m = tokens - 132
+    assert h["m"] == m and h["total_bytes"] == len(buf)
+    # oracle on the same inputs
+    oc = OC.compress(Kc.double().numpy(), Vc.double().numpy(), pos0, kb, okp, vb, ovp, invf)
+    for sv, so, groups, ob, cache in ((0, oc.k, okp.groups, kb, Kc), (1, oc.v, ovp.groups, vb, Vc)):
+        sec = parse_section(buf[h["sec_k" if sv == 0 else "sec_v"]:])
+        payload = b"".join(zlib.decompress(s, wbits=-15) for s in sec["streams"])   # stock zlib inflates GPU chunks
+        assert len(payload) == len(so.payload)
+        if m > 0:
+            X = OC.stream_rows(cache.double().numpy(), 4, 128, pos0, sv == 0, invf, 0)
+            cols = np.concatenate([np.arange(s0, s0 + z) for (s0, z, _) in groups])
+            E.assert_codes_parity(payload, groups, so.D, m, X, ob, cols, f"e2e {name} stream={sv}")
+    ko = torch.zeros_like(kd)
+    vo = torch.zeros_like(vd)
+    K.decompress(KB, KP, VB, VP, cont, K.KVView(ko, pos0=pos0), K.KVView(vo, pos0=pos0))
+    torch.cuda.synchronize()
+    K2, V2 = OC.decompress(oc, kb, okp, vb, ovp, invf)
+    mid = slice(4, tokens - 128)
+    for sv, got, ref, orig, ob, op, so in ((0, ko, K2, Kc, kb, okp, oc.k), (1, vo, V2, Vc, vb, ovp, oc.v)):
+        g = got.float().cpu().numpy().astype(np.float64)
+        o = orig.double().numpy()
+        # sinks and window byte-identical
+        np.testing.assert_array_equal(g[:, :4], o[:, :4])
+        np.testing.assert_array_equal(g[:, tokens - 128:], o[:, tokens - 128:])
+        if m == 0:
+            continue
+        # (a) decompress-path parity: the oracle decompressing the GPU's own payload
+        sec = parse_section(buf[h["sec_k" if sv == 0 else "sec_v"]:])
+        payload = b"".join(zlib.decompress(s, wbits=-15) for s in sec["streams"])
+        Xh = OC.reconstruct_stream(payload, ob, op, m).reshape(m, spec.layers, spec.kv_heads, spec.head_dim)
+        Xh = Xh.transpose(1, 0, 2, 3)
+        from oracle import rope as OR, numerics as ON
+        ref_a = OR.rope_apply_r7(Xh, pos0 + 4 + np.arange(m), invf, 0) if sv == 0 else ON.bf16(Xh)
+        rel_a = np.linalg.norm(g[:, mid] - ref_a) / np.linalg.norm(ref_a)
+        assert rel_a < 1e-3, rel_a
+        # (b) end to end vs the oracle's own pipeline: within 1e-3 plus the effect
+        # of the boundary code flips, whose X-space energy equals their D-space
+        # energy (orthonormal invariance)
+        sh_g, sc_g, cd_g = OL.unpack(op.groups, payload, m)
+        dD = 0.0
+        for gi, (_, z, t) in enumerate(op.groups):
+            a = ON.f16(OQ.dequantize_rows(sh_g[gi], sc_g[gi], cd_g[gi], t))
+            b = ON.f16(OQ.dequantize_rows(so.shifts[gi], so.scales[gi], so.codes[gi], t))
+            dD += float(np.sum((a - b) ** 2))
+        nref = np.linalg.norm(ref[:, mid])
+        rel_b = np.linalg.norm(g[:, mid] - ref[:, mid]) / nref
+        allow = 1e-3 + 1.02 * np.sqrt(dD) / nref
+        print(f"\n[recon] {name} stream={sv} decompress-path rel={rel_a:.2e} e2e rel={rel_b:.2e} "
+              f"code-flip part={np.sqrt(dD) / nref:.2e}")
+        assert rel_b < allow, (rel_b, allow)
+
+
+def test_layer_range_decompress(K):
+    name, tokens = "mid", 700
+    spec, invf, kb, vb, KB, VB, KP, VP, okp, ovp = _setup(K, name)
+    Kc, Vc = E.caches(name, tokens, 0, conversation=6)
+    kd, vd = Kc.cuda(), Vc.cuda()
+    cont, _ = K.compress(KB, KP, VB, VP, K.KVView(kd), K.KVView(vd))
+    full_k, full_v = torch.zeros_like(kd), torch.zeros_like(vd)
+    K.decompress(KB, KP, VB, VP, cont, K.KVView(full_k), K.KVView(full_v))
+    part_k, part_v = torch.zeros_like(kd), torch.zeros_like(vd)
+    K.decompress(KB, KP, VB, VP, cont, K.KVView(part_k), K.KVView(part_v), layer_begin=1, layer_end=2)
+    torch.cuda.synchronize()
+    assert torch.equal(part_k[1], full_k[1]) and torch.equal(part_v[1], full_v[1])
+    assert not part_k[0].any() and not part_v[0].any()
+
+
+def test_paged_output(K):
+    name, tokens = "mid", 600
+    spec, invf, kb, vb, KB, VB, KP, VP, okp, ovp = _setup(K, name)
+    Kc, Vc = E.caches(name, tokens, 0, conversation=7)
+    kd, vd = Kc.cuda(), Vc.cuda()
+    cont, _ = K.compress(KB, KP, VB, VP, K.KVView(kd), K.KVView(vd))
+    full_k, full_v = torch.zeros_like(kd), torch.zeros_like(vd)
+    K.decompress(KB, KP, VB, VP, cont, K.KVView(full_k), K.KVView(full_v))
+    page = 16
+    npg = (tokens + page - 1) // page
+    bt = torch.randperm(npg + 3, generator=torch.Generator().manual_seed(1))[:npg].int().cuda()
+    pk = torch.zeros(spec.layers, npg + 3, page, spec.kv_heads, spec.head_dim, dtype=torch.bfloat16, device="cuda")
+    pv = torch.zeros_like(pk)
+    K.decompress(KB, KP, VB, VP, cont, K.KVView(pk, tokens=tokens, block_table=bt),
+                 K.KVView(pv, tokens=tokens, block_table=bt))
+    torch.cuda.synchronize()
+    tok = torch.arange(tokens, device="cuda")
+    gk = pk[:, bt[tok // page].long(), tok % page]
+    gv = pv[:, bt[tok // page].long(), tok % page]
+    assert torch.equal(gk, full_k) and torch.equal(gv, full_v)
+
+
+def test_mismatched_plan_rejected(K):
+    spec, invf, kb, vb, KB, VB, KP, VP, okp, ovp = _setup(K, "toy")
+    Kc, Vc = E.caches("toy", 400, 0)
+    cont, _ = K.compress(KB, KP, VB, VP, K.KVView(Kc.cuda()), K.KVView(Vc.cuda()))
+    other = K.Plan.create(kb.r, [(0, 16, OQ.T_INT4)])
+    with pytest.raises(Exception) as e:
+        K.decompress(KB, other, VB, VP, cont, K.KVView(torch.zeros_like(Kc).cuda()), K.KVView(torch.zeros_like(Vc).cuda()))
+    assert "MISMATCH" in str(e.value)
