@@ -107,6 +107,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     n0 = blockIdx.x * kMaxTileN;
     ncols = min(kMaxTileN, P.ncols - n0);
   }
+  if constexpr (MODE == EPI_XTX) {
+    if (n0 + kMaxTileN <= m0) return;                    // strictly below the diagonal: symmetric, skipped
+  }
   const int n_mma = (ncols + 15) & ~15;
   const int num_kb = (P.K + kBlockK - 1) / kBlockK;
 

@@ -282,3 +282,88 @@ def decompress(kb: Basis, kp: Plan, vb: Basis, vp: Plan, container: torch.Tensor
     check(lib().kvtc_decompress(kb.h, kp.h, vb.h, vp.h, _ptr(container), container.numel(), layer_begin, layer_end,
                                 C.byref(k_out.c), C.byref(v_out.c), _ptr(workspace), workspace.numel(),
                                 _stream(stream)))
+
+
+# ------------------------------------------------------------- calibration
+def _samples(samples):
+    s = np.ascontiguousarray(np.asarray(samples, dtype=np.int64).reshape(-1, 2))
+    return s, s.ctypes.data_as(C.POINTER(C.c_int64))
+
+
+def _views(views):
+    arr = (L.View * len(views))(*[v.c for v in views])
+    return arr
+
+
+def calibrate(views: list, samples, which: int, rank_cap: int = 10000, inv_freq=None, pairing: int = 0,
+              stream=None) -> Basis:
+    """kvtc_calibrate: single-process accumulate + finalize."""
+    s, sp = _samples(samples)
+    arr = _views(views)
+    rope, keep = _rope(inv_freq, pairing) if which == L.KEYS else (None, None)
+    out = C.c_void_p()
+    check(lib().kvtc_calibrate(arr, len(views), sp, len(s), which, C.byref(rope) if rope else None, rank_cap,
+                               _stream(stream), C.byref(out)))
+    return Basis(out, views[0].shape, which)
+
+
+def calibrate_accumulate(views: list, samples, which: int, sum_x: torch.Tensor, xtx: torch.Tensor, inv_freq=None,
+                         pairing: int = 0, stream=None, workspace: torch.Tensor | None = None):
+    """Adds this process's sum_x (fp64 [p]) and X^T X (fp32 [p, p]) — the
+    quantities a multi-GPU caller all-reduces before calibrate_finalize."""
+    s, sp = _samples(samples)
+    arr = _views(views)
+    rope, keep = _rope(inv_freq, pairing) if which == L.KEYS else (None, None)
+    shp = L.Shape(*views[0].shape)
+    wsb = int(lib().kvtc_calibrate_workspace_bytes(C.byref(shp)))
+    if workspace is None or workspace.numel() < wsb:
+        workspace = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    check(lib().kvtc_calibrate_accumulate(arr, len(views), sp, len(s), which, C.byref(rope) if rope else None,
+                                          _ptr(sum_x), _ptr(xtx), _ptr(workspace), workspace.numel(),
+                                          _stream(stream)))
+    return workspace
+
+
+def calibrate_finalize(shape, which: int, sum_x: torch.Tensor, xtx: torch.Tensor, n: int, rank_cap: int = 10000,
+                       inv_freq=None, pairing: int = 0, stream=None) -> Basis:
+    rope, keep = _rope(inv_freq, pairing) if which == L.KEYS else (None, None)
+    out = C.c_void_p()
+    check(lib().kvtc_calibrate_finalize(C.byref(L.Shape(*shape)), which, C.byref(rope) if rope else None,
+                                        _ptr(sum_x), _ptr(xtx), n, rank_cap, _stream(stream), C.byref(out)))
+    return Basis(out, tuple(shape), which)
+
+
+# -------------------------------------------------------------- allocation
+def dp_config(target_cr: float, sizes=(1, 16, 64, 256, 1024), type_mask: int = 0xF, dp_row_cap: int = 32768,
+              feature_bits: int = 16):
+    sz = np.ascontiguousarray(np.asarray(sizes, dtype=np.int32))
+    cfg = L.DPConfig(float(target_cr), feature_bits, len(sz), _i32p(sz), type_mask, dp_row_cap)
+    return cfg, sz
+
+
+def allocate_bits_from_coeffs(P: torch.Tensor, p_original: int, target_cr: float, sizes=(1, 16, 64, 256, 1024),
+                              type_mask: int = 0xF, dp_row_cap: int = 32768, stream=None) -> Plan:
+    cfg, keep = dp_config(target_cr, sizes, type_mask, dp_row_cap)
+    out = C.c_void_p()
+    check(lib().kvtc_allocate_bits_from_coeffs(_ptr(P), P.shape[0], P.shape[1], p_original, C.byref(cfg),
+                                               _stream(stream), C.byref(out)))
+    return Plan(out)
+
+
+def allocate_bits(basis: Basis, views: list, samples, target_cr: float, sizes=(1, 16, 64, 256, 1024),
+                  type_mask: int = 0xF, dp_row_cap: int = 32768, stream=None) -> Plan:
+    cfg, keep = dp_config(target_cr, sizes, type_mask, dp_row_cap)
+    s, sp = _samples(samples)
+    arr = _views(views)
+    out = C.c_void_p()
+    check(lib().kvtc_allocate_bits(basis.h, arr, len(views), sp, len(s), C.byref(cfg), _stream(stream),
+                                   C.byref(out)))
+    return Plan(out)
+
+
+def dp_best_table(P: torch.Tensor, budget: int, sizes=(1, 16, 64, 256, 1024), type_mask: int = 0xF, stream=None):
+    cfg, keep = dp_config(1.0, sizes, type_mask, P.shape[0])
+    r = P.shape[1]
+    out = torch.empty(r + 1, budget // 2 + 1, dtype=torch.float64, device="cuda")
+    check(lib().kvtc_dp_best_table(_ptr(P), P.shape[0], r, budget, C.byref(cfg), _ptr(out), _stream(stream)))
+    return out
