@@ -1,0 +1,416 @@
+#!/usr/bin/env python
+"""KVTC hot-path benchmark (BASELINE.json metric): KV GB/s (16-bit equivalent)
+of compress + decompress at ~20x CR on the Llama-3.1-8B shape (configs[1]).
+
+A step = kvtc_compress (keys and values: un-RoPE gather, fused tcgen05 projection
++ quantise + pack, chunked DEFLATE) + kvtc_decompress (inflate, dequantise,
+tcgen05 inverse projection + mu + RoPE, raw sinks/window) of one 32K-token
+conversation per GPU.  GB/s = 2 streams x 2 B x p x m / step time, m = t - s - w.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+Multi-GPU: torchrun, one conversation per rank (weak scaling, no data-path
+collective); calibration statistics are all-reduced over NCCL in the untimed
+setup.  See DESIGN.md §8 for the measurement recipe.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "KV GB/s (16-bit equiv) compress+decompress at ~20x CR"
+UNIT = "GB/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ----------------------------------------------------------------- helpers
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        return m["hbm_gbs"], m["bf16_tflops"], m.get("bf16_tflops_sustained", m["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ------------------------------------------------------------------- setup
+def build_artifacts(K, spec, args, rank, world, dist):
+    """Calibration (K6, NCCL all-reduce of X^T X when world > 1) and the DP (K7/K8).
+    Untimed setup; deterministic, so every rank ends with the same basis and plan."""
+    from kvtc_inputs import generate, sample_positions
+    shape = (spec.layers, spec.kv_heads, spec.head_dim)
+    invf = spec.inv_freq().numpy().astype(np.float32)
+    lens = [args.cal_tokens] * args.cal_seqs
+    samples = sample_positions(lens, args.ncal, sinks=4, seed=7)
+    bases, plans, info = [], [], {}
+    for stream in (0, 1):
+        t0 = time.time()
+        caches = [generate(spec, stream, L, pos0=0, conversation=1000 + i, device="cuda") for i, L in enumerate(lens)]
+        views = [K.KVView(c) for c in caches]
+        torch.cuda.synchronize()
+        tg = time.time()
+        p = spec.p
+        sum_x = torch.zeros(p, dtype=torch.float64, device="cuda")
+        xtx = torch.zeros(p, p, dtype=torch.float32, device="cuda")
+        K.calibrate_accumulate(views, samples[rank::world], stream, sum_x, xtx, inv_freq=invf)
+        if world > 1:
+            dist.all_reduce(sum_x)
+            dist.all_reduce(xtx)
+        torch.cuda.synchronize()
+        tx = time.time()
+        basis = K.calibrate_finalize(shape, stream, sum_x, xtx, len(samples), args.rank_cap, inv_freq=invf)
+        del sum_x, xtx
+        torch.cuda.empty_cache()
+        te = time.time()
+        plan = K.allocate_bits(basis, views, samples, args.cr)
+        td = time.time()
+        pi = plan.info()
+        info[("k", "v")[stream]] = {"gen_s": round(tg - t0, 2), "xtx_s": round(tx - tg, 2), "eig_s": round(te - tx, 2),
+                                    "dp_s": round(td - te, 2), "r": basis.get()[1].shape[1] if False else None,
+                                    "r_eff": pi.r_eff, "groups": len(pi.groups),
+                                    "bits_per_token": pi.bits_per_token, "budget": pi.budget,
+                                    "r_nz": sum(z for (_, z, _) in pi.groups)}
+        log(f"[setup] stream {stream}: {info[('k', 'v')[stream]]}")
+        bases.append(basis)
+        plans.append(plan)
+        del caches, views
+        torch.cuda.empty_cache()
+    return bases, plans, info
+
+
+def oracle_sample(bases, plans, K_host, V_host, spec, ntok: int):
+    """The oracle (as it stands) on a bounded sample: compress + decompress of
+    the first ntok middle tokens of the conversation, both streams."""
+    from oracle import codec as OC
+    from oracle import dp as ODP
+    from oracle import pca as OPCA
+    invf = spec.inv_freq().double().numpy()
+    obs, ops = [], []
+    for b, pl in zip(bases, plans):
+        mu, V, sg = b.get()
+        pi = pl.info()
+        r_use = max(1, pi.r_eff)                      # columns past r_eff are never read
+        obs.append(OPCA.Basis(mu=mu.astype(np.float64), V=V[:, :r_use].astype(np.float64), sigma=sg[:r_use], n=0))
+        ops.append(ODP.Plan(r=r_use, blocks=list(pi.groups)))
+    t = ntok + 132
+    Kc = K_host[:, :t].double().numpy()
+    Vc = V_host[:, :t].double().numpy()
+    try:
+        import threadpoolctl
+        blas = threadpoolctl.threadpool_info()
+        cores = max([x.get("num_threads", 1) for x in blas] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    t0 = time.perf_counter()
+    c = OC.compress(Kc, Vc, 0, obs[0], ops[0], obs[1], ops[1], invf)
+    OC.decompress(c, obs[0], ops[0], obs[1], ops[1], invf)
+    dt = time.perf_counter() - t0
+    gbs = 2 * 2 * spec.p * ntok / dt / 1e9
+    return gbs, dt, cores, c.stats
+
+
+# -------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="llama8b")
+    ap.add_argument("--tokens", type=int, default=32768)
+    ap.add_argument("--cr", type=float, default=16.0)
+    ap.add_argument("--cal-seqs", type=int, default=2)
+    ap.add_argument("--cal-tokens", type=int, default=32768)
+    ap.add_argument("--ncal", type=int, default=65000)
+    ap.add_argument("--rank-cap", type=int, default=8192)
+    ap.add_argument("--cpu-tokens", type=int, default=32)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    world, rank, local = dist_env()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    if args.impl == "reference" and rank != 0:
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    from paper_2511_01815_b200 import kvtc as K
+    from kvtc_inputs import make_spec, generate
+    K.device_check()
+    spec = make_spec(args.config)
+    p, t = spec.p, args.tokens
+    s_, w_ = 4, 128
+    m = t - s_ - w_
+    hbm, bf16_burst, bf16_sus, peak_src = peaks()
+    log(f"[bench] rank {rank}/{world} config={args.config} p={p} t={t} m={m} impl={args.impl}")
+
+    t_setup = time.time()
+    bases, plans, setup_info = build_artifacts(K, spec, args, rank, world, dist)
+    setup_s = time.time() - t_setup
+    kb, vb = bases
+    kp, vp = plans
+
+    # this rank's conversation (weak scaling: one 32K-token conversation per GPU)
+    Kc = generate(spec, 0, t, pos0=0, conversation=rank, device="cuda")
+    Vc = generate(spec, 1, t, pos0=0, conversation=rank, device="cuda")
+    kview, vview = K.KVView(Kc), K.KVView(Vc)
+    Ko, Vo = torch.zeros_like(Kc), torch.zeros_like(Vc)
+    koview, voview = K.KVView(Ko), K.KVView(Vo)
+    cap, wsb = K.compress_sizes(kb, kp, vb, vp, kview)
+    cont = torch.empty(cap, dtype=torch.uint8, device="cuda")
+    cws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    cont_valid, st = K.compress(kb, kp, vb, vp, kview, vview, out=cont, workspace=cws)
+    info = K.container_info(cont_valid)
+    dws = torch.empty(K.decompress_workspace_bytes(kb, kp, vb, vp, cont[:256].cpu().numpy().tobytes()),
+                      dtype=torch.uint8, device="cuda")
+    bytes16 = 2 * 2 * p * m                                    # K+V middle tokens, 16-bit
+    cr = bytes16 / (info.entropy_bytes[0] + info.entropy_bytes[1])
+    cr_pre = bytes16 / (info.payload_bytes[0] + info.payload_bytes[1])
+
+    if args.impl == "reference":
+        # the oracle as it stands, on host cores, on a bounded sample of the same workload
+        Kh, Vh = Kc.cpu(), Vc.cpu()
+        for _ in range(args.warmup):
+            oracle_sample(bases, plans, Kh, Vh, spec, min(8, args.cpu_tokens))
+        vals, secs = [], 0.0
+        for _ in range(args.steps):
+            gbs, dt, cores, stats = oracle_sample(bases, plans, Kh, Vh, spec, args.cpu_tokens)
+            vals.append(gbs)
+            secs += dt
+        v = statistics.mean(vals)
+        line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": f"{args.config} {t}-token conversation, CR target {args.cr:g}",
+                           "sample": f"{args.cpu_tokens} middle tokens per step"},
+                "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                                 "sample": f"{args.cpu_tokens} middle tokens of the {args.config} conversation, "
+                                           "compress+decompress, both streams"},
+                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                "setup": "basis/plan from kvtc_calibrate + kvtc_allocate_bits (untimed inputs; the oracle's own "
+                         "fp64 eigh of a 32768^2 covariance does not finish in minutes on the host)"}
+        print(json.dumps(line), flush=True)
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    stream = torch.cuda.current_stream()
+
+    def step():
+        K.compress(kb, kp, vb, vp, kview, vview, out=cont, workspace=cws, sync_len=False)
+        K.decompress(kb, kp, vb, vp, cont, koview, voview, workspace=dws)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # ---- timed region: device events, L2 (126 MB) << 4.3 GB of inputs per step
+    clocks = ClockSampler(local)
+    clocks.start()
+    K.profile_enable(True)
+    K.launch_count_reset()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms_total = ev0.elapsed_time(ev1)
+    launches = K.launch_count()
+    prof = K.profile_read()
+    K.profile_enable(False)
+    clk = clocks.stop()
+    ms_step = ms_total / args.steps
+    if dist:
+        tt = torch.tensor([ms_step], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_step = float(tt.item())
+    value = world * bytes16 / (ms_step * 1e-3) / 1e9
+
+    # ---- roofline of the dominant kernel (from the live stage events)
+    kinfo, vinfo = kp.info(), vp.info()
+    rnz = [sum(z for (_, z, _) in kinfo.groups), sum(z for (_, z, _) in vinfo.groups)]
+    gemm_flops = 2.0 * m * p * (rnz[0] + rnz[1])              # one launch pair (K and V) per direction
+    stages = {}
+    for name, (ms, calls) in prof.items():
+        stages[name] = {"ms_per_step": ms / args.steps, "calls_per_step": calls / args.steps}
+    for nm in ("c.project_quant_gemm", "d.reconstruct_gemm"):
+        if nm in stages:
+            tfl = gemm_flops / (stages[nm]["ms_per_step"] * 1e-3) / 1e12
+            stages[nm]["tflops"] = tfl
+            stages[nm]["frac_of_sustained_bf16"] = tfl / bf16_sus
+    pay = info.payload_bytes[0] + info.payload_bytes[1]
+    ent = info.entropy_bytes[0] + info.entropy_bytes[1]
+    for nm, b in (("c.deflate", pay + ent), ("d.inflate", pay + ent), ("d.dequant", pay + m * 2 * sum(rnz)),
+                  ("c.gather_unrope", 2 * 2 * p * m), ("c.gather", 2 * 2 * p * m)):
+        if nm in stages:
+            gbs = b / (stages[nm]["ms_per_step"] * 1e-3) / 1e9
+            stages[nm]["gbs"] = gbs
+            stages[nm]["frac_of_hbm"] = gbs / hbm
+    dom = max(("c.project_quant_gemm", "d.reconstruct_gemm"), key=lambda n: stages.get(n, {}).get("ms_per_step", 0))
+    dom_ms = stages[dom]["ms_per_step"] / 2                  # per launch (K or V), averaged
+    achieved = gemm_flops / 2 / (dom_ms * 1e-3) / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(dom)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": bf16_sus, "unit": "TFLOP/s",
+                "frac": achieved / bf16_sus, "traffic": traffic,
+                "peak_source": f"{peak_src} bf16 sustained (kernel timed inside the step)",
+                "algorithmic": f"2*m*p*r_nz flops per launch, m={m}, p={p}, r_nz={rnz}"}
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        Kh = torch.empty_like(Kc, device="cpu").pin_memory()
+        Vh = torch.empty_like(Vc, device="cpu").pin_memory()
+        Kh.copy_(Kc)
+        Vh.copy_(Vc)
+        Koh = torch.empty_like(Kh).pin_memory()
+        Voh = torch.empty_like(Vh).pin_memory()
+        Kd, Vd = torch.empty_like(Kc), torch.empty_like(Vc)
+        kdv, vdv = K.KVView(Kd), K.KVView(Vd)
+
+        def e2e_step():
+            Kd.copy_(Kh, non_blocking=True)
+            Vd.copy_(Vh, non_blocking=True)
+            K.compress(kb, kp, vb, vp, kdv, vdv, out=cont, workspace=cws, sync_len=False)
+            K.decompress(kb, kp, vb, vp, cont, koview, voview, workspace=dws)
+            Koh.copy_(Ko, non_blocking=True)
+            Voh.copy_(Vo, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / args.steps
+        if dist:
+            tt = torch.tensor([ems], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ems = float(tt.item())
+        e2e = {"value": world * bytes16 / (ems * 1e-3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": int(Kh.numel() * 2 * 2), "d2h_bytes_per_step": int(Koh.numel() * 2 * 2),
+               "ms_per_step": ems}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        gbs, dt, cores, stats = oracle_sample(bases, plans, Kc.cpu(), Vc.cpu(), spec, args.cpu_tokens)
+        cpu = {"value": gbs, "unit": UNIT, "cores": cores, "kind": "oracle", "seconds": dt,
+               "sample": f"{args.cpu_tokens} middle tokens of the {args.config} conversation, compress+decompress "
+                         "of both streams (fp64 NumPy + zlib, the oracle as it stands)"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "bf16", "data": "synthetic (kvtc_inputs, DESIGN.md §5)",
+                "config": {"workload": f"{args.config}: {spec.layers} layers x {spec.kv_heads} KV heads x "
+                                       f"{spec.head_dim}, {t}-token conversation per GPU, CR target {args.cr:g}",
+                           "tokens_per_gpu": t, "middle_tokens": m, "p": p, "parallelism": f"weak x{world}",
+                           "l2": "inputs 4.3 GB per step >> 126 MB L2 (no flush needed)",
+                           "cr": cr, "cr_pre_deflate": cr_pre, "r_eff": [kinfo.r_eff, vinfo.r_eff], "r_nz": rnz,
+                           "setup_s": round(setup_s, 1), "setup": setup_info},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "clocks": clk, "stages": stages}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -270,6 +270,19 @@ kvtc_status kvtc_stage_reconstruct(const kvtc_basis *b, const kvtc_plan *plan, c
                                    int64_t m, int64_t tok_begin, int32_t layer_begin, int32_t layer_end,
                                    const kvtc_kv_view *out, void *stream);
 
+/* ------------------------------------------------------------- diagnostics
+ * Per-stage device timing with CUDA events recorded on the caller's stream
+ * around each stage of kvtc_compress / kvtc_decompress (off by default; enabling
+ * resets).  kvtc_profile_read synchronises the recorded events and returns the
+ * number of distinct stages (<= cap): names are written NUL-separated into
+ * names_host (capacity names_cap bytes), total milliseconds and call counts into
+ * ms_host / calls_host.  kvtc_launch_count: kernels this library launched since
+ * the last reset (all entry points). */
+void kvtc_profile_enable(int32_t on);
+int32_t kvtc_profile_read(char *names_host, size_t names_cap, double *ms_host, int32_t *calls_host, int32_t cap);
+int64_t kvtc_launch_count(void);
+void kvtc_launch_count_reset(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -381,6 +381,7 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
   h.section_off[0] = L.k_off;
 
   // raw sinks + window, K then V: [layers][nraw][h*d] each
+  ProfScope ps_raw("c.raw_tokens", st);
   const int64_t hd = int64_t(k->shape.kv_heads) * k->shape.head_dim;
   auto *rawk = reinterpret_cast<__nv_bfloat16 *>(o + KVTC_HEADER_BYTES);
   auto *rawv = rawk + int64_t(k->shape.layers) * L.nraw * hd;
@@ -406,15 +407,34 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
   }
   KVTC_CUDA_TRY(cudaMemcpyAsync(lens + 2, &h.section_off[0], 8, cudaMemcpyHostToDevice, st));
   // ---- keys: un-RoPE gather (K1) -> fused projection + quantisation (K2) -> DEFLATE (K3)
-  if ((s = rope_table_for(kb, k->pos0 + pol->sinks, L.m, cs, st))) return s;
-  if ((s = launch_gather(*k, kbases, pol->sinks, L.m, cs, kb->pairing, X, st))) return s;
-  if ((s = run_project_quant(kb, kpl, kop, X, L.m, payload, st))) return s;
-  if ((s = launch_deflate(payload, L.pay[0], pol->chunk_bytes, o, lens + 2, lens + 0, dwsp, dws, st))) return s;
+  {
+    ProfScope ps("c.gather_unrope", st);
+    if ((s = rope_table_for(kb, k->pos0 + pol->sinks, L.m, cs, st))) return s;
+    if ((s = launch_gather(*k, kbases, pol->sinks, L.m, cs, kb->pairing, X, st))) return s;
+  }
+  {
+    ProfScope ps("c.project_quant_gemm", st);
+    if ((s = run_project_quant(kb, kpl, kop, X, L.m, payload, st))) return s;
+  }
+  {
+    ProfScope ps("c.deflate", st);
+    if ((s = launch_deflate(payload, L.pay[0], pol->chunk_bytes, o, lens + 2, lens + 0, dwsp, dws, st))) return s;
+  }
   offset_after_kernel<<<1, 1, 0, st>>>(lens + 2, lens + 0, lens + 3);
+  KVTC_LAUNCH_CHECK();
   // ---- values
-  if ((s = launch_gather(*v, vbases, pol->sinks, L.m, nullptr, 0, X, st))) return s;
-  if ((s = run_project_quant(vb, vpl, vop, X, L.m, payload, st))) return s;
-  if ((s = launch_deflate(payload, L.pay[1], pol->chunk_bytes, o, lens + 3, lens + 1, dwsp, dws, st))) return s;
+  {
+    ProfScope ps("c.gather", st);
+    if ((s = launch_gather(*v, vbases, pol->sinks, L.m, nullptr, 0, X, st))) return s;
+  }
+  {
+    ProfScope ps("c.project_quant_gemm", st);
+    if ((s = run_project_quant(vb, vpl, vop, X, L.m, payload, st))) return s;
+  }
+  {
+    ProfScope ps("c.deflate", st);
+    if ((s = launch_deflate(payload, L.pay[1], pol->chunk_bytes, o, lens + 3, lens + 1, dwsp, dws, st))) return s;
+  }
   header_kernel<<<1, 1, 0, st>>>(h, o, lens, lens + 2);
   KVTC_LAUNCH_CHECK();
   if (out_len_host) {
@@ -540,13 +560,23 @@ extern "C" kvtc_status kvtc_decompress(const kvtc_basis *kb, const kvtc_plan *kp
     const Operands *op;
     if ((s = plan_operands(b, pl, &op))) return s;
     const uint32_t nch = uint32_t((h.payload_bytes[sv] + h.chunk_bytes - 1) / h.chunk_bytes);
-    if ((s = launch_inflate_section(ib, sec_off_dev + sv, h.payload_bytes[sv], nch, payload, err, st))) return s;
-    if ((s = launch_dequant(pl->d_pgroups, pl->d_codes_off_full, pl->G, plan_codes_off_last(pl, h.m % kTileM),
-                            pl->tile_bytes, payload, h.m, Dh, ld, st)))
-      return s;
-    if (pl->r_nz == 0) KVTC_CUDA_TRY(cudaMemsetAsync(Dh, 0, h.m * ld * 2, st));
-    if ((s = run_reconstruct(b, pl, op, Dh, ld, h.m, h.sinks, layer_begin, layer_end, vw, bs, cs, st))) return s;
+    {
+      ProfScope ps("d.inflate", st);
+      if ((s = launch_inflate_section(ib, sec_off_dev + sv, h.payload_bytes[sv], nch, payload, err, st))) return s;
+    }
+    {
+      ProfScope ps("d.dequant", st);
+      if ((s = launch_dequant(pl->d_pgroups, pl->d_codes_off_full, pl->G, plan_codes_off_last(pl, h.m % kTileM),
+                              pl->tile_bytes, payload, h.m, Dh, ld, st)))
+        return s;
+      if (pl->r_nz == 0) KVTC_CUDA_TRY(cudaMemsetAsync(Dh, 0, h.m * ld * 2, st));
+    }
+    {
+      ProfScope ps("d.reconstruct_gemm", st);
+      if ((s = run_reconstruct(b, pl, op, Dh, ld, h.m, h.sinks, layer_begin, layer_end, vw, bs, cs, st))) return s;
+    }
     const __nv_bfloat16 *raw = sv ? rawv : rawk;
+    ProfScope ps("d.raw_tokens", st);
     if ((s = launch_unpack_raw(raw, nraw, 0, h.sinks, *vw, bs, 0, layer_begin, layer_end, st))) return s;
     if ((s = launch_unpack_raw(raw, nraw, h.sinks, h.window, *vw, bs, t - h.window, layer_begin, layer_end, st)))
       return s;

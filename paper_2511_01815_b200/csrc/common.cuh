@@ -34,8 +34,10 @@ void set_error(const char *fmt, ...);
       return KVTC_E_INVALID;             \
     }                                    \
   } while (0)
+void note_launch();
 #define KVTC_LAUNCH_CHECK()                                                          \
   do {                                                                               \
+    ::kvtc::note_launch();                                                           \
     cudaError_t e_ = cudaGetLastError();                                             \
     if (e_ != cudaSuccess) {                                                         \
       ::kvtc::set_error("%s:%d launch: %s", __FILE__, __LINE__, cudaGetErrorString(e_)); \

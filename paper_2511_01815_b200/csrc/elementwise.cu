@@ -141,10 +141,25 @@ struct SeqInfo {
   __nv_bfloat16 *const *bases;  // device array [layers]
 };
 
+// cos/sin of every sampled row's absolute position (R1 table, one entry per (row, j))
+__global__ void rows_rope_table_kernel(const SeqInfo *seqs, const int64_t *rows, int64_t n, int half,
+                                       const float *invf, float2 *cs) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= n * half) return;
+  const int64_t r = i / half;
+  const int j = int(i % half);
+  const float pos = float(seqs[rows[2 * r]].pos0 + rows[2 * r + 1]);
+  const float theta = __fmul_rn(pos, invf[j]);
+  double s, c;
+  sincos(double(theta), &s, &c);
+  cs[i] = make_float2(__double2float_rn(c), __double2float_rn(s));
+}
+
+// one thread = one rotation pair (or two plain elements) of one sampled row
 __global__ void gather_rows_kernel(const SeqInfo *seqs, const int64_t *rows, int64_t n, int layers, int heads, int d,
-                                   const float *invf, int unrope, int pairing, int64_t ld, __nv_bfloat16 *X) {
+                                   const float2 *cs, int pairing, int64_t ld, __nv_bfloat16 *X) {
   const int64_t p = int64_t(layers) * heads * d;
-  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;   // one thread = one pair of elements
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (i >= n * (p / 2)) return;
   const int64_t r = i / (p / 2);
   const int64_t q = i % (p / 2);
@@ -158,13 +173,7 @@ __global__ void gather_rows_kernel(const SeqInfo *seqs, const int64_t *rows, int
   const int i1 = pairing == 0 ? j : 2 * j;
   const int i2 = pairing == 0 ? j + d / 2 : 2 * j + 1;
   __nv_bfloat16 o1 = src[i1], o2 = src[i2];
-  if (unrope) {
-    const float theta = __fmul_rn(float(s.pos0 + tok), invf[j]);
-    double sn, cs;
-    sincos(double(theta), &sn, &cs);
-    unrope_pair(__bfloat162float(o1), __bfloat162float(o2), make_float2(__double2float_rn(cs), __double2float_rn(sn)),
-                o1, o2);
-  }
+  if (cs) unrope_pair(__bfloat162float(o1), __bfloat162float(o2), cs[r * (d / 2) + j], o1, o2);
   __nv_bfloat16 *dst = X + r * ld + int64_t(layer) * heads * d + head * d;
   dst[i1] = o1;
   dst[i2] = o2;
@@ -173,14 +182,7 @@ __global__ void gather_rows_kernel(const SeqInfo *seqs, const int64_t *rows, int
 kvtc_status launch_gather_rows(const kvtc_kv_view *seqs, int32_t nseq, __nv_bfloat16 *const *bases_dev,
                                const int64_t *rows_dev, int64_t n, const float *invf_dev, int32_t unrope,
                                int32_t pairing, int64_t ld, __nv_bfloat16 *X, cudaStream_t st) {
-  // bases_dev: device array [nseq * layers]; SeqInfo array built in a tiny device buffer
-  static thread_local SeqInfo *d_info = nullptr;
-  static thread_local int32_t d_cap = 0;
-  if (nseq > d_cap) {
-    if (d_info) cudaFree(d_info);
-    KVTC_CUDA_TRY(cudaMalloc(&d_info, sizeof(SeqInfo) * nseq));
-    d_cap = nseq;
-  }
+  // bases_dev: device array [nseq * layers]
   std::vector<SeqInfo> h(nseq);
   const int L = seqs[0].shape.layers;
   for (int i = 0; i < nseq; ++i) {
@@ -190,15 +192,26 @@ kvtc_status launch_gather_rows(const kvtc_kv_view *seqs, int32_t nseq, __nv_bflo
     h[i].block_table = seqs[i].block_table;
     h[i].bases = bases_dev + int64_t(i) * L;
   }
-  KVTC_CUDA_TRY(cudaMemcpyAsync(d_info, h.data(), sizeof(SeqInfo) * nseq, cudaMemcpyHostToDevice, st));
   const kvtc_shape &sh = seqs[0].shape;
+  const int half = sh.head_dim / 2;
+  SeqInfo *d_info = nullptr;
+  float2 *cs = nullptr;
+  KVTC_CUDA_TRY(cudaMallocAsync(&d_info, sizeof(SeqInfo) * nseq, st));
+  // pageable -> device: returns once the source has been staged, so h may go out of scope
+  KVTC_CUDA_TRY(cudaMemcpyAsync(d_info, h.data(), sizeof(SeqInfo) * nseq, cudaMemcpyHostToDevice, st));
+  if (unrope && n > 0) {
+    KVTC_CUDA_TRY(cudaMallocAsync(&cs, sizeof(float2) * n * half, st));
+    rows_rope_table_kernel<<<unsigned(ceil_div(n * half, 256)), 256, 0, st>>>(d_info, rows_dev, n, half, invf_dev, cs);
+    KVTC_LAUNCH_CHECK();
+  }
   const int64_t total = n * (int64_t(sh.layers) * sh.kv_heads * sh.head_dim / 2);
-  if (total == 0) return KVTC_OK;
-  gather_rows_kernel<<<unsigned(ceil_div(total, 256)), 256, 0, st>>>(d_info, rows_dev, n, sh.layers, sh.kv_heads,
-                                                                      sh.head_dim, invf_dev, unrope, pairing, ld, X);
-  KVTC_LAUNCH_CHECK();
-  // keep h alive until the copy is consumed
-  KVTC_CUDA_TRY(cudaStreamSynchronize(st));
+  if (total > 0) {
+    gather_rows_kernel<<<unsigned(ceil_div(total, 256)), 256, 0, st>>>(d_info, rows_dev, n, sh.layers, sh.kv_heads,
+                                                                        sh.head_dim, cs, pairing, ld, X);
+    KVTC_LAUNCH_CHECK();
+  }
+  if (cs) cudaFreeAsync(cs, st);
+  cudaFreeAsync(d_info, st);
   return KVTC_OK;
 }
 

@@ -353,6 +353,7 @@ static kvtc_status launch(const CUtensorMap *tmA, const CUtensorMap *tmB, const 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   KVTC_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_kernel<MODE>, *tmA, *tmB, p));
+  note_launch();
   return KVTC_OK;
 }
 

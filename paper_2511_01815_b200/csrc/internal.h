@@ -138,4 +138,12 @@ kvtc_status launch_inflate_raw(const uint8_t *in, const int64_t *in_off, const i
                                uint8_t *out, const int64_t *out_off, const int64_t *out_len, int32_t *status,
                                cudaStream_t st);
 
+// Stage timing (kvtc_profile_*): records an event pair around a scope when enabled.
+struct ProfScope {
+  int slot = -1;
+  cudaStream_t st;
+  ProfScope(const char *name, cudaStream_t s);
+  ~ProfScope();
+};
+
 }  // namespace kvtc

@@ -367,3 +367,26 @@ def dp_best_table(P: torch.Tensor, budget: int, sizes=(1, 16, 64, 256, 1024), ty
     out = torch.empty(r + 1, budget // 2 + 1, dtype=torch.float64, device="cuda")
     check(lib().kvtc_dp_best_table(_ptr(P), P.shape[0], r, budget, C.byref(cfg), _ptr(out), _stream(stream)))
     return out
+
+
+# ------------------------------------------------------------ diagnostics
+def profile_enable(on: bool = True):
+    lib().kvtc_profile_enable(int(on))
+
+
+def profile_read() -> dict:
+    """{stage: (total_ms, calls)} of the stages recorded since profile_enable."""
+    names = C.create_string_buffer(8192)
+    ms = (C.c_double * 64)()
+    calls = (C.c_int32 * 64)()
+    n = lib().kvtc_profile_read(names, 8192, ms, calls, 64)
+    keys = names.raw.split(b"\0")[:n]
+    return {keys[i].decode(): (ms[i], calls[i]) for i in range(n)}
+
+
+def launch_count() -> int:
+    return int(lib().kvtc_launch_count())
+
+
+def launch_count_reset():
+    lib().kvtc_launch_count_reset()
