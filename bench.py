@@ -53,7 +53,7 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -186,7 +186,7 @@ def oracle_sample(bases, plans, K_host, V_host, spec, ntok: int):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="llama8b")
@@ -195,7 +195,11 @@ def main():
     ap.add_argument("--cal-seqs", type=int, default=2)
     ap.add_argument("--cal-tokens", type=int, default=32768)
     ap.add_argument("--ncal", type=int, default=65000)
-    ap.add_argument("--rank-cap", type=int, default=8192)
+    ap.add_argument("--rank-cap", type=int, default=10000)          # P:L974 (Llama / NeMo cap 10K)
+    ap.add_argument("--beta", type=float, default=None)             # synthetic spectrum knob
+    ap.add_argument("--noise", type=float, default=None)            # synthetic isotropic-noise fraction
+    ap.add_argument("--latent", type=int, default=None)             # synthetic latent rank K
+    ap.add_argument("--setup-only", action="store_true")
     ap.add_argument("--cpu-tokens", type=int, default=32)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -218,7 +222,14 @@ def main():
     from paper_2511_01815_b200 import kvtc as K
     from kvtc_inputs import make_spec, generate
     K.device_check()
-    spec = make_spec(args.config)
+    over = {}
+    if args.beta is not None:
+        over["beta"] = args.beta
+    if args.noise is not None:
+        over["noise_frac"] = args.noise
+    if args.latent is not None:
+        over["latent"] = args.latent
+    spec = make_spec(args.config, **over)
     p, t = spec.p, args.tokens
     s_, w_ = 4, 128
     m = t - s_ - w_
@@ -230,6 +241,11 @@ def main():
     setup_s = time.time() - t_setup
     kb, vb = bases
     kp, vp = plans
+    if args.setup_only:
+        print(json.dumps({"setup_s": round(setup_s, 1), "beta": spec.beta, "noise": spec.noise_frac, "latent": spec.latent,
+                          "r_eff": [setup_info["k"]["r_eff"], setup_info["v"]["r_eff"]],
+                          "groups": [setup_info["k"]["groups"], setup_info["v"]["groups"]]}), flush=True)
+        return
 
     # this rank's conversation (weak scaling: one 32K-token conversation per GPU)
     Kc = generate(spec, 0, t, pos0=0, conversation=rank, device="cuda")

@@ -75,12 +75,13 @@ class SynthSpec:
 SHAPES = {
     # BASELINE.json configs[0]: 1 layer, 2 KV heads x 64, 512 tokens
     "toy": SynthSpec("toy", 1, 2, 64, latent=32, rope_base=10000.0),
-    # configs[1]: Llama-3.1-8B shape (32 x 8 x 128), public rope_theta 5e5
-    "llama8b": SynthSpec("llama8b", 32, 8, 128, latent=8192, rope_base=500000.0),
+    # configs[1]: Llama-3.1-8B shape (32 x 8 x 128), public rope_theta 5e5.  Latent rank
+    # p/8 and 0.1 % noise: frozen after the tuning run of DESIGN.md §5 (r_eff at CR 16 ~ 4.3K)
+    "llama8b": SynthSpec("llama8b", 32, 8, 128, latent=4096, rope_base=500000.0, noise_frac=0.001),
     # configs[2]: Mistral-NeMo-12B shape (40 x 8 x 128), rope_theta 1e6
-    "nemo12b": SynthSpec("nemo12b", 40, 8, 128, latent=8192, rope_base=1000000.0),
+    "nemo12b": SynthSpec("nemo12b", 40, 8, 128, latent=5120, rope_base=1000000.0, noise_frac=0.001),
     # configs[3]: Llama-3.3-70B, one 10-layer shard of 80 x 8 x 128
-    "llama70b_shard": SynthSpec("llama70b_shard", 10, 8, 128, latent=4096, rope_base=500000.0),
+    "llama70b_shard": SynthSpec("llama70b_shard", 10, 8, 128, latent=1280, rope_base=500000.0, noise_frac=0.001),
 }
 
 

@@ -381,12 +381,12 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
   h.section_off[0] = L.k_off;
 
   // raw sinks + window, K then V: [layers][nraw][h*d] each
-  ProfScope ps_raw("c.raw_tokens", st);
   const int64_t hd = int64_t(k->shape.kv_heads) * k->shape.head_dim;
   auto *rawk = reinterpret_cast<__nv_bfloat16 *>(o + KVTC_HEADER_BYTES);
   auto *rawv = rawk + int64_t(k->shape.layers) * L.nraw * hd;
   const int64_t t = k->tokens;
   if (L.m) {
+    ProfScope ps_raw("c.raw_tokens", st);
     for (int sv = 0; sv < 2; ++sv) {
       const kvtc_kv_view *vw = sv ? v : k;
       __nv_bfloat16 *const *bs = sv ? vbases : kbases;
@@ -576,10 +576,12 @@ extern "C" kvtc_status kvtc_decompress(const kvtc_basis *kb, const kvtc_plan *kp
       if ((s = run_reconstruct(b, pl, op, Dh, ld, h.m, h.sinks, layer_begin, layer_end, vw, bs, cs, st))) return s;
     }
     const __nv_bfloat16 *raw = sv ? rawv : rawk;
-    ProfScope ps("d.raw_tokens", st);
-    if ((s = launch_unpack_raw(raw, nraw, 0, h.sinks, *vw, bs, 0, layer_begin, layer_end, st))) return s;
-    if ((s = launch_unpack_raw(raw, nraw, h.sinks, h.window, *vw, bs, t - h.window, layer_begin, layer_end, st)))
-      return s;
+    {
+      ProfScope ps("d.raw_tokens", st);
+      if ((s = launch_unpack_raw(raw, nraw, 0, h.sinks, *vw, bs, 0, layer_begin, layer_end, st))) return s;
+      if ((s = launch_unpack_raw(raw, nraw, h.sinks, h.window, *vw, bs, t - h.window, layer_begin, layer_end, st)))
+        return s;
+    }
   }
   return KVTC_OK;
 }

@@ -91,3 +91,21 @@ def test_calibrate_vs_oracle(K, name):
         well = gaps[:k] > 1e-3 * ob.sigma[0] ** 2
         assert np.all(cos[well] > 0.999), cos[well].min()
         np.testing.assert_array_less(-1e-6, np.sum(V[:, :k] * ob.V[:, :k], axis=0)[well])
+
+
+def test_randomized_svd_path(K, monkeypatch):
+    """The large-p finalize path (randomized SVD, P:L235, 8 power iterations,
+    P:L974) forced on the mid shape: leading directions match the oracle."""
+    monkeypatch.setenv("KVTC_CALIB_RSVD", "1")
+    spec, invf, kb, vb, Ck, Cv = E.setup("mid")
+    cal = generate(spec, 1, 3200, pos0=0, conversation=100).cuda()
+    samples = sample_positions([3200], 3000, sinks=spec.sinks, seed=1)
+    B = K.calibrate([K.KVView(cal)], samples, 1, 256)
+    mu, V, sg = B.get()
+    assert V.shape == (spec.p, 256)
+    k = 64
+    np.testing.assert_allclose(sg[:k], vb.sigma[:k], rtol=1e-3)
+    cos = np.abs(np.sum(V[:, :k].astype(np.float64) * vb.V[:, :k], axis=0))
+    gaps = np.abs(np.diff(vb.sigma[: k + 1] ** 2))
+    well = gaps[:k] > 1e-2 * vb.sigma[0] ** 2
+    assert np.all(cos[well] > 0.99), cos[well].min()
