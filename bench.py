@@ -241,6 +241,10 @@ def main():
     setup_s = time.time() - t_setup
     kb, vb = bases
     kp, vp = plans
+    if os.environ.get("KVTC_DUMP_PLANS"):
+        with open(os.environ["KVTC_DUMP_PLANS"], "w") as f:
+            json.dump({"config": args.config, "cr": args.cr, "k": kp.info().groups, "v": vp.info().groups,
+                       "r": [kp.info().r, vp.info().r]}, f)
     if args.setup_only:
         print(json.dumps({"setup_s": round(setup_s, 1), "beta": spec.beta, "noise": spec.noise_frac, "latent": spec.latent,
                           "r_eff": [setup_info["k"]["r_eff"], setup_info["v"]["r_eff"]],
