@@ -11,10 +11,18 @@
 //                  or paged cache.
 //   EPI_XTX    K6  calibration: S += C^T C over a chunk of rows.
 //
-// One CTA computes a 128 x N (N <= 256) fp32 tile in TMEM.  Warp roles: warp 0
-// TMA producer, warp 1 single-thread tcgen05.mma issuer, warp 2 TMEM allocator,
-// warps 4-7 epilogue (warp w reads TMEM lanes 32*(w%4) .. +31).  Operands are
-// K-major, 128 B swizzled, 4-stage mbarrier pipeline.
+// Persistent kernel, one CTA per SM: tiles of 128 x N (N <= 256) are handed out
+// statically in a grouped raster (kGroupM M-blocks x all N tiles) so that the
+// ~148 tiles in flight share A and B tiles in L2 and stay in lock-step.  Warp
+// roles: warp 0 TMA producer, warp 1 single-thread tcgen05.mma issuer, warp 2
+// TMEM allocator, warps 4-7 epilogue (warp w reads TMEM lanes 32*(w%4)..+31).
+// Operands K-major, 128 B swizzled, 4-stage mbarrier ring; two fp32 TMEM
+// accumulators (2 x 256 columns) so the epilogue of tile i overlaps the MMAs of
+// tile i+1 (EPI_QUANT stages D in the ring's shared memory, so there the
+// producer waits for the epilogue instead).  Split-group launches (clusters)
+// run one tile per CTA.
+#include <algorithm>
+
 #include "internal.h"
 #include "quant.cuh"
 
@@ -27,7 +35,8 @@ constexpr int kStageBytes = kABytes + kBBytes;     // 48 KiB
 constexpr int kStagePitch = 257;                   // fp32 words per staged row (conflict-free)
 constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 2048;
 constexpr int kThreads = 256;
-constexpr int kTmemCols = 256;
+constexpr int kTmemCols = 512;                     // two 256-column accumulators
+constexpr int kGroupM = 8;                         // raster group (M-blocks)
 
 enum { EPI_F32 = 0, EPI_QUANT = 1, EPI_RECON = 2, EPI_XTX = 3 };
 
@@ -36,6 +45,7 @@ struct Params {
   int64_t m;
   int32_t ncols;       // F32 / XTX: valid N extent; RECON: n_end
   int32_t n_begin;     // RECON
+  int32_t num_m, num_n;   // tile grid (num_n = N tiles or segments)
   const float *bias;   // F32 / QUANT: [r_nz]; RECON: mu [p]
   float *D;            // F32 / XTX output
   int64_t ldd;
@@ -55,16 +65,11 @@ struct Params {
   const int32_t *block_table;
   int64_t tok_begin;
   int32_t fmt;         // 0 fp16, 1 bf16 operands
-  int32_t tile_n;      // RECON N tile
+  int32_t tile_n;      // RECON / F32 / XTX N tile
 };
 
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
 }
 __device__ __forceinline__ float2 ld_peer_f2(const float2 *local, uint32_t cta) {
   uint32_t a = smem_u32(local), ra;
@@ -72,6 +77,48 @@ __device__ __forceinline__ float2 ld_peer_f2(const float2 *local, uint32_t cta) 
   float2 v;
   asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(ra) : "memory");
   return v;
+}
+
+struct Tile {
+  int mb, nb;   // M-block, N tile / segment
+  bool valid;
+};
+
+// Static persistent schedule: tile t -> (mb, nb) in groups of kGroupM M-blocks.
+template <int MODE>
+__device__ __forceinline__ Tile tile_of(const Params &P, int64_t t) {
+  Tile T;
+  const int64_t per_group = int64_t(kGroupM) * P.num_n;
+  const int64_t g = t / per_group;
+  const int first = int(g * kGroupM);
+  const int gm = min(kGroupM, P.num_m - first);
+  const int64_t r = t - g * per_group;
+  T.mb = first + int(r % gm);
+  T.nb = int(r / gm);
+  T.valid = true;
+  if constexpr (MODE == EPI_XTX) {
+    // strictly below the diagonal: symmetric, skipped
+    if (int64_t(T.nb) * P.tile_n + P.tile_n <= int64_t(T.mb) * kTileM) T.valid = false;
+  }
+  return T;
+}
+
+template <int MODE>
+__device__ __forceinline__ void tile_geometry(const Params &P, const Tile &T, int &n0, int &ncols, int &g0, int &g1) {
+  g0 = g1 = 0;
+  if constexpr (MODE == EPI_QUANT) {
+    const SegDesc sd = P.segs[T.nb];
+    n0 = sd.col0;
+    ncols = sd.width;
+    g0 = sd.g_begin;
+    g1 = sd.g_end;
+  } else if constexpr (MODE == EPI_RECON) {
+    n0 = P.n_begin + T.nb * P.tile_n;
+    ncols = min(P.tile_n, P.ncols - n0);
+  } else {
+    n0 = T.nb * P.tile_n;
+    ncols = min(P.tile_n, P.ncols - n0);
+  }
 }
 
 template <int MODE>
@@ -83,34 +130,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t *tiles = smem;
   uint64_t *full_bar = reinterpret_cast<uint64_t *>(smem + kStages * kStageBytes);
   uint64_t *empty_bar = full_bar + kStages;
-  uint64_t *tmem_full = empty_bar + kStages;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
-  float2 *red = reinterpret_cast<float2 *>(smem + kStages * kStageBytes + 128);   // [128] row min/max
+  uint64_t *tmem_full = empty_bar + kStages;      // [2]
+  uint64_t *tmem_empty = tmem_full + 2;           // [2]
+  uint64_t *epi_done = tmem_empty + 2;            // [1] QUANT: staging smem released
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(epi_done + 1);
+  float2 *red = reinterpret_cast<float2 *>(smem + kStages * kStageBytes + 256);   // [128] row min/max
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const int64_t m0 = int64_t(blockIdx.y) * kTileM;
-
-  // tile geometry
-  int n0, ncols;
-  int seg_g0 = 0, seg_g1 = 0;
-  if constexpr (MODE == EPI_QUANT) {
-    const SegDesc sd = P.segs[blockIdx.x];
-    n0 = sd.col0;
-    ncols = sd.width;
-    seg_g0 = sd.g_begin;
-    seg_g1 = sd.g_end;
-  } else if constexpr (MODE == EPI_RECON) {
-    n0 = P.n_begin + blockIdx.x * P.tile_n;
-    ncols = min(P.tile_n, P.ncols - n0);
-  } else {
-    n0 = blockIdx.x * kMaxTileN;
-    ncols = min(kMaxTileN, P.ncols - n0);
-  }
-  if constexpr (MODE == EPI_XTX) {
-    if (n0 + kMaxTileN <= m0) return;                    // strictly below the diagonal: symmetric, skipped
-  }
-  const int n_mma = (ncols + 15) & ~15;
+  const bool split = (MODE == EPI_QUANT) && P.parts > 1;
+  // split launches: exactly one tile per CTA (grid = pieces x M-blocks, clusters along x)
+  const int64_t total = split ? 1 : int64_t(P.num_m) * P.num_n;
+  const int64_t t_first = split ? 0 : blockIdx.x;
+  const int64_t t_step = split ? 1 : int64_t(gridDim.x);
   const int num_kb = (P.K + kBlockK - 1) / kBlockK;
 
   if (threadIdx.x == 0) {
@@ -120,7 +152,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tmem_full[a], 1);
+      mbar_init(&tmem_empty[a], 128);
+    }
+    mbar_init(epi_done, 128);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
@@ -129,204 +165,253 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  auto get_tile = [&](int64_t t) {
+    if (split) {
+      Tile T;
+      T.mb = blockIdx.y;
+      T.nb = blockIdx.x;
+      T.valid = true;
+      return T;
+    }
+    return tile_of<MODE>(P, t);
+  };
+
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer
-    for (int kb = 0; kb < num_kb; ++kb) {
-      const int s = kb % kStages;
-      if (kb >= kStages) mbar_wait(&empty_bar[s], ((kb / kStages) - 1) & 1);
-      uint8_t *a = tiles + s * kStageBytes;
-      uint8_t *b = a + kABytes;
-      mbar_arrive_expect_tx(&full_bar[s], kStageBytes);
-      tma_load_2d(a, &tmA, &full_bar[s], kb * kBlockK, int32_t(m0));
-      tma_load_2d(b, &tmB, &full_bar[s], kb * kBlockK, n0);
+    uint32_t it = 0, ntile = 0;
+    for (int64_t t = t_first; t < total; t += t_step) {
+      const Tile T = get_tile(t);
+      if (!T.valid) continue;
+      int n0, ncols, g0, g1;
+      tile_geometry<MODE>(P, T, n0, ncols, g0, g1);
+      if (MODE == EPI_QUANT && ntile > 0) mbar_wait(epi_done, (ntile - 1) & 1);   // staging smem free again
+      for (int kb = 0; kb < num_kb; ++kb, ++it) {
+        const int s = it % kStages;
+        if (it >= kStages) mbar_wait(&empty_bar[s], ((it / kStages) - 1) & 1);
+        uint8_t *a = tiles + s * kStageBytes;
+        uint8_t *b = a + kABytes;
+        mbar_arrive_expect_tx(&full_bar[s], kStageBytes);
+        tma_load_2d(a, &tmA, &full_bar[s], kb * kBlockK, T.mb * kTileM);
+        tma_load_2d(b, &tmB, &full_bar[s], kb * kBlockK, n0);
+      }
+      ++ntile;
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer (one thread)
-    const uint32_t idesc = make_idesc_f16(P.fmt, kTileM, n_mma);
-    for (int kb = 0; kb < num_kb; ++kb) {
-      const int s = kb % kStages;
-      mbar_wait(&full_bar[s], (kb / kStages) & 1);
+    uint32_t it = 0, acc_it = 0;
+    for (int64_t t = t_first; t < total; t += t_step) {
+      const Tile T = get_tile(t);
+      if (!T.valid) continue;
+      int n0, ncols, g0, g1;
+      tile_geometry<MODE>(P, T, n0, ncols, g0, g1);
+      const int n_mma = (ncols + 15) & ~15;
+      const uint32_t idesc = make_idesc_f16(P.fmt, kTileM, n_mma);
+      const uint32_t acc = acc_it & 1;
+      if (acc_it >= 2) mbar_wait(&tmem_empty[acc], ((acc_it / 2) - 1) & 1);
       tc_fence_after();
-      const uint64_t ad = make_sdesc_sw128(tiles + s * kStageBytes);
-      const uint64_t bd = make_sdesc_sw128(tiles + s * kStageBytes + kABytes);
+      const uint32_t tacc = tmem_base + acc * kMaxTileN;
+      for (int kb = 0; kb < num_kb; ++kb, ++it) {
+        const int s = it % kStages;
+        mbar_wait(&full_bar[s], (it / kStages) & 1);
+        tc_fence_after();
+        const uint64_t ad = make_sdesc_sw128(tiles + s * kStageBytes);
+        const uint64_t bd = make_sdesc_sw128(tiles + s * kStageBytes + kABytes);
 #pragma unroll
-      for (int k = 0; k < kBlockK / 16; ++k)
-        umma_f16(tmem_base, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
-      umma_commit(&empty_bar[s]);
+        for (int k = 0; k < kBlockK / 16; ++k) umma_f16(tacc, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+        umma_commit(&empty_bar[s]);
+      }
+      umma_commit(&tmem_full[acc]);
+      ++acc_it;
     }
-    umma_commit(tmem_full);
-  }
+  } else if (warp >= 4) {
+    // ---------------- epilogue
+    const int row = (warp & 3) * 32 + lane;                 // TMEM lane == tile row
+    uint32_t acc_it = 0;
+    for (int64_t t = t_first; t < total; t += t_step) {
+      const Tile T = get_tile(t);
+      if (!T.valid) continue;
+      int n0, ncols, seg_g0, seg_g1;
+      tile_geometry<MODE>(P, T, n0, ncols, seg_g0, seg_g1);
+      const int n_mma = (ncols + 15) & ~15;
+      const int64_t m0 = int64_t(T.mb) * kTileM;
+      const int64_t tok = m0 + row;
+      const bool valid = tok < P.m;
+      const uint32_t acc = acc_it & 1;
+      mbar_wait(&tmem_full[acc], (acc_it / 2) & 1);
+      tc_fence_after();
+      const uint32_t trow = tmem_base + acc * kMaxTileN + (uint32_t((warp & 3) * 32) << 16);
 
-  // ---------------- epilogue
-  const bool epi = warp >= 4;
-  const int row = (warp & 3) * 32 + lane;                 // TMEM lane == tile row
-  const int64_t tok = m0 + row;
-  const bool valid = tok < P.m;
-  const uint32_t trow = tmem_base + (uint32_t((warp & 3) * 32) << 16);
-  if (epi) {
-    mbar_wait(tmem_full, 0);
-    tc_fence_after();
-  }
-
-  if constexpr (MODE == EPI_F32 || MODE == EPI_XTX) {
-    if (epi) {
-      for (int c = 0; c < n_mma; c += 16) {
-        float v[16];
-        tmem_ld16(trow + c, v);
-        if (valid) {
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int col = n0 + c + j;
-            if (c + j < ncols) {
-              float *dst = P.D + tok * P.ldd + col;
-              if constexpr (MODE == EPI_F32) *dst = __fsub_rn(v[j], P.bias[col]);
-              else *dst += v[j];
-            }
-          }
-        }
-      }
-    }
-  } else if constexpr (MODE == EPI_QUANT) {
-    // stage this thread's row of D (fp32, minus the bias mu V_c) in shared memory
-    float *stage = reinterpret_cast<float *>(tiles);
-    float *xr = stage + row * kStagePitch;
-    if (epi) {
-      for (int c = 0; c < n_mma; c += 16) {
-        float v[16];
-        tmem_ld16(trow + c, v);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) xr[c + j] = (c + j < ncols) ? __fsub_rn(v[j], P.bias[n0 + c + j]) : 0.0f;
-      }
-    }
-    const int ntok = int(P.m - m0 < kTileM ? P.m - m0 : kTileM);
-    const bool last = ntok < kTileM;
-    uint8_t *tile_base = P.payload + (m0 / kTileM) * P.tile_bytes;
-    float rmn = 0.f, rmx = 0.f;
-    if (P.parts > 1) {
-      // split group: one piece per CTA; exchange row min/max over the cluster (DSMEM)
-      const GroupDesc gd = P.groups[seg_g0];
-      if (epi) {
-        float mn = xr[gd.col], mx = xr[gd.col];
-        for (int c = 1; c < gd.size; ++c) {
-          mn = fminf(mn, xr[gd.col + c]);
-          mx = fmaxf(mx, xr[gd.col + c]);
-        }
-        red[row] = make_float2(mn, mx);
-      }
-      cluster_sync_all();
-      if (epi) {
-        rmn = red[row].x;
-        rmx = red[row].y;
-        for (int q = 0; q < P.parts; ++q) {
-          const float2 o = ld_peer_f2(&red[row], q);
-          rmn = fminf(rmn, o.x);
-          rmx = fmaxf(rmx, o.y);
-        }
-      }
-      cluster_sync_all();
-    }
-    if (epi) {
-      for (int gi = seg_g0; gi < seg_g1; ++gi) {
-        const GroupDesc gd = P.groups[gi];
-        const float *x = xr + gd.col;
-        float mn, mx;
-        if (P.parts > 1) {
-          mn = rmn;
-          mx = rmx;
-        } else {
-          mn = x[0];
-          mx = x[0];
-          for (int c = 1; c < gd.size; ++c) {
-            mn = fminf(mn, x[c]);
-            mx = fmaxf(mx, x[c]);
-          }
-        }
-        uint8_t *cb = tile_base + (last ? P.codes_off_last[gd.gidx] : gd.codes_off);
-        emit_group(x, gd.size, gd.full_size, gd.part, gd.type, gd.gidx, mn, mx, valid, row, lane, (warp & 3) * 32,
-                   ntok, last, tile_base, cb);
-      }
-    }
-  } else if constexpr (MODE == EPI_RECON) {
-    if (epi) {
-      // tcgen05.ld is warp-collective: every lane loads, only valid rows store
-      const int d = P.head_dim;
-      const int hd = P.heads * d;
-      const int layer = n0 / hd;
-      const int head0 = (n0 % hd) / d;
-      const int64_t ctok = P.tok_begin + tok;
-      __nv_bfloat16 *rowp = nullptr;
-      if (valid) {
-        int64_t slot = ctok;
-        if (P.layout == KVTC_LAYOUT_PAGED)
-          slot = int64_t(P.block_table[ctok / P.page_tokens]) * P.page_tokens + (ctok % P.page_tokens);
-        rowp = P.layer_base[layer] + slot * hd;
-      }
-      const float2 *cs = (P.cs && valid) ? P.cs + tok * (d / 2) : nullptr;
-      const bool rot = P.cs != nullptr;
-      for (int hh = 0; hh < ncols / d; ++hh) {
-        const int f = n0 + hh * d;                         // first feature of the head
-        __nv_bfloat16 *dst = valid ? rowp + (head0 + hh) * d : nullptr;
-        if (P.pairing == 0 || !rot) {
-          for (int c = 0; c < d / 2; c += 16) {
-            float lo[16], hi[16];
-            tmem_ld16(trow + hh * d + c, lo);
-            tmem_ld16(trow + hh * d + d / 2 + c, hi);
-            if (!valid) continue;
-            if (num_kb == 0) {
-#pragma unroll
-              for (int j = 0; j < 16; ++j) lo[j] = hi[j] = 0.0f;
-            }
-            __align__(16) __nv_bfloat16 olo[16], ohi[16];
+      if constexpr (MODE == EPI_F32 || MODE == EPI_XTX) {
+        for (int c = 0; c < n_mma; c += 16) {
+          float v[16];
+          tmem_ld16(trow + c, v);
+          if (valid && num_kb > 0) {
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-              const float x1 = __fadd_rn(lo[j], P.bias[f + c + j]);
-              const float x2 = __fadd_rn(hi[j], P.bias[f + d / 2 + c + j]);
-              float y1 = x1, y2 = x2;
-              if (rot) {
-                const float2 t = cs[c + j];
-                y1 = __fsub_rn(__fmul_rn(x1, t.x), __fmul_rn(x2, t.y));
-                y2 = __fadd_rn(__fmul_rn(x2, t.x), __fmul_rn(x1, t.y));
+              const int col = n0 + c + j;
+              if (c + j < ncols) {
+                float *dst = P.D + tok * P.ldd + col;
+                if constexpr (MODE == EPI_F32) *dst = __fsub_rn(v[j], P.bias[col]);
+                else *dst += v[j];
               }
-              olo[j] = __float2bfloat16_rn(y1);
-              ohi[j] = __float2bfloat16_rn(y2);
             }
-            uint4 *a = reinterpret_cast<uint4 *>(dst + c);
-            uint4 *b = reinterpret_cast<uint4 *>(dst + d / 2 + c);
-            a[0] = reinterpret_cast<uint4 *>(olo)[0];
-            a[1] = reinterpret_cast<uint4 *>(olo)[1];
-            b[0] = reinterpret_cast<uint4 *>(ohi)[0];
-            b[1] = reinterpret_cast<uint4 *>(ohi)[1];
-          }
-        } else {
-          for (int c = 0; c < d; c += 16) {
-            float v[16];
-            tmem_ld16(trow + hh * d + c, v);
-            if (!valid) continue;
-            if (num_kb == 0) {
-#pragma unroll
-              for (int j = 0; j < 16; ++j) v[j] = 0.0f;
-            }
-            __align__(16) __nv_bfloat16 o[16];
-#pragma unroll
-            for (int j = 0; j < 16; j += 2) {
-              const float x1 = __fadd_rn(v[j], P.bias[f + c + j]);
-              const float x2 = __fadd_rn(v[j + 1], P.bias[f + c + j + 1]);
-              const float2 t = cs[(c + j) / 2];
-              o[j] = __float2bfloat16_rn(__fsub_rn(__fmul_rn(x1, t.x), __fmul_rn(x2, t.y)));
-              o[j + 1] = __float2bfloat16_rn(__fadd_rn(__fmul_rn(x2, t.x), __fmul_rn(x1, t.y)));
-            }
-            uint4 *a = reinterpret_cast<uint4 *>(dst + c);
-            a[0] = reinterpret_cast<uint4 *>(o)[0];
-            a[1] = reinterpret_cast<uint4 *>(o)[1];
           }
         }
+        tc_fence_before();
+        mbar_arrive(&tmem_empty[acc]);
+      } else if constexpr (MODE == EPI_QUANT) {
+        // stage this thread's row of D (fp32, minus the bias mu V_c) in the ring's smem
+        float *xr = reinterpret_cast<float *>(tiles) + row * kStagePitch;
+        for (int c = 0; c < n_mma; c += 16) {
+          float v[16];
+          tmem_ld16(trow + c, v);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) xr[c + j] = (c + j < ncols) ? __fsub_rn(v[j], P.bias[n0 + c + j]) : 0.0f;
+        }
+        tc_fence_before();
+        mbar_arrive(&tmem_empty[acc]);                     // accumulator free for tile i+2
+        const int ntok = int(P.m - m0 < kTileM ? P.m - m0 : kTileM);
+        const bool last = ntok < kTileM;
+        uint8_t *tile_base = P.payload + T.mb * P.tile_bytes;
+        float rmn = 0.f, rmx = 0.f;
+        if (split) {
+          // one piece per CTA; exchange row min/max over the cluster (DSMEM)
+          const GroupDesc gd = P.groups[seg_g0];
+          float mn = xr[gd.col], mx = xr[gd.col];
+          for (int c = 1; c < gd.size; ++c) {
+            mn = fminf(mn, xr[gd.col + c]);
+            mx = fmaxf(mx, xr[gd.col + c]);
+          }
+          red[row] = make_float2(mn, mx);
+          cluster_sync_all();
+          rmn = red[row].x;
+          rmx = red[row].y;
+          for (int q = 0; q < P.parts; ++q) {
+            const float2 o = ld_peer_f2(&red[row], q);
+            rmn = fminf(rmn, o.x);
+            rmx = fmaxf(rmx, o.y);
+          }
+          cluster_sync_all();
+        }
+        for (int gi = seg_g0; gi < seg_g1; ++gi) {
+          const GroupDesc gd = P.groups[gi];
+          const float *x = xr + gd.col;
+          float mn, mx;
+          if (split) {
+            mn = rmn;
+            mx = rmx;
+          } else {
+            mn = x[0];
+            mx = x[0];
+            for (int c = 1; c < gd.size; ++c) {
+              mn = fminf(mn, x[c]);
+              mx = fmaxf(mx, x[c]);
+            }
+          }
+          uint8_t *cb = tile_base + (last ? P.codes_off_last[gd.gidx] : gd.codes_off);
+          emit_group(x, gd.size, gd.full_size, gd.part, gd.type, gd.gidx, mn, mx, valid, row, lane,
+                     (warp & 3) * 32, ntok, last, tile_base, cb);
+        }
+        mbar_arrive(epi_done);                             // staging smem may be overwritten
+      } else if constexpr (MODE == EPI_RECON) {
+        // tcgen05.ld is warp-collective: every lane loads, only valid rows store
+        const int d = P.head_dim;
+        const int hd = P.heads * d;
+        const int layer = n0 / hd;
+        const int head0 = (n0 % hd) / d;
+        const int64_t ctok = P.tok_begin + tok;
+        __nv_bfloat16 *rowp = nullptr;
+        if (valid) {
+          int64_t slot = ctok;
+          if (P.layout == KVTC_LAYOUT_PAGED)
+            slot = int64_t(P.block_table[ctok / P.page_tokens]) * P.page_tokens + (ctok % P.page_tokens);
+          rowp = P.layer_base[layer] + slot * hd;
+        }
+        const float2 *cs = (P.cs && valid) ? P.cs + tok * (d / 2) : nullptr;
+        const bool rot = P.cs != nullptr;
+        for (int hh = 0; hh < ncols / d; ++hh) {
+          const int f = n0 + hh * d;                         // first feature of the head
+          __nv_bfloat16 *dst = valid ? rowp + (head0 + hh) * d : nullptr;
+          if (P.pairing == 0 || !rot) {
+            for (int c = 0; c < d / 2; c += 16) {
+              float lo[16], hi[16];
+              tmem_ld16(trow + hh * d + c, lo);
+              tmem_ld16(trow + hh * d + d / 2 + c, hi);
+              if (!valid) continue;
+              if (num_kb == 0) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) lo[j] = hi[j] = 0.0f;
+              }
+              __align__(16) __nv_bfloat16 olo[16], ohi[16];
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                const float x1 = __fadd_rn(lo[j], P.bias[f + c + j]);
+                const float x2 = __fadd_rn(hi[j], P.bias[f + d / 2 + c + j]);
+                float y1 = x1, y2 = x2;
+                if (rot) {
+                  const float2 tt = cs[c + j];
+                  y1 = __fsub_rn(__fmul_rn(x1, tt.x), __fmul_rn(x2, tt.y));
+                  y2 = __fadd_rn(__fmul_rn(x2, tt.x), __fmul_rn(x1, tt.y));
+                }
+                olo[j] = __float2bfloat16_rn(y1);
+                ohi[j] = __float2bfloat16_rn(y2);
+              }
+              uint4 *a = reinterpret_cast<uint4 *>(dst + c);
+              uint4 *b = reinterpret_cast<uint4 *>(dst + d / 2 + c);
+              a[0] = reinterpret_cast<uint4 *>(olo)[0];
+              a[1] = reinterpret_cast<uint4 *>(olo)[1];
+              b[0] = reinterpret_cast<uint4 *>(ohi)[0];
+              b[1] = reinterpret_cast<uint4 *>(ohi)[1];
+            }
+          } else {
+            for (int c = 0; c < d; c += 16) {
+              float v[16];
+              tmem_ld16(trow + hh * d + c, v);
+              if (!valid) continue;
+              if (num_kb == 0) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[j] = 0.0f;
+              }
+              __align__(16) __nv_bfloat16 o[16];
+#pragma unroll
+              for (int j = 0; j < 16; j += 2) {
+                const float x1 = __fadd_rn(v[j], P.bias[f + c + j]);
+                const float x2 = __fadd_rn(v[j + 1], P.bias[f + c + j + 1]);
+                const float2 tt = cs[(c + j) / 2];
+                o[j] = __float2bfloat16_rn(__fsub_rn(__fmul_rn(x1, tt.x), __fmul_rn(x2, tt.y)));
+                o[j + 1] = __float2bfloat16_rn(__fadd_rn(__fmul_rn(x2, tt.x), __fmul_rn(x1, tt.y)));
+              }
+              uint4 *a = reinterpret_cast<uint4 *>(dst + c);
+              a[0] = reinterpret_cast<uint4 *>(o)[0];
+              a[1] = reinterpret_cast<uint4 *>(o)[1];
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tmem_empty[acc]);
       }
+      ++acc_it;
     }
   }
-
+  // split launches: the non-epilogue warps join the epilogue's two cluster barriers
+  if (split && warp < 4) {
+    __syncwarp();
+    cluster_sync_all();
+    cluster_sync_all();
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == 2) tmem_dealloc<kTmemCols>(tmem_base);
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
 }
 
 template <int MODE>
@@ -357,6 +442,8 @@ static kvtc_status launch(const CUtensorMap *tmA, const CUtensorMap *tmB, const 
   return KVTC_OK;
 }
 
+static unsigned persistent_grid(int64_t tiles) { return unsigned(std::min<int64_t>(tiles, num_sms())); }
+
 kvtc_status launch_gemm_project_f32(const GemmCompressArgs &a, int32_t ncols, cudaStream_t st) {
   Params p = {};
   p.K = a.K;
@@ -366,8 +453,10 @@ kvtc_status launch_gemm_project_f32(const GemmCompressArgs &a, int32_t ncols, cu
   p.D = a.D;
   p.ldd = a.ldd;
   p.fmt = 1;
-  dim3 grid(unsigned(ceil_div(ncols, kMaxTileN)), unsigned(ceil_div(a.m, kTileM)));
-  return launch<EPI_F32>(a.tmA, a.tmB, p, grid, 1, st);
+  p.tile_n = kMaxTileN;
+  p.num_m = int32_t(ceil_div(a.m, kTileM));
+  p.num_n = int32_t(ceil_div(ncols, kMaxTileN));
+  return launch<EPI_F32>(a.tmA, a.tmB, p, dim3(persistent_grid(int64_t(p.num_m) * p.num_n)), 1, st);
 }
 
 kvtc_status launch_gemm_project_quant(const GemmCompressArgs &a, cudaStream_t st) {
@@ -383,8 +472,11 @@ kvtc_status launch_gemm_project_quant(const GemmCompressArgs &a, cudaStream_t st
   p.tile_bytes = a.tile_bytes;
   p.codes_off_last = a.codes_off_last;
   p.fmt = 1;
-  dim3 grid(unsigned(a.nsegs), unsigned(ceil_div(a.m, kTileM)));
-  return launch<EPI_QUANT>(a.tmA, a.tmB, p, grid, a.parts, st);
+  p.num_m = int32_t(ceil_div(a.m, kTileM));
+  p.num_n = a.nsegs;
+  if (a.parts > 1)   // split groups: one tile per CTA, clusters along x
+    return launch<EPI_QUANT>(a.tmA, a.tmB, p, dim3(unsigned(a.nsegs), unsigned(p.num_m)), a.parts, st);
+  return launch<EPI_QUANT>(a.tmA, a.tmB, p, dim3(persistent_grid(int64_t(p.num_m) * p.num_n)), 1, st);
 }
 
 kvtc_status launch_gemm_reconstruct(const GemmDecompressArgs &a, cudaStream_t st) {
@@ -406,8 +498,9 @@ kvtc_status launch_gemm_reconstruct(const GemmDecompressArgs &a, cudaStream_t st
   p.tok_begin = a.tok_begin;
   p.fmt = 0;
   p.tile_n = a.tile_n;
-  dim3 grid(unsigned(ceil_div(a.n_end - a.n_begin, a.tile_n)), unsigned(ceil_div(a.m, kTileM)));
-  return launch<EPI_RECON>(a.tmA, a.tmB, p, grid, 1, st);
+  p.num_m = int32_t(ceil_div(a.m, kTileM));
+  p.num_n = int32_t(ceil_div(a.n_end - a.n_begin, a.tile_n));
+  return launch<EPI_RECON>(a.tmA, a.tmB, p, dim3(persistent_grid(int64_t(p.num_m) * p.num_n)), 1, st);
 }
 
 kvtc_status launch_gemm_xtx(const CUtensorMap *tmA, const CUtensorMap *tmB, int32_t p_, int32_t nk, float *S,
@@ -419,8 +512,10 @@ kvtc_status launch_gemm_xtx(const CUtensorMap *tmA, const CUtensorMap *tmB, int3
   p.D = S;
   p.ldd = p_;
   p.fmt = 1;
-  dim3 grid(unsigned(ceil_div(p_, kMaxTileN)), unsigned(ceil_div(p_, kTileM)));
-  return launch<EPI_XTX>(tmA, tmB, p, grid, 1, st);
+  p.tile_n = kMaxTileN;
+  p.num_m = int32_t(ceil_div(p_, kTileM));
+  p.num_n = int32_t(ceil_div(p_, kMaxTileN));
+  return launch<EPI_XTX>(tmA, tmB, p, dim3(persistent_grid(int64_t(p.num_m) * p.num_n)), 1, st);
 }
 
 }  // namespace kvtc
