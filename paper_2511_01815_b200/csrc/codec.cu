@@ -485,7 +485,8 @@ extern "C" size_t kvtc_decompress_workspace_bytes(const kvtc_basis *kb, const kv
   b.take<void *>(h.layers);
   b.take<void *>(h.layers);
   b.take<int32_t>(4);
-  b.take<uint8_t>(std::max(h.payload_bytes[0], h.payload_bytes[1]) + 16);
+  b.take<uint8_t>(h.payload_bytes[0] + 16);
+  b.take<uint8_t>(h.payload_bytes[1] + 16);
   b.take<__half>(h.m * std::max(std::max(kp->r_nz_pad, vp->r_nz_pad), 8));
   b.take<float2>(h.m * (kb->shape.head_dim / 2));
   return b.used + 256;
@@ -533,7 +534,9 @@ extern "C" kvtc_status kvtc_decompress(const kvtc_basis *kb, const kvtc_plan *kp
   auto *kbases = ws.take<__nv_bfloat16 *>(h.layers);
   auto *vbases = ws.take<__nv_bfloat16 *>(h.layers);
   int32_t *err = ws.take<int32_t>(4);
-  uint8_t *payload = ws.take<uint8_t>(std::max(h.payload_bytes[0], h.payload_bytes[1]) + 16);
+  uint8_t *payloads[2];
+  payloads[0] = ws.take<uint8_t>(h.payload_bytes[0] + 16);
+  payloads[1] = ws.take<uint8_t>(h.payload_bytes[1] + 16);
   const int64_t ld = std::max(std::max(kp->r_nz_pad, vp->r_nz_pad), 8);
   __half *Dh = ws.take<__half>(h.m * ld);
   float2 *cs = ws.take<float2>(h.m * (h.head_dim / 2));
@@ -552,6 +555,15 @@ extern "C" kvtc_status kvtc_decompress(const kvtc_basis *kb, const kvtc_plan *kp
   // device copy of the section offsets lives in the container header itself
   const uint64_t *sec_off_dev = reinterpret_cast<const uint64_t *>(ib + offsetof(ContainerHeader, section_off));
   if (kb->has_rope && (s = rope_table_for(kb, h.pos0 + h.sinks, h.m, cs, st))) return s;
+  {
+    // both streams' chunks in one inflate launch (warp per chunk)
+    ProfScope ps("d.inflate", st);
+    const uint32_t nk = uint32_t((h.payload_bytes[0] + h.chunk_bytes - 1) / h.chunk_bytes);
+    const uint32_t nv = uint32_t((h.payload_bytes[1] + h.chunk_bytes - 1) / h.chunk_bytes);
+    if ((s = launch_inflate_sections(ib, sec_off_dev, h.payload_bytes[0], nk, payloads[0], sec_off_dev + 1,
+                                     h.payload_bytes[1], nv, payloads[1], err, st)))
+      return s;
+  }
   for (int sv = 0; sv < 2; ++sv) {
     const kvtc_basis *b = sv ? vb : kb;
     kvtc_plan *pl = const_cast<kvtc_plan *>(sv ? vp : kp);
@@ -559,11 +571,7 @@ extern "C" kvtc_status kvtc_decompress(const kvtc_basis *kb, const kvtc_plan *kp
     __nv_bfloat16 *const *bs = sv ? vbases : kbases;
     const Operands *op;
     if ((s = plan_operands(b, pl, &op))) return s;
-    const uint32_t nch = uint32_t((h.payload_bytes[sv] + h.chunk_bytes - 1) / h.chunk_bytes);
-    {
-      ProfScope ps("d.inflate", st);
-      if ((s = launch_inflate_section(ib, sec_off_dev + sv, h.payload_bytes[sv], nch, payload, err, st))) return s;
-    }
+    const uint8_t *payload = payloads[sv];
     {
       ProfScope ps("d.dequant", st);
       if ((s = launch_dequant(pl->d_pgroups, pl->d_codes_off_full, pl->G, plan_codes_off_last(pl, h.m % kTileM),

@@ -208,18 +208,20 @@ __device__ void rank_sort(const uint32_t *freq, int nsym, int *sorted, int *nz_o
 }
 
 struct EncShared {
+  uint32_t whist[kEncThreads / 32][kLitSyms + 3];   // warp-private histograms
   uint32_t hist[kLitSyms + 3];
   uint32_t clhist[19];
   int sorted[kLitSyms + 3];
   int work[kLitSyms + 3];
-  int nz, clnz;
+  int num[33];
+  int nz;
   uint8_t len[kLitSyms + 3];
   uint16_t rev[kLitSyms + 3];
+  uint32_t sym[256];                                 // rev | len << 16 for literals
   uint8_t cllen[19];
   uint16_t clrev[19];
   uint16_t rle_sym[kLitSyms + 8];
   uint8_t rle_extra[kLitSyms + 8];
-  int nrle;
   uint32_t hdr[160];   // header bits (<= 5120)
   uint32_t hdr_bits;
   uint32_t total_bits;
@@ -227,10 +229,64 @@ struct EncShared {
   typename cub::BlockScan<uint32_t, kEncThreads>::TempStorage scan;
 };
 
-__global__ void __launch_bounds__(kEncThreads) deflate_encode_kernel(const uint8_t *in, uint64_t n, int32_t chunk,
-                                                                     uint8_t *slots, uint64_t stride,
-                                                                     uint32_t *chunk_bytes, uint32_t *chunk_kind,
-                                                                     uint32_t *index) {
+// Single-thread code-length builder over shared arrays (see build_lengths).
+__device__ void build_lengths_s(const uint32_t *freq, const int *sorted, int nz, int maxbits, uint8_t *len, int nsym,
+                                int *work, int *num) {
+  for (int s = 0; s < nsym; ++s) len[s] = 0;
+  if (nz == 0) return;
+  if (nz == 1) {
+    len[sorted[0]] = 1;
+    return;
+  }
+  for (int i = 0; i < nz; ++i) work[i] = int(freq[sorted[i]]);
+  min_redundancy_lengths(work, nz);
+  for (int i = 0; i < 33; ++i) num[i] = 0;
+  for (int i = 0; i < nz; ++i) num[work[i] > 32 ? 32 : work[i]]++;
+  for (int i = maxbits + 1; i <= 32; i++) {
+    num[maxbits] += num[i];
+    num[i] = 0;
+  }
+  uint32_t total = 0;
+  for (int i = maxbits; i > 0; i--) total += uint32_t(num[i]) << (maxbits - i);
+  while (total != (1u << maxbits)) {
+    num[maxbits]--;
+    for (int i = maxbits - 1; i > 0; i--)
+      if (num[i]) {
+        num[i]--;
+        num[i + 1] += 2;
+        break;
+      }
+    total--;
+  }
+  int j = nz;
+  for (int l = 1; l <= maxbits; ++l)
+    for (int k = num[l]; k > 0; --k) len[sorted[--j]] = uint8_t(l);
+}
+
+// LSB-first word writer into shared memory (block header).
+struct WordWriter {
+  uint32_t *buf;
+  uint64_t acc;
+  uint32_t nb, w;
+  __device__ void put(uint32_t v, int n) {
+    acc |= uint64_t(v & ((1u << n) - 1)) << nb;
+    nb += n;
+    if (nb >= 32) {
+      buf[w++] = uint32_t(acc);
+      acc >>= 32;
+      nb -= 32;
+    }
+  }
+  __device__ uint32_t finish() {
+    if (nb) buf[w] = uint32_t(acc);
+    return w * 32 + nb;
+  }
+};
+
+__global__ void __launch_bounds__(kEncThreads, 2) deflate_encode_kernel(const uint8_t *in, uint64_t n, int32_t chunk,
+                                                                        uint8_t *slots, uint64_t stride,
+                                                                        uint32_t *chunk_bytes, uint32_t *chunk_kind,
+                                                                        uint32_t *index) {
   __shared__ EncShared S;
   const int c = blockIdx.x;
   const uint64_t base = uint64_t(c) * chunk;
@@ -238,23 +294,33 @@ __global__ void __launch_bounds__(kEncThreads) deflate_encode_kernel(const uint8
   const uint8_t *src = in + base;
   uint8_t *out = slots + uint64_t(c) * stride;
   const int t = threadIdx.x;
+  const int warp = t / 32;
   const uint32_t piece = uint32_t(chunk) / kEncThreads;
-  const uint32_t p0 = min(nc, t * piece), p1 = min(nc, (t + 1) * piece);
+  const uint32_t p0 = umin32(nc, t * piece), p1 = umin32(nc, (t + 1) * piece);
 
-  for (int s = t; s < kLitSyms + 3; s += kEncThreads) S.hist[s] = 0;
+  for (int s = t; s < (kEncThreads / 32) * (kLitSyms + 3); s += kEncThreads) (&S.whist[0][0])[s] = 0;
   if (t < 19) S.clhist[t] = 0;
   if (t < 160) S.hdr[t] = 0;
   __syncthreads();
-  // ---- histogram (16-byte vector loads when aligned)
+  // ---- histogram: 16-byte vector loads over the whole chunk, warp-private bins
   {
-    uint32_t i = p0;
-    for (; i + 16 <= p1 && ((reinterpret_cast<uintptr_t>(src + i) & 15) == 0); i += 16) {
-      const uint4 v = *reinterpret_cast<const uint4 *>(src + i);
-      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    const bool aligned = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+    const uint32_t nvec = aligned ? nc / 16 : 0;
+    uint32_t *h = S.whist[warp];
+    for (uint32_t v = t; v < nvec; v += kEncThreads) {
+      const uint4 q = __ldg(reinterpret_cast<const uint4 *>(src) + v);
+      const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-      for (int k = 0; k < 16; ++k) atomicAdd(&S.hist[(w[k >> 2] >> (8 * (k & 3))) & 0xFF], 1u);
+      for (int k = 0; k < 16; ++k) atomicAdd(&h[(w4[k >> 2] >> (8 * (k & 3))) & 0xFF], 1u);
     }
-    for (; i < p1; ++i) atomicAdd(&S.hist[src[i]], 1u);
+    for (uint32_t i = nvec * 16 + t; i < nc; i += kEncThreads) atomicAdd(&h[src[i]], 1u);
+  }
+  __syncthreads();
+  for (int s = t; s < kLitSyms; s += kEncThreads) {
+    uint32_t v = 0;
+#pragma unroll
+    for (int w = 0; w < kEncThreads / 32; ++w) v += S.whist[w][s];
+    S.hist[s] = v;
   }
   __syncthreads();
   if (t == 0) S.hist[256] = 1;  // end-of-block
@@ -262,18 +328,15 @@ __global__ void __launch_bounds__(kEncThreads) deflate_encode_kernel(const uint8
   rank_sort(S.hist, kLitSyms, S.sorted, &S.nz);
   __syncthreads();
   if (t == 0) {
-    build_lengths(S.hist, S.sorted, S.nz, kMaxBits, S.len, kLitSyms, S.work);
+    build_lengths_s(S.hist, S.sorted, S.nz, kMaxBits, S.len, kLitSyms, S.work, S.num);
     canonical_codes(S.len, kLitSyms, S.rev);
     // code-length sequence: 257 literal/length lengths + 1 distance length (0)
-    uint8_t seq[kLitSyms + 1];
-    for (int s = 0; s < kLitSyms; ++s) seq[s] = S.len[s];
-    seq[kLitSyms] = 0;
     const int nseq = kLitSyms + 1;
     int nr = 0;
     for (int i = 0; i < nseq;) {
-      const uint8_t v = seq[i];
+      const uint8_t v = i < kLitSyms ? S.len[i] : 0;
       int run = 1;
-      while (i + run < nseq && seq[i + run] == v) run++;
+      while (i + run < nseq && (i + run < kLitSyms ? S.len[i + run] : 0) == v) run++;
       if (v == 0) {
         int left = run;
         while (left >= 11) {
@@ -295,32 +358,26 @@ __global__ void __launch_bounds__(kEncThreads) deflate_encode_kernel(const uint8
       }
       i += run;
     }
-    S.nrle = nr;
     for (int i = 0; i < nr; ++i) S.clhist[S.rle_sym[i]]++;
     // a complete code-length code needs >= 2 used symbols
     int used = 0;
     for (int i = 0; i < 19; ++i) used += S.clhist[i] != 0;
-    if (used < 2) {
-      for (int i = 0; i < 19 && used < 2; ++i)
-        if (!S.clhist[i]) { S.clhist[i] = 1; used++; }
-    }
-    int csorted[19], cwork[19];
+    for (int i = 0; i < 19 && used < 2; ++i)
+      if (!S.clhist[i]) { S.clhist[i] = 1; used++; }
+    int csorted[19];
     int cnz = 0;
-    for (int pass = 0; pass < 1; ++pass) {
-      // tiny insertion sort by (freq, symbol)
-      for (int s = 0; s < 19; ++s)
-        if (S.clhist[s]) {
-          int k = cnz++;
-          while (k > 0 && (S.clhist[csorted[k - 1]] > S.clhist[s])) { csorted[k] = csorted[k - 1]; --k; }
-          csorted[k] = s;
-        }
-    }
-    build_lengths(S.clhist, csorted, cnz, 7, S.cllen, 19, cwork);
+    for (int s = 0; s < 19; ++s)
+      if (S.clhist[s]) {
+        int k = cnz++;
+        while (k > 0 && (S.clhist[csorted[k - 1]] > S.clhist[s])) { csorted[k] = csorted[k - 1]; --k; }
+        csorted[k] = s;
+      }
+    build_lengths_s(S.clhist, csorted, cnz, 7, S.cllen, 19, S.work, S.num);
     canonical_codes(S.cllen, 19, S.clrev);
     const int order[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
     int hclen = 19;
     while (hclen > 4 && S.cllen[order[hclen - 1]] == 0) hclen--;
-    BitWriter bw{S.hdr, 0};
+    WordWriter bw{S.hdr, 0, 0, 0};
     bw.put(1, 1);            // BFINAL
     bw.put(2, 2);            // BTYPE = 10 (dynamic Huffman)
     bw.put(0, 5);            // HLIT  = 257 - 257
@@ -334,12 +391,24 @@ __global__ void __launch_bounds__(kEncThreads) deflate_encode_kernel(const uint8
       else if (s == 17) bw.put(S.rle_extra[i], 3);
       else if (s == 18) bw.put(S.rle_extra[i], 7);
     }
-    S.hdr_bits = bw.nbits;
+    S.hdr_bits = bw.finish();
   }
   __syncthreads();
+  S.sym[t] = uint32_t(S.rev[t]) | (uint32_t(S.len[t]) << 16);     // kEncThreads == 256 literals
+  __syncthreads();
   // ---- bit counts per piece, exclusive scan
+  const bool vec = ((reinterpret_cast<uintptr_t>(src + p0) & 15) == 0) && ((p1 - p0) % 16 == 0);
   uint32_t mybits = 0;
-  for (uint32_t i = p0; i < p1; ++i) mybits += S.len[src[i]];
+  if (vec) {
+    for (uint32_t i = p0; i < p1; i += 16) {
+      const uint4 q = __ldg(reinterpret_cast<const uint4 *>(src + i));
+      const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int k = 0; k < 16; ++k) mybits += S.sym[(w4[k >> 2] >> (8 * (k & 3))) & 0xFF] >> 16;
+    }
+  } else {
+    for (uint32_t i = p0; i < p1; ++i) mybits += S.sym[src[i]] >> 16;
+  }
   if (t == 0) mybits += S.hdr_bits;
   if (p1 == nc && p0 < p1) mybits += S.len[256];  // EOB after the last byte
   if (nc == 0 && t == 0) mybits += S.len[256];
@@ -370,7 +439,8 @@ __global__ void __launch_bounds__(kEncThreads) deflate_encode_kernel(const uint8
   // ---- segment index (bit offset of each 1/32 of the chunk)
   const uint32_t pieces_per_seg = kEncThreads / kNSeg;
   if (t % pieces_per_seg == 0) index[uint64_t(c) * kNSeg + t / pieces_per_seg] = myoff + (t == 0 ? S.hdr_bits : 0);
-  // ---- emission: full words stored, partial edge words OR-ed atomically
+  // ---- emission: words wholly inside this thread's bit range are stored,
+  // the two edge words (shared with the neighbours) are OR-ed atomically
   uint32_t *ow = reinterpret_cast<uint32_t *>(out);
   const uint32_t w_first = myoff >> 5, w_last = (myoff + mybits - 1) >> 5;
   if (mybits) {
@@ -380,38 +450,43 @@ __global__ void __launch_bounds__(kEncThreads) deflate_encode_kernel(const uint8
   __syncthreads();
   if (mybits) {
     uint64_t acc = 0;
-    uint32_t nb = myoff & 31;     // bits already "occupied" in the first word (left zeros)
+    uint32_t nb = myoff & 31;
     uint32_t w = w_first;
-    auto flush = [&](bool final_) {
-      while (nb >= 32 || (final_ && nb > 0)) {
+    bool edge = nb != 0;                                 // first word shared with the previous thread
+    if (t == 0) {
+      // the block header: whole words copied, the partial last word seeds the accumulator
+      const uint32_t hw = S.hdr_bits >> 5;
+      for (uint32_t i = 0; i < hw; ++i) ow[i] = S.hdr[i];
+      w = hw;
+      nb = S.hdr_bits & 31;
+      acc = nb ? (S.hdr[hw] & ((1u << nb) - 1)) : 0;
+      edge = false;
+    }
+    auto put = [&](uint32_t e) {
+      acc |= uint64_t(e & 0xFFFF) << nb;
+      nb += e >> 16;
+      if (nb >= 32) {
         const uint32_t word = uint32_t(acc);
-        if (w == w_first || w == w_last) atomicOr(&ow[w], word);
+        if (edge || w == w_last) atomicOr(&ow[w], word);
         else ow[w] = word;
+        edge = false;
         acc >>= 32;
-        nb = nb >= 32 ? nb - 32 : 0;
+        nb -= 32;
         ++w;
       }
     };
-    if (t == 0) {
-      for (uint32_t i = 0; i < S.hdr_bits; i += 16) {
-        const uint32_t k = umin32(16, S.hdr_bits - i);
-        const uint32_t v = (S.hdr[i >> 5] >> (i & 31)) & ((1u << k) - 1);
-        acc |= uint64_t(v) << nb;
-        nb += k;
-        flush(false);
+    if (vec) {
+      for (uint32_t i = p0; i < p1; i += 16) {
+        const uint4 q = __ldg(reinterpret_cast<const uint4 *>(src + i));
+        const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int k = 0; k < 16; ++k) put(S.sym[(w4[k >> 2] >> (8 * (k & 3))) & 0xFF]);
       }
+    } else {
+      for (uint32_t i = p0; i < p1; ++i) put(S.sym[src[i]]);
     }
-    for (uint32_t i = p0; i < p1; ++i) {
-      const uint8_t s = src[i];
-      acc |= uint64_t(S.rev[s]) << nb;
-      nb += S.len[s];
-      flush(false);
-    }
-    if (p1 == nc) {
-      acc |= uint64_t(S.rev[256]) << nb;
-      nb += S.len[256];
-    }
-    flush(true);
+    if (p1 == nc) put(uint32_t(S.rev[256]) | (uint32_t(S.len[256]) << 16));
+    if (nb) atomicOr(&ow[w], uint32_t(acc));
   }
   if (t == 0) {
     chunk_bytes[c] = (S.total_bits + 7) / 8;
@@ -590,77 +665,153 @@ __device__ int parse_dynamic(BitReader &br, uint8_t *lens, int &nlen, int &ndist
 }
 
 // ---- fast path: our indexed Huffman-literal chunks, warp per chunk
+// Bit reader over shared-memory words (header parsing).
+struct SmemBits {
+  const uint32_t *w;
+  uint32_t pos;
+  __device__ uint32_t get(int n) {   // n <= 25
+    const uint32_t wi = pos >> 5;
+    const uint64_t v = (uint64_t(w[wi]) | (uint64_t(w[wi + 1]) << 32)) >> (pos & 31);
+    pos += n;
+    return uint32_t(v) & ((1u << n) - 1);
+  }
+};
+__device__ int huff_decode_s(SmemBits &br, const Huff &h) {
+  int code = 0, first = 0, index = 0;
+  for (int l = 1; l < 16; ++l) {
+    code |= int(br.get(1));
+    const int count = h.count[l];
+    if (code - count < first) return h.symbol[index + (code - first)];
+    index += count;
+    first += count;
+    first <<= 1;
+    code <<= 1;
+  }
+  return -10;
+}
+
+constexpr int kHdrWords = 512;     // first 2 KiB of a chunk stream hold its block header
+
 struct FastShared {
-  uint16_t table[1024];        // (sym << 4) | len for codes <= 10 bits; 0 = slow
+  uint32_t hdr[kHdrWords + 2];
+  uint16_t table[1024];            // (sym << 4) | len for codes <= 10 bits; 0 = slow path
+  uint16_t code[260];
   Huff h;
   uint8_t lens[320];
   int status;
 };
 
-__global__ void __launch_bounds__(32) inflate_fast_kernel(const uint8_t *base, const uint64_t *off_dev,
-                                                          uint64_t n_out, uint32_t nchunks, uint8_t *out,
-                                                          int32_t *err) {
+struct InflateJobs {
+  const uint8_t *base;
+  const uint64_t *off_dev[2];      // device section offsets from base (nullable = 0)
+  uint64_t n_out[2];
+  uint32_t nch[2];
+  uint8_t *out[2];
+};
+
+__global__ void __launch_bounds__(32) inflate_fast_kernel(InflateJobs J, int32_t *err) {
   __shared__ FastShared S;
-  const uint8_t *section = base + (off_dev ? *off_dev : 0);
+  const int job = blockIdx.x < J.nch[0] ? 0 : 1;
+  const uint32_t c = job == 0 ? blockIdx.x : blockIdx.x - J.nch[0];
+  const uint8_t *section = J.base + (J.off_dev[job] ? *J.off_dev[job] : 0);
   const SectionHeader *hdr = reinterpret_cast<const SectionHeader *>(section);
-  if (hdr->magic != kSectionMagic || hdr->raw_bytes != n_out || hdr->nchunks != nchunks || hdr->nseg != kNSeg) {
-    if (threadIdx.x == 0) atomicExch(err, -20);
+  const int lane = threadIdx.x;
+  if (hdr->magic != kSectionMagic || hdr->raw_bytes != J.n_out[job] || hdr->nchunks != J.nch[job] ||
+      hdr->nseg != kNSeg) {
+    if (lane == 0) atomicExch(err, -20);
     return;
   }
-  const uint32_t c = blockIdx.x;
   const ChunkEntry e = reinterpret_cast<const ChunkEntry *>(section + sizeof(SectionHeader))[c];
   const uint32_t *index =
       reinterpret_cast<const uint32_t *>(section + sizeof(SectionHeader) + uint64_t(hdr->nchunks) * sizeof(ChunkEntry));
   const uint8_t *stream = section + hdr->data_offset + e.offset;
   const uint64_t obase = uint64_t(c) * hdr->chunk_bytes;
   const uint32_t nc = uint32_t(umin64(hdr->chunk_bytes, hdr->raw_bytes - obase));
-  const int lane = threadIdx.x;
-  uint8_t *o = out + obase;
+  uint8_t *o = J.out[job] + obase;
   if (e.kind == 1) {
     for (uint32_t i = lane; i < nc; i += 32) o[i] = stream[(i / 32768) * (32768 + 5) + 5 + (i % 32768)];
     return;
   }
+  // header bytes -> shared memory (coalesced), parsed by lane 0 from there
+  const uint32_t *words = reinterpret_cast<const uint32_t *>(stream);
+  const uint32_t nw = umin32((e.bytes + 3) / 4, kHdrWords);
+  for (uint32_t i = lane; i < kHdrWords + 2; i += 32) S.hdr[i] = i < nw ? __ldg(words + i) : 0u;
+  __syncwarp();
   if (lane == 0) {
-    BitReader br{stream, e.bytes, 0};
-    const uint32_t bfinal = br.bits(1), btype = br.bits(2);
-    int nlen, ndist;
-    int st = (btype == 2 && bfinal == 1) ? parse_dynamic(br, S.lens, nlen, ndist) : -1;
-    if (st == 0 && huff_build(S.h, S.lens, 257) < 0) st = -4;
+    SmemBits br{S.hdr, 0};
+    int st = 0;
+    const uint32_t bfinal = br.get(1), btype = br.get(2);
+    if (bfinal != 1 || btype != 2) st = -1;
+    int nlen = 0, ndist = 0;
+    if (!st) {
+      nlen = int(br.get(5)) + 257;
+      ndist = int(br.get(5)) + 1;
+      const int ncode = int(br.get(4)) + 4;
+      const int order[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
+      uint8_t cl[19];
+      for (int i = 0; i < 19; ++i) cl[i] = 0;
+      for (int i = 0; i < ncode; ++i) cl[order[i]] = uint8_t(br.get(3));
+      Huff hc;
+      if (nlen > 286 || ndist > 30 || huff_build(hc, cl, 19) != 0) st = -4;
+      int idx = 0;
+      while (!st && idx < nlen + ndist) {
+        const int sym = huff_decode_s(br, hc);
+        if (sym < 0) { st = sym; break; }
+        if (sym < 16) { S.lens[idx++] = uint8_t(sym); continue; }
+        int rep;
+        uint8_t v = 0;
+        if (sym == 16) {
+          if (idx == 0) { st = -5; break; }
+          v = S.lens[idx - 1];
+          rep = 3 + int(br.get(2));
+        } else if (sym == 17) {
+          rep = 3 + int(br.get(3));
+        } else {
+          rep = 11 + int(br.get(7));
+        }
+        if (idx + rep > nlen + ndist) { st = -6; break; }
+        while (rep--) S.lens[idx++] = v;
+      }
+      if (!st && (br.pos > 32u * kHdrWords || nlen != 257)) st = -7;   // our encoder: literals + EOB only
+    }
+    if (!st && huff_build(S.h, S.lens, 257) < 0) st = -4;
+    if (!st) {
+      // canonical codes (RFC 1951 §3.2.2)
+      int next[16], cnt[16] = {0};
+      for (int s = 0; s < 257; ++s) cnt[S.lens[s]]++;
+      cnt[0] = 0;
+      int code = 0;
+      for (int b = 1; b < 16; ++b) {
+        code = (code + cnt[b - 1]) << 1;
+        next[b] = code;
+      }
+      for (int s = 0; s < 257; ++s) S.code[s] = S.lens[s] ? uint16_t(next[S.lens[s]]++) : 0;
+    }
     S.status = st;
     if (st) atomicExch(err, st);
   }
-  __syncwarp();
-  if (S.status) return;
-  // 10-bit lookup table from canonical codes
   for (int i = lane; i < 1024; i += 32) S.table[i] = 0;
   __syncwarp();
-  if (lane == 0) {
-    int code = 0, k = 0;
-    for (int l = 1; l <= 15; ++l) {
-      for (int j = 0; j < S.h.count[l]; ++j, ++k, ++code) {
-        if (l <= 10) {
-          const int sym = S.h.symbol[k];
-          const uint32_t rev = __brev(uint32_t(code)) >> (32 - l);
-          for (uint32_t f = rev; f < 1024; f += (1u << l)) S.table[f] = uint16_t((sym << 4) | l);
-        }
-      }
-      code <<= 1;
-    }
+  if (S.status) return;
+  for (int s = lane; s < 257; s += 32) {
+    const int l = S.lens[s];
+    if (l == 0 || l > 10) continue;
+    const uint32_t rev = __brev(uint32_t(S.code[s])) >> (32 - l);
+    for (uint32_t f = rev; f < 1024; f += (1u << l)) S.table[f] = uint16_t((s << 4) | l);
   }
   __syncwarp();
   const uint32_t seg = hdr->seg_bytes;
-  const uint32_t s0 = lane * seg, s1 = min(nc, (lane + 1) * seg);
+  const uint32_t s0 = lane * seg, s1 = umin32(nc, (lane + 1) * seg);
   if (s0 >= s1) return;
-  const uint32_t *words = reinterpret_cast<const uint32_t *>(stream);
   uint64_t pos = index[uint64_t(c) * kNSeg + lane];
   uint64_t wi = pos >> 5;
-  uint64_t buf = uint64_t(words[wi++]) >> (pos & 31);
+  uint64_t buf = uint64_t(__ldg(words + wi++)) >> (pos & 31);
   int cnt = 32 - int(pos & 31);
   uint32_t outw = 0;
   int nout = 0;
   for (uint32_t i = s0; i < s1; ++i) {
     if (cnt <= 32) {
-      buf |= uint64_t(words[wi++]) << cnt;
+      buf |= uint64_t(__ldg(words + wi++)) << cnt;
       cnt += 32;
     }
     const uint16_t te = S.table[buf & 1023];
@@ -703,12 +854,28 @@ __global__ void __launch_bounds__(32) inflate_fast_kernel(const uint8_t *base, c
   for (int k = 0; k < nout; ++k) o[s1 - nout + k] = (outw >> (8 * k)) & 0xFF;
 }
 
-kvtc_status launch_inflate_section(const uint8_t *base, const uint64_t *off_dev, uint64_t n_out, uint32_t nchunks,
-                                   uint8_t *out, int32_t *err, cudaStream_t st) {
-  if (nchunks == 0) return KVTC_OK;
-  inflate_fast_kernel<<<nchunks, 32, 0, st>>>(base, off_dev, n_out, nchunks, out, err);
+kvtc_status launch_inflate_sections(const uint8_t *base, const uint64_t *off_dev0, uint64_t n0, uint32_t nch0,
+                                    uint8_t *out0, const uint64_t *off_dev1, uint64_t n1, uint32_t nch1,
+                                    uint8_t *out1, int32_t *err, cudaStream_t st) {
+  InflateJobs J;
+  J.base = base;
+  J.off_dev[0] = off_dev0;
+  J.off_dev[1] = off_dev1;
+  J.n_out[0] = n0;
+  J.n_out[1] = n1;
+  J.nch[0] = nch0;
+  J.nch[1] = nch1;
+  J.out[0] = out0;
+  J.out[1] = out1;
+  if (nch0 + nch1 == 0) return KVTC_OK;
+  inflate_fast_kernel<<<nch0 + nch1, 32, 0, st>>>(J, err);
   KVTC_LAUNCH_CHECK();
   return KVTC_OK;
+}
+
+kvtc_status launch_inflate_section(const uint8_t *base, const uint64_t *off_dev, uint64_t n_out, uint32_t nchunks,
+                                   uint8_t *out, int32_t *err, cudaStream_t st) {
+  return launch_inflate_sections(base, off_dev, n_out, nchunks, out, nullptr, 0, 0, nullptr, err, st);
 }
 
 // Validates a section header (host copy) against the expected payload size.

@@ -258,33 +258,50 @@ kvtc_status launch_quant_pack_simt(const SegDesc *segs, const GroupDesc *groups,
 }
 
 // ---------------------------------------------------------------- dequant
-// Block = one tile x one group; thread = token row.  x^ = code*scale + shift in
-// fp32 (fp8: e4m3(code)*scale + shift), then D^ = fp16(x^) (R5).
-__global__ void __launch_bounds__(128) dequant_kernel(const PlanGroup *groups, const int64_t *codes_off_full,
-                                                      int32_t G, const int64_t *codes_off_last, int64_t tile_bytes,
-                                                      const uint8_t *payload, int64_t m, __half *Dh, int64_t ld) {
-  const int g = blockIdx.x;
-  const PlanGroup pg = groups[g];
-  const int row = threadIdx.x;
+// Block = one tile x a run of kDqGroups groups.  For each group the block walks
+// the (token, code) pairs in the order the payload stores them (token-major,
+// code fastest), so code reads and D^ writes (the token's size_g consecutive
+// fp16) are both coalesced.  x^ = code*scale + shift in fp32 (fp8: e4m3(code)*
+// scale + shift), D^ = fp16(x^) (R5).
+constexpr int kDqGroups = 8;
+constexpr int kDqThreads = 256;
+
+__global__ void __launch_bounds__(kDqThreads) dequant_kernel(const PlanGroup *groups, const int64_t *codes_off_full,
+                                                             int32_t G, const int64_t *codes_off_last,
+                                                             int64_t tile_bytes, const uint8_t *payload, int64_t m,
+                                                             __half *Dh, int64_t ld) {
+  __shared__ float s_shift[kTileM], s_scale[kTileM];
   const int64_t m0 = int64_t(blockIdx.y) * kTileM;
-  const int64_t tok = m0 + row;
-  if (tok >= m) return;
   const int ntok = int(m - m0 < kTileM ? m - m0 : kTileM);
   const bool last = ntok < kTileM;
   const uint8_t *tile = payload + blockIdx.y * tile_bytes;
-  const uint8_t *pp = tile + 4 * (int64_t(g) * ntok + row);
-  const uint16_t sh = uint16_t(pp[0]) | (uint16_t(pp[1]) << 8);
-  const uint16_t sc = uint16_t(pp[2]) | (uint16_t(pp[3]) << 8);
-  const float shift = f16_val(sh), scale = f16_val(sc);
-  const uint8_t *cb = tile + (last ? codes_off_last[g] : codes_off_full[g]);
-  const int b = bits_of(pg.type);
-  const int64_t bit0 = int64_t(row) * pg.size * b;
-  __half *out = Dh + tok * ld + pg.col;
-  for (int c = 0; c < pg.size; ++c) {
-    const int64_t bit = bit0 + int64_t(c) * b;
-    const uint32_t code = (cb[bit >> 3] >> (bit & 7)) & ((1u << b) - 1);
-    const float v = pg.type == KVTC_T_FP8 ? e4m3_to_f32(uint8_t(code)) : float(code);
-    out[c] = __float2half_rn(__fadd_rn(__fmul_rn(v, scale), shift));
+  const int g_end = min(G, int(blockIdx.x + 1) * kDqGroups);
+  for (int g = blockIdx.x * kDqGroups; g < g_end; ++g) {
+    const PlanGroup pg = groups[g];
+    __syncthreads();
+    for (int r = threadIdx.x; r < ntok; r += kDqThreads) {
+      const uint8_t *pp = tile + 4 * (int64_t(g) * ntok + r);
+      const uint16_t sh = uint16_t(pp[0]) | (uint16_t(pp[1]) << 8);
+      const uint16_t sc = uint16_t(pp[2]) | (uint16_t(pp[3]) << 8);
+      s_shift[r] = f16_val(sh);
+      s_scale[r] = f16_val(sc);
+    }
+    __syncthreads();
+    const uint8_t *cb = tile + (last ? codes_off_last[g] : codes_off_full[g]);
+    const int b = bits_of(pg.type);
+    const uint32_t mask = (1u << b) - 1;
+    const int size = pg.size;
+    const bool pow2 = (size & (size - 1)) == 0;
+    const int lg = pow2 ? __ffs(size) - 1 : 0;
+    const int n = ntok * size;
+    for (int e = threadIdx.x; e < n; e += kDqThreads) {
+      const int tau = pow2 ? (e >> lg) : e / size;
+      const int c = pow2 ? (e & (size - 1)) : e % size;
+      const int64_t bit = int64_t(e) * b;
+      const uint32_t code = (cb[bit >> 3] >> (bit & 7)) & mask;
+      const float v = pg.type == KVTC_T_FP8 ? e4m3_to_f32(uint8_t(code)) : float(code);
+      Dh[(m0 + tau) * ld + pg.col + c] = __float2half_rn(__fadd_rn(__fmul_rn(v, s_scale[tau]), s_shift[tau]));
+    }
   }
 }
 
@@ -292,8 +309,9 @@ kvtc_status launch_dequant(const PlanGroup *groups_dev, const int64_t *codes_off
                            const int64_t *codes_off_last, int64_t tile_bytes, const uint8_t *payload, int64_t m,
                            __half *Dh, int64_t ld, cudaStream_t st) {
   if (G == 0 || m == 0) return KVTC_OK;
-  dim3 grid(unsigned(G), unsigned(ceil_div(m, kTileM)));
-  dequant_kernel<<<grid, 128, 0, st>>>(groups_dev, codes_off_full, G, codes_off_last, tile_bytes, payload, m, Dh, ld);
+  dim3 grid(unsigned(ceil_div(G, kDqGroups)), unsigned(ceil_div(m, kTileM)));
+  dequant_kernel<<<grid, kDqThreads, 0, st>>>(groups_dev, codes_off_full, G, codes_off_last, tile_bytes, payload, m,
+                                               Dh, ld);
   KVTC_LAUNCH_CHECK();
   return KVTC_OK;
 }

@@ -133,6 +133,10 @@ kvtc_status launch_deflate(const uint8_t *in, size_t n, int32_t chunk, uint8_t *
 kvtc_status launch_inflate_section(const uint8_t *base, const uint64_t *off_dev, uint64_t n_out, uint32_t nchunks,
                                    uint8_t *out, int32_t *err, cudaStream_t st);
 kvtc_status check_section_header(const void *hdr_host, size_t len, size_t n_out, uint32_t *nchunks);
+// Both streams' sections in one launch (warp per chunk); sections at base + *off_dev.
+kvtc_status launch_inflate_sections(const uint8_t *base, const uint64_t *off_dev0, uint64_t n0, uint32_t nch0,
+                                    uint8_t *out0, const uint64_t *off_dev1, uint64_t n1, uint32_t nch1,
+                                    uint8_t *out1, int32_t *err, cudaStream_t st);
 constexpr size_t kSectionHeaderBytes = 64;
 kvtc_status launch_inflate_raw(const uint8_t *in, const int64_t *in_off, const int64_t *in_len, int32_t n,
                                uint8_t *out, const int64_t *out_off, const int64_t *out_len, int32_t *status,
