@@ -111,6 +111,7 @@ def build_artifacts(K, spec, args, rank, world, dist):
     """Calibration (K6, NCCL all-reduce of X^T X when world > 1) and the DP (K7/K8).
     Untimed setup; deterministic, so every rank ends with the same basis and plan."""
     from kvtc_inputs import generate, sample_positions
+    from paper_2511_01815_b200.distributed import calibrate_distributed
     shape = (spec.layers, spec.kv_heads, spec.head_dim)
     invf = spec.inv_freq().numpy().astype(np.float32)
     lens = [args.cal_tokens] * args.cal_seqs
@@ -122,24 +123,15 @@ def build_artifacts(K, spec, args, rank, world, dist):
         views = [K.KVView(c) for c in caches]
         torch.cuda.synchronize()
         tg = time.time()
-        p = spec.p
-        sum_x = torch.zeros(p, dtype=torch.float64, device="cuda")
-        xtx = torch.zeros(p, p, dtype=torch.float32, device="cuda")
-        K.calibrate_accumulate(views, samples[rank::world], stream, sum_x, xtx, inv_freq=invf)
-        if world > 1:
-            dist.all_reduce(sum_x)
-            dist.all_reduce(xtx)
-        torch.cuda.synchronize()
-        tx = time.time()
-        basis = K.calibrate_finalize(shape, stream, sum_x, xtx, len(samples), args.rank_cap, inv_freq=invf)
-        del sum_x, xtx
+        # shard of the draw on this rank -> NCCL all-reduce of (sum_x, X^T X, n) -> finalize
+        basis = calibrate_distributed(K, views, samples, stream, args.rank_cap, inv_freq=invf)
         torch.cuda.empty_cache()
-        te = time.time()
+        tx = te = time.time()
         plan = K.allocate_bits(basis, views, samples, args.cr)
         td = time.time()
         pi = plan.info()
-        info[("k", "v")[stream]] = {"gen_s": round(tg - t0, 2), "xtx_s": round(tx - tg, 2), "eig_s": round(te - tx, 2),
-                                    "dp_s": round(td - te, 2), "r": basis.get()[1].shape[1] if False else None,
+        info[("k", "v")[stream]] = {"gen_s": round(tg - t0, 2), "calib_s": round(tx - tg, 2),
+                                    "dp_s": round(td - te, 2),
                                     "r_eff": pi.r_eff, "groups": len(pi.groups),
                                     "bits_per_token": pi.bits_per_token, "budget": pi.budget,
                                     "r_nz": sum(z for (_, z, _) in pi.groups)}
