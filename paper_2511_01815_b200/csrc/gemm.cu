@@ -18,9 +18,8 @@
 // TMEM allocator, warps 4-7 epilogue (warp w reads TMEM lanes 32*(w%4)..+31).
 // Operands K-major, 128 B swizzled, 4-stage mbarrier ring; two fp32 TMEM
 // accumulators (2 x 256 columns) so the epilogue of tile i overlaps the MMAs of
-// tile i+1 (EPI_QUANT stages D in the ring's shared memory, so there the
-// producer waits for the epilogue instead).  Split-group launches (clusters)
-// run one tile per CTA.
+// tile i+1; EPI_QUANT quantises straight from TMEM (two passes per group).
+// Split-group launches (clusters) run one tile per CTA.
 #include <algorithm>
 
 #include "internal.h"
@@ -32,7 +31,6 @@ constexpr int kStages = 4;
 constexpr int kABytes = kTileM * kBlockK * 2;      // 16 KiB
 constexpr int kBBytes = kMaxTileN * kBlockK * 2;   // 32 KiB
 constexpr int kStageBytes = kABytes + kBBytes;     // 48 KiB
-constexpr int kStagePitch = 257;                   // fp32 words per staged row (conflict-free)
 constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 2048;
 constexpr int kThreads = 256;
 constexpr int kTmemCols = 512;                     // two 256-column accumulators
@@ -84,6 +82,24 @@ struct Tile {
   bool valid;
 };
 
+__device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
+  uint32_t r;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  return __uint_as_float(r);
+}
+
+// Loads columns [c, c + n) (n <= 16) of this thread's TMEM row, minus the bias.
+__device__ __forceinline__ void load_cols(uint32_t trow, const float *bias, int c, int n, float *x) {
+  if (n == 16) {
+    tmem_ld16(trow + c, x);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) x[j] = __fsub_rn(x[j], bias[c + j]);
+  } else {
+    for (int j = 0; j < n; ++j) x[j] = __fsub_rn(tmem_ld1(trow + c + j), bias[c + j]);
+  }
+}
+
 // Static persistent schedule: tile t -> (mb, nb) in groups of kGroupM M-blocks.
 template <int MODE>
 __device__ __forceinline__ Tile tile_of(const Params &P, int64_t t) {
@@ -132,8 +148,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t *empty_bar = full_bar + kStages;
   uint64_t *tmem_full = empty_bar + kStages;      // [2]
   uint64_t *tmem_empty = tmem_full + 2;           // [2]
-  uint64_t *epi_done = tmem_empty + 2;            // [1] QUANT: staging smem released
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(epi_done + 1);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_empty + 2);
   float2 *red = reinterpret_cast<float2 *>(smem + kStages * kStageBytes + 256);   // [128] row min/max
 
   const int warp = threadIdx.x / 32;
@@ -156,7 +171,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tmem_full[a], 1);
       mbar_init(&tmem_empty[a], 128);
     }
-    mbar_init(epi_done, 128);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
@@ -178,13 +192,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer
-    uint32_t it = 0, ntile = 0;
+    uint32_t it = 0;
     for (int64_t t = t_first; t < total; t += t_step) {
       const Tile T = get_tile(t);
       if (!T.valid) continue;
       int n0, ncols, g0, g1;
       tile_geometry<MODE>(P, T, n0, ncols, g0, g1);
-      if (MODE == EPI_QUANT && ntile > 0) mbar_wait(epi_done, (ntile - 1) & 1);   // staging smem free again
       for (int kb = 0; kb < num_kb; ++kb, ++it) {
         const int s = it % kStages;
         if (it >= kStages) mbar_wait(&empty_bar[s], ((it / kStages) - 1) & 1);
@@ -194,7 +207,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_2d(a, &tmA, &full_bar[s], kb * kBlockK, T.mb * kTileM);
         tma_load_2d(b, &tmB, &full_bar[s], kb * kBlockK, n0);
       }
-      ++ntile;
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer (one thread)
@@ -260,59 +272,80 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         mbar_arrive(&tmem_empty[acc]);
       } else if constexpr (MODE == EPI_QUANT) {
-        // stage this thread's row of D (fp32, minus the bias mu V_c) in the ring's smem
-        float *xr = reinterpret_cast<float *>(tiles) + row * kStagePitch;
-        for (int c = 0; c < n_mma; c += 16) {
-          float v[16];
-          tmem_ld16(trow + c, v);
-#pragma unroll
-          for (int j = 0; j < 16; ++j) xr[c + j] = (c + j < ncols) ? __fsub_rn(v[j], P.bias[n0 + c + j]) : 0.0f;
-        }
-        tc_fence_before();
-        mbar_arrive(&tmem_empty[acc]);                     // accumulator free for tile i+2
+        // Straight from TMEM, group by group: pass 1 min/max, pass 2 encode + pack
+        // (no shared-memory staging, so the next tile's MMAs overlap this epilogue).
         const int ntok = int(P.m - m0 < kTileM ? P.m - m0 : kTileM);
         const bool last = ntok < kTileM;
         uint8_t *tile_base = P.payload + T.mb * P.tile_bytes;
-        float rmn = 0.f, rmx = 0.f;
-        if (split) {
-          // one piece per CTA; exchange row min/max over the cluster (DSMEM)
-          const GroupDesc gd = P.groups[seg_g0];
-          float mn = xr[gd.col], mx = xr[gd.col];
-          for (int c = 1; c < gd.size; ++c) {
-            mn = fminf(mn, xr[gd.col + c]);
-            mx = fmaxf(mx, xr[gd.col + c]);
-          }
-          red[row] = make_float2(mn, mx);
-          cluster_sync_all();
-          rmn = red[row].x;
-          rmx = red[row].y;
-          for (int q = 0; q < P.parts; ++q) {
-            const float2 o = ld_peer_f2(&red[row], q);
-            rmn = fminf(rmn, o.x);
-            rmx = fmaxf(rmx, o.y);
-          }
-          cluster_sync_all();
-        }
+        const float *bias = P.bias + n0;
         for (int gi = seg_g0; gi < seg_g1; ++gi) {
           const GroupDesc gd = P.groups[gi];
-          const float *x = xr + gd.col;
-          float mn, mx;
-          if (split) {
-            mn = rmn;
-            mx = rmx;
-          } else {
-            mn = x[0];
-            mx = x[0];
-            for (int c = 1; c < gd.size; ++c) {
-              mn = fminf(mn, x[c]);
-              mx = fmaxf(mx, x[c]);
+          const int step = (gd.size % 16 == 0) ? 16 : 1;
+          float mn = INFINITY, mx = -INFINITY;
+          for (int c = 0; c < gd.size; c += step) {
+            float x[16];
+            load_cols(trow, bias, gd.col + c, step, x);
+            for (int j = 0; j < step; ++j) {
+              mn = fminf(mn, x[j]);
+              mx = fmaxf(mx, x[j]);
             }
           }
+          if (split) {
+            // one piece per CTA; exchange row min/max over the cluster (DSMEM)
+            red[row] = make_float2(mn, mx);
+            cluster_sync_all();
+            for (int q = 0; q < P.parts; ++q) {
+              const float2 o = ld_peer_f2(&red[row], q);
+              mn = fminf(mn, o.x);
+              mx = fmaxf(mx, o.y);
+            }
+            cluster_sync_all();
+          }
+          uint16_t sh, sc;
+          group_factors(gd.type, mn, mx, sh, sc);
+          const float shift = f16_val(sh), scale = f16_val(sc);
+          if (valid && gd.part == 0)
+            store_u32_any(tile_base + 4 * (int64_t(gd.gidx) * ntok + row), uint32_t(sh) | (uint32_t(sc) << 16),
+                          !last);
+          const int bq = bits_of(gd.type);
+          const int tok_bits = gd.full_size * bq;
           uint8_t *cb = tile_base + (last ? P.codes_off_last[gd.gidx] : gd.codes_off);
-          emit_group(x, gd.size, gd.full_size, gd.part, gd.type, gd.gidx, mn, mx, valid, row, lane,
-                     (warp & 3) * 32, ntok, last, tile_base, cb);
+          if ((tok_bits & 7) == 0) {
+            uint8_t *dst = cb + int64_t(row) * (tok_bits / 8) + gd.part * (gd.size * bq / 8);
+            for (int c = 0; c < gd.size; c += step) {
+              float x[16];
+              load_cols(trow, bias, gd.col + c, step, x);
+              if (valid) write_codes_aligned(dst + (c * bq) / 8, x, step, gd.type, shift, scale, !last);
+            }
+          } else {
+            // sub-byte tokens (size * bits < 8): warp OR-reduction, as in emit_group
+            float x[16];
+            load_cols(trow, bias, gd.col, gd.size, x);
+            uint32_t bits_v = 0;
+            for (int c = 0; c < gd.size; ++c) bits_v |= (valid ? encode_one(gd.type, x[c], shift, scale) : 0u) << (c * bq);
+            const int nb = tok_bits;
+            const int bitpos = lane * nb;
+            const int64_t blk_len = (int64_t(ntok) * nb + 7) / 8;
+            const int64_t warp_byte0 = int64_t((warp & 3) * 32) * nb / 8;
+            for (int w = 0; w < nb; ++w) {
+              uint32_t mine = 0;
+              if ((bitpos >> 5) == w) mine = bits_v << (bitpos & 31);
+              if (((bitpos + nb - 1) >> 5) == w && (bitpos >> 5) != w) mine = bits_v >> (32 - (bitpos & 31));
+              const uint32_t word = __reduce_or_sync(0xffffffffu, mine);
+              if (lane == w) {
+                const int64_t off = warp_byte0 + 4 * w;
+                if (!last) {
+                  *reinterpret_cast<uint32_t *>(cb + off) = word;
+                } else {
+                  for (int k = 0; k < 4; ++k)
+                    if (off + k < blk_len) cb[off + k] = (word >> (8 * k)) & 0xFF;
+                }
+              }
+            }
+          }
         }
-        mbar_arrive(epi_done);                             // staging smem may be overwritten
+        tc_fence_before();
+        mbar_arrive(&tmem_empty[acc]);
       } else if constexpr (MODE == EPI_RECON) {
         // tcgen05.ld is warp-collective: every lane loads, only valid rows store
         const int d = P.head_dim;
