@@ -362,10 +362,10 @@ kvtc_status plan_operands(const kvtc_basis *b, kvtc_plan *pl, const Operands **o
       KVTC_CUDA_TRY(cudaDeviceSynchronize());
       cudaFree(d_pc);
       kvtc_status st = make_tmap_2d(&op.tm_VcT, op.VcT, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, b->p, op.r_nz,
-                                    uint64_t(b->p) * 2, kBlockK, kMaxTileN);
+                                    uint64_t(b->p) * 2, kBlockK, kMaxTileN / 2);
       if (st != KVTC_OK) return st;
       st = make_tmap_2d(&op.tm_Vd, op.Vd, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, op.r_nz, b->p, uint64_t(op.r_nz_pad) * 2,
-                        kBlockK, kMaxTileN);
+                        kBlockK, kMaxTileN / 2);
       if (st != KVTC_OK) return st;
     }
     op.ready = true;

@@ -247,7 +247,7 @@ extern "C" kvtc_status kvtc_calibrate_accumulate(const kvtc_kv_view *seqs, int32
     KVTC_LAUNCH_CHECK();
     CUtensorMap tA, tB;
     if ((s = make_tmap_2d(&tA, Ct, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, nk_pad, p, nk_pad * 2, kBlockK, kTileM))) return s;
-    if ((s = make_tmap_2d(&tB, Ct, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, nk_pad, p, nk_pad * 2, kBlockK, kMaxTileN)))
+    if ((s = make_tmap_2d(&tB, Ct, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, nk_pad, p, nk_pad * 2, kBlockK, kMaxTileN / 2)))
       return s;
     if ((s = launch_gemm_xtx(&tA, &tB, int32_t(p), int32_t(nk_pad), xtx, st))) return s;
   }

@@ -1,6 +1,7 @@
 // codec.cu — stage entry points and the compress / decompress orchestration
 // with the container format of DESIGN.md §4.
 #include <cstring>
+#include <mutex>
 
 #include "api_internal.h"
 
@@ -111,6 +112,28 @@ kvtc_status run_reconstruct(const kvtc_basis *b, const kvtc_plan *pl, const Oper
   return launch_gemm_reconstruct(a, st);
 }
 
+// Library-internal side stream (one per device) used to overlap the integer
+// codec kernels (DEFLATE / inflate / dequantise) with the tensor-core GEMMs of
+// the other stream: a persistent GEMM CTA (197 KB smem, 256 threads) leaves room
+// on every SM for one codec CTA.  Fork/join with events on the caller's stream.
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+};
+SideStream *side_stream() {
+  static std::mutex mu;
+  static SideStream per_dev[16];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  SideStream &S = per_dev[dev & 15];
+  if (!S.s) {
+    cudaStreamCreateWithFlags(&S.s, cudaStreamNonBlocking);
+    for (auto &e : S.ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  }
+  return &S;
+}
+
 bool same_shape(const kvtc_shape &a, const kvtc_shape &b) {
   return a.layers == b.layers && a.kv_heads == b.kv_heads && a.head_dim == b.head_dim;
 }
@@ -141,7 +164,7 @@ extern "C" kvtc_status kvtc_stage_project(const kvtc_basis *b, const kvtc_plan *
     ncols = op->r_nz;
   } else {
     if ((s = make_tmap_2d(&tB, b->d_VcT, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, b->p, b->r, uint64_t(b->p) * 2, kBlockK,
-                          kMaxTileN)))
+                          kMaxTileN / 2)))
       return s;
     a.tmB = &tB;
     a.bias = b->d_bias;
@@ -312,7 +335,8 @@ extern "C" size_t kvtc_compress_workspace_bytes(const kvtc_basis *kb, const kvtc
   b.take<uint64_t>(8);
   b.take<__nv_bfloat16>(L.m * kb->p);
   b.take<float2>(L.m * (kb->shape.head_dim / 2));
-  b.take<uint8_t>(std::max(L.pay[0], L.pay[1]) + 16);
+  b.take<uint8_t>(L.pay[0] + 16);
+  b.take<uint8_t>(L.pay[1] + 16);
   b.take<uint8_t>(deflate_workspace(std::max(L.pay[0], L.pay[1]), pol->chunk_bytes));
   return b.used + 256;
 }
@@ -352,7 +376,8 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
   uint64_t *lens = ws.take<uint64_t>(8);     // [0..1] section lengths, [2..3] section offsets
   auto *X = ws.take<__nv_bfloat16>(L.m * kb->p);
   float2 *cs = ws.take<float2>(L.m * (kb->shape.head_dim / 2));
-  uint8_t *payload = ws.take<uint8_t>(std::max(L.pay[0], L.pay[1]) + 16);
+  uint8_t *payload_k = ws.take<uint8_t>(L.pay[0] + 16);
+  uint8_t *payload_v = ws.take<uint8_t>(L.pay[1] + 16);
   const size_t dws = deflate_workspace(std::max(L.pay[0], L.pay[1]), pol->chunk_bytes);
   void *dwsp = ws.take<uint8_t>(dws);
   if ((s = upload_bases(k, kbases, st)) || (s = upload_bases(v, vbases, st))) return s;
@@ -406,7 +431,10 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
     return KVTC_NOTHING_TO_COMPRESS;
   }
   KVTC_CUDA_TRY(cudaMemcpyAsync(lens + 2, &h.section_off[0], 8, cudaMemcpyHostToDevice, st));
-  // ---- keys: un-RoPE gather (K1) -> fused projection + quantisation (K2) -> DEFLATE (K3)
+  // ---- keys: un-RoPE gather (K1) -> fused projection + quantisation (K2); the
+  // keys' DEFLATE (K3) then runs on the side stream while the values' gather and
+  // GEMM run on the caller's stream, and the values' DEFLATE follows it there.
+  SideStream *ss = side_stream();
   {
     ProfScope ps("c.gather_unrope", st);
     if ((s = rope_table_for(kb, k->pos0 + pol->sinks, L.m, cs, st))) return s;
@@ -414,13 +442,15 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
   }
   {
     ProfScope ps("c.project_quant_gemm", st);
-    if ((s = run_project_quant(kb, kpl, kop, X, L.m, payload, st))) return s;
+    if ((s = run_project_quant(kb, kpl, kop, X, L.m, payload_k, st))) return s;
   }
+  KVTC_CUDA_TRY(cudaEventRecord(ss->ev[0], st));
+  KVTC_CUDA_TRY(cudaStreamWaitEvent(ss->s, ss->ev[0], 0));
   {
-    ProfScope ps("c.deflate", st);
-    if ((s = launch_deflate(payload, L.pay[0], pol->chunk_bytes, o, lens + 2, lens + 0, dwsp, dws, st))) return s;
+    ProfScope ps("c.deflate_overlapped", ss->s);
+    if ((s = launch_deflate(payload_k, L.pay[0], pol->chunk_bytes, o, lens + 2, lens + 0, dwsp, dws, ss->s))) return s;
   }
-  offset_after_kernel<<<1, 1, 0, st>>>(lens + 2, lens + 0, lens + 3);
+  offset_after_kernel<<<1, 1, 0, ss->s>>>(lens + 2, lens + 0, lens + 3);
   KVTC_LAUNCH_CHECK();
   // ---- values
   {
@@ -429,11 +459,13 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
   }
   {
     ProfScope ps("c.project_quant_gemm", st);
-    if ((s = run_project_quant(vb, vpl, vop, X, L.m, payload, st))) return s;
+    if ((s = run_project_quant(vb, vpl, vop, X, L.m, payload_v, st))) return s;
   }
+  KVTC_CUDA_TRY(cudaEventRecord(ss->ev[1], ss->s));
+  KVTC_CUDA_TRY(cudaStreamWaitEvent(st, ss->ev[1], 0));          // join: K section written, V offset known
   {
     ProfScope ps("c.deflate", st);
-    if ((s = launch_deflate(payload, L.pay[1], pol->chunk_bytes, o, lens + 3, lens + 1, dwsp, dws, st))) return s;
+    if ((s = launch_deflate(payload_v, L.pay[1], pol->chunk_bytes, o, lens + 3, lens + 1, dwsp, dws, st))) return s;
   }
   header_kernel<<<1, 1, 0, st>>>(h, o, lens, lens + 2);
   KVTC_LAUNCH_CHECK();
@@ -488,6 +520,7 @@ extern "C" size_t kvtc_decompress_workspace_bytes(const kvtc_basis *kb, const kv
   b.take<uint8_t>(h.payload_bytes[0] + 16);
   b.take<uint8_t>(h.payload_bytes[1] + 16);
   b.take<__half>(h.m * std::max(std::max(kp->r_nz_pad, vp->r_nz_pad), 8));
+  b.take<__half>(h.m * std::max(std::max(kp->r_nz_pad, vp->r_nz_pad), 8));
   b.take<float2>(h.m * (kb->shape.head_dim / 2));
   return b.used + 256;
 }
@@ -539,6 +572,7 @@ extern "C" kvtc_status kvtc_decompress(const kvtc_basis *kb, const kvtc_plan *kp
   payloads[1] = ws.take<uint8_t>(h.payload_bytes[1] + 16);
   const int64_t ld = std::max(std::max(kp->r_nz_pad, vp->r_nz_pad), 8);
   __half *Dh = ws.take<__half>(h.m * ld);
+  __half *Dh_v = ws.take<__half>(h.m * ld);
   float2 *cs = ws.take<float2>(h.m * (h.head_dim / 2));
   if ((s = upload_bases(k_out, kbases, st)) || (s = upload_bases(v_out, vbases, st))) return s;
   KVTC_CUDA_TRY(cudaMemsetAsync(err, 0, 4, st));
@@ -555,15 +589,30 @@ extern "C" kvtc_status kvtc_decompress(const kvtc_basis *kb, const kvtc_plan *kp
   // device copy of the section offsets lives in the container header itself
   const uint64_t *sec_off_dev = reinterpret_cast<const uint64_t *>(ib + offsetof(ContainerHeader, section_off));
   if (kb->has_rope && (s = rope_table_for(kb, h.pos0 + h.sinks, h.m, cs, st))) return s;
-  {
-    // both streams' chunks in one inflate launch (warp per chunk)
-    ProfScope ps("d.inflate", st);
-    const uint32_t nk = uint32_t((h.payload_bytes[0] + h.chunk_bytes - 1) / h.chunk_bytes);
-    const uint32_t nv = uint32_t((h.payload_bytes[1] + h.chunk_bytes - 1) / h.chunk_bytes);
-    if ((s = launch_inflate_sections(ib, sec_off_dev, h.payload_bytes[0], nk, payloads[0], sec_off_dev + 1,
-                                     h.payload_bytes[1], nv, payloads[1], err, st)))
-      return s;
+  // keys: inflate -> dequantise -> GEMM on the caller's stream; values: inflate ->
+  // dequantise on the side stream (overlapping the keys' GEMM), then their GEMM.
+  SideStream *ss = side_stream();
+  KVTC_CUDA_TRY(cudaEventRecord(ss->ev[2], st));                 // header/bases/err ready
+  KVTC_CUDA_TRY(cudaStreamWaitEvent(ss->s, ss->ev[2], 0));
+  __half *Dhs[2] = {Dh, Dh_v};
+  for (int sv = 0; sv < 2; ++sv) {
+    cudaStream_t cs_ = sv ? ss->s : st;
+    kvtc_plan *pl = const_cast<kvtc_plan *>(sv ? vp : kp);
+    const uint32_t nch = uint32_t((h.payload_bytes[sv] + h.chunk_bytes - 1) / h.chunk_bytes);
+    {
+      ProfScope ps(sv ? "d.inflate_overlapped" : "d.inflate", cs_);
+      if ((s = launch_inflate_section(ib, sec_off_dev + sv, h.payload_bytes[sv], nch, payloads[sv], err, cs_)))
+        return s;
+    }
+    {
+      ProfScope ps(sv ? "d.dequant_overlapped" : "d.dequant", cs_);
+      if ((s = launch_dequant(pl->d_pgroups, pl->d_codes_off_full, pl->G, plan_codes_off_last(pl, h.m % kTileM),
+                              pl->tile_bytes, payloads[sv], h.m, Dhs[sv], ld, cs_)))
+        return s;
+      if (pl->r_nz == 0) KVTC_CUDA_TRY(cudaMemsetAsync(Dhs[sv], 0, h.m * ld * 2, cs_));
+    }
   }
+  KVTC_CUDA_TRY(cudaEventRecord(ss->ev[3], ss->s));
   for (int sv = 0; sv < 2; ++sv) {
     const kvtc_basis *b = sv ? vb : kb;
     kvtc_plan *pl = const_cast<kvtc_plan *>(sv ? vp : kp);
@@ -571,17 +620,10 @@ extern "C" kvtc_status kvtc_decompress(const kvtc_basis *kb, const kvtc_plan *kp
     __nv_bfloat16 *const *bs = sv ? vbases : kbases;
     const Operands *op;
     if ((s = plan_operands(b, pl, &op))) return s;
-    const uint8_t *payload = payloads[sv];
-    {
-      ProfScope ps("d.dequant", st);
-      if ((s = launch_dequant(pl->d_pgroups, pl->d_codes_off_full, pl->G, plan_codes_off_last(pl, h.m % kTileM),
-                              pl->tile_bytes, payload, h.m, Dh, ld, st)))
-        return s;
-      if (pl->r_nz == 0) KVTC_CUDA_TRY(cudaMemsetAsync(Dh, 0, h.m * ld * 2, st));
-    }
+    if (sv == 1) KVTC_CUDA_TRY(cudaStreamWaitEvent(st, ss->ev[3], 0));   // join
     {
       ProfScope ps("d.reconstruct_gemm", st);
-      if ((s = run_reconstruct(b, pl, op, Dh, ld, h.m, h.sinks, layer_begin, layer_end, vw, bs, cs, st))) return s;
+      if ((s = run_reconstruct(b, pl, op, Dhs[sv], ld, h.m, h.sinks, layer_begin, layer_end, vw, bs, cs, st))) return s;
     }
     const __nv_bfloat16 *raw = sv ? rawv : rawk;
     {

@@ -27,11 +27,18 @@
 
 namespace kvtc {
 
-constexpr int kStages = 4;
-constexpr int kABytes = kTileM * kBlockK * 2;      // 16 KiB
-constexpr int kBBytes = kMaxTileN * kBlockK * 2;   // 32 KiB
-constexpr int kStageBytes = kABytes + kBBytes;     // 48 KiB
-constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 2048;
+// Single-CTA tiles: A 128 x 64 + B 256 x 64 per stage (48 KiB), 4 stages.
+// CTA pairs (cta_group::2, M = 256): each CTA holds its A half (128 rows) and
+// its B half (N/2 <= 128 rows): 32 KiB per stage, 6 stages.
+template <bool PAIR>
+struct Cfg {
+  static constexpr int kStages = PAIR ? 6 : 4;
+  static constexpr int kABytes = kTileM * kBlockK * 2;                        // 16 KiB
+  static constexpr int kBBytes = (PAIR ? kMaxTileN / 2 : kMaxTileN) * kBlockK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 2048;
+};
+constexpr int kBBoxRows = 128;                     // B tensor maps load 128 rows per box
 constexpr int kThreads = 256;
 constexpr int kTmemCols = 512;                     // two 256-column accumulators
 constexpr int kGroupM = 8;                         // raster group (M-blocks)
@@ -102,19 +109,21 @@ __device__ __forceinline__ void load_cols(uint32_t trow, const float *bias, int 
 
 // Static persistent schedule: tile t -> (mb, nb) in groups of kGroupM M-blocks.
 template <int MODE>
-__device__ __forceinline__ Tile tile_of(const Params &P, int64_t t) {
+__device__ __forceinline__ Tile tile_of(const Params &P, int64_t t, int num_mt) {
   Tile T;
   const int64_t per_group = int64_t(kGroupM) * P.num_n;
   const int64_t g = t / per_group;
   const int first = int(g * kGroupM);
-  const int gm = min(kGroupM, P.num_m - first);
+  const int gm = min(kGroupM, num_mt - first);
   const int64_t r = t - g * per_group;
   T.mb = first + int(r % gm);
   T.nb = int(r / gm);
   T.valid = true;
   if constexpr (MODE == EPI_XTX) {
     // strictly below the diagonal: symmetric, skipped
-    if (int64_t(T.nb) * P.tile_n + P.tile_n <= int64_t(T.mb) * kTileM) T.valid = false;
+    // pairs: T.mb is the pair index here (rows 256 mp ..); skipped only if the whole pair is below
+    const int64_t row0 = int64_t(T.mb) * kTileM * (P.parts == -2 ? 2 : 1);
+    if (int64_t(T.nb) * P.tile_n + P.tile_n <= row0) T.valid = false;
   }
   return T;
 }
@@ -137,10 +146,55 @@ __device__ __forceinline__ void tile_geometry(const Params &P, const Tile &T, in
   }
 }
 
-template <int MODE>
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// 2-D TMA load whose completion is signalled on the PAIR LEADER's mbarrier
+// (peer bit cleared), as required for cta_group::2 MMAs.
+__device__ __forceinline__ void tma_load_2d_pair(void *smem_dst, const CUtensorMap *m, uint64_t *bar, int32_t c0,
+                                                 int32_t c1) {
+  const uint32_t mbar = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(mbar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void umma_f16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// commit of the leader's MMAs, arriving on the same barrier offset in both CTAs
+__device__ __forceinline__ void umma_commit_pair(uint64_t *bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(uint16_t(3))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t *local_bar, uint32_t cta) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(local_bar)), "r"(cta));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+}
+
+template <int MODE, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ Params P) {
+  using C = Cfg<PAIR>;
+  constexpr int kStages = C::kStages;
+  constexpr int kABytes = C::kABytes;
+  constexpr int kStageBytes = C::kStageBytes;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *tiles = smem;
@@ -154,10 +208,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   const bool split = (MODE == EPI_QUANT) && P.parts > 1;
+  const uint32_t rank = PAIR ? cluster_rank() : 0;
+  const bool leader = rank == 0;
+  // pairs: tiles are M-pairs (256 rows); CTA rank r holds M-block 2 mp + r
+  const int num_mt = PAIR ? (P.num_m + 1) / 2 : P.num_m;
   // split launches: exactly one tile per CTA (grid = pieces x M-blocks, clusters along x)
-  const int64_t total = split ? 1 : int64_t(P.num_m) * P.num_n;
-  const int64_t t_first = split ? 0 : blockIdx.x;
-  const int64_t t_step = split ? 1 : int64_t(gridDim.x);
+  const int64_t total = split ? 1 : int64_t(num_mt) * P.num_n;
+  const int64_t t_first = split ? 0 : (PAIR ? blockIdx.x / 2 : blockIdx.x);
+  const int64_t t_step = split ? 1 : int64_t(PAIR ? gridDim.x / 2 : gridDim.x);
   const int num_kb = (P.K + kBlockK - 1) / kBlockK;
 
   if (threadIdx.x == 0) {
@@ -169,13 +227,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tmem_full[a], 1);
-      mbar_init(&tmem_empty[a], 128);
+      mbar_init(&tmem_empty[a], PAIR ? 256 : 128);      // pairs: both CTAs' epilogues release the leader's acc
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
+  if (warp == 2) {
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "n"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      tmem_alloc<kTmemCols>(tmem_slot);
+    }
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();        // peer barriers initialised before any remote arrive / TMA
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -187,7 +254,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       T.valid = true;
       return T;
     }
-    return tile_of<MODE>(P, t);
+    Tile T = tile_of<MODE>(P, t, num_mt);
+    if (PAIR) T.mb = 2 * T.mb + int(rank);      // this CTA's M-block
+    return T;
   };
 
   if (warp == 0 && lane == 0) {
@@ -198,18 +267,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (!T.valid) continue;
       int n0, ncols, g0, g1;
       tile_geometry<MODE>(P, T, n0, ncols, g0, g1);
+      const int n_mma = (ncols + 15) & ~15;
       for (int kb = 0; kb < num_kb; ++kb, ++it) {
         const int s = it % kStages;
         if (it >= kStages) mbar_wait(&empty_bar[s], ((it / kStages) - 1) & 1);
         uint8_t *a = tiles + s * kStageBytes;
         uint8_t *b = a + kABytes;
-        mbar_arrive_expect_tx(&full_bar[s], kStageBytes);
-        tma_load_2d(a, &tmA, &full_bar[s], kb * kBlockK, T.mb * kTileM);
-        tma_load_2d(b, &tmB, &full_bar[s], kb * kBlockK, n0);
+        if constexpr (PAIR) {
+          // both CTAs' bytes land on the leader's barrier
+          if (leader) mbar_arrive_expect_tx(&full_bar[s], 2 * kStageBytes);
+          tma_load_2d_pair(a, &tmA, &full_bar[s], kb * kBlockK, T.mb * kTileM);
+          tma_load_2d_pair(b, &tmB, &full_bar[s], kb * kBlockK, n0 + int(rank) * (n_mma / 2));
+        } else {
+          mbar_arrive_expect_tx(&full_bar[s], kStageBytes);
+          tma_load_2d(a, &tmA, &full_bar[s], kb * kBlockK, T.mb * kTileM);
+          tma_load_2d(b, &tmB, &full_bar[s], kb * kBlockK, n0);
+          tma_load_2d(b + kBBoxRows * 128, &tmB, &full_bar[s], kb * kBlockK, n0 + kBBoxRows);
+        }
       }
     }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer (one thread)
+  } else if (warp == 1 && lane == 0 && leader) {
+    // ---------------- MMA issuer (one thread; the pair leader issues for both CTAs)
     uint32_t it = 0, acc_it = 0;
     for (int64_t t = t_first; t < total; t += t_step) {
       const Tile T = get_tile(t);
@@ -217,7 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int n0, ncols, g0, g1;
       tile_geometry<MODE>(P, T, n0, ncols, g0, g1);
       const int n_mma = (ncols + 15) & ~15;
-      const uint32_t idesc = make_idesc_f16(P.fmt, kTileM, n_mma);
+      const uint32_t idesc = make_idesc_f16(P.fmt, PAIR ? 2 * kTileM : kTileM, n_mma);
       const uint32_t acc = acc_it & 1;
       if (acc_it >= 2) mbar_wait(&tmem_empty[acc], ((acc_it / 2) - 1) & 1);
       tc_fence_after();
@@ -228,15 +306,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint64_t ad = make_sdesc_sw128(tiles + s * kStageBytes);
         const uint64_t bd = make_sdesc_sw128(tiles + s * kStageBytes + kABytes);
+        if constexpr (PAIR) {
 #pragma unroll
-        for (int k = 0; k < kBlockK / 16; ++k) umma_f16(tacc, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
-        umma_commit(&empty_bar[s]);
+          for (int k = 0; k < kBlockK / 16; ++k)
+            umma_f16_pair(tacc, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+          umma_commit_pair(&empty_bar[s]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < kBlockK / 16; ++k) umma_f16(tacc, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+          umma_commit(&empty_bar[s]);
+        }
       }
-      umma_commit(&tmem_full[acc]);
+      if constexpr (PAIR) umma_commit_pair(&tmem_full[acc]);
+      else umma_commit(&tmem_full[acc]);
       ++acc_it;
     }
   } else if (warp >= 4) {
     // ---------------- epilogue
+    auto release_acc = [&](uint32_t a) {
+      if (!PAIR || leader) mbar_arrive(&tmem_empty[a]);
+      else mbar_arrive_remote(&tmem_empty[a], 0);
+    };
     const int row = (warp & 3) * 32 + lane;                 // TMEM lane == tile row
     uint32_t acc_it = 0;
     for (int64_t t = t_first; t < total; t += t_step) {
@@ -270,7 +360,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         tc_fence_before();
-        mbar_arrive(&tmem_empty[acc]);
+        release_acc(acc);
       } else if constexpr (MODE == EPI_QUANT) {
         // Straight from TMEM, group by group: pass 1 min/max, pass 2 encode + pack
         // (no shared-memory staging, so the next tile's MMAs overlap this epilogue).
@@ -345,7 +435,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         tc_fence_before();
-        mbar_arrive(&tmem_empty[acc]);
+        release_acc(acc);
       } else if constexpr (MODE == EPI_RECON) {
         // tcgen05.ld is warp-collective: every lane loads, only valid rows store
         const int d = P.head_dim;
@@ -421,7 +511,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         tc_fence_before();
-        mbar_arrive(&tmem_empty[acc]);
+        release_acc(acc);
       }
       ++acc_it;
     }
@@ -433,8 +523,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     cluster_sync_all();
   }
   tc_fence_before();
-  __syncthreads();
-  if (warp == 2) tmem_dealloc<kTmemCols>(tmem_base);
+  if constexpr (PAIR) {
+    __syncwarp();
+    cluster_sync_all();                          // both CTAs done with the pair's TMEM and smem
+    if (warp == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(kTmemCols));
+  } else {
+    __syncthreads();
+    if (warp == 2) tmem_dealloc<kTmemCols>(tmem_base);
+  }
 }
 
 static int num_sms() {
@@ -447,14 +544,16 @@ static int num_sms() {
   return n;
 }
 
-template <int MODE>
+template <int MODE, bool PAIR>
 static kvtc_status launch(const CUtensorMap *tmA, const CUtensorMap *tmB, const Params &p, dim3 grid, int cluster,
                           cudaStream_t st) {
   static bool configured = false;
+  constexpr int kSmemBytes = Cfg<PAIR>::kSmemBytes;
   if (!configured) {
-    KVTC_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    KVTC_CUDA_TRY(
+        cudaFuncSetAttribute(gemm_kernel<MODE, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
     if (MODE == EPI_QUANT)
-      KVTC_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<MODE>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      KVTC_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<MODE, PAIR>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     configured = true;
   }
   if (grid.x == 0 || grid.y == 0) return KVTC_OK;
@@ -470,12 +569,15 @@ static kvtc_status launch(const CUtensorMap *tmA, const CUtensorMap *tmB, const 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  KVTC_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_kernel<MODE>, *tmA, *tmB, p));
+  KVTC_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_kernel<MODE, PAIR>, *tmA, *tmB, p));
   note_launch();
   return KVTC_OK;
 }
 
-static unsigned persistent_grid(int64_t tiles) { return unsigned(std::min<int64_t>(tiles, num_sms())); }
+// pairs: 2 CTAs per pair-tile, grid even, at most one CTA per SM
+static unsigned pair_grid(int64_t pair_tiles) {
+  return unsigned(2 * std::min<int64_t>(pair_tiles, num_sms() / 2));
+}
 
 kvtc_status launch_gemm_project_f32(const GemmCompressArgs &a, int32_t ncols, cudaStream_t st) {
   Params p = {};
@@ -489,7 +591,7 @@ kvtc_status launch_gemm_project_f32(const GemmCompressArgs &a, int32_t ncols, cu
   p.tile_n = kMaxTileN;
   p.num_m = int32_t(ceil_div(a.m, kTileM));
   p.num_n = int32_t(ceil_div(ncols, kMaxTileN));
-  return launch<EPI_F32>(a.tmA, a.tmB, p, dim3(persistent_grid(int64_t(p.num_m) * p.num_n)), 1, st);
+  return launch<EPI_F32, true>(a.tmA, a.tmB, p, dim3(pair_grid(int64_t((p.num_m + 1) / 2) * p.num_n)), 2, st);
 }
 
 kvtc_status launch_gemm_project_quant(const GemmCompressArgs &a, cudaStream_t st) {
@@ -508,8 +610,8 @@ kvtc_status launch_gemm_project_quant(const GemmCompressArgs &a, cudaStream_t st
   p.num_m = int32_t(ceil_div(a.m, kTileM));
   p.num_n = a.nsegs;
   if (a.parts > 1)   // split groups: one tile per CTA, clusters along x
-    return launch<EPI_QUANT>(a.tmA, a.tmB, p, dim3(unsigned(a.nsegs), unsigned(p.num_m)), a.parts, st);
-  return launch<EPI_QUANT>(a.tmA, a.tmB, p, dim3(persistent_grid(int64_t(p.num_m) * p.num_n)), 1, st);
+    return launch<EPI_QUANT, false>(a.tmA, a.tmB, p, dim3(unsigned(a.nsegs), unsigned(p.num_m)), a.parts, st);
+  return launch<EPI_QUANT, true>(a.tmA, a.tmB, p, dim3(pair_grid(int64_t((p.num_m + 1) / 2) * p.num_n)), 2, st);
 }
 
 kvtc_status launch_gemm_reconstruct(const GemmDecompressArgs &a, cudaStream_t st) {
@@ -533,7 +635,7 @@ kvtc_status launch_gemm_reconstruct(const GemmDecompressArgs &a, cudaStream_t st
   p.tile_n = a.tile_n;
   p.num_m = int32_t(ceil_div(a.m, kTileM));
   p.num_n = int32_t(ceil_div(a.n_end - a.n_begin, a.tile_n));
-  return launch<EPI_RECON>(a.tmA, a.tmB, p, dim3(persistent_grid(int64_t(p.num_m) * p.num_n)), 1, st);
+  return launch<EPI_RECON, true>(a.tmA, a.tmB, p, dim3(pair_grid(int64_t((p.num_m + 1) / 2) * p.num_n)), 2, st);
 }
 
 kvtc_status launch_gemm_xtx(const CUtensorMap *tmA, const CUtensorMap *tmB, int32_t p_, int32_t nk, float *S,
@@ -548,7 +650,8 @@ kvtc_status launch_gemm_xtx(const CUtensorMap *tmA, const CUtensorMap *tmB, int3
   p.tile_n = kMaxTileN;
   p.num_m = int32_t(ceil_div(p_, kTileM));
   p.num_n = int32_t(ceil_div(p_, kMaxTileN));
-  return launch<EPI_XTX>(tmA, tmB, p, dim3(persistent_grid(int64_t(p.num_m) * p.num_n)), 1, st);
+  p.parts = -2;                                   // marks pair tiling for the symmetric skip
+  return launch<EPI_XTX, true>(tmA, tmB, p, dim3(pair_grid(int64_t((p.num_m + 1) / 2) * p.num_n)), 2, st);
 }
 
 }  // namespace kvtc

@@ -53,7 +53,7 @@ kvtc_status make_tmap_2d(CUtensorMap *m, const void *base, CUtensorMapDataType d
 // ------------------------------------------------------------------ launchers
 struct GemmCompressArgs {
   const CUtensorMap *tmA;  // X [m x p] bf16, box {64, 128}
-  const CUtensorMap *tmB;  // VcT [r_nz x p] bf16, box {64, 256}
+  const CUtensorMap *tmB;  // VcT [r_nz x p] bf16, box {64, 128}
   int32_t K;               // p
   int64_t m;
   const float *bias;       // [r_nz]
@@ -75,7 +75,7 @@ kvtc_status launch_gemm_project_quant(const GemmCompressArgs &a, cudaStream_t st
 
 struct GemmDecompressArgs {
   const CUtensorMap *tmA;  // D^ [m x r_nz_pad] fp16, box {64, 128}
-  const CUtensorMap *tmB;  // Vd [p x r_nz_pad] fp16, box {64, 256}
+  const CUtensorMap *tmB;  // Vd [p x r_nz_pad] fp16, box {64, 128}
   int32_t K;               // r_nz_pad
   int64_t m;
   int32_t n_begin, n_end;  // feature range (multiple of 256)
@@ -92,7 +92,7 @@ struct GemmDecompressArgs {
 kvtc_status launch_gemm_reconstruct(const GemmDecompressArgs &a, cudaStream_t st);
 
 // XtX accumulation: S[p x p] += C^T C for a chunk Ct [p x nk] (K-major);
-// tmA box {64, 128}, tmB box {64, 256} over the same Ct.
+// tmA and tmB: box {64, 128} over the same Ct.
 kvtc_status launch_gemm_xtx(const CUtensorMap *tmA, const CUtensorMap *tmB, int32_t p, int32_t nk, float *S,
                             cudaStream_t st);
 
