@@ -24,8 +24,8 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t
                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-kvtc_status make_tmap_2d(CUtensorMap *m, const void *base, CUtensorMapDataType dt, uint64_t inner, uint64_t outer,
-                         uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer) {
+namespace {
+kvtc_status encode_fn(EncodeTiledFn *out) {
   static EncodeTiledFn fn = nullptr;
   if (!fn) {
     cudaDriverEntryPointQueryResult q;
@@ -37,6 +37,34 @@ kvtc_status make_tmap_2d(CUtensorMap *m, const void *base, CUtensorMapDataType d
     }
     fn = reinterpret_cast<EncodeTiledFn>(p);
   }
+  *out = fn;
+  return KVTC_OK;
+}
+}  // namespace
+
+kvtc_status make_tmap_3d(CUtensorMap *m, const void *base, CUtensorMapDataType dt, uint64_t d0, uint64_t d1,
+                         uint64_t d2, uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box0, uint32_t box1) {
+  EncodeTiledFn fn;
+  kvtc_status s = encode_fn(&fn);
+  if (s) return s;
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {stride1_bytes, stride2_bytes};
+  cuuint32_t box[3] = {box0, box1, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, dt, 3, const_cast<void *>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (3d) failed (%d)", int(r));
+    return KVTC_E_CUDA;
+  }
+  return KVTC_OK;
+}
+
+kvtc_status make_tmap_2d(CUtensorMap *m, const void *base, CUtensorMapDataType dt, uint64_t inner, uint64_t outer,
+                         uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer) {
+  EncodeTiledFn fn;
+  kvtc_status s = encode_fn(&fn);
+  if (s) return s;
   if (outer == 0 || inner == 0) {
     set_error("empty tensor map");
     return KVTC_E_INVALID;

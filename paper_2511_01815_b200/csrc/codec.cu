@@ -1,5 +1,6 @@
 // codec.cu — stage entry points and the compress / decompress orchestration
 // with the container format of DESIGN.md §4.
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -34,8 +35,12 @@ __global__ void header_kernel(ContainerHeader h, uint8_t *out, const uint64_t *l
   }
   *reinterpret_cast<ContainerHeader *>(out) = h;
 }
-__global__ void offset_after_kernel(const uint64_t *off, const uint64_t *len, uint64_t *next) {
-  *next = *off + ((*len + 15) & ~15ull);
+// next = 16-aligned end of the K section; the alignment gap is zeroed so the
+// container bytes are a function of the input alone.
+__global__ void offset_after_kernel(const uint64_t *off, const uint64_t *len, uint64_t *next, uint8_t *out) {
+  const uint64_t end = *off + *len, aligned = *off + ((*len + 15) & ~15ull);
+  for (uint64_t i = end; i < aligned; ++i) out[i] = 0;
+  *next = aligned;
 }
 
 inline uint64_t align16(uint64_t x) { return (x + 15) & ~15ull; }
@@ -50,14 +55,41 @@ kvtc_status tmap_X(CUtensorMap *m, const void *X, int64_t rows, int64_t p) {
                       kTileM);
 }
 
+// A contiguous cache whose layers sit at a constant positive stride can be read
+// by the GEMM in place through a 3-D tensor map (no gathered copy of X): rows
+// are tokens, the K axis walks layer by layer.  Returns false if not eligible.
+bool direct_view_map(const kvtc_kv_view &v, int64_t tok0, CUtensorMap *m) {
+  const int64_t hd = int64_t(v.shape.kv_heads) * v.shape.head_dim;
+  if (v.layout != KVTC_LAYOUT_CONTIGUOUS || hd % kBlockK || v.tokens > INT32_MAX / 2 || tok0 < 0) return false;
+  const auto base = reinterpret_cast<uintptr_t>(v.layer_base_host[0]);
+  if (base % 16) return false;
+  uint64_t stride = uint64_t(v.tokens) * hd * 2;
+  if (v.shape.layers > 1) {
+    const auto b1 = reinterpret_cast<uintptr_t>(v.layer_base_host[1]);
+    if (b1 <= base || (b1 - base) % 16) return false;
+    stride = b1 - base;
+    for (int l = 2; l < v.shape.layers; ++l)
+      if (reinterpret_cast<uintptr_t>(v.layer_base_host[l]) != base + l * stride) return false;
+  }
+  return make_tmap_3d(m, v.layer_base_host[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, uint64_t(hd), uint64_t(v.tokens),
+                      uint64_t(v.shape.layers), uint64_t(hd) * 2, stride, kBlockK, kTileM) == KVTC_OK;
+}
+
+// X: the gathered rows [m x p], or nullptr with `direct` = the 3-D map of the
+// cache itself (rows = tokens tok0 ..).
 kvtc_status run_project_quant(const kvtc_basis *b, kvtc_plan *pl, const Operands *op, const void *X, int64_t m,
-                              uint8_t *payload, cudaStream_t st) {
+                              uint8_t *payload, cudaStream_t st, const CUtensorMap *direct = nullptr,
+                              int64_t tok0 = 0) {
   if (m == 0 || pl->G == 0) return KVTC_OK;
   CUtensorMap tA;
-  kvtc_status s = tmap_X(&tA, X, m, b->p);
-  if (s) return s;
+  kvtc_status s = KVTC_OK;
+  if (!direct && (s = tmap_X(&tA, X, m, b->p))) return s;
   GemmCompressArgs a = {};
-  a.tmA = &tA;
+  a.tmA = direct ? direct : &tA;
+  if (direct) {
+    a.a_hd = b->shape.kv_heads * b->shape.head_dim;
+    a.a_row0 = tok0;
+  }
   a.tmB = &op->tm_VcT;
   a.K = b->p;
   a.m = m;
@@ -132,6 +164,12 @@ SideStream *side_stream() {
     for (auto &e : S.ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
   }
   return &S;
+}
+
+// KVTC_NO_DIRECT=1 forces the gathered path (tests compare the two).
+bool direct_off() {
+  const char *e = getenv("KVTC_NO_DIRECT");
+  return e && e[0] == '1';
 }
 
 bool same_shape(const kvtc_shape &a, const kvtc_shape &b) {
@@ -450,16 +488,18 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
     ProfScope ps("c.deflate_overlapped", ss->s);
     if ((s = launch_deflate(payload_k, L.pay[0], pol->chunk_bytes, o, lens + 2, lens + 0, dwsp, dws, ss->s))) return s;
   }
-  offset_after_kernel<<<1, 1, 0, ss->s>>>(lens + 2, lens + 0, lens + 3);
+  offset_after_kernel<<<1, 1, 0, ss->s>>>(lens + 2, lens + 0, lens + 3, o);
   KVTC_LAUNCH_CHECK();
-  // ---- values
-  {
+  // ---- values: read in place when the cache layout allows it
+  CUtensorMap tV;
+  const bool v_direct = !direct_off() && direct_view_map(*v, pol->sinks, &tV);
+  if (!v_direct) {
     ProfScope ps("c.gather", st);
     if ((s = launch_gather(*v, vbases, pol->sinks, L.m, nullptr, 0, X, st))) return s;
   }
   {
     ProfScope ps("c.project_quant_gemm", st);
-    if ((s = run_project_quant(vb, vpl, vop, X, L.m, payload_v, st))) return s;
+    if ((s = run_project_quant(vb, vpl, vop, X, L.m, payload_v, st, v_direct ? &tV : nullptr, pol->sinks))) return s;
   }
   KVTC_CUDA_TRY(cudaEventRecord(ss->ev[1], ss->s));
   KVTC_CUDA_TRY(cudaStreamWaitEvent(st, ss->ev[1], 0));          // join: K section written, V offset known
@@ -591,9 +631,9 @@ extern "C" kvtc_status kvtc_decompress(const kvtc_basis *kb, const kvtc_plan *kp
   if (kb->has_rope && (s = rope_table_for(kb, h.pos0 + h.sinks, h.m, cs, st))) return s;
   // keys: inflate -> dequantise -> GEMM on the caller's stream; values: inflate ->
   // dequantise on the side stream (overlapping the keys' GEMM), then their GEMM.
+  // The values' inflate waits for the keys' inflate (which then has the whole GPU:
+  // it is latency-bound and two concurrent inflates each run at half speed).
   SideStream *ss = side_stream();
-  KVTC_CUDA_TRY(cudaEventRecord(ss->ev[2], st));                 // header/bases/err ready
-  KVTC_CUDA_TRY(cudaStreamWaitEvent(ss->s, ss->ev[2], 0));
   __half *Dhs[2] = {Dh, Dh_v};
   for (int sv = 0; sv < 2; ++sv) {
     cudaStream_t cs_ = sv ? ss->s : st;
@@ -603,6 +643,10 @@ extern "C" kvtc_status kvtc_decompress(const kvtc_basis *kb, const kvtc_plan *kp
       ProfScope ps(sv ? "d.inflate_overlapped" : "d.inflate", cs_);
       if ((s = launch_inflate_section(ib, sec_off_dev + sv, h.payload_bytes[sv], nch, payloads[sv], err, cs_)))
         return s;
+    }
+    if (sv == 0) {
+      KVTC_CUDA_TRY(cudaEventRecord(ss->ev[2], st));             // header/bases/err ready, keys inflated
+      KVTC_CUDA_TRY(cudaStreamWaitEvent(ss->s, ss->ev[2], 0));
     }
     {
       ProfScope ps(sv ? "d.dequant_overlapped" : "d.dequant", cs_);

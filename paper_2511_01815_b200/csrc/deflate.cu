@@ -19,8 +19,9 @@
 // (stored / fixed / dynamic blocks, LZ77 back-references) for foreign streams.
 //
 // Section layout: 64-byte header, chunk table [nchunks] x
-// {u64 offset, u32 bytes, u32 kind}, segment index [nchunks][32] u32, then the
-// chunk streams, each starting 4-byte aligned.
+// {u64 offset, u32 bytes, u32 kind}, segment index [nchunks][64] u16 (bit
+// length of each 1/64 of the chunk's symbols; segment 0 starts right after the
+// block header), then the chunk streams, each starting 4-byte aligned.
 #include <cub/block/block_scan.cuh>
 
 #include "internal.h"
@@ -29,7 +30,8 @@ namespace kvtc {
 
 constexpr uint32_t kSectionMagic = 0x4454564Bu;  // "KVTD"
 constexpr int kEncThreads = 256;
-constexpr int kNSeg = 32;
+constexpr int kNSeg = 64;
+constexpr uint32_t kSectionVersion = 2;
 constexpr int kLitSyms = 257;                    // 0..255 literals + 256 end-of-block
 constexpr int kMaxBits = 15;
 
@@ -60,12 +62,12 @@ __host__ __device__ inline uint64_t slot_stride(int32_t chunk) { return ((stored
 
 size_t deflate_section_bound(size_t n, int32_t chunk) {
   const size_t nch = (n + chunk - 1) / chunk;
-  return sizeof(SectionHeader) + nch * sizeof(ChunkEntry) + nch * kNSeg * 4 + nch * ((stored_bytes(chunk) + 3) & ~3u) +
-         16;
+  return sizeof(SectionHeader) + nch * sizeof(ChunkEntry) + ((nch * kNSeg * 2 + 3) & ~size_t(3)) +
+         nch * ((stored_bytes(chunk) + 3) & ~3u) + 16;
 }
 size_t deflate_workspace(size_t n, int32_t chunk) {
   const size_t nch = (n + chunk - 1) / chunk;
-  return nch * slot_stride(chunk) + nch * 8 + nch * kNSeg * 4 + 256;
+  return nch * slot_stride(chunk) + nch * 8 + nch * kNSeg * 2 + 256;
 }
 
 // ---------------------------------------------------------- Huffman lengths
@@ -225,6 +227,7 @@ struct EncShared {
   uint32_t hdr[160];   // header bits (<= 5120)
   uint32_t hdr_bits;
   uint32_t total_bits;
+  uint32_t segst[kNSeg];
   int use_stored;
   typename cub::BlockScan<uint32_t, kEncThreads>::TempStorage scan;
 };
@@ -286,7 +289,7 @@ struct WordWriter {
 __global__ void __launch_bounds__(kEncThreads, 2) deflate_encode_kernel(const uint8_t *in, uint64_t n, int32_t chunk,
                                                                         uint8_t *slots, uint64_t stride,
                                                                         uint32_t *chunk_bytes, uint32_t *chunk_kind,
-                                                                        uint32_t *index) {
+                                                                        uint16_t *index) {
   __shared__ EncShared S;
   const int c = blockIdx.x;
   const uint64_t base = uint64_t(c) * chunk;
@@ -436,9 +439,11 @@ __global__ void __launch_bounds__(kEncThreads, 2) deflate_encode_kernel(const ui
     }
     return;
   }
-  // ---- segment index (bit offset of each 1/32 of the chunk)
+  // ---- segment index: bit length of each 1/64 of the chunk (<= 15 * 1024 bits)
   const uint32_t pieces_per_seg = kEncThreads / kNSeg;
-  if (t % pieces_per_seg == 0) index[uint64_t(c) * kNSeg + t / pieces_per_seg] = myoff + (t == 0 ? S.hdr_bits : 0);
+  if (t % pieces_per_seg == 0) S.segst[t / pieces_per_seg] = myoff + (t == 0 ? S.hdr_bits : 0);
+  __syncthreads();
+  if (t < kNSeg) index[uint64_t(c) * kNSeg + t] = uint16_t((t + 1 < kNSeg ? S.segst[t + 1] : S.total_bits) - S.segst[t]);
   // ---- emission: words wholly inside this thread's bit range are stored,
   // the two edge words (shared with the neighbours) are OR-ed atomically
   uint32_t *ow = reinterpret_cast<uint32_t *>(out);
@@ -504,7 +509,8 @@ __global__ void __launch_bounds__(1024) section_layout_kernel(const uint32_t *ch
   __shared__ uint64_t carry;
   SectionHeader *h = reinterpret_cast<SectionHeader *>(out);
   ChunkEntry *tab = reinterpret_cast<ChunkEntry *>(out + sizeof(SectionHeader));
-  const uint64_t data_off = sizeof(SectionHeader) + uint64_t(nch) * sizeof(ChunkEntry) + uint64_t(nch) * kNSeg * 4;
+  const uint64_t data_off =
+      sizeof(SectionHeader) + uint64_t(nch) * sizeof(ChunkEntry) + ((uint64_t(nch) * kNSeg * 2 + 3) & ~3ull);
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
   for (uint32_t b = 0; b < nch; b += 1024) {
@@ -524,7 +530,7 @@ __global__ void __launch_bounds__(1024) section_layout_kernel(const uint32_t *ch
   if (threadIdx.x == 0) {
     SectionHeader hh = {};
     hh.magic = kSectionMagic;
-    hh.version = 1;
+    hh.version = kSectionVersion;
     hh.raw_bytes = n;
     hh.chunk_bytes = uint32_t(chunk);
     hh.nchunks = nch;
@@ -537,18 +543,22 @@ __global__ void __launch_bounds__(1024) section_layout_kernel(const uint32_t *ch
   }
 }
 
-__global__ void section_copy_kernel(const uint8_t *slots, uint64_t stride, const uint32_t *index, uint32_t nch,
+__global__ void section_copy_kernel(const uint8_t *slots, uint64_t stride, const uint16_t *index, uint32_t nch,
                                     uint8_t *out_base, const uint64_t *off_dev) {
   uint8_t *out = out_base + (off_dev ? *off_dev : 0);
   const uint32_t c = blockIdx.x;
   const SectionHeader *h = reinterpret_cast<const SectionHeader *>(out);
   const ChunkEntry e = reinterpret_cast<const ChunkEntry *>(out + sizeof(SectionHeader))[c];
-  uint32_t *idx = reinterpret_cast<uint32_t *>(out + sizeof(SectionHeader) + uint64_t(nch) * sizeof(ChunkEntry));
+  uint16_t *idx = reinterpret_cast<uint16_t *>(out + sizeof(SectionHeader) + uint64_t(nch) * sizeof(ChunkEntry));
   if (threadIdx.x < kNSeg) idx[uint64_t(c) * kNSeg + threadIdx.x] = e.kind == 0 ? index[uint64_t(c) * kNSeg + threadIdx.x] : 0;
   const uint32_t *s = reinterpret_cast<const uint32_t *>(slots + uint64_t(c) * stride);
   uint32_t *d = reinterpret_cast<uint32_t *>(out + h->data_offset + e.offset);
   const uint32_t words = (e.bytes + 3) / 4;
-  for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) d[i] = s[i];
+  for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) {
+    uint32_t v = s[i];
+    if (i == words - 1 && (e.bytes & 3)) v &= (1u << (8 * (e.bytes & 3))) - 1;   // deterministic padding
+    d[i] = v;
+  }
 }
 
 kvtc_status launch_deflate(const uint8_t *in, size_t n, int32_t chunk, uint8_t *out, const uint64_t *off_dev,
@@ -560,7 +570,7 @@ kvtc_status launch_deflate(const uint8_t *in, size_t n, int32_t chunk, uint8_t *
   uint8_t *slots = static_cast<uint8_t *>(ws);
   uint32_t *cbytes = reinterpret_cast<uint32_t *>(slots + nch * stride);
   uint32_t *ckind = cbytes + nch;
-  uint32_t *index = ckind + nch;
+  uint16_t *index = reinterpret_cast<uint16_t *>(ckind + nch);
   if (nch > 0) {
     deflate_encode_kernel<<<nch, kEncThreads, 0, st>>>(in, n, chunk, slots, stride, cbytes, ckind, index);
     KVTC_LAUNCH_CHECK();
@@ -664,7 +674,7 @@ __device__ int parse_dynamic(BitReader &br, uint8_t *lens, int &nlen, int &ndist
   return 0;
 }
 
-// ---- fast path: our indexed Huffman-literal chunks, warp per chunk
+// ---- fast path: our indexed Huffman-literal chunks, 64 threads per chunk
 // Bit reader over shared-memory words (header parsing).
 struct SmemBits {
   const uint32_t *w;
@@ -691,13 +701,19 @@ __device__ int huff_decode_s(SmemBits &br, const Huff &h) {
 }
 
 constexpr int kHdrWords = 512;     // first 2 KiB of a chunk stream hold its block header
+constexpr int kTabBits = 11;       // first-level decode table: codes <= 11 bits in one lookup
+constexpr int kInfThreads = kNSeg; // one thread per segment, 2 warps per chunk
+static_assert(kNSeg == 64, "the segment-start scan below assumes two warps");
 
 struct FastShared {
   uint32_t hdr[kHdrWords + 2];
-  uint16_t table[1024];            // (sym << 4) | len for codes <= 10 bits; 0 = slow path
+  uint16_t table[1 << kTabBits];   // (sym << 4) | len for codes <= kTabBits; 0 = slow path
   uint16_t code[260];
   Huff h;
   uint8_t lens[320];
+  uint8_t cltab[128];              // code-length code: (sym << 3) | len, 7-bit lookup
+  uint32_t segstart[kNSeg];
+  uint32_t hdr_bits;
   int status;
 };
 
@@ -709,112 +725,167 @@ struct InflateJobs {
   uint8_t *out[2];
 };
 
-__global__ void __launch_bounds__(32) inflate_fast_kernel(InflateJobs J, int32_t *err) {
+__constant__ uint8_t c_cl_order[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
+
+// Canonical codes (RFC 1951 §3.2.2) bit-reversed for LSB-first lookup.
+__device__ void reversed_codes(const uint8_t *len, int n, uint16_t *rev) {
+  int cnt[16] = {0}, next[16];
+  for (int s = 0; s < n; ++s) cnt[len[s]]++;
+  cnt[0] = 0;
+  int code = 0;
+  for (int b = 1; b < 16; ++b) {
+    code = (code + cnt[b - 1]) << 1;
+    next[b] = code;
+  }
+  for (int s = 0; s < n; ++s)
+    rev[s] = len[s] ? uint16_t(__brev(uint32_t(next[len[s]]++)) >> (32 - len[s])) : 0;
+}
+
+// Block header of one of our chunk streams (literals + EOB, one final dynamic
+// block), parsed by one thread from the shared-memory copy of its first words.
+__device__ int parse_header_fast(FastShared &S) {
+  SmemBits br{S.hdr, 0};
+  const uint32_t bfinal = br.get(1), btype = br.get(2);
+  if (bfinal != 1 || btype != 2) return -1;
+  const int nlen = int(br.get(5)) + 257;
+  const int ndist = int(br.get(5)) + 1;
+  const int ncode = int(br.get(4)) + 4;
+  if (nlen != 257 || ndist > 30) return -7;            // our encoder: literals + EOB only
+  uint8_t cl[19];
+  for (int i = 0; i < 19; ++i) cl[i] = 0;
+  for (int i = 0; i < ncode; ++i) cl[c_cl_order[i]] = uint8_t(br.get(3));
+  {
+    Huff hc;
+    if (huff_build(hc, cl, 19) != 0) return -4;        // complete code-length code required
+    uint16_t rv[19];
+    reversed_codes(cl, 19, rv);
+    for (int sym = 0; sym < 19; ++sym)
+      if (cl[sym])
+        for (uint32_t f = rv[sym]; f < 128; f += 1u << cl[sym]) S.cltab[f] = uint8_t((sym << 3) | cl[sym]);
+  }
+  int idx = 0;
+  const int total = nlen + ndist;
+  while (idx < total) {
+    const uint32_t w = S.hdr[br.pos >> 5], w2 = S.hdr[(br.pos >> 5) + 1];
+    const uint32_t peek = uint32_t(((uint64_t(w) | (uint64_t(w2) << 32)) >> (br.pos & 31)) & 127u);
+    const uint8_t e = S.cltab[peek];
+    br.pos += e & 7;
+    const int sym = e >> 3;
+    if (sym < 16) {
+      S.lens[idx++] = uint8_t(sym);
+      continue;
+    }
+    int rep;
+    uint8_t v = 0;
+    if (sym == 16) {
+      if (idx == 0) return -5;
+      v = S.lens[idx - 1];
+      rep = 3 + int(br.get(2));
+    } else if (sym == 17) {
+      rep = 3 + int(br.get(3));
+    } else {
+      rep = 11 + int(br.get(7));
+    }
+    if (idx + rep > total) return -6;
+    while (rep--) S.lens[idx++] = v;
+    if (br.pos > 32u * kHdrWords) return -7;
+  }
+  if (br.pos > 32u * kHdrWords) return -7;
+  if (S.lens[256] == 0) return -9;
+  if (huff_build(S.h, S.lens, 257) < 0) return -4;
+  reversed_codes(S.lens, 257, S.code);
+  S.hdr_bits = br.pos;
+  return 0;
+}
+
+// Slow path for codes longer than kTabBits: canonical bit-serial decode.
+__device__ __forceinline__ int decode_long(const Huff &h, uint64_t &buf, int &cnt) {
+  int code = 0, first = 0, idx = 0;
+  for (int l = 1; l < 16; ++l) {
+    code |= int(buf & 1);
+    buf >>= 1;
+    cnt--;
+    const int count = h.count[l];
+    if (code - count < first) return h.symbol[idx + (code - first)];
+    idx += count;
+    first += count;
+    first <<= 1;
+    code <<= 1;
+  }
+  return -1;
+}
+
+__global__ void __launch_bounds__(kInfThreads) inflate_fast_kernel(InflateJobs J, int32_t *err) {
   __shared__ FastShared S;
   const int job = blockIdx.x < J.nch[0] ? 0 : 1;
   const uint32_t c = job == 0 ? blockIdx.x : blockIdx.x - J.nch[0];
   const uint8_t *section = J.base + (J.off_dev[job] ? *J.off_dev[job] : 0);
   const SectionHeader *hdr = reinterpret_cast<const SectionHeader *>(section);
-  const int lane = threadIdx.x;
-  if (hdr->magic != kSectionMagic || hdr->raw_bytes != J.n_out[job] || hdr->nchunks != J.nch[job] ||
-      hdr->nseg != kNSeg) {
-    if (lane == 0) atomicExch(err, -20);
+  const int tid = threadIdx.x;
+  if (hdr->magic != kSectionMagic || hdr->version != kSectionVersion || hdr->raw_bytes != J.n_out[job] ||
+      hdr->nchunks != J.nch[job] || hdr->nseg != kNSeg || hdr->seg_bytes * kNSeg != hdr->chunk_bytes ||
+      hdr->seg_bytes % 16) {
+    if (tid == 0) atomicExch(err, -20);
     return;
   }
   const ChunkEntry e = reinterpret_cast<const ChunkEntry *>(section + sizeof(SectionHeader))[c];
-  const uint32_t *index =
-      reinterpret_cast<const uint32_t *>(section + sizeof(SectionHeader) + uint64_t(hdr->nchunks) * sizeof(ChunkEntry));
+  const uint16_t *index =
+      reinterpret_cast<const uint16_t *>(section + sizeof(SectionHeader) + uint64_t(hdr->nchunks) * sizeof(ChunkEntry));
   const uint8_t *stream = section + hdr->data_offset + e.offset;
   const uint64_t obase = uint64_t(c) * hdr->chunk_bytes;
   const uint32_t nc = uint32_t(umin64(hdr->chunk_bytes, hdr->raw_bytes - obase));
   uint8_t *o = J.out[job] + obase;
   if (e.kind == 1) {
-    for (uint32_t i = lane; i < nc; i += 32) o[i] = stream[(i / 32768) * (32768 + 5) + 5 + (i % 32768)];
+    for (uint32_t i = tid; i < nc; i += kInfThreads) o[i] = stream[(i / 32768) * (32768 + 5) + 5 + (i % 32768)];
     return;
   }
-  // header bytes -> shared memory (coalesced), parsed by lane 0 from there
+  // header words -> shared memory (coalesced), parsed by thread 0 from there
   const uint32_t *words = reinterpret_cast<const uint32_t *>(stream);
   const uint32_t nw = umin32((e.bytes + 3) / 4, kHdrWords);
-  for (uint32_t i = lane; i < kHdrWords + 2; i += 32) S.hdr[i] = i < nw ? __ldg(words + i) : 0u;
-  __syncwarp();
-  if (lane == 0) {
-    SmemBits br{S.hdr, 0};
-    int st = 0;
-    const uint32_t bfinal = br.get(1), btype = br.get(2);
-    if (bfinal != 1 || btype != 2) st = -1;
-    int nlen = 0, ndist = 0;
-    if (!st) {
-      nlen = int(br.get(5)) + 257;
-      ndist = int(br.get(5)) + 1;
-      const int ncode = int(br.get(4)) + 4;
-      const int order[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
-      uint8_t cl[19];
-      for (int i = 0; i < 19; ++i) cl[i] = 0;
-      for (int i = 0; i < ncode; ++i) cl[order[i]] = uint8_t(br.get(3));
-      Huff hc;
-      if (nlen > 286 || ndist > 30 || huff_build(hc, cl, 19) != 0) st = -4;
-      int idx = 0;
-      while (!st && idx < nlen + ndist) {
-        const int sym = huff_decode_s(br, hc);
-        if (sym < 0) { st = sym; break; }
-        if (sym < 16) { S.lens[idx++] = uint8_t(sym); continue; }
-        int rep;
-        uint8_t v = 0;
-        if (sym == 16) {
-          if (idx == 0) { st = -5; break; }
-          v = S.lens[idx - 1];
-          rep = 3 + int(br.get(2));
-        } else if (sym == 17) {
-          rep = 3 + int(br.get(3));
-        } else {
-          rep = 11 + int(br.get(7));
-        }
-        if (idx + rep > nlen + ndist) { st = -6; break; }
-        while (rep--) S.lens[idx++] = v;
-      }
-      if (!st && (br.pos > 32u * kHdrWords || nlen != 257)) st = -7;   // our encoder: literals + EOB only
-    }
-    if (!st && huff_build(S.h, S.lens, 257) < 0) st = -4;
-    if (!st) {
-      // canonical codes (RFC 1951 §3.2.2)
-      int next[16], cnt[16] = {0};
-      for (int s = 0; s < 257; ++s) cnt[S.lens[s]]++;
-      cnt[0] = 0;
-      int code = 0;
-      for (int b = 1; b < 16; ++b) {
-        code = (code + cnt[b - 1]) << 1;
-        next[b] = code;
-      }
-      for (int s = 0; s < 257; ++s) S.code[s] = S.lens[s] ? uint16_t(next[S.lens[s]]++) : 0;
-    }
+  for (uint32_t i = tid; i < kHdrWords + 2; i += kInfThreads) S.hdr[i] = i < nw ? __ldg(words + i) : 0u;
+  for (int i = tid; i < (1 << kTabBits); i += kInfThreads) S.table[i] = 0;
+  const uint32_t mylen = index[uint64_t(c) * kNSeg + tid];
+  __syncthreads();
+  if (tid == 0) {
+    const int st = parse_header_fast(S);
     S.status = st;
     if (st) atomicExch(err, st);
   }
-  for (int i = lane; i < 1024; i += 32) S.table[i] = 0;
-  __syncwarp();
+  __syncthreads();
   if (S.status) return;
-  for (int s = lane; s < 257; s += 32) {
-    const int l = S.lens[s];
-    if (l == 0 || l > 10) continue;
-    const uint32_t rev = __brev(uint32_t(S.code[s])) >> (32 - l);
-    for (uint32_t f = rev; f < 1024; f += (1u << l)) S.table[f] = uint16_t((s << 4) | l);
+  for (int sym = tid; sym < 257; sym += kInfThreads) {
+    const int l = S.lens[sym];
+    if (l == 0 || l > kTabBits) continue;
+    for (uint32_t f = S.code[sym]; f < (1u << kTabBits); f += (1u << l)) S.table[f] = uint16_t((sym << 4) | l);
   }
-  __syncwarp();
+  // segment start = header bits + exclusive prefix of the segment lengths
+  {
+    uint32_t v = mylen;
+    const int lane = tid & 31;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, v, d);
+      if (lane >= d) v += y;
+    }
+    S.segstart[tid] = v;                     // inclusive within the warp
+  }
+  __syncthreads();
   const uint32_t seg = hdr->seg_bytes;
-  const uint32_t s0 = lane * seg, s1 = umin32(nc, (lane + 1) * seg);
+  const uint32_t s0 = tid * seg, s1 = umin32(nc, (tid + 1) * seg);
   if (s0 >= s1) return;
-  uint64_t pos = index[uint64_t(c) * kNSeg + lane];
+  uint64_t pos = S.hdr_bits + S.segstart[tid] - mylen + (tid >= 32 ? S.segstart[31] : 0);
+  const uint64_t wend = (e.bytes + 3) / 4;
   uint64_t wi = pos >> 5;
   uint64_t buf = uint64_t(__ldg(words + wi++)) >> (pos & 31);
   int cnt = 32 - int(pos & 31);
-  uint32_t outw = 0;
-  int nout = 0;
-  for (uint32_t i = s0; i < s1; ++i) {
+  bool bad = false;
+  auto next_sym = [&]() -> uint32_t {
     if (cnt <= 32) {
-      buf |= uint64_t(__ldg(words + wi++)) << cnt;
+      buf |= uint64_t(wi < wend ? __ldg(words + wi) : 0u) << cnt;
+      ++wi;
       cnt += 32;
     }
-    const uint16_t te = S.table[buf & 1023];
+    const uint16_t te = S.table[buf & ((1u << kTabBits) - 1)];
     int sym;
     if (te) {
       sym = te >> 4;
@@ -822,36 +893,22 @@ __global__ void __launch_bounds__(32) inflate_fast_kernel(InflateJobs J, int32_t
       buf >>= l;
       cnt -= l;
     } else {
-      // canonical decode for codes longer than 10 bits
-      int code = 0, first = 0, idx = 0;
-      sym = -1;
-      for (int l = 1; l < 16; ++l) {
-        code |= int(buf & 1);
-        buf >>= 1;
-        cnt--;
-        const int count = S.h.count[l];
-        if (code - count < first) {
-          sym = S.h.symbol[idx + (code - first)];
-          break;
-        }
-        idx += count;
-        first += count;
-        first <<= 1;
-        code <<= 1;
-      }
+      sym = decode_long(S.h, buf, cnt);
     }
-    if (sym < 0 || sym > 255) {
-      atomicExch(err, -7);
-      return;
-    }
-    outw |= uint32_t(sym) << (8 * nout);
-    if (++nout == 4) {
-      *reinterpret_cast<uint32_t *>(o + i - 3) = outw;
-      outw = 0;
-      nout = 0;
-    }
+    bad |= uint32_t(sym) > 255u;
+    return uint32_t(sym) & 0xFF;
+  };
+  uint32_t i = s0;
+  // 16 symbols -> one 16-byte store (segments are 16-byte aligned)
+  const bool vec_out = (reinterpret_cast<uintptr_t>(o) & 15) == 0;
+  for (; vec_out && i + 16 <= s1; i += 16) {
+    uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < 16; ++k) w[k >> 2] |= next_sym() << (8 * (k & 3));
+    *reinterpret_cast<uint4 *>(o + i) = make_uint4(w[0], w[1], w[2], w[3]);
   }
-  for (int k = 0; k < nout; ++k) o[s1 - nout + k] = (outw >> (8 * k)) & 0xFF;
+  for (; i < s1; ++i) o[i] = uint8_t(next_sym());
+  if (bad) atomicExch(err, -7);
 }
 
 kvtc_status launch_inflate_sections(const uint8_t *base, const uint64_t *off_dev0, uint64_t n0, uint32_t nch0,
@@ -868,7 +925,7 @@ kvtc_status launch_inflate_sections(const uint8_t *base, const uint64_t *off_dev
   J.out[0] = out0;
   J.out[1] = out1;
   if (nch0 + nch1 == 0) return KVTC_OK;
-  inflate_fast_kernel<<<nch0 + nch1, 32, 0, st>>>(J, err);
+  inflate_fast_kernel<<<nch0 + nch1, kInfThreads, 0, st>>>(J, err);
   KVTC_LAUNCH_CHECK();
   return KVTC_OK;
 }
@@ -881,7 +938,7 @@ kvtc_status launch_inflate_section(const uint8_t *base, const uint64_t *off_dev,
 // Validates a section header (host copy) against the expected payload size.
 kvtc_status check_section_header(const void *hdr_host, size_t len, size_t n_out, uint32_t *nchunks) {
   const SectionHeader *h = static_cast<const SectionHeader *>(hdr_host);
-  if (h->magic != kSectionMagic || h->version != 1 || h->section_bytes > len || h->raw_bytes != n_out ||
+  if (h->magic != kSectionMagic || h->version != kSectionVersion || h->section_bytes > len || h->raw_bytes != n_out ||
       h->nseg != kNSeg || h->chunk_bytes == 0 || h->nchunks != (n_out + h->chunk_bytes - 1) / h->chunk_bytes) {
     set_error("corrupt entropy section header");
     return KVTC_E_CORRUPT;

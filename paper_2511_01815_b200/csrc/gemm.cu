@@ -71,6 +71,8 @@ struct Params {
   int64_t tok_begin;
   int32_t fmt;         // 0 fp16, 1 bf16 operands
   int32_t tile_n;      // RECON / F32 / XTX N tile
+  int32_t a_hd;        // > 0: A is the 3-D cache map (GemmCompressArgs::a_hd)
+  int64_t a_row0;
 };
 
 __device__ __forceinline__ void cluster_sync_all() {
@@ -160,6 +162,15 @@ __device__ __forceinline__ void tma_load_2d_pair(void *smem_dst, const CUtensorM
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
       "%4}], [%2];" ::"r"(smem_u32(smem_dst)),
       "l"(reinterpret_cast<uint64_t>(m)), "r"(mbar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_pair(void *smem_dst, const CUtensorMap *m, uint64_t *bar, int32_t c0,
+                                                 int32_t c1, int32_t c2) {
+  const uint32_t mbar = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4, %5}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(mbar), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
 __device__ __forceinline__ void umma_f16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
@@ -276,11 +287,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (PAIR) {
           // both CTAs' bytes land on the leader's barrier
           if (leader) mbar_arrive_expect_tx(&full_bar[s], 2 * kStageBytes);
-          tma_load_2d_pair(a, &tmA, &full_bar[s], kb * kBlockK, T.mb * kTileM);
+          if (P.a_hd)
+            tma_load_3d_pair(a, &tmA, &full_bar[s], (kb * kBlockK) % P.a_hd, int(P.a_row0) + T.mb * kTileM,
+                             (kb * kBlockK) / P.a_hd);
+          else
+            tma_load_2d_pair(a, &tmA, &full_bar[s], kb * kBlockK, T.mb * kTileM);
           tma_load_2d_pair(b, &tmB, &full_bar[s], kb * kBlockK, n0 + int(rank) * (n_mma / 2));
         } else {
           mbar_arrive_expect_tx(&full_bar[s], kStageBytes);
-          tma_load_2d(a, &tmA, &full_bar[s], kb * kBlockK, T.mb * kTileM);
+          if (P.a_hd)
+            tma_load_3d(a, &tmA, &full_bar[s], (kb * kBlockK) % P.a_hd, int(P.a_row0) + T.mb * kTileM,
+                        (kb * kBlockK) / P.a_hd);
+          else
+            tma_load_2d(a, &tmA, &full_bar[s], kb * kBlockK, T.mb * kTileM);
           tma_load_2d(b, &tmB, &full_bar[s], kb * kBlockK, n0);
           tma_load_2d(b + kBBoxRows * 128, &tmB, &full_bar[s], kb * kBlockK, n0 + kBBoxRows);
         }
@@ -607,6 +626,8 @@ kvtc_status launch_gemm_project_quant(const GemmCompressArgs &a, cudaStream_t st
   p.tile_bytes = a.tile_bytes;
   p.codes_off_last = a.codes_off_last;
   p.fmt = 1;
+  p.a_hd = a.a_hd;
+  p.a_row0 = a.a_row0;
   p.num_m = int32_t(ceil_div(a.m, kTileM));
   p.num_n = a.nsegs;
   if (a.parts > 1)   // split groups: one tile per CTA, clusters along x

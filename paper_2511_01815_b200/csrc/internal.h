@@ -49,6 +49,10 @@ struct kvtc_plan_impl;
 // CUDA driver entry point for cuTensorMapEncodeTiled (no libcuda link needed)
 kvtc_status make_tmap_2d(CUtensorMap *m, const void *base, CUtensorMapDataType dt, uint64_t inner, uint64_t outer,
                          uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer);
+// 3-D map {d0, d1, d2} (strides of dims 1, 2 in bytes), box {box0, box1, 1}:
+// the per-layer contiguous cache [layers][tokens][h*d] read in place.
+kvtc_status make_tmap_3d(CUtensorMap *m, const void *base, CUtensorMapDataType dt, uint64_t d0, uint64_t d1,
+                         uint64_t d2, uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box0, uint32_t box1);
 
 // ------------------------------------------------------------------ launchers
 struct GemmCompressArgs {
@@ -69,6 +73,10 @@ struct GemmCompressArgs {
   int32_t G;               // number of non-None groups
   int64_t tile_bytes;      // bytes of a full tile
   const int64_t *codes_off_last;  // [G] code-block offsets of the last partial tile
+  // a_hd > 0: tmA is the 3-D map {hd, tokens, layers} of a contiguous cache and
+  // row r of X is token a_row0 + r (k-block kb = layer kb*64/hd, column kb*64%hd)
+  int32_t a_hd;
+  int64_t a_row0;
 };
 kvtc_status launch_gemm_project_f32(const GemmCompressArgs &a, int32_t ncols, cudaStream_t st);
 kvtc_status launch_gemm_project_quant(const GemmCompressArgs &a, cudaStream_t st);

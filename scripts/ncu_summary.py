@@ -83,8 +83,9 @@ if __name__ == "__main__":
                      f"{f(d.get('dram_write'), 1e9)} | {f(d.get('dram_read_pct'), 1, 1)} | {f(d.get('l2_pct'), 1, 1)} | "
                      f"{f(tp, 1, 1)} | {f(d.get('sm_pct'), 1, 1)} | {f(d.get('occupancy_pct'), 1, 1)} | "
                      f"{f(d.get('regs'), 1, 0)} |")
-        key = {"kvtc::gemm_kernel<1>": "c.project_quant_gemm", "kvtc::gemm_kernel<2>": "d.reconstruct_gemm"}.get(
-            d["kernel"])
+        kn = d["kernel"].replace(" ", "")
+        key = ("c.project_quant_gemm" if kn.startswith("kvtc::gemm_kernel<1,true>") or kn == "kvtc::gemm_kernel<1>"
+               else "d.reconstruct_gemm" if kn.startswith("kvtc::gemm_kernel<2") else None)
         if key and key not in traffic and d.get("dram_read") is not None:
             traffic[key] = d["dram_read"] + (d.get("dram_write") or 0)
     open(md, "w").write("\n".join(lines) + "\n")

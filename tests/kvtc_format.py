@@ -12,10 +12,11 @@ CONTAINER_HDR = struct.Struct("<II6iqqqQQ2Q2Q2Q2QQ2Q")
 
 def parse_section(buf: bytes):
     magic, ver, raw, chunk, nch, seg, nseg, data_off, total = SECTION_HDR.unpack_from(buf, 0)
-    assert magic == 0x4454564B and ver == 1
+    assert magic == 0x4454564B and ver == 2
     tab = np.frombuffer(buf, dtype=np.dtype([("off", "<u8"), ("bytes", "<u4"), ("kind", "<u4")]), count=nch,
                         offset=64)
-    idx = np.frombuffer(buf, dtype="<u4", count=nch * nseg, offset=64 + 16 * nch).reshape(nch, nseg)
+    idx = np.frombuffer(buf, dtype="<u2", count=nch * nseg, offset=64 + 16 * nch).reshape(nch, nseg)
+    assert data_off == 64 + 16 * nch + ((2 * nch * nseg + 3) & ~3)
     streams = [buf[data_off + int(e["off"]): data_off + int(e["off"]) + int(e["bytes"])] for e in tab]
     return dict(raw=raw, chunk=chunk, nchunks=nch, seg=seg, nseg=nseg, data_off=data_off, total=total,
                 table=tab, index=idx, streams=streams)
@@ -29,3 +30,110 @@ def parse_container(buf: bytes):
     h = dict(zip(names, f))
     assert h["magic"] == 0x4354564B
     return h
+
+
+def dynamic_header_bits(stream: bytes) -> int:
+    """Bit length of the (single, final, dynamic) DEFLATE block header at the
+    start of `stream` (RFC 1951 §3.2.7): the segment index counts from there."""
+    bits = int.from_bytes(stream[:2048], "little")
+    pos = 0
+
+    def get(n):
+        nonlocal pos
+        v = (bits >> pos) & ((1 << n) - 1)
+        pos += n
+        return v
+
+    return _dynamic_header(stream)[0]
+
+
+def _canonical(lens):
+    """(reversed code, length) per symbol, RFC 1951 §3.2.2."""
+    cnt = [0] * 16
+    for ln in lens:
+        cnt[ln] += 1
+    cnt[0] = 0
+    nxt, code = [0] * 16, 0
+    for b in range(1, 16):
+        code = (code + cnt[b - 1]) << 1
+        nxt[b] = code
+    out = []
+    for ln in lens:
+        if ln:
+            c = nxt[ln]
+            nxt[ln] += 1
+            out.append((int(format(c, f"0{ln}b")[::-1], 2), ln))
+        else:
+            out.append((0, 0))
+    return out
+
+
+def segment_bit_lengths(stream: bytes, nbytes: int, seg_bytes: int, nseg: int):
+    """Decode one literal-only chunk stream symbol by symbol and return the bit
+    length of each seg_bytes-symbol segment (the section's u16 index; the last
+    segment includes the end-of-block code)."""
+    hbits, lens = _dynamic_header(stream)
+    codes = _canonical(lens[:257])
+    table = np.full(1 << 15, -1, dtype=np.int64)
+    for sym, (rc, ln) in enumerate(codes):
+        if ln:
+            table[rc::1 << ln] = (sym << 4) | ln
+    bits = np.unpackbits(np.frombuffer(stream + b"\0" * 4, dtype=np.uint8), bitorder="little").astype(np.int64)
+    win = np.zeros(len(bits) - 15, dtype=np.int64)
+    for k in range(15):
+        win += bits[k:len(bits) - 15 + k] << k
+    pos, starts, out = hbits, [], []
+    for i in range(nbytes + 1):
+        if i % seg_bytes == 0 and i < nbytes:
+            starts.append(pos)
+        e = int(table[win[pos]])
+        assert e >= 0
+        sym = e >> 4
+        assert (sym == 256) == (i == nbytes)
+        if i < nbytes:
+            out.append(sym)
+        pos += e & 15
+    ends = starts[1:] + [pos]
+    lengths = [b - a for a, b in zip(starts, ends)] + [0] * (nseg - len(starts))
+    return lengths, bytes(out), pos
+
+
+def _dynamic_header(stream: bytes):
+    bits = int.from_bytes(stream[:2048], "little")
+    pos = 0
+
+    def get(n):
+        nonlocal pos
+        v = (bits >> pos) & ((1 << n) - 1)
+        pos += n
+        return v
+
+    assert get(1) == 1 and get(2) == 2
+    nlen, ndist, ncode = get(5) + 257, get(5) + 1, get(4) + 4
+    order = [16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15]
+    cl = [0] * 19
+    for i in range(ncode):
+        cl[order[i]] = get(3)
+    # canonical code-length code, decoded bit by bit (MSB-first code bits)
+    codes, code = {}, 0
+    for ln in range(1, 8):
+        for sym in range(19):
+            if cl[sym] == ln:
+                codes[(ln, code)] = sym
+                code += 1
+        code <<= 1
+    lens = []
+    while len(lens) < nlen + ndist:
+        c, ln = 0, 0
+        while (ln, c) not in codes:
+            c = (c << 1) | get(1)
+            ln += 1
+            assert ln <= 7
+        sym = codes[(ln, c)]
+        if sym < 16:
+            lens.append(sym)
+        elif sym == 16:
+            lens += [lens[-1]] * (3 + get(2))
+        else:
+            lens += [0] * (3 + get(3) if sym == 17 else 11 + get(7))
+    return pos, lens

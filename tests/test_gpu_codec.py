@@ -145,3 +145,28 @@ def test_mismatched_plan_rejected(K):
     with pytest.raises(Exception) as e:
         K.decompress(KB, other, VB, VP, cont, K.KVView(torch.zeros_like(Kc).cuda()), K.KVView(torch.zeros_like(Vc).cuda()))
     assert "MISMATCH" in str(e.value)
+
+
+def test_direct_cache_read_matches_gather(K, monkeypatch):
+    """The values' GEMM reads a contiguous cache in place through a 3-D tensor
+    map; the container must be byte-identical to the gathered path's, for a
+    tight cache, an over-allocated one (layer stride > tokens) and per-layer
+    tensors at unrelated addresses (gather fallback)."""
+    name, tokens = "mid", 900
+    spec, invf, kb, vb, KB, VB, KP, VP, okp, ovp = _setup(K, name)
+    Kc, Vc = E.caches(name, tokens, 0, conversation=8)
+    kd, vd = Kc.cuda(), Vc.cuda()
+
+    def run(vview):
+        cont, _ = K.compress(KB, KP, VB, VP, K.KVView(kd), vview)
+        torch.cuda.synchronize()
+        return cont.cpu().numpy().tobytes()
+
+    direct = run(K.KVView(vd))
+    big = torch.zeros(spec.layers, tokens + 77, spec.kv_heads, spec.head_dim, dtype=torch.bfloat16, device="cuda")
+    big[:, :tokens] = vd
+    strided = run(K.KVView(big, tokens=tokens))
+    separate = run(K.KVView([vd[i].clone() for i in range(spec.layers)]))
+    monkeypatch.setenv("KVTC_NO_DIRECT", "1")
+    gathered = run(K.KVView(vd))
+    assert direct == gathered and strided == gathered and separate == gathered

@@ -6,7 +6,7 @@ import pytest
 import torch
 
 from tests import gpu_env as E
-from tests.kvtc_format import parse_section
+from tests.kvtc_format import parse_section, segment_bit_lengths
 
 pytestmark = pytest.mark.gpu
 
@@ -131,6 +131,18 @@ def test_deflate_roundtrip_zlib(K):
         # every chunk is an independent raw DEFLATE stream stock zlib inflates
         got = b"".join(zlib.decompress(s, wbits=-15) for s in info["streams"])
         assert got == data.tobytes()
+        # the side index: bit length of each 1/64 of a chunk, checked by decoding
+        # the first chunks symbol by symbol (Q19)
+        assert info["nseg"] == 64 and info["seg"] * 64 == info["chunk"]
+        for c in range(min(2, info["nchunks"])):
+            if info["table"][c]["kind"] != 0:
+                assert not info["index"][c].any()
+                continue
+            nb = min(info["chunk"], len(data) - c * info["chunk"])
+            lens, dec, end = segment_bit_lengths(info["streams"][c], nb, info["seg"], 64)
+            assert dec == data.tobytes()[c * info["chunk"]: c * info["chunk"] + nb]
+            assert list(info["index"][c]) == lens
+            assert (end + 7) // 8 == info["table"][c]["bytes"]
         # and the GPU inflates its own section
         back = K.inflate(sec, len(data))
         assert torch.equal(back.cpu(), t.cpu())
