@@ -238,6 +238,7 @@ extern "C" kvtc_status kvtc_basis_get(const kvtc_basis *b, int32_t *p, int32_t *
 // =================================================================== plan
 kvtc_plan::~kvtc_plan() {
   cudaFree(d_segs);
+  cudaFree(d_wide);
   cudaFree(d_gdesc);
   cudaFree(d_pgroups);
   cudaFree(d_codes_off_full);
@@ -276,15 +277,19 @@ kvtc_status plan_compile(kvtc_plan *pl) {
     off[g] = o;
     o += (int64_t(kTileM) * pl->groups[g].size * bits_of(pl->groups[g].type) + 7) / 8;
   }
-  // segments: unsplit groups packed greedily into <= 256-column tiles; wider
-  // groups (multiple of 256) split into 256-column pieces, one cluster each.
+  // segments: groups of <= 256 columns packed greedily into <= 256-column tiles;
+  // wider groups (k * 256) become k pieces whose tiles store fp32 coefficients
+  // to a scratch, quantised afterwards by quant_wide_kernel (the row min/max
+  // spans the pieces).
   std::vector<SegDesc> segs;
   std::vector<GroupDesc> gd;
-  std::map<int, std::vector<std::pair<SegDesc, GroupDesc>>> split;
-  SegDesc cur{-1, 0, 0, 0};
+  std::vector<SegDesc> wide_segs;
+  std::vector<WideDesc> wide;
+  int wcol = 0;
+  SegDesc cur{-1, 0, 0, 0, -1};
   auto close = [&]() {
     if (cur.col0 >= 0 && cur.g_end > cur.g_begin) segs.push_back(cur);
-    cur = SegDesc{-1, 0, int32_t(gd.size()), int32_t(gd.size())};
+    cur = SegDesc{-1, 0, int32_t(gd.size()), int32_t(gd.size()), -1};
   };
   close();
   for (int g = 0; g < G; ++g) {
@@ -298,29 +303,26 @@ kvtc_status plan_compile(kvtc_plan *pl) {
       cur.width = pg.col + pg.size - cur.col0;
       cur.g_end = int32_t(gd.size());
     } else {
-      if (pg.size % kMaxTileN != 0 || pg.size / kMaxTileN > 8) {
-        set_error("group size %d unsupported (sizes > 256 must be k*256, k <= 8)", pg.size);
+      if (pg.size % kMaxTileN != 0) {
+        set_error("group size %d unsupported (sizes > 256 must be multiples of 256)", pg.size);
         return KVTC_E_INVALID;
       }
-      const int parts = pg.size / kMaxTileN;
-      for (int q = 0; q < parts; ++q)
-        split[parts].push_back({SegDesc{pg.col + q * kMaxTileN, kMaxTileN, 0, 0},
-                                GroupDesc{0, kMaxTileN, pg.size, pg.type, g, q, off[g]}});
+      for (int q = 0; q < pg.size / kMaxTileN; ++q)
+        wide_segs.push_back(SegDesc{pg.col + q * kMaxTileN, kMaxTileN, 0, 0, wcol + q * kMaxTileN});
+      wide.push_back(WideDesc{g, pg.size, pg.type, pg.col, wcol, 0, off[g]});
+      wcol += pg.size;
     }
   }
   close();
-  pl->launches.clear();
-  pl->launches.push_back({0, int32_t(segs.size()), 1});
-  for (auto &kv : split) {
-    const int begin = int(segs.size());
-    for (auto &sg : kv.second) {
-      SegDesc s = sg.first;
-      s.g_begin = int32_t(gd.size());
-      gd.push_back(sg.second);
-      s.g_end = int32_t(gd.size());
-      segs.push_back(s);
-    }
-    pl->launches.push_back({begin, int32_t(kv.second.size()), kv.first});
+  for (SegDesc &w : wide_segs) {
+    w.g_begin = w.g_end = int32_t(gd.size());
+    segs.push_back(w);
+  }
+  pl->nwide = int(wide.size());
+  pl->wide_cols = wcol;
+  if (!wide.empty()) {
+    KVTC_CUDA_TRY(cudaMalloc(&pl->d_wide, wide.size() * sizeof(WideDesc)));
+    KVTC_CUDA_TRY(cudaMemcpy(pl->d_wide, wide.data(), wide.size() * sizeof(WideDesc), cudaMemcpyHostToDevice));
   }
   pl->nsegs = int(segs.size());
   KVTC_CUDA_TRY(cudaMalloc(&pl->d_segs, std::max<size_t>(1, segs.size()) * sizeof(SegDesc)));

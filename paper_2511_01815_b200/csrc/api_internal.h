@@ -27,10 +27,6 @@ struct kvtc_basis {
   ~kvtc_basis();
 };
 
-struct SegLaunch {
-  int32_t seg_begin, nseg, parts;
-};
-
 // Bit allocation of one stream compiled for the kernels.
 struct kvtc_plan {
   int32_t r = 0;
@@ -42,8 +38,9 @@ struct kvtc_plan {
   int64_t budget = -1;
   int64_t tile_bytes = 0;
   int32_t nsegs = 0;
-  std::vector<SegLaunch> launches;
+  int32_t nwide = 0, wide_cols = 0;     // groups wider than a tile, their total columns
   kvtc::SegDesc *d_segs = nullptr;
+  kvtc::WideDesc *d_wide = nullptr;
   kvtc::GroupDesc *d_gdesc = nullptr;
   kvtc::PlanGroup *d_pgroups = nullptr;
   int64_t *d_codes_off_full = nullptr;

@@ -76,11 +76,13 @@ bool direct_view_map(const kvtc_kv_view &v, int64_t tok0, CUtensorMap *m) {
 }
 
 // X: the gathered rows [m x p], or nullptr with `direct` = the 3-D map of the
-// cache itself (rows = tokens tok0 ..).
+// cache itself (rows = tokens tok0 ..).  wide: fp32 scratch [m x wide_cols] for
+// the plan's wide groups (nullptr if it has none).
 kvtc_status run_project_quant(const kvtc_basis *b, kvtc_plan *pl, const Operands *op, const void *X, int64_t m,
-                              uint8_t *payload, cudaStream_t st, const CUtensorMap *direct = nullptr,
+                              uint8_t *payload, float *wide, cudaStream_t st, const CUtensorMap *direct = nullptr,
                               int64_t tok0 = 0) {
   if (m == 0 || pl->G == 0) return KVTC_OK;
+  KVTC_CHECK_ARG(pl->nwide == 0 || wide, "wide-group scratch");
   CUtensorMap tA;
   kvtc_status s = KVTC_OK;
   if (!direct && (s = tmap_X(&tA, X, m, b->p))) return s;
@@ -99,14 +101,13 @@ kvtc_status run_project_quant(const kvtc_basis *b, kvtc_plan *pl, const Operands
   a.tile_bytes = pl->tile_bytes;
   a.codes_off_last = plan_codes_off_last(pl, m % kTileM);
   a.groups = pl->d_gdesc;
-  for (const SegLaunch &L : pl->launches) {
-    if (L.nseg == 0) continue;
-    a.segs = pl->d_segs + L.seg_begin;
-    a.nsegs = L.nseg;
-    a.parts = L.parts;
-    if ((s = launch_gemm_project_quant(a, st))) return s;
-  }
-  return KVTC_OK;
+  a.segs = pl->d_segs;
+  a.nsegs = pl->nsegs;
+  a.D = wide;
+  a.ldd = pl->wide_cols;
+  if ((s = launch_gemm_project_quant(a, st))) return s;
+  return launch_quant_wide(pl->d_wide, pl->nwide, wide, pl->wide_cols, 1, m, pl->tile_bytes, a.codes_off_last,
+                           payload, st);
 }
 
 kvtc_status run_reconstruct(const kvtc_basis *b, const kvtc_plan *pl, const Operands *op, const __half *Dh,
@@ -166,6 +167,12 @@ SideStream *side_stream() {
   return &S;
 }
 
+// KVTC_NO_OVERLAP=1 runs the codec kernels on the caller's stream (measurements).
+bool overlap_off() {
+  const char *e = getenv("KVTC_NO_OVERLAP");
+  return e && e[0] == '1';
+}
+
 // KVTC_NO_DIRECT=1 forces the gathered path (tests compare the two).
 bool direct_off() {
   const char *e = getenv("KVTC_NO_DIRECT");
@@ -216,8 +223,12 @@ extern "C" kvtc_status kvtc_stage_quantize_pack(const kvtc_plan *plan, const flo
                                                 void *stream) {
   KVTC_CHECK_ARG(plan && D && payload && m >= 0, "quantize_pack arguments");
   auto *pl = const_cast<kvtc_plan *>(plan);
-  return launch_quant_pack_simt(pl->d_segs, pl->d_gdesc, pl->nsegs, pl->G, D, pl->r_nz, m, pl->tile_bytes,
-                                plan_codes_off_last(pl, m % kTileM), payload, static_cast<cudaStream_t>(stream));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t *col = plan_codes_off_last(pl, m % kTileM);
+  kvtc_status s = launch_quant_pack_simt(pl->d_segs, pl->d_gdesc, pl->nsegs, pl->G, D, pl->r_nz, m, pl->tile_bytes,
+                                         col, payload, st);
+  if (s) return s;
+  return launch_quant_wide(pl->d_wide, pl->nwide, D, pl->r_nz, 0, m, pl->tile_bytes, col, payload, st);
 }
 
 extern "C" kvtc_status kvtc_stage_project_quantize(const kvtc_basis *b, const kvtc_plan *plan, const void *X,
@@ -227,7 +238,12 @@ extern "C" kvtc_status kvtc_stage_project_quantize(const kvtc_basis *b, const kv
   const Operands *op;
   kvtc_status s = plan_operands(b, pl, &op);
   if (s) return s;
-  return run_project_quant(b, pl, op, X, m, payload, static_cast<cudaStream_t>(stream));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float *wide = nullptr;      // stream-ordered scratch for the wide groups
+  if (pl->nwide && m) KVTC_CUDA_TRY(cudaMallocAsync(&wide, size_t(m) * pl->wide_cols * sizeof(float), st));
+  s = run_project_quant(b, pl, op, X, m, payload, wide, st);
+  if (wide) cudaFreeAsync(wide, st);
+  return s;
 }
 
 extern "C" size_t kvtc_deflate_bound(size_t n, int32_t chunk_bytes) { return deflate_section_bound(n, chunk_bytes); }
@@ -376,6 +392,7 @@ extern "C" size_t kvtc_compress_workspace_bytes(const kvtc_basis *kb, const kvtc
   b.take<uint8_t>(L.pay[0] + 16);
   b.take<uint8_t>(L.pay[1] + 16);
   b.take<uint8_t>(deflate_workspace(std::max(L.pay[0], L.pay[1]), pol->chunk_bytes));
+  b.take<float>(L.m * std::max(kp->wide_cols, vp->wide_cols));
   return b.used + 256;
 }
 
@@ -418,6 +435,7 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
   uint8_t *payload_v = ws.take<uint8_t>(L.pay[1] + 16);
   const size_t dws = deflate_workspace(std::max(L.pay[0], L.pay[1]), pol->chunk_bytes);
   void *dwsp = ws.take<uint8_t>(dws);
+  float *wide = ws.take<float>(L.m * std::max(kp->wide_cols, vp->wide_cols));
   if ((s = upload_bases(k, kbases, st)) || (s = upload_bases(v, vbases, st))) return s;
 
   uint8_t *o = static_cast<uint8_t *>(out);
@@ -473,6 +491,7 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
   // keys' DEFLATE (K3) then runs on the side stream while the values' gather and
   // GEMM run on the caller's stream, and the values' DEFLATE follows it there.
   SideStream *ss = side_stream();
+  cudaStream_t aux = overlap_off() ? st : ss->s;
   {
     ProfScope ps("c.gather_unrope", st);
     if ((s = rope_table_for(kb, k->pos0 + pol->sinks, L.m, cs, st))) return s;
@@ -480,15 +499,15 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
   }
   {
     ProfScope ps("c.project_quant_gemm", st);
-    if ((s = run_project_quant(kb, kpl, kop, X, L.m, payload_k, st))) return s;
+    if ((s = run_project_quant(kb, kpl, kop, X, L.m, payload_k, wide, st))) return s;
   }
   KVTC_CUDA_TRY(cudaEventRecord(ss->ev[0], st));
-  KVTC_CUDA_TRY(cudaStreamWaitEvent(ss->s, ss->ev[0], 0));
+  KVTC_CUDA_TRY(cudaStreamWaitEvent(aux, ss->ev[0], 0));
   {
-    ProfScope ps("c.deflate_overlapped", ss->s);
-    if ((s = launch_deflate(payload_k, L.pay[0], pol->chunk_bytes, o, lens + 2, lens + 0, dwsp, dws, ss->s))) return s;
+    ProfScope ps("c.deflate_overlapped", aux);
+    if ((s = launch_deflate(payload_k, L.pay[0], pol->chunk_bytes, o, lens + 2, lens + 0, dwsp, dws, aux))) return s;
   }
-  offset_after_kernel<<<1, 1, 0, ss->s>>>(lens + 2, lens + 0, lens + 3, o);
+  offset_after_kernel<<<1, 1, 0, aux>>>(lens + 2, lens + 0, lens + 3, o);
   KVTC_LAUNCH_CHECK();
   // ---- values: read in place when the cache layout allows it
   CUtensorMap tV;
@@ -499,9 +518,10 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
   }
   {
     ProfScope ps("c.project_quant_gemm", st);
-    if ((s = run_project_quant(vb, vpl, vop, X, L.m, payload_v, st, v_direct ? &tV : nullptr, pol->sinks))) return s;
+    if ((s = run_project_quant(vb, vpl, vop, X, L.m, payload_v, wide, st, v_direct ? &tV : nullptr, pol->sinks)))
+      return s;
   }
-  KVTC_CUDA_TRY(cudaEventRecord(ss->ev[1], ss->s));
+  KVTC_CUDA_TRY(cudaEventRecord(ss->ev[1], aux));
   KVTC_CUDA_TRY(cudaStreamWaitEvent(st, ss->ev[1], 0));          // join: K section written, V offset known
   {
     ProfScope ps("c.deflate", st);
@@ -634,9 +654,10 @@ extern "C" kvtc_status kvtc_decompress(const kvtc_basis *kb, const kvtc_plan *kp
   // The values' inflate waits for the keys' inflate (which then has the whole GPU:
   // it is latency-bound and two concurrent inflates each run at half speed).
   SideStream *ss = side_stream();
+  cudaStream_t aux = overlap_off() ? st : ss->s;
   __half *Dhs[2] = {Dh, Dh_v};
   for (int sv = 0; sv < 2; ++sv) {
-    cudaStream_t cs_ = sv ? ss->s : st;
+    cudaStream_t cs_ = sv ? aux : st;
     kvtc_plan *pl = const_cast<kvtc_plan *>(sv ? vp : kp);
     const uint32_t nch = uint32_t((h.payload_bytes[sv] + h.chunk_bytes - 1) / h.chunk_bytes);
     {
@@ -646,7 +667,7 @@ extern "C" kvtc_status kvtc_decompress(const kvtc_basis *kb, const kvtc_plan *kp
     }
     if (sv == 0) {
       KVTC_CUDA_TRY(cudaEventRecord(ss->ev[2], st));             // header/bases/err ready, keys inflated
-      KVTC_CUDA_TRY(cudaStreamWaitEvent(ss->s, ss->ev[2], 0));
+      KVTC_CUDA_TRY(cudaStreamWaitEvent(aux, ss->ev[2], 0));
     }
     {
       ProfScope ps(sv ? "d.dequant_overlapped" : "d.dequant", cs_);
@@ -656,7 +677,7 @@ extern "C" kvtc_status kvtc_decompress(const kvtc_basis *kb, const kvtc_plan *kp
       if (pl->r_nz == 0) KVTC_CUDA_TRY(cudaMemsetAsync(Dhs[sv], 0, h.m * ld * 2, cs_));
     }
   }
-  KVTC_CUDA_TRY(cudaEventRecord(ss->ev[3], ss->s));
+  KVTC_CUDA_TRY(cudaEventRecord(ss->ev[3], aux));
   for (int sv = 0; sv < 2; ++sv) {
     const kvtc_basis *b = sv ? vb : kb;
     kvtc_plan *pl = const_cast<kvtc_plan *>(sv ? vp : kp);

@@ -4,17 +4,21 @@
 // algorithm" and runs on the GPU.  Reading Q15: 64 KiB chunks, each
 // an independent raw DEFLATE stream that stock zlib inflates (wbits = -15).
 //
-// Encoder (one CTA of 256 threads per chunk): byte histogram -> length-limited
-// canonical Huffman code (<= 15 bits; in-place minimum-redundancy lengths +
-// Kraft-sum repair) -> one dynamic block (literals + EOB only, no LZ77 matches in
-// this version) -> each thread emits the bits of 1/256 of the chunk at an offset
-// from a block-wide exclusive scan.  Falls back to stored blocks when smaller.
-// While emitting, the bit offset of every 1/32 of the chunk ("segment") is
-// recorded in a side index that lives in the section, NOT in the DEFLATE stream.
+// Encoder (one CTA of 64 threads per chunk, ~14 chunks resident per SM so the
+// serial code construction of one chunk overlaps the parallel passes of the
+// others): byte histogram -> length-limited canonical Huffman code (<= 15 bits;
+// in-place minimum-redundancy lengths + Kraft-sum repair) -> one dynamic block
+// (literals + EOB only, no LZ77 matches in this version) -> thread j emits the
+// bits of segment j (1/64 of the chunk) at an offset from a block-wide
+// exclusive scan.  Falls back to stored blocks when smaller.  The bit length of
+// every segment goes to a u16 side index that lives in the section, NOT in the
+// DEFLATE stream.
 //
-// Decoder, fast path (one warp per chunk): lane 0 parses the block header, the
-// warp builds a 10-bit lookup table in shared memory, then lane j decodes
-// segment j from its recorded bit offset — 32 independent serial decoders.
+// Decoder, fast path (64 threads per chunk): thread 0 parses the block header
+// (table-driven code-length decode), the block builds a two-level table (11-bit
+// first level + 4-bit subtables for longer codes) in shared memory, then thread
+// j decodes segment j from the prefix sum of the index — 64 independent serial
+// decoders with one word of read-ahead and 16-byte output stores.
 // Decoder, generic path (kvtc_stage_inflate_raw): a complete sequential inflater
 // (stored / fixed / dynamic blocks, LZ77 back-references) for foreign streams.
 //
@@ -29,7 +33,7 @@
 namespace kvtc {
 
 constexpr uint32_t kSectionMagic = 0x4454564Bu;  // "KVTD"
-constexpr int kEncThreads = 256;
+constexpr int kEncThreads = 64;   // one thread per segment; ~14 chunks resident per SM
 constexpr int kNSeg = 64;
 constexpr uint32_t kSectionVersion = 2;
 constexpr int kLitSyms = 257;                    // 0..255 literals + 256 end-of-block
@@ -286,7 +290,7 @@ struct WordWriter {
   }
 };
 
-__global__ void __launch_bounds__(kEncThreads, 2) deflate_encode_kernel(const uint8_t *in, uint64_t n, int32_t chunk,
+__global__ void __launch_bounds__(kEncThreads, 14) deflate_encode_kernel(const uint8_t *in, uint64_t n, int32_t chunk,
                                                                         uint8_t *slots, uint64_t stride,
                                                                         uint32_t *chunk_bytes, uint32_t *chunk_kind,
                                                                         uint16_t *index) {
@@ -303,7 +307,7 @@ __global__ void __launch_bounds__(kEncThreads, 2) deflate_encode_kernel(const ui
 
   for (int s = t; s < (kEncThreads / 32) * (kLitSyms + 3); s += kEncThreads) (&S.whist[0][0])[s] = 0;
   if (t < 19) S.clhist[t] = 0;
-  if (t < 160) S.hdr[t] = 0;
+  for (int i = t; i < 160; i += kEncThreads) S.hdr[i] = 0;
   __syncthreads();
   // ---- histogram: 16-byte vector loads over the whole chunk, warp-private bins
   {
@@ -397,7 +401,7 @@ __global__ void __launch_bounds__(kEncThreads, 2) deflate_encode_kernel(const ui
     S.hdr_bits = bw.finish();
   }
   __syncthreads();
-  S.sym[t] = uint32_t(S.rev[t]) | (uint32_t(S.len[t]) << 16);     // kEncThreads == 256 literals
+  for (int i = t; i < 256; i += kEncThreads) S.sym[i] = uint32_t(S.rev[i]) | (uint32_t(S.len[i]) << 16);
   __syncthreads();
   // ---- bit counts per piece, exclusive scan
   const bool vec = ((reinterpret_cast<uintptr_t>(src + p0) & 15) == 0) && ((p1 - p0) % 16 == 0);
@@ -702,12 +706,18 @@ __device__ int huff_decode_s(SmemBits &br, const Huff &h) {
 
 constexpr int kHdrWords = 512;     // first 2 KiB of a chunk stream hold its block header
 constexpr int kTabBits = 11;       // first-level decode table: codes <= 11 bits in one lookup
+constexpr int kSubBits = 15 - kTabBits;
+// Canonical codes longer than kTabBits fill a contiguous range at the end of the
+// code space of measure <= 256 * 2^-12, i.e. at most 2^kTabBits / 16 + 1 distinct
+// first-level prefixes.
+constexpr int kSubTabs = (1 << kTabBits) / 16 + 1;
 constexpr int kInfThreads = kNSeg; // one thread per segment, 2 warps per chunk
 static_assert(kNSeg == 64, "the segment-start scan below assumes two warps");
 
 struct FastShared {
   uint32_t hdr[kHdrWords + 2];
-  uint16_t table[1 << kTabBits];   // (sym << 4) | len for codes <= kTabBits; 0 = slow path
+  uint16_t table[1 << kTabBits];   // (sym << 4) | len; 0x8000 | k: longer code, subtable k
+  uint16_t sub[kSubTabs << kSubBits];  // second level: the next kSubBits bits
   uint16_t code[260];
   Huff h;
   uint8_t lens[320];
@@ -798,23 +808,6 @@ __device__ int parse_header_fast(FastShared &S) {
   return 0;
 }
 
-// Slow path for codes longer than kTabBits: canonical bit-serial decode.
-__device__ __forceinline__ int decode_long(const Huff &h, uint64_t &buf, int &cnt) {
-  int code = 0, first = 0, idx = 0;
-  for (int l = 1; l < 16; ++l) {
-    code |= int(buf & 1);
-    buf >>= 1;
-    cnt--;
-    const int count = h.count[l];
-    if (code - count < first) return h.symbol[idx + (code - first)];
-    idx += count;
-    first += count;
-    first <<= 1;
-    code <<= 1;
-  }
-  return -1;
-}
-
 __global__ void __launch_bounds__(kInfThreads) inflate_fast_kernel(InflateJobs J, int32_t *err) {
   __shared__ FastShared S;
   const int job = blockIdx.x < J.nch[0] ? 0 : 1;
@@ -844,6 +837,7 @@ __global__ void __launch_bounds__(kInfThreads) inflate_fast_kernel(InflateJobs J
   const uint32_t nw = umin32((e.bytes + 3) / 4, kHdrWords);
   for (uint32_t i = tid; i < kHdrWords + 2; i += kInfThreads) S.hdr[i] = i < nw ? __ldg(words + i) : 0u;
   for (int i = tid; i < (1 << kTabBits); i += kInfThreads) S.table[i] = 0;
+  for (int i = tid; i < (kSubTabs << kSubBits); i += kInfThreads) S.sub[i] = 0;
   const uint32_t mylen = index[uint64_t(c) * kNSeg + tid];
   __syncthreads();
   if (tid == 0) {
@@ -858,6 +852,26 @@ __global__ void __launch_bounds__(kInfThreads) inflate_fast_kernel(InflateJobs J
     if (l == 0 || l > kTabBits) continue;
     for (uint32_t f = S.code[sym]; f < (1u << kTabBits); f += (1u << l)) S.table[f] = uint16_t((sym << 4) | l);
   }
+  if (tid == 0) {
+    // long codes: one subtable per distinct first-level prefix
+    int nsub = 0;
+    for (int sym = 0; sym < 257 && !S.status; ++sym) {
+      const int l = S.lens[sym];
+      if (l <= kTabBits) continue;
+      const uint32_t pre = S.code[sym] & ((1u << kTabBits) - 1);
+      if (!(S.table[pre] & 0x8000)) {
+        if (nsub == kSubTabs) {
+          S.status = -8;
+          atomicExch(err, -8);
+          break;
+        }
+        S.table[pre] = uint16_t(0x8000 | nsub++);
+      }
+      uint16_t *st = S.sub + ((S.table[pre] & 0x7FFF) << kSubBits);
+      for (uint32_t f = S.code[sym] >> kTabBits; f < (1u << kSubBits); f += (1u << (l - kTabBits)))
+        st[f] = uint16_t((sym << 4) | l);
+    }
+  }
   // segment start = header bits + exclusive prefix of the segment lengths
   {
     uint32_t v = mylen;
@@ -870,6 +884,7 @@ __global__ void __launch_bounds__(kInfThreads) inflate_fast_kernel(InflateJobs J
     S.segstart[tid] = v;                     // inclusive within the warp
   }
   __syncthreads();
+  if (S.status) return;
   const uint32_t seg = hdr->seg_bytes;
   const uint32_t s0 = tid * seg, s1 = umin32(nc, (tid + 1) * seg);
   if (s0 >= s1) return;
@@ -878,25 +893,24 @@ __global__ void __launch_bounds__(kInfThreads) inflate_fast_kernel(InflateJobs J
   uint64_t wi = pos >> 5;
   uint64_t buf = uint64_t(__ldg(words + wi++)) >> (pos & 31);
   int cnt = 32 - int(pos & 31);
+  uint32_t nextw = wi < wend ? __ldg(words + wi) : 0u;   // one word of read-ahead
+  ++wi;
   bool bad = false;
   auto next_sym = [&]() -> uint32_t {
     if (cnt <= 32) {
-      buf |= uint64_t(wi < wend ? __ldg(words + wi) : 0u) << cnt;
-      ++wi;
+      buf |= uint64_t(nextw) << cnt;
       cnt += 32;
+      nextw = wi < wend ? __ldg(words + wi) : 0u;
+      ++wi;
     }
-    const uint16_t te = S.table[buf & ((1u << kTabBits) - 1)];
-    int sym;
-    if (te) {
-      sym = te >> 4;
-      const int l = te & 15;
-      buf >>= l;
-      cnt -= l;
-    } else {
-      sym = decode_long(S.h, buf, cnt);
-    }
-    bad |= uint32_t(sym) > 255u;
-    return uint32_t(sym) & 0xFF;
+    uint32_t te = S.table[buf & ((1u << kTabBits) - 1)];
+    if (te & 0x8000) te = S.sub[((te & 0x7FFF) << kSubBits) | ((buf >> kTabBits) & ((1u << kSubBits) - 1))];
+    const uint32_t sym = te >> 4;
+    const int l = te & 15;
+    buf >>= l;
+    cnt -= l;
+    bad |= (sym > 255u) | (l == 0);
+    return sym & 0xFF;
   };
   uint32_t i = s0;
   // 16 symbols -> one 16-byte store (segments are 16-byte aligned)

@@ -233,7 +233,6 @@ __global__ void __launch_bounds__(128) quant_pack_simt_kernel(const SegDesc *seg
   const float *xr = D + (valid ? tok : 0) * ldd + sd.col0;
   for (int gi = sd.g_begin; gi < sd.g_end; ++gi) {
     const GroupDesc gd = groups[gi];
-    // the SIMT reference handles split groups by scanning all pieces itself
     const float *xg = xr + gd.col - gd.part * gd.size;
     float mn = xg[0], mx = xg[0];
     for (int c = 1; c < gd.full_size; ++c) {
@@ -244,6 +243,75 @@ __global__ void __launch_bounds__(128) quant_pack_simt_kernel(const SegDesc *seg
     emit_group(xr + gd.col, gd.size, gd.full_size, gd.part, gd.type, gd.gidx, mn, mx, valid, row, lane, row & ~31,
                ntok, last, tile_base, cb);
   }
+}
+
+// ------------------------------------------------- wide groups (size k*256)
+// Block = one payload tile x one wide group; warp per token row: coalesced
+// float4 reads of the row's fp32 coefficients, warp min/max, then lane j packs
+// code words j, j+32, ... (Q2/Q3/Q5, R3/R4 via quant.cuh).
+__device__ __forceinline__ float4 load4(const float *p, bool vec) {
+  return vec ? *reinterpret_cast<const float4 *>(p) : make_float4(p[0], p[1], p[2], p[3]);
+}
+
+__global__ void __launch_bounds__(128) quant_wide_kernel(const WideDesc *wide, const float *D, int64_t ldd,
+                                                         int use_wcol, int64_t m, int64_t tile_bytes,
+                                                         const int64_t *codes_off_last, uint8_t *payload) {
+  const WideDesc wd = wide[blockIdx.x];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t m0 = int64_t(blockIdx.y) * kTileM;
+  const int ntok = int(m - m0 < kTileM ? m - m0 : kTileM);
+  const bool last = ntok < kTileM;
+  uint8_t *tile_base = payload + blockIdx.y * tile_bytes;
+  uint8_t *cb = tile_base + (last ? codes_off_last[wd.gidx] : wd.codes_off);
+  const int b = bits_of(wd.type);
+  const int per_word = 32 / b;
+  const int words = wd.size * b / 32;
+  const int64_t tok_bytes = int64_t(wd.size) * b / 8;
+  for (int r = warp; r < ntok; r += 4) {
+    const float *x = D + (m0 + r) * ldd + (use_wcol ? wd.wcol : wd.col);
+    const bool vec = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+    float mn = INFINITY, mx = -INFINITY;
+    for (int c = 4 * lane; c < wd.size; c += 128) {
+      const float4 v = load4(x + c, vec);
+      mn = fminf(fminf(mn, v.x), fminf(fminf(v.y, v.z), v.w));
+      mx = fmaxf(fmaxf(mx, v.x), fmaxf(fmaxf(v.y, v.z), v.w));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    uint16_t sh, sc;
+    group_factors(wd.type, mn, mx, sh, sc);
+    const float shift = f16_val(sh), scale = f16_val(sc);
+    if (lane == 0) {
+      uint8_t *pp = tile_base + 4 * (int64_t(wd.gidx) * ntok + r);
+      store_u32_any(pp, uint32_t(sh) | (uint32_t(sc) << 16), (reinterpret_cast<uintptr_t>(pp) & 3) == 0);
+    }
+    uint8_t *dst = cb + int64_t(r) * tok_bytes;
+    const bool al = (reinterpret_cast<uintptr_t>(dst) & 3) == 0;
+    for (int w = lane; w < words; w += 32) {
+      uint32_t word = 0;
+      for (int j = 0; j < per_word; j += 4) {
+        const float4 v = load4(x + w * per_word + j, vec);
+        word |= encode_one(wd.type, v.x, shift, scale) << (j * b);
+        word |= encode_one(wd.type, v.y, shift, scale) << ((j + 1) * b);
+        word |= encode_one(wd.type, v.z, shift, scale) << ((j + 2) * b);
+        word |= encode_one(wd.type, v.w, shift, scale) << ((j + 3) * b);
+      }
+      store_u32_any(dst + 4 * w, word, al);
+    }
+  }
+}
+
+kvtc_status launch_quant_wide(const WideDesc *wide, int32_t nwide, const float *D, int64_t ldd, int use_wcol,
+                              int64_t m, int64_t tile_bytes, const int64_t *codes_off_last, uint8_t *payload,
+                              cudaStream_t st) {
+  if (nwide == 0 || m == 0) return KVTC_OK;
+  dim3 grid(unsigned(nwide), unsigned(ceil_div(m, kTileM)));
+  quant_wide_kernel<<<grid, 128, 0, st>>>(wide, D, ldd, use_wcol, m, tile_bytes, codes_off_last, payload);
+  KVTC_LAUNCH_CHECK();
+  return KVTC_OK;
 }
 
 kvtc_status launch_quant_pack_simt(const SegDesc *segs, const GroupDesc *groups, int32_t nsegs, int32_t G,
@@ -258,19 +326,28 @@ kvtc_status launch_quant_pack_simt(const SegDesc *segs, const GroupDesc *groups,
 }
 
 // ---------------------------------------------------------------- dequant
-// Block = one tile x a run of kDqGroups groups.  For each group the block walks
-// the (token, code) pairs in the order the payload stores them (token-major,
-// code fastest), so code reads and D^ writes (the token's size_g consecutive
-// fp16) are both coalesced.  x^ = code*scale + shift in fp32 (fp8: e4m3(code)*
-// scale + shift), D^ = fp16(x^) (R5).
+// Block = one tile x a run of kDqGroups groups.  A thread owns 8 consecutive
+// codes of one token (every group size but 1 is a multiple of 8): one 2/4/8-byte
+// code read, the token's (shift, scale) read straight from the params section,
+// one 16-byte fp16 store when the column is 8-aligned.  x^ = code*scale + shift
+// in fp32 (fp8: e4m3(code)*scale + shift), D^ = fp16(x^) (R5).
 constexpr int kDqGroups = 8;
 constexpr int kDqThreads = 256;
+
+__device__ __forceinline__ uint64_t load_le(const uint8_t *p, int n) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  if (n == 8 && (a & 7) == 0) return *reinterpret_cast<const uint64_t *>(p);
+  if (n == 4 && (a & 3) == 0) return *reinterpret_cast<const uint32_t *>(p);
+  if (n == 2 && (a & 1) == 0) return *reinterpret_cast<const uint16_t *>(p);
+  uint64_t v = 0;
+  for (int i = 0; i < n; ++i) v |= uint64_t(p[i]) << (8 * i);
+  return v;
+}
 
 __global__ void __launch_bounds__(kDqThreads) dequant_kernel(const PlanGroup *groups, const int64_t *codes_off_full,
                                                              int32_t G, const int64_t *codes_off_last,
                                                              int64_t tile_bytes, const uint8_t *payload, int64_t m,
                                                              __half *Dh, int64_t ld) {
-  __shared__ float s_shift[kTileM], s_scale[kTileM];
   const int64_t m0 = int64_t(blockIdx.y) * kTileM;
   const int ntok = int(m - m0 < kTileM ? m - m0 : kTileM);
   const bool last = ntok < kTileM;
@@ -278,29 +355,49 @@ __global__ void __launch_bounds__(kDqThreads) dequant_kernel(const PlanGroup *gr
   const int g_end = min(G, int(blockIdx.x + 1) * kDqGroups);
   for (int g = blockIdx.x * kDqGroups; g < g_end; ++g) {
     const PlanGroup pg = groups[g];
-    __syncthreads();
-    for (int r = threadIdx.x; r < ntok; r += kDqThreads) {
-      const uint8_t *pp = tile + 4 * (int64_t(g) * ntok + r);
-      const uint16_t sh = uint16_t(pp[0]) | (uint16_t(pp[1]) << 8);
-      const uint16_t sc = uint16_t(pp[2]) | (uint16_t(pp[3]) << 8);
-      s_shift[r] = f16_val(sh);
-      s_scale[r] = f16_val(sc);
-    }
-    __syncthreads();
     const uint8_t *cb = tile + (last ? codes_off_last[g] : codes_off_full[g]);
+    const uint8_t *params = tile + 4 * int64_t(g) * ntok;
     const int b = bits_of(pg.type);
     const uint32_t mask = (1u << b) - 1;
+    const bool fp8 = pg.type == KVTC_T_FP8;
     const int size = pg.size;
-    const bool pow2 = (size & (size - 1)) == 0;
-    const int lg = pow2 ? __ffs(size) - 1 : 0;
-    const int n = ntok * size;
-    for (int e = threadIdx.x; e < n; e += kDqThreads) {
-      const int tau = pow2 ? (e >> lg) : e / size;
-      const int c = pow2 ? (e & (size - 1)) : e % size;
-      const int64_t bit = int64_t(e) * b;
-      const uint32_t code = (cb[bit >> 3] >> (bit & 7)) & mask;
-      const float v = pg.type == KVTC_T_FP8 ? e4m3_to_f32(uint8_t(code)) : float(code);
-      Dh[(m0 + tau) * ld + pg.col + c] = __float2half_rn(__fadd_rn(__fmul_rn(v, s_scale[tau]), s_shift[tau]));
+    if (size % 8 == 0) {
+      const int per_tok = size / 8;
+      const int n = ntok * per_tok;
+      const bool vec = (pg.col % 8 == 0) && (ld % 8 == 0);
+      for (int j = threadIdx.x; j < n; j += kDqThreads) {
+        const int tau = j / per_tok;
+        const int c0 = (j - tau * per_tok) * 8;
+        const uint32_t pr = uint32_t(load_le(params + 4 * tau, 4));
+        const float shift = f16_val(uint16_t(pr & 0xFFFF)), scale = f16_val(uint16_t(pr >> 16));
+        const uint64_t codes = load_le(cb + (int64_t(j) * 8 * b) / 8, b);     // 8 codes = b bytes
+        __align__(16) __half out[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t code = uint32_t(codes >> (k * b)) & mask;
+          const float v = fp8 ? e4m3_to_f32(uint8_t(code)) : float(code);
+          out[k] = __float2half_rn(__fadd_rn(__fmul_rn(v, scale), shift));
+        }
+        __half *dst = Dh + (m0 + tau) * ld + pg.col + c0;
+        if (vec) {
+          *reinterpret_cast<uint4 *>(dst) = *reinterpret_cast<const uint4 *>(out);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) dst[k] = out[k];
+        }
+      }
+    } else {
+      const int n = ntok * size;
+      for (int e = threadIdx.x; e < n; e += kDqThreads) {
+        const int tau = e / size;
+        const int c = e - tau * size;
+        const uint32_t pr = uint32_t(load_le(params + 4 * tau, 4));
+        const float shift = f16_val(uint16_t(pr & 0xFFFF)), scale = f16_val(uint16_t(pr >> 16));
+        const int64_t bit = int64_t(e) * b;
+        const uint32_t code = (cb[bit >> 3] >> (bit & 7)) & mask;
+        const float v = fp8 ? e4m3_to_f32(uint8_t(code)) : float(code);
+        Dh[(m0 + tau) * ld + pg.col + c] = __float2half_rn(__fadd_rn(__fmul_rn(v, scale), shift));
+      }
     }
   }
 }

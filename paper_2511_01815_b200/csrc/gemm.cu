@@ -3,8 +3,9 @@
 //   EPI_QUANT  K2  compress: D = X V_c - mu V_c and, straight from
 //                  TMEM, per-(token, group) min/max -> fp16 shift/scale -> codes
 //                  -> bit-pack into the §4 payload.  D never
-//                  reaches HBM.  Groups wider than one tile (1024) are split over
-//                  a thread-block cluster that exchanges row min/max through DSMEM.
+//                  reaches HBM, except the pieces of groups wider than one tile
+//                  (1024): those tiles store fp32 D to a scratch that
+//                  quant_wide_kernel quantises (its row min/max spans 4 tiles).
 //   EPI_F32        the same GEMM with an fp32 D output (DP coefficients, tests).
 //   EPI_RECON  K5  decompress: X^ = D^ V_d^T + mu, keys
 //                  re-rotated (RoPE, R7), bf16 RNE, scattered into a contiguous
@@ -19,8 +20,9 @@
 // Operands K-major, 128 B swizzled, 4-stage mbarrier ring; two fp32 TMEM
 // accumulators (2 x 256 columns) so the epilogue of tile i overlaps the MMAs of
 // tile i+1; EPI_QUANT quantises straight from TMEM (two passes per group).
-// Split-group launches (clusters) run one tile per CTA.
+// Pieces of groups wider than a tile store fp32 coefficients for quant_wide.
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.h"
 #include "quant.cuh"
@@ -58,7 +60,7 @@ struct Params {
   uint8_t *payload;
   const SegDesc *segs;
   const GroupDesc *groups;
-  int32_t parts;
+  int32_t parts;       // XTX: -2 marks pair tiling for the symmetric skip
   int32_t G;
   int64_t tile_bytes;
   const int64_t *codes_off_last;
@@ -73,17 +75,12 @@ struct Params {
   int32_t tile_n;      // RECON / F32 / XTX N tile
   int32_t a_hd;        // > 0: A is the 3-D cache map (GemmCompressArgs::a_hd)
   int64_t a_row0;
+  int32_t group_m;     // raster group (M-blocks or M-pairs)
+  int32_t hint_a, hint_b;   // L2 policies of the A / B loads
 };
 
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ float2 ld_peer_f2(const float2 *local, uint32_t cta) {
-  uint32_t a = smem_u32(local), ra;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(cta));
-  float2 v;
-  asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(ra) : "memory");
-  return v;
 }
 
 struct Tile {
@@ -113,10 +110,10 @@ __device__ __forceinline__ void load_cols(uint32_t trow, const float *bias, int 
 template <int MODE>
 __device__ __forceinline__ Tile tile_of(const Params &P, int64_t t, int num_mt) {
   Tile T;
-  const int64_t per_group = int64_t(kGroupM) * P.num_n;
+  const int64_t per_group = int64_t(P.group_m) * P.num_n;
   const int64_t g = t / per_group;
-  const int first = int(g * kGroupM);
-  const int gm = min(kGroupM, num_mt - first);
+  const int first = int(g * P.group_m);
+  const int gm = min(P.group_m, num_mt - first);
   const int64_t r = t - g * per_group;
   T.mb = first + int(r % gm);
   T.nb = int(r / gm);
@@ -173,6 +170,47 @@ __device__ __forceinline__ void tma_load_3d_pair(void *smem_dst, const CUtensorM
       "l"(reinterpret_cast<uint64_t>(m)), "r"(mbar), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+// L2 eviction-priority hints for TMA loads (0 none, 1 evict_first, 2 evict_last).
+__device__ __forceinline__ uint64_t l2_policy(int h) {
+  uint64_t p = 0;
+  if (h == 1) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  else if (h == 2) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tma_2d_hint(bool pair, void *smem_dst, const CUtensorMap *m, uint64_t *bar, int32_t c0,
+                                            int32_t c1, uint64_t pol) {
+  if (pair) {
+    const uint32_t mbar = smem_u32(bar) & 0xFEFFFFFFu;
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(mbar), "r"(c0), "r"(c1), "l"(pol)
+        : "memory");
+  } else {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, "
+        "{%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(pol)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tma_3d_hint(bool pair, void *smem_dst, const CUtensorMap *m, uint64_t *bar, int32_t c0,
+                                            int32_t c1, int32_t c2, uint64_t pol) {
+  if (pair) {
+    const uint32_t mbar = smem_u32(bar) & 0xFEFFFFFFu;
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(mbar), "r"(c0), "r"(c1), "r"(c2), "l"(pol)
+        : "memory");
+  } else {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, "
+        "{%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "l"(pol)
+        : "memory");
+  }
+}
 __device__ __forceinline__ void umma_f16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                               uint32_t accumulate) {
   asm volatile(
@@ -214,19 +252,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t *tmem_full = empty_bar + kStages;      // [2]
   uint64_t *tmem_empty = tmem_full + 2;           // [2]
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_empty + 2);
-  float2 *red = reinterpret_cast<float2 *>(smem + kStages * kStageBytes + 256);   // [128] row min/max
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const bool split = (MODE == EPI_QUANT) && P.parts > 1;
   const uint32_t rank = PAIR ? cluster_rank() : 0;
   const bool leader = rank == 0;
   // pairs: tiles are M-pairs (256 rows); CTA rank r holds M-block 2 mp + r
   const int num_mt = PAIR ? (P.num_m + 1) / 2 : P.num_m;
-  // split launches: exactly one tile per CTA (grid = pieces x M-blocks, clusters along x)
-  const int64_t total = split ? 1 : int64_t(num_mt) * P.num_n;
-  const int64_t t_first = split ? 0 : (PAIR ? blockIdx.x / 2 : blockIdx.x);
-  const int64_t t_step = split ? 1 : int64_t(PAIR ? gridDim.x / 2 : gridDim.x);
+  const int64_t total = int64_t(num_mt) * P.num_n;
+  const int64_t t_first = PAIR ? blockIdx.x / 2 : blockIdx.x;
+  const int64_t t_step = int64_t(PAIR ? gridDim.x / 2 : gridDim.x);
   const int num_kb = (P.K + kBlockK - 1) / kBlockK;
 
   if (threadIdx.x == 0) {
@@ -258,13 +293,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   auto get_tile = [&](int64_t t) {
-    if (split) {
-      Tile T;
-      T.mb = blockIdx.y;
-      T.nb = blockIdx.x;
-      T.valid = true;
-      return T;
-    }
     Tile T = tile_of<MODE>(P, t, num_mt);
     if (PAIR) T.mb = 2 * T.mb + int(rank);      // this CTA's M-block
     return T;
@@ -273,6 +301,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer
     uint32_t it = 0;
+    const uint64_t pol_a = l2_policy(P.hint_a);
+    const uint64_t pol_b = l2_policy(P.hint_b);
     for (int64_t t = t_first; t < total; t += t_step) {
       const Tile T = get_tile(t);
       if (!T.valid) continue;
@@ -284,24 +314,30 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (it >= kStages) mbar_wait(&empty_bar[s], ((it / kStages) - 1) & 1);
         uint8_t *a = tiles + s * kStageBytes;
         uint8_t *b = a + kABytes;
+        const int32_t ka = kb * kBlockK;
         if constexpr (PAIR) {
           // both CTAs' bytes land on the leader's barrier
           if (leader) mbar_arrive_expect_tx(&full_bar[s], 2 * kStageBytes);
-          if (P.a_hd)
-            tma_load_3d_pair(a, &tmA, &full_bar[s], (kb * kBlockK) % P.a_hd, int(P.a_row0) + T.mb * kTileM,
-                             (kb * kBlockK) / P.a_hd);
+          if (P.a_hd && P.hint_a)
+            tma_3d_hint(true, a, &tmA, &full_bar[s], ka % P.a_hd, int(P.a_row0) + T.mb * kTileM, ka / P.a_hd, pol_a);
+          else if (P.a_hd)
+            tma_load_3d_pair(a, &tmA, &full_bar[s], ka % P.a_hd, int(P.a_row0) + T.mb * kTileM, ka / P.a_hd);
+          else if (P.hint_a)
+            tma_2d_hint(true, a, &tmA, &full_bar[s], ka, T.mb * kTileM, pol_a);
           else
-            tma_load_2d_pair(a, &tmA, &full_bar[s], kb * kBlockK, T.mb * kTileM);
-          tma_load_2d_pair(b, &tmB, &full_bar[s], kb * kBlockK, n0 + int(rank) * (n_mma / 2));
+            tma_load_2d_pair(a, &tmA, &full_bar[s], ka, T.mb * kTileM);
+          if (P.hint_b)
+            tma_2d_hint(true, b, &tmB, &full_bar[s], ka, n0 + int(rank) * (n_mma / 2), pol_b);
+          else
+            tma_load_2d_pair(b, &tmB, &full_bar[s], ka, n0 + int(rank) * (n_mma / 2));
         } else {
           mbar_arrive_expect_tx(&full_bar[s], kStageBytes);
           if (P.a_hd)
-            tma_load_3d(a, &tmA, &full_bar[s], (kb * kBlockK) % P.a_hd, int(P.a_row0) + T.mb * kTileM,
-                        (kb * kBlockK) / P.a_hd);
+            tma_load_3d(a, &tmA, &full_bar[s], ka % P.a_hd, int(P.a_row0) + T.mb * kTileM, ka / P.a_hd);
           else
-            tma_load_2d(a, &tmA, &full_bar[s], kb * kBlockK, T.mb * kTileM);
-          tma_load_2d(b, &tmB, &full_bar[s], kb * kBlockK, n0);
-          tma_load_2d(b + kBBoxRows * 128, &tmB, &full_bar[s], kb * kBlockK, n0 + kBBoxRows);
+            tma_load_2d(a, &tmA, &full_bar[s], ka, T.mb * kTileM);
+          tma_load_2d(b, &tmB, &full_bar[s], ka, n0);
+          tma_load_2d(b + kBBoxRows * 128, &tmB, &full_bar[s], ka, n0 + kBBoxRows);
         }
       }
     }
@@ -387,6 +423,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool last = ntok < kTileM;
         uint8_t *tile_base = P.payload + T.mb * P.tile_bytes;
         const float *bias = P.bias + n0;
+        const int f32_col = P.segs[T.nb].f32_col;
+        if (f32_col >= 0) {
+          // piece of a wide group: fp32 D - mu V_c to the scratch
+          float *dst = P.D + (valid ? tok : 0) * P.ldd + f32_col;
+          for (int c = 0; c < ncols; c += 16) {
+            float x[16];
+            load_cols(trow, bias, c, 16, x);
+            if (valid) {
+#pragma unroll
+              for (int j = 0; j < 16; j += 4)
+                *reinterpret_cast<float4 *>(dst + c + j) = make_float4(x[j], x[j + 1], x[j + 2], x[j + 3]);
+            }
+          }
+        }
         for (int gi = seg_g0; gi < seg_g1; ++gi) {
           const GroupDesc gd = P.groups[gi];
           const int step = (gd.size % 16 == 0) ? 16 : 1;
@@ -398,17 +448,6 @@ __global__ void __launch_bounds__(kThreads, 1)
               mn = fminf(mn, x[j]);
               mx = fmaxf(mx, x[j]);
             }
-          }
-          if (split) {
-            // one piece per CTA; exchange row min/max over the cluster (DSMEM)
-            red[row] = make_float2(mn, mx);
-            cluster_sync_all();
-            for (int q = 0; q < P.parts; ++q) {
-              const float2 o = ld_peer_f2(&red[row], q);
-              mn = fminf(mn, o.x);
-              mx = fmaxf(mx, o.y);
-            }
-            cluster_sync_all();
           }
           uint16_t sh, sc;
           group_factors(gd.type, mn, mx, sh, sc);
@@ -535,12 +574,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       ++acc_it;
     }
   }
-  // split launches: the non-epilogue warps join the epilogue's two cluster barriers
-  if (split && warp < 4) {
-    __syncwarp();
-    cluster_sync_all();
-    cluster_sync_all();
-  }
   tc_fence_before();
   if constexpr (PAIR) {
     __syncwarp();
@@ -571,11 +604,21 @@ static kvtc_status launch(const CUtensorMap *tmA, const CUtensorMap *tmB, const 
   if (!configured) {
     KVTC_CUDA_TRY(
         cudaFuncSetAttribute(gemm_kernel<MODE, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-    if (MODE == EPI_QUANT)
-      KVTC_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<MODE, PAIR>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     configured = true;
   }
   if (grid.x == 0 || grid.y == 0) return KVTC_OK;
+  Params pp = p;
+  {
+    static const char *names[4] = {"KVTC_GROUP_M_F32", "KVTC_GROUP_M_QUANT", "KVTC_GROUP_M_RECON", "KVTC_GROUP_M_XTX"};
+    const char *e = getenv(names[MODE]);
+    // defaults from an ncu sweep at base clocks (scripts/sweep_env.py): fewer
+    // DRAM re-reads of the streamed operand
+    static const int defaults[4] = {kGroupM, 4, 16, kGroupM};
+    pp.group_m = e ? std::max(1, atoi(e)) : defaults[MODE];
+    const char *ha = getenv("KVTC_HINT_A"), *hb = getenv("KVTC_HINT_B");
+    if (ha) pp.hint_a = atoi(ha);
+    if (hb) pp.hint_b = atoi(hb);
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(kThreads);
@@ -588,7 +631,7 @@ static kvtc_status launch(const CUtensorMap *tmA, const CUtensorMap *tmB, const 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  KVTC_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_kernel<MODE, PAIR>, *tmA, *tmB, p));
+  KVTC_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_kernel<MODE, PAIR>, *tmA, *tmB, pp));
   note_launch();
   return KVTC_OK;
 }
@@ -621,7 +664,6 @@ kvtc_status launch_gemm_project_quant(const GemmCompressArgs &a, cudaStream_t st
   p.payload = a.payload;
   p.segs = a.segs;
   p.groups = a.groups;
-  p.parts = a.parts;
   p.G = a.G;
   p.tile_bytes = a.tile_bytes;
   p.codes_off_last = a.codes_off_last;
@@ -630,8 +672,8 @@ kvtc_status launch_gemm_project_quant(const GemmCompressArgs &a, cudaStream_t st
   p.a_row0 = a.a_row0;
   p.num_m = int32_t(ceil_div(a.m, kTileM));
   p.num_n = a.nsegs;
-  if (a.parts > 1)   // split groups: one tile per CTA, clusters along x
-    return launch<EPI_QUANT, false>(a.tmA, a.tmB, p, dim3(unsigned(a.nsegs), unsigned(p.num_m)), a.parts, st);
+  p.D = a.D;
+  p.ldd = a.ldd;
   return launch<EPI_QUANT, true>(a.tmA, a.tmB, p, dim3(pair_grid(int64_t((p.num_m + 1) / 2) * p.num_n)), 2, st);
 }
 

@@ -31,6 +31,18 @@ struct SegDesc {
   int32_t col0;       // first compacted column of the tile
   int32_t width;      // columns used
   int32_t g_begin, g_end;  // GroupDesc range
+  int32_t f32_col;    // >= 0: a 256-column piece of a wide group; the epilogue
+                      // stores D - mu V_c (fp32) at this column of the wide scratch
+};
+// A group wider than one tile (size = k * 256): quantised after the GEMM from
+// its fp32 coefficients (quant_wide_kernel).
+struct WideDesc {
+  int32_t gidx;       // index among non-None groups (params slot)
+  int32_t size, type;
+  int32_t col;        // compacted column (D [m x r_nz])
+  int32_t wcol;       // column in the wide scratch [m x wide_cols]
+  int32_t pad;
+  int64_t codes_off;  // code block offset in a FULL tile
 };
 
 // Operands of a (basis, plan) pair, compacted to the plan's non-None PCs.
@@ -61,15 +73,14 @@ struct GemmCompressArgs {
   int32_t K;               // p
   int64_t m;
   const float *bias;       // [r_nz]
-  // mode F32
-  float *D;                // [m x ldd]
+  // mode F32: D [m x ldd]; mode quantise: the wide-group scratch [m x ldd]
+  float *D;
   int64_t ldd;
   // mode quantise
   uint8_t *payload;
   const SegDesc *segs;
   const GroupDesc *groups;
   int32_t nsegs;
-  int32_t parts;           // cluster size along x (1 = unsplit)
   int32_t G;               // number of non-None groups
   int64_t tile_bytes;      // bytes of a full tile
   const int64_t *codes_off_last;  // [G] code-block offsets of the last partial tile
@@ -112,6 +123,9 @@ kvtc_status launch_gather(const kvtc_kv_view &v, __nv_bfloat16 *const *layer_bas
 kvtc_status launch_gather_rows(const kvtc_kv_view *seqs, int32_t nseq, __nv_bfloat16 *const *bases_dev,
                                const int64_t *rows_dev, int64_t n, const float *invf_dev, int32_t unrope,
                                int32_t pairing, int64_t ld, __nv_bfloat16 *X, cudaStream_t st);
+// Wide groups: D [m x ldd] fp32; column of group w = use_wcol ? wcol : col.
+kvtc_status launch_quant_wide(const WideDesc *wide, int32_t nwide, const float *D, int64_t ldd, int use_wcol, int64_t m,
+                              int64_t tile_bytes, const int64_t *codes_off_last, uint8_t *payload, cudaStream_t st);
 kvtc_status launch_quant_pack_simt(const SegDesc *segs, const GroupDesc *groups, int32_t nsegs, int32_t G,
                                    const float *D, int64_t ldd, int64_t m, int64_t tile_bytes,
                                    const int64_t *codes_off_last, uint8_t *payload, cudaStream_t st);
