@@ -120,7 +120,7 @@ __global__ void plan_operands_kernel(const int32_t *pc, int r_nz, int p, int r_p
   if (i >= int64_t(p) * r_nz) return;
   const int j = int(i / p), f = int(i % p);
   const int src = pc[j];
-  VcT[int64_t(j) * p + f] = VcT_full[int64_t(src) * p + f];
+  VcT[int64_t(j) * (p + kXPad) + f] = VcT_full[int64_t(src) * p + f];
   Vd[int64_t(f) * r_nz_pad + j] = Vd_full[int64_t(f) * r_pad_full + src];
   if (f == 0) bias[j] = bias_full[src];
 }
@@ -382,7 +382,8 @@ kvtc_status plan_operands(const kvtc_basis *b, kvtc_plan *pl, const Operands **o
       int32_t *d_pc = nullptr;
       KVTC_CUDA_TRY(cudaMalloc(&d_pc, pc.size() * 4));
       KVTC_CUDA_TRY(cudaMemcpy(d_pc, pc.data(), pc.size() * 4, cudaMemcpyHostToDevice));
-      KVTC_CUDA_TRY(cudaMalloc(&op.VcT, int64_t(op.r_nz) * b->p * 2));
+      KVTC_CUDA_TRY(cudaMalloc(&op.VcT, int64_t(op.r_nz) * (b->p + kXPad) * 2));
+      KVTC_CUDA_TRY(cudaMemset(op.VcT, 0, int64_t(op.r_nz) * (b->p + kXPad) * 2));
       KVTC_CUDA_TRY(cudaMalloc(&op.Vd, int64_t(b->p) * op.r_nz_pad * 2));
       KVTC_CUDA_TRY(cudaMalloc(&op.bias, op.r_nz * 4));
       KVTC_CUDA_TRY(cudaMemset(op.Vd, 0, int64_t(b->p) * op.r_nz_pad * 2));
@@ -392,7 +393,7 @@ kvtc_status plan_operands(const kvtc_basis *b, kvtc_plan *pl, const Operands **o
       KVTC_CUDA_TRY(cudaDeviceSynchronize());
       cudaFree(d_pc);
       kvtc_status st = make_tmap_2d(&op.tm_VcT, op.VcT, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, b->p, op.r_nz,
-                                    uint64_t(b->p) * 2, kBlockK, kMaxTileN / 2);
+                                    uint64_t(b->p + kXPad) * 2, kBlockK, kMaxTileN / 2);
       if (st != KVTC_OK) return st;
       st = make_tmap_2d(&op.tm_Vd, op.Vd, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, op.r_nz, b->p, uint64_t(op.r_nz_pad) * 2,
                         kBlockK, kMaxTileN / 2);

@@ -50,9 +50,9 @@ kvtc_status rope_table_for(const kvtc_basis *b, int64_t pos_first, int64_t m, fl
   return launch_rope_table(b->d_invf, b->shape.head_dim / 2, pos_first, m, cs, st);
 }
 
-kvtc_status tmap_X(CUtensorMap *m, const void *X, int64_t rows, int64_t p) {
-  return make_tmap_2d(m, X, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, uint64_t(p), uint64_t(rows), uint64_t(p) * 2, kBlockK,
-                      kTileM);
+kvtc_status tmap_X(CUtensorMap *m, const void *X, int64_t rows, int64_t p, int64_t ld = 0) {
+  return make_tmap_2d(m, X, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, uint64_t(p), uint64_t(rows), uint64_t(ld ? ld : p) * 2,
+                      kBlockK, kTileM);
 }
 
 // A contiguous cache whose layers sit at a constant positive stride can be read
@@ -80,12 +80,12 @@ bool direct_view_map(const kvtc_kv_view &v, int64_t tok0, CUtensorMap *m) {
 // the plan's wide groups (nullptr if it has none).
 kvtc_status run_project_quant(const kvtc_basis *b, kvtc_plan *pl, const Operands *op, const void *X, int64_t m,
                               uint8_t *payload, float *wide, cudaStream_t st, const CUtensorMap *direct = nullptr,
-                              int64_t tok0 = 0) {
+                              int64_t tok0 = 0, int64_t ldx = 0) {
   if (m == 0 || pl->G == 0) return KVTC_OK;
   KVTC_CHECK_ARG(pl->nwide == 0 || wide, "wide-group scratch");
   CUtensorMap tA;
   kvtc_status s = KVTC_OK;
-  if (!direct && (s = tmap_X(&tA, X, m, b->p))) return s;
+  if (!direct && (s = tmap_X(&tA, X, m, b->p, ldx))) return s;
   GemmCompressArgs a = {};
   a.tmA = direct ? direct : &tA;
   if (direct) {
@@ -147,24 +147,29 @@ kvtc_status run_reconstruct(const kvtc_basis *b, const kvtc_plan *pl, const Oper
 
 // Library-internal side stream (one per device) used to overlap the integer
 // codec kernels (DEFLATE / inflate / dequantise) with the tensor-core GEMMs of
-// the other stream: a persistent GEMM CTA (197 KB smem, 256 threads) leaves room
-// on every SM for one codec CTA.  Fork/join with events on the caller's stream.
+// the other stream: a persistent GEMM CTA (196 KB smem, 256 threads) leaves 32 KB
+// on every SM, room for two codec CTAs of a bounded grid (corun_ctas(2)).
+// Fork/join with events on the caller's stream.
 struct SideStream {
   cudaStream_t s = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 };
 SideStream *side_stream() {
-  static std::mutex mu;
-  static SideStream per_dev[16];
+  // per host thread and device: concurrent callers never share the fork/join events
+  static thread_local SideStream per_dev[16];
   int dev = 0;
   cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lk(mu);
   SideStream &S = per_dev[dev & 15];
   if (!S.s) {
     cudaStreamCreateWithFlags(&S.s, cudaStreamNonBlocking);
     for (auto &e : S.ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
   }
   return &S;
+}
+
+bool env_flag(const char *name, bool dflt) {
+  const char *e = getenv(name);
+  return e ? e[0] == '1' : dflt;
 }
 
 // KVTC_NO_OVERLAP=1 runs the codec kernels on the caller's stream (measurements).
@@ -387,11 +392,12 @@ extern "C" size_t kvtc_compress_workspace_bytes(const kvtc_basis *kb, const kvtc
   b.take<void *>(k->shape.layers);
   b.take<void *>(k->shape.layers);
   b.take<uint64_t>(8);
-  b.take<__nv_bfloat16>(L.m * kb->p);
+  b.take<__nv_bfloat16>(L.m * (kb->p + kXPad));
   b.take<float2>(L.m * (kb->shape.head_dim / 2));
   b.take<uint8_t>(L.pay[0] + 16);
   b.take<uint8_t>(L.pay[1] + 16);
-  b.take<uint8_t>(deflate_workspace(std::max(L.pay[0], L.pay[1]), pol->chunk_bytes));
+  b.take<uint8_t>(deflate_workspace(L.pay[0], pol->chunk_bytes));
+  b.take<uint8_t>(deflate_workspace(L.pay[1], pol->chunk_bytes));
   b.take<float>(L.m * std::max(kp->wide_cols, vp->wide_cols));
   return b.used + 256;
 }
@@ -429,12 +435,15 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
   auto *kbases = ws.take<__nv_bfloat16 *>(k->shape.layers);
   auto *vbases = ws.take<__nv_bfloat16 *>(k->shape.layers);
   uint64_t *lens = ws.take<uint64_t>(8);     // [0..1] section lengths, [2..3] section offsets
-  auto *X = ws.take<__nv_bfloat16>(L.m * kb->p);
+  const int64_t ldx = kb->p + kXPad;
+  auto *X = ws.take<__nv_bfloat16>(L.m * ldx);
   float2 *cs = ws.take<float2>(L.m * (kb->shape.head_dim / 2));
   uint8_t *payload_k = ws.take<uint8_t>(L.pay[0] + 16);
   uint8_t *payload_v = ws.take<uint8_t>(L.pay[1] + 16);
-  const size_t dws = deflate_workspace(std::max(L.pay[0], L.pay[1]), pol->chunk_bytes);
-  void *dwsp = ws.take<uint8_t>(dws);
+  const size_t dws[2] = {deflate_workspace(L.pay[0], pol->chunk_bytes), deflate_workspace(L.pay[1], pol->chunk_bytes)};
+  void *dwsp[2];
+  dwsp[0] = ws.take<uint8_t>(dws[0]);
+  dwsp[1] = ws.take<uint8_t>(dws[1]);
   float *wide = ws.take<float>(L.m * std::max(kp->wide_cols, vp->wide_cols));
   if ((s = upload_bases(k, kbases, st)) || (s = upload_bases(v, vbases, st))) return s;
 
@@ -487,45 +496,81 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
     return KVTC_NOTHING_TO_COMPRESS;
   }
   KVTC_CUDA_TRY(cudaMemcpyAsync(lens + 2, &h.section_off[0], 8, cudaMemcpyHostToDevice, st));
-  // ---- keys: un-RoPE gather (K1) -> fused projection + quantisation (K2); the
-  // keys' DEFLATE (K3) then runs on the side stream while the values' gather and
-  // GEMM run on the caller's stream, and the values' DEFLATE follows it there.
+  // Schedule: the tensor-core GEMMs run back to back on the
+  // caller's stream; the HBM/integer kernels of the OTHER stream run beside them
+  // on the side stream with bounded grids (2 CTAs per SM next to the persistent
+  // GEMM CTA).  With a contiguous value cache read in place by the GEMM:
+  //   st : V GEMM --------------------------> K GEMM -> K DEFLATE -> assemble
+  //   aux: K un-RoPE gather -> (after V GEMM)  V DEFLATE ------------^
+  // Otherwise X is shared: K gather -> K GEMM -> V gather -> V GEMM -> V DEFLATE,
+  // with the keys' DEFLATE beside the values' gather/GEMM.  Each stream's
+  // encoder writes its own slots; the sections are assembled at the end (K first).
   SideStream *ss = side_stream();
-  cudaStream_t aux = overlap_off() ? st : ss->s;
-  {
-    ProfScope ps("c.gather_unrope", st);
-    if ((s = rope_table_for(kb, k->pos0 + pol->sinks, L.m, cs, st))) return s;
-    if ((s = launch_gather(*k, kbases, pol->sinks, L.m, cs, kb->pairing, X, st))) return s;
-  }
-  {
-    ProfScope ps("c.project_quant_gemm", st);
-    if ((s = run_project_quant(kb, kpl, kop, X, L.m, payload_k, wide, st))) return s;
-  }
-  KVTC_CUDA_TRY(cudaEventRecord(ss->ev[0], st));
-  KVTC_CUDA_TRY(cudaStreamWaitEvent(aux, ss->ev[0], 0));
-  {
-    ProfScope ps("c.deflate_overlapped", aux);
-    if ((s = launch_deflate(payload_k, L.pay[0], pol->chunk_bytes, o, lens + 2, lens + 0, dwsp, dws, aux))) return s;
-  }
-  offset_after_kernel<<<1, 1, 0, aux>>>(lens + 2, lens + 0, lens + 3, o);
-  KVTC_LAUNCH_CHECK();
-  // ---- values: read in place when the cache layout allows it
+  const bool ovl = !overlap_off();
+  cudaStream_t aux = ovl ? ss->s : st;
+  const int side_ctas = ovl ? corun_ctas(2) : 0;
   CUtensorMap tV;
   const bool v_direct = !direct_off() && direct_view_map(*v, pol->sinks, &tV);
-  if (!v_direct) {
-    ProfScope ps("c.gather", st);
-    if ((s = launch_gather(*v, vbases, pol->sinks, L.m, nullptr, 0, X, st))) return s;
-  }
-  {
+  auto gather_keys = [&](cudaStream_t q, int ctas, const char *tag) -> kvtc_status {
+    ProfScope ps(tag, q);
+    kvtc_status r = rope_table_for(kb, k->pos0 + pol->sinks, L.m, cs, q);
+    if (r) return r;
+    return launch_gather(*k, kbases, pol->sinks, L.m, cs, kb->pairing, X, q, ctas, ldx);
+  };
+  auto gemm = [&](int sv, bool direct) -> kvtc_status {
     ProfScope ps("c.project_quant_gemm", st);
-    if ((s = run_project_quant(vb, vpl, vop, X, L.m, payload_v, wide, st, v_direct ? &tV : nullptr, pol->sinks)))
+    return sv ? run_project_quant(vb, vpl, vop, X, L.m, payload_v, wide, st, direct ? &tV : nullptr, pol->sinks, ldx)
+              : run_project_quant(kb, kpl, kop, X, L.m, payload_k, wide, st, nullptr, 0, ldx);
+  };
+  auto encode = [&](int sv, cudaStream_t q, int ctas, const char *tag) -> kvtc_status {
+    ProfScope ps(tag, q);
+    return launch_deflate_encode(sv ? payload_v : payload_k, L.pay[sv], pol->chunk_bytes, dwsp[sv], dws[sv], ctas, q);
+  };
+  KVTC_CUDA_TRY(cudaEventRecord(ss->ev[0], st));                 // fork point: bases, raw tokens
+  if (v_direct) {
+    // tuning knobs (scripts/sweep_env.py): KVTC_C_GATHER_SIDE=0 runs the keys'
+    // gather before the values' GEMM instead of beside it; KVTC_C_DEFLATE_SIDE=0
+    // runs both encoders after the GEMMs instead of the values' beside the keys' GEMM
+    const bool gather_side = ovl && env_flag("KVTC_C_GATHER_SIDE", true);
+    const bool deflate_side = ovl && env_flag("KVTC_C_DEFLATE_SIDE", true);
+    if (!gather_side && (s = gather_keys(st, 0, "c.gather_unrope"))) return s;
+    if ((s = gemm(1, true))) return s;
+    KVTC_CUDA_TRY(cudaEventRecord(ss->ev[2], st));               // V payload ready
+    if (gather_side) {
+      KVTC_CUDA_TRY(cudaStreamWaitEvent(aux, ss->ev[0], 0));
+      if ((s = gather_keys(aux, corun_ctas(3), "c.gather_unrope_overlapped"))) return s;
+      KVTC_CUDA_TRY(cudaEventRecord(ss->ev[1], aux));            // X (keys) ready
+      KVTC_CUDA_TRY(cudaStreamWaitEvent(st, ss->ev[1], 0));
+    }
+    if ((s = gemm(0, false))) return s;
+    if (deflate_side) {
+      KVTC_CUDA_TRY(cudaStreamWaitEvent(aux, ss->ev[2], 0));
+      if ((s = encode(1, aux, side_ctas, "c.deflate_overlapped"))) return s;
+    } else if ((s = encode(1, st, 0, "c.deflate"))) {
       return s;
+    }
+    if ((s = encode(0, st, 0, "c.deflate"))) return s;
+  } else {
+    if ((s = gather_keys(st, 0, "c.gather_unrope"))) return s;
+    if ((s = gemm(0, false))) return s;
+    KVTC_CUDA_TRY(cudaEventRecord(ss->ev[2], st));               // K payload ready
+    {
+      ProfScope ps("c.gather", st);
+      if ((s = launch_gather(*v, vbases, pol->sinks, L.m, nullptr, 0, X, st, 0, ldx))) return s;
+    }
+    if ((s = gemm(1, false))) return s;
+    KVTC_CUDA_TRY(cudaStreamWaitEvent(aux, ss->ev[2], 0));
+    if ((s = encode(0, aux, side_ctas, ovl ? "c.deflate_overlapped" : "c.deflate"))) return s;
+    if ((s = encode(1, st, 0, "c.deflate"))) return s;
   }
-  KVTC_CUDA_TRY(cudaEventRecord(ss->ev[1], aux));
-  KVTC_CUDA_TRY(cudaStreamWaitEvent(st, ss->ev[1], 0));          // join: K section written, V offset known
+  KVTC_CUDA_TRY(cudaEventRecord(ss->ev[3], aux));
+  KVTC_CUDA_TRY(cudaStreamWaitEvent(st, ss->ev[3], 0));          // join: both streams encoded
   {
-    ProfScope ps("c.deflate", st);
-    if ((s = launch_deflate(payload_v, L.pay[1], pol->chunk_bytes, o, lens + 3, lens + 1, dwsp, dws, st))) return s;
+    ProfScope ps("c.assemble", st);
+    if ((s = launch_deflate_assemble(L.pay[0], pol->chunk_bytes, dwsp[0], o, lens + 2, lens + 0, st))) return s;
+    offset_after_kernel<<<1, 1, 0, st>>>(lens + 2, lens + 0, lens + 3, o);
+    KVTC_LAUNCH_CHECK();
+    if ((s = launch_deflate_assemble(L.pay[1], pol->chunk_bytes, dwsp[1], o, lens + 3, lens + 1, st))) return s;
   }
   header_kernel<<<1, 1, 0, st>>>(h, o, lens, lens + 2);
   KVTC_LAUNCH_CHECK();
@@ -649,35 +694,35 @@ extern "C" kvtc_status kvtc_decompress(const kvtc_basis *kb, const kvtc_plan *kp
   // device copy of the section offsets lives in the container header itself
   const uint64_t *sec_off_dev = reinterpret_cast<const uint64_t *>(ib + offsetof(ContainerHeader, section_off));
   if (kb->has_rope && (s = rope_table_for(kb, h.pos0 + h.sinks, h.m, cs, st))) return s;
-  // keys: inflate -> dequantise -> GEMM on the caller's stream; values: inflate ->
-  // dequantise on the side stream (overlapping the keys' GEMM), then their GEMM.
-  // The values' inflate waits for the keys' inflate (which then has the whole GPU:
-  // it is latency-bound and two concurrent inflates each run at half speed).
+  // Both streams' DEFLATE sections are inflated by ONE full-grid launch (the
+  // inflater is latency-bound: as a bounded side-stream grid it ran 3-5x slower
+  // and delayed the values' GEMM); then keys: dequantise -> GEMM on the caller's
+  // stream, values: dequantise on the side stream (bounded grid, beside the keys'
+  // GEMM, enqueued after it) -> GEMM.
   SideStream *ss = side_stream();
-  cudaStream_t aux = overlap_off() ? st : ss->s;
+  const bool ovl = !overlap_off();
+  cudaStream_t aux = ovl ? ss->s : st;
   __half *Dhs[2] = {Dh, Dh_v};
-  for (int sv = 0; sv < 2; ++sv) {
-    cudaStream_t cs_ = sv ? aux : st;
-    kvtc_plan *pl = const_cast<kvtc_plan *>(sv ? vp : kp);
-    const uint32_t nch = uint32_t((h.payload_bytes[sv] + h.chunk_bytes - 1) / h.chunk_bytes);
-    {
-      ProfScope ps(sv ? "d.inflate_overlapped" : "d.inflate", cs_);
-      if ((s = launch_inflate_section(ib, sec_off_dev + sv, h.payload_bytes[sv], nch, payloads[sv], err, cs_)))
-        return s;
-    }
-    if (sv == 0) {
-      KVTC_CUDA_TRY(cudaEventRecord(ss->ev[2], st));             // header/bases/err ready, keys inflated
-      KVTC_CUDA_TRY(cudaStreamWaitEvent(aux, ss->ev[2], 0));
-    }
-    {
-      ProfScope ps(sv ? "d.dequant_overlapped" : "d.dequant", cs_);
-      if ((s = launch_dequant(pl->d_pgroups, pl->d_codes_off_full, pl->G, plan_codes_off_last(pl, h.m % kTileM),
-                              pl->tile_bytes, payloads[sv], h.m, Dhs[sv], ld, cs_)))
-        return s;
-      if (pl->r_nz == 0) KVTC_CUDA_TRY(cudaMemsetAsync(Dhs[sv], 0, h.m * ld * 2, cs_));
-    }
+  {
+    ProfScope ps("d.inflate", st);
+    uint32_t nch[2];
+    for (int sv = 0; sv < 2; ++sv) nch[sv] = uint32_t((h.payload_bytes[sv] + h.chunk_bytes - 1) / h.chunk_bytes);
+    if ((s = launch_inflate_sections(ib, sec_off_dev, h.payload_bytes[0], nch[0], payloads[0], sec_off_dev + 1,
+                                     h.payload_bytes[1], nch[1], payloads[1], err, st)))
+      return s;
   }
-  KVTC_CUDA_TRY(cudaEventRecord(ss->ev[3], aux));
+  auto expand = [&](int sv, cudaStream_t q, int ctas) -> kvtc_status {
+    kvtc_plan *pl = const_cast<kvtc_plan *>(sv ? vp : kp);
+    ProfScope ps(sv && ovl ? "d.dequant_overlapped" : "d.dequant", q);
+    kvtc_status r;
+    if ((r = launch_dequant(pl->d_pgroups, pl->d_codes_off_full, pl->G, plan_codes_off_last(pl, h.m % kTileM),
+                            pl->tile_bytes, payloads[sv], h.m, Dhs[sv], ld, q, ctas)))
+      return r;
+    if (pl->r_nz == 0) KVTC_CUDA_TRY(cudaMemsetAsync(Dhs[sv], 0, h.m * ld * 2, q));
+    return KVTC_OK;
+  };
+  if ((s = expand(0, st, 0))) return s;
+  KVTC_CUDA_TRY(cudaEventRecord(ss->ev[2], st));                 // header/bases/err ready, keys expanded
   for (int sv = 0; sv < 2; ++sv) {
     const kvtc_basis *b = sv ? vb : kb;
     kvtc_plan *pl = const_cast<kvtc_plan *>(sv ? vp : kp);
@@ -685,10 +730,15 @@ extern "C" kvtc_status kvtc_decompress(const kvtc_basis *kb, const kvtc_plan *kp
     __nv_bfloat16 *const *bs = sv ? vbases : kbases;
     const Operands *op;
     if ((s = plan_operands(b, pl, &op))) return s;
-    if (sv == 1) KVTC_CUDA_TRY(cudaStreamWaitEvent(st, ss->ev[3], 0));   // join
+    if (sv == 1) KVTC_CUDA_TRY(cudaStreamWaitEvent(st, ss->ev[3], 0));   // join: values expanded
     {
       ProfScope ps("d.reconstruct_gemm", st);
       if ((s = run_reconstruct(b, pl, op, Dhs[sv], ld, h.m, h.sinks, layer_begin, layer_end, vw, bs, cs, st))) return s;
+    }
+    if (sv == 0) {
+      KVTC_CUDA_TRY(cudaStreamWaitEvent(aux, ss->ev[2], 0));
+      if ((s = expand(1, aux, ovl ? corun_ctas(2) : 0))) return s;
+      KVTC_CUDA_TRY(cudaEventRecord(ss->ev[3], aux));
     }
     const __nv_bfloat16 *raw = sv ? rawv : rawk;
     {

@@ -46,6 +46,9 @@ void note_launch();
   } while (0)
 
 constexpr int kTileM = 128;        // tokens per tile (and per payload tile, §4)
+constexpr int kXPad = 64;          // row padding (elements) of the K-major GEMM operands X and V_c^T:
+                                   // p * 2 B = 64 KiB row strides map every row of a TMA box to the
+                                   // same L2 set (ncu: 50 % hit rate); +128 B spreads them
 constexpr int kBlockK = 64;        // 64 x 16-bit = 128 B rows: one SWIZZLE_128B atom
 constexpr int kMaxTileN = 256;     // UMMA N limit for cta_group::1, M = 128
 

@@ -26,6 +26,7 @@
 // {u64 offset, u32 bytes, u32 kind}, segment index [nchunks][64] u16 (bit
 // length of each 1/64 of the chunk's symbols; segment 0 starts right after the
 // block header), then the chunk streams, each starting 4-byte aligned.
+#include <cub/block/block_radix_sort.cuh>
 #include <cub/block/block_scan.cuh>
 
 #include "internal.h"
@@ -194,27 +195,16 @@ struct BitWriter {
   }
 };
 
-__device__ void rank_sort(const uint32_t *freq, int nsym, int *sorted, int *nz_out) {
-  // parallel rank sort of symbols with freq > 0 by (freq, symbol); all threads call
-  for (int s = threadIdx.x; s < nsym; s += blockDim.x) {
-    const uint32_t f = freq[s];
-    if (f == 0) continue;
-    int rank = 0;
-    for (int j = 0; j < nsym; ++j) {
-      const uint32_t g = freq[j];
-      if (g != 0 && (g < f || (g == f && j < s))) rank++;
-    }
-    sorted[rank] = s;
-  }
-  if (threadIdx.x == 0) {
-    int nz = 0;
-    for (int s = 0; s < nsym; ++s) nz += freq[s] != 0;
-    *nz_out = nz;
-  }
-}
+
+constexpr int kSortItems = 5;                       // 64 x 5 >= 257 sort keys
+using EncSort = cub::BlockRadixSort<uint32_t, kEncThreads, kSortItems>;
 
 struct EncShared {
-  uint32_t whist[kEncThreads / 32][kLitSyms + 3];   // warp-private histograms
+  union {
+    uint32_t whist[kEncThreads / 32][kLitSyms + 3];   // warp-private histograms
+    typename EncSort::TempStorage sort;               // (freq, symbol) radix sort, after the merge
+  } u;
+  uint32_t skeys[kEncThreads * kSortItems];         // sorted (freq << 9 | symbol) keys
   uint32_t hist[kLitSyms + 3];
   uint32_t clhist[19];
   int sorted[kLitSyms + 3];
@@ -290,12 +280,9 @@ struct WordWriter {
   }
 };
 
-__global__ void __launch_bounds__(kEncThreads, 14) deflate_encode_kernel(const uint8_t *in, uint64_t n, int32_t chunk,
-                                                                        uint8_t *slots, uint64_t stride,
-                                                                        uint32_t *chunk_bytes, uint32_t *chunk_kind,
-                                                                        uint16_t *index) {
-  __shared__ EncShared S;
-  const int c = blockIdx.x;
+__device__ __forceinline__ void encode_chunk(EncShared &S, const int c, const uint8_t *in, uint64_t n, int32_t chunk,
+                                             uint8_t *slots, uint64_t stride, uint32_t *chunk_bytes,
+                                             uint32_t *chunk_kind, uint16_t *index) {
   const uint64_t base = uint64_t(c) * chunk;
   const uint32_t nc = uint32_t(umin64(chunk, n - base));
   const uint8_t *src = in + base;
@@ -305,7 +292,7 @@ __global__ void __launch_bounds__(kEncThreads, 14) deflate_encode_kernel(const u
   const uint32_t piece = uint32_t(chunk) / kEncThreads;
   const uint32_t p0 = umin32(nc, t * piece), p1 = umin32(nc, (t + 1) * piece);
 
-  for (int s = t; s < (kEncThreads / 32) * (kLitSyms + 3); s += kEncThreads) (&S.whist[0][0])[s] = 0;
+  for (int s = t; s < (kEncThreads / 32) * (kLitSyms + 3); s += kEncThreads) (&S.u.whist[0][0])[s] = 0;
   if (t < 19) S.clhist[t] = 0;
   for (int i = t; i < 160; i += kEncThreads) S.hdr[i] = 0;
   __syncthreads();
@@ -313,7 +300,7 @@ __global__ void __launch_bounds__(kEncThreads, 14) deflate_encode_kernel(const u
   {
     const bool aligned = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
     const uint32_t nvec = aligned ? nc / 16 : 0;
-    uint32_t *h = S.whist[warp];
+    uint32_t *h = S.u.whist[warp];
     for (uint32_t v = t; v < nvec; v += kEncThreads) {
       const uint4 q = __ldg(reinterpret_cast<const uint4 *>(src) + v);
       const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
@@ -326,13 +313,30 @@ __global__ void __launch_bounds__(kEncThreads, 14) deflate_encode_kernel(const u
   for (int s = t; s < kLitSyms; s += kEncThreads) {
     uint32_t v = 0;
 #pragma unroll
-    for (int w = 0; w < kEncThreads / 32; ++w) v += S.whist[w][s];
+    for (int w = 0; w < kEncThreads / 32; ++w) v += S.u.whist[w][s];
     S.hist[s] = v;
   }
   __syncthreads();
   if (t == 0) S.hist[256] = 1;  // end-of-block
   __syncthreads();
-  rank_sort(S.hist, kLitSyms, S.sorted, &S.nz);
+  // symbols by (freq, symbol) ascending: one radix sort of unique 26-bit keys
+  // (freq <= 2^16 + 1, symbol < 512); zero-frequency symbols sort first.
+  {
+    uint32_t keys[kSortItems];
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) {
+      const int sym = t * kSortItems + i;
+      keys[i] = sym < kLitSyms ? (S.hist[sym] << 9) | uint32_t(sym) : 0x3FFFFFFu;
+    }
+    EncSort(S.u.sort).Sort(keys, 0, 26);
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) S.skeys[t * kSortItems + i] = keys[i];
+  }
+  __syncthreads();
+  for (int i = t; i < kLitSyms; i += kEncThreads)
+    if ((S.skeys[i] >> 9) != 0 && (i == 0 || (S.skeys[i - 1] >> 9) == 0)) S.nz = kLitSyms - i;
+  __syncthreads();
+  for (int j = t; j < S.nz; j += kEncThreads) S.sorted[j] = int(S.skeys[kLitSyms - S.nz + j] & 511u);
   __syncthreads();
   if (t == 0) {
     build_lengths_s(S.hist, S.sorted, S.nz, kMaxBits, S.len, kLitSyms, S.work, S.num);
@@ -484,12 +488,28 @@ __global__ void __launch_bounds__(kEncThreads, 14) deflate_encode_kernel(const u
         ++w;
       }
     };
+    // two codes (<= 15 bits each) per accumulator step: nb < 32 before, < 62 after
+    auto put2 = [&](uint32_t e0, uint32_t e1) {
+      const uint32_t l0 = e0 >> 16;
+      acc |= uint64_t((e0 & 0xFFFF) | ((e1 & 0xFFFF) << l0)) << nb;
+      nb += l0 + (e1 >> 16);
+      if (nb >= 32) {
+        const uint32_t word = uint32_t(acc);
+        if (edge || w == w_last) atomicOr(&ow[w], word);
+        else ow[w] = word;
+        edge = false;
+        acc >>= 32;
+        nb -= 32;
+        ++w;
+      }
+    };
     if (vec) {
       for (uint32_t i = p0; i < p1; i += 16) {
         const uint4 q = __ldg(reinterpret_cast<const uint4 *>(src + i));
         const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-        for (int k = 0; k < 16; ++k) put(S.sym[(w4[k >> 2] >> (8 * (k & 3))) & 0xFF]);
+        for (int k = 0; k < 16; k += 2)
+          put2(S.sym[__byte_perm(w4[k >> 2], 0, 0x4440 | (k & 3))], S.sym[__byte_perm(w4[k >> 2], 0, 0x4440 | ((k + 1) & 3))]);
       }
     } else {
       for (uint32_t i = p0; i < p1; ++i) put(S.sym[src[i]]);
@@ -500,6 +520,20 @@ __global__ void __launch_bounds__(kEncThreads, 14) deflate_encode_kernel(const u
   if (t == 0) {
     chunk_bytes[c] = (S.total_bits + 7) / 8;
     chunk_kind[c] = 0;
+  }
+}
+
+// Grid-stride over chunks: the full grid (one CTA per chunk, ~14 per SM) when the
+// encoder has the GPU, or a bounded grid (a few CTAs per SM) when it runs beside
+// a persistent GEMM on the side stream, so the GEMM CTA always fits.
+__global__ void __launch_bounds__(kEncThreads, 14) deflate_encode_kernel(const uint8_t *in, uint64_t n, int32_t chunk,
+                                                                        uint32_t nch, uint8_t *slots, uint64_t stride,
+                                                                        uint32_t *chunk_bytes, uint32_t *chunk_kind,
+                                                                        uint16_t *index) {
+  __shared__ EncShared S;
+  for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
+    encode_chunk(S, int(c), in, n, chunk, slots, stride, chunk_bytes, chunk_kind, index);
+    __syncthreads();
   }
 }
 
@@ -565,27 +599,67 @@ __global__ void section_copy_kernel(const uint8_t *slots, uint64_t stride, const
   }
 }
 
-kvtc_status launch_deflate(const uint8_t *in, size_t n, int32_t chunk, uint8_t *out, const uint64_t *off_dev,
-                           uint64_t *section_len_dev, void *ws, size_t ws_bytes, cudaStream_t st) {
+namespace {
+struct DeflateWs {
+  uint32_t nch;
+  uint64_t stride;
+  uint8_t *slots;
+  uint32_t *cbytes, *ckind;
+  uint16_t *index;
+};
+DeflateWs deflate_ws(size_t n, int32_t chunk, void *ws) {
+  DeflateWs w;
+  w.nch = uint32_t((n + chunk - 1) / chunk);
+  w.stride = slot_stride(chunk);
+  w.slots = static_cast<uint8_t *>(ws);
+  w.cbytes = reinterpret_cast<uint32_t *>(w.slots + w.nch * w.stride);
+  w.ckind = w.cbytes + w.nch;
+  w.index = reinterpret_cast<uint16_t *>(w.ckind + w.nch);
+  return w;
+}
+}  // namespace
+
+int corun_ctas(int per_sm) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms * per_sm;
+}
+
+kvtc_status launch_deflate_encode(const uint8_t *in, size_t n, int32_t chunk, void *ws, size_t ws_bytes,
+                                  int32_t max_ctas, cudaStream_t st) {
   KVTC_CHECK_ARG(chunk == 16384 || chunk == 32768 || chunk == 65536, "chunk_bytes must be 16/32/64 KiB");
   KVTC_CHECK_ARG(ws_bytes >= deflate_workspace(n, chunk), "deflate workspace");
-  const uint32_t nch = uint32_t((n + chunk - 1) / chunk);
-  const uint64_t stride = slot_stride(chunk);
-  uint8_t *slots = static_cast<uint8_t *>(ws);
-  uint32_t *cbytes = reinterpret_cast<uint32_t *>(slots + nch * stride);
-  uint32_t *ckind = cbytes + nch;
-  uint16_t *index = reinterpret_cast<uint16_t *>(ckind + nch);
-  if (nch > 0) {
-    deflate_encode_kernel<<<nch, kEncThreads, 0, st>>>(in, n, chunk, slots, stride, cbytes, ckind, index);
-    KVTC_LAUNCH_CHECK();
-  }
-  section_layout_kernel<<<1, 1024, 0, st>>>(cbytes, ckind, nch, n, chunk, out, off_dev, section_len_dev);
+  const DeflateWs w = deflate_ws(n, chunk, ws);
+  if (w.nch == 0) return KVTC_OK;
+  const uint32_t grid = max_ctas > 0 ? std::min<uint32_t>(w.nch, uint32_t(max_ctas)) : w.nch;
+  KVTC_MAX_CARVEOUT(deflate_encode_kernel);
+  deflate_encode_kernel<<<grid, kEncThreads, 0, st>>>(in, n, chunk, w.nch, w.slots, w.stride, w.cbytes, w.ckind,
+                                                      w.index);
   KVTC_LAUNCH_CHECK();
-  if (nch > 0) {
-    section_copy_kernel<<<nch, 256, 0, st>>>(slots, stride, index, nch, out, off_dev);
+  return KVTC_OK;
+}
+
+kvtc_status launch_deflate_assemble(size_t n, int32_t chunk, const void *ws, uint8_t *out, const uint64_t *off_dev,
+                                    uint64_t *section_len_dev, cudaStream_t st) {
+  const DeflateWs w = deflate_ws(n, chunk, const_cast<void *>(ws));
+  section_layout_kernel<<<1, 1024, 0, st>>>(w.cbytes, w.ckind, w.nch, n, chunk, out, off_dev, section_len_dev);
+  KVTC_LAUNCH_CHECK();
+  if (w.nch > 0) {
+    section_copy_kernel<<<w.nch, 256, 0, st>>>(w.slots, w.stride, w.index, w.nch, out, off_dev);
     KVTC_LAUNCH_CHECK();
   }
   return KVTC_OK;
+}
+
+kvtc_status launch_deflate(const uint8_t *in, size_t n, int32_t chunk, uint8_t *out, const uint64_t *off_dev,
+                           uint64_t *section_len_dev, void *ws, size_t ws_bytes, cudaStream_t st) {
+  kvtc_status s = launch_deflate_encode(in, n, chunk, ws, ws_bytes, 0, st);
+  if (s) return s;
+  return launch_deflate_assemble(n, chunk, ws, out, off_dev, section_len_dev, st);
 }
 
 // ================================================================ decoders
@@ -808,10 +882,9 @@ __device__ int parse_header_fast(FastShared &S) {
   return 0;
 }
 
-__global__ void __launch_bounds__(kInfThreads) inflate_fast_kernel(InflateJobs J, int32_t *err) {
-  __shared__ FastShared S;
-  const int job = blockIdx.x < J.nch[0] ? 0 : 1;
-  const uint32_t c = job == 0 ? blockIdx.x : blockIdx.x - J.nch[0];
+__device__ __forceinline__ void inflate_chunk(FastShared &S, const uint32_t b, const InflateJobs &J, int32_t *err) {
+  const int job = b < J.nch[0] ? 0 : 1;
+  const uint32_t c = job == 0 ? b : b - J.nch[0];
   const uint8_t *section = J.base + (J.off_dev[job] ? *J.off_dev[job] : 0);
   const SectionHeader *hdr = reinterpret_cast<const SectionHeader *>(section);
   const int tid = threadIdx.x;
@@ -893,14 +966,20 @@ __global__ void __launch_bounds__(kInfThreads) inflate_fast_kernel(InflateJobs J
   uint64_t wi = pos >> 5;
   uint64_t buf = uint64_t(__ldg(words + wi++)) >> (pos & 31);
   int cnt = 32 - int(pos & 31);
-  uint32_t nextw = wi < wend ? __ldg(words + wi) : 0u;   // one word of read-ahead
-  ++wi;
+  // three words of read-ahead in flight per lane (each lane streams its own
+  // segment, so loads are not coalesced: hide their latency instead)
+  uint32_t nw0 = wi < wend ? __ldg(words + wi) : 0u;
+  uint32_t nw1 = wi + 1 < wend ? __ldg(words + wi + 1) : 0u;
+  uint32_t nw2 = wi + 2 < wend ? __ldg(words + wi + 2) : 0u;
+  wi += 3;
   bool bad = false;
   auto next_sym = [&]() -> uint32_t {
     if (cnt <= 32) {
-      buf |= uint64_t(nextw) << cnt;
+      buf |= uint64_t(nw0) << cnt;
       cnt += 32;
-      nextw = wi < wend ? __ldg(words + wi) : 0u;
+      nw0 = nw1;
+      nw1 = nw2;
+      nw2 = wi < wend ? __ldg(words + wi) : 0u;
       ++wi;
     }
     uint32_t te = S.table[buf & ((1u << kTabBits) - 1)];
@@ -925,9 +1004,20 @@ __global__ void __launch_bounds__(kInfThreads) inflate_fast_kernel(InflateJobs J
   if (bad) atomicExch(err, -7);
 }
 
+// Grid-stride over the chunks of both jobs (full grid alone; bounded grid
+// beside a persistent GEMM, see deflate_encode_kernel).
+__global__ void __launch_bounds__(kInfThreads) inflate_fast_kernel(InflateJobs J, int32_t *err) {
+  __shared__ FastShared S;
+  const uint32_t total = J.nch[0] + J.nch[1];
+  for (uint32_t b = blockIdx.x; b < total; b += gridDim.x) {
+    inflate_chunk(S, b, J, err);
+    __syncthreads();
+  }
+}
+
 kvtc_status launch_inflate_sections(const uint8_t *base, const uint64_t *off_dev0, uint64_t n0, uint32_t nch0,
                                     uint8_t *out0, const uint64_t *off_dev1, uint64_t n1, uint32_t nch1,
-                                    uint8_t *out1, int32_t *err, cudaStream_t st) {
+                                    uint8_t *out1, int32_t *err, cudaStream_t st, int32_t max_ctas) {
   InflateJobs J;
   J.base = base;
   J.off_dev[0] = off_dev0;
@@ -939,14 +1029,16 @@ kvtc_status launch_inflate_sections(const uint8_t *base, const uint64_t *off_dev
   J.out[0] = out0;
   J.out[1] = out1;
   if (nch0 + nch1 == 0) return KVTC_OK;
-  inflate_fast_kernel<<<nch0 + nch1, kInfThreads, 0, st>>>(J, err);
+  const uint32_t grid = max_ctas > 0 ? std::min<uint32_t>(nch0 + nch1, uint32_t(max_ctas)) : nch0 + nch1;
+  KVTC_MAX_CARVEOUT(inflate_fast_kernel);
+  inflate_fast_kernel<<<grid, kInfThreads, 0, st>>>(J, err);
   KVTC_LAUNCH_CHECK();
   return KVTC_OK;
 }
 
 kvtc_status launch_inflate_section(const uint8_t *base, const uint64_t *off_dev, uint64_t n_out, uint32_t nchunks,
-                                   uint8_t *out, int32_t *err, cudaStream_t st) {
-  return launch_inflate_sections(base, off_dev, n_out, nchunks, out, nullptr, 0, 0, nullptr, err, st);
+                                   uint8_t *out, int32_t *err, cudaStream_t st, int32_t max_ctas) {
+  return launch_inflate_sections(base, off_dev, n_out, nchunks, out, nullptr, 0, 0, nullptr, err, st, max_ctas);
 }
 
 // Validates a section header (host copy) against the expected payload size.

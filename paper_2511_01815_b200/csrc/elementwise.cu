@@ -56,24 +56,16 @@ struct GatherArgs {
   int64_t tok_begin, ntok;
   const float2 *cs;  // [ntok x d/2] or null (values)
   __nv_bfloat16 *X;
+  int64_t ldx;       // row stride of X (elements, >= layers * heads * d)
 };
 
-__global__ void gather_kernel(GatherArgs a) {
-  const int vec_per_head = a.d / 16;  // threads per head (each: 8 lo + 8 hi elements)
-  const int64_t per_tok = int64_t(a.layers) * a.heads * vec_per_head;
-  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (i >= per_tok * a.ntok) return;
-  const int64_t r = i / per_tok;
-  int64_t rem = i % per_tok;
-  const int layer = int(rem / (a.heads * vec_per_head));
-  rem %= (a.heads * vec_per_head);
-  const int head = int(rem / vec_per_head);
-  const int v = int(rem % vec_per_head);
+__device__ __forceinline__ void gather_unit(const GatherArgs &a, const int64_t r, const int layer, const int head,
+                                            const int v) {
   const int64_t tok = a.tok_begin + r;
   const int64_t slot = view_slot(a.layout, a.page_tokens, a.block_table, tok);
   const int hd = a.heads * a.d;
   const __nv_bfloat16 *src = a.bases[layer] + slot * hd + head * a.d;
-  __nv_bfloat16 *dst = a.X + r * (int64_t(a.layers) * hd) + int64_t(layer) * hd + head * a.d;
+  __nv_bfloat16 *dst = a.X + r * a.ldx + int64_t(layer) * hd + head * a.d;
   if (a.pairing == 0) {
     const int j0 = v * 8;  // low-half offset
     uint4 lo = *reinterpret_cast<const uint4 *>(src + j0);
@@ -111,8 +103,27 @@ __global__ void gather_kernel(GatherArgs a) {
   }
 }
 
+// Grid-stride over (token, layer, head, 16-element piece) units; a bounded grid
+// when it overlaps a persistent GEMM (codec.cu).  32-bit index math (the launcher
+// falls back to 64-bit only past 2^32 units).
+template <typename Idx>
+__global__ void __launch_bounds__(256) gather_kernel(GatherArgs a, Idx total) {
+  const Idx vph = Idx(a.d / 16);                      // threads per head (8 lo + 8 hi elements each)
+  const Idx per_layer = Idx(a.heads) * vph;
+  const Idx per_tok = Idx(a.layers) * per_layer;
+  for (Idx i = Idx(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += Idx(gridDim.x) * blockDim.x) {
+    const Idx r = i / per_tok;
+    Idx rem = i - r * per_tok;
+    const Idx layer = rem / per_layer;
+    rem -= layer * per_layer;
+    const Idx head = rem / vph;
+    gather_unit(a, int64_t(r), int(layer), int(head), int(rem - head * vph));
+  }
+}
+
 kvtc_status launch_gather(const kvtc_kv_view &v, __nv_bfloat16 *const *layer_base_dev, int64_t tok_begin,
-                          int64_t ntok, const float2 *cs, int32_t pairing, __nv_bfloat16 *X, cudaStream_t st) {
+                          int64_t ntok, const float2 *cs, int32_t pairing, __nv_bfloat16 *X, cudaStream_t st,
+                          int32_t max_ctas, int64_t ldx) {
   GatherArgs a;
   a.bases = layer_base_dev;
   a.layout = v.layout;
@@ -126,9 +137,19 @@ kvtc_status launch_gather(const kvtc_kv_view &v, __nv_bfloat16 *const *layer_bas
   a.ntok = ntok;
   a.cs = cs;
   a.X = X;
+  a.ldx = ldx > 0 ? ldx : int64_t(v.shape.layers) * v.shape.kv_heads * v.shape.head_dim;
   const int64_t total = ntok * v.shape.layers * v.shape.kv_heads * (v.shape.head_dim / 16);
   if (total == 0) return KVTC_OK;
-  gather_kernel<<<unsigned(ceil_div(total, 256)), 256, 0, st>>>(a);
+  int64_t grid = ceil_div(total, 256);
+  if (max_ctas > 0) grid = std::min<int64_t>(grid, max_ctas);
+  grid = std::min<int64_t>(grid, int64_t(1) << 30);
+  if (total < (int64_t(1) << 32) - int64_t(grid) * 256) {
+    KVTC_MAX_CARVEOUT(gather_kernel<uint32_t>);
+    gather_kernel<uint32_t><<<unsigned(grid), 256, 0, st>>>(a, uint32_t(total));
+  } else {
+    KVTC_MAX_CARVEOUT(gather_kernel<uint64_t>);
+    gather_kernel<uint64_t><<<unsigned(grid), 256, 0, st>>>(a, uint64_t(total));
+  }
   KVTC_LAUNCH_CHECK();
   return KVTC_OK;
 }
@@ -348,12 +369,16 @@ __global__ void __launch_bounds__(kDqThreads) dequant_kernel(const PlanGroup *gr
                                                              int32_t G, const int64_t *codes_off_last,
                                                              int64_t tile_bytes, const uint8_t *payload, int64_t m,
                                                              __half *Dh, int64_t ld) {
-  const int64_t m0 = int64_t(blockIdx.y) * kTileM;
+  const int64_t gx = (G + kDqGroups - 1) / kDqGroups;
+  const int64_t nblk = gx * ((m + kTileM - 1) / kTileM);
+  for (int64_t bid = blockIdx.x; bid < nblk; bid += gridDim.x) {
+  const int64_t by = bid / gx, bx = bid - by * gx;
+  const int64_t m0 = by * kTileM;
   const int ntok = int(m - m0 < kTileM ? m - m0 : kTileM);
   const bool last = ntok < kTileM;
-  const uint8_t *tile = payload + blockIdx.y * tile_bytes;
-  const int g_end = min(G, int(blockIdx.x + 1) * kDqGroups);
-  for (int g = blockIdx.x * kDqGroups; g < g_end; ++g) {
+  const uint8_t *tile = payload + by * tile_bytes;
+  const int g_end = min(G, int(bx + 1) * kDqGroups);
+  for (int g = int(bx) * kDqGroups; g < g_end; ++g) {
     const PlanGroup pg = groups[g];
     const uint8_t *cb = tile + (last ? codes_off_last[g] : codes_off_full[g]);
     const uint8_t *params = tile + 4 * int64_t(g) * ntok;
@@ -400,14 +425,18 @@ __global__ void __launch_bounds__(kDqThreads) dequant_kernel(const PlanGroup *gr
       }
     }
   }
+  }
 }
 
 kvtc_status launch_dequant(const PlanGroup *groups_dev, const int64_t *codes_off_full, int32_t G,
                            const int64_t *codes_off_last, int64_t tile_bytes, const uint8_t *payload, int64_t m,
-                           __half *Dh, int64_t ld, cudaStream_t st) {
+                           __half *Dh, int64_t ld, cudaStream_t st, int32_t max_ctas) {
   if (G == 0 || m == 0) return KVTC_OK;
-  dim3 grid(unsigned(ceil_div(G, kDqGroups)), unsigned(ceil_div(m, kTileM)));
-  dequant_kernel<<<grid, kDqThreads, 0, st>>>(groups_dev, codes_off_full, G, codes_off_last, tile_bytes, payload, m,
+  int64_t grid = ceil_div(G, kDqGroups) * ceil_div(m, kTileM);
+  if (max_ctas > 0) grid = std::min<int64_t>(grid, max_ctas);
+  grid = std::min<int64_t>(grid, int64_t(1) << 30);
+  KVTC_MAX_CARVEOUT(dequant_kernel);
+  dequant_kernel<<<unsigned(grid), kDqThreads, 0, st>>>(groups_dev, codes_off_full, G, codes_off_last, tile_bytes, payload, m,
                                                Dh, ld);
   KVTC_LAUNCH_CHECK();
   return KVTC_OK;

@@ -22,6 +22,7 @@
 // tile i+1; EPI_QUANT quantises straight from TMEM (two passes per group).
 // Pieces of groups wider than a tile store fp32 coefficients for quant_wide.
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 
 #include "internal.h"
@@ -77,6 +78,7 @@ struct Params {
   int64_t a_row0;
   int32_t group_m;     // raster group (M-blocks or M-pairs)
   int32_t hint_a, hint_b;   // L2 policies of the A / B loads
+  unsigned long long *tile_sync;   // non-null: producers align tile starts (see tile_barrier)
 };
 
 __device__ __forceinline__ void cluster_sync_all() {
@@ -236,6 +238,24 @@ __device__ __forceinline__ void mbar_arrive_remote(uint64_t *local_bar, uint32_t
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
 }
 
+// Soft tile barrier of the TMA producers: the CTAs of one wave of tiles share
+// their A / B k-blocks through L2 only while they stay in step; a producer
+// that is ahead waits (bounded spin, never a hang) before its s-th tile until
+// every CTA has started its s-th tile.  target(s) counts the CTAs that have an
+// s-th tile under the static schedule.
+__device__ __forceinline__ void tile_barrier(unsigned long long *ctr, int64_t s, int64_t total, int64_t n_units,
+                                             int per_unit) {
+  const int64_t full = total / n_units, rem = total % n_units;
+  const int64_t target = int64_t(per_unit) * (n_units * min(s + 1, full) + (s + 1 > full ? rem : 0));
+  atomicAdd(ctr, 1ull);
+  unsigned long long v;
+  for (int spin = 0; spin < (1 << 21); ++spin) {
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+    if (int64_t(v) >= target) break;
+    __nanosleep(100);
+  }
+}
+
 template <int MODE, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -303,9 +323,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t it = 0;
     const uint64_t pol_a = l2_policy(P.hint_a);
     const uint64_t pol_b = l2_policy(P.hint_b);
+    int64_t seq = 0;
     for (int64_t t = t_first; t < total; t += t_step) {
       const Tile T = get_tile(t);
       if (!T.valid) continue;
+      if (MODE != EPI_XTX && P.tile_sync) tile_barrier(P.tile_sync, seq++, total, t_step, PAIR ? 2 : 1);
       int n0, ncols, g0, g1;
       tile_geometry<MODE>(P, T, n0, ncols, g0, g1);
       const int n_mma = (ncols + 15) & ~15;
@@ -604,6 +626,9 @@ static kvtc_status launch(const CUtensorMap *tmA, const CUtensorMap *tmB, const 
   if (!configured) {
     KVTC_CUDA_TRY(
         cudaFuncSetAttribute(gemm_kernel<MODE, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    // the 228 KB configuration, shared with the side-stream kernels (internal.h)
+    KVTC_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<MODE, PAIR>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                       int(cudaSharedmemCarveoutMaxShared)));
     configured = true;
   }
   if (grid.x == 0 || grid.y == 0) return KVTC_OK;
@@ -618,6 +643,15 @@ static kvtc_status launch(const CUtensorMap *tmA, const CUtensorMap *tmB, const 
     const char *ha = getenv("KVTC_HINT_A"), *hb = getenv("KVTC_HINT_B");
     if (ha) pp.hint_a = atoi(ha);
     if (hb) pp.hint_b = atoi(hb);
+    const char *ts = getenv("KVTC_TILE_SYNC");
+    if (ts && (atoi(ts) >> MODE) & 1) {
+      // one zeroed counter per launch from a ring of 4096 (launches in flight never share one)
+      static unsigned long long *ring = nullptr;
+      static std::atomic<uint32_t> next{0};
+      if (!ring) KVTC_CUDA_TRY(cudaMalloc(&ring, 4096 * sizeof(unsigned long long)));
+      pp.tile_sync = ring + (next.fetch_add(1) % 4096);
+      KVTC_CUDA_TRY(cudaMemsetAsync(pp.tile_sync, 0, sizeof(unsigned long long), st));
+    }
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;

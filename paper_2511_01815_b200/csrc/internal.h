@@ -2,6 +2,7 @@
 // translation units (not part of the ABI).
 #pragma once
 
+#include <algorithm>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -48,7 +49,7 @@ struct WideDesc {
 // Operands of a (basis, plan) pair, compacted to the plan's non-None PCs.
 struct Operands {
   int32_t r_nz = 0, r_nz_pad = 0;
-  __nv_bfloat16 *VcT = nullptr;  // [r_nz x p]  rows = PCs (compress B operand, K-major)
+  __nv_bfloat16 *VcT = nullptr;  // [r_nz x (p + kXPad)]  rows = PCs (compress B operand, K-major)
   float *bias = nullptr;         // [r_nz] mu V_c (fp32)
   __half *Vd = nullptr;          // [p x r_nz_pad] (decompress B operand, K-major)
   CUtensorMap tm_VcT, tm_Vd;
@@ -119,7 +120,8 @@ kvtc_status launch_gemm_xtx(const CUtensorMap *tmA, const CUtensorMap *tmB, int3
 kvtc_status launch_rope_table(const float *invf_dev, int32_t half, int64_t pos_first, int64_t n, float2 *cs,
                               cudaStream_t st);
 kvtc_status launch_gather(const kvtc_kv_view &v, __nv_bfloat16 *const *layer_base_dev, int64_t tok_begin,
-                          int64_t ntok, const float2 *cs, int32_t pairing, __nv_bfloat16 *X, cudaStream_t st);
+                          int64_t ntok, const float2 *cs, int32_t pairing, __nv_bfloat16 *X, cudaStream_t st,
+                          int32_t max_ctas = 0, int64_t ldx = 0);   // ldx 0: dense rows (p)
 kvtc_status launch_gather_rows(const kvtc_kv_view *seqs, int32_t nseq, __nv_bfloat16 *const *bases_dev,
                                const int64_t *rows_dev, int64_t n, const float *invf_dev, int32_t unrope,
                                int32_t pairing, int64_t ld, __nv_bfloat16 *X, cudaStream_t st);
@@ -133,7 +135,7 @@ kvtc_status launch_codes_off_last(const int32_t *gsize, const int32_t *gbits, in
                                   int64_t *out, cudaStream_t st);
 kvtc_status launch_dequant(const PlanGroup *groups_dev, const int64_t *codes_off_full, int32_t G,
                            const int64_t *codes_off_last, int64_t tile_bytes, const uint8_t *payload, int64_t m,
-                           __half *Dh, int64_t ld, cudaStream_t st);
+                           __half *Dh, int64_t ld, cudaStream_t st, int32_t max_ctas = 0);
 kvtc_status launch_copy_tokens(const kvtc_kv_view &src, __nv_bfloat16 *const *src_bases, int64_t src_tok,
                                const kvtc_kv_view &dst, __nv_bfloat16 *const *dst_bases, int64_t dst_tok,
                                int64_t ntok, int32_t layer_begin, int32_t layer_end, cudaStream_t st);
@@ -152,13 +154,35 @@ size_t deflate_workspace(size_t n, int32_t chunk);
 // The section is written at out + (off_dev ? *off_dev : 0) (device offset).
 kvtc_status launch_deflate(const uint8_t *in, size_t n, int32_t chunk, uint8_t *out, const uint64_t *off_dev,
                            uint64_t *section_len_dev, void *ws, size_t ws_bytes, cudaStream_t st);
+// Two phases of launch_deflate: chunk encoder into the workspace slots (max_ctas
+// > 0 bounds the grid so the kernel can run beside a persistent GEMM), then the
+// section layout + copy to out (workspace untouched in between).
+kvtc_status launch_deflate_encode(const uint8_t *in, size_t n, int32_t chunk, void *ws, size_t ws_bytes,
+                                  int32_t max_ctas, cudaStream_t st);
+kvtc_status launch_deflate_assemble(size_t n, int32_t chunk, const void *ws, uint8_t *out, const uint64_t *off_dev,
+                                    uint64_t *section_len_dev, cudaStream_t st);
+// SM count x per_sm: the bounded grid of a side-stream kernel overlapping a GEMM.
+int corun_ctas(int per_sm);
+// Kernels that share an SM must run under the same shared-memory carveout: the
+// persistent GEMMs (196 KB) and every kernel that overlaps them on the side
+// stream request the maximum (228 KB), which leaves 32 KB next to a GEMM CTA.
+// (Without it ncu shows 196 / 32 / 228 KB configs and the side kernels wait for
+// the GEMM to finish.)
+#define KVTC_MAX_CARVEOUT(kernel)                                                                     \
+  do {                                                                                              \
+    static const bool kvtc_carveout_set_ = (cudaFuncSetAttribute(reinterpret_cast<const void *>(kernel), \
+                                                                 cudaFuncAttributePreferredSharedMemoryCarveout, \
+                                                                 int(cudaSharedmemCarveoutMaxShared)),  \
+                                            true);                                                  \
+    (void)kvtc_carveout_set_;                                                                       \
+  } while (0)
 kvtc_status launch_inflate_section(const uint8_t *base, const uint64_t *off_dev, uint64_t n_out, uint32_t nchunks,
-                                   uint8_t *out, int32_t *err, cudaStream_t st);
+                                   uint8_t *out, int32_t *err, cudaStream_t st, int32_t max_ctas = 0);
 kvtc_status check_section_header(const void *hdr_host, size_t len, size_t n_out, uint32_t *nchunks);
 // Both streams' sections in one launch (warp per chunk); sections at base + *off_dev.
 kvtc_status launch_inflate_sections(const uint8_t *base, const uint64_t *off_dev0, uint64_t n0, uint32_t nch0,
                                     uint8_t *out0, const uint64_t *off_dev1, uint64_t n1, uint32_t nch1,
-                                    uint8_t *out1, int32_t *err, cudaStream_t st);
+                                    uint8_t *out1, int32_t *err, cudaStream_t st, int32_t max_ctas = 0);
 constexpr size_t kSectionHeaderBytes = 64;
 kvtc_status launch_inflate_raw(const uint8_t *in, const int64_t *in_off, const int64_t *in_len, int32_t n,
                                uint8_t *out, const int64_t *out_off, const int64_t *out_len, int32_t *status,

@@ -35,7 +35,8 @@ def main():
     dws = torch.empty(K.decompress_workspace_bytes(kb, kp, vb, vp, cont[:256].cpu().numpy().tobytes()),
                       dtype=torch.uint8, device="cuda")
     base = dict(os.environ)
-    for var in ["baseline"] + args.variants + ["baseline"]:
+    order = ["baseline"] + [x for v in args.variants for x in (v, "baseline")]
+    for var in order:
         os.environ.clear()
         os.environ.update(base)
         if var != "baseline":
@@ -57,7 +58,7 @@ def main():
         st = K.profile_read()
         K.profile_enable(False)
         step = e0.elapsed_time(e1) / args.iters
-        parts = " ".join(f"{k}={v[0] / args.iters:.2f}" for k, v in st.items() if "gemm" in k)
+        parts = " ".join(f"{k}={v[0] / args.iters:.2f}" for k, v in st.items())
         print(f"[sweep] {var:40s} step={step:.2f} ms {parts}", flush=True)
 
 
