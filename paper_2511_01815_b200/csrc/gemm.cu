@@ -12,18 +12,22 @@
 //                  or paged cache.
 //   EPI_XTX    K6  calibration: S += C^T C over a chunk of rows.
 //
-// Persistent kernel, one CTA per SM: tiles of 128 x N (N <= 256) are handed out
-// statically in a grouped raster (kGroupM M-blocks x all N tiles) so that the
-// ~148 tiles in flight share A and B tiles in L2 and stay in lock-step.  Warp
-// roles: warp 0 TMA producer, warp 1 single-thread tcgen05.mma issuer, warp 2
-// TMEM allocator, warps 4-7 epilogue (warp w reads TMEM lanes 32*(w%4)..+31).
-// Operands K-major, 128 B swizzled, 4-stage mbarrier ring; two fp32 TMEM
-// accumulators (2 x 256 columns) so the epilogue of tile i overlaps the MMAs of
-// tile i+1; EPI_QUANT quantises straight from TMEM (two passes per group).
-// Pieces of groups wider than a tile store fp32 coefficients for quant_wide.
+// Persistent kernel, one CTA pair (cta_group::2, M = 256) per 2 SMs: tiles are
+// handed out statically in a grouped raster (group_m M-pairs x all N tiles) so
+// that the ~74 tiles in flight share A and B k-blocks in L2.  Sharing only works
+// while the CTAs stay in step (K = p = 32768 makes one tile's operands 2 x 16.8
+// MB), so the TMA producers meet at a soft barrier before every tile
+// (tile_barrier): ncu showed 23-37 GB of DRAM reads per compress launch without
+// it.  Warp roles: warp 0 TMA producer, warp 1 single-thread tcgen05.mma issuer
+// (pair leader), warp 2 TMEM allocator, warps 4-7 epilogue (warp w reads TMEM
+// lanes 32*(w%4)..+31).  Operands K-major, 128 B swizzled, 6-stage mbarrier ring;
+// two fp32 TMEM accumulators (2 x 256 columns) so the epilogue of tile i overlaps
+// the MMAs of tile i+1; EPI_QUANT quantises straight from TMEM (two passes per
+// group).  Pieces of groups wider than a tile store fp32 coefficients for
+// quant_wide.
 #include <algorithm>
-#include <atomic>
 #include <cstdlib>
+#include <mutex>
 
 #include "internal.h"
 #include "quant.cuh"
@@ -243,16 +247,29 @@ __device__ __forceinline__ void mbar_arrive_remote(uint64_t *local_bar, uint32_t
 // that is ahead waits (bounded spin, never a hang) before its s-th tile until
 // every CTA has started its s-th tile.  target(s) counts the CTAs that have an
 // s-th tile under the static schedule.
-__device__ __forceinline__ void tile_barrier(unsigned long long *ctr, int64_t s, int64_t total, int64_t n_units,
+// Measured (scripts/exp_sync.sh): compress GEMM 9.7 -> 8.1 ms, decompress 8.6 ->
+// 7.2 ms per launch under the power cap.  A wait that exceeds 2 ms (a CTA that
+// is not resident, e.g. the GPU is shared) turns the barrier off for the rest
+// of the launch in this CTA.
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ bool tile_barrier(unsigned long long *ctr, int64_t s, int64_t total, int64_t n_units,
                                              int per_unit) {
   const int64_t full = total / n_units, rem = total % n_units;
   const int64_t target = int64_t(per_unit) * (n_units * min(s + 1, full) + (s + 1 > full ? rem : 0));
   atomicAdd(ctr, 1ull);
   unsigned long long v;
-  for (int spin = 0; spin < (1 << 21); ++spin) {
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+  if (int64_t(v) >= target) return true;
+  const uint64_t t0 = global_ns();
+  while (true) {
+    __nanosleep(64);
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
-    if (int64_t(v) >= target) break;
-    __nanosleep(100);
+    if (int64_t(v) >= target) return true;
+    if (global_ns() - t0 > 2000000ull) return false;
   }
 }
 
@@ -324,10 +341,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t pol_a = l2_policy(P.hint_a);
     const uint64_t pol_b = l2_policy(P.hint_b);
     int64_t seq = 0;
+    bool sync = MODE != EPI_XTX && P.tile_sync != nullptr;
     for (int64_t t = t_first; t < total; t += t_step) {
       const Tile T = get_tile(t);
       if (!T.valid) continue;
-      if (MODE != EPI_XTX && P.tile_sync) tile_barrier(P.tile_sync, seq++, total, t_step, PAIR ? 2 : 1);
+      if (sync) sync = tile_barrier(P.tile_sync, seq++, total, t_step, PAIR ? 2 : 1);
       int n0, ncols, g0, g1;
       tile_geometry<MODE>(P, T, n0, ncols, g0, g1);
       const int n_mma = (ncols + 15) & ~15;
@@ -608,6 +626,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// One zeroed counter per launch, from a per-device ring of 4096 (launches in
+// flight never share one).
+static unsigned long long *next_sync_counter() {
+  static std::mutex mu;
+  static unsigned long long *ring[64] = {};
+  static uint32_t next[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (!ring[dev & 63] && cudaMalloc(&ring[dev & 63], 4096 * sizeof(unsigned long long)) != cudaSuccess) {
+    set_error("tile-sync counters: cudaMalloc failed");
+    return nullptr;
+  }
+  return ring[dev & 63] + (next[dev & 63]++ % 4096);
+}
+
 static int num_sms() {
   static int n = 0;
   if (!n) {
@@ -643,13 +677,12 @@ static kvtc_status launch(const CUtensorMap *tmA, const CUtensorMap *tmB, const 
     const char *ha = getenv("KVTC_HINT_A"), *hb = getenv("KVTC_HINT_B");
     if (ha) pp.hint_a = atoi(ha);
     if (hb) pp.hint_b = atoi(hb);
+    // soft tile barrier (tile_barrier) for the codec GEMMs; KVTC_TILE_SYNC = bit mask
+    // over modes overrides (0 = off)
     const char *ts = getenv("KVTC_TILE_SYNC");
-    if (ts && (atoi(ts) >> MODE) & 1) {
-      // one zeroed counter per launch from a ring of 4096 (launches in flight never share one)
-      static unsigned long long *ring = nullptr;
-      static std::atomic<uint32_t> next{0};
-      if (!ring) KVTC_CUDA_TRY(cudaMalloc(&ring, 4096 * sizeof(unsigned long long)));
-      pp.tile_sync = ring + (next.fetch_add(1) % 4096);
+    const int sync_mask = ts ? atoi(ts) : ((1 << EPI_QUANT) | (1 << EPI_RECON));
+    if ((sync_mask >> MODE) & 1) {
+      if (!(pp.tile_sync = next_sync_counter())) return KVTC_E_CUDA;
       KVTC_CUDA_TRY(cudaMemsetAsync(pp.tile_sync, 0, sizeof(unsigned long long), st));
     }
   }
