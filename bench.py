@@ -174,6 +174,91 @@ def oracle_sample(bases, plans, K_host, V_host, spec, ntok: int):
     return gbs, dt, cores, c.stats
 
 
+# ---------------------------------------------------------- multi-conversation
+def run_multiconv(args, K, spec, kb, kp, vb, vp, setup_s, setup_info, world, rank, local, dist):
+    """BASELINE config 5: 256 Llama-3.1-8B-shaped conversations of t ~ U[8192,
+    32768] tokens, assigned to ranks longest-first (LPT); each rank
+    compresses + decompresses its share in waves (generate one cache, time its
+    round trip, drop it: 634 GiB of bf16 KV never fits at once).  Only codec time
+    is timed (CUDA events around each round trip on the launching stream, summed);
+    value = all ranks' 16-bit bytes / the slowest rank's codec time (strong
+    scaling: the 256 conversations are fixed as N grows)."""
+    from kvtc_inputs import generate, lengths_for
+    from paper_2511_01815_b200.distributed import lpt_assign
+    lens = lengths_for(args.convs, 8192, 32768, seed=0)
+    mine = lpt_assign(lens, world)[rank]
+    p = spec.p
+    stream = torch.cuda.current_stream()
+    tmax = max(lens)
+    cap, wsb = K.compress_sizes(kb, kp, vb, vp, K.KVView(torch.empty((spec.layers, tmax, spec.kv_heads, spec.head_dim),
+                                                                     dtype=torch.bfloat16, device="cuda")))
+    cont = torch.empty(cap, dtype=torch.uint8, device="cuda")
+    cws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    # decompress workspace sized by the longest conversation (it grows with m)
+    ci_max = int(np.argmax(lens))
+    Kc = generate(spec, 0, lens[ci_max], pos0=0, conversation=ci_max, device="cuda")
+    Vc = generate(spec, 1, lens[ci_max], pos0=0, conversation=ci_max, device="cuda")
+    K.compress(kb, kp, vb, vp, K.KVView(Kc), K.KVView(Vc), out=cont, workspace=cws)
+    dws = torch.empty(K.decompress_workspace_bytes(kb, kp, vb, vp, cont[:256].cpu().numpy().tobytes()),
+                      dtype=torch.uint8, device="cuda")
+    del Kc, Vc
+    clocks = ClockSampler(local)
+
+    def one(ci):
+        t = lens[ci]
+        Kc = generate(spec, 0, t, pos0=0, conversation=ci, device="cuda")
+        Vc = generate(spec, 1, t, pos0=0, conversation=ci, device="cuda")
+        Ko, Vo = torch.empty_like(Kc), torch.empty_like(Vc)
+        kv, vv, kov, vov = K.KVView(Kc), K.KVView(Vc), K.KVView(Ko), K.KVView(Vo)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        K.compress(kb, kp, vb, vp, kv, vv, out=cont, workspace=cws, sync_len=False)
+        K.decompress(kb, kp, vb, vp, cont, kov, vov, workspace=dws)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ok = torch.equal(Ko[:, :4], Kc[:, :4]) and torch.equal(Vo[:, t - 128:], Vc[:, t - 128:])
+        return e0.elapsed_time(e1), 2 * 2 * p * (t - 132), ok
+
+    for _ in range(args.warmup):
+        one(mine[0])
+    if dist:
+        dist.barrier()
+    clocks.start()
+    ms, nbytes, allok = 0.0, 0, True
+    for _ in range(args.steps):
+        for ci in mine:
+            dt, b, ok = one(ci)
+            ms += dt
+            nbytes += b
+            allok &= ok
+    clk = clocks.stop()
+    tot = torch.tensor([ms, float(nbytes)], dtype=torch.float64, device="cuda")
+    if dist:
+        mx = tot.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+        ms_max, nb_all = float(mx[0]), float(tot[1])
+    else:
+        ms_max, nb_all = ms, float(nbytes)
+    if rank == 0:
+        line = {"metric": METRIC, "value": nb_all / (ms_max * 1e-3) / 1e9, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic (kvtc_inputs, DESIGN.md §5)",
+                "config": {"workload": f"multiconv: {args.convs} llama8b-shaped conversations, t ~ U[8192, 32768] "
+                                       f"(seed 0), LPT over {world} rank(s), codec time only (caches generated "
+                                       "per conversation, untimed)",
+                           "conversations": args.convs, "tokens_total": int(sum(lens)),
+                           "per_rank_conversations": len(mine), "setup_s": round(setup_s, 1),
+                           "sinks_window_roundtrip_ok": bool(allok)},
+                "gpu_launches": None, "clocks": clk}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 # -------------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
@@ -195,6 +280,7 @@ def main():
     ap.add_argument("--cpu-tokens", type=int, default=32)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--convs", type=int, default=256)                # multiconv: number of conversations
     args = ap.parse_args()
 
     world, rank, local = dist_env()
@@ -221,7 +307,7 @@ def main():
         over["noise_frac"] = args.noise
     if args.latent is not None:
         over["latent"] = args.latent
-    spec = make_spec(args.config, **over)
+    spec = make_spec("llama8b" if args.config == "multiconv" else args.config, **over)
     p, t = spec.p, args.tokens
     s_, w_ = 4, 128
     m = t - s_ - w_
@@ -233,6 +319,9 @@ def main():
     setup_s = time.time() - t_setup
     kb, vb = bases
     kp, vp = plans
+    if args.config == "multiconv":
+        run_multiconv(args, K, spec, kb, kp, vb, vp, setup_s, setup_info, world, rank, local, dist)
+        return
     if os.environ.get("KVTC_DUMP_PLANS"):
         with open(os.environ["KVTC_DUMP_PLANS"], "w") as f:
             json.dump({"config": args.config, "cr": args.cr, "k": kp.info().groups, "v": vp.info().groups,

@@ -517,14 +517,23 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
     if (r) return r;
     return launch_gather(*k, kbases, pol->sinks, L.m, cs, kb->pairing, X, q, ctas, ldx);
   };
-  auto gemm = [&](int sv, bool direct) -> kvtc_status {
+  // rows [r0, r1) of a stream (r0 a multiple of the 128-token tile): payload tiles
+  // and wide-group scratch rows are addressed from r0
+  auto gemm = [&](int sv, bool direct, int64_t r0 = 0, int64_t r1 = -1) -> kvtc_status {
     ProfScope ps("c.project_quant_gemm", st);
-    return sv ? run_project_quant(vb, vpl, vop, X, L.m, payload_v, wide, st, direct ? &tV : nullptr, pol->sinks, ldx)
-              : run_project_quant(kb, kpl, kop, X, L.m, payload_k, wide, st, nullptr, 0, ldx);
+    if (r1 < 0) r1 = L.m;
+    const kvtc_plan *pl = sv ? vpl : kpl;
+    uint8_t *pay = (sv ? payload_v : payload_k) + (r0 / kTileM) * pl->tile_bytes;
+    float *wd = wide ? wide + r0 * pl->wide_cols : nullptr;      // scratch rows of stride wide_cols
+    return sv ? run_project_quant(vb, vpl, vop, X, r1 - r0, pay, wd, st, direct ? &tV : nullptr, pol->sinks + r0,
+                                  ldx)
+              : run_project_quant(kb, kpl, kop, X + r0 * ldx, r1 - r0, pay, wd, st, nullptr, 0, ldx);
   };
-  auto encode = [&](int sv, cudaStream_t q, int ctas, const char *tag) -> kvtc_status {
+  auto encode = [&](int sv, cudaStream_t q, int ctas, const char *tag, uint32_t c0 = 0,
+                    uint32_t c1 = 0xFFFFFFFFu) -> kvtc_status {
     ProfScope ps(tag, q);
-    return launch_deflate_encode(sv ? payload_v : payload_k, L.pay[sv], pol->chunk_bytes, dwsp[sv], dws[sv], ctas, q);
+    return launch_deflate_encode(sv ? payload_v : payload_k, L.pay[sv], pol->chunk_bytes, dwsp[sv], dws[sv], ctas, q,
+                                 c0, c1);
   };
   KVTC_CUDA_TRY(cudaEventRecord(ss->ev[0], st));                 // fork point: bases, raw tokens
   if (v_direct) {
@@ -542,14 +551,32 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
       KVTC_CUDA_TRY(cudaEventRecord(ss->ev[1], aux));            // X (keys) ready
       KVTC_CUDA_TRY(cudaStreamWaitEvent(st, ss->ev[1], 0));
     }
-    if ((s = gemm(0, false))) return s;
+    // keys' GEMM in two row halves when KVTC_C_SPLIT=1 (measured slower: the encoder
+    // beside the GEMM halves costs more GEMM time than the shorter tail saves): the chunks of
+    // the first half are encoded beside the second half, so only the second
+    // half's encoder is left after the last GEMM
+    const int64_t tiles = (L.m + kTileM - 1) / kTileM;
+    const int64_t half = (tiles / 2) * kTileM;
+    const uint32_t c_half = uint32_t(uint64_t(half / kTileM) * kpl->tile_bytes / uint64_t(pol->chunk_bytes));
+    const bool split = deflate_side && env_flag("KVTC_C_SPLIT", false) && half > 0 && c_half > 0;
+    if (deflate_side) KVTC_CUDA_TRY(cudaStreamWaitEvent(aux, ss->ev[2], 0));
+    if (split) {
+      if ((s = gemm(0, false, 0, half))) return s;
+      KVTC_CUDA_TRY(cudaEventRecord(ss->ev[1], st));             // first half of the keys' payload ready
+      if ((s = gemm(0, false, half, L.m))) return s;
+    } else if ((s = gemm(0, false))) {
+      return s;
+    }
     if (deflate_side) {
-      KVTC_CUDA_TRY(cudaStreamWaitEvent(aux, ss->ev[2], 0));
       if ((s = encode(1, aux, side_ctas, "c.deflate_overlapped"))) return s;
+      if (split) {
+        KVTC_CUDA_TRY(cudaStreamWaitEvent(aux, ss->ev[1], 0));
+        if ((s = encode(0, aux, side_ctas, "c.deflate_overlapped", 0, c_half))) return s;
+      }
     } else if ((s = encode(1, st, 0, "c.deflate"))) {
       return s;
     }
-    if ((s = encode(0, st, 0, "c.deflate"))) return s;
+    if ((s = encode(0, st, 0, "c.deflate", split ? c_half : 0))) return s;
   } else {
     if ((s = gather_keys(st, 0, "c.gather_unrope"))) return s;
     if ((s = gemm(0, false))) return s;

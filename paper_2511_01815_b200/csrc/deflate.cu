@@ -4,13 +4,14 @@
 // algorithm" and runs on the GPU.  Reading Q15: 64 KiB chunks, each
 // an independent raw DEFLATE stream that stock zlib inflates (wbits = -15).
 //
-// Encoder (one CTA of 64 threads per chunk, ~14 chunks resident per SM so the
+// Encoder (one CTA of 128 threads per chunk, ~14 chunks resident per SM so the
 // serial code construction of one chunk overlaps the parallel passes of the
-// others): byte histogram -> length-limited canonical Huffman code (<= 15 bits;
+// others): byte histogram (warp-private bins) -> symbols radix-sorted by
+// (frequency, symbol) -> length-limited canonical Huffman code (<= 15 bits;
 // in-place minimum-redundancy lengths + Kraft-sum repair) -> one dynamic block
 // (literals + EOB only, no LZ77 matches in this version) -> thread j emits the
-// bits of segment j (1/64 of the chunk) at an offset from a block-wide
-// exclusive scan.  Falls back to stored blocks when smaller.  The bit length of
+// bits of 1/128 of the chunk, two codes per accumulator step, at an offset from
+// a block-wide exclusive scan.  Falls back to stored blocks when smaller.  The bit length of
 // every segment goes to a u16 side index that lives in the section, NOT in the
 // DEFLATE stream.
 //
@@ -18,14 +19,15 @@
 // (table-driven code-length decode), the block builds a two-level table (11-bit
 // first level + 4-bit subtables for longer codes) in shared memory, then thread
 // j decodes segment j from the prefix sum of the index — 64 independent serial
-// decoders with one word of read-ahead and 16-byte output stores.
+// decoders with 16-byte reads, two blocks of read-ahead and 16-byte stores.
 // Decoder, generic path (kvtc_stage_inflate_raw): a complete sequential inflater
 // (stored / fixed / dynamic blocks, LZ77 back-references) for foreign streams.
 //
 // Section layout: 64-byte header, chunk table [nchunks] x
 // {u64 offset, u32 bytes, u32 kind}, segment index [nchunks][64] u16 (bit
 // length of each 1/64 of the chunk's symbols; segment 0 starts right after the
-// block header), then the chunk streams, each starting 4-byte aligned.
+// block header), then the chunk streams, each starting 16-byte aligned and zero-padded to
+// a multiple of 16 bytes (the inflater reads 16-byte words).
 #include <cub/block/block_radix_sort.cuh>
 #include <cub/block/block_scan.cuh>
 
@@ -34,9 +36,9 @@
 namespace kvtc {
 
 constexpr uint32_t kSectionMagic = 0x4454564Bu;  // "KVTD"
-constexpr int kEncThreads = 64;   // one thread per segment; ~14 chunks resident per SM
+constexpr int kEncThreads = 128;  // two threads per index segment; ~14 chunks resident per SM
 constexpr int kNSeg = 64;
-constexpr uint32_t kSectionVersion = 2;
+constexpr uint32_t kSectionVersion = 3;
 constexpr int kLitSyms = 257;                    // 0..255 literals + 256 end-of-block
 constexpr int kMaxBits = 15;
 
@@ -67,8 +69,8 @@ __host__ __device__ inline uint64_t slot_stride(int32_t chunk) { return ((stored
 
 size_t deflate_section_bound(size_t n, int32_t chunk) {
   const size_t nch = (n + chunk - 1) / chunk;
-  return sizeof(SectionHeader) + nch * sizeof(ChunkEntry) + ((nch * kNSeg * 2 + 3) & ~size_t(3)) +
-         nch * ((stored_bytes(chunk) + 3) & ~3u) + 16;
+  return sizeof(SectionHeader) + nch * sizeof(ChunkEntry) + ((nch * kNSeg * 2 + 15) & ~size_t(15)) +
+         nch * ((stored_bytes(chunk) + 15) & ~15u) + 16;
 }
 size_t deflate_workspace(size_t n, int32_t chunk) {
   const size_t nch = (n + chunk - 1) / chunk;
@@ -196,7 +198,7 @@ struct BitWriter {
 };
 
 
-constexpr int kSortItems = 5;                       // 64 x 5 >= 257 sort keys
+constexpr int kSortItems = (kLitSyms + kEncThreads - 1) / kEncThreads;   // >= 257 sort keys
 using EncSort = cub::BlockRadixSort<uint32_t, kEncThreads, kSortItems>;
 
 struct EncShared {
@@ -527,11 +529,11 @@ __device__ __forceinline__ void encode_chunk(EncShared &S, const int c, const ui
 // encoder has the GPU, or a bounded grid (a few CTAs per SM) when it runs beside
 // a persistent GEMM on the side stream, so the GEMM CTA always fits.
 __global__ void __launch_bounds__(kEncThreads, 14) deflate_encode_kernel(const uint8_t *in, uint64_t n, int32_t chunk,
-                                                                        uint32_t nch, uint8_t *slots, uint64_t stride,
-                                                                        uint32_t *chunk_bytes, uint32_t *chunk_kind,
-                                                                        uint16_t *index) {
+                                                                        uint32_t c_begin, uint32_t c_end, uint8_t *slots,
+                                                                        uint64_t stride, uint32_t *chunk_bytes,
+                                                                        uint32_t *chunk_kind, uint16_t *index) {
   __shared__ EncShared S;
-  for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
+  for (uint32_t c = c_begin + blockIdx.x; c < c_end; c += gridDim.x) {
     encode_chunk(S, int(c), in, n, chunk, slots, stride, chunk_bytes, chunk_kind, index);
     __syncthreads();
   }
@@ -548,12 +550,12 @@ __global__ void __launch_bounds__(1024) section_layout_kernel(const uint32_t *ch
   SectionHeader *h = reinterpret_cast<SectionHeader *>(out);
   ChunkEntry *tab = reinterpret_cast<ChunkEntry *>(out + sizeof(SectionHeader));
   const uint64_t data_off =
-      sizeof(SectionHeader) + uint64_t(nch) * sizeof(ChunkEntry) + ((uint64_t(nch) * kNSeg * 2 + 3) & ~3ull);
+      sizeof(SectionHeader) + uint64_t(nch) * sizeof(ChunkEntry) + ((uint64_t(nch) * kNSeg * 2 + 15) & ~15ull);
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
   for (uint32_t b = 0; b < nch; b += 1024) {
     const uint32_t i = b + threadIdx.x;
-    const uint64_t sz = i < nch ? ((uint64_t(chunk_bytes[i]) + 3) & ~3ull) : 0;
+    const uint64_t sz = i < nch ? ((uint64_t(chunk_bytes[i]) + 15) & ~15ull) : 0;
     uint64_t off, tot;
     cub::BlockScan<uint64_t, 1024>(tmp).ExclusiveSum(sz, off, tot);
     if (i < nch) {
@@ -591,9 +593,9 @@ __global__ void section_copy_kernel(const uint8_t *slots, uint64_t stride, const
   if (threadIdx.x < kNSeg) idx[uint64_t(c) * kNSeg + threadIdx.x] = e.kind == 0 ? index[uint64_t(c) * kNSeg + threadIdx.x] : 0;
   const uint32_t *s = reinterpret_cast<const uint32_t *>(slots + uint64_t(c) * stride);
   uint32_t *d = reinterpret_cast<uint32_t *>(out + h->data_offset + e.offset);
-  const uint32_t words = (e.bytes + 3) / 4;
-  for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) {
-    uint32_t v = s[i];
+  const uint32_t words = (e.bytes + 3) / 4, padded = ((e.bytes + 15) / 16) * 4;
+  for (uint32_t i = threadIdx.x; i < padded; i += blockDim.x) {
+    uint32_t v = i < words ? s[i] : 0u;
     if (i == words - 1 && (e.bytes & 3)) v &= (1u << (8 * (e.bytes & 3))) - 1;   // deterministic padding
     d[i] = v;
   }
@@ -630,15 +632,17 @@ int corun_ctas(int per_sm) {
 }
 
 kvtc_status launch_deflate_encode(const uint8_t *in, size_t n, int32_t chunk, void *ws, size_t ws_bytes,
-                                  int32_t max_ctas, cudaStream_t st) {
+                                  int32_t max_ctas, cudaStream_t st, uint32_t c_begin, uint32_t c_end) {
   KVTC_CHECK_ARG(chunk == 16384 || chunk == 32768 || chunk == 65536, "chunk_bytes must be 16/32/64 KiB");
   KVTC_CHECK_ARG(ws_bytes >= deflate_workspace(n, chunk), "deflate workspace");
   const DeflateWs w = deflate_ws(n, chunk, ws);
-  if (w.nch == 0) return KVTC_OK;
-  const uint32_t grid = max_ctas > 0 ? std::min<uint32_t>(w.nch, uint32_t(max_ctas)) : w.nch;
+  c_end = std::min(c_end, w.nch);
+  if (c_begin >= c_end) return KVTC_OK;
+  const uint32_t nc = c_end - c_begin;
+  const uint32_t grid = max_ctas > 0 ? std::min<uint32_t>(nc, uint32_t(max_ctas)) : nc;
   KVTC_MAX_CARVEOUT(deflate_encode_kernel);
-  deflate_encode_kernel<<<grid, kEncThreads, 0, st>>>(in, n, chunk, w.nch, w.slots, w.stride, w.cbytes, w.ckind,
-                                                      w.index);
+  deflate_encode_kernel<<<grid, kEncThreads, 0, st>>>(in, n, chunk, c_begin, c_end, w.slots, w.stride, w.cbytes,
+                                                      w.ckind, w.index);
   KVTC_LAUNCH_CHECK();
   return KVTC_OK;
 }
@@ -788,8 +792,12 @@ constexpr int kSubTabs = (1 << kTabBits) / 16 + 1;
 constexpr int kInfThreads = kNSeg; // one thread per segment, 2 warps per chunk
 static_assert(kNSeg == 64, "the segment-start scan below assumes two warps");
 
+constexpr int kRing = 4;           // per-lane ring of 16-byte stream blocks (cp.async read-ahead)
 struct FastShared {
-  uint32_t hdr[kHdrWords + 2];
+  union {
+    uint32_t hdr[kHdrWords + 2];   // header words (header parse), then
+    uint4 ring[kRing][kNSeg];      // per-lane read-ahead blocks (segment decode)
+  };
   uint16_t table[1 << kTabBits];   // (sym << 4) | len; 0x8000 | k: longer code, subtable k
   uint16_t sub[kSubTabs << kSubBits];  // second level: the next kSubBits bits
   uint16_t code[260];
@@ -962,26 +970,48 @@ __device__ __forceinline__ void inflate_chunk(FastShared &S, const uint32_t b, c
   const uint32_t s0 = tid * seg, s1 = umin32(nc, (tid + 1) * seg);
   if (s0 >= s1) return;
   uint64_t pos = S.hdr_bits + S.segstart[tid] - mylen + (tid >= 32 ? S.segstart[31] : 0);
-  const uint64_t wend = (e.bytes + 3) / 4;
-  uint64_t wi = pos >> 5;
-  uint64_t buf = uint64_t(__ldg(words + wi++)) >> (pos & 31);
-  int cnt = 32 - int(pos & 31);
-  // three words of read-ahead in flight per lane (each lane streams its own
-  // segment, so loads are not coalesced: hide their latency instead)
-  uint32_t nw0 = wi < wend ? __ldg(words + wi) : 0u;
-  uint32_t nw1 = wi + 1 < wend ? __ldg(words + wi + 1) : 0u;
-  uint32_t nw2 = wi + 2 < wend ? __ldg(words + wi + 2) : 0u;
-  wi += 3;
-  bool bad = false;
-  auto next_sym = [&]() -> uint32_t {
-    if (cnt <= 32) {
-      buf |= uint64_t(nw0) << cnt;
-      cnt += 32;
-      nw0 = nw1;
-      nw1 = nw2;
-      nw2 = wi < wend ? __ldg(words + wi) : 0u;
-      ++wi;
+  // Read-ahead through shared memory: each lane streams its own segment, so
+  // loads cannot be coalesced; 16-byte cp.async copies of the next three blocks
+  // fill a per-lane ring and complete in the background.  (Rotating prefetched
+  // registers instead made every rotation wait for its load: ncu showed ~40 % of
+  // the samples stalled on it.)  The stream is 16-byte aligned and zero-padded.
+  const uint4 *blk = reinterpret_cast<const uint4 *>(stream);
+  const uint32_t nblk = (e.bytes + 15) / 16;
+  auto issue = [&](uint32_t b) {
+    if (b < nblk) {
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&S.ring[b % kRing][tid])),
+                   "l"(blk + b)
+                   : "memory");
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  uint32_t cb = uint32_t(pos >> 7);        // current block
+  for (int k = 0; k < kRing; ++k) issue(cb + k);
+  asm volatile("cp.async.wait_group %0;" ::"n"(kRing - 1) : "memory");
+  uint4 cur = cb < nblk ? S.ring[cb % kRing][tid] : make_uint4(0, 0, 0, 0);
+  int wsel = int(pos >> 5) & 3;
+  auto take = [&]() -> uint32_t {
+    const uint32_t w = wsel == 0 ? cur.x : wsel == 1 ? cur.y : wsel == 2 ? cur.z : cur.w;
+    if (++wsel == 4) {
+      wsel = 0;
+      ++cb;
+      asm volatile("cp.async.wait_group %0;" ::"n"(kRing - 2) : "memory");   // block cb landed
+      cur = cb < nblk ? S.ring[cb % kRing][tid] : make_uint4(0, 0, 0, 0);
+      issue(cb + kRing - 1);                 // into the slot of block cb - 1, consumed
+    }
+    return w;
+  };
+  uint64_t buf = uint64_t(take()) >> (pos & 31);
+  int cnt = 32 - int(pos & 31);
+  bool bad = false;
+  // >= 30 valid bits after a refill: two codes (<= 15 bits each) per check
+  auto refill = [&]() {
+    if (cnt < 30) {
+      buf |= uint64_t(take()) << cnt;
+      cnt += 32;
+    }
+  };
+  auto decode = [&]() -> uint32_t {
     uint32_t te = S.table[buf & ((1u << kTabBits) - 1)];
     if (te & 0x8000) te = S.sub[((te & 0x7FFF) << kSubBits) | ((buf >> kTabBits) & ((1u << kSubBits) - 1))];
     const uint32_t sym = te >> 4;
@@ -997,10 +1027,18 @@ __device__ __forceinline__ void inflate_chunk(FastShared &S, const uint32_t b, c
   for (; vec_out && i + 16 <= s1; i += 16) {
     uint32_t w[4] = {0, 0, 0, 0};
 #pragma unroll
-    for (int k = 0; k < 16; ++k) w[k >> 2] |= next_sym() << (8 * (k & 3));
+    for (int k = 0; k < 16; k += 2) {
+      refill();
+      w[k >> 2] |= decode() << (8 * (k & 3));
+      w[k >> 2] |= decode() << (8 * ((k + 1) & 3));
+    }
     *reinterpret_cast<uint4 *>(o + i) = make_uint4(w[0], w[1], w[2], w[3]);
   }
-  for (; i < s1; ++i) o[i] = uint8_t(next_sym());
+  for (; i < s1; ++i) {
+    refill();
+    o[i] = uint8_t(decode());
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");   // no copy may land in the next chunk's header
   if (bad) atomicExch(err, -7);
 }
 

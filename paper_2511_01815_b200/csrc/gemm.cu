@@ -37,13 +37,18 @@ namespace kvtc {
 // Single-CTA tiles: A 128 x 64 + B 256 x 64 per stage (48 KiB), 4 stages.
 // CTA pairs (cta_group::2, M = 256): each CTA holds its A half (128 rows) and
 // its B half (N/2 <= 128 rows): 32 KiB per stage, 6 stages.
-template <bool PAIR>
+// NSUB = 2 (compress): a tile is two 256-column segments sharing the A k-block;
+// two MMAs per k-slice into both TMEM accumulators (512 columns, no double
+// buffering), 48 KiB per stage, 4 stages: 25 % less L2 traffic per flop.
+template <bool PAIR, int NSUB = 1>
 struct Cfg {
-  static constexpr int kStages = PAIR ? 6 : 4;
+  static constexpr int kStages = NSUB == 2 ? 4 : (PAIR ? 6 : 4);
   static constexpr int kABytes = kTileM * kBlockK * 2;                        // 16 KiB
-  static constexpr int kBBytes = (PAIR ? kMaxTileN / 2 : kMaxTileN) * kBlockK * 2;
+  static constexpr int kBSubBytes = (PAIR ? kMaxTileN / 2 : kMaxTileN) * kBlockK * 2;
+  static constexpr int kBBytes = NSUB * kBSubBytes;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 2048;
+  static constexpr int kAccBufs = NSUB == 2 ? 1 : 2;
 };
 constexpr int kBBoxRows = 128;                     // B tensor maps load 128 rows per box
 constexpr int kThreads = 256;
@@ -83,6 +88,8 @@ struct Params {
   int32_t group_m;     // raster group (M-blocks or M-pairs)
   int32_t hint_a, hint_b;   // L2 policies of the A / B loads
   unsigned long long *tile_sync;   // non-null: producers align tile starts (see tile_barrier)
+  int32_t sync_lag;                // a producer may run this many tiles ahead of the slowest
+  int32_t nsegs;                   // QUANT: number of 256-column segments
 };
 
 __device__ __forceinline__ void cluster_sync_all() {
@@ -133,11 +140,11 @@ __device__ __forceinline__ Tile tile_of(const Params &P, int64_t t, int num_mt) 
   return T;
 }
 
-template <int MODE>
+template <int MODE, int NSUB = 1>
 __device__ __forceinline__ void tile_geometry(const Params &P, const Tile &T, int &n0, int &ncols, int &g0, int &g1) {
   g0 = g1 = 0;
   if constexpr (MODE == EPI_QUANT) {
-    const SegDesc sd = P.segs[T.nb];
+    const SegDesc sd = P.segs[T.nb * NSUB];
     n0 = sd.col0;
     ncols = sd.width;
     g0 = sd.g_begin;
@@ -257,10 +264,12 @@ __device__ __forceinline__ uint64_t global_ns() {
   return t;
 }
 __device__ __forceinline__ bool tile_barrier(unsigned long long *ctr, int64_t s, int64_t total, int64_t n_units,
-                                             int per_unit) {
+                                             int per_unit, int lag) {
+  atomicAdd(ctr, 1ull);
+  s -= lag;
+  if (s < 0) return true;
   const int64_t full = total / n_units, rem = total % n_units;
   const int64_t target = int64_t(per_unit) * (n_units * min(s + 1, full) + (s + 1 > full ? rem : 0));
-  atomicAdd(ctr, 1ull);
   unsigned long long v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
   if (int64_t(v) >= target) return true;
@@ -273,14 +282,26 @@ __device__ __forceinline__ bool tile_barrier(unsigned long long *ctr, int64_t s,
   }
 }
 
-template <int MODE, bool PAIR>
-__global__ void __launch_bounds__(kThreads, 1)
+// Segments (256-column pieces of the compacted N axis) of a compress tile.
+template <int NSUB>
+__device__ __forceinline__ int tile_nsub(const Params &P, const Tile &T) {
+  return NSUB == 1 ? 1 : min(NSUB, P.nsegs - T.nb * NSUB);
+}
+
+// Register budget: the compress GEMM runs beside the side-stream gather / encoder
+// CTAs (2-3 per SM), so it is held to 128 registers (min 2 blocks); the
+// decompress GEMM (beside the dequantiser) may use more.
+template <int MODE, bool PAIR, int NSUB>
+__global__ void __launch_bounds__(kThreads, MODE == EPI_RECON ? 1 : 2)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ Params P) {
-  using C = Cfg<PAIR>;
+  static_assert(NSUB == 1 || (MODE == EPI_QUANT && PAIR), "two-segment tiles: compress, CTA pairs");
+  using C = Cfg<PAIR, NSUB>;
   constexpr int kStages = C::kStages;
   constexpr int kABytes = C::kABytes;
   constexpr int kStageBytes = C::kStageBytes;
+  constexpr int kBSub = C::kBSubBytes;
+  constexpr int kAccBufs = C::kAccBufs;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *tiles = smem;
@@ -345,17 +366,30 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int64_t t = t_first; t < total; t += t_step) {
       const Tile T = get_tile(t);
       if (!T.valid) continue;
-      if (sync) sync = tile_barrier(P.tile_sync, seq++, total, t_step, PAIR ? 2 : 1);
+      if (sync) sync = tile_barrier(P.tile_sync, seq++, total, t_step, PAIR ? 2 : 1, P.sync_lag);
       int n0, ncols, g0, g1;
-      tile_geometry<MODE>(P, T, n0, ncols, g0, g1);
+      tile_geometry<MODE, NSUB>(P, T, n0, ncols, g0, g1);
       const int n_mma = (ncols + 15) & ~15;
+      const int nsub = tile_nsub<NSUB>(P, T);
       for (int kb = 0; kb < num_kb; ++kb, ++it) {
         const int s = it % kStages;
         if (it >= kStages) mbar_wait(&empty_bar[s], ((it / kStages) - 1) & 1);
         uint8_t *a = tiles + s * kStageBytes;
         uint8_t *b = a + kABytes;
         const int32_t ka = kb * kBlockK;
-        if constexpr (PAIR) {
+        if constexpr (NSUB == 2) {
+          // A k-block + one B k-block per segment; both CTAs' bytes on the leader's barrier
+          if (leader) mbar_arrive_expect_tx(&full_bar[s], 2 * (kABytes + nsub * kBSub));
+          if (P.a_hd)
+            tma_load_3d_pair(a, &tmA, &full_bar[s], ka % P.a_hd, int(P.a_row0) + T.mb * kTileM, ka / P.a_hd);
+          else
+            tma_load_2d_pair(a, &tmA, &full_bar[s], ka, T.mb * kTileM);
+          for (int sb = 0; sb < nsub; ++sb) {
+            const SegDesc sd = P.segs[T.nb * NSUB + sb];
+            const int nm = (sd.width + 15) & ~15;
+            tma_load_2d_pair(b + sb * kBSub, &tmB, &full_bar[s], ka, sd.col0 + int(rank) * (nm / 2));
+          }
+        } else if constexpr (PAIR) {
           // both CTAs' bytes land on the leader's barrier
           if (leader) mbar_arrive_expect_tx(&full_bar[s], 2 * kStageBytes);
           if (P.a_hd && P.hint_a)
@@ -388,20 +422,36 @@ __global__ void __launch_bounds__(kThreads, 1)
       const Tile T = get_tile(t);
       if (!T.valid) continue;
       int n0, ncols, g0, g1;
-      tile_geometry<MODE>(P, T, n0, ncols, g0, g1);
+      tile_geometry<MODE, NSUB>(P, T, n0, ncols, g0, g1);
       const int n_mma = (ncols + 15) & ~15;
       const uint32_t idesc = make_idesc_f16(P.fmt, PAIR ? 2 * kTileM : kTileM, n_mma);
-      const uint32_t acc = acc_it & 1;
-      if (acc_it >= 2) mbar_wait(&tmem_empty[acc], ((acc_it / 2) - 1) & 1);
+      const uint32_t acc = acc_it % kAccBufs;
+      if (acc_it >= kAccBufs) mbar_wait(&tmem_empty[acc], ((acc_it / kAccBufs) - 1) & 1);
       tc_fence_after();
       const uint32_t tacc = tmem_base + acc * kMaxTileN;
+      const int nsub = tile_nsub<NSUB>(P, T);
+      uint32_t idesc_sub[NSUB];
+#pragma unroll
+      for (int sb = 0; sb < NSUB; ++sb)
+        idesc_sub[sb] = NSUB == 1 ? idesc
+                                  : make_idesc_f16(P.fmt, 2 * kTileM,
+                                                   sb < nsub ? (P.segs[T.nb * NSUB + sb].width + 15) & ~15 : 16);
       for (int kb = 0; kb < num_kb; ++kb, ++it) {
         const int s = it % kStages;
         mbar_wait(&full_bar[s], (it / kStages) & 1);
         tc_fence_after();
         const uint64_t ad = make_sdesc_sw128(tiles + s * kStageBytes);
         const uint64_t bd = make_sdesc_sw128(tiles + s * kStageBytes + kABytes);
-        if constexpr (PAIR) {
+        if constexpr (NSUB == 2) {
+          // segment sb accumulates in TMEM columns [256 sb, 256 sb + 256)
+#pragma unroll
+          for (int k = 0; k < kBlockK / 16; ++k)
+            for (int sb = 0; sb < nsub; ++sb)
+              umma_f16_pair(tmem_base + sb * kMaxTileN, ad + 2 * k,
+                            make_sdesc_sw128(tiles + s * kStageBytes + kABytes + sb * kBSub) + 2 * k, idesc_sub[sb],
+                            (kb | k) != 0);
+          umma_commit_pair(&empty_bar[s]);
+        } else if constexpr (PAIR) {
 #pragma unroll
           for (int k = 0; k < kBlockK / 16; ++k)
             umma_f16_pair(tacc, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
@@ -428,13 +478,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const Tile T = get_tile(t);
       if (!T.valid) continue;
       int n0, ncols, seg_g0, seg_g1;
-      tile_geometry<MODE>(P, T, n0, ncols, seg_g0, seg_g1);
+      tile_geometry<MODE, NSUB>(P, T, n0, ncols, seg_g0, seg_g1);
       const int n_mma = (ncols + 15) & ~15;
       const int64_t m0 = int64_t(T.mb) * kTileM;
       const int64_t tok = m0 + row;
       const bool valid = tok < P.m;
-      const uint32_t acc = acc_it & 1;
-      mbar_wait(&tmem_full[acc], (acc_it / 2) & 1);
+      const uint32_t acc = acc_it % kAccBufs;
+      mbar_wait(&tmem_full[acc], (acc_it / kAccBufs) & 1);
       tc_fence_after();
       const uint32_t trow = tmem_base + acc * kMaxTileN + (uint32_t((warp & 3) * 32) << 16);
 
@@ -462,14 +512,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ntok = int(P.m - m0 < kTileM ? P.m - m0 : kTileM);
         const bool last = ntok < kTileM;
         uint8_t *tile_base = P.payload + T.mb * P.tile_bytes;
-        const float *bias = P.bias + n0;
-        const int f32_col = P.segs[T.nb].f32_col;
+        const int nsub = tile_nsub<NSUB>(P, T);
+        for (int sb = 0; sb < nsub; ++sb) {
+        const SegDesc sdq = P.segs[T.nb * NSUB + sb];
+        const uint32_t trow_s = trow + (NSUB == 2 ? uint32_t(sb * kMaxTileN) : 0u);
+        const float *bias = P.bias + sdq.col0;
+        const int f32_col = sdq.f32_col;
+        const int ncols_s = sdq.width;
         if (f32_col >= 0) {
           // piece of a wide group: fp32 D - mu V_c to the scratch
           float *dst = P.D + (valid ? tok : 0) * P.ldd + f32_col;
-          for (int c = 0; c < ncols; c += 16) {
+          for (int c = 0; c < ncols_s; c += 16) {
             float x[16];
-            load_cols(trow, bias, c, 16, x);
+            load_cols(trow_s, bias, c, 16, x);
             if (valid) {
 #pragma unroll
               for (int j = 0; j < 16; j += 4)
@@ -477,13 +532,104 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        for (int gi = seg_g0; gi < seg_g1; ++gi) {
+        // sub-byte code block of one group (tokens of size * bits < 8 bits): OR-reduction over the warp
+        auto emit_subbyte = [&](const GroupDesc &g, uint32_t bits_v) {
+          const int nb = g.full_size * bits_of(g.type);
+          const int bitpos = lane * nb;
+          uint8_t *cb = tile_base + (last ? P.codes_off_last[g.gidx] : g.codes_off);
+          const int64_t blk_len = (int64_t(ntok) * nb + 7) / 8;
+          const int64_t warp_byte0 = int64_t((warp & 3) * 32) * nb / 8;
+          for (int w = 0; w < nb; ++w) {
+            uint32_t mine = 0;
+            if ((bitpos >> 5) == w) mine = bits_v << (bitpos & 31);
+            if (((bitpos + nb - 1) >> 5) == w && (bitpos >> 5) != w) mine = bits_v >> (32 - (bitpos & 31));
+            const uint32_t word = __reduce_or_sync(0xffffffffu, mine);
+            if (lane == w) {
+              const int64_t off = warp_byte0 + 4 * w;
+              if (!last) {
+                *reinterpret_cast<uint32_t *>(cb + off) = word;
+              } else {
+                for (int k = 0; k < 4; ++k)
+                  if (off + k < blk_len) cb[off + k] = (word >> (8 * k)) & 0xFF;
+              }
+            }
+          }
+        };
+        auto store_params = [&](const GroupDesc &g, uint16_t sh, uint16_t sc) {
+          if (valid && g.part == 0)
+            store_u32_any(tile_base + 4 * (int64_t(g.gidx) * ntok + row), uint32_t(sh) | (uint32_t(sc) << 16), !last);
+        };
+        for (int gi = sdq.g_begin; gi < sdq.g_end;) {
           const GroupDesc gd = P.groups[gi];
+          if (gd.full_size == 1) {
+            // a run of size-1 groups (the DP's fp16-exact "keep" option, Q1): up to 16
+            // columns per TMEM load instead of two single-column round trips each
+            int n = 1;
+            while (n < 16 && gi + n < sdq.g_end && P.groups[gi + n].full_size == 1) ++n;
+            float v[16];
+            if (gd.col + 16 <= kMaxTileN) {
+              tmem_ld16(trow_s + gd.col, v);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) v[j] = j < n ? tmem_ld1(trow_s + gd.col + j) : 0.0f;
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              if (j >= n) break;
+              const GroupDesc g = P.groups[gi + j];
+              const float x = __fsub_rn(v[j], bias[g.col]);
+              uint16_t sh, sc;
+              group_factors(g.type, x, x, sh, sc);
+              store_params(g, sh, sc);
+              emit_subbyte(g, valid ? encode_one(g.type, x, f16_val(sh), f16_val(sc)) : 0u);
+            }
+            gi += n;
+            continue;
+          }
+          if (gd.size % 16 == 0 && gd.size <= 64 && gd.size == gd.full_size) {
+            // one TMEM pass: all columns in registers (one wait), min/max, encode
+            const int nq = gd.size / 16;
+            uint32_t r[64];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (q < nq) tmem_ld16_nw(trow_s + gd.col + 16 * q, r + 16 * q);
+            tmem_wait_ld();
+            float mn = INFINITY, mx = -INFINITY;
+#pragma unroll
+            for (int j = 0; j < 64; ++j) {
+              if (j < gd.size) {
+                const float x = __fsub_rn(__uint_as_float(r[j]), bias[gd.col + j]);
+                mn = fminf(mn, x);
+                mx = fmaxf(mx, x);
+              }
+            }
+            uint16_t sh, sc;
+            group_factors(gd.type, mn, mx, sh, sc);
+            store_params(gd, sh, sc);
+            const int bq = bits_of(gd.type);
+            uint8_t *cb = tile_base + (last ? P.codes_off_last[gd.gidx] : gd.codes_off);
+            if (valid) {
+              const float shift = f16_val(sh), scale = f16_val(sc);
+              uint8_t *dst = cb + int64_t(row) * (gd.size * bq / 8);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                if (q < nq) {
+                  float x[16];
+#pragma unroll
+                  for (int j = 0; j < 16; ++j) x[j] = __fsub_rn(__uint_as_float(r[16 * q + j]), bias[gd.col + 16 * q + j]);
+                  write_codes16(dst + 2 * q * bq, x, gd.type, shift, scale, !last);
+                }
+              }
+            }
+            ++gi;
+            continue;
+          }
+          // generic: two TMEM passes (groups and pieces wider than 64 columns)
           const int step = (gd.size % 16 == 0) ? 16 : 1;
           float mn = INFINITY, mx = -INFINITY;
           for (int c = 0; c < gd.size; c += step) {
             float x[16];
-            load_cols(trow, bias, gd.col + c, step, x);
+            load_cols(trow_s, bias, gd.col + c, step, x);
             for (int j = 0; j < step; ++j) {
               mn = fminf(mn, x[j]);
               mx = fmaxf(mx, x[j]);
@@ -492,9 +638,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint16_t sh, sc;
           group_factors(gd.type, mn, mx, sh, sc);
           const float shift = f16_val(sh), scale = f16_val(sc);
-          if (valid && gd.part == 0)
-            store_u32_any(tile_base + 4 * (int64_t(gd.gidx) * ntok + row), uint32_t(sh) | (uint32_t(sc) << 16),
-                          !last);
+          store_params(gd, sh, sc);
           const int bq = bits_of(gd.type);
           const int tok_bits = gd.full_size * bq;
           uint8_t *cb = tile_base + (last ? P.codes_off_last[gd.gidx] : gd.codes_off);
@@ -502,35 +646,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint8_t *dst = cb + int64_t(row) * (tok_bits / 8) + gd.part * (gd.size * bq / 8);
             for (int c = 0; c < gd.size; c += step) {
               float x[16];
-              load_cols(trow, bias, gd.col + c, step, x);
+              load_cols(trow_s, bias, gd.col + c, step, x);
               if (valid) write_codes_aligned(dst + (c * bq) / 8, x, step, gd.type, shift, scale, !last);
             }
           } else {
-            // sub-byte tokens (size * bits < 8): warp OR-reduction, as in emit_group
             float x[16];
-            load_cols(trow, bias, gd.col, gd.size, x);
+            load_cols(trow_s, bias, gd.col, gd.size, x);
             uint32_t bits_v = 0;
             for (int c = 0; c < gd.size; ++c) bits_v |= (valid ? encode_one(gd.type, x[c], shift, scale) : 0u) << (c * bq);
-            const int nb = tok_bits;
-            const int bitpos = lane * nb;
-            const int64_t blk_len = (int64_t(ntok) * nb + 7) / 8;
-            const int64_t warp_byte0 = int64_t((warp & 3) * 32) * nb / 8;
-            for (int w = 0; w < nb; ++w) {
-              uint32_t mine = 0;
-              if ((bitpos >> 5) == w) mine = bits_v << (bitpos & 31);
-              if (((bitpos + nb - 1) >> 5) == w && (bitpos >> 5) != w) mine = bits_v >> (32 - (bitpos & 31));
-              const uint32_t word = __reduce_or_sync(0xffffffffu, mine);
-              if (lane == w) {
-                const int64_t off = warp_byte0 + 4 * w;
-                if (!last) {
-                  *reinterpret_cast<uint32_t *>(cb + off) = word;
-                } else {
-                  for (int k = 0; k < 4; ++k)
-                    if (off + k < blk_len) cb[off + k] = (word >> (8 * k)) & 0xFF;
-                }
-              }
-            }
+            emit_subbyte(gd, bits_v);
           }
+          ++gi;
+        }
         }
         tc_fence_before();
         release_acc(acc);
@@ -652,16 +779,17 @@ static int num_sms() {
   return n;
 }
 
-template <int MODE, bool PAIR>
+template <int MODE, bool PAIR, int NSUB = 1>
 static kvtc_status launch(const CUtensorMap *tmA, const CUtensorMap *tmB, const Params &p, dim3 grid, int cluster,
                           cudaStream_t st) {
   static bool configured = false;
-  constexpr int kSmemBytes = Cfg<PAIR>::kSmemBytes;
+  constexpr int kSmemBytes = Cfg<PAIR, NSUB>::kSmemBytes;
   if (!configured) {
-    KVTC_CUDA_TRY(
-        cudaFuncSetAttribute(gemm_kernel<MODE, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    KVTC_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<MODE, PAIR, NSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kSmemBytes));
     // the 228 KB configuration, shared with the side-stream kernels (internal.h)
-    KVTC_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<MODE, PAIR>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    KVTC_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<MODE, PAIR, NSUB>,
+                                       cudaFuncAttributePreferredSharedMemoryCarveout,
                                        int(cudaSharedmemCarveoutMaxShared)));
     configured = true;
   }
@@ -681,6 +809,12 @@ static kvtc_status launch(const CUtensorMap *tmA, const CUtensorMap *tmB, const 
     // over modes overrides (0 = off)
     const char *ts = getenv("KVTC_TILE_SYNC");
     const int sync_mask = ts ? atoi(ts) : ((1 << EPI_QUANT) | (1 << EPI_RECON));
+    // lag: compress tiles (512 k-steps) must start together; decompress tiles (68
+    // k-steps) tolerate one tile of drift (KVTC_SYNC_LAG_<MODE> overrides)
+    static const char *lag_names[4] = {"KVTC_SYNC_LAG_F32", "KVTC_SYNC_LAG_QUANT", "KVTC_SYNC_LAG_RECON",
+                                       "KVTC_SYNC_LAG_XTX"};
+    const char *lg = getenv(lag_names[MODE]);
+    pp.sync_lag = lg ? std::max(0, atoi(lg)) : (MODE == EPI_RECON ? 1 : 0);
     if ((sync_mask >> MODE) & 1) {
       if (!(pp.tile_sync = next_sync_counter())) return KVTC_E_CUDA;
       KVTC_CUDA_TRY(cudaMemsetAsync(pp.tile_sync, 0, sizeof(unsigned long long), st));
@@ -698,7 +832,7 @@ static kvtc_status launch(const CUtensorMap *tmA, const CUtensorMap *tmB, const 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  KVTC_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_kernel<MODE, PAIR>, *tmA, *tmB, pp));
+  KVTC_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_kernel<MODE, PAIR, NSUB>, *tmA, *tmB, pp));
   note_launch();
   return KVTC_OK;
 }
@@ -738,9 +872,18 @@ kvtc_status launch_gemm_project_quant(const GemmCompressArgs &a, cudaStream_t st
   p.a_hd = a.a_hd;
   p.a_row0 = a.a_row0;
   p.num_m = int32_t(ceil_div(a.m, kTileM));
-  p.num_n = a.nsegs;
+  p.nsegs = a.nsegs;
   p.D = a.D;
   p.ldd = a.ldd;
+  // KVTC_QUANT_NSUB=2: two segments per tile (Cfg<true, 2>, 25 % less L2 traffic);
+  // measured slower (tensor pipe 58 % vs 88 %: the 512-column epilogue is not
+  // overlapped), so one segment per tile with double-buffered TMEM is the default
+  const char *e = getenv("KVTC_QUANT_NSUB");
+  if (e && atoi(e) == 2) {
+    p.num_n = (a.nsegs + 1) / 2;
+    return launch<EPI_QUANT, true, 2>(a.tmA, a.tmB, p, dim3(pair_grid(int64_t((p.num_m + 1) / 2) * p.num_n)), 2, st);
+  }
+  p.num_n = a.nsegs;
   return launch<EPI_QUANT, true>(a.tmA, a.tmB, p, dim3(pair_grid(int64_t((p.num_m + 1) / 2) * p.num_n)), 2, st);
 }
 

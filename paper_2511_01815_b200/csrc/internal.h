@@ -158,7 +158,8 @@ kvtc_status launch_deflate(const uint8_t *in, size_t n, int32_t chunk, uint8_t *
 // > 0 bounds the grid so the kernel can run beside a persistent GEMM), then the
 // section layout + copy to out (workspace untouched in between).
 kvtc_status launch_deflate_encode(const uint8_t *in, size_t n, int32_t chunk, void *ws, size_t ws_bytes,
-                                  int32_t max_ctas, cudaStream_t st);
+                                  int32_t max_ctas, cudaStream_t st, uint32_t c_begin = 0,
+                                  uint32_t c_end = 0xFFFFFFFFu);   // chunk range [c_begin, c_end)
 kvtc_status launch_deflate_assemble(size_t n, int32_t chunk, const void *ws, uint8_t *out, const uint64_t *off_dev,
                                     uint64_t *section_len_dev, cudaStream_t st);
 // SM count x per_sm: the bounded grid of a side-stream kernel overlapping a GEMM.

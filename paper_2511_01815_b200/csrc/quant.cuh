@@ -55,6 +55,24 @@ __device__ __forceinline__ void write_codes_aligned(uint8_t *dst, const float *x
   }
 }
 
+// The codes of 16 coefficients (byte-aligned), fully unrolled so x stays in registers.
+__device__ __forceinline__ void write_codes16(uint8_t *dst, const float *x, int type, float shift, float scale,
+                                              bool aligned4) {
+  uint32_t c[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) c[j] = encode_one(type, x[j], shift, scale);
+  const int b = bits_of(type);
+  const int per = 32 / b;                       // codes per 32-bit word: 16 / 8 / 4
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    if (w * per >= 16) break;
+    uint32_t v = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (j >= w * per && j < (w + 1) * per) v |= c[j] << ((j - w * per) * b);
+    store_u32_any(dst + 4 * w, v, aligned4);
+  }
+}
 
 // Emit shift/scale (part 0 only) and the codes of one (token, group piece).
 //   x: the piece's fp32 coefficients (D - mu V_c), mn/mx: the row min/max over

@@ -59,6 +59,28 @@ def mid_plan_groups():
     return g
 
 
+def runs_plan_groups():
+    """Explicit plan over 2048 PCs with long runs of size-1 groups (the DP's
+    fp16-exact option, 112 of them in the bench plan): a run of 40 from column 0,
+    and one that crosses the 256-column segment boundary from an unaligned
+    compacted column (120), so the fused epilogue's 16-column batches hit the
+    segment edge."""
+    g = []
+    c = 0
+    types = (T2, T4, T8)
+    for i in range(40):
+        g.append((c, 1, types[i % 3])); c += 1
+    g.append((c, 16, T4)); c += 16
+    g.append((c, 64, T2)); c += 64
+    c += 3                                          # None gap
+    for i in range(150):
+        g.append((c, 1, types[(i + 1) % 3])); c += 1
+    g.append((c, 64, T8)); c += 64
+    g.append((c, 256, T4)); c += 256
+    assert c <= 2048
+    return g
+
+
 def toy_plans(cr: float = 16):
     spec, invf, kb, vb, Ck, Cv = setup("toy")
     kp, _, _ = ODP.allocate(OPCA.dp_coefficients(kb, Ck), cr, spec.p)

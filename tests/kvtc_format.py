@@ -12,11 +12,12 @@ CONTAINER_HDR = struct.Struct("<II6iqqqQQ2Q2Q2Q2QQ2Q")
 
 def parse_section(buf: bytes):
     magic, ver, raw, chunk, nch, seg, nseg, data_off, total = SECTION_HDR.unpack_from(buf, 0)
-    assert magic == 0x4454564B and ver == 2
+    assert magic == 0x4454564B and ver == 3
     tab = np.frombuffer(buf, dtype=np.dtype([("off", "<u8"), ("bytes", "<u4"), ("kind", "<u4")]), count=nch,
                         offset=64)
     idx = np.frombuffer(buf, dtype="<u2", count=nch * nseg, offset=64 + 16 * nch).reshape(nch, nseg)
-    assert data_off == 64 + 16 * nch + ((2 * nch * nseg + 3) & ~3)
+    assert data_off == 64 + 16 * nch + ((2 * nch * nseg + 15) & ~15)
+    assert all(int(e["off"]) % 16 == 0 for e in tab)
     streams = [buf[data_off + int(e["off"]): data_off + int(e["off"]) + int(e["bytes"])] for e in tab]
     return dict(raw=raw, chunk=chunk, nchunks=nch, seg=seg, nseg=nseg, data_off=data_off, total=total,
                 table=tab, index=idx, streams=streams)

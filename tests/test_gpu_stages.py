@@ -64,10 +64,12 @@ def test_gather_paged_layout(K):
 
 
 def _plan_for(name):
-    spec, invf, kb, vb, Ck, Cv = E.setup(name)
     if name == "toy":
         kp, vp = E.toy_plans(16)
         return kp.groups, vp.groups
+    if name == "mid-runs":
+        g = E.runs_plan_groups()
+        return g, g
     g = E.mid_plan_groups()
     return g, g
 
@@ -86,10 +88,11 @@ def test_project_fp32(K, name, tokens):
     assert err < 2e-5, err
 
 
-@pytest.mark.parametrize("name,tokens", [("toy", 512), ("mid", 1000), ("mid", 132 + 128 * 3)])
+@pytest.mark.parametrize("name,tokens", [("toy", 512), ("mid", 1000), ("mid", 132 + 128 * 3), ("mid-runs", 777)])
 def test_quantize_pack_and_fused(K, name, tokens):
-    spec, invf, kb, vb, Ck, Cv = E.setup(name)
     gk, gv = _plan_for(name)
+    name = "mid" if name == "mid-runs" else name
+    spec, invf, kb, vb, Ck, Cv = E.setup(name)
     Kc, Vc = E.caches(name, tokens, 0)
     m = tokens - 132
     shape = (spec.layers, spec.kv_heads, spec.head_dim)
