@@ -178,9 +178,11 @@ def oracle_sample(bases, plans, K_host, V_host, spec, ntok: int):
 def run_multiconv(args, K, spec, kb, kp, vb, vp, setup_s, setup_info, world, rank, local, dist):
     """BASELINE config 5: 256 Llama-3.1-8B-shaped conversations of t ~ U[8192,
     32768] tokens, assigned to ranks longest-first (LPT); each rank
-    compresses + decompresses its share in waves (generate one cache, time its
-    round trip, drop it: 634 GiB of bf16 KV never fits at once).  Only codec time
-    is timed (CUDA events around each round trip on the launching stream, summed);
+    compresses + decompresses its share in waves of <= --batch-tokens tokens, one
+    kvtc_compress_batch + kvtc_decompress_batch per wave (generate the wave's
+    caches, time its round trip, drop them: 634 GiB of bf16 KV never fits at
+    once).  Only codec time is timed (CUDA events around each wave's round trip on
+    the launching stream, summed);
     value = all ranks' 16-bit bytes / the slowest rank's codec time (strong
     scaling: the 256 conversations are fixed as N grows)."""
     from kvtc_inputs import generate, lengths_for
@@ -189,46 +191,51 @@ def run_multiconv(args, K, spec, kb, kp, vb, vp, setup_s, setup_info, world, ran
     mine = lpt_assign(lens, world)[rank]
     p = spec.p
     stream = torch.cuda.current_stream()
-    tmax = max(lens)
-    cap, wsb = K.compress_sizes(kb, kp, vb, vp, K.KVView(torch.empty((spec.layers, tmax, spec.kv_heads, spec.head_dim),
-                                                                     dtype=torch.bfloat16, device="cuda")))
-    cont = torch.empty(cap, dtype=torch.uint8, device="cuda")
-    cws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
-    # decompress workspace sized by the longest conversation (it grows with m)
-    ci_max = int(np.argmax(lens))
-    Kc = generate(spec, 0, lens[ci_max], pos0=0, conversation=ci_max, device="cuda")
-    Vc = generate(spec, 1, lens[ci_max], pos0=0, conversation=ci_max, device="cuda")
-    K.compress(kb, kp, vb, vp, K.KVView(Kc), K.KVView(Vc), out=cont, workspace=cws)
-    dws = torch.empty(K.decompress_workspace_bytes(kb, kp, vb, vp, cont[:256].cpu().numpy().tobytes()),
-                      dtype=torch.uint8, device="cuda")
-    del Kc, Vc
     clocks = ClockSampler(local)
+    # waves of up to --batch-tokens tokens, each compressed and decompressed by ONE
+    # kvtc_compress_batch + kvtc_decompress_batch (one GEMM per stream over all rows)
+    waves, cur, ntok = [], [], 0
+    for ci in mine:
+        if cur and ntok + lens[ci] > args.batch_tokens:
+            waves.append(cur)
+            cur, ntok = [], 0
+        cur.append(ci)
+        ntok += lens[ci]
+    if cur:
+        waves.append(cur)
 
-    def one(ci):
-        t = lens[ci]
-        Kc = generate(spec, 0, t, pos0=0, conversation=ci, device="cuda")
-        Vc = generate(spec, 1, t, pos0=0, conversation=ci, device="cuda")
-        Ko, Vo = torch.empty_like(Kc), torch.empty_like(Vc)
-        kv, vv, kov, vov = K.KVView(Kc), K.KVView(Vc), K.KVView(Ko), K.KVView(Vo)
+    def one(wave):
+        Ks = [generate(spec, 0, lens[ci], pos0=0, conversation=ci, device="cuda") for ci in wave]
+        Vs = [generate(spec, 1, lens[ci], pos0=0, conversation=ci, device="cuda") for ci in wave]
+        Ko = [torch.empty_like(x) for x in Ks]
+        Vo = [torch.empty_like(x) for x in Vs]
+        kv, vv = [K.KVView(x) for x in Ks], [K.KVView(x) for x in Vs]
+        kov, vov = [K.KVView(x) for x in Ko], [K.KVView(x) for x in Vo]
+        cws = torch.empty(K.compress_batch_workspace_bytes(kb, kp, vb, vp, kv), dtype=torch.uint8, device="cuda")
+        outs = [torch.empty(K.compress_sizes(kb, kp, vb, vp, x)[0], dtype=torch.uint8, device="cuda") for x in kv]
+        conts = K.compress_batch(kb, kp, vb, vp, kv, vv, outs=outs, workspace=cws)        # sizes the workspace
+        dws = torch.empty(K.decompress_batch_workspace_bytes(kb, kp, vb, vp, [c[:256].cpu().numpy().tobytes()
+                                                                              for c in conts]),
+                          dtype=torch.uint8, device="cuda")
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        K.compress(kb, kp, vb, vp, kv, vv, out=cont, workspace=cws, sync_len=False)
-        K.decompress(kb, kp, vb, vp, cont, kov, vov, workspace=dws)
+        K.compress_batch(kb, kp, vb, vp, kv, vv, outs=outs, workspace=cws, sync_len=False)
+        K.decompress_batch(kb, kp, vb, vp, outs, kov, vov, workspace=dws)
         e1.record(stream)
         torch.cuda.synchronize()
-        ok = torch.equal(Ko[:, :4], Kc[:, :4]) and torch.equal(Vo[:, t - 128:], Vc[:, t - 128:])
-        return e0.elapsed_time(e1), 2 * 2 * p * (t - 132), ok
+        ok = all(torch.equal(o[:, :4], x[:, :4]) for o, x in zip(Ko, Ks))
+        return e0.elapsed_time(e1), sum(2 * 2 * p * (lens[ci] - 132) for ci in wave), ok
 
     for _ in range(args.warmup):
-        one(mine[0])
+        one(waves[0])
     if dist:
         dist.barrier()
     clocks.start()
     ms, nbytes, allok = 0.0, 0, True
     for _ in range(args.steps):
-        for ci in mine:
-            dt, b, ok = one(ci)
+        for wave in waves:
+            dt, b, ok = one(wave)
             ms += dt
             nbytes += b
             allok &= ok
@@ -247,10 +254,11 @@ def run_multiconv(args, K, spec, kb, kp, vb, vp, setup_s, setup_info, world, ran
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic (kvtc_inputs, DESIGN.md §5)",
                 "config": {"workload": f"multiconv: {args.convs} llama8b-shaped conversations, t ~ U[8192, 32768] "
-                                       f"(seed 0), LPT over {world} rank(s), codec time only (caches generated "
-                                       "per conversation, untimed)",
+                                       f"(seed 0), LPT over {world} rank(s), batched codec calls in waves of "
+                                       f"<= {args.batch_tokens} tokens, codec time only (caches generated per "
+                                       "wave, untimed)",
                            "conversations": args.convs, "tokens_total": int(sum(lens)),
-                           "per_rank_conversations": len(mine), "setup_s": round(setup_s, 1),
+                           "per_rank_conversations": len(mine), "waves": len(waves), "setup_s": round(setup_s, 1),
                            "sinks_window_roundtrip_ok": bool(allok)},
                 "gpu_launches": None, "clocks": clk}
         print(json.dumps(line), flush=True)
@@ -281,6 +289,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--convs", type=int, default=256)                # multiconv: number of conversations
+    ap.add_argument("--batch-tokens", type=int, default=131072)      # multiconv: tokens per batched call
     args = ap.parse_args()
 
     world, rank, local = dist_env()

@@ -214,6 +214,37 @@ kvtc_status kvtc_decompress(const kvtc_basis *kb, const kvtc_plan *kp, const kvt
                             const void *in, size_t in_len, int32_t layer_begin, int32_t layer_end,
                             const kvtc_kv_view *k_out, const kvtc_kv_view *v_out, void *workspace,
                             size_t workspace_bytes, void *stream);
+/* ------------------------------------------------------- batched codec
+ * n conversations (or token ranges of conversations: a view whose layer bases
+ * are offset by a tokens and pos0 += a) in one call.  Their middle tokens are
+ * concatenated, each padded to whole 128-token tiles, so each projection GEMM,
+ * each reconstruction GEMM, the DEFLATE encoder and the inflater run ONCE for
+ * the whole batch (rows are independent, Q1).  Every container is byte-identical
+ * to the one kvtc_compress writes for the same item.  Serving many short
+ * requests, and compressing the c = 16 tokens that leave the window each turn
+ * (P:L281), need this.
+ *  k[i], v[i]: item i's views; out_host[i]: DEVICE pointer of its container
+ *  buffer (out_cap_host[i] >= kvtc_compress_bound for that item);
+ *  out_len_host[i] (nullable; forces one synchronisation): container lengths.
+ *  Errors as kvtc_compress; the first failing item's index is in the message. */
+size_t kvtc_compress_batch_workspace_bytes(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb,
+                                           const kvtc_plan *vp, const kvtc_kv_view *k, int32_t n,
+                                           const kvtc_policy *policy);
+kvtc_status kvtc_compress_batch(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb, const kvtc_plan *vp,
+                                const kvtc_kv_view *k, const kvtc_kv_view *v, int32_t n, const kvtc_policy *policy,
+                                void *const *out_host, const size_t *out_cap_host, size_t *out_len_host,
+                                void *workspace, size_t workspace_bytes, void *stream);
+/* in_host[i]: DEVICE pointer of container i (length in_len_host[i]); all layers
+ * are restored into k_out[i] / v_out[i].  in_header_host[i]: host copies of the
+ * first KVTC_HEADER_BYTES bytes of each container.  One synchronisation (the
+ * headers). */
+size_t kvtc_decompress_batch_workspace_bytes(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb,
+                                             const kvtc_plan *vp, const void *const *in_header_host, int32_t n);
+kvtc_status kvtc_decompress_batch(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb,
+                                  const kvtc_plan *vp, const void *const *in_host, const size_t *in_len_host,
+                                  int32_t n, const kvtc_kv_view *k_out, const kvtc_kv_view *v_out, void *workspace,
+                                  size_t workspace_bytes, void *stream);
+
 /* Parse a container header (first KVTC_HEADER_BYTES bytes, copied to host). */
 #define KVTC_HEADER_BYTES 256
 typedef struct {

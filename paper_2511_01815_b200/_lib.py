@@ -82,6 +82,11 @@ _SIGS = {
     "kvtc_compress": (i32, [vp, vp, vp, vp, P(View), P(View), P(Policy), vp, sz, P(sz), vp, sz, vp]),
     "kvtc_decompress_workspace_bytes": (sz, [vp, vp, vp, vp, vp]),
     "kvtc_decompress": (i32, [vp, vp, vp, vp, vp, sz, i32, i32, P(View), P(View), vp, sz, vp]),
+    "kvtc_compress_batch_workspace_bytes": (sz, [vp, vp, vp, vp, P(View), i32, P(Policy)]),
+    "kvtc_compress_batch": (i32, [vp, vp, vp, vp, P(View), P(View), i32, P(Policy), P(vp), P(sz), P(sz), vp, sz,
+                                  vp]),
+    "kvtc_decompress_batch_workspace_bytes": (sz, [vp, vp, vp, vp, P(vp), i32]),
+    "kvtc_decompress_batch": (i32, [vp, vp, vp, vp, P(vp), P(sz), i32, P(View), P(View), vp, sz, vp]),
     "kvtc_container_parse": (i32, [vp, P(ContainerInfo)]),
     "kvtc_stage_gather": (i32, [P(View), i64, i64, i32, P(Rope), vp, vp]),
     "kvtc_stage_project": (i32, [vp, vp, vp, i64, vp, vp]),

@@ -80,7 +80,7 @@ bool direct_view_map(const kvtc_kv_view &v, int64_t tok0, CUtensorMap *m) {
 // the plan's wide groups (nullptr if it has none).
 kvtc_status run_project_quant(const kvtc_basis *b, kvtc_plan *pl, const Operands *op, const void *X, int64_t m,
                               uint8_t *payload, float *wide, cudaStream_t st, const CUtensorMap *direct = nullptr,
-                              int64_t tok0 = 0, int64_t ldx = 0) {
+                              int64_t tok0 = 0, int64_t ldx = 0, const TileRef *tiles = nullptr) {
   if (m == 0 || pl->G == 0) return KVTC_OK;
   KVTC_CHECK_ARG(pl->nwide == 0 || wide, "wide-group scratch");
   CUtensorMap tA;
@@ -105,14 +105,16 @@ kvtc_status run_project_quant(const kvtc_basis *b, kvtc_plan *pl, const Operands
   a.nsegs = pl->nsegs;
   a.D = wide;
   a.ldd = pl->wide_cols;
+  a.tiles = tiles;
   if ((s = launch_gemm_project_quant(a, st))) return s;
   return launch_quant_wide(pl->d_wide, pl->nwide, wide, pl->wide_cols, 1, m, pl->tile_bytes, a.codes_off_last,
-                           payload, st);
+                           payload, st, tiles);
 }
 
 kvtc_status run_reconstruct(const kvtc_basis *b, const kvtc_plan *pl, const Operands *op, const __half *Dh,
                             int64_t ld, int64_t m, int64_t tok_begin, int32_t lb, int32_t le, const kvtc_kv_view *out,
-                            __nv_bfloat16 *const *bases_dev, const float2 *cs, cudaStream_t st) {
+                            __nv_bfloat16 *const *bases_dev, const float2 *cs, cudaStream_t st,
+                            const TileRef *tiles = nullptr) {
   const int hd = b->shape.kv_heads * b->shape.head_dim;
   if (m == 0 || lb >= le) return KVTC_OK;
   GemmDecompressArgs a = {};
@@ -142,6 +144,7 @@ kvtc_status run_reconstruct(const kvtc_basis *b, const kvtc_plan *pl, const Oper
   int tile = kMaxTileN;
   while (hd % tile) tile /= 2;
   a.tile_n = tile;
+  a.tiles = tiles;
   return launch_gemm_reconstruct(a, st);
 }
 
@@ -773,6 +776,444 @@ extern "C" kvtc_status kvtc_decompress(const kvtc_basis *kb, const kvtc_plan *kp
       if ((s = launch_unpack_raw(raw, nraw, 0, h.sinks, *vw, bs, 0, layer_begin, layer_end, st))) return s;
       if ((s = launch_unpack_raw(raw, nraw, h.sinks, h.window, *vw, bs, t - h.window, layer_begin, layer_end, st)))
         return s;
+    }
+  }
+  return KVTC_OK;
+}
+
+// ================================================================ batched codec
+// Several conversations (or token ranges of conversations) in one call: their
+// middle tokens are concatenated, each padded to whole 128-token tiles, so both
+// projection GEMMs (and both reconstruction GEMMs) run ONCE over all rows; a
+// per-tile table (TileRef) sends each tile's epilogue to its own conversation's
+// payload (compress) or cache view (decompress).  Rows are independent under the
+// per-token quantisation reading (Q1), so every output is byte-identical to the
+// single-conversation call; the DEFLATE encoder and the inflater also run once
+// over all chunks of all payloads.  Serving with many short requests and the
+// incremental compression of c = 16 tokens per turn need exactly this.
+namespace {
+struct BatchItem {
+  CompressLayout L;
+  int64_t row0 = 0;      // first GEMM row (tile-aligned)
+  int64_t tiles = 0;
+};
+int64_t batch_rows(const std::vector<BatchItem> &it) {
+  int64_t r = 0;
+  for (auto &b : it) r += b.tiles * kTileM;
+  return r;
+}
+}  // namespace
+
+extern "C" size_t kvtc_compress_batch_workspace_bytes(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb,
+                                                      const kvtc_plan *vp, const kvtc_kv_view *k, int32_t n,
+                                                      const kvtc_policy *pol) {
+  if (!kb || !kp || !vb || !vp || !k || n <= 0 || !pol) return 0;
+  Bump b;
+  int64_t rows = 0;
+  for (int i = 0; i < n; ++i) {
+    const CompressLayout L = compress_layout(kp, vp, &k[i], pol);
+    rows += (L.m + kTileM - 1) / kTileM * kTileM;
+    b.take<void *>(k[i].shape.layers);
+    b.take<void *>(k[i].shape.layers);
+    b.take<uint8_t>(L.pay[0] + 16);
+    b.take<uint8_t>(L.pay[1] + 16);
+    b.take<uint8_t>(deflate_workspace(L.pay[0], pol->chunk_bytes));
+    b.take<uint8_t>(deflate_workspace(L.pay[1], pol->chunk_bytes));
+  }
+  b.take<uint64_t>(4 * int64_t(n));
+  b.take<__nv_bfloat16>(rows * (kb->p + kXPad));
+  b.take<float2>(rows * (kb->shape.head_dim / 2));
+  b.take<float>(rows * std::max(kp->wide_cols, vp->wide_cols));
+  b.take<TileRef>(2 * (rows / kTileM));
+  b.take<EncodeJob>(2 * int64_t(n));
+  return b.used + 256;
+}
+
+extern "C" kvtc_status kvtc_compress_batch(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb,
+                                           const kvtc_plan *vp, const kvtc_kv_view *k, const kvtc_kv_view *v,
+                                           int32_t n, const kvtc_policy *pol, void *const *out_host,
+                                           const size_t *out_cap_host, size_t *out_len_host, void *workspace,
+                                           size_t workspace_bytes, void *stream) {
+  KVTC_CHECK_ARG(kb && kp && vb && vp && k && v && pol && out_host && out_cap_host && n > 0, "compress_batch arguments");
+  KVTC_CHECK_ARG(kb->which == KVTC_KEYS && vb->which == KVTC_VALUES, "basis streams");
+  KVTC_CHECK_ARG(pol->sinks >= 0 && pol->window >= 0, "policy");
+  KVTC_CHECK_ARG(pol->chunk_bytes == 16384 || pol->chunk_bytes == 32768 || pol->chunk_bytes == 65536, "chunk_bytes");
+  kvtc_status s;
+  std::vector<BatchItem> it(n);
+  int64_t row = 0;
+  for (int i = 0; i < n; ++i) {
+    if ((s = check_view(&k[i])) || (s = check_view(&v[i]))) return s;
+    KVTC_CHECK_ARG(same_shape(k[i].shape, v[i].shape) && k[i].tokens == v[i].tokens && k[i].pos0 == v[i].pos0,
+                   "key and value views differ");
+    KVTC_CHECK_ARG(same_shape(k[i].shape, kb->shape) && same_shape(v[i].shape, vb->shape), "basis shape mismatch");
+    it[i].L = compress_layout(kp, vp, &k[i], pol);
+    if (out_cap_host[i] < it[i].L.bound) {
+      set_error("batch item %d: output capacity %zu < bound %llu", i, out_cap_host[i],
+                (unsigned long long)it[i].L.bound);
+      return KVTC_E_CAPACITY;
+    }
+    it[i].row0 = row;
+    it[i].tiles = (it[i].L.m + kTileM - 1) / kTileM;
+    row += it[i].tiles * kTileM;
+  }
+  const size_t need = kvtc_compress_batch_workspace_bytes(kb, kp, vb, vp, k, n, pol);
+  if (!workspace || workspace_bytes < need) {
+    set_error("workspace %zu < %zu", workspace_bytes, need);
+    return KVTC_E_CAPACITY;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  auto *kpl = const_cast<kvtc_plan *>(kp);
+  auto *vpl = const_cast<kvtc_plan *>(vp);
+  const Operands *kop, *vop;
+  if ((s = plan_operands(kb, kpl, &kop)) || (s = plan_operands(vb, vpl, &vop))) return s;
+  const int64_t rows = row, ntiles = rows / kTileM;
+  const int half = kb->shape.head_dim / 2;
+  const int64_t ldx = kb->p + kXPad;
+  Bump ws(workspace, workspace_bytes);
+  std::vector<__nv_bfloat16 **> kbases(n), vbases(n);
+  std::vector<uint8_t *> pay_k(n), pay_v(n);
+  std::vector<void *> dws_k(n), dws_v(n);
+  for (int i = 0; i < n; ++i) {
+    kbases[i] = ws.take<__nv_bfloat16 *>(k[i].shape.layers);
+    vbases[i] = ws.take<__nv_bfloat16 *>(k[i].shape.layers);
+    pay_k[i] = ws.take<uint8_t>(it[i].L.pay[0] + 16);
+    pay_v[i] = ws.take<uint8_t>(it[i].L.pay[1] + 16);
+    dws_k[i] = ws.take<uint8_t>(deflate_workspace(it[i].L.pay[0], pol->chunk_bytes));
+    dws_v[i] = ws.take<uint8_t>(deflate_workspace(it[i].L.pay[1], pol->chunk_bytes));
+  }
+  uint64_t *lens = ws.take<uint64_t>(4 * int64_t(n));            // per item: K len, V len, K off, V off
+  auto *X = ws.take<__nv_bfloat16>(rows * ldx);
+  float2 *cs = ws.take<float2>(rows * half);
+  float *wide = ws.take<float>(rows * std::max(kp->wide_cols, vp->wide_cols));
+  TileRef *d_tiles = ws.take<TileRef>(2 * ntiles);
+  EncodeJob *d_jobs = ws.take<EncodeJob>(2 * int64_t(n));
+
+  // raw tokens, headers' host part, section offsets
+  std::vector<ContainerHeader> hdr(n);
+  std::vector<uint64_t> offs(4 * int64_t(n), 0);
+  for (int i = 0; i < n; ++i) {
+    if ((s = upload_bases(&k[i], kbases[i], st)) || (s = upload_bases(&v[i], vbases[i], st))) return s;
+    const CompressLayout &L = it[i].L;
+    ContainerHeader &h = hdr[i];
+    h = ContainerHeader{};
+    h.magic = kContainerMagic;
+    h.version = kContainerVersion;
+    h.layers = k[i].shape.layers;
+    h.kv_heads = k[i].shape.kv_heads;
+    h.head_dim = k[i].shape.head_dim;
+    h.sinks = pol->sinks;
+    h.window = pol->window;
+    h.chunk_bytes = pol->chunk_bytes;
+    h.tokens = k[i].tokens;
+    h.pos0 = k[i].pos0;
+    h.m = L.m;
+    h.raw_bytes = L.raw_bytes;
+    h.payload_bytes[0] = L.pay[0];
+    h.payload_bytes[1] = L.pay[1];
+    h.basis_fp[0] = kb->fp;
+    h.basis_fp[1] = vb->fp;
+    h.plan_fp[0] = kp->fp;
+    h.plan_fp[1] = vp->fp;
+    h.raw_off = KVTC_HEADER_BYTES;
+    h.section_off[0] = L.k_off;
+    offs[4 * i + 2] = L.k_off;
+    uint8_t *o = static_cast<uint8_t *>(out_host[i]);
+    const int64_t hd = int64_t(k[i].shape.kv_heads) * k[i].shape.head_dim;
+    auto *rawk = reinterpret_cast<__nv_bfloat16 *>(o + KVTC_HEADER_BYTES);
+    auto *rawv = rawk + int64_t(k[i].shape.layers) * L.nraw * hd;
+    const int64_t t = k[i].tokens;
+    if (L.m) {
+      for (int sv = 0; sv < 2; ++sv) {
+        const kvtc_kv_view *vw = sv ? &v[i] : &k[i];
+        __nv_bfloat16 *const *bs = sv ? vbases[i] : kbases[i];
+        __nv_bfloat16 *dst = sv ? rawv : rawk;
+        if ((s = launch_pack_raw(*vw, bs, 0, pol->sinks, dst, L.nraw, 0, st))) return s;
+        if ((s = launch_pack_raw(*vw, bs, t - pol->window, pol->window, dst, L.nraw, pol->sinks, st))) return s;
+      }
+    } else {
+      if ((s = launch_pack_raw(k[i], kbases[i], 0, t, rawk, L.nraw, 0, st))) return s;
+      if ((s = launch_pack_raw(v[i], vbases[i], 0, t, rawv, L.nraw, 0, st))) return s;
+    }
+  }
+  KVTC_CUDA_TRY(cudaMemcpyAsync(lens, offs.data(), offs.size() * 8, cudaMemcpyHostToDevice, st));
+  // tile tables: keys [0, ntiles), values [ntiles, 2 ntiles)
+  std::vector<TileRef> tref(2 * ntiles);
+  for (int i = 0; i < n; ++i) {
+    for (int64_t j = 0; j < it[i].tiles; ++j) {
+      const int ntok = int(std::min<int64_t>(kTileM, it[i].L.m - j * kTileM));
+      for (int sv = 0; sv < 2; ++sv) {
+        kvtc_plan *pl = sv ? vpl : kpl;
+        TileRef &r = tref[sv * ntiles + it[i].row0 / kTileM + j];
+        r = TileRef{};
+        r.payload = (sv ? pay_v[i] : pay_k[i]) + j * pl->tile_bytes;
+        r.codes_off = plan_codes_off_last(pl, ntok);
+        r.ntok = ntok;
+        if (!r.codes_off) {
+          set_error("code offsets: allocation failed");
+          return KVTC_E_NOMEM;
+        }
+      }
+    }
+  }
+  if (ntiles)
+    KVTC_CUDA_TRY(cudaMemcpyAsync(d_tiles, tref.data(), tref.size() * sizeof(TileRef), cudaMemcpyHostToDevice, st));
+  // keys: un-RoPE gather of every item into its rows, one GEMM; then the values
+  for (int sv = 0; sv < 2 && ntiles; ++sv) {
+    {
+      ProfScope ps(sv ? "cb.gather" : "cb.gather_unrope", st);
+      for (int i = 0; i < n; ++i) {
+        if (!it[i].L.m) continue;
+        __nv_bfloat16 *Xi = X + it[i].row0 * ldx;
+        if (sv == 0) {
+          if ((s = rope_table_for(kb, k[i].pos0 + pol->sinks, it[i].L.m, cs + it[i].row0 * half, st))) return s;
+          if ((s = launch_gather(k[i], kbases[i], pol->sinks, it[i].L.m, cs + it[i].row0 * half, kb->pairing, Xi, st,
+                                 0, ldx)))
+            return s;
+        } else if ((s = launch_gather(v[i], vbases[i], pol->sinks, it[i].L.m, nullptr, 0, Xi, st, 0, ldx))) {
+          return s;
+        }
+      }
+    }
+    ProfScope ps("cb.project_quant_gemm", st);
+    if ((s = run_project_quant(sv ? vb : kb, sv ? vpl : kpl, sv ? vop : kop, X, rows, nullptr, wide, st, nullptr, 0,
+                               ldx, d_tiles + sv * ntiles)))
+      return s;
+  }
+  // DEFLATE of all payloads in one launch, then per-item section assembly
+  {
+    ProfScope ps("cb.deflate", st);
+    std::vector<EncodeJob> jobs;
+    uint32_t c0 = 0;
+    for (int i = 0; i < n; ++i)
+      for (int sv = 0; sv < 2; ++sv) {
+        const uint64_t pb = it[i].L.pay[sv];
+        if (!it[i].L.m || pb == 0) continue;
+        EncodeJob j{};
+        j.in = sv ? pay_v[i] : pay_k[i];
+        j.n = pb;
+        j.ws = sv ? dws_v[i] : dws_k[i];
+        j.chunk0 = c0;
+        c0 += uint32_t((pb + pol->chunk_bytes - 1) / pol->chunk_bytes);
+        jobs.push_back(j);
+      }
+    if (!jobs.empty()) {
+      KVTC_CUDA_TRY(cudaMemcpyAsync(d_jobs, jobs.data(), jobs.size() * sizeof(EncodeJob), cudaMemcpyHostToDevice, st));
+      if ((s = launch_deflate_encode_batch(d_jobs, int32_t(jobs.size()), c0, pol->chunk_bytes, st))) return s;
+    }
+  }
+  {
+    ProfScope ps("cb.assemble", st);
+    for (int i = 0; i < n; ++i) {
+      uint8_t *o = static_cast<uint8_t *>(out_host[i]);
+      if (!it[i].L.m) {
+        header_kernel<<<1, 1, 0, st>>>(hdr[i], o, nullptr, nullptr);
+        KVTC_LAUNCH_CHECK();
+        continue;
+      }
+      uint64_t *li = lens + 4 * i;
+      if ((s = launch_deflate_assemble(it[i].L.pay[0], pol->chunk_bytes, dws_k[i], o, li + 2, li + 0, st))) return s;
+      offset_after_kernel<<<1, 1, 0, st>>>(li + 2, li + 0, li + 3, o);
+      KVTC_LAUNCH_CHECK();
+      if ((s = launch_deflate_assemble(it[i].L.pay[1], pol->chunk_bytes, dws_v[i], o, li + 3, li + 1, st))) return s;
+      header_kernel<<<1, 1, 0, st>>>(hdr[i], o, li, li + 2);
+      KVTC_LAUNCH_CHECK();
+    }
+  }
+  if (out_len_host) {
+    std::vector<uint64_t> l(4 * int64_t(n));
+    KVTC_CUDA_TRY(cudaMemcpyAsync(l.data(), lens, l.size() * 8, cudaMemcpyDeviceToHost, st));
+    KVTC_CUDA_TRY(cudaStreamSynchronize(st));
+    for (int i = 0; i < n; ++i)
+      out_len_host[i] = it[i].L.m ? size_t(l[4 * i + 3] + l[4 * i + 1]) : size_t(KVTC_HEADER_BYTES + it[i].L.raw_bytes);
+  }
+  return KVTC_OK;
+}
+
+extern "C" size_t kvtc_decompress_batch_workspace_bytes(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb,
+                                                        const kvtc_plan *vp, const void *const *in_header_host,
+                                                        int32_t n) {
+  if (!kb || !kp || !vb || !vp || !in_header_host || n <= 0) return 0;
+  Bump b;
+  int64_t rows = 0;
+  for (int i = 0; i < n; ++i) {
+    ContainerHeader h;
+    memcpy(&h, in_header_host[i], sizeof(h));
+    rows += (h.m + kTileM - 1) / kTileM * kTileM;
+    b.take<void *>(h.layers);
+    b.take<void *>(h.layers);
+    b.take<uint8_t>(h.payload_bytes[0] + 16);
+    b.take<uint8_t>(h.payload_bytes[1] + 16);
+  }
+  const int64_t ld = std::max(std::max(kp->r_nz_pad, vp->r_nz_pad), 8);
+  b.take<int32_t>(4);
+  b.take<__half>(rows * ld);
+  b.take<__half>(rows * ld);
+  b.take<float2>(rows * (kb->shape.head_dim / 2));
+  b.take<TileRef>(2 * (rows / kTileM));
+  b.take<InflateJob>(2 * int64_t(n));
+  return b.used + 256;
+}
+
+extern "C" kvtc_status kvtc_decompress_batch(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb,
+                                             const kvtc_plan *vp, const void *const *in_host, const size_t *in_len_host,
+                                             int32_t n, const kvtc_kv_view *k_out, const kvtc_kv_view *v_out,
+                                             void *workspace, size_t workspace_bytes, void *stream) {
+  KVTC_CHECK_ARG(kb && kp && vb && vp && in_host && in_len_host && k_out && v_out && n > 0,
+                 "decompress_batch arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  kvtc_status s;
+  // all headers in one device-to-host round trip
+  std::vector<ContainerHeader> hdr(n);
+  for (int i = 0; i < n; ++i) {
+    KVTC_CHECK_ARG(in_len_host[i] >= KVTC_HEADER_BYTES, "container too short");
+    KVTC_CUDA_TRY(cudaMemcpyAsync(&hdr[i], in_host[i], sizeof(ContainerHeader), cudaMemcpyDeviceToHost, st));
+  }
+  KVTC_CUDA_TRY(cudaStreamSynchronize(st));
+  std::vector<BatchItem> it(n);
+  std::vector<const void *> hptr(n);
+  int64_t row = 0;
+  for (int i = 0; i < n; ++i) {
+    const ContainerHeader &h = hdr[i];
+    kvtc_container_info info;
+    if ((s = kvtc_container_parse(&h, &info))) return s;
+    if ((s = check_view(&k_out[i])) || (s = check_view(&v_out[i]))) return s;
+    const kvtc_shape shp{h.layers, h.kv_heads, h.head_dim};
+    if (!same_shape(shp, k_out[i].shape) || !same_shape(shp, v_out[i].shape) || k_out[i].tokens != h.tokens ||
+        v_out[i].tokens != h.tokens || !same_shape(shp, kb->shape) || !same_shape(shp, vb->shape)) {
+      set_error("batch item %d: container shape does not match the output views / bases", i);
+      return KVTC_E_MISMATCH;
+    }
+    if (h.basis_fp[0] != kb->fp || h.basis_fp[1] != vb->fp || h.plan_fp[0] != kp->fp || h.plan_fp[1] != vp->fp) {
+      set_error("batch item %d: container was written with a different basis or plan", i);
+      return KVTC_E_MISMATCH;
+    }
+    if (info.total_bytes > in_len_host[i]) {
+      set_error("batch item %d: container length %llu > buffer %zu", i, (unsigned long long)info.total_bytes,
+                in_len_host[i]);
+      return KVTC_E_CORRUPT;
+    }
+    if (h.m && (h.payload_bytes[0] != kvtc_payload_bytes(kp, h.m) ||
+                h.payload_bytes[1] != kvtc_payload_bytes(vp, h.m))) {
+      set_error("batch item %d: payload sizes do not match the plans", i);
+      return KVTC_E_CORRUPT;
+    }
+    it[i].row0 = row;
+    it[i].tiles = (h.m + kTileM - 1) / kTileM;
+    row += it[i].tiles * kTileM;
+    hptr[i] = &hdr[i];
+  }
+  const size_t need = kvtc_decompress_batch_workspace_bytes(kb, kp, vb, vp, hptr.data(), n);
+  if (!workspace || workspace_bytes < need) {
+    set_error("workspace %zu < %zu", workspace_bytes, need);
+    return KVTC_E_CAPACITY;
+  }
+  const int64_t rows = row, ntiles = rows / kTileM;
+  const int half = kb->shape.head_dim / 2;
+  const int64_t ld = std::max(std::max(kp->r_nz_pad, vp->r_nz_pad), 8);
+  Bump ws(workspace, workspace_bytes);
+  std::vector<__nv_bfloat16 **> kbases(n), vbases(n);
+  std::vector<uint8_t *> pay_k(n), pay_v(n);
+  for (int i = 0; i < n; ++i) {
+    kbases[i] = ws.take<__nv_bfloat16 *>(hdr[i].layers);
+    vbases[i] = ws.take<__nv_bfloat16 *>(hdr[i].layers);
+    pay_k[i] = ws.take<uint8_t>(hdr[i].payload_bytes[0] + 16);
+    pay_v[i] = ws.take<uint8_t>(hdr[i].payload_bytes[1] + 16);
+  }
+  int32_t *err = ws.take<int32_t>(4);
+  __half *Dh = ws.take<__half>(rows * ld);
+  __half *Dh_v = ws.take<__half>(rows * ld);
+  float2 *cs = ws.take<float2>(rows * half);
+  TileRef *d_tiles = ws.take<TileRef>(2 * ntiles);
+  InflateJob *d_jobs = ws.take<InflateJob>(2 * int64_t(n));
+  KVTC_CUDA_TRY(cudaMemsetAsync(err, 0, 4, st));
+  for (int i = 0; i < n; ++i)
+    if ((s = upload_bases(&k_out[i], kbases[i], st)) || (s = upload_bases(&v_out[i], vbases[i], st))) return s;
+  // every section of every item: one inflate launch
+  {
+    ProfScope ps("db.inflate", st);
+    std::vector<InflateJob> jobs;
+    uint32_t c0 = 0;
+    for (int i = 0; i < n; ++i)
+      for (int sv = 0; sv < 2; ++sv) {
+        const ContainerHeader &h = hdr[i];
+        if (!h.m || h.payload_bytes[sv] == 0) continue;
+        InflateJob j{};
+        j.section = static_cast<const uint8_t *>(in_host[i]) + h.section_off[sv];
+        j.n_out = h.payload_bytes[sv];
+        j.nch = uint32_t((h.payload_bytes[sv] + h.chunk_bytes - 1) / h.chunk_bytes);
+        j.chunk0 = c0;
+        j.out = sv ? pay_v[i] : pay_k[i];
+        c0 += j.nch;
+        jobs.push_back(j);
+      }
+    if (!jobs.empty()) {
+      KVTC_CUDA_TRY(cudaMemcpyAsync(d_jobs, jobs.data(), jobs.size() * sizeof(InflateJob), cudaMemcpyHostToDevice, st));
+      if ((s = launch_inflate_batch(d_jobs, int32_t(jobs.size()), c0, err, st))) return s;
+    }
+  }
+  // dequantise into each item's rows, RoPE tables, tile tables
+  std::vector<TileRef> tref(2 * ntiles);
+  {
+    ProfScope ps("db.dequant", st);
+    for (int i = 0; i < n; ++i) {
+      const ContainerHeader &h = hdr[i];
+      if (!h.m) continue;
+      for (int sv = 0; sv < 2; ++sv) {
+        kvtc_plan *pl = const_cast<kvtc_plan *>(sv ? vp : kp);
+        __half *D = (sv ? Dh_v : Dh) + it[i].row0 * ld;
+        if ((s = launch_dequant(pl->d_pgroups, pl->d_codes_off_full, pl->G, plan_codes_off_last(pl, h.m % kTileM),
+                                pl->tile_bytes, sv ? pay_v[i] : pay_k[i], h.m, D, ld, st)))
+          return s;
+        if (pl->r_nz == 0) KVTC_CUDA_TRY(cudaMemsetAsync(D, 0, h.m * ld * 2, st));
+        for (int64_t j = 0; j < it[i].tiles; ++j) {
+          const kvtc_kv_view &vw = sv ? v_out[i] : k_out[i];
+          TileRef &r = tref[sv * ntiles + it[i].row0 / kTileM + j];
+          r = TileRef{};
+          r.bases = sv ? vbases[i] : kbases[i];
+          r.block_table = vw.block_table;
+          r.layout = vw.layout;
+          r.page_tokens = vw.page_tokens;
+          r.tok0 = h.sinks + j * kTileM;
+          r.ntok = int(std::min<int64_t>(kTileM, h.m - j * kTileM));
+        }
+      }
+      if (kb->has_rope && (s = rope_table_for(kb, h.pos0 + h.sinks, h.m, cs + it[i].row0 * half, st))) return s;
+    }
+  }
+  if (ntiles)
+    KVTC_CUDA_TRY(cudaMemcpyAsync(d_tiles, tref.data(), tref.size() * sizeof(TileRef), cudaMemcpyHostToDevice, st));
+  for (int sv = 0; sv < 2 && ntiles; ++sv) {
+    const kvtc_basis *b = sv ? vb : kb;
+    kvtc_plan *pl = const_cast<kvtc_plan *>(sv ? vp : kp);
+    const Operands *op;
+    if ((s = plan_operands(b, pl, &op))) return s;
+    ProfScope ps("db.reconstruct_gemm", st);
+    // the view arguments only carry the shape here: every tile's output comes from its TileRef
+    if ((s = run_reconstruct(b, pl, op, sv ? Dh_v : Dh, ld, rows, 0, 0, b->shape.layers, sv ? &v_out[0] : &k_out[0],
+                             sv ? vbases[0] : kbases[0], cs, st, d_tiles + sv * ntiles)))
+      return s;
+  }
+  {
+    ProfScope ps("db.raw_tokens", st);
+    for (int i = 0; i < n; ++i) {
+      const ContainerHeader &h = hdr[i];
+      const uint8_t *ib = static_cast<const uint8_t *>(in_host[i]);
+      const int64_t t = h.tokens;
+      const int64_t nraw = h.m ? int64_t(h.sinks) + h.window : t;
+      const int64_t hd = int64_t(h.kv_heads) * h.head_dim;
+      const auto *rawk = reinterpret_cast<const __nv_bfloat16 *>(ib + h.raw_off);
+      const auto *rawv = rawk + int64_t(h.layers) * nraw * hd;
+      for (int sv = 0; sv < 2; ++sv) {
+        const kvtc_kv_view &vw = sv ? v_out[i] : k_out[i];
+        __nv_bfloat16 *const *bs = sv ? vbases[i] : kbases[i];
+        const __nv_bfloat16 *raw = sv ? rawv : rawk;
+        if (!h.m) {
+          if ((s = launch_unpack_raw(raw, nraw, 0, t, vw, bs, 0, 0, h.layers, st))) return s;
+          continue;
+        }
+        if ((s = launch_unpack_raw(raw, nraw, 0, h.sinks, vw, bs, 0, 0, h.layers, st))) return s;
+        if ((s = launch_unpack_raw(raw, nraw, h.sinks, h.window, vw, bs, t - h.window, 0, h.layers, st))) return s;
+      }
     }
   }
   return KVTC_OK;

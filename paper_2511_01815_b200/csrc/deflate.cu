@@ -609,7 +609,7 @@ struct DeflateWs {
   uint32_t *cbytes, *ckind;
   uint16_t *index;
 };
-DeflateWs deflate_ws(size_t n, int32_t chunk, void *ws) {
+__host__ __device__ DeflateWs deflate_ws(size_t n, int32_t chunk, void *ws) {
   DeflateWs w;
   w.nch = uint32_t((n + chunk - 1) / chunk);
   w.stride = slot_stride(chunk);
@@ -643,6 +643,35 @@ kvtc_status launch_deflate_encode(const uint8_t *in, size_t n, int32_t chunk, vo
   KVTC_MAX_CARVEOUT(deflate_encode_kernel);
   deflate_encode_kernel<<<grid, kEncThreads, 0, st>>>(in, n, chunk, c_begin, c_end, w.slots, w.stride, w.cbytes,
                                                       w.ckind, w.index);
+  KVTC_LAUNCH_CHECK();
+  return KVTC_OK;
+}
+
+// Batched codec: the chunks of many payloads in one launch (jobs[j].chunk0 ascending).
+__global__ void __launch_bounds__(kEncThreads, 14) deflate_encode_batch_kernel(const EncodeJob *jobs, int32_t njobs,
+                                                                              uint32_t total, int32_t chunk) {
+  __shared__ EncShared S;
+  const uint64_t stride = slot_stride(chunk);
+  for (uint32_t b = blockIdx.x; b < total; b += gridDim.x) {
+    int lo = 0, hi = njobs - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) / 2;
+      if (jobs[mid].chunk0 <= b) lo = mid;
+      else hi = mid - 1;
+    }
+    const EncodeJob jb = jobs[lo];
+    const DeflateWs w = deflate_ws(jb.n, chunk, jb.ws);
+    encode_chunk(S, int(b - jb.chunk0), jb.in, jb.n, chunk, w.slots, stride, w.cbytes, w.ckind, w.index);
+    __syncthreads();
+  }
+}
+
+kvtc_status launch_deflate_encode_batch(const EncodeJob *jobs_dev, int32_t njobs, uint32_t total_chunks,
+                                        int32_t chunk, cudaStream_t st) {
+  KVTC_CHECK_ARG(chunk == 16384 || chunk == 32768 || chunk == 65536, "chunk_bytes must be 16/32/64 KiB");
+  if (njobs == 0 || total_chunks == 0) return KVTC_OK;
+  KVTC_MAX_CARVEOUT(deflate_encode_batch_kernel);
+  deflate_encode_batch_kernel<<<total_chunks, kEncThreads, 0, st>>>(jobs_dev, njobs, total_chunks, chunk);
   KVTC_LAUNCH_CHECK();
   return KVTC_OK;
 }
@@ -890,14 +919,13 @@ __device__ int parse_header_fast(FastShared &S) {
   return 0;
 }
 
-__device__ __forceinline__ void inflate_chunk(FastShared &S, const uint32_t b, const InflateJobs &J, int32_t *err) {
-  const int job = b < J.nch[0] ? 0 : 1;
-  const uint32_t c = job == 0 ? b : b - J.nch[0];
-  const uint8_t *section = J.base + (J.off_dev[job] ? *J.off_dev[job] : 0);
+// Chunk c of the section at `section` (raw size n_out, nch chunks) into out_base.
+__device__ __forceinline__ void inflate_chunk(FastShared &S, const uint8_t *section, uint64_t n_out, uint32_t nch,
+                                              uint32_t c, uint8_t *out_base, int32_t *err) {
   const SectionHeader *hdr = reinterpret_cast<const SectionHeader *>(section);
   const int tid = threadIdx.x;
-  if (hdr->magic != kSectionMagic || hdr->version != kSectionVersion || hdr->raw_bytes != J.n_out[job] ||
-      hdr->nchunks != J.nch[job] || hdr->nseg != kNSeg || hdr->seg_bytes * kNSeg != hdr->chunk_bytes ||
+  if (hdr->magic != kSectionMagic || hdr->version != kSectionVersion || hdr->raw_bytes != n_out ||
+      hdr->nchunks != nch || hdr->nseg != kNSeg || hdr->seg_bytes * kNSeg != hdr->chunk_bytes ||
       hdr->seg_bytes % 16) {
     if (tid == 0) atomicExch(err, -20);
     return;
@@ -908,7 +936,7 @@ __device__ __forceinline__ void inflate_chunk(FastShared &S, const uint32_t b, c
   const uint8_t *stream = section + hdr->data_offset + e.offset;
   const uint64_t obase = uint64_t(c) * hdr->chunk_bytes;
   const uint32_t nc = uint32_t(umin64(hdr->chunk_bytes, hdr->raw_bytes - obase));
-  uint8_t *o = J.out[job] + obase;
+  uint8_t *o = out_base + obase;
   if (e.kind == 1) {
     for (uint32_t i = tid; i < nc; i += kInfThreads) o[i] = stream[(i / 32768) * (32768 + 5) + 5 + (i % 32768)];
     return;
@@ -1048,9 +1076,38 @@ __global__ void __launch_bounds__(kInfThreads) inflate_fast_kernel(InflateJobs J
   __shared__ FastShared S;
   const uint32_t total = J.nch[0] + J.nch[1];
   for (uint32_t b = blockIdx.x; b < total; b += gridDim.x) {
-    inflate_chunk(S, b, J, err);
+    const int job = b < J.nch[0] ? 0 : 1;
+    const uint32_t c = job == 0 ? b : b - J.nch[0];
+    inflate_chunk(S, J.base + (J.off_dev[job] ? *J.off_dev[job] : 0), J.n_out[job], J.nch[job], c, J.out[job], err);
     __syncthreads();
   }
+}
+
+// Batched codec: any number of sections; jobs[j].chunk0 = first global chunk of
+// job j (ascending), a binary search maps a chunk to its job.
+__global__ void __launch_bounds__(kInfThreads) inflate_batch_kernel(const InflateJob *jobs, int32_t njobs,
+                                                                   uint32_t total, int32_t *err) {
+  __shared__ FastShared S;
+  for (uint32_t b = blockIdx.x; b < total; b += gridDim.x) {
+    int lo = 0, hi = njobs - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) / 2;
+      if (jobs[mid].chunk0 <= b) lo = mid;
+      else hi = mid - 1;
+    }
+    const InflateJob jb = jobs[lo];
+    inflate_chunk(S, jb.section, jb.n_out, jb.nch, b - jb.chunk0, jb.out, err);
+    __syncthreads();
+  }
+}
+
+kvtc_status launch_inflate_batch(const InflateJob *jobs_dev, int32_t njobs, uint32_t total_chunks, int32_t *err,
+                                 cudaStream_t st) {
+  if (njobs == 0 || total_chunks == 0) return KVTC_OK;
+  KVTC_MAX_CARVEOUT(inflate_batch_kernel);
+  inflate_batch_kernel<<<total_chunks, kInfThreads, 0, st>>>(jobs_dev, njobs, total_chunks, err);
+  KVTC_LAUNCH_CHECK();
+  return KVTC_OK;
 }
 
 kvtc_status launch_inflate_sections(const uint8_t *base, const uint64_t *off_dev0, uint64_t n0, uint32_t nch0,

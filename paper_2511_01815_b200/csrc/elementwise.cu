@@ -276,14 +276,16 @@ __device__ __forceinline__ float4 load4(const float *p, bool vec) {
 
 __global__ void __launch_bounds__(128) quant_wide_kernel(const WideDesc *wide, const float *D, int64_t ldd,
                                                          int use_wcol, int64_t m, int64_t tile_bytes,
-                                                         const int64_t *codes_off_last, uint8_t *payload) {
+                                                         const int64_t *codes_off_last, uint8_t *payload,
+                                                         const TileRef *tiles) {
   const WideDesc wd = wide[blockIdx.x];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t m0 = int64_t(blockIdx.y) * kTileM;
-  const int ntok = int(m - m0 < kTileM ? m - m0 : kTileM);
+  const TileRef *tref = tiles ? tiles + blockIdx.y : nullptr;
+  const int ntok = tref ? tref->ntok : int(m - m0 < kTileM ? m - m0 : kTileM);
   const bool last = ntok < kTileM;
-  uint8_t *tile_base = payload + blockIdx.y * tile_bytes;
-  uint8_t *cb = tile_base + (last ? codes_off_last[wd.gidx] : wd.codes_off);
+  uint8_t *tile_base = tref ? tref->payload : payload + blockIdx.y * tile_bytes;
+  uint8_t *cb = tile_base + (last ? (tref ? tref->codes_off : codes_off_last)[wd.gidx] : wd.codes_off);
   const int b = bits_of(wd.type);
   const int per_word = 32 / b;
   const int words = wd.size * b / 32;
@@ -327,10 +329,10 @@ __global__ void __launch_bounds__(128) quant_wide_kernel(const WideDesc *wide, c
 
 kvtc_status launch_quant_wide(const WideDesc *wide, int32_t nwide, const float *D, int64_t ldd, int use_wcol,
                               int64_t m, int64_t tile_bytes, const int64_t *codes_off_last, uint8_t *payload,
-                              cudaStream_t st) {
+                              cudaStream_t st, const TileRef *tiles) {
   if (nwide == 0 || m == 0) return KVTC_OK;
   dim3 grid(unsigned(nwide), unsigned(ceil_div(m, kTileM)));
-  quant_wide_kernel<<<grid, 128, 0, st>>>(wide, D, ldd, use_wcol, m, tile_bytes, codes_off_last, payload);
+  quant_wide_kernel<<<grid, 128, 0, st>>>(wide, D, ldd, use_wcol, m, tile_bytes, codes_off_last, payload, tiles);
   KVTC_LAUNCH_CHECK();
   return KVTC_OK;
 }

@@ -90,6 +90,7 @@ struct Params {
   unsigned long long *tile_sync;   // non-null: producers align tile starts (see tile_barrier)
   int32_t sync_lag;                // a producer may run this many tiles ahead of the slowest
   int32_t nsegs;                   // QUANT: number of 256-column segments
+  const TileRef *tiles;            // batched rows (QUANT / RECON), else null
 };
 
 __device__ __forceinline__ void cluster_sync_all() {
@@ -482,7 +483,11 @@ __global__ void __launch_bounds__(kThreads, MODE == EPI_RECON ? 1 : 2)
       const int n_mma = (ncols + 15) & ~15;
       const int64_t m0 = int64_t(T.mb) * kTileM;
       const int64_t tok = m0 + row;
-      const bool valid = tok < P.m;
+      // batched rows: the tile's table entry (the odd M-block of the last CTA pair
+      // may lie past the table: no entry, no valid rows)
+      const TileRef *tref =
+          (MODE == EPI_QUANT || MODE == EPI_RECON) && P.tiles && T.mb < P.num_m ? P.tiles + T.mb : nullptr;
+      const bool valid = tref ? row < tref->ntok : tok < P.m;
       const uint32_t acc = acc_it % kAccBufs;
       mbar_wait(&tmem_full[acc], (acc_it / kAccBufs) & 1);
       tc_fence_after();
@@ -509,9 +514,10 @@ __global__ void __launch_bounds__(kThreads, MODE == EPI_RECON ? 1 : 2)
       } else if constexpr (MODE == EPI_QUANT) {
         // Straight from TMEM, group by group: pass 1 min/max, pass 2 encode + pack
         // (no shared-memory staging, so the next tile's MMAs overlap this epilogue).
-        const int ntok = int(P.m - m0 < kTileM ? P.m - m0 : kTileM);
+        const int ntok = tref ? tref->ntok : int(P.m - m0 < kTileM ? (P.m > m0 ? P.m - m0 : 0) : kTileM);
         const bool last = ntok < kTileM;
-        uint8_t *tile_base = P.payload + T.mb * P.tile_bytes;
+        uint8_t *tile_base = tref ? tref->payload : P.payload + T.mb * P.tile_bytes;
+        const int64_t *codes_off_last = tref ? tref->codes_off : P.codes_off_last;
         const int nsub = tile_nsub<NSUB>(P, T);
         for (int sb = 0; sb < nsub; ++sb) {
         const SegDesc sdq = P.segs[T.nb * NSUB + sb];
@@ -536,7 +542,7 @@ __global__ void __launch_bounds__(kThreads, MODE == EPI_RECON ? 1 : 2)
         auto emit_subbyte = [&](const GroupDesc &g, uint32_t bits_v) {
           const int nb = g.full_size * bits_of(g.type);
           const int bitpos = lane * nb;
-          uint8_t *cb = tile_base + (last ? P.codes_off_last[g.gidx] : g.codes_off);
+          uint8_t *cb = tile_base + (last ? codes_off_last[g.gidx] : g.codes_off);
           const int64_t blk_len = (int64_t(ntok) * nb + 7) / 8;
           const int64_t warp_byte0 = int64_t((warp & 3) * 32) * nb / 8;
           for (int w = 0; w < nb; ++w) {
@@ -607,7 +613,7 @@ __global__ void __launch_bounds__(kThreads, MODE == EPI_RECON ? 1 : 2)
             group_factors(gd.type, mn, mx, sh, sc);
             store_params(gd, sh, sc);
             const int bq = bits_of(gd.type);
-            uint8_t *cb = tile_base + (last ? P.codes_off_last[gd.gidx] : gd.codes_off);
+            uint8_t *cb = tile_base + (last ? codes_off_last[gd.gidx] : gd.codes_off);
             if (valid) {
               const float shift = f16_val(sh), scale = f16_val(sc);
               uint8_t *dst = cb + int64_t(row) * (gd.size * bq / 8);
@@ -641,7 +647,7 @@ __global__ void __launch_bounds__(kThreads, MODE == EPI_RECON ? 1 : 2)
           store_params(gd, sh, sc);
           const int bq = bits_of(gd.type);
           const int tok_bits = gd.full_size * bq;
-          uint8_t *cb = tile_base + (last ? P.codes_off_last[gd.gidx] : gd.codes_off);
+          uint8_t *cb = tile_base + (last ? codes_off_last[gd.gidx] : gd.codes_off);
           if ((tok_bits & 7) == 0) {
             uint8_t *dst = cb + int64_t(row) * (tok_bits / 8) + gd.part * (gd.size * bq / 8);
             for (int c = 0; c < gd.size; c += step) {
@@ -667,13 +673,15 @@ __global__ void __launch_bounds__(kThreads, MODE == EPI_RECON ? 1 : 2)
         const int hd = P.heads * d;
         const int layer = n0 / hd;
         const int head0 = (n0 % hd) / d;
-        const int64_t ctok = P.tok_begin + tok;
+        const int64_t ctok = tref ? tref->tok0 + row : P.tok_begin + tok;
         __nv_bfloat16 *rowp = nullptr;
         if (valid) {
           int64_t slot = ctok;
-          if (P.layout == KVTC_LAYOUT_PAGED)
-            slot = int64_t(P.block_table[ctok / P.page_tokens]) * P.page_tokens + (ctok % P.page_tokens);
-          rowp = P.layer_base[layer] + slot * hd;
+          const int lay = tref ? tref->layout : P.layout;
+          const int pt = tref ? tref->page_tokens : P.page_tokens;
+          const int32_t *bt = tref ? tref->block_table : P.block_table;
+          if (lay == KVTC_LAYOUT_PAGED) slot = int64_t(bt[ctok / pt]) * pt + (ctok % pt);
+          rowp = (tref ? tref->bases : P.layer_base)[layer] + slot * hd;
         }
         const float2 *cs = (P.cs && valid) ? P.cs + tok * (d / 2) : nullptr;
         const bool rot = P.cs != nullptr;
@@ -875,6 +883,7 @@ kvtc_status launch_gemm_project_quant(const GemmCompressArgs &a, cudaStream_t st
   p.nsegs = a.nsegs;
   p.D = a.D;
   p.ldd = a.ldd;
+  p.tiles = a.tiles;
   // KVTC_QUANT_NSUB=2: two segments per tile (Cfg<true, 2>, 25 % less L2 traffic);
   // measured slower (tensor pipe 58 % vs 88 %: the 512-column epilogue is not
   // overlapped), so one segment per tile with double-buffered TMEM is the default
@@ -904,6 +913,7 @@ kvtc_status launch_gemm_reconstruct(const GemmDecompressArgs &a, cudaStream_t st
   p.layer_base = a.layer_base;
   p.block_table = a.block_table;
   p.tok_begin = a.tok_begin;
+  p.tiles = a.tiles;
   p.fmt = 0;
   p.tile_n = a.tile_n;
   p.num_m = int32_t(ceil_div(a.m, kTileM));

@@ -46,6 +46,20 @@ struct WideDesc {
   int64_t codes_off;  // code block offset in a FULL tile
 };
 
+// Batched codec (kvtc_compress_batch / kvtc_decompress_batch): ONE GEMM over the
+// concatenated rows of several conversations, each padded to whole 128-token
+// tiles; tile mb of the GEMM refers to one tile of one conversation.
+struct TileRef {
+  uint8_t *payload;                 // compress: this tile's payload bytes
+  const int64_t *codes_off;         // compress: code-block offsets (full or partial tile)
+  __nv_bfloat16 *const *bases;      // decompress: the conversation's device layer-base array
+  const int32_t *block_table;       // decompress: paged layout
+  int64_t tok0;                     // decompress: cache token of the tile's first row
+  int32_t ntok;                     // valid rows (<= 128)
+  int32_t layout, page_tokens;      // decompress: output view layout
+  int32_t pad;
+};
+
 // Operands of a (basis, plan) pair, compacted to the plan's non-None PCs.
 struct Operands {
   int32_t r_nz = 0, r_nz_pad = 0;
@@ -89,6 +103,7 @@ struct GemmCompressArgs {
   // row r of X is token a_row0 + r (k-block kb = layer kb*64/hd, column kb*64%hd)
   int32_t a_hd;
   int64_t a_row0;
+  const TileRef *tiles;    // non-null: batched rows (tile mb -> tiles[mb]); payload / m unused
 };
 kvtc_status launch_gemm_project_f32(const GemmCompressArgs &a, int32_t ncols, cudaStream_t st);
 kvtc_status launch_gemm_project_quant(const GemmCompressArgs &a, cudaStream_t st);
@@ -108,6 +123,7 @@ struct GemmDecompressArgs {
   const int32_t *block_table;
   int64_t tok_begin;                 // cache token index of row 0
   int32_t tile_n;                    // N tile (<= 256, divides heads*head_dim)
+  const TileRef *tiles;              // non-null: batched rows; the output view comes from tiles[mb]
 };
 kvtc_status launch_gemm_reconstruct(const GemmDecompressArgs &a, cudaStream_t st);
 
@@ -127,7 +143,8 @@ kvtc_status launch_gather_rows(const kvtc_kv_view *seqs, int32_t nseq, __nv_bflo
                                int32_t pairing, int64_t ld, __nv_bfloat16 *X, cudaStream_t st);
 // Wide groups: D [m x ldd] fp32; column of group w = use_wcol ? wcol : col.
 kvtc_status launch_quant_wide(const WideDesc *wide, int32_t nwide, const float *D, int64_t ldd, int use_wcol, int64_t m,
-                              int64_t tile_bytes, const int64_t *codes_off_last, uint8_t *payload, cudaStream_t st);
+                              int64_t tile_bytes, const int64_t *codes_off_last, uint8_t *payload, cudaStream_t st,
+                              const TileRef *tiles = nullptr);
 kvtc_status launch_quant_pack_simt(const SegDesc *segs, const GroupDesc *groups, int32_t nsegs, int32_t G,
                                    const float *D, int64_t ldd, int64_t m, int64_t tile_bytes,
                                    const int64_t *codes_off_last, uint8_t *payload, cudaStream_t st);
@@ -162,6 +179,16 @@ kvtc_status launch_deflate_encode(const uint8_t *in, size_t n, int32_t chunk, vo
                                   uint32_t c_end = 0xFFFFFFFFu);   // chunk range [c_begin, c_end)
 kvtc_status launch_deflate_assemble(size_t n, int32_t chunk, const void *ws, uint8_t *out, const uint64_t *off_dev,
                                     uint64_t *section_len_dev, cudaStream_t st);
+// Batched codec: one payload's DEFLATE job (its own workspace of
+// deflate_workspace(n) bytes; chunk0 = first global chunk, ascending).
+struct EncodeJob {
+  const uint8_t *in;
+  uint64_t n;
+  void *ws;
+  uint32_t chunk0, pad;
+};
+kvtc_status launch_deflate_encode_batch(const EncodeJob *jobs_dev, int32_t njobs, uint32_t total_chunks,
+                                        int32_t chunk, cudaStream_t st);
 // SM count x per_sm: the bounded grid of a side-stream kernel overlapping a GEMM.
 int corun_ctas(int per_sm);
 // Kernels that share an SM must run under the same shared-memory carveout: the
@@ -185,6 +212,15 @@ kvtc_status launch_inflate_sections(const uint8_t *base, const uint64_t *off_dev
                                     uint8_t *out0, const uint64_t *off_dev1, uint64_t n1, uint32_t nch1,
                                     uint8_t *out1, int32_t *err, cudaStream_t st, int32_t max_ctas = 0);
 constexpr size_t kSectionHeaderBytes = 64;
+// One section of a batched inflate (device table, chunk0 ascending).
+struct InflateJob {
+  const uint8_t *section;
+  uint64_t n_out;
+  uint32_t nch, chunk0;
+  uint8_t *out;
+};
+kvtc_status launch_inflate_batch(const InflateJob *jobs_dev, int32_t njobs, uint32_t total_chunks, int32_t *err,
+                                 cudaStream_t st);
 kvtc_status launch_inflate_raw(const uint8_t *in, const int64_t *in_off, const int64_t *in_len, int32_t n,
                                uint8_t *out, const int64_t *out_off, const int64_t *out_len, int32_t *status,
                                cudaStream_t st);

@@ -284,6 +284,57 @@ def decompress(kb: Basis, kp: Plan, vb: Basis, vp: Plan, container: torch.Tensor
                                 _stream(stream)))
 
 
+# ------------------------------------------------------------ batched codec
+def compress_batch(kb: Basis, kp: Plan, vb: Basis, vp: Plan, ks: list, vs: list, sinks: int = 4, window: int = 128,
+                   chunk_bytes: int = 65536, stream=None, outs: list | None = None, workspace=None,
+                   sync_len: bool = True):
+    """kvtc_compress_batch: one container per (ks[i], vs[i]); returns the list of
+    containers (trimmed to their lengths when sync_len)."""
+    n = len(ks)
+    pol = L.Policy(sinks, window, chunk_bytes)
+    karr, varr = _views(ks), _views(vs)
+    if outs is None:
+        outs = [torch.empty(int(lib().kvtc_compress_bound(kp.h, vp.h, C.byref(k.c), C.byref(pol))),
+                            dtype=torch.uint8, device="cuda") for k in ks]
+    if workspace is None:
+        wsb = int(lib().kvtc_compress_batch_workspace_bytes(kb.h, kp.h, vb.h, vp.h, karr, n, C.byref(pol)))
+        workspace = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    ptrs = (C.c_void_p * n)(*[o.data_ptr() for o in outs])
+    caps = (C.c_size_t * n)(*[o.numel() for o in outs])
+    lens = (C.c_size_t * n)()
+    check(lib().kvtc_compress_batch(kb.h, kp.h, vb.h, vp.h, karr, varr, n, C.byref(pol), ptrs, caps,
+                                    lens if sync_len else None, _ptr(workspace), workspace.numel(), _stream(stream)))
+    return [o[: lens[i]] for i, o in enumerate(outs)] if sync_len else outs
+
+
+def compress_batch_workspace_bytes(kb, kp, vb, vp, ks: list, sinks=4, window=128, chunk_bytes=65536) -> int:
+    pol = L.Policy(sinks, window, chunk_bytes)
+    return int(lib().kvtc_compress_batch_workspace_bytes(kb.h, kp.h, vb.h, vp.h, _views(ks), len(ks), C.byref(pol)))
+
+
+def decompress_batch(kb: Basis, kp: Plan, vb: Basis, vp: Plan, containers: list, k_outs: list, v_outs: list,
+                     stream=None, workspace=None, headers: list | None = None):
+    """kvtc_decompress_batch: every container into its (k_outs[i], v_outs[i])."""
+    n = len(containers)
+    if workspace is None:
+        if headers is None:
+            headers = [c[: L.HEADER_BYTES].cpu().numpy().tobytes() for c in containers]
+        hb = [C.create_string_buffer(h, len(h)) for h in headers]
+        hp = (C.c_void_p * n)(*[C.cast(b, C.c_void_p) for b in hb])
+        wsb = int(lib().kvtc_decompress_batch_workspace_bytes(kb.h, kp.h, vb.h, vp.h, hp, n))
+        workspace = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    ptrs = (C.c_void_p * n)(*[c.data_ptr() for c in containers])
+    lens = (C.c_size_t * n)(*[c.numel() for c in containers])
+    check(lib().kvtc_decompress_batch(kb.h, kp.h, vb.h, vp.h, ptrs, lens, n, _views(k_outs), _views(v_outs),
+                                      _ptr(workspace), workspace.numel(), _stream(stream)))
+
+
+def decompress_batch_workspace_bytes(kb, kp, vb, vp, headers: list) -> int:
+    hb = [C.create_string_buffer(h, len(h)) for h in headers]
+    hp = (C.c_void_p * len(headers))(*[C.cast(b, C.c_void_p) for b in hb])
+    return int(lib().kvtc_decompress_batch_workspace_bytes(kb.h, kp.h, vb.h, vp.h, hp, len(headers)))
+
+
 # ------------------------------------------------------------- calibration
 def _samples(samples):
     s = np.ascontiguousarray(np.asarray(samples, dtype=np.int64).reshape(-1, 2))

@@ -84,8 +84,9 @@ if __name__ == "__main__":
                      f"{f(tp, 1, 1)} | {f(d.get('sm_pct'), 1, 1)} | {f(d.get('occupancy_pct'), 1, 1)} | "
                      f"{f(d.get('regs'), 1, 0)} |")
         kn = d["kernel"].replace(" ", "")
-        key = ("c.project_quant_gemm" if kn.startswith("kvtc::gemm_kernel<1")
-               else "d.reconstruct_gemm" if kn.startswith("kvtc::gemm_kernel<2") else None)
+        kn = kn.replace("kvtc::", "")
+        key = ("c.project_quant_gemm" if kn.startswith("gemm_kernel<1")
+               else "d.reconstruct_gemm" if kn.startswith("gemm_kernel<2") else None)
         if key and key not in traffic and d.get("dram_read") is not None:
             traffic[key] = d["dram_read"] + (d.get("dram_write") or 0)
     open(md, "w").write("\n".join(lines) + "\n")
