@@ -822,6 +822,7 @@ extern "C" size_t kvtc_compress_batch_workspace_bytes(const kvtc_basis *kb, cons
   }
   b.take<uint64_t>(4 * int64_t(n));
   b.take<__nv_bfloat16>(rows * (kb->p + kXPad));
+  b.take<__nv_bfloat16>(rows * (kb->p + kXPad));
   b.take<float2>(rows * (kb->shape.head_dim / 2));
   b.take<float>(rows * std::max(kp->wide_cols, vp->wide_cols));
   b.take<TileRef>(2 * (rows / kTileM));
@@ -883,6 +884,7 @@ extern "C" kvtc_status kvtc_compress_batch(const kvtc_basis *kb, const kvtc_plan
   }
   uint64_t *lens = ws.take<uint64_t>(4 * int64_t(n));            // per item: K len, V len, K off, V off
   auto *X = ws.take<__nv_bfloat16>(rows * ldx);
+  auto *X2 = ws.take<__nv_bfloat16>(rows * ldx);          // the values' rows (gathered beside the keys' GEMM)
   float2 *cs = ws.take<float2>(rows * half);
   float *wide = ws.take<float>(rows * std::max(kp->wide_cols, vp->wide_cols));
   TileRef *d_tiles = ws.take<TileRef>(2 * ntiles);
@@ -957,50 +959,81 @@ extern "C" kvtc_status kvtc_compress_batch(const kvtc_basis *kb, const kvtc_plan
   }
   if (ntiles)
     KVTC_CUDA_TRY(cudaMemcpyAsync(d_tiles, tref.data(), tref.size() * sizeof(TileRef), cudaMemcpyHostToDevice, st));
-  // keys: un-RoPE gather of every item into its rows, one GEMM; then the values
-  for (int sv = 0; sv < 2 && ntiles; ++sv) {
+  // Schedule (as kvtc_compress): st: keys' gathers -> keys' GEMM ->
+  // values' GEMM -> values' DEFLATE -> assemble; aux (bounded grids beside the
+  // GEMMs): values' gathers into X2, then the keys' DEFLATE.
+  SideStream *ss = side_stream();
+  const bool ovl = !overlap_off();
+  cudaStream_t aux = ovl ? ss->s : st;
+  KVTC_CUDA_TRY(cudaEventRecord(ss->ev[0], st));                 // bases, raw tokens, tables uploaded
+  std::vector<EncodeJob> jobs[2];
+  uint32_t nchunks[2] = {0, 0};
+  for (int sv = 0; sv < 2; ++sv)
+    for (int i = 0; i < n; ++i) {
+      const uint64_t pb = it[i].L.pay[sv];
+      if (!it[i].L.m || pb == 0) continue;
+      EncodeJob j{};
+      j.in = sv ? pay_v[i] : pay_k[i];
+      j.n = pb;
+      j.ws = sv ? dws_v[i] : dws_k[i];
+      j.chunk0 = nchunks[sv];
+      nchunks[sv] += uint32_t((pb + pol->chunk_bytes - 1) / pol->chunk_bytes);
+      jobs[sv].push_back(j);
+    }
+  for (int sv = 0; sv < 2; ++sv)
+    if (!jobs[sv].empty())
+      KVTC_CUDA_TRY(cudaMemcpyAsync(d_jobs + sv * n, jobs[sv].data(), jobs[sv].size() * sizeof(EncodeJob),
+                                    cudaMemcpyHostToDevice, st));
+  if (ntiles) {
     {
-      ProfScope ps(sv ? "cb.gather" : "cb.gather_unrope", st);
+      ProfScope ps("cb.gather_unrope", st);
       for (int i = 0; i < n; ++i) {
         if (!it[i].L.m) continue;
-        __nv_bfloat16 *Xi = X + it[i].row0 * ldx;
-        if (sv == 0) {
-          if ((s = rope_table_for(kb, k[i].pos0 + pol->sinks, it[i].L.m, cs + it[i].row0 * half, st))) return s;
-          if ((s = launch_gather(k[i], kbases[i], pol->sinks, it[i].L.m, cs + it[i].row0 * half, kb->pairing, Xi, st,
-                                 0, ldx)))
-            return s;
-        } else if ((s = launch_gather(v[i], vbases[i], pol->sinks, it[i].L.m, nullptr, 0, Xi, st, 0, ldx))) {
+        if ((s = rope_table_for(kb, k[i].pos0 + pol->sinks, it[i].L.m, cs + it[i].row0 * half, st))) return s;
+        if ((s = launch_gather(k[i], kbases[i], pol->sinks, it[i].L.m, cs + it[i].row0 * half, kb->pairing,
+                               X + it[i].row0 * ldx, st, 0, ldx)))
           return s;
-        }
       }
     }
-    ProfScope ps("cb.project_quant_gemm", st);
-    if ((s = run_project_quant(sv ? vb : kb, sv ? vpl : kpl, sv ? vop : kop, X, rows, nullptr, wide, st, nullptr, 0,
-                               ldx, d_tiles + sv * ntiles)))
-      return s;
-  }
-  // DEFLATE of all payloads in one launch, then per-item section assembly
-  {
-    ProfScope ps("cb.deflate", st);
-    std::vector<EncodeJob> jobs;
-    uint32_t c0 = 0;
-    for (int i = 0; i < n; ++i)
-      for (int sv = 0; sv < 2; ++sv) {
-        const uint64_t pb = it[i].L.pay[sv];
-        if (!it[i].L.m || pb == 0) continue;
-        EncodeJob j{};
-        j.in = sv ? pay_v[i] : pay_k[i];
-        j.n = pb;
-        j.ws = sv ? dws_v[i] : dws_k[i];
-        j.chunk0 = c0;
-        c0 += uint32_t((pb + pol->chunk_bytes - 1) / pol->chunk_bytes);
-        jobs.push_back(j);
+    {
+      ProfScope ps("cb.project_quant_gemm", st);
+      if ((s = run_project_quant(kb, kpl, kop, X, rows, nullptr, wide, st, nullptr, 0, ldx, d_tiles))) return s;
+    }
+    KVTC_CUDA_TRY(cudaEventRecord(ss->ev[2], st));               // keys' payloads ready
+    KVTC_CUDA_TRY(cudaStreamWaitEvent(aux, ss->ev[0], 0));
+    {
+      ProfScope ps(ovl ? "cb.gather_overlapped" : "cb.gather", aux);
+      for (int i = 0; i < n; ++i) {
+        if (!it[i].L.m) continue;
+        if ((s = launch_gather(v[i], vbases[i], pol->sinks, it[i].L.m, nullptr, 0, X2 + it[i].row0 * ldx, aux,
+                               ovl ? corun_ctas(3) : 0, ldx)))
+          return s;
       }
-    if (!jobs.empty()) {
-      KVTC_CUDA_TRY(cudaMemcpyAsync(d_jobs, jobs.data(), jobs.size() * sizeof(EncodeJob), cudaMemcpyHostToDevice, st));
-      if ((s = launch_deflate_encode_batch(d_jobs, int32_t(jobs.size()), c0, pol->chunk_bytes, st))) return s;
+    }
+    KVTC_CUDA_TRY(cudaEventRecord(ss->ev[1], aux));              // values gathered
+    KVTC_CUDA_TRY(cudaStreamWaitEvent(st, ss->ev[1], 0));
+    {
+      ProfScope ps("cb.project_quant_gemm", st);
+      if ((s = run_project_quant(vb, vpl, vop, X2, rows, nullptr, wide, st, nullptr, 0, ldx, d_tiles + ntiles)))
+        return s;
+    }
+    KVTC_CUDA_TRY(cudaStreamWaitEvent(aux, ss->ev[2], 0));
+    {
+      ProfScope ps(ovl ? "cb.deflate_overlapped" : "cb.deflate", aux);
+      if (!jobs[0].empty() &&
+          (s = launch_deflate_encode_batch(d_jobs, int32_t(jobs[0].size()), nchunks[0], pol->chunk_bytes, aux,
+                                           ovl ? corun_ctas(2) : 0)))
+        return s;
+    }
+    {
+      ProfScope ps("cb.deflate", st);
+      if (!jobs[1].empty() &&
+          (s = launch_deflate_encode_batch(d_jobs + n, int32_t(jobs[1].size()), nchunks[1], pol->chunk_bytes, st)))
+        return s;
     }
   }
+  KVTC_CUDA_TRY(cudaEventRecord(ss->ev[3], aux));
+  KVTC_CUDA_TRY(cudaStreamWaitEvent(st, ss->ev[3], 0));          // join
   {
     ProfScope ps("cb.assemble", st);
     for (int i = 0; i < n; ++i) {
@@ -1151,47 +1184,72 @@ extern "C" kvtc_status kvtc_decompress_batch(const kvtc_basis *kb, const kvtc_pl
       if ((s = launch_inflate_batch(d_jobs, int32_t(jobs.size()), c0, err, st))) return s;
     }
   }
-  // dequantise into each item's rows, RoPE tables, tile tables
+  // dequantise into each item's rows (keys on st, values on aux beside the keys'
+  // GEMM), RoPE tables, tile tables
+  SideStream *ss = side_stream();
+  const bool ovl = !overlap_off();
+  cudaStream_t aux = ovl ? ss->s : st;
   std::vector<TileRef> tref(2 * ntiles);
-  {
-    ProfScope ps("db.dequant", st);
-    for (int i = 0; i < n; ++i) {
-      const ContainerHeader &h = hdr[i];
-      if (!h.m) continue;
+  for (int i = 0; i < n; ++i) {
+    const ContainerHeader &h = hdr[i];
+    for (int64_t j = 0; j < it[i].tiles; ++j)
       for (int sv = 0; sv < 2; ++sv) {
-        kvtc_plan *pl = const_cast<kvtc_plan *>(sv ? vp : kp);
-        __half *D = (sv ? Dh_v : Dh) + it[i].row0 * ld;
-        if ((s = launch_dequant(pl->d_pgroups, pl->d_codes_off_full, pl->G, plan_codes_off_last(pl, h.m % kTileM),
-                                pl->tile_bytes, sv ? pay_v[i] : pay_k[i], h.m, D, ld, st)))
-          return s;
-        if (pl->r_nz == 0) KVTC_CUDA_TRY(cudaMemsetAsync(D, 0, h.m * ld * 2, st));
-        for (int64_t j = 0; j < it[i].tiles; ++j) {
-          const kvtc_kv_view &vw = sv ? v_out[i] : k_out[i];
-          TileRef &r = tref[sv * ntiles + it[i].row0 / kTileM + j];
-          r = TileRef{};
-          r.bases = sv ? vbases[i] : kbases[i];
-          r.block_table = vw.block_table;
-          r.layout = vw.layout;
-          r.page_tokens = vw.page_tokens;
-          r.tok0 = h.sinks + j * kTileM;
-          r.ntok = int(std::min<int64_t>(kTileM, h.m - j * kTileM));
-        }
+        const kvtc_kv_view &vw = sv ? v_out[i] : k_out[i];
+        TileRef &r = tref[sv * ntiles + it[i].row0 / kTileM + j];
+        r = TileRef{};
+        r.bases = sv ? vbases[i] : kbases[i];
+        r.block_table = vw.block_table;
+        r.layout = vw.layout;
+        r.page_tokens = vw.page_tokens;
+        r.tok0 = h.sinks + j * kTileM;
+        r.ntok = int(std::min<int64_t>(kTileM, h.m - j * kTileM));
       }
-      if (kb->has_rope && (s = rope_table_for(kb, h.pos0 + h.sinks, h.m, cs + it[i].row0 * half, st))) return s;
-    }
   }
   if (ntiles)
     KVTC_CUDA_TRY(cudaMemcpyAsync(d_tiles, tref.data(), tref.size() * sizeof(TileRef), cudaMemcpyHostToDevice, st));
+  auto dequant_all = [&](int sv, cudaStream_t q, int ctas) -> kvtc_status {
+    kvtc_plan *pl = const_cast<kvtc_plan *>(sv ? vp : kp);
+    for (int i = 0; i < n; ++i) {
+      const ContainerHeader &h = hdr[i];
+      if (!h.m) continue;
+      __half *D = (sv ? Dh_v : Dh) + it[i].row0 * ld;
+      kvtc_status r = launch_dequant(pl->d_pgroups, pl->d_codes_off_full, pl->G, plan_codes_off_last(pl, h.m % kTileM),
+                                     pl->tile_bytes, sv ? pay_v[i] : pay_k[i], h.m, D, ld, q, ctas);
+      if (r) return r;
+      if (pl->r_nz == 0) KVTC_CUDA_TRY(cudaMemsetAsync(D, 0, h.m * ld * 2, q));
+    }
+    return KVTC_OK;
+  };
+  {
+    ProfScope ps("db.dequant", st);
+    if ((s = dequant_all(0, st, 0))) return s;
+    for (int i = 0; i < n; ++i)
+      if (hdr[i].m && kb->has_rope &&
+          (s = rope_table_for(kb, hdr[i].pos0 + hdr[i].sinks, hdr[i].m, cs + it[i].row0 * half, st)))
+        return s;
+  }
+  KVTC_CUDA_TRY(cudaEventRecord(ss->ev[2], st));                 // payloads inflated, keys expanded
   for (int sv = 0; sv < 2 && ntiles; ++sv) {
     const kvtc_basis *b = sv ? vb : kb;
     kvtc_plan *pl = const_cast<kvtc_plan *>(sv ? vp : kp);
     const Operands *op;
     if ((s = plan_operands(b, pl, &op))) return s;
-    ProfScope ps("db.reconstruct_gemm", st);
-    // the view arguments only carry the shape here: every tile's output comes from its TileRef
-    if ((s = run_reconstruct(b, pl, op, sv ? Dh_v : Dh, ld, rows, 0, 0, b->shape.layers, sv ? &v_out[0] : &k_out[0],
-                             sv ? vbases[0] : kbases[0], cs, st, d_tiles + sv * ntiles)))
-      return s;
+    if (sv == 1) KVTC_CUDA_TRY(cudaStreamWaitEvent(st, ss->ev[3], 0));
+    {
+      ProfScope ps("db.reconstruct_gemm", st);
+      // the view arguments only carry the shape here: every tile's output comes from its TileRef
+      if ((s = run_reconstruct(b, pl, op, sv ? Dh_v : Dh, ld, rows, 0, 0, b->shape.layers, sv ? &v_out[0] : &k_out[0],
+                               sv ? vbases[0] : kbases[0], cs, st, d_tiles + sv * ntiles)))
+        return s;
+    }
+    if (sv == 0) {
+      KVTC_CUDA_TRY(cudaStreamWaitEvent(aux, ss->ev[2], 0));
+      {
+        ProfScope ps(ovl ? "db.dequant_overlapped" : "db.dequant", aux);
+        if ((s = dequant_all(1, aux, ovl ? corun_ctas(2) : 0))) return s;
+      }
+      KVTC_CUDA_TRY(cudaEventRecord(ss->ev[3], aux));
+    }
   }
   {
     ProfScope ps("db.raw_tokens", st);

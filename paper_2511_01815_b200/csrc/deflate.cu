@@ -667,11 +667,12 @@ __global__ void __launch_bounds__(kEncThreads, 14) deflate_encode_batch_kernel(c
 }
 
 kvtc_status launch_deflate_encode_batch(const EncodeJob *jobs_dev, int32_t njobs, uint32_t total_chunks,
-                                        int32_t chunk, cudaStream_t st) {
+                                        int32_t chunk, cudaStream_t st, int32_t max_ctas) {
   KVTC_CHECK_ARG(chunk == 16384 || chunk == 32768 || chunk == 65536, "chunk_bytes must be 16/32/64 KiB");
   if (njobs == 0 || total_chunks == 0) return KVTC_OK;
   KVTC_MAX_CARVEOUT(deflate_encode_batch_kernel);
-  deflate_encode_batch_kernel<<<total_chunks, kEncThreads, 0, st>>>(jobs_dev, njobs, total_chunks, chunk);
+  const uint32_t grid = max_ctas > 0 ? std::min<uint32_t>(total_chunks, uint32_t(max_ctas)) : total_chunks;
+  deflate_encode_batch_kernel<<<grid, kEncThreads, 0, st>>>(jobs_dev, njobs, total_chunks, chunk);
   KVTC_LAUNCH_CHECK();
   return KVTC_OK;
 }

@@ -188,7 +188,7 @@ struct EncodeJob {
   uint32_t chunk0, pad;
 };
 kvtc_status launch_deflate_encode_batch(const EncodeJob *jobs_dev, int32_t njobs, uint32_t total_chunks,
-                                        int32_t chunk, cudaStream_t st);
+                                        int32_t chunk, cudaStream_t st, int32_t max_ctas = 0);
 // SM count x per_sm: the bounded grid of a side-stream kernel overlapping a GEMM.
 int corun_ctas(int per_sm);
 // Kernels that share an SM must run under the same shared-memory carveout: the
