@@ -170,6 +170,17 @@ kvtc_status kvtc_allocate_bits_from_coeffs(const float *P, int64_t n, int32_t r,
 kvtc_status kvtc_allocate_bits(const kvtc_basis *b, const kvtc_kv_view *seqs, int32_t nseq,
                                const int64_t *samples_host, int64_t n, const kvtc_dp_config *cfg,
                                void *stream, kvtc_plan **out);
+/* Plans for several target CRs (crs_host[ncr]; cfg->target_cr ignored) from ONE
+ * DP table computed at the largest budget: column b of the DP does not depend on
+ * how many columns were computed, so each plan equals the single-CR plan
+ * bit for bit ("backtracking can use the tables"; the paper's CR sweeps,
+ * P:L333).  out[ncr] receives one plan handle per CR. */
+kvtc_status kvtc_allocate_bits_multi(const kvtc_basis *b, const kvtc_kv_view *seqs, int32_t nseq,
+                                     const int64_t *samples_host, int64_t n, const kvtc_dp_config *cfg,
+                                     const double *crs_host, int32_t ncr, void *stream, kvtc_plan **out);
+kvtc_status kvtc_allocate_bits_from_coeffs_multi(const float *P, int64_t n, int32_t r, int32_t p_original,
+                                                 const kvtc_dp_config *cfg, const double *crs_host, int32_t ncr,
+                                                 void *stream, kvtc_plan **out);
 /* DP tables for parity tests: best_error at even budgets, [(r+1) x (B/2+1)]
  * fp64 row-major (device, caller-allocated). */
 kvtc_status kvtc_dp_best_table(const float *P, int64_t n, int32_t r, int64_t budget,

@@ -73,6 +73,8 @@ _SIGS = {
     "kvtc_calibrate": (i32, [P(View), i32, P(i64), i64, i32, P(Rope), i32, vp, P(vp)]),
     "kvtc_allocate_bits_from_coeffs": (i32, [vp, i64, i32, i32, P(DPConfig), vp, P(vp)]),
     "kvtc_allocate_bits": (i32, [vp, P(View), i32, P(i64), i64, P(DPConfig), vp, P(vp)]),
+    "kvtc_allocate_bits_multi": (i32, [vp, P(View), i32, P(i64), i64, P(DPConfig), P(f64), i32, vp, P(vp)]),
+    "kvtc_allocate_bits_from_coeffs_multi": (i32, [vp, i64, i32, i32, P(DPConfig), P(f64), i32, vp, P(vp)]),
     "kvtc_dp_best_table": (i32, [vp, i64, i32, i64, P(DPConfig), vp, vp]),
     "kvtc_plan_create": (i32, [i32, i32, P(i32), P(i32), P(i32), P(vp)]),
     "kvtc_plan_destroy": (i32, [vp]),

@@ -414,25 +414,15 @@ extern "C" kvtc_status kvtc_dp_best_table(const float *P, int64_t n, int32_t r, 
   return s;
 }
 
-extern "C" kvtc_status kvtc_allocate_bits_from_coeffs(const float *P, int64_t n, int32_t r, int32_t p_original,
-                                                      const kvtc_dp_config *cfg, void *stream, kvtc_plan **out) {
-  KVTC_CHECK_ARG(cfg && out && cfg->target_cr > 0 && p_original > 0, "allocate arguments");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int64_t cap = cfg->dp_row_cap > 0 ? cfg->dp_row_cap : 32768;     // P:L1145, Q8
-  n = std::min(n, cap);
-  const int64_t B = budget_from(cfg, p_original);
-  DPRun run;
-  std::vector<int32_t> sizes;
-  kvtc_status s = dp_full(P, n, r, B, cfg, st, run, sizes);
-  if (s) {
-    dp_free(run);
-    return s;
-  }
+namespace {
+// Plan of budget column B (bits) from a finished DP run: backtrack (Q7) and compile.
+kvtc_status backtrack_plan(const DPRun &run, int32_t r, int64_t B, const std::vector<int32_t> &sizes,
+                           cudaStream_t st, kvtc_plan **out) {
   int32_t *d_out = nullptr;
   double *d_err = nullptr;
+  int32_t *d_sizes = nullptr;
   KVTC_CUDA_TRY(cudaMalloc(&d_out, (1 + 3 * size_t(r)) * 4));
   KVTC_CUDA_TRY(cudaMalloc(&d_err, 8));
-  int32_t *d_sizes = nullptr;
   KVTC_CUDA_TRY(cudaMalloc(&d_sizes, sizes.size() * 4));
   KVTC_CUDA_TRY(cudaMemcpy(d_sizes, sizes.data(), sizes.size() * 4, cudaMemcpyHostToDevice));
   dp_backtrack_kernel<<<1, 1, 0, st>>>(run.ptr, r, run.W, B / 2, d_sizes, d_out, run.best, d_err);
@@ -445,7 +435,6 @@ extern "C" kvtc_status kvtc_allocate_bits_from_coeffs(const float *P, int64_t n,
   cudaFree(d_out);
   cudaFree(d_err);
   cudaFree(d_sizes);
-  dp_free(run);
   const int ng = h[0];
   std::vector<int32_t> gs, gz, gt;
   for (int k = ng - 1; k >= 0; --k) {            // reverse: PC order
@@ -455,18 +444,60 @@ extern "C" kvtc_status kvtc_allocate_bits_from_coeffs(const float *P, int64_t n,
     gt.push_back(h[1 + 3 * k + 2]);
   }
   kvtc_plan *pl = nullptr;
-  s = kvtc_plan_create(r, int32_t(gs.size()), gs.data(), gz.data(), gt.data(), &pl);
+  kvtc_status s = kvtc_plan_create(r, int32_t(gs.size()), gs.data(), gz.data(), gt.data(), &pl);
   if (s) return s;
   pl->expected_error = err;
   pl->budget = B;
   *out = pl;
   return KVTC_OK;
 }
+}  // namespace
+
+extern "C" kvtc_status kvtc_allocate_bits_from_coeffs(const float *P, int64_t n, int32_t r, int32_t p_original,
+                                                      const kvtc_dp_config *cfg, void *stream, kvtc_plan **out) {
+  KVTC_CHECK_ARG(cfg && out && cfg->target_cr > 0 && p_original > 0, "allocate arguments");
+  return kvtc_allocate_bits_from_coeffs_multi(P, n, r, p_original, cfg, &cfg->target_cr, 1, stream, out);
+}
+
+// One DP table at the largest budget serves every target CR: column b of the
+// table does not depend on how many columns were computed, so the plan of budget
+// B' is the backtrack from (r, B') (Q6/Q7; pinned against single-CR plans).
+extern "C" kvtc_status kvtc_allocate_bits_from_coeffs_multi(const float *P, int64_t n, int32_t r, int32_t p_original,
+                                                            const kvtc_dp_config *cfg, const double *crs_host,
+                                                            int32_t ncr, void *stream, kvtc_plan **out) {
+  KVTC_CHECK_ARG(cfg && out && crs_host && ncr > 0 && p_original > 0, "allocate arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t cap = cfg->dp_row_cap > 0 ? cfg->dp_row_cap : 32768;     // P:L1145, Q8
+  n = std::min(n, cap);
+  std::vector<int64_t> Bs(ncr);
+  int64_t Bmax = 0;
+  for (int i = 0; i < ncr; ++i) {
+    KVTC_CHECK_ARG(crs_host[i] > 0, "target_cr must be > 0");
+    kvtc_dp_config c = *cfg;
+    c.target_cr = crs_host[i];
+    Bs[i] = budget_from(&c, p_original);
+    Bmax = std::max(Bmax, Bs[i]);
+  }
+  DPRun run;
+  std::vector<int32_t> sizes;
+  kvtc_status s = dp_full(P, n, r, Bmax, cfg, st, run, sizes);
+  for (int i = 0; i < ncr && s == KVTC_OK; ++i) s = backtrack_plan(run, r, Bs[i], sizes, st, &out[i]);
+  dp_free(run);
+  return s;
+}
 
 extern "C" kvtc_status kvtc_allocate_bits(const kvtc_basis *b, const kvtc_kv_view *seqs, int32_t nseq,
                                           const int64_t *samples_host, int64_t n, const kvtc_dp_config *cfg,
                                           void *stream, kvtc_plan **out) {
-  KVTC_CHECK_ARG(b && seqs && nseq > 0 && samples_host && n > 0 && cfg && out, "allocate arguments");
+  KVTC_CHECK_ARG(cfg, "allocate arguments");
+  return kvtc_allocate_bits_multi(b, seqs, nseq, samples_host, n, cfg, &cfg->target_cr, 1, stream, out);
+}
+
+extern "C" kvtc_status kvtc_allocate_bits_multi(const kvtc_basis *b, const kvtc_kv_view *seqs, int32_t nseq,
+                                                const int64_t *samples_host, int64_t n, const kvtc_dp_config *cfg,
+                                                const double *crs_host, int32_t ncr, void *stream, kvtc_plan **out) {
+  KVTC_CHECK_ARG(b && seqs && nseq > 0 && samples_host && n > 0 && cfg && out && crs_host && ncr > 0,
+                 "allocate arguments");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t cap = cfg->dp_row_cap > 0 ? cfg->dp_row_cap : 32768;
   const int64_t nd = std::min(n, cap);                       // first rows in sample order (Q8)
@@ -487,7 +518,7 @@ extern "C" kvtc_status kvtc_allocate_bits(const kvtc_basis *b, const kvtc_kv_vie
   KVTC_CUDA_TRY(cudaMemcpy(rows, samples_host, size_t(nd) * 16, cudaMemcpyHostToDevice));
   s = launch_gather_rows(seqs, nseq, bases, rows, nd, b->d_invf, b->has_rope ? 1 : 0, b->pairing, b->p, X, st);
   if (s == KVTC_OK) s = kvtc_stage_project(b, nullptr, X, nd, P, stream);
-  if (s == KVTC_OK) s = kvtc_allocate_bits_from_coeffs(P, nd, b->r, b->p, cfg, stream, out);
+  if (s == KVTC_OK) s = kvtc_allocate_bits_from_coeffs_multi(P, nd, b->r, b->p, cfg, crs_host, ncr, stream, out);
   cudaStreamSynchronize(st);
   cudaFree(bases);
   cudaFree(X);

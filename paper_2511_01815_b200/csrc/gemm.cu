@@ -817,12 +817,13 @@ static kvtc_status launch(const CUtensorMap *tmA, const CUtensorMap *tmB, const 
     // over modes overrides (0 = off)
     const char *ts = getenv("KVTC_TILE_SYNC");
     const int sync_mask = ts ? atoi(ts) : ((1 << EPI_QUANT) | (1 << EPI_RECON));
-    // lag: compress tiles (512 k-steps) must start together; decompress tiles (68
-    // k-steps) tolerate one tile of drift (KVTC_SYNC_LAG_<MODE> overrides)
+    // lag 0: every tile starts together (KVTC_SYNC_LAG_<MODE> = k lets a producer
+    // run k tiles ahead; lag 1 on the decompress GEMM doubled its DRAM reads in ncu
+    // for no step-time gain)
     static const char *lag_names[4] = {"KVTC_SYNC_LAG_F32", "KVTC_SYNC_LAG_QUANT", "KVTC_SYNC_LAG_RECON",
                                        "KVTC_SYNC_LAG_XTX"};
     const char *lg = getenv(lag_names[MODE]);
-    pp.sync_lag = lg ? std::max(0, atoi(lg)) : (MODE == EPI_RECON ? 1 : 0);
+    pp.sync_lag = lg ? std::max(0, atoi(lg)) : 0;
     if ((sync_mask >> MODE) & 1) {
       if (!(pp.tile_sync = next_sync_counter())) return KVTC_E_CUDA;
       KVTC_CUDA_TRY(cudaMemsetAsync(pp.tile_sync, 0, sizeof(unsigned long long), st));

@@ -412,6 +412,29 @@ def allocate_bits(basis: Basis, views: list, samples, target_cr: float, sizes=(1
     return Plan(out)
 
 
+def allocate_bits_multi(basis: Basis, views: list, samples, target_crs, sizes=(1, 16, 64, 256, 1024),
+                        type_mask: int = 0xF, dp_row_cap: int = 32768, stream=None) -> list:
+    """kvtc_allocate_bits_multi: one plan per target CR from one DP table."""
+    cfg, keep = dp_config(max(target_crs), sizes, type_mask, dp_row_cap)
+    s, sp = _samples(samples)
+    arr = _views(views)
+    crs = (C.c_double * len(target_crs))(*target_crs)
+    outs = (C.c_void_p * len(target_crs))()
+    check(lib().kvtc_allocate_bits_multi(basis.h, arr, len(views), sp, len(s), C.byref(cfg), crs, len(target_crs),
+                                         _stream(stream), outs))
+    return [Plan(C.c_void_p(o)) for o in outs]
+
+
+def allocate_bits_from_coeffs_multi(P: torch.Tensor, p_original: int, target_crs, sizes=(1, 16, 64, 256, 1024),
+                                    type_mask: int = 0xF, dp_row_cap: int = 32768, stream=None) -> list:
+    cfg, keep = dp_config(max(target_crs), sizes, type_mask, dp_row_cap)
+    crs = (C.c_double * len(target_crs))(*target_crs)
+    outs = (C.c_void_p * len(target_crs))()
+    check(lib().kvtc_allocate_bits_from_coeffs_multi(_ptr(P), P.shape[0], P.shape[1], p_original, C.byref(cfg), crs,
+                                                     len(target_crs), _stream(stream), outs))
+    return [Plan(C.c_void_p(o)) for o in outs]
+
+
 def dp_best_table(P: torch.Tensor, budget: int, sizes=(1, 16, 64, 256, 1024), type_mask: int = 0xF, stream=None):
     cfg, keep = dp_config(1.0, sizes, type_mask, P.shape[0])
     r = P.shape[1]

@@ -71,6 +71,21 @@ def test_dp_on_calibrated_coefficients(K):
             assert info.expected_error == res.best[-1, B]
 
 
+def test_multi_cr_plans_equal_oracle_plans(K):
+    """One DP table at the largest budget, one backtrack per CR (kvtc_allocate_bits_
+    from_coeffs_multi) == the oracle's DP run separately at every CR."""
+    spec, invf, kb, vb, Ck, Cv = E.setup("toy")
+    P = OPCA.dp_coefficients(kb, Ck).astype(np.float32)
+    crs = [32.0, 4.0, 16.0, 8.0, 12.5]
+    plans = K.allocate_bits_from_coeffs_multi(torch.from_numpy(P).cuda(), spec.p, crs)
+    for cr, plan in zip(crs, plans):
+        oplan, res, B = ODP.allocate(P.astype(np.float64), cr, spec.p)
+        info = plan.info()
+        assert info.budget == B
+        assert info.groups == [tuple(g) for g in oplan.groups], cr
+        assert info.expected_error == res.best[-1, B]
+
+
 @pytest.mark.parametrize("name", ["toy", "mid"])
 def test_calibrate_vs_oracle(K, name):
     spec, invf, kb, vb, Ck, Cv = E.setup(name)

@@ -108,19 +108,29 @@ def _check(K, spec, KB, VB, KP, VP, t, pos0, label):
     return 2 * 2 * p * m / comp
 
 
+SWEEP = [8.0, 16.0, 32.0]
+
+
 @pytest.fixture(scope="module")
 def nemo(K):
+    """One calibration, and ONE DP table per stream for the whole CR sweep
+    (kvtc_allocate_bits_multi), checked against a separate DP run at CR 16."""
     from kvtc_inputs import make_spec
     spec = make_spec("nemo12b")
     (kb, vb), samples = _bases(K, spec)
-    return spec, kb, vb, samples
+    (KB, kviews, _), (VB, vviews, _) = kb, vb
+    kplans = K.allocate_bits_multi(KB, kviews, samples, SWEEP)
+    vplans = K.allocate_bits_multi(VB, vviews, samples, SWEEP)
+    single = K.allocate_bits(KB, kviews, samples, 16.0)
+    assert single.info().groups == kplans[1].info().groups
+    assert single.info().expected_error == kplans[1].info().expected_error
+    return spec, kb, vb, samples, dict(zip(SWEEP, zip(kplans, vplans)))
 
 
-@pytest.mark.parametrize("cr_target", [8.0, 16.0, 32.0])
+@pytest.mark.parametrize("cr_target", SWEEP)
 def test_nemo12b_cr_sweep(K, nemo, cr_target):
-    spec, (KB, kviews, _), (VB, vviews, _), samples = nemo
-    KP = K.allocate_bits(KB, kviews, samples, cr_target)
-    VP = K.allocate_bits(VB, vviews, samples, cr_target)
+    spec, (KB, kviews, _), (VB, vviews, _), samples, plans = nemo
+    KP, VP = plans[cr_target]
     p = spec.layers * spec.kv_heads * spec.head_dim
     assert KP.info().budget == int(16 * p // cr_target)
     cr = _check(K, spec, KB, VB, KP, VP, 65536, 0, f"nemo12b cr{cr_target:g}")
