@@ -90,6 +90,7 @@ struct Params {
   unsigned long long *tile_sync;   // non-null: producers align tile starts (see tile_barrier)
   int32_t sync_lag;                // a producer may run this many tiles ahead of the slowest
   int32_t nsegs;                   // QUANT: number of 256-column segments
+  int32_t epi_skip;                // measurement only (KVTC_EPI_SKIP=1): release TMEM without an epilogue
   const TileRef *tiles;            // batched rows (QUANT / RECON), else null
 };
 
@@ -518,7 +519,7 @@ __global__ void __launch_bounds__(kThreads, MODE == EPI_RECON ? 1 : 2)
         const bool last = ntok < kTileM;
         uint8_t *tile_base = tref ? tref->payload : P.payload + T.mb * P.tile_bytes;
         const int64_t *codes_off_last = tref ? tref->codes_off : P.codes_off_last;
-        const int nsub = tile_nsub<NSUB>(P, T);
+        const int nsub = P.epi_skip ? 0 : tile_nsub<NSUB>(P, T);
         for (int sb = 0; sb < nsub; ++sb) {
         const SegDesc sdq = P.segs[T.nb * NSUB + sb];
         const uint32_t trow_s = trow + (NSUB == 2 ? uint32_t(sb * kMaxTileN) : 0u);
@@ -806,15 +807,17 @@ static kvtc_status launch(const CUtensorMap *tmA, const CUtensorMap *tmB, const 
   {
     static const char *names[4] = {"KVTC_GROUP_M_F32", "KVTC_GROUP_M_QUANT", "KVTC_GROUP_M_RECON", "KVTC_GROUP_M_XTX"};
     const char *e = getenv(names[MODE]);
-    // defaults from an ncu sweep at base clocks (scripts/sweep_env.py): fewer
-    // DRAM re-reads of the streamed operand
-    static const int defaults[4] = {kGroupM, 4, 16, kGroupM};
+    // defaults from interleaved A/B sweeps of the bench step with the tile barrier on
+    // (scripts/sweep_env.py; 16 beat 4 and 8 on the compress GEMM by ~0.4 ms per step)
+    static const int defaults[4] = {kGroupM, 16, 16, kGroupM};
     pp.group_m = e ? std::max(1, atoi(e)) : defaults[MODE];
     const char *ha = getenv("KVTC_HINT_A"), *hb = getenv("KVTC_HINT_B");
     if (ha) pp.hint_a = atoi(ha);
     if (hb) pp.hint_b = atoi(hb);
     // soft tile barrier (tile_barrier) for the codec GEMMs; KVTC_TILE_SYNC = bit mask
     // over modes overrides (0 = off)
+    const char *es = getenv("KVTC_EPI_SKIP");
+    pp.epi_skip = es && es[0] == '1';
     const char *ts = getenv("KVTC_TILE_SYNC");
     const int sync_mask = ts ? atoi(ts) : ((1 << EPI_QUANT) | (1 << EPI_RECON));
     // lag 0: every tile starts together (KVTC_SYNC_LAG_<MODE> = k lets a producer
