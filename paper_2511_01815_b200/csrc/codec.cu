@@ -58,7 +58,8 @@ kvtc_status tmap_X(CUtensorMap *m, const void *X, int64_t rows, int64_t p, int64
 // A contiguous cache whose layers sit at a constant positive stride can be read
 // by the GEMM in place through a 3-D tensor map (no gathered copy of X): rows
 // are tokens, the K axis walks layer by layer.  Returns false if not eligible.
-bool direct_view_map(const kvtc_kv_view &v, int64_t tok0, CUtensorMap *m) {
+bool direct_view_map(const kvtc_kv_view &v, int64_t tok0, CUtensorMap *m, int64_t *layer_rows) {
+  *layer_rows = 0;
   const int64_t hd = int64_t(v.shape.kv_heads) * v.shape.head_dim;
   if (v.layout != KVTC_LAYOUT_CONTIGUOUS || hd % kBlockK || v.tokens > INT32_MAX / 2 || tok0 < 0) return false;
   const auto base = reinterpret_cast<uintptr_t>(v.layer_base_host[0]);
@@ -71,6 +72,14 @@ bool direct_view_map(const kvtc_kv_view &v, int64_t tok0, CUtensorMap *m) {
     for (int l = 2; l < v.shape.layers; ++l)
       if (reinterpret_cast<uintptr_t>(v.layer_base_host[l]) != base + l * stride) return false;
   }
+  // layers packed back to back (one [layers][tokens][h*d] tensor): KVTC_DIRECT_2D=1
+  // reads it through a 2-D map over [layers * tokens][h*d] instead
+  const char *e2 = getenv("KVTC_DIRECT_2D");
+  if (e2 && e2[0] == '1' && stride == uint64_t(v.tokens) * hd * 2 && v.tokens * v.shape.layers < INT32_MAX / 2) {
+    *layer_rows = v.tokens;
+    return make_tmap_2d(m, v.layer_base_host[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, uint64_t(hd),
+                        uint64_t(v.tokens) * v.shape.layers, uint64_t(hd) * 2, kBlockK, kTileM) == KVTC_OK;
+  }
   return make_tmap_3d(m, v.layer_base_host[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, uint64_t(hd), uint64_t(v.tokens),
                       uint64_t(v.shape.layers), uint64_t(hd) * 2, stride, kBlockK, kTileM) == KVTC_OK;
 }
@@ -80,7 +89,8 @@ bool direct_view_map(const kvtc_kv_view &v, int64_t tok0, CUtensorMap *m) {
 // the plan's wide groups (nullptr if it has none).
 kvtc_status run_project_quant(const kvtc_basis *b, kvtc_plan *pl, const Operands *op, const void *X, int64_t m,
                               uint8_t *payload, float *wide, cudaStream_t st, const CUtensorMap *direct = nullptr,
-                              int64_t tok0 = 0, int64_t ldx = 0, const TileRef *tiles = nullptr) {
+                              int64_t tok0 = 0, int64_t ldx = 0, const TileRef *tiles = nullptr,
+                              int64_t layer_rows = 0) {
   if (m == 0 || pl->G == 0) return KVTC_OK;
   KVTC_CHECK_ARG(pl->nwide == 0 || wide, "wide-group scratch");
   CUtensorMap tA;
@@ -91,6 +101,7 @@ kvtc_status run_project_quant(const kvtc_basis *b, kvtc_plan *pl, const Operands
   if (direct) {
     a.a_hd = b->shape.kv_heads * b->shape.head_dim;
     a.a_row0 = tok0;
+    a.a_layer_rows = layer_rows;
   }
   a.tmB = &op->tm_VcT;
   a.K = b->p;
@@ -513,7 +524,8 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
   cudaStream_t aux = ovl ? ss->s : st;
   const int side_ctas = ovl ? corun_ctas(2) : 0;
   CUtensorMap tV;
-  const bool v_direct = !direct_off() && direct_view_map(*v, pol->sinks, &tV);
+  int64_t v_layer_rows = 0;
+  const bool v_direct = !direct_off() && direct_view_map(*v, pol->sinks, &tV, &v_layer_rows);
   auto gather_keys = [&](cudaStream_t q, int ctas, const char *tag) -> kvtc_status {
     ProfScope ps(tag, q);
     kvtc_status r = rope_table_for(kb, k->pos0 + pol->sinks, L.m, cs, q);
@@ -529,7 +541,7 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
     uint8_t *pay = (sv ? payload_v : payload_k) + (r0 / kTileM) * pl->tile_bytes;
     float *wd = wide ? wide + r0 * pl->wide_cols : nullptr;      // scratch rows of stride wide_cols
     return sv ? run_project_quant(vb, vpl, vop, X, r1 - r0, pay, wd, st, direct ? &tV : nullptr, pol->sinks + r0,
-                                  ldx)
+                                  ldx, nullptr, v_layer_rows)
               : run_project_quant(kb, kpl, kop, X + r0 * ldx, r1 - r0, pay, wd, st, nullptr, 0, ldx);
   };
   auto encode = [&](int sv, cudaStream_t q, int ctas, const char *tag, uint32_t c0 = 0,

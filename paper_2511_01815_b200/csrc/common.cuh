@@ -84,19 +84,32 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// try_wait with a suspend-time hint: the waiting thread is descheduled until the
+// phase completes (or ~hint ns pass) instead of spinning, so waiting producer /
+// MMA / epilogue warps do not take issue slots from the working ones (ncu showed
+// the spin loops among the most-executed instructions of the GEMMs).
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t *bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+      : "memory");
+  return ok != 0;
+}
 // Waits for the phase; a wait longer than ~4 s (a pipeline that can no longer
 // complete) traps, so the launch fails with an error instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
   uint64_t t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  for (uint32_t n = 1;; ++n) {
-    if (mbar_try_wait(bar, parity)) return;
-    if ((n & 1023) == 0) {
-      uint64_t t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      if (t - t0 > 4000000000ull) __trap();
-    }
+  while (true) {
+    if (mbar_try_wait_sleep(bar, parity)) return;
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 4000000000ull) __trap();
   }
 }
 

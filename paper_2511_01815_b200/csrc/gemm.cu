@@ -84,6 +84,7 @@ struct Params {
   int32_t fmt;         // 0 fp16, 1 bf16 operands
   int32_t tile_n;      // RECON / F32 / XTX N tile
   int32_t a_hd;        // > 0: A is the 3-D cache map (GemmCompressArgs::a_hd)
+  int64_t a_layer_rows;  // > 0: A is a 2-D map over [layers * tokens][h*d] (layer stride = tokens rows)
   int64_t a_row0;
   int32_t group_m;     // raster group (M-blocks or M-pairs)
   int32_t hint_a, hint_b;   // L2 policies of the A / B loads
@@ -396,6 +397,9 @@ __global__ void __launch_bounds__(kThreads, MODE == EPI_RECON ? 1 : 2)
           if (leader) mbar_arrive_expect_tx(&full_bar[s], 2 * kStageBytes);
           if (P.a_hd && P.hint_a)
             tma_3d_hint(true, a, &tmA, &full_bar[s], ka % P.a_hd, int(P.a_row0) + T.mb * kTileM, ka / P.a_hd, pol_a);
+          else if (P.a_hd && P.a_layer_rows)
+            tma_load_2d_pair(a, &tmA, &full_bar[s], ka % P.a_hd,
+                             int((ka / P.a_hd) * P.a_layer_rows + P.a_row0) + T.mb * kTileM);
           else if (P.a_hd)
             tma_load_3d_pair(a, &tmA, &full_bar[s], ka % P.a_hd, int(P.a_row0) + T.mb * kTileM, ka / P.a_hd);
           else if (P.hint_a)
@@ -882,6 +886,7 @@ kvtc_status launch_gemm_project_quant(const GemmCompressArgs &a, cudaStream_t st
   p.codes_off_last = a.codes_off_last;
   p.fmt = 1;
   p.a_hd = a.a_hd;
+  p.a_layer_rows = a.a_layer_rows;
   p.a_row0 = a.a_row0;
   p.num_m = int32_t(ceil_div(a.m, kTileM));
   p.nsegs = a.nsegs;

@@ -103,6 +103,7 @@ struct GemmCompressArgs {
   // row r of X is token a_row0 + r (k-block kb = layer kb*64/hd, column kb*64%hd)
   int32_t a_hd;
   int64_t a_row0;
+  int64_t a_layer_rows;    // a_hd > 0 and a_layer_rows > 0: tmA is a 2-D map over [layers * tokens][h*d]
   const TileRef *tiles;    // non-null: batched rows (tile mb -> tiles[mb]); payload / m unused
 };
 kvtc_status launch_gemm_project_f32(const GemmCompressArgs &a, int32_t ncols, cudaStream_t st);

@@ -1,0 +1,17 @@
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_exp14.log 2>&1 || exit 1
+timeout 900 python -m pytest tests/test_gpu_stages.py tests/test_gpu_codec.py tests/test_gpu_calib_dp.py -x -q > gpurun_out/pytest_exp14.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_exp14.log | cut -c1-200
+timeout 1200 python scripts/sweep_env.py KVTC_QUANT_NSUB=2 --iters 10 > gpurun_out/sweep_exp14.log 2>&1; echo sweep rc=$?
+grep sweep gpurun_out/sweep_exp14.log | cut -c1-330
+for V in "KVTC_QUANT_NSUB=1" "KVTC_QUANT_NSUB=2" "KVTC_QUANT_NSUB=2 KVTC_EPI_SKIP=1"; do
+env $V timeout 900 ncu --metrics gpu__time_duration.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,sm__cycles_elapsed.avg.per_second,lts__t_bytes.sum,dram__bytes_read.sum -k regex:gemm --profile-from-start off --clock-control none --csv --log-file gpurun_out/ncu_exp14.csv python scripts/profile_run.py > /dev/null 2>&1
+python - "$V" <<'PY'
+import csv, sys
+rows=list(csv.reader(open("gpurun_out/ncu_exp14.csv")))
+hdr=None; d={}
+for r in rows:
+    if r and r[0]=="ID": hdr=r; continue
+    if hdr and len(r)==len(hdr):
+        x=dict(zip(hdr,r)); d.setdefault(x["ID"],{"k":x["Kernel Name"][:20]})[x["Metric Name"]]=x["Metric Value"]
+for i,x in list(d.items())[:4]: print(sys.argv[1], x["k"], {k.split("__")[1][:22]:v for k,v in x.items() if k!="k"})
+PY
+done

@@ -163,10 +163,13 @@ def test_direct_cache_read_matches_gather(K, monkeypatch):
         return cont.cpu().numpy().tobytes()
 
     direct = run(K.KVView(vd))
+    monkeypatch.setenv("KVTC_DIRECT_2D", "1")          # packed layers through a 2-D map
+    direct2d = run(K.KVView(vd))
+    monkeypatch.delenv("KVTC_DIRECT_2D")
     big = torch.zeros(spec.layers, tokens + 77, spec.kv_heads, spec.head_dim, dtype=torch.bfloat16, device="cuda")
     big[:, :tokens] = vd
     strided = run(K.KVView(big, tokens=tokens))
     separate = run(K.KVView([vd[i].clone() for i in range(spec.layers)]))
     monkeypatch.setenv("KVTC_NO_DIRECT", "1")
     gathered = run(K.KVView(vd))
-    assert direct == gathered and strided == gathered and separate == gathered
+    assert direct == gathered and direct2d == gathered and strided == gathered and separate == gathered
