@@ -458,6 +458,29 @@ def main():
                 "peak_source": f"{peak_src} bf16 sustained (kernel timed inside the step)",
                 "algorithmic": f"2*m*p*r_nz flops per launch, m={m}, p={p}, r_nz={rnz}"}
 
+    # ---- layer-streamed decompression: time until layer 0 is rebuilt
+    # (inflate + dequantise once, then one layer's V^T columns) vs all layers
+    streaming = None
+    if not args.no_e2e:
+        sd = K.StreamedDecompress(kb, kp, vb, vp, cont)          # warm-up + workspace
+        t0, t1, t2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        firsts, alls = [], []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t0.record(stream)
+            sd.begin()
+            sd.layers(koview, voview, 0, 1)
+            t1.record(stream)
+            sd.layers(koview, voview, 1, spec.layers)
+            t2.record(stream)
+            torch.cuda.synchronize()
+            firsts.append(t0.elapsed_time(t1))
+            alls.append(t0.elapsed_time(t2))
+        streaming = {"first_layer_ms": statistics.median(firsts), "all_layers_ms": statistics.median(alls),
+                     "layers": spec.layers,
+                     "what": "kvtc_decompress_begin (inflate + dequantise once) + kvtc_decompress_layers(0, 1): "
+                             "attention on layer 0 can start after first_layer_ms"}
+
     # ---- end to end through the public API with host buffers: every step copies
     # that step's K/V from pinned host memory to the device (H2D), compresses and
     # decompresses it, and reads the reconstructed K/V back (D2H).  Steps are
@@ -611,6 +634,7 @@ def main():
                            "cr": cr, "cr_pre_deflate": cr_pre, "r_eff": [kinfo.r_eff, vinfo.r_eff], "r_nz": rnz,
                            "setup_s": round(setup_s, 1), "setup": setup_info},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "layer_streaming": streaming,
                 "clocks": clk, "stages": stages}
         print(json.dumps(line), flush=True)
     if dist:

@@ -225,6 +225,25 @@ kvtc_status kvtc_decompress(const kvtc_basis *kb, const kvtc_plan *kp, const kvt
                             const void *in, size_t in_len, int32_t layer_begin, int32_t layer_end,
                             const kvtc_kv_view *k_out, const kvtc_kv_view *v_out, void *workspace,
                             size_t workspace_bytes, void *stream);
+/* ------------------------------------------- layer-streamed decompression
+ * the inverse projection "can be performed layer-by-layer using
+ * sub-matrices of V^T, allowing generation to begin early".  The PCA
+ * coefficients mix all layers, so kvtc_decompress_begin inflates and
+ * dequantises the container ONCE into `workspace` (kvtc_decompress_workspace_bytes
+ * of it; one synchronisation to read the header); each kvtc_decompress_layers
+ * call then rebuilds layers [layer_begin, layer_end) only (their h*d columns of
+ * V^T, plus those layers' raw sink / window tokens), reading the coefficients from
+ * the same workspace.  header_host: the container's first KVTC_HEADER_BYTES
+ * bytes on the host.  The workspace must not be reused in between.  Results equal
+ * kvtc_decompress bit for bit. */
+kvtc_status kvtc_decompress_begin(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb,
+                                  const kvtc_plan *vp, const void *in, size_t in_len, void *workspace,
+                                  size_t workspace_bytes, void *stream);
+kvtc_status kvtc_decompress_layers(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb,
+                                   const kvtc_plan *vp, const void *in, const void *header_host, int32_t layer_begin,
+                                   int32_t layer_end, const kvtc_kv_view *k_out, const kvtc_kv_view *v_out,
+                                   void *workspace, size_t workspace_bytes, void *stream);
+
 /* ------------------------------------------------------- batched codec
  * n conversations (or token ranges of conversations: a view whose layer bases
  * are offset by a tokens and pos0 += a) in one call.  Their middle tokens are

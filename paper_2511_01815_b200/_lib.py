@@ -84,6 +84,8 @@ _SIGS = {
     "kvtc_compress": (i32, [vp, vp, vp, vp, P(View), P(View), P(Policy), vp, sz, P(sz), vp, sz, vp]),
     "kvtc_decompress_workspace_bytes": (sz, [vp, vp, vp, vp, vp]),
     "kvtc_decompress": (i32, [vp, vp, vp, vp, vp, sz, i32, i32, P(View), P(View), vp, sz, vp]),
+    "kvtc_decompress_begin": (i32, [vp, vp, vp, vp, vp, sz, vp, sz, vp]),
+    "kvtc_decompress_layers": (i32, [vp, vp, vp, vp, vp, C.c_char_p, i32, i32, P(View), P(View), vp, sz, vp]),
     "kvtc_compress_batch_workspace_bytes": (sz, [vp, vp, vp, vp, P(View), i32, P(Policy)]),
     "kvtc_compress_batch": (i32, [vp, vp, vp, vp, P(View), P(View), i32, P(Policy), P(vp), P(sz), P(sz), vp, sz,
                                   vp]),

@@ -793,6 +793,163 @@ extern "C" kvtc_status kvtc_decompress(const kvtc_basis *kb, const kvtc_plan *kp
   return KVTC_OK;
 }
 
+// ============================================== layer-streamed decompression
+// "the inverse projection ... can be performed layer-by-layer using
+// sub-matrices of V^T, allowing generation to begin early".  The coefficients D^
+// mix all layers, so inflate + dequantise run ONCE (kvtc_decompress_begin, into
+// the caller's workspace); each kvtc_decompress_layers call then runs only the
+// reconstruction GEMMs over its layers' h*d columns of V_d^T (and copies those
+// layers' raw tokens), so a consumer can start on layer 0 while later layers are
+// still being rebuilt.  Workspace layout = kvtc_decompress's.
+namespace {
+kvtc_status read_checked_header(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb, const kvtc_plan *vp,
+                                const void *header_host, size_t in_len, ContainerHeader *out) {
+  ContainerHeader h;
+  memcpy(&h, header_host, sizeof(h));
+  kvtc_container_info info;
+  kvtc_status s = kvtc_container_parse(&h, &info);
+  if (s) return s;
+  const kvtc_shape shp{h.layers, h.kv_heads, h.head_dim};
+  if (!same_shape(shp, kb->shape) || !same_shape(shp, vb->shape)) {
+    set_error("container shape does not match the bases");
+    return KVTC_E_MISMATCH;
+  }
+  if (h.basis_fp[0] != kb->fp || h.basis_fp[1] != vb->fp || h.plan_fp[0] != kp->fp || h.plan_fp[1] != vp->fp) {
+    set_error("container was written with a different basis or plan");
+    return KVTC_E_MISMATCH;
+  }
+  if (in_len && info.total_bytes > in_len) {
+    set_error("container length %llu > buffer %zu", (unsigned long long)info.total_bytes, in_len);
+    return KVTC_E_CORRUPT;
+  }
+  if (h.m && (h.payload_bytes[0] != kvtc_payload_bytes(kp, h.m) || h.payload_bytes[1] != kvtc_payload_bytes(vp, h.m))) {
+    set_error("payload sizes do not match the plans");
+    return KVTC_E_CORRUPT;
+  }
+  *out = h;
+  return KVTC_OK;
+}
+struct DecompWs {
+  __nv_bfloat16 **kbases, **vbases;
+  int32_t *err;
+  uint8_t *payloads[2];
+  __half *Dh[2];
+  float2 *cs;
+  int64_t ld;
+};
+DecompWs carve_decomp(const kvtc_plan *kp, const kvtc_plan *vp, const ContainerHeader &h, void *workspace,
+                      size_t workspace_bytes) {
+  Bump ws(workspace, workspace_bytes);
+  DecompWs w;
+  w.kbases = ws.take<__nv_bfloat16 *>(h.layers);
+  w.vbases = ws.take<__nv_bfloat16 *>(h.layers);
+  w.err = ws.take<int32_t>(4);
+  w.payloads[0] = ws.take<uint8_t>(h.payload_bytes[0] + 16);
+  w.payloads[1] = ws.take<uint8_t>(h.payload_bytes[1] + 16);
+  w.ld = std::max(std::max(kp->r_nz_pad, vp->r_nz_pad), 8);
+  w.Dh[0] = ws.take<__half>(h.m * w.ld);
+  w.Dh[1] = ws.take<__half>(h.m * w.ld);
+  w.cs = ws.take<float2>(h.m * (h.head_dim / 2));
+  return w;
+}
+}  // namespace
+
+extern "C" kvtc_status kvtc_decompress_begin(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb,
+                                             const kvtc_plan *vp, const void *in, size_t in_len, void *workspace,
+                                             size_t workspace_bytes, void *stream) {
+  KVTC_CHECK_ARG(kb && kp && vb && vp && in && in_len >= KVTC_HEADER_BYTES, "decompress_begin arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ContainerHeader hh;
+  KVTC_CUDA_TRY(cudaMemcpyAsync(&hh, in, sizeof(hh), cudaMemcpyDeviceToHost, st));
+  KVTC_CUDA_TRY(cudaStreamSynchronize(st));
+  ContainerHeader h;
+  kvtc_status s = read_checked_header(kb, kp, vb, vp, &hh, in_len, &h);
+  if (s) return s;
+  const size_t need = kvtc_decompress_workspace_bytes(kb, kp, vb, vp, &h);
+  if (!workspace || workspace_bytes < need) {
+    set_error("workspace %zu < %zu", workspace_bytes, need);
+    return KVTC_E_CAPACITY;
+  }
+  if (!h.m) return KVTC_OK;
+  DecompWs w = carve_decomp(kp, vp, h, workspace, workspace_bytes);
+  const uint8_t *ib = static_cast<const uint8_t *>(in);
+  const uint64_t *sec_off_dev = reinterpret_cast<const uint64_t *>(ib + offsetof(ContainerHeader, section_off));
+  KVTC_CUDA_TRY(cudaMemsetAsync(w.err, 0, 4, st));
+  {
+    ProfScope ps("d.inflate", st);
+    uint32_t nch[2];
+    for (int sv = 0; sv < 2; ++sv) nch[sv] = uint32_t((h.payload_bytes[sv] + h.chunk_bytes - 1) / h.chunk_bytes);
+    if ((s = launch_inflate_sections(ib, sec_off_dev, h.payload_bytes[0], nch[0], w.payloads[0], sec_off_dev + 1,
+                                     h.payload_bytes[1], nch[1], w.payloads[1], w.err, st)))
+      return s;
+  }
+  ProfScope ps("d.dequant", st);
+  for (int sv = 0; sv < 2; ++sv) {
+    kvtc_plan *pl = const_cast<kvtc_plan *>(sv ? vp : kp);
+    if ((s = launch_dequant(pl->d_pgroups, pl->d_codes_off_full, pl->G, plan_codes_off_last(pl, h.m % kTileM),
+                            pl->tile_bytes, w.payloads[sv], h.m, w.Dh[sv], w.ld, st)))
+      return s;
+    if (pl->r_nz == 0) KVTC_CUDA_TRY(cudaMemsetAsync(w.Dh[sv], 0, h.m * w.ld * 2, st));
+  }
+  if (kb->has_rope && (s = rope_table_for(kb, h.pos0 + h.sinks, h.m, w.cs, st))) return s;
+  return KVTC_OK;
+}
+
+extern "C" kvtc_status kvtc_decompress_layers(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb,
+                                              const kvtc_plan *vp, const void *in, const void *header_host,
+                                              int32_t layer_begin, int32_t layer_end, const kvtc_kv_view *k_out,
+                                              const kvtc_kv_view *v_out, void *workspace, size_t workspace_bytes,
+                                              void *stream) {
+  KVTC_CHECK_ARG(kb && kp && vb && vp && in && header_host && k_out && v_out, "decompress_layers arguments");
+  kvtc_status s;
+  if ((s = check_view(k_out)) || (s = check_view(v_out))) return s;
+  ContainerHeader h;
+  if ((s = read_checked_header(kb, kp, vb, vp, header_host, 0, &h))) return s;
+  const kvtc_shape shp{h.layers, h.kv_heads, h.head_dim};
+  if (!same_shape(shp, k_out->shape) || !same_shape(shp, v_out->shape) || k_out->tokens != h.tokens ||
+      v_out->tokens != h.tokens) {
+    set_error("container shape does not match the output views");
+    return KVTC_E_MISMATCH;
+  }
+  KVTC_CHECK_ARG(0 <= layer_begin && layer_begin <= layer_end && layer_end <= h.layers, "layer range");
+  const size_t need = kvtc_decompress_workspace_bytes(kb, kp, vb, vp, &h);
+  if (!workspace || workspace_bytes < need) {
+    set_error("workspace %zu < %zu", workspace_bytes, need);
+    return KVTC_E_CAPACITY;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  DecompWs w = carve_decomp(kp, vp, h, workspace, workspace_bytes);
+  if ((s = upload_bases(k_out, w.kbases, st)) || (s = upload_bases(v_out, w.vbases, st))) return s;
+  const uint8_t *ib = static_cast<const uint8_t *>(in);
+  const int64_t t = h.tokens;
+  const int64_t nraw = h.m ? int64_t(h.sinks) + h.window : t;
+  const int64_t hd = int64_t(h.kv_heads) * h.head_dim;
+  const auto *rawk = reinterpret_cast<const __nv_bfloat16 *>(ib + h.raw_off);
+  const auto *rawv = rawk + int64_t(h.layers) * nraw * hd;
+  for (int sv = 0; sv < 2; ++sv) {
+    const kvtc_basis *b = sv ? vb : kb;
+    kvtc_plan *pl = const_cast<kvtc_plan *>(sv ? vp : kp);
+    const kvtc_kv_view *vw = sv ? v_out : k_out;
+    __nv_bfloat16 *const *bs = sv ? w.vbases : w.kbases;
+    const __nv_bfloat16 *raw = sv ? rawv : rawk;
+    if (!h.m) {
+      if ((s = launch_unpack_raw(raw, nraw, 0, t, *vw, bs, 0, layer_begin, layer_end, st))) return s;
+      continue;
+    }
+    const Operands *op;
+    if ((s = plan_operands(b, pl, &op))) return s;
+    {
+      ProfScope ps("d.reconstruct_gemm", st);
+      if ((s = run_reconstruct(b, pl, op, w.Dh[sv], w.ld, h.m, h.sinks, layer_begin, layer_end, vw, bs, w.cs, st)))
+        return s;
+    }
+    if ((s = launch_unpack_raw(raw, nraw, 0, h.sinks, *vw, bs, 0, layer_begin, layer_end, st))) return s;
+    if ((s = launch_unpack_raw(raw, nraw, h.sinks, h.window, *vw, bs, t - h.window, layer_begin, layer_end, st)))
+      return s;
+  }
+  return KVTC_OK;
+}
+
 // ================================================================ batched codec
 // Several conversations (or token ranges of conversations) in one call: their
 // middle tokens are concatenated, each padded to whole 128-token tiles, so both

@@ -284,6 +284,32 @@ def decompress(kb: Basis, kp: Plan, vb: Basis, vp: Plan, container: torch.Tensor
                                 _stream(stream)))
 
 
+# ------------------------------------------------- layer-streamed decompression
+class StreamedDecompress:
+    """kvtc_decompress_begin once, then kvtc_decompress_layers per layer range
+    (P:L210): inflate + dequantise once, each range runs only its V^T columns."""
+
+    def __init__(self, kb: Basis, kp: Plan, vb: Basis, vp: Plan, container: torch.Tensor, stream=None):
+        self.args = (kb, kp, vb, vp)
+        self.container = container
+        self.header = container[: L.HEADER_BYTES].cpu().numpy().tobytes()
+        self.workspace = torch.empty(decompress_workspace_bytes(kb, kp, vb, vp, self.header), dtype=torch.uint8,
+                                     device="cuda")
+        self.begin(stream)
+
+    def begin(self, stream=None):
+        """(Re-)runs kvtc_decompress_begin: inflate + dequantise into the workspace."""
+        kb, kp, vb, vp = self.args
+        check(lib().kvtc_decompress_begin(kb.h, kp.h, vb.h, vp.h, _ptr(self.container), self.container.numel(),
+                                          _ptr(self.workspace), self.workspace.numel(), _stream(stream)))
+
+    def layers(self, k_out: KVView, v_out: KVView, layer_begin: int, layer_end: int, stream=None):
+        kb, kp, vb, vp = self.args
+        check(lib().kvtc_decompress_layers(kb.h, kp.h, vb.h, vp.h, _ptr(self.container), C.c_char_p(self.header),
+                                           layer_begin, layer_end, C.byref(k_out.c), C.byref(v_out.c),
+                                           _ptr(self.workspace), self.workspace.numel(), _stream(stream)))
+
+
 # ------------------------------------------------------------ batched codec
 def compress_batch(kb: Basis, kp: Plan, vb: Basis, vp: Plan, ks: list, vs: list, sinks: int = 4, window: int = 128,
                    chunk_bytes: int = 65536, stream=None, outs: list | None = None, workspace=None,

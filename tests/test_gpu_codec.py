@@ -115,6 +115,25 @@ def test_layer_range_decompress(K):
     assert not part_k[0].any() and not part_v[0].any()
 
 
+@pytest.mark.parametrize("name,tokens", [("mid", 700), ("toy", 400)])
+def test_layer_streamed_decompress(K, name, tokens):
+    """kvtc_decompress_begin once + kvtc_decompress_layers per layer
+    == kvtc_decompress, bit for bit; layers not yet requested stay untouched."""
+    spec, invf, kb, vb, KB, VB, KP, VP, okp, ovp = _setup(K, name)
+    Kc, Vc = E.caches(name, tokens, 17, conversation=9)
+    kd, vd = Kc.cuda(), Vc.cuda()
+    cont, _ = K.compress(KB, KP, VB, VP, K.KVView(kd, pos0=17), K.KVView(vd, pos0=17))
+    full_k, full_v = torch.zeros_like(kd), torch.zeros_like(vd)
+    K.decompress(KB, KP, VB, VP, cont, K.KVView(full_k, pos0=17), K.KVView(full_v, pos0=17))
+    sk, sv = torch.zeros_like(kd), torch.zeros_like(vd)
+    sd = K.StreamedDecompress(KB, KP, VB, VP, cont)
+    for l in range(spec.layers):
+        sd.layers(K.KVView(sk, pos0=17), K.KVView(sv, pos0=17), l, l + 1)
+        torch.cuda.synchronize()
+        assert torch.equal(sk[: l + 1], full_k[: l + 1]) and torch.equal(sv[: l + 1], full_v[: l + 1])
+        assert not sk[l + 1:].any() and not sv[l + 1:].any()
+
+
 def test_paged_output(K):
     name, tokens = "mid", 600
     spec, invf, kb, vb, KB, VB, KP, VP, okp, ovp = _setup(K, name)
