@@ -946,8 +946,9 @@ __device__ __forceinline__ void inflate_chunk(FastShared &S, const uint8_t *sect
   const uint32_t *words = reinterpret_cast<const uint32_t *>(stream);
   const uint32_t nw = umin32((e.bytes + 3) / 4, kHdrWords);
   for (uint32_t i = tid; i < kHdrWords + 2; i += kInfThreads) S.hdr[i] = i < nw ? __ldg(words + i) : 0u;
-  for (int i = tid; i < (1 << kTabBits); i += kInfThreads) S.table[i] = 0;
-  for (int i = tid; i < (kSubTabs << kSubBits); i += kInfThreads) S.sub[i] = 0;
+  // 0x4000 marks "no code here" (len 0): a corrupt stream sets it in `bad`
+  for (int i = tid; i < (1 << kTabBits); i += kInfThreads) S.table[i] = 0x4000;
+  for (int i = tid; i < (kSubTabs << kSubBits); i += kInfThreads) S.sub[i] = 0x4000;
   const uint32_t mylen = index[uint64_t(c) * kNSeg + tid];
   __syncthreads();
   if (tid == 0) {
@@ -1000,75 +1001,67 @@ __device__ __forceinline__ void inflate_chunk(FastShared &S, const uint8_t *sect
   if (s0 >= s1) return;
   uint64_t pos = S.hdr_bits + S.segstart[tid] - mylen + (tid >= 32 ? S.segstart[31] : 0);
   // Read-ahead through shared memory: each lane streams its own segment, so
-  // loads cannot be coalesced; 16-byte cp.async copies of the next three blocks
-  // fill a per-lane ring and complete in the background.  (Rotating prefetched
-  // registers instead made every rotation wait for its load: ncu showed ~40 % of
-  // the samples stalled on it.)  The stream is 16-byte aligned and zero-padded.
+  // loads cannot be coalesced; 16-byte cp.async copies fill a per-lane ring of 4
+  // blocks in the background.  (Rotating prefetched registers instead made every
+  // rotation wait for its load: ncu showed ~40 % of the samples stalled on it.)
+  // Decoding is branch-free per code: the 32 bits at the bit position come from
+  // two ring words and a funnel shift, so refills are not if-converted into every
+  // symbol (the earlier 64-bit bit buffer cost ~35 instructions per symbol); the
+  // ring advances once per 8 codes (8 x 15 bits + 32 stay inside 3 blocks).
+  // The stream is 16-byte aligned and zero-padded.
   const uint4 *blk = reinterpret_cast<const uint4 *>(stream);
   const uint32_t nblk = (e.bytes + 15) / 16;
-  auto issue = [&](uint32_t b) {
-    if (b < nblk) {
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&S.ring[b % kRing][tid])),
-                   "l"(blk + b)
-                   : "memory");
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  uint32_t cb = uint32_t(pos >> 7);        // current block
-  for (int k = 0; k < kRing; ++k) issue(cb + k);
-  asm volatile("cp.async.wait_group %0;" ::"n"(kRing - 1) : "memory");
-  uint4 cur = cb < nblk ? S.ring[cb % kRing][tid] : make_uint4(0, 0, 0, 0);
-  int wsel = int(pos >> 5) & 3;
-  auto take = [&]() -> uint32_t {
-    const uint32_t w = wsel == 0 ? cur.x : wsel == 1 ? cur.y : wsel == 2 ? cur.z : cur.w;
-    if (++wsel == 4) {
-      wsel = 0;
-      ++cb;
-      asm volatile("cp.async.wait_group %0;" ::"n"(kRing - 2) : "memory");   // block cb landed
-      cur = cb < nblk ? S.ring[cb % kRing][tid] : make_uint4(0, 0, 0, 0);
-      issue(cb + kRing - 1);                 // into the slot of block cb - 1, consumed
-    }
-    return w;
-  };
-  uint64_t buf = uint64_t(take()) >> (pos & 31);
-  int cnt = 32 - int(pos & 31);
-  bool bad = false;
-  // >= 30 valid bits after a refill: two codes (<= 15 bits each) per check
-  auto refill = [&]() {
-    if (cnt < 30) {
-      buf |= uint64_t(take()) << cnt;
-      cnt += 32;
+  uint32_t issued = uint32_t(pos >> 7);    // next block to copy into the ring
+  auto issue_upto = [&](uint32_t last) {   // copies blocks [issued, last] (slot b % 4)
+    for (; issued <= last; ++issued) {
+      if (issued < nblk)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&S.ring[issued % kRing][tid])),
+                     "l"(blk + issued)
+                     : "memory");
+      asm volatile("cp.async.commit_group;" ::: "memory");
     }
   };
+  const uint32_t *ring32 = reinterpret_cast<const uint32_t *>(&S.ring[0][0]);
+  auto word = [&](uint32_t gw) -> uint32_t {    // stream word gw (its block is resident)
+    return ring32[(((gw >> 2) % kRing) * kNSeg + tid) * 4 + (gw & 3)];
+  };
+  uint32_t bp = uint32_t(pos);
+  uint32_t bad = 0;
   auto decode = [&]() -> uint32_t {
-    uint32_t te = S.table[buf & ((1u << kTabBits) - 1)];
-    if (te & 0x8000) te = S.sub[((te & 0x7FFF) << kSubBits) | ((buf >> kTabBits) & ((1u << kSubBits) - 1))];
-    const uint32_t sym = te >> 4;
-    const int l = te & 15;
-    buf >>= l;
-    cnt -= l;
-    bad |= (sym > 255u) | (l == 0);
-    return sym & 0xFF;
+    const uint32_t w = bp >> 5;
+    const uint32_t bits = __funnelshift_r(word(w), word(w + 1), bp & 31);
+    uint32_t te = S.table[bits & ((1u << kTabBits) - 1)];
+    if (te & 0x8000) te = S.sub[((te & 0x7FFF) << kSubBits) | ((bits >> kTabBits) & ((1u << kSubBits) - 1))];
+    bp += te & 15;
+    bad |= te;                               // 0x4000: no code / 0x1000: end-of-block inside a segment
+    return (te >> 4) & 0xFF;
+  };
+  auto advance = [&]() {                     // blocks of bp .. bp + 8 x 15 + 32 bits resident
+    issue_upto((bp >> 7) + kRing - 1);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
   };
   uint32_t i = s0;
-  // 16 symbols -> one 16-byte store (segments are 16-byte aligned)
+  // 16 codes -> one 16-byte store (segments are 16-byte aligned)
   const bool vec_out = (reinterpret_cast<uintptr_t>(o) & 15) == 0;
   for (; vec_out && i + 16 <= s1; i += 16) {
-    uint32_t w[4] = {0, 0, 0, 0};
+    uint32_t w[4];
 #pragma unroll
-    for (int k = 0; k < 16; k += 2) {
-      refill();
-      w[k >> 2] |= decode() << (8 * (k & 3));
-      w[k >> 2] |= decode() << (8 * ((k + 1) & 3));
+    for (int h = 0; h < 2; ++h) {
+      advance();
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const uint32_t b0 = decode(), b1 = decode(), b2 = decode(), b3 = decode();
+        w[2 * h + q] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
+      }
     }
     *reinterpret_cast<uint4 *>(o + i) = make_uint4(w[0], w[1], w[2], w[3]);
   }
   for (; i < s1; ++i) {
-    refill();
+    if (((i - s0) & 7) == 0) advance();
     o[i] = uint8_t(decode());
   }
+  if (bad & 0x5000) atomicExch(err, -7);
   asm volatile("cp.async.wait_all;" ::: "memory");   // no copy may land in the next chunk's header
-  if (bad) atomicExch(err, -7);
 }
 
 // Grid-stride over the chunks of both jobs (full grid alone; bounded grid
