@@ -40,12 +40,15 @@ namespace kvtc {
 // NSUB = 2 (compress): a tile is two 256-column segments sharing the A k-block;
 // two MMAs per k-slice into both TMEM accumulators (512 columns, no double
 // buffering), 48 KiB per stage, 4 stages: 25 % less L2 traffic per flop.
-template <bool PAIR, int NSUB = 1>
+// KB = 2: two 64-column k-blocks per pipeline stage (64 KiB stages, 3 of them):
+// half the barrier round trips per MMA (pairs, one segment only).
+template <bool PAIR, int NSUB = 1, int KB = 1>
 struct Cfg {
-  static constexpr int kStages = NSUB == 2 ? 4 : (PAIR ? 6 : 4);
-  static constexpr int kABytes = kTileM * kBlockK * 2;                        // 16 KiB
+  static constexpr int kStages = KB == 2 ? 3 : (NSUB == 2 ? 4 : (PAIR ? 6 : 4));
+  static constexpr int kABlock = kTileM * kBlockK * 2;                        // 16 KiB per k-block
+  static constexpr int kABytes = KB * kABlock;
   static constexpr int kBSubBytes = (PAIR ? kMaxTileN / 2 : kMaxTileN) * kBlockK * 2;
-  static constexpr int kBBytes = NSUB * kBSubBytes;
+  static constexpr int kBBytes = KB * NSUB * kBSubBytes;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 2048;
   static constexpr int kAccBufs = NSUB == 2 ? 1 : 2;
@@ -294,12 +297,13 @@ __device__ __forceinline__ int tile_nsub(const Params &P, const Tile &T) {
 // Register budget: the compress GEMM runs beside the side-stream gather / encoder
 // CTAs (2-3 per SM), so it is held to 128 registers (min 2 blocks); the
 // decompress GEMM (beside the dequantiser) may use more.
-template <int MODE, bool PAIR, int NSUB>
+template <int MODE, bool PAIR, int NSUB, int KB>
 __global__ void __launch_bounds__(kThreads, MODE == EPI_RECON ? 1 : 2)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ Params P) {
   static_assert(NSUB == 1 || (MODE == EPI_QUANT && PAIR), "two-segment tiles: compress, CTA pairs");
-  using C = Cfg<PAIR, NSUB>;
+  static_assert(KB == 1 || (PAIR && NSUB == 1), "two k-blocks per stage: CTA pairs, one segment");
+  using C = Cfg<PAIR, NSUB, KB>;
   constexpr int kStages = C::kStages;
   constexpr int kABytes = C::kABytes;
   constexpr int kStageBytes = C::kStageBytes;
@@ -324,6 +328,7 @@ __global__ void __launch_bounds__(kThreads, MODE == EPI_RECON ? 1 : 2)
   const int64_t t_first = PAIR ? blockIdx.x / 2 : blockIdx.x;
   const int64_t t_step = int64_t(PAIR ? gridDim.x / 2 : gridDim.x);
   const int num_kb = (P.K + kBlockK - 1) / kBlockK;
+  const int num_st = (num_kb + KB - 1) / KB;       // pipeline stages per tile
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmA);
@@ -374,12 +379,12 @@ __global__ void __launch_bounds__(kThreads, MODE == EPI_RECON ? 1 : 2)
       tile_geometry<MODE, NSUB>(P, T, n0, ncols, g0, g1);
       const int n_mma = (ncols + 15) & ~15;
       const int nsub = tile_nsub<NSUB>(P, T);
-      for (int kb = 0; kb < num_kb; ++kb, ++it) {
+      for (int ks = 0; ks < num_st; ++ks, ++it) {
         const int s = it % kStages;
         if (it >= kStages) mbar_wait(&empty_bar[s], ((it / kStages) - 1) & 1);
         uint8_t *a = tiles + s * kStageBytes;
         uint8_t *b = a + kABytes;
-        const int32_t ka = kb * kBlockK;
+        const int32_t ka = ks * KB * kBlockK;
         if constexpr (NSUB == 2) {
           // A k-block + one B k-block per segment; both CTAs' bytes on the leader's barrier
           if (leader) mbar_arrive_expect_tx(&full_bar[s], 2 * (kABytes + nsub * kBSub));
@@ -391,6 +396,22 @@ __global__ void __launch_bounds__(kThreads, MODE == EPI_RECON ? 1 : 2)
             const SegDesc sd = P.segs[T.nb * NSUB + sb];
             const int nm = (sd.width + 15) & ~15;
             tma_load_2d_pair(b + sb * kBSub, &tmB, &full_bar[s], ka, sd.col0 + int(rank) * (nm / 2));
+          }
+        } else if constexpr (KB == 2) {
+          // two k-blocks per stage: A blocks then B blocks; both CTAs' bytes on the leader's barrier
+          if (leader) mbar_arrive_expect_tx(&full_bar[s], 2 * kStageBytes);
+#pragma unroll
+          for (int kk = 0; kk < KB; ++kk) {
+            const int32_t kak = ka + kk * kBlockK;
+            uint8_t *ak = a + kk * C::kABlock;
+            if (P.a_hd && P.a_layer_rows)
+              tma_load_2d_pair(ak, &tmA, &full_bar[s], kak % P.a_hd,
+                               int((kak / P.a_hd) * P.a_layer_rows + P.a_row0) + T.mb * kTileM);
+            else if (P.a_hd)
+              tma_load_3d_pair(ak, &tmA, &full_bar[s], kak % P.a_hd, int(P.a_row0) + T.mb * kTileM, kak / P.a_hd);
+            else
+              tma_load_2d_pair(ak, &tmA, &full_bar[s], kak, T.mb * kTileM);
+            tma_load_2d_pair(b + kk * kBSub, &tmB, &full_bar[s], kak, n0 + int(rank) * (n_mma / 2));
           }
         } else if constexpr (PAIR) {
           // both CTAs' bytes land on the leader's barrier
@@ -442,13 +463,24 @@ __global__ void __launch_bounds__(kThreads, MODE == EPI_RECON ? 1 : 2)
         idesc_sub[sb] = NSUB == 1 ? idesc
                                   : make_idesc_f16(P.fmt, 2 * kTileM,
                                                    sb < nsub ? (P.segs[T.nb * NSUB + sb].width + 15) & ~15 : 16);
-      for (int kb = 0; kb < num_kb; ++kb, ++it) {
+      for (int ks = 0; ks < num_st; ++ks, ++it) {
+        const int kb = ks;                         // KB == 1: stage == k-block
         const int s = it % kStages;
         mbar_wait(&full_bar[s], (it / kStages) & 1);
         tc_fence_after();
         const uint64_t ad = make_sdesc_sw128(tiles + s * kStageBytes);
         const uint64_t bd = make_sdesc_sw128(tiles + s * kStageBytes + kABytes);
-        if constexpr (NSUB == 2) {
+        if constexpr (KB == 2) {
+#pragma unroll
+          for (int kk = 0; kk < KB; ++kk) {
+            const uint64_t adk = make_sdesc_sw128(tiles + s * kStageBytes + kk * C::kABlock);
+            const uint64_t bdk = make_sdesc_sw128(tiles + s * kStageBytes + kABytes + kk * kBSub);
+#pragma unroll
+            for (int k = 0; k < kBlockK / 16; ++k)
+              umma_f16_pair(tacc, adk + 2 * k, bdk + 2 * k, idesc, (ks | kk | k) != 0);
+          }
+          umma_commit_pair(&empty_bar[s]);
+        } else if constexpr (NSUB == 2) {
           // segment sb accumulates in TMEM columns [256 sb, 256 sb + 256)
 #pragma unroll
           for (int k = 0; k < kBlockK / 16; ++k)
@@ -792,16 +824,16 @@ static int num_sms() {
   return n;
 }
 
-template <int MODE, bool PAIR, int NSUB = 1>
+template <int MODE, bool PAIR, int NSUB = 1, int KB = 1>
 static kvtc_status launch(const CUtensorMap *tmA, const CUtensorMap *tmB, const Params &p, dim3 grid, int cluster,
                           cudaStream_t st) {
   static bool configured = false;
-  constexpr int kSmemBytes = Cfg<PAIR, NSUB>::kSmemBytes;
+  constexpr int kSmemBytes = Cfg<PAIR, NSUB, KB>::kSmemBytes;
   if (!configured) {
-    KVTC_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<MODE, PAIR, NSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       kSmemBytes));
+    KVTC_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<MODE, PAIR, NSUB, KB>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
     // the 228 KB configuration, shared with the side-stream kernels (internal.h)
-    KVTC_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<MODE, PAIR, NSUB>,
+    KVTC_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<MODE, PAIR, NSUB, KB>,
                                        cudaFuncAttributePreferredSharedMemoryCarveout,
                                        int(cudaSharedmemCarveoutMaxShared)));
     configured = true;
@@ -848,9 +880,15 @@ static kvtc_status launch(const CUtensorMap *tmA, const CUtensorMap *tmB, const 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  KVTC_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_kernel<MODE, PAIR, NSUB>, *tmA, *tmB, pp));
+  KVTC_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_kernel<MODE, PAIR, NSUB, KB>, *tmA, *tmB, pp));
   note_launch();
   return KVTC_OK;
+}
+
+// KVTC_KB2 = bit mask over modes: 128-column (two k-block) pipeline stages
+static bool kb2_for(int mode) {
+  const char *e = getenv("KVTC_KB2");
+  return e && ((atoi(e) >> mode) & 1);
 }
 
 // pairs: 2 CTAs per pair-tile, grid even, at most one CTA per SM
@@ -902,6 +940,9 @@ kvtc_status launch_gemm_project_quant(const GemmCompressArgs &a, cudaStream_t st
     return launch<EPI_QUANT, true, 2>(a.tmA, a.tmB, p, dim3(pair_grid(int64_t((p.num_m + 1) / 2) * p.num_n)), 2, st);
   }
   p.num_n = a.nsegs;
+  if (kb2_for(EPI_QUANT))
+    return launch<EPI_QUANT, true, 1, 2>(a.tmA, a.tmB, p, dim3(pair_grid(int64_t((p.num_m + 1) / 2) * p.num_n)), 2,
+                                         st);
   return launch<EPI_QUANT, true>(a.tmA, a.tmB, p, dim3(pair_grid(int64_t((p.num_m + 1) / 2) * p.num_n)), 2, st);
 }
 
@@ -927,6 +968,9 @@ kvtc_status launch_gemm_reconstruct(const GemmDecompressArgs &a, cudaStream_t st
   p.tile_n = a.tile_n;
   p.num_m = int32_t(ceil_div(a.m, kTileM));
   p.num_n = int32_t(ceil_div(a.n_end - a.n_begin, a.tile_n));
+  if (kb2_for(EPI_RECON))
+    return launch<EPI_RECON, true, 1, 2>(a.tmA, a.tmB, p, dim3(pair_grid(int64_t((p.num_m + 1) / 2) * p.num_n)), 2,
+                                         st);
   return launch<EPI_RECON, true>(a.tmA, a.tmB, p, dim3(pair_grid(int64_t((p.num_m + 1) / 2) * p.num_n)), 2, st);
 }
 
