@@ -181,6 +181,12 @@ SideStream *side_stream() {
   return &S;
 }
 
+// Per-SM CTAs of a side-stream kernel beside a GEMM (tuning: KVTC_CORUN_<KIND>).
+int corun_per_sm(const char *name, int dflt) {
+  const char *e = getenv(name);
+  return e ? std::max(1, atoi(e)) : dflt;
+}
+
 bool env_flag(const char *name, bool dflt) {
   const char *e = getenv(name);
   return e ? e[0] == '1' : dflt;
@@ -522,7 +528,7 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
   SideStream *ss = side_stream();
   const bool ovl = !overlap_off();
   cudaStream_t aux = ovl ? ss->s : st;
-  const int side_ctas = ovl ? corun_ctas(2) : 0;
+  const int side_ctas = ovl ? corun_ctas(corun_per_sm("KVTC_CORUN_DEFLATE", 2)) : 0;
   CUtensorMap tV;
   int64_t v_layer_rows = 0;
   const bool v_direct = !direct_off() && direct_view_map(*v, pol->sinks, &tV, &v_layer_rows);
@@ -562,7 +568,8 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
     KVTC_CUDA_TRY(cudaEventRecord(ss->ev[2], st));               // V payload ready
     if (gather_side) {
       KVTC_CUDA_TRY(cudaStreamWaitEvent(aux, ss->ev[0], 0));
-      if ((s = gather_keys(aux, corun_ctas(3), "c.gather_unrope_overlapped"))) return s;
+      if ((s = gather_keys(aux, corun_ctas(corun_per_sm("KVTC_CORUN_GATHER", 3)), "c.gather_unrope_overlapped")))
+        return s;
       KVTC_CUDA_TRY(cudaEventRecord(ss->ev[1], aux));            // X (keys) ready
       KVTC_CUDA_TRY(cudaStreamWaitEvent(st, ss->ev[1], 0));
     }
@@ -779,7 +786,7 @@ extern "C" kvtc_status kvtc_decompress(const kvtc_basis *kb, const kvtc_plan *kp
     }
     if (sv == 0) {
       KVTC_CUDA_TRY(cudaStreamWaitEvent(aux, ss->ev[2], 0));
-      if ((s = expand(1, aux, ovl ? corun_ctas(2) : 0))) return s;
+      if ((s = expand(1, aux, ovl ? corun_ctas(corun_per_sm("KVTC_CORUN_DEQUANT", 2)) : 0))) return s;
       KVTC_CUDA_TRY(cudaEventRecord(ss->ev[3], aux));
     }
     const __nv_bfloat16 *raw = sv ? rawv : rawk;
