@@ -630,7 +630,7 @@ def main():
                 "config": {"workload": f"{args.config}: {spec.layers} layers x {spec.kv_heads} KV heads x "
                                        f"{spec.head_dim}, {t}-token conversation per GPU, CR target {args.cr:g}",
                            "tokens_per_gpu": t, "middle_tokens": m, "p": p, "parallelism": f"weak x{world}",
-                           "l2": "inputs 4.3 GB per step >> 126 MB L2 (no flush needed)",
+                           "l2": f"inputs {2 * 2 * p * t / 1e9:.1f} GB per step >> 126 MB L2 (no flush needed)",
                            "cr": cr, "cr_pre_deflate": cr_pre, "r_eff": [kinfo.r_eff, vinfo.r_eff], "r_nz": rnz,
                            "setup_s": round(setup_s, 1), "setup": setup_info},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
