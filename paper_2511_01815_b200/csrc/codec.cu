@@ -90,7 +90,7 @@ bool direct_view_map(const kvtc_kv_view &v, int64_t tok0, CUtensorMap *m, int64_
 kvtc_status run_project_quant(const kvtc_basis *b, kvtc_plan *pl, const Operands *op, const void *X, int64_t m,
                               uint8_t *payload, float *wide, cudaStream_t st, const CUtensorMap *direct = nullptr,
                               int64_t tok0 = 0, int64_t ldx = 0, const TileRef *tiles = nullptr,
-                              int64_t layer_rows = 0) {
+                              int64_t layer_rows = 0, bool defer_wide = false) {
   if (m == 0 || pl->G == 0) return KVTC_OK;
   KVTC_CHECK_ARG(pl->nwide == 0 || wide, "wide-group scratch");
   CUtensorMap tA;
@@ -118,8 +118,16 @@ kvtc_status run_project_quant(const kvtc_basis *b, kvtc_plan *pl, const Operands
   a.ldd = pl->wide_cols;
   a.tiles = tiles;
   if ((s = launch_gemm_project_quant(a, st))) return s;
+  // groups wider than a tile: quantised from the fp32 scratch (defer_wide: the
+  // caller launches run_quant_wide itself, e.g. on the side stream)
+  if (defer_wide) return KVTC_OK;
   return launch_quant_wide(pl->d_wide, pl->nwide, wide, pl->wide_cols, 1, m, pl->tile_bytes, a.codes_off_last,
                            payload, st, tiles);
+}
+
+kvtc_status run_quant_wide(kvtc_plan *pl, float *wide, int64_t m, uint8_t *payload, cudaStream_t st) {
+  return launch_quant_wide(pl->d_wide, pl->nwide, wide, pl->wide_cols, 1, m, pl->tile_bytes,
+                           plan_codes_off_last(pl, m % kTileM), payload, st);
 }
 
 kvtc_status run_reconstruct(const kvtc_basis *b, const kvtc_plan *pl, const Operands *op, const __half *Dh,
@@ -419,6 +427,7 @@ extern "C" size_t kvtc_compress_workspace_bytes(const kvtc_basis *kb, const kvtc
   b.take<uint8_t>(deflate_workspace(L.pay[0], pol->chunk_bytes));
   b.take<uint8_t>(deflate_workspace(L.pay[1], pol->chunk_bytes));
   b.take<float>(L.m * std::max(kp->wide_cols, vp->wide_cols));
+  b.take<float>(L.m * vp->wide_cols);                      // the values' own (quantised on the side stream)
   return b.used + 256;
 }
 
@@ -465,6 +474,7 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
   dwsp[0] = ws.take<uint8_t>(dws[0]);
   dwsp[1] = ws.take<uint8_t>(dws[1]);
   float *wide = ws.take<float>(L.m * std::max(kp->wide_cols, vp->wide_cols));
+  float *wide_v = ws.take<float>(L.m * vp->wide_cols);
   if ((s = upload_bases(k, kbases, st)) || (s = upload_bases(v, vbases, st))) return s;
 
   uint8_t *o = static_cast<uint8_t *>(out);
@@ -540,14 +550,18 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
   };
   // rows [r0, r1) of a stream (r0 a multiple of the 128-token tile): payload tiles
   // and wide-group scratch rows are addressed from r0
+  bool defer_v_wide = false;
   auto gemm = [&](int sv, bool direct, int64_t r0 = 0, int64_t r1 = -1) -> kvtc_status {
     ProfScope ps("c.project_quant_gemm", st);
     if (r1 < 0) r1 = L.m;
     const kvtc_plan *pl = sv ? vpl : kpl;
     uint8_t *pay = (sv ? payload_v : payload_k) + (r0 / kTileM) * pl->tile_bytes;
     float *wd = wide ? wide + r0 * pl->wide_cols : nullptr;      // scratch rows of stride wide_cols
+    // the values' wide groups go to their own scratch and are quantised on the side
+    // stream (before their DEFLATE) when the schedule overlaps it
+    if (sv && defer_v_wide) wd = wide_v;
     return sv ? run_project_quant(vb, vpl, vop, X, r1 - r0, pay, wd, st, direct ? &tV : nullptr, pol->sinks + r0,
-                                  ldx, nullptr, v_layer_rows)
+                                  ldx, nullptr, v_layer_rows, defer_v_wide)
               : run_project_quant(kb, kpl, kop, X + r0 * ldx, r1 - r0, pay, wd, st, nullptr, 0, ldx);
   };
   auto encode = [&](int sv, cudaStream_t q, int ctas, const char *tag, uint32_t c0 = 0,
@@ -563,6 +577,7 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
     // runs both encoders after the GEMMs instead of the values' beside the keys' GEMM
     const bool gather_side = ovl && env_flag("KVTC_C_GATHER_SIDE", true);
     const bool deflate_side = ovl && env_flag("KVTC_C_DEFLATE_SIDE", true);
+    defer_v_wide = deflate_side && vpl->nwide > 0;
     if (!gather_side && (s = gather_keys(st, 0, "c.gather_unrope"))) return s;
     if ((s = gemm(1, true))) return s;
     KVTC_CUDA_TRY(cudaEventRecord(ss->ev[2], st));               // V payload ready
@@ -590,6 +605,10 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
       return s;
     }
     if (deflate_side) {
+      if (defer_v_wide) {
+        ProfScope ps("c.quant_wide_overlapped", aux);
+        if ((s = run_quant_wide(vpl, wide_v, L.m, payload_v, aux))) return s;
+      }
       if ((s = encode(1, aux, side_ctas, "c.deflate_overlapped"))) return s;
       if (split) {
         KVTC_CUDA_TRY(cudaStreamWaitEvent(aux, ss->ev[1], 0));

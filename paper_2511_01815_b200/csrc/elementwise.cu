@@ -332,6 +332,7 @@ kvtc_status launch_quant_wide(const WideDesc *wide, int32_t nwide, const float *
                               cudaStream_t st, const TileRef *tiles) {
   if (nwide == 0 || m == 0) return KVTC_OK;
   dim3 grid(unsigned(nwide), unsigned(ceil_div(m, kTileM)));
+  KVTC_MAX_CARVEOUT(quant_wide_kernel);             // may run beside a GEMM (values' wide groups)
   quant_wide_kernel<<<grid, 128, 0, st>>>(wide, D, ldd, use_wcol, m, tile_bytes, codes_off_last, payload, tiles);
   KVTC_LAUNCH_CHECK();
   return KVTC_OK;
