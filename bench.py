@@ -388,9 +388,19 @@ def main():
 
     stream = torch.cuda.current_stream()
 
-    def step():
+    dir_events = []                                            # (start, mid, end) per timed step
+
+    def step(mark=False):
+        if mark:
+            e = tuple(torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e[0].record(stream)
         K.compress(kb, kp, vb, vp, kview, vview, out=cont, workspace=cws, sync_len=False)
+        if mark:
+            e[1].record(stream)
         K.decompress(kb, kp, vb, vp, cont, koview, voview, workspace=dws)
+        if mark:
+            e[2].record(stream)
+            dir_events.append(e)
 
     for _ in range(args.warmup):
         step()
@@ -406,9 +416,11 @@ def main():
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for _ in range(args.steps):
-        step()
+        step(mark=True)
     ev1.record(stream)
     torch.cuda.synchronize()
+    c_ms = statistics.median([a.elapsed_time(b) for a, b, _ in dir_events])
+    d_ms = statistics.median([b.elapsed_time(c) for _, b, c in dir_events])
     if dist:
         dist.barrier()
     ms_total = ev0.elapsed_time(ev1)
@@ -635,6 +647,9 @@ def main():
                            "setup_s": round(setup_s, 1), "setup": setup_info},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "layer_streaming": streaming,
+                "directions": {"compress_ms": c_ms, "decompress_ms": d_ms,
+                               "compress_gbs": bytes16 / (c_ms * 1e-3) / 1e9,
+                               "decompress_gbs": bytes16 / (d_ms * 1e-3) / 1e9},
                 "clocks": clk, "stages": stages}
         print(json.dumps(line), flush=True)
     if dist:
