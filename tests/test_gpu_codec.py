@@ -134,6 +134,47 @@ def test_layer_streamed_decompress(K, name, tokens):
         assert not sk[l + 1:].any() and not sv[l + 1:].any()
 
 
+def test_empty_plan_reconstructs_the_mean(K):
+    """A plan with no groups (every PC None): nothing is coded, the
+    middle tokens decompress to the mean mu (re-rotated for keys, R7), exactly as
+    the oracle's decompression of the same container; sinks / window raw."""
+    name, tokens, pos0 = "mid", 500, 9
+    spec, invf, kb, vb, KB, VB, KP, VP, okp, ovp = _setup(K, name)
+    EP = K.Plan.create(kb.r, [])
+    EPV = K.Plan.create(vb.r, [])
+    Kc, Vc = E.caches(name, tokens, pos0, conversation=11)
+    kd, vd = Kc.cuda(), Vc.cuda()
+    cont, st = K.compress(KB, EP, VB, EPV, K.KVView(kd, pos0=pos0), K.KVView(vd, pos0=pos0))
+    ko, vo = torch.zeros_like(kd), torch.zeros_like(vd)
+    K.decompress(KB, EP, VB, EPV, cont, K.KVView(ko, pos0=pos0), K.KVView(vo, pos0=pos0))
+    torch.cuda.synchronize()
+    eok, eov = ODP.Plan(r=kb.r, blocks=[]), ODP.Plan(r=vb.r, blocks=[])
+    oc = OC.compress(Kc.double().numpy(), Vc.double().numpy(), pos0, kb, eok, vb, eov, invf)
+    K2, V2 = OC.decompress(oc, kb, eok, vb, eov, invf)
+    for got, ref, orig in ((ko, K2, Kc), (vo, V2, Vc)):
+        g = got.float().cpu().numpy().astype(np.float64)
+        np.testing.assert_array_equal(g[:, :4], orig.double().numpy()[:, :4])
+        np.testing.assert_array_equal(g[:, tokens - 128:], orig.double().numpy()[:, tokens - 128:])
+        mid = slice(4, tokens - 128)
+        rel = np.linalg.norm(g[:, mid] - ref[:, mid]) / np.linalg.norm(ref[:, mid])
+        assert rel < 1e-3, rel
+
+
+@pytest.mark.parametrize("tokens", [1, 100, 132])
+def test_passthrough_short_conversation(K, tokens):
+    """t <= s + w (Q17): KVTC_NOTHING_TO_COMPRESS, the container holds the raw
+    tokens, and decompression restores them bit for bit."""
+    spec, invf, kb, vb, KB, VB, KP, VP, okp, ovp = _setup(K, "mid")
+    Kc, Vc = E.caches("mid", tokens, 0, conversation=12)
+    kd, vd = Kc.cuda(), Vc.cuda()
+    cont, st = K.compress(KB, KP, VB, VP, K.KVView(kd), K.KVView(vd))
+    assert st == 1                                      # KVTC_NOTHING_TO_COMPRESS
+    ko, vo = torch.zeros_like(kd), torch.zeros_like(vd)
+    K.decompress(KB, KP, VB, VP, cont, K.KVView(ko), K.KVView(vo))
+    torch.cuda.synchronize()
+    assert torch.equal(ko, kd) and torch.equal(vo, vd)
+
+
 def test_paged_output(K):
     name, tokens = "mid", 600
     spec, invf, kb, vb, KB, VB, KP, VP, okp, ovp = _setup(K, name)
