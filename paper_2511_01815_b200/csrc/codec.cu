@@ -771,18 +771,30 @@ extern "C" kvtc_status kvtc_decompress(const kvtc_basis *kb, const kvtc_plan *kp
   const bool ovl = !overlap_off();
   cudaStream_t aux = ovl ? ss->s : st;
   __half *Dhs[2] = {Dh, Dh_v};
+  // KVTC_D_INFLATE_SIDE=1: inflate only the keys here and the values' section on
+  // the side stream beside the keys' GEMM (bounded grid)
+  const bool inflate_side = ovl && env_flag("KVTC_D_INFLATE_SIDE", false);
+  uint32_t nch[2];
+  for (int sv = 0; sv < 2; ++sv) nch[sv] = uint32_t((h.payload_bytes[sv] + h.chunk_bytes - 1) / h.chunk_bytes);
   {
     ProfScope ps("d.inflate", st);
-    uint32_t nch[2];
-    for (int sv = 0; sv < 2; ++sv) nch[sv] = uint32_t((h.payload_bytes[sv] + h.chunk_bytes - 1) / h.chunk_bytes);
-    if ((s = launch_inflate_sections(ib, sec_off_dev, h.payload_bytes[0], nch[0], payloads[0], sec_off_dev + 1,
-                                     h.payload_bytes[1], nch[1], payloads[1], err, st)))
+    if (inflate_side) {
+      if ((s = launch_inflate_section(ib, sec_off_dev, h.payload_bytes[0], nch[0], payloads[0], err, st))) return s;
+    } else if ((s = launch_inflate_sections(ib, sec_off_dev, h.payload_bytes[0], nch[0], payloads[0], sec_off_dev + 1,
+                                            h.payload_bytes[1], nch[1], payloads[1], err, st))) {
       return s;
+    }
   }
   auto expand = [&](int sv, cudaStream_t q, int ctas) -> kvtc_status {
     kvtc_plan *pl = const_cast<kvtc_plan *>(sv ? vp : kp);
-    ProfScope ps(sv && ovl ? "d.dequant_overlapped" : "d.dequant", q);
     kvtc_status r;
+    if (sv && inflate_side) {
+      ProfScope ps("d.inflate_overlapped", q);
+      if ((r = launch_inflate_section(ib, sec_off_dev + 1, h.payload_bytes[1], nch[1], payloads[1], err, q,
+                                      corun_ctas(corun_per_sm("KVTC_CORUN_INFLATE", 2)))))
+        return r;
+    }
+    ProfScope ps(sv && ovl ? "d.dequant_overlapped" : "d.dequant", q);
     if ((r = launch_dequant(pl->d_pgroups, pl->d_codes_off_full, pl->G, plan_codes_off_last(pl, h.m % kTileM),
                             pl->tile_bytes, payloads[sv], h.m, Dhs[sv], ld, q, ctas)))
       return r;
