@@ -421,6 +421,8 @@ def main():
     torch.cuda.synchronize()
     c_ms = statistics.median([a.elapsed_time(b) for a, b, _ in dir_events])
     d_ms = statistics.median([b.elapsed_time(c) for _, b, c in dir_events])
+    per_step = sorted(a.elapsed_time(c) for a, _, c in dir_events)
+    pct = lambda q: per_step[min(len(per_step) - 1, int(round(q * (len(per_step) - 1))))]
     if dist:
         dist.barrier()
     ms_total = ev0.elapsed_time(ev1)
@@ -647,6 +649,7 @@ def main():
                            "setup_s": round(setup_s, 1), "setup": setup_info},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "layer_streaming": streaming,
+                "step_ms_percentiles": {"p10": pct(0.1), "p50": pct(0.5), "p90": pct(0.9)},
                 "directions": {"compress_ms": c_ms, "decompress_ms": d_ms,
                                "compress_gbs": bytes16 / (c_ms * 1e-3) / 1e9,
                                "decompress_gbs": bytes16 / (d_ms * 1e-3) / 1e9},
