@@ -352,8 +352,9 @@ def main():
     cws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
     cont_valid, st = K.compress(kb, kp, vb, vp, kview, vview, out=cont, workspace=cws)
     info = K.container_info(cont_valid)
-    dws = torch.empty(K.decompress_workspace_bytes(kb, kp, vb, vp, cont[:256].cpu().numpy().tobytes()),
-                      dtype=torch.uint8, device="cuda")
+    hdr = cont[:256].cpu().numpy().tobytes()                  # the container header, read once (host copy)
+    dws = torch.empty(K.decompress_workspace_bytes(kb, kp, vb, vp, hdr), dtype=torch.uint8, device="cuda")
+    dstatus = torch.zeros(1, dtype=torch.int32, device="cuda")  # integrity verdict of every timed decompress
     bytes16 = 2 * 2 * p * m                                    # K+V middle tokens, 16-bit
     cr = bytes16 / (info.entropy_bytes[0] + info.entropy_bytes[1])
     cr_pre = bytes16 / (info.payload_bytes[0] + info.payload_bytes[1])
@@ -397,7 +398,7 @@ def main():
         K.compress(kb, kp, vb, vp, kview, vview, out=cont, workspace=cws, sync_len=False)
         if mark:
             e[1].record(stream)
-        K.decompress(kb, kp, vb, vp, cont, koview, voview, workspace=dws)
+        K.decompress_async(kb, kp, vb, vp, cont, hdr, koview, voview, dstatus, workspace=dws)
         if mark:
             e[2].record(stream)
             dir_events.append(e)
@@ -426,6 +427,7 @@ def main():
     if dist:
         dist.barrier()
     ms_total = ev0.elapsed_time(ev1)
+    assert int(dstatus.item()) == 0, "a timed decompression reported KVTC_E_CORRUPT"
     launches = K.launch_count()
     prof = K.profile_read()
     K.profile_enable(False)
@@ -540,7 +542,8 @@ def main():
                     stream.wait_event(ev_out[sl])
                 K.compress(kb, kp, vb, vp, in_views[sl][0], in_views[sl][1], out=cont, workspace=cws,
                            sync_len=False)
-                K.decompress(kb, kp, vb, vp, cont, out_views[sl][0], out_views[sl][1], workspace=dws)
+                K.decompress_async(kb, kp, vb, vp, cont, hdr, out_views[sl][0], out_views[sl][1], dstatus,
+                                   workspace=dws)
                 ev_used[sl].record(stream)
                 with torch.cuda.stream(d2h):
                     d2h.wait_event(ev_used[sl])
@@ -605,7 +608,8 @@ def main():
                 if i >= 1:
                     sp = (i - 1) % 2
                     stream.wait_event(ev_h[sp])
-                    K.decompress(kb, kp, vb, vp, cland[sp], out_views[sp][0], out_views[sp][1], workspace=dws)
+                    K.decompress_async(kb, kp, vb, vp, cland[sp], hdr, out_views[sp][0], out_views[sp][1], dstatus,
+                                       workspace=dws)
                     ev_d[sp].record(stream)
 
         offload_run(2)

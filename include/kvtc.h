@@ -32,14 +32,14 @@
 extern "C" {
 #endif
 
-#define KVTC_ABI_VERSION 1
+#define KVTC_ABI_VERSION 2
 
 typedef enum {
   KVTC_OK = 0,
   KVTC_NOTHING_TO_COMPRESS = 1, /* t <= s + w: container holds raw tokens only (Q17)   */
   KVTC_E_INVALID = -1,          /* bad argument / shape                                */
   KVTC_E_NUMERIC = -2,          /* a 16-bit shift/scale overflowed (Q4)                */
-  KVTC_E_CORRUPT = -3,          /* malformed container or DEFLATE stream               */
+  KVTC_E_CORRUPT = -3,          /* malformed container / DEFLATE stream / checksum     */
   KVTC_E_MISMATCH = -4,         /* basis / plan / shape fingerprint mismatch           */
   KVTC_E_CAPACITY = -5,         /* output or workspace buffer too small                */
   KVTC_E_CUDA = -6,             /* CUDA runtime / driver error                         */
@@ -186,7 +186,11 @@ kvtc_status kvtc_allocate_bits_from_coeffs_multi(const float *P, int64_t n, int3
 kvtc_status kvtc_dp_best_table(const float *P, int64_t n, int32_t r, int64_t budget,
                                const kvtc_dp_config *cfg, double *best_even, void *stream);
 /* Explicit plan: ngroups non-None groups (start_host, size_host, type_host),
- * contiguous-free, non-overlapping, increasing start, within [0, r). */
+ * non-overlapping, increasing start, within [0, r).  Group sizes the kernels
+ * support (KVTC_E_INVALID otherwise): 1..256 with size*bits a multiple of 8 or
+ * below 32 (sub-byte tokens are packed within one 32-bit word), and multiples
+ * of 256 above that.  The paper's sizes {1, 16, 64, 256, 1024} all
+ * qualify; the same rule applies to kvtc_dp_config.sizes_host. */
 kvtc_status kvtc_plan_create(int32_t r, int32_t ngroups, const int32_t *start_host, const int32_t *size_host,
                              const int32_t *type_host, kvtc_plan **out);
 kvtc_status kvtc_plan_destroy(kvtc_plan *p);
@@ -201,7 +205,10 @@ kvtc_status kvtc_plan_get(const kvtc_plan *p, int32_t *r, int32_t *ngroups, int3
  * t - s - w middle tokens of each stream go through un-RoPE (keys, R1) ->
  * D = X V_c - mu V_c (tcgen05 GEMM) -> per-(token, group) shift/scale/codes ->
  * bit-pack (§4 layout) -> chunked DEFLATE; everything in one container
- * written to out (device).  Output layout: DESIGN.md §4.
+ * written to out (device, 16-byte aligned).  Output layout: DESIGN.md §4.
+ * A non-finite 16-bit shift or scale (Q4) flags the container: compress returns
+ * KVTC_E_NUMERIC when it synchronises (out_len_host != NULL), and decompressing
+ * a flagged container returns KVTC_E_NUMERIC.
  * kvtc_compress_bound: capacity that always suffices (stored-block worst case).
  * kvtc_compress_workspace_bytes: device scratch needed for the call.
  * *out_len_host (nullable) receives the container length (synchronises). */
@@ -218,13 +225,38 @@ kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_
  * into k_out / v_out (contiguous or paged views of the same shape and tokens).
  * Only layers [layer_begin, layer_end) are reconstructed ("layer-by-layer using
  * sub-matrices of V^T"); sinks/window of those layers are restored
- * byte-identical.  in: device container of in_len bytes. */
+ * byte-identical.  in: device container of in_len bytes, 16-byte aligned.
+ *
+ * Integrity ("This step is lossless"): the result is either exactly what
+ * kvtc_compress encoded, or an error.  The header is validated on the host (its
+ * checksum, every size and offset re-derived from the shape; reads never leave
+ * [in, in + in_len)); the inflater checks every stream against the section's
+ * side index; the inflated payloads and the raw sink/window section are checked
+ * against the container's 64-bit checksums.  Any failure ->
+ * KVTC_E_CORRUPT (the views may then hold partial output).  A container whose
+ * compression flagged a 16-bit factor overflow -> KVTC_E_NUMERIC.
+ *
+ * kvtc_decompress reads the header (one device-to-host copy + synchronisation)
+ * and synchronises again at the end to report the verdict.
+ * kvtc_decompress_async never synchronises: header_host is the container's first
+ * KVTC_HEADER_BYTES bytes (as returned by compress, or copied once), and the
+ * verdict is written asynchronously to *status_dev (device int32: 0 = intact,
+ * KVTC_E_CORRUPT otherwise) on `stream`; header / argument errors are returned
+ * immediately. */
+/* Workspace of a decompression of the container whose header is given (host
+ * copy of its first KVTC_HEADER_BYTES bytes); 0 for a header that does not
+ * validate (the decompress call then reports why). */
 size_t kvtc_decompress_workspace_bytes(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb,
                                        const kvtc_plan *vp, const void *in_header_host);
 kvtc_status kvtc_decompress(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb, const kvtc_plan *vp,
                             const void *in, size_t in_len, int32_t layer_begin, int32_t layer_end,
                             const kvtc_kv_view *k_out, const kvtc_kv_view *v_out, void *workspace,
                             size_t workspace_bytes, void *stream);
+kvtc_status kvtc_decompress_async(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb,
+                                  const kvtc_plan *vp, const void *in, size_t in_len, const void *header_host,
+                                  int32_t layer_begin, int32_t layer_end, const kvtc_kv_view *k_out,
+                                  const kvtc_kv_view *v_out, int32_t *status_dev, void *workspace,
+                                  size_t workspace_bytes, void *stream);
 /* ------------------------------------------- layer-streamed decompression
  * the inverse projection "can be performed layer-by-layer using
  * sub-matrices of V^T, allowing generation to begin early".  The PCA
@@ -275,7 +307,10 @@ kvtc_status kvtc_decompress_batch(const kvtc_basis *kb, const kvtc_plan *kp, con
                                   int32_t n, const kvtc_kv_view *k_out, const kvtc_kv_view *v_out, void *workspace,
                                   size_t workspace_bytes, void *stream);
 
-/* Parse a container header (first KVTC_HEADER_BYTES bytes, copied to host). */
+/* Parse a container header (first KVTC_HEADER_BYTES bytes, copied to host).
+ * info is filled in any case; the status is the header validation (KVTC_OK,
+ * KVTC_E_CORRUPT for a damaged / inconsistent header, KVTC_E_NUMERIC for a
+ * container flagged at compression). */
 #define KVTC_HEADER_BYTES 256
 typedef struct {
   uint32_t magic, version;
@@ -286,6 +321,10 @@ typedef struct {
   uint64_t payload_bytes[2];      /* pre-DEFLATE payload per stream                    */
   uint64_t entropy_bytes[2];      /* DEFLATE streams + chunk tables + indices          */
   uint64_t basis_fp[2], plan_fp[2];
+  uint32_t flags;                 /* bit 0: a 16-bit shift/scale overflowed (Q4)        */
+  uint32_t reserved;
+  uint64_t payload_hash[2];       /* 64-bit checksums                    */
+  uint64_t raw_hash;
 } kvtc_container_info;
 kvtc_status kvtc_container_parse(const void *header_host, kvtc_container_info *info);
 

@@ -55,7 +55,8 @@ class ContainerInfo(C.Structure):
                 ("head_dim", C.c_int32), ("sinks", C.c_int32), ("window", C.c_int32), ("chunk_bytes", C.c_int32),
                 ("tokens", C.c_int64), ("pos0", C.c_int64), ("m", C.c_int64), ("total_bytes", C.c_uint64),
                 ("raw_bytes", C.c_uint64), ("payload_bytes", C.c_uint64 * 2), ("entropy_bytes", C.c_uint64 * 2),
-                ("basis_fp", C.c_uint64 * 2), ("plan_fp", C.c_uint64 * 2)]
+                ("basis_fp", C.c_uint64 * 2), ("plan_fp", C.c_uint64 * 2), ("flags", C.c_uint32),
+                ("reserved", C.c_uint32), ("payload_hash", C.c_uint64 * 2), ("raw_hash", C.c_uint64)]
 
 
 vp, i32, i64, u64, sz, f64 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_size_t, C.c_double
@@ -84,6 +85,8 @@ _SIGS = {
     "kvtc_compress": (i32, [vp, vp, vp, vp, P(View), P(View), P(Policy), vp, sz, P(sz), vp, sz, vp]),
     "kvtc_decompress_workspace_bytes": (sz, [vp, vp, vp, vp, vp]),
     "kvtc_decompress": (i32, [vp, vp, vp, vp, vp, sz, i32, i32, P(View), P(View), vp, sz, vp]),
+    "kvtc_decompress_async": (i32, [vp, vp, vp, vp, vp, sz, C.c_char_p, i32, i32, P(View), P(View), vp, vp, sz,
+                                    vp]),
     "kvtc_decompress_begin": (i32, [vp, vp, vp, vp, vp, sz, vp, sz, vp]),
     "kvtc_decompress_layers": (i32, [vp, vp, vp, vp, vp, C.c_char_p, i32, i32, P(View), P(View), vp, sz, vp]),
     "kvtc_compress_batch_workspace_bytes": (sz, [vp, vp, vp, vp, P(View), i32, P(Policy)]),

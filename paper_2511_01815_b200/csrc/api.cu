@@ -214,6 +214,10 @@ extern "C" kvtc_status kvtc_basis_create(const kvtc_shape *shape, kvtc_stream wh
   h = fnv1a(&which, sizeof(which), h);
   h = fnv1a(b->mu.data(), b->mu.size() * 4, h);
   h = fnv1a(b->V.data(), b->V.size() * 4, h);
+  // the RoPE description is part of the transform (keys are re-rotated with it)
+  const int32_t rope_meta[2] = {b->has_rope ? 1 : 0, b->pairing};
+  h = fnv1a(rope_meta, sizeof(rope_meta), h);
+  if (b->has_rope) h = fnv1a(b->invf.data(), b->invf.size() * 4, h);
   b->fp = h;
   *out = b;
   return KVTC_OK;
@@ -415,9 +419,12 @@ extern "C" kvtc_status kvtc_plan_create(int32_t r, int32_t ngroups, const int32_
   int prev_end = 0;
   for (int g = 0; g < ngroups; ++g) {
     const int s = start_host[g], z = size_host[g], t = type_host[g];
-    if (z <= 0 || s < prev_end || s + z > r || t < KVTC_T_INT2 || t > KVTC_T_FP8) {
+    if (z <= 0 || s < prev_end || s + z > r || t < KVTC_T_INT2 || t > KVTC_T_FP8 ||
+        !group_size_supported(z, bits_of(t))) {
       delete pl;
-      set_error("invalid: group %d (start %d size %d type %d)", g, s, z, t);
+      set_error("invalid: group %d (start %d size %d type %d)%s", g, s, z, t,
+                z > 0 && t >= KVTC_T_INT2 && t <= KVTC_T_FP8 && !group_size_supported(z, bits_of(t))
+                    ? ": unsupported group size (see kvtc_plan_create)" : "");
       return KVTC_E_INVALID;
     }
     pl->groups.push_back(PlanGroup{s, z, t, 0});

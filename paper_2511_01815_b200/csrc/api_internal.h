@@ -54,6 +54,15 @@ struct kvtc_plan {
 int64_t plan_tile_bytes(const kvtc_plan *pl, int64_t ntok);
 
 namespace kvtc {
+// Group sizes the compress / decompress kernels support for a type of `bits`
+// bits: up to one 256-column tile with whole-byte tokens, or sub-byte tokens
+// packed within one 32-bit word (the epilogue's warp OR-reduction); wider groups
+// must be whole 256-column pieces.  {1, 16, 64, 256, 1024} qualify.
+inline bool group_size_supported(int size, int bits) {
+  if (size < 1) return false;
+  if (size <= kMaxTileN) return (size * bits) % 8 == 0 || size * bits < 32;
+  return size % kMaxTileN == 0;
+}
 uint64_t fnv1a(const void *data, size_t n, uint64_t h);
 kvtc_status plan_compile(kvtc_plan *pl);
 const int64_t *plan_codes_off_last(kvtc_plan *pl, int64_t ntok);

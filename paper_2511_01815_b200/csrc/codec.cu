@@ -11,8 +11,12 @@ using namespace kvtc;
 namespace {
 
 constexpr uint32_t kContainerMagic = 0x4354564Bu;  // "KVTC"
-constexpr uint32_t kContainerVersion = 1;
+constexpr uint32_t kContainerVersion = 2;
+constexpr uint32_t kFlagNumeric = 1u;              // an fp16 shift / scale overflowed (Q4)
 
+// DESIGN.md §4.  Integrity (integrity.cu): payload_hash = checksum of each
+// stream's payload before DEFLATE, raw_hash = of the raw sink / window section,
+// header_hash = of bytes [0, 248) of this header.
 struct ContainerHeader {
   uint32_t magic, version;
   int32_t layers, kv_heads, head_dim, sinks, window, chunk_bytes;
@@ -21,18 +25,32 @@ struct ContainerHeader {
   uint64_t payload_bytes[2], entropy_bytes[2];
   uint64_t basis_fp[2], plan_fp[2];
   uint64_t raw_off, section_off[2];
-  uint8_t pad[256 - 160];
+  uint32_t flags, reserved;
+  uint64_t payload_hash[2], raw_hash;
+  uint8_t pad[248 - 192];
+  uint64_t header_hash;
 };
 static_assert(sizeof(ContainerHeader) == KVTC_HEADER_BYTES, "container header size");
+static_assert(offsetof(ContainerHeader, header_hash) == 248, "header hash last");
 
-__global__ void header_kernel(ContainerHeader h, uint8_t *out, const uint64_t *lens, uint64_t *offs) {
-  // offs[0] = K section offset (host-known), offs[1] = V section offset (= after K)
+// Device scratch words of one container written by compress (zeroed first):
+// [0..1] section lengths K/V, [2..3] section offsets K/V, [4] status bits,
+// [5..6] payload checksums K/V, [7] raw-section checksum.
+constexpr int kCompressWords = 8;
+
+// lens: nullable (passthrough container); aux = lens (see kCompressWords).
+__global__ void header_kernel(ContainerHeader h, uint8_t *out, const uint64_t *lens, const uint64_t *w) {
   if (lens) {
     h.entropy_bytes[0] = lens[0];
     h.entropy_bytes[1] = lens[1];
-    h.section_off[1] = offs[1];
-    h.total_bytes = offs[1] + lens[1];
+    h.section_off[1] = lens[3];
+    h.total_bytes = lens[3] + lens[1];
+    h.payload_hash[0] = w[5];
+    h.payload_hash[1] = w[6];
   }
+  h.flags = (w[4] & 1) ? kFlagNumeric : 0u;
+  h.raw_hash = w[7];
+  h.header_hash = hash_words(reinterpret_cast<const uint64_t *>(&h), 31, kSeedHeader);
   *reinterpret_cast<ContainerHeader *>(out) = h;
 }
 // next = 16-aligned end of the K section; the alignment gap is zeroed so the
@@ -41,6 +59,13 @@ __global__ void offset_after_kernel(const uint64_t *off, const uint64_t *len, ui
   const uint64_t end = *off + *len, aligned = *off + ((*len + 15) & ~15ull);
   for (uint64_t i = end; i < aligned; ++i) out[i] = 0;
   *next = aligned;
+}
+// The decompress status word: 0, or KVTC_E_CORRUPT when the inflater or a
+// checksum flagged the container.
+__global__ void status_kernel(const int32_t *err, int32_t nerr, int32_t *status_out) {
+  int32_t bad = 0;
+  for (int i = 0; i < nerr; ++i) bad |= err[i];
+  *status_out = bad ? int32_t(KVTC_E_CORRUPT) : 0;
 }
 
 inline uint64_t align16(uint64_t x) { return (x + 15) & ~15ull; }
@@ -90,7 +115,7 @@ bool direct_view_map(const kvtc_kv_view &v, int64_t tok0, CUtensorMap *m, int64_
 kvtc_status run_project_quant(const kvtc_basis *b, kvtc_plan *pl, const Operands *op, const void *X, int64_t m,
                               uint8_t *payload, float *wide, cudaStream_t st, const CUtensorMap *direct = nullptr,
                               int64_t tok0 = 0, int64_t ldx = 0, const TileRef *tiles = nullptr,
-                              int64_t layer_rows = 0, bool defer_wide = false) {
+                              int64_t layer_rows = 0, bool defer_wide = false, int32_t *status = nullptr) {
   if (m == 0 || pl->G == 0) return KVTC_OK;
   KVTC_CHECK_ARG(pl->nwide == 0 || wide, "wide-group scratch");
   CUtensorMap tA;
@@ -117,17 +142,19 @@ kvtc_status run_project_quant(const kvtc_basis *b, kvtc_plan *pl, const Operands
   a.D = wide;
   a.ldd = pl->wide_cols;
   a.tiles = tiles;
+  a.status = status;
   if ((s = launch_gemm_project_quant(a, st))) return s;
   // groups wider than a tile: quantised from the fp32 scratch (defer_wide: the
   // caller launches run_quant_wide itself, e.g. on the side stream)
   if (defer_wide) return KVTC_OK;
   return launch_quant_wide(pl->d_wide, pl->nwide, wide, pl->wide_cols, 1, m, pl->tile_bytes, a.codes_off_last,
-                           payload, st, tiles);
+                           payload, st, tiles, status);
 }
 
-kvtc_status run_quant_wide(kvtc_plan *pl, float *wide, int64_t m, uint8_t *payload, cudaStream_t st) {
+kvtc_status run_quant_wide(kvtc_plan *pl, float *wide, int64_t m, uint8_t *payload, cudaStream_t st,
+                           int32_t *status) {
   return launch_quant_wide(pl->d_wide, pl->nwide, wide, pl->wide_cols, 1, m, pl->tile_bytes,
-                           plan_codes_off_last(pl, m % kTileM), payload, st);
+                           plan_codes_off_last(pl, m % kTileM), payload, st, nullptr, status);
 }
 
 kvtc_status run_reconstruct(const kvtc_basis *b, const kvtc_plan *pl, const Operands *op, const __half *Dh,
@@ -318,7 +345,7 @@ extern "C" kvtc_status kvtc_stage_inflate(const uint8_t *section, size_t len, ui
   int32_t *err = nullptr;
   KVTC_CUDA_TRY(cudaMallocAsync(&err, 4, st));
   KVTC_CUDA_TRY(cudaMemsetAsync(err, 0, 4, st));
-  s = launch_inflate_section(section, nullptr, n_out, nch, out, err, st);
+  s = launch_inflate_section(section, len, n_out, nch, out, err, st);
   int32_t herr = 0;
   KVTC_CUDA_TRY(cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st));
   KVTC_CUDA_TRY(cudaStreamSynchronize(st));
@@ -463,7 +490,8 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
   Bump ws(workspace, workspace_bytes);
   auto *kbases = ws.take<__nv_bfloat16 *>(k->shape.layers);
   auto *vbases = ws.take<__nv_bfloat16 *>(k->shape.layers);
-  uint64_t *lens = ws.take<uint64_t>(8);     // [0..1] section lengths, [2..3] section offsets
+  uint64_t *lens = ws.take<uint64_t>(kCompressWords);     // see kCompressWords
+  int32_t *cstatus = reinterpret_cast<int32_t *>(lens + 4);
   const int64_t ldx = kb->p + kXPad;
   auto *X = ws.take<__nv_bfloat16>(L.m * ldx);
   float2 *cs = ws.take<float2>(L.m * (kb->shape.head_dim / 2));
@@ -476,6 +504,7 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
   float *wide = ws.take<float>(L.m * std::max(kp->wide_cols, vp->wide_cols));
   float *wide_v = ws.take<float>(L.m * vp->wide_cols);
   if ((s = upload_bases(k, kbases, st)) || (s = upload_bases(v, vbases, st))) return s;
+  KVTC_CUDA_TRY(cudaMemsetAsync(lens, 0, kCompressWords * 8, st));
 
   uint8_t *o = static_cast<uint8_t *>(out);
   ContainerHeader h = {};
@@ -514,10 +543,12 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
       if ((s = launch_pack_raw(*vw, bs, 0, pol->sinks, dst, L.nraw, 0, st))) return s;
       if ((s = launch_pack_raw(*vw, bs, t - pol->window, pol->window, dst, L.nraw, pol->sinks, st))) return s;
     }
+    if ((s = launch_hash(rawk, L.raw_bytes, kSeedRaw, lens + 7, st))) return s;
   } else {
     if ((s = launch_pack_raw(*k, kbases, 0, t, rawk, L.nraw, 0, st))) return s;
     if ((s = launch_pack_raw(*v, vbases, 0, t, rawv, L.nraw, 0, st))) return s;
-    header_kernel<<<1, 1, 0, st>>>(h, o, nullptr, nullptr);
+    if ((s = launch_hash(rawk, L.raw_bytes, kSeedRaw, lens + 7, st))) return s;
+    header_kernel<<<1, 1, 0, st>>>(h, o, nullptr, lens);
     KVTC_LAUNCH_CHECK();
     if (out_len_host) {
       KVTC_CUDA_TRY(cudaStreamSynchronize(st));
@@ -561,12 +592,18 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
     // stream (before their DEFLATE) when the schedule overlaps it
     if (sv && defer_v_wide) wd = wide_v;
     return sv ? run_project_quant(vb, vpl, vop, X, r1 - r0, pay, wd, st, direct ? &tV : nullptr, pol->sinks + r0,
-                                  ldx, nullptr, v_layer_rows, defer_v_wide)
-              : run_project_quant(kb, kpl, kop, X + r0 * ldx, r1 - r0, pay, wd, st, nullptr, 0, ldx);
+                                  ldx, nullptr, v_layer_rows, defer_v_wide, cstatus)
+              : run_project_quant(kb, kpl, kop, X + r0 * ldx, r1 - r0, pay, wd, st, nullptr, 0, ldx, nullptr, 0,
+                                  false, cstatus);
   };
+  // the payload checksum is taken on the encoder's stream right before the call
+  // that encodes the last chunk range: the whole payload is complete there
   auto encode = [&](int sv, cudaStream_t q, int ctas, const char *tag, uint32_t c0 = 0,
                     uint32_t c1 = 0xFFFFFFFFu) -> kvtc_status {
     ProfScope ps(tag, q);
+    kvtc_status r;
+    if (c1 == 0xFFFFFFFFu && (r = launch_hash(sv ? payload_v : payload_k, L.pay[sv], kSeedPayload, lens + 5 + sv, q, ctas)))
+      return r;
     return launch_deflate_encode(sv ? payload_v : payload_k, L.pay[sv], pol->chunk_bytes, dwsp[sv], dws[sv], ctas, q,
                                  c0, c1);
   };
@@ -607,7 +644,7 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
     if (deflate_side) {
       if (defer_v_wide) {
         ProfScope ps("c.quant_wide_overlapped", aux);
-        if ((s = run_quant_wide(vpl, wide_v, L.m, payload_v, aux))) return s;
+        if ((s = run_quant_wide(vpl, wide_v, L.m, payload_v, aux, cstatus))) return s;
       }
       if ((s = encode(1, aux, side_ctas, "c.deflate_overlapped"))) return s;
       if (split) {
@@ -640,25 +677,69 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
     KVTC_LAUNCH_CHECK();
     if ((s = launch_deflate_assemble(L.pay[1], pol->chunk_bytes, dwsp[1], o, lens + 3, lens + 1, st))) return s;
   }
-  header_kernel<<<1, 1, 0, st>>>(h, o, lens, lens + 2);
+  header_kernel<<<1, 1, 0, st>>>(h, o, lens, lens);
   KVTC_LAUNCH_CHECK();
   if (out_len_host) {
-    uint64_t l4[4];
-    KVTC_CUDA_TRY(cudaMemcpyAsync(l4, lens, 32, cudaMemcpyDeviceToHost, st));
+    uint64_t l4[kCompressWords];
+    KVTC_CUDA_TRY(cudaMemcpyAsync(l4, lens, sizeof(l4), cudaMemcpyDeviceToHost, st));
     KVTC_CUDA_TRY(cudaStreamSynchronize(st));
     *out_len_host = size_t(l4[3] + l4[1]);      // V section offset + V section length
+    if (l4[4] & 1) {
+      set_error("a 16-bit shift/scale overflowed (container flagged)");
+      return KVTC_E_NUMERIC;
+    }
   }
   return KVTC_OK;
 }
+
+namespace {
+// Internal consistency of a container header (host copy): its checksum, its
+// flags, and every size / offset the decompressor uses, re-derived from the
+// shape — so a damaged or crafted header can make no read outside the container
+// and no write outside the caller's views.
+kvtc_status validate_header(const ContainerHeader &h) {
+  auto bad = [](const char *what) {
+    set_error("corrupt container: %s", what);
+    return KVTC_E_CORRUPT;
+  };
+  if (h.magic != kContainerMagic || h.version != kContainerVersion) {
+    set_error("not a KVTC container (magic %08x version %u)", h.magic, h.version);
+    return KVTC_E_CORRUPT;
+  }
+  if (hash_words(reinterpret_cast<const uint64_t *>(&h), 31, kSeedHeader) != h.header_hash)
+    return bad("header checksum");
+  if (h.layers <= 0 || h.layers > 65536 || h.kv_heads <= 0 || h.kv_heads > 65536 || h.head_dim <= 0 ||
+      h.head_dim > 4096 || h.head_dim % 32 || h.sinks < 0 || h.window < 0 || h.tokens < 0 ||
+      h.tokens > (int64_t(1) << 40) || (h.chunk_bytes != 16384 && h.chunk_bytes != 32768 && h.chunk_bytes != 65536))
+    return bad("shape / policy fields");
+  const int64_t sw = int64_t(h.sinks) + h.window;
+  const int64_t m = h.tokens > sw ? h.tokens - sw : 0;
+  if (h.m != m) return bad("m != tokens - sinks - window");
+  const int64_t nraw = m ? sw : h.tokens;
+  const uint64_t raw = 2ull * uint64_t(h.layers) * uint64_t(nraw) * uint64_t(h.kv_heads) * uint64_t(h.head_dim) * 2;
+  if (h.raw_off != KVTC_HEADER_BYTES || h.raw_bytes != raw) return bad("raw section size / offset");
+  if (m) {
+    const uint64_t k_off = align16(KVTC_HEADER_BYTES + raw);
+    if (h.section_off[0] != k_off || h.section_off[1] != k_off + align16(h.entropy_bytes[0]) ||
+        h.entropy_bytes[0] < kSectionHeaderBytes || h.entropy_bytes[1] < kSectionHeaderBytes ||
+        h.entropy_bytes[0] > (uint64_t(1) << 50) || h.entropy_bytes[1] > (uint64_t(1) << 50) ||
+        h.total_bytes != h.section_off[1] + h.entropy_bytes[1])
+      return bad("section offsets / lengths");
+  }
+  if (h.flags & ~kFlagNumeric) return bad("unknown flags");
+  if (h.flags & kFlagNumeric) {
+    set_error("container flagged at compression: a 16-bit shift/scale overflowed (Q4)");
+    return KVTC_E_NUMERIC;
+  }
+  return KVTC_OK;
+}
+}  // namespace
 
 extern "C" kvtc_status kvtc_container_parse(const void *header_host, kvtc_container_info *info) {
   KVTC_CHECK_ARG(header_host && info, "container_parse arguments");
   ContainerHeader h;
   memcpy(&h, header_host, sizeof(h));
-  if (h.magic != kContainerMagic || h.version != kContainerVersion) {
-    set_error("not a KVTC container (magic %08x version %u)", h.magic, h.version);
-    return KVTC_E_CORRUPT;
-  }
+  *info = kvtc_container_info{};
   info->magic = h.magic;
   info->version = h.version;
   info->layers = h.layers;
@@ -677,169 +758,16 @@ extern "C" kvtc_status kvtc_container_parse(const void *header_host, kvtc_contai
     info->entropy_bytes[s] = h.entropy_bytes[s];
     info->basis_fp[s] = h.basis_fp[s];
     info->plan_fp[s] = h.plan_fp[s];
+    info->payload_hash[s] = h.payload_hash[s];
   }
-  return KVTC_OK;
+  info->flags = h.flags;
+  info->raw_hash = h.raw_hash;
+  return validate_header(h);
 }
 
-extern "C" size_t kvtc_decompress_workspace_bytes(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb,
-                                                  const kvtc_plan *vp, const void *in_header_host) {
-  if (!kb || !kp || !vb || !vp || !in_header_host) return 0;
-  ContainerHeader h;
-  memcpy(&h, in_header_host, sizeof(h));
-  Bump b;
-  b.take<void *>(h.layers);
-  b.take<void *>(h.layers);
-  b.take<int32_t>(4);
-  b.take<uint8_t>(h.payload_bytes[0] + 16);
-  b.take<uint8_t>(h.payload_bytes[1] + 16);
-  b.take<__half>(h.m * std::max(std::max(kp->r_nz_pad, vp->r_nz_pad), 8));
-  b.take<__half>(h.m * std::max(std::max(kp->r_nz_pad, vp->r_nz_pad), 8));
-  b.take<float2>(h.m * (kb->shape.head_dim / 2));
-  return b.used + 256;
-}
-
-extern "C" kvtc_status kvtc_decompress(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb,
-                                       const kvtc_plan *vp, const void *in, size_t in_len, int32_t layer_begin,
-                                       int32_t layer_end, const kvtc_kv_view *k_out, const kvtc_kv_view *v_out,
-                                       void *workspace, size_t workspace_bytes, void *stream) {
-  KVTC_CHECK_ARG(kb && kp && vb && vp && in && k_out && v_out, "decompress arguments");
-  kvtc_status s;
-  if ((s = check_view(k_out)) || (s = check_view(v_out))) return s;
-  KVTC_CHECK_ARG(in_len >= KVTC_HEADER_BYTES, "container too short");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  ContainerHeader h;
-  KVTC_CUDA_TRY(cudaMemcpyAsync(&h, in, sizeof(h), cudaMemcpyDeviceToHost, st));
-  KVTC_CUDA_TRY(cudaStreamSynchronize(st));
-  kvtc_container_info info;
-  if ((s = kvtc_container_parse(&h, &info))) return s;
-  const kvtc_shape shp{h.layers, h.kv_heads, h.head_dim};
-  if (!same_shape(shp, k_out->shape) || !same_shape(shp, v_out->shape) || k_out->tokens != h.tokens ||
-      v_out->tokens != h.tokens || !same_shape(shp, kb->shape) || !same_shape(shp, vb->shape)) {
-    set_error("container shape does not match the output views / bases");
-    return KVTC_E_MISMATCH;
-  }
-  if (h.basis_fp[0] != kb->fp || h.basis_fp[1] != vb->fp || h.plan_fp[0] != kp->fp || h.plan_fp[1] != vp->fp) {
-    set_error("container was written with a different basis or plan");
-    return KVTC_E_MISMATCH;
-  }
-  if (info.total_bytes > in_len) {
-    set_error("container length %llu > buffer %zu", (unsigned long long)info.total_bytes, in_len);
-    return KVTC_E_CORRUPT;
-  }
-  if (h.m && (h.payload_bytes[0] != kvtc_payload_bytes(kp, h.m) || h.payload_bytes[1] != kvtc_payload_bytes(vp, h.m))) {
-    set_error("payload sizes do not match the plans");
-    return KVTC_E_CORRUPT;
-  }
-  KVTC_CHECK_ARG(0 <= layer_begin && layer_begin <= layer_end && layer_end <= h.layers, "layer range");
-  const size_t need = kvtc_decompress_workspace_bytes(kb, kp, vb, vp, &h);
-  if (!workspace || workspace_bytes < need) {
-    set_error("workspace %zu < %zu", workspace_bytes, need);
-    return KVTC_E_CAPACITY;
-  }
-  Bump ws(workspace, workspace_bytes);
-  auto *kbases = ws.take<__nv_bfloat16 *>(h.layers);
-  auto *vbases = ws.take<__nv_bfloat16 *>(h.layers);
-  int32_t *err = ws.take<int32_t>(4);
-  uint8_t *payloads[2];
-  payloads[0] = ws.take<uint8_t>(h.payload_bytes[0] + 16);
-  payloads[1] = ws.take<uint8_t>(h.payload_bytes[1] + 16);
-  const int64_t ld = std::max(std::max(kp->r_nz_pad, vp->r_nz_pad), 8);
-  __half *Dh = ws.take<__half>(h.m * ld);
-  __half *Dh_v = ws.take<__half>(h.m * ld);
-  float2 *cs = ws.take<float2>(h.m * (h.head_dim / 2));
-  if ((s = upload_bases(k_out, kbases, st)) || (s = upload_bases(v_out, vbases, st))) return s;
-  KVTC_CUDA_TRY(cudaMemsetAsync(err, 0, 4, st));
-  const uint8_t *ib = static_cast<const uint8_t *>(in);
-  const int64_t t = h.tokens;
-  const int64_t nraw = h.m ? int64_t(h.sinks) + h.window : t;
-  const int64_t hd = int64_t(h.kv_heads) * h.head_dim;
-  const auto *rawk = reinterpret_cast<const __nv_bfloat16 *>(ib + h.raw_off);
-  const auto *rawv = rawk + int64_t(h.layers) * nraw * hd;
-  if (!h.m) {
-    if ((s = launch_unpack_raw(rawk, nraw, 0, t, *k_out, kbases, 0, layer_begin, layer_end, st))) return s;
-    return launch_unpack_raw(rawv, nraw, 0, t, *v_out, vbases, 0, layer_begin, layer_end, st);
-  }
-  // device copy of the section offsets lives in the container header itself
-  const uint64_t *sec_off_dev = reinterpret_cast<const uint64_t *>(ib + offsetof(ContainerHeader, section_off));
-  if (kb->has_rope && (s = rope_table_for(kb, h.pos0 + h.sinks, h.m, cs, st))) return s;
-  // Both streams' DEFLATE sections are inflated by ONE full-grid launch (the
-  // inflater is latency-bound: as a bounded side-stream grid it ran 3-5x slower
-  // and delayed the values' GEMM); then keys: dequantise -> GEMM on the caller's
-  // stream, values: dequantise on the side stream (bounded grid, beside the keys'
-  // GEMM, enqueued after it) -> GEMM.
-  SideStream *ss = side_stream();
-  const bool ovl = !overlap_off();
-  cudaStream_t aux = ovl ? ss->s : st;
-  __half *Dhs[2] = {Dh, Dh_v};
-  // KVTC_D_INFLATE_SIDE=1: inflate only the keys here and the values' section on
-  // the side stream beside the keys' GEMM (bounded grid)
-  const bool inflate_side = ovl && env_flag("KVTC_D_INFLATE_SIDE", false);
-  uint32_t nch[2];
-  for (int sv = 0; sv < 2; ++sv) nch[sv] = uint32_t((h.payload_bytes[sv] + h.chunk_bytes - 1) / h.chunk_bytes);
-  {
-    ProfScope ps("d.inflate", st);
-    if (inflate_side) {
-      if ((s = launch_inflate_section(ib, sec_off_dev, h.payload_bytes[0], nch[0], payloads[0], err, st))) return s;
-    } else if ((s = launch_inflate_sections(ib, sec_off_dev, h.payload_bytes[0], nch[0], payloads[0], sec_off_dev + 1,
-                                            h.payload_bytes[1], nch[1], payloads[1], err, st))) {
-      return s;
-    }
-  }
-  auto expand = [&](int sv, cudaStream_t q, int ctas) -> kvtc_status {
-    kvtc_plan *pl = const_cast<kvtc_plan *>(sv ? vp : kp);
-    kvtc_status r;
-    if (sv && inflate_side) {
-      ProfScope ps("d.inflate_overlapped", q);
-      if ((r = launch_inflate_section(ib, sec_off_dev + 1, h.payload_bytes[1], nch[1], payloads[1], err, q,
-                                      corun_ctas(corun_per_sm("KVTC_CORUN_INFLATE", 2)))))
-        return r;
-    }
-    ProfScope ps(sv && ovl ? "d.dequant_overlapped" : "d.dequant", q);
-    if ((r = launch_dequant(pl->d_pgroups, pl->d_codes_off_full, pl->G, plan_codes_off_last(pl, h.m % kTileM),
-                            pl->tile_bytes, payloads[sv], h.m, Dhs[sv], ld, q, ctas)))
-      return r;
-    if (pl->r_nz == 0) KVTC_CUDA_TRY(cudaMemsetAsync(Dhs[sv], 0, h.m * ld * 2, q));
-    return KVTC_OK;
-  };
-  if ((s = expand(0, st, 0))) return s;
-  KVTC_CUDA_TRY(cudaEventRecord(ss->ev[2], st));                 // header/bases/err ready, keys expanded
-  for (int sv = 0; sv < 2; ++sv) {
-    const kvtc_basis *b = sv ? vb : kb;
-    kvtc_plan *pl = const_cast<kvtc_plan *>(sv ? vp : kp);
-    const kvtc_kv_view *vw = sv ? v_out : k_out;
-    __nv_bfloat16 *const *bs = sv ? vbases : kbases;
-    const Operands *op;
-    if ((s = plan_operands(b, pl, &op))) return s;
-    if (sv == 1) KVTC_CUDA_TRY(cudaStreamWaitEvent(st, ss->ev[3], 0));   // join: values expanded
-    {
-      ProfScope ps("d.reconstruct_gemm", st);
-      if ((s = run_reconstruct(b, pl, op, Dhs[sv], ld, h.m, h.sinks, layer_begin, layer_end, vw, bs, cs, st))) return s;
-    }
-    if (sv == 0) {
-      KVTC_CUDA_TRY(cudaStreamWaitEvent(aux, ss->ev[2], 0));
-      if ((s = expand(1, aux, ovl ? corun_ctas(corun_per_sm("KVTC_CORUN_DEQUANT", 2)) : 0))) return s;
-      KVTC_CUDA_TRY(cudaEventRecord(ss->ev[3], aux));
-    }
-    const __nv_bfloat16 *raw = sv ? rawv : rawk;
-    {
-      ProfScope ps("d.raw_tokens", st);
-      if ((s = launch_unpack_raw(raw, nraw, 0, h.sinks, *vw, bs, 0, layer_begin, layer_end, st))) return s;
-      if ((s = launch_unpack_raw(raw, nraw, h.sinks, h.window, *vw, bs, t - h.window, layer_begin, layer_end, st)))
-        return s;
-    }
-  }
-  return KVTC_OK;
-}
-
-// ============================================== layer-streamed decompression
-// P:L210: "the inverse projection ... can be performed layer-by-layer using
-// sub-matrices of V^T, allowing generation to begin early".  The coefficients D^
-// mix all layers, so inflate + dequantise run ONCE (kvtc_decompress_begin, into
-// the caller's workspace); each kvtc_decompress_layers call then runs only the
-// reconstruction GEMMs over its layers' h*d columns of V_d^T (and copies those
-// layers' raw tokens), so a consumer can start on layer 0 while later layers are
-// still being rebuilt.  Workspace layout = kvtc_decompress's.
 namespace {
+// Header (host copy) checked against the container rules and the caller's
+// bases / plans; in_len > 0 also bounds the container length.
 kvtc_status read_checked_header(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb, const kvtc_plan *vp,
                                 const void *header_host, size_t in_len, ContainerHeader *out) {
   ContainerHeader h;
@@ -861,15 +789,18 @@ kvtc_status read_checked_header(const kvtc_basis *kb, const kvtc_plan *kp, const
     return KVTC_E_CORRUPT;
   }
   if (h.m && (h.payload_bytes[0] != kvtc_payload_bytes(kp, h.m) || h.payload_bytes[1] != kvtc_payload_bytes(vp, h.m))) {
-    set_error("payload sizes do not match the plans");
+    set_error("corrupt container: payload sizes do not match the plans");
     return KVTC_E_CORRUPT;
   }
   *out = h;
   return KVTC_OK;
 }
+
+// Workspace of one decompression (kvtc_decompress_workspace_bytes).
 struct DecompWs {
   __nv_bfloat16 **kbases, **vbases;
-  int32_t *err;
+  int32_t *err;          // [0] inflater, [1] checksum mismatch bits, [2] status word, [3] unused
+  uint64_t *hsum;        // checksums of the inflated payloads K/V and of the raw section
   uint8_t *payloads[2];
   __half *Dh[2];
   float2 *cs;
@@ -882,6 +813,7 @@ DecompWs carve_decomp(const kvtc_plan *kp, const kvtc_plan *vp, const ContainerH
   w.kbases = ws.take<__nv_bfloat16 *>(h.layers);
   w.vbases = ws.take<__nv_bfloat16 *>(h.layers);
   w.err = ws.take<int32_t>(4);
+  w.hsum = ws.take<uint64_t>(4);
   w.payloads[0] = ws.take<uint8_t>(h.payload_bytes[0] + 16);
   w.payloads[1] = ws.take<uint8_t>(h.payload_bytes[1] + 16);
   w.ld = std::max(std::max(kp->r_nz_pad, vp->r_nz_pad), 8);
@@ -890,12 +822,205 @@ DecompWs carve_decomp(const kvtc_plan *kp, const kvtc_plan *vp, const ContainerH
   w.cs = ws.take<float2>(h.m * (h.head_dim / 2));
   return w;
 }
+
+// Both sections through ONE inflate launch (the inflater is latency-bound: as a
+// bounded side-stream grid it ran 3-5x slower and delayed the values' GEMM).
+// Every read is bounded by the section lengths of the validated header.
+kvtc_status enqueue_inflate(const uint8_t *ib, const ContainerHeader &h, const DecompWs &w, cudaStream_t st) {
+  uint32_t nch[2];
+  for (int sv = 0; sv < 2; ++sv) nch[sv] = uint32_t((h.payload_bytes[sv] + h.chunk_bytes - 1) / h.chunk_bytes);
+  ProfScope ps("d.inflate", st);
+  return launch_inflate_sections(ib + h.section_off[0], h.entropy_bytes[0], h.payload_bytes[0], nch[0], w.payloads[0],
+                                 ib + h.section_off[1], h.entropy_bytes[1], h.payload_bytes[1], nch[1], w.payloads[1],
+                                 w.err, st);
+}
+// Checksums of the inflated payloads and of the raw section against the header
+// (integrity.cu): mismatch bits 1 / 2 (payload K / V), 4 (raw section).
+kvtc_status enqueue_checks(const uint8_t *ib, const ContainerHeader &h, const DecompWs &w, cudaStream_t q,
+                           int32_t ctas) {
+  kvtc_status s;
+  if (h.m)
+    for (int sv = 0; sv < 2; ++sv)
+      if ((s = launch_hash(w.payloads[sv], h.payload_bytes[sv], kSeedPayload, w.hsum + sv, q, ctas)) ||
+          (s = launch_hash_check(w.hsum + sv, h.payload_hash[sv], 1 << sv, w.err + 1, q)))
+        return s;
+  if ((s = launch_hash(ib + h.raw_off, h.raw_bytes, kSeedRaw, w.hsum + 2, q, ctas)) ||
+      (s = launch_hash_check(w.hsum + 2, h.raw_hash, 4, w.err + 1, q)))
+    return s;
+  return KVTC_OK;
+}
+kvtc_status enqueue_status(const DecompWs &w, int32_t *status_dev, cudaStream_t st) {
+  status_kernel<<<1, 1, 0, st>>>(w.err, 2, status_dev ? status_dev : w.err + 2);
+  KVTC_LAUNCH_CHECK();
+  return KVTC_OK;
+}
+kvtc_status read_status(const DecompWs &w, cudaStream_t st) {
+  int32_t v = 0;
+  KVTC_CUDA_TRY(cudaMemcpyAsync(&v, w.err + 2, 4, cudaMemcpyDeviceToHost, st));
+  KVTC_CUDA_TRY(cudaStreamSynchronize(st));
+  if (v) {
+    set_error("corrupt container: DEFLATE stream or checksum mismatch");
+    return KVTC_E_CORRUPT;
+  }
+  return KVTC_OK;
+}
+
+// The whole decompression of a validated header, enqueued without host
+// synchronisation.  Schedule: keys: dequantise -> GEMM on the caller's stream;
+// values: dequantise + the checksums on the side stream (bounded grid, beside the
+// keys' GEMM) -> GEMM; then the raw sinks / window and the status word.
+kvtc_status decompress_enqueue(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb, const kvtc_plan *vp,
+                               const uint8_t *ib, const ContainerHeader &h, int32_t layer_begin, int32_t layer_end,
+                               const kvtc_kv_view *k_out, const kvtc_kv_view *v_out, int32_t *status_dev,
+                               void *workspace, size_t workspace_bytes, cudaStream_t st) {
+  kvtc_status s;
+  if ((s = check_view(k_out)) || (s = check_view(v_out))) return s;
+  const kvtc_shape shp{h.layers, h.kv_heads, h.head_dim};
+  if (!same_shape(shp, k_out->shape) || !same_shape(shp, v_out->shape) || k_out->tokens != h.tokens ||
+      v_out->tokens != h.tokens) {
+    set_error("container shape does not match the output views");
+    return KVTC_E_MISMATCH;
+  }
+  KVTC_CHECK_ARG(0 <= layer_begin && layer_begin <= layer_end && layer_end <= h.layers, "layer range");
+  KVTC_CHECK_ARG((reinterpret_cast<uintptr_t>(ib) & 15) == 0, "container must be 16-byte aligned");
+  const size_t need = kvtc_decompress_workspace_bytes(kb, kp, vb, vp, &h);
+  if (!workspace || workspace_bytes < need) {
+    set_error("workspace %zu < %zu", workspace_bytes, need);
+    return KVTC_E_CAPACITY;
+  }
+  DecompWs w = carve_decomp(kp, vp, h, workspace, workspace_bytes);
+  if ((s = upload_bases(k_out, w.kbases, st)) || (s = upload_bases(v_out, w.vbases, st))) return s;
+  KVTC_CUDA_TRY(cudaMemsetAsync(w.err, 0, 16, st));
+  KVTC_CUDA_TRY(cudaMemsetAsync(w.hsum, 0, 32, st));
+  const int64_t t = h.tokens;
+  const int64_t nraw = h.m ? int64_t(h.sinks) + h.window : t;
+  const int64_t hd = int64_t(h.kv_heads) * h.head_dim;
+  const auto *rawk = reinterpret_cast<const __nv_bfloat16 *>(ib + h.raw_off);
+  const auto *rawv = rawk + int64_t(h.layers) * nraw * hd;
+  if (!h.m) {
+    if ((s = enqueue_checks(ib, h, w, st, 0))) return s;
+    if ((s = launch_unpack_raw(rawk, nraw, 0, t, *k_out, w.kbases, 0, layer_begin, layer_end, st))) return s;
+    if ((s = launch_unpack_raw(rawv, nraw, 0, t, *v_out, w.vbases, 0, layer_begin, layer_end, st))) return s;
+    return enqueue_status(w, status_dev, st);
+  }
+  if (kb->has_rope && (s = rope_table_for(kb, h.pos0 + h.sinks, h.m, w.cs, st))) return s;
+  SideStream *ss = side_stream();
+  const bool ovl = !overlap_off();
+  cudaStream_t aux = ovl ? ss->s : st;
+  if ((s = enqueue_inflate(ib, h, w, st))) return s;
+  auto expand = [&](int sv, cudaStream_t q, int ctas) -> kvtc_status {
+    kvtc_plan *pl = const_cast<kvtc_plan *>(sv ? vp : kp);
+    kvtc_status r;
+    ProfScope ps(sv && ovl ? "d.dequant_overlapped" : "d.dequant", q);
+    if ((r = launch_dequant(pl->d_pgroups, pl->d_codes_off_full, pl->G, plan_codes_off_last(pl, h.m % kTileM),
+                            pl->tile_bytes, w.payloads[sv], h.m, w.Dh[sv], w.ld, q, ctas)))
+      return r;
+    if (pl->r_nz == 0) KVTC_CUDA_TRY(cudaMemsetAsync(w.Dh[sv], 0, h.m * w.ld * 2, q));
+    return KVTC_OK;
+  };
+  if ((s = expand(0, st, 0))) return s;
+  KVTC_CUDA_TRY(cudaEventRecord(ss->ev[2], st));                 // inflated, keys expanded
+  for (int sv = 0; sv < 2; ++sv) {
+    const kvtc_basis *b = sv ? vb : kb;
+    kvtc_plan *pl = const_cast<kvtc_plan *>(sv ? vp : kp);
+    const kvtc_kv_view *vw = sv ? v_out : k_out;
+    __nv_bfloat16 *const *bs = sv ? w.vbases : w.kbases;
+    const Operands *op;
+    if ((s = plan_operands(b, pl, &op))) return s;
+    if (sv == 1) KVTC_CUDA_TRY(cudaStreamWaitEvent(st, ss->ev[3], 0));   // join: values expanded, checks done
+    {
+      ProfScope ps("d.reconstruct_gemm", st);
+      if ((s = run_reconstruct(b, pl, op, w.Dh[sv], w.ld, h.m, h.sinks, layer_begin, layer_end, vw, bs, w.cs, st)))
+        return s;
+    }
+    if (sv == 0) {
+      KVTC_CUDA_TRY(cudaStreamWaitEvent(aux, ss->ev[2], 0));
+      const int ctas = ovl ? corun_ctas(corun_per_sm("KVTC_CORUN_DEQUANT", 2)) : 0;
+      if ((s = expand(1, aux, ctas))) return s;
+      {
+        ProfScope ps(ovl ? "d.checksum_overlapped" : "d.checksum", aux);
+        if ((s = enqueue_checks(ib, h, w, aux, ctas))) return s;
+      }
+      KVTC_CUDA_TRY(cudaEventRecord(ss->ev[3], aux));
+    }
+    const __nv_bfloat16 *raw = sv ? rawv : rawk;
+    {
+      ProfScope ps("d.raw_tokens", st);
+      if ((s = launch_unpack_raw(raw, nraw, 0, h.sinks, *vw, bs, 0, layer_begin, layer_end, st))) return s;
+      if ((s = launch_unpack_raw(raw, nraw, h.sinks, h.window, *vw, bs, t - h.window, layer_begin, layer_end, st)))
+        return s;
+    }
+  }
+  return enqueue_status(w, status_dev, st);
+}
 }  // namespace
 
+extern "C" size_t kvtc_decompress_workspace_bytes(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb,
+                                                  const kvtc_plan *vp, const void *in_header_host) {
+  if (!kb || !kp || !vb || !vp || !in_header_host) return 0;
+  ContainerHeader h;
+  memcpy(&h, in_header_host, sizeof(h));
+  if (validate_header(h) != KVTC_OK) return 0;     // the call itself reports why
+  Bump b;
+  b.take<void *>(h.layers);
+  b.take<void *>(h.layers);
+  b.take<int32_t>(4);
+  b.take<uint64_t>(4);
+  b.take<uint8_t>(h.payload_bytes[0] + 16);
+  b.take<uint8_t>(h.payload_bytes[1] + 16);
+  b.take<__half>(h.m * std::max(std::max(kp->r_nz_pad, vp->r_nz_pad), 8));
+  b.take<__half>(h.m * std::max(std::max(kp->r_nz_pad, vp->r_nz_pad), 8));
+  b.take<float2>(h.m * (kb->shape.head_dim / 2));
+  return b.used + 256;
+}
+
+extern "C" kvtc_status kvtc_decompress(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb,
+                                       const kvtc_plan *vp, const void *in, size_t in_len, int32_t layer_begin,
+                                       int32_t layer_end, const kvtc_kv_view *k_out, const kvtc_kv_view *v_out,
+                                       void *workspace, size_t workspace_bytes, void *stream) {
+  KVTC_CHECK_ARG(kb && kp && vb && vp && in && k_out && v_out, "decompress arguments");
+  KVTC_CHECK_ARG(in_len >= KVTC_HEADER_BYTES, "container too short");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ContainerHeader hh, h;
+  KVTC_CUDA_TRY(cudaMemcpyAsync(&hh, in, sizeof(hh), cudaMemcpyDeviceToHost, st));
+  KVTC_CUDA_TRY(cudaStreamSynchronize(st));
+  kvtc_status s = read_checked_header(kb, kp, vb, vp, &hh, in_len, &h);
+  if (s) return s;
+  if ((s = decompress_enqueue(kb, kp, vb, vp, static_cast<const uint8_t *>(in), h, layer_begin, layer_end, k_out,
+                              v_out, nullptr, workspace, workspace_bytes, st)))
+    return s;
+  return read_status(carve_decomp(kp, vp, h, workspace, workspace_bytes), st);
+}
+
+extern "C" kvtc_status kvtc_decompress_async(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb,
+                                             const kvtc_plan *vp, const void *in, size_t in_len,
+                                             const void *header_host, int32_t layer_begin, int32_t layer_end,
+                                             const kvtc_kv_view *k_out, const kvtc_kv_view *v_out,
+                                             int32_t *status_dev, void *workspace, size_t workspace_bytes,
+                                             void *stream) {
+  KVTC_CHECK_ARG(kb && kp && vb && vp && in && header_host && k_out && v_out, "decompress_async arguments");
+  KVTC_CHECK_ARG(in_len >= KVTC_HEADER_BYTES, "container too short");
+  ContainerHeader h;
+  kvtc_status s = read_checked_header(kb, kp, vb, vp, header_host, in_len, &h);
+  if (s) return s;
+  return decompress_enqueue(kb, kp, vb, vp, static_cast<const uint8_t *>(in), h, layer_begin, layer_end, k_out, v_out,
+                            status_dev, workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
+}
+
+// ============================================== layer-streamed decompression
+// P:L210: "the inverse projection ... can be performed layer-by-layer using
+// sub-matrices of V^T, allowing generation to begin early".  The coefficients D^
+// mix all layers, so inflate + dequantise run ONCE (kvtc_decompress_begin, into
+// the caller's workspace, which also verifies the checksums); each
+// kvtc_decompress_layers call then runs only the reconstruction GEMMs over its
+// layers' h*d columns of V_d^T (and copies those layers' raw tokens), so a
+// consumer can start on layer 0 while later layers are still being rebuilt.
+// Workspace layout = kvtc_decompress's.
 extern "C" kvtc_status kvtc_decompress_begin(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb,
                                              const kvtc_plan *vp, const void *in, size_t in_len, void *workspace,
                                              size_t workspace_bytes, void *stream) {
   KVTC_CHECK_ARG(kb && kp && vb && vp && in && in_len >= KVTC_HEADER_BYTES, "decompress_begin arguments");
+  KVTC_CHECK_ARG((reinterpret_cast<uintptr_t>(in) & 15) == 0, "container must be 16-byte aligned");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   ContainerHeader hh;
   KVTC_CUDA_TRY(cudaMemcpyAsync(&hh, in, sizeof(hh), cudaMemcpyDeviceToHost, st));
@@ -908,29 +1033,24 @@ extern "C" kvtc_status kvtc_decompress_begin(const kvtc_basis *kb, const kvtc_pl
     set_error("workspace %zu < %zu", workspace_bytes, need);
     return KVTC_E_CAPACITY;
   }
-  if (!h.m) return KVTC_OK;
   DecompWs w = carve_decomp(kp, vp, h, workspace, workspace_bytes);
   const uint8_t *ib = static_cast<const uint8_t *>(in);
-  const uint64_t *sec_off_dev = reinterpret_cast<const uint64_t *>(ib + offsetof(ContainerHeader, section_off));
-  KVTC_CUDA_TRY(cudaMemsetAsync(w.err, 0, 4, st));
-  {
-    ProfScope ps("d.inflate", st);
-    uint32_t nch[2];
-    for (int sv = 0; sv < 2; ++sv) nch[sv] = uint32_t((h.payload_bytes[sv] + h.chunk_bytes - 1) / h.chunk_bytes);
-    if ((s = launch_inflate_sections(ib, sec_off_dev, h.payload_bytes[0], nch[0], w.payloads[0], sec_off_dev + 1,
-                                     h.payload_bytes[1], nch[1], w.payloads[1], w.err, st)))
-      return s;
+  KVTC_CUDA_TRY(cudaMemsetAsync(w.err, 0, 16, st));
+  KVTC_CUDA_TRY(cudaMemsetAsync(w.hsum, 0, 32, st));
+  if (h.m) {
+    if ((s = enqueue_inflate(ib, h, w, st))) return s;
+    ProfScope ps("d.dequant", st);
+    for (int sv = 0; sv < 2; ++sv) {
+      kvtc_plan *pl = const_cast<kvtc_plan *>(sv ? vp : kp);
+      if ((s = launch_dequant(pl->d_pgroups, pl->d_codes_off_full, pl->G, plan_codes_off_last(pl, h.m % kTileM),
+                              pl->tile_bytes, w.payloads[sv], h.m, w.Dh[sv], w.ld, st)))
+        return s;
+      if (pl->r_nz == 0) KVTC_CUDA_TRY(cudaMemsetAsync(w.Dh[sv], 0, h.m * w.ld * 2, st));
+    }
+    if (kb->has_rope && (s = rope_table_for(kb, h.pos0 + h.sinks, h.m, w.cs, st))) return s;
   }
-  ProfScope ps("d.dequant", st);
-  for (int sv = 0; sv < 2; ++sv) {
-    kvtc_plan *pl = const_cast<kvtc_plan *>(sv ? vp : kp);
-    if ((s = launch_dequant(pl->d_pgroups, pl->d_codes_off_full, pl->G, plan_codes_off_last(pl, h.m % kTileM),
-                            pl->tile_bytes, w.payloads[sv], h.m, w.Dh[sv], w.ld, st)))
-      return s;
-    if (pl->r_nz == 0) KVTC_CUDA_TRY(cudaMemsetAsync(w.Dh[sv], 0, h.m * w.ld * 2, st));
-  }
-  if (kb->has_rope && (s = rope_table_for(kb, h.pos0 + h.sinks, h.m, w.cs, st))) return s;
-  return KVTC_OK;
+  if ((s = enqueue_checks(ib, h, w, st, 0)) || (s = enqueue_status(w, nullptr, st))) return s;
+  return read_status(w, st);
 }
 
 extern "C" kvtc_status kvtc_decompress_layers(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb,
@@ -1027,13 +1147,14 @@ extern "C" size_t kvtc_compress_batch_workspace_bytes(const kvtc_basis *kb, cons
     b.take<uint8_t>(deflate_workspace(L.pay[0], pol->chunk_bytes));
     b.take<uint8_t>(deflate_workspace(L.pay[1], pol->chunk_bytes));
   }
-  b.take<uint64_t>(4 * int64_t(n));
+  b.take<uint64_t>(kCompressWords * int64_t(n));
   b.take<__nv_bfloat16>(rows * (kb->p + kXPad));
   b.take<__nv_bfloat16>(rows * (kb->p + kXPad));
   b.take<float2>(rows * (kb->shape.head_dim / 2));
   b.take<float>(rows * std::max(kp->wide_cols, vp->wide_cols));
   b.take<TileRef>(2 * (rows / kTileM));
   b.take<EncodeJob>(2 * int64_t(n));
+  b.take<HashJob>(3 * int64_t(n));
   return b.used + 256;
 }
 
@@ -1089,17 +1210,20 @@ extern "C" kvtc_status kvtc_compress_batch(const kvtc_basis *kb, const kvtc_plan
     dws_k[i] = ws.take<uint8_t>(deflate_workspace(it[i].L.pay[0], pol->chunk_bytes));
     dws_v[i] = ws.take<uint8_t>(deflate_workspace(it[i].L.pay[1], pol->chunk_bytes));
   }
-  uint64_t *lens = ws.take<uint64_t>(4 * int64_t(n));            // per item: K len, V len, K off, V off
+  uint64_t *lens = ws.take<uint64_t>(kCompressWords * int64_t(n));   // per item: see kCompressWords
   auto *X = ws.take<__nv_bfloat16>(rows * ldx);
   auto *X2 = ws.take<__nv_bfloat16>(rows * ldx);          // the values' rows (gathered beside the keys' GEMM)
   float2 *cs = ws.take<float2>(rows * half);
   float *wide = ws.take<float>(rows * std::max(kp->wide_cols, vp->wide_cols));
   TileRef *d_tiles = ws.take<TileRef>(2 * ntiles);
   EncodeJob *d_jobs = ws.take<EncodeJob>(2 * int64_t(n));
+  HashJob *d_hjobs = ws.take<HashJob>(3 * int64_t(n));            // raw sections, K payloads, V payloads
 
   // raw tokens, headers' host part, section offsets
   std::vector<ContainerHeader> hdr(n);
-  std::vector<uint64_t> offs(4 * int64_t(n), 0);
+  std::vector<uint64_t> offs(kCompressWords * int64_t(n), 0);
+  std::vector<HashJob> hjobs(3 * int64_t(n));
+  uint64_t max_raw = 0, max_pay[2] = {0, 0};
   for (int i = 0; i < n; ++i) {
     if ((s = upload_bases(&k[i], kbases[i], st)) || (s = upload_bases(&v[i], vbases[i], st))) return s;
     const CompressLayout &L = it[i].L;
@@ -1125,7 +1249,7 @@ extern "C" kvtc_status kvtc_compress_batch(const kvtc_basis *kb, const kvtc_plan
     h.plan_fp[1] = vp->fp;
     h.raw_off = KVTC_HEADER_BYTES;
     h.section_off[0] = L.k_off;
-    offs[4 * i + 2] = L.k_off;
+    offs[kCompressWords * i + 2] = L.k_off;
     uint8_t *o = static_cast<uint8_t *>(out_host[i]);
     const int64_t hd = int64_t(k[i].shape.kv_heads) * k[i].shape.head_dim;
     auto *rawk = reinterpret_cast<__nv_bfloat16 *>(o + KVTC_HEADER_BYTES);
@@ -1143,8 +1267,16 @@ extern "C" kvtc_status kvtc_compress_batch(const kvtc_basis *kb, const kvtc_plan
       if ((s = launch_pack_raw(k[i], kbases[i], 0, t, rawk, L.nraw, 0, st))) return s;
       if ((s = launch_pack_raw(v[i], vbases[i], 0, t, rawv, L.nraw, 0, st))) return s;
     }
+    uint64_t *li = lens + kCompressWords * i;
+    hjobs[i] = HashJob{reinterpret_cast<const uint8_t *>(rawk), uint64_t(L.raw_bytes), kSeedRaw, li + 7};
+    for (int sv = 0; sv < 2; ++sv)
+      hjobs[(1 + sv) * int64_t(n) + i] = HashJob{sv ? pay_v[i] : pay_k[i], L.pay[sv], kSeedPayload, li + 5 + sv};
+    max_raw = std::max<uint64_t>(max_raw, L.raw_bytes);
+    for (int sv = 0; sv < 2; ++sv) max_pay[sv] = std::max<uint64_t>(max_pay[sv], L.m ? L.pay[sv] : 0);
   }
   KVTC_CUDA_TRY(cudaMemcpyAsync(lens, offs.data(), offs.size() * 8, cudaMemcpyHostToDevice, st));
+  KVTC_CUDA_TRY(cudaMemcpyAsync(d_hjobs, hjobs.data(), hjobs.size() * sizeof(HashJob), cudaMemcpyHostToDevice, st));
+  if ((s = launch_hash_batch(d_hjobs, n, max_raw, st))) return s;
   // tile tables: keys [0, ntiles), values [ntiles, 2 ntiles)
   std::vector<TileRef> tref(2 * ntiles);
   for (int i = 0; i < n; ++i) {
@@ -1157,6 +1289,7 @@ extern "C" kvtc_status kvtc_compress_batch(const kvtc_basis *kb, const kvtc_plan
         r.payload = (sv ? pay_v[i] : pay_k[i]) + j * pl->tile_bytes;
         r.codes_off = plan_codes_off_last(pl, ntok);
         r.ntok = ntok;
+        r.status = reinterpret_cast<int32_t *>(lens + kCompressWords * i + 4);
         if (!r.codes_off) {
           set_error("code offsets: allocation failed");
           return KVTC_E_NOMEM;
@@ -1227,6 +1360,7 @@ extern "C" kvtc_status kvtc_compress_batch(const kvtc_basis *kb, const kvtc_plan
     KVTC_CUDA_TRY(cudaStreamWaitEvent(aux, ss->ev[2], 0));
     {
       ProfScope ps(ovl ? "cb.deflate_overlapped" : "cb.deflate", aux);
+      if ((s = launch_hash_batch(d_hjobs + n, n, max_pay[0], aux, ovl ? corun_ctas(2) : 0))) return s;
       if (!jobs[0].empty() &&
           (s = launch_deflate_encode_batch(d_jobs, int32_t(jobs[0].size()), nchunks[0], pol->chunk_bytes, aux,
                                            ovl ? corun_ctas(2) : 0)))
@@ -1234,6 +1368,7 @@ extern "C" kvtc_status kvtc_compress_batch(const kvtc_basis *kb, const kvtc_plan
     }
     {
       ProfScope ps("cb.deflate", st);
+      if ((s = launch_hash_batch(d_hjobs + 2 * int64_t(n), n, max_pay[1], st))) return s;
       if (!jobs[1].empty() &&
           (s = launch_deflate_encode_batch(d_jobs + n, int32_t(jobs[1].size()), nchunks[1], pol->chunk_bytes, st)))
         return s;
@@ -1245,26 +1380,34 @@ extern "C" kvtc_status kvtc_compress_batch(const kvtc_basis *kb, const kvtc_plan
     ProfScope ps("cb.assemble", st);
     for (int i = 0; i < n; ++i) {
       uint8_t *o = static_cast<uint8_t *>(out_host[i]);
+      uint64_t *li = lens + kCompressWords * i;
       if (!it[i].L.m) {
-        header_kernel<<<1, 1, 0, st>>>(hdr[i], o, nullptr, nullptr);
+        header_kernel<<<1, 1, 0, st>>>(hdr[i], o, nullptr, li);
         KVTC_LAUNCH_CHECK();
         continue;
       }
-      uint64_t *li = lens + 4 * i;
       if ((s = launch_deflate_assemble(it[i].L.pay[0], pol->chunk_bytes, dws_k[i], o, li + 2, li + 0, st))) return s;
       offset_after_kernel<<<1, 1, 0, st>>>(li + 2, li + 0, li + 3, o);
       KVTC_LAUNCH_CHECK();
       if ((s = launch_deflate_assemble(it[i].L.pay[1], pol->chunk_bytes, dws_v[i], o, li + 3, li + 1, st))) return s;
-      header_kernel<<<1, 1, 0, st>>>(hdr[i], o, li, li + 2);
+      header_kernel<<<1, 1, 0, st>>>(hdr[i], o, li, li);
       KVTC_LAUNCH_CHECK();
     }
   }
   if (out_len_host) {
-    std::vector<uint64_t> l(4 * int64_t(n));
+    std::vector<uint64_t> l(kCompressWords * int64_t(n));
     KVTC_CUDA_TRY(cudaMemcpyAsync(l.data(), lens, l.size() * 8, cudaMemcpyDeviceToHost, st));
     KVTC_CUDA_TRY(cudaStreamSynchronize(st));
-    for (int i = 0; i < n; ++i)
-      out_len_host[i] = it[i].L.m ? size_t(l[4 * i + 3] + l[4 * i + 1]) : size_t(KVTC_HEADER_BYTES + it[i].L.raw_bytes);
+    int bad = -1;
+    for (int i = 0; i < n; ++i) {
+      const uint64_t *li = l.data() + kCompressWords * i;
+      out_len_host[i] = it[i].L.m ? size_t(li[3] + li[1]) : size_t(KVTC_HEADER_BYTES + it[i].L.raw_bytes);
+      if ((li[4] & 1) && bad < 0) bad = i;
+    }
+    if (bad >= 0) {
+      set_error("batch item %d: a 16-bit shift/scale overflowed (container flagged)", bad);
+      return KVTC_E_NUMERIC;
+    }
   }
   return KVTC_OK;
 }
@@ -1278,6 +1421,7 @@ extern "C" size_t kvtc_decompress_batch_workspace_bytes(const kvtc_basis *kb, co
   for (int i = 0; i < n; ++i) {
     ContainerHeader h;
     memcpy(&h, in_header_host[i], sizeof(h));
+    if (validate_header(h) != KVTC_OK) return 0;   // the call itself reports why
     rows += (h.m + kTileM - 1) / kTileM * kTileM;
     b.take<void *>(h.layers);
     b.take<void *>(h.layers);
@@ -1291,6 +1435,10 @@ extern "C" size_t kvtc_decompress_batch_workspace_bytes(const kvtc_basis *kb, co
   b.take<float2>(rows * (kb->shape.head_dim / 2));
   b.take<TileRef>(2 * (rows / kTileM));
   b.take<InflateJob>(2 * int64_t(n));
+  b.take<int32_t>(n);
+  b.take<uint64_t>(3 * int64_t(n));
+  b.take<uint64_t>(3 * int64_t(n));
+  b.take<HashJob>(3 * int64_t(n));
   return b.used + 256;
 }
 
@@ -1313,29 +1461,19 @@ extern "C" kvtc_status kvtc_decompress_batch(const kvtc_basis *kb, const kvtc_pl
   std::vector<const void *> hptr(n);
   int64_t row = 0;
   for (int i = 0; i < n; ++i) {
-    const ContainerHeader &h = hdr[i];
-    kvtc_container_info info;
-    if ((s = kvtc_container_parse(&h, &info))) return s;
+    ContainerHeader h;
+    if ((s = read_checked_header(kb, kp, vb, vp, &hdr[i], in_len_host[i], &h))) {
+      const std::string msg = kvtc_last_error();
+      set_error("batch item %d: %s", i, msg.c_str());
+      return s;
+    }
+    KVTC_CHECK_ARG((reinterpret_cast<uintptr_t>(in_host[i]) & 15) == 0, "containers must be 16-byte aligned");
     if ((s = check_view(&k_out[i])) || (s = check_view(&v_out[i]))) return s;
     const kvtc_shape shp{h.layers, h.kv_heads, h.head_dim};
     if (!same_shape(shp, k_out[i].shape) || !same_shape(shp, v_out[i].shape) || k_out[i].tokens != h.tokens ||
-        v_out[i].tokens != h.tokens || !same_shape(shp, kb->shape) || !same_shape(shp, vb->shape)) {
-      set_error("batch item %d: container shape does not match the output views / bases", i);
+        v_out[i].tokens != h.tokens) {
+      set_error("batch item %d: container shape does not match the output views", i);
       return KVTC_E_MISMATCH;
-    }
-    if (h.basis_fp[0] != kb->fp || h.basis_fp[1] != vb->fp || h.plan_fp[0] != kp->fp || h.plan_fp[1] != vp->fp) {
-      set_error("batch item %d: container was written with a different basis or plan", i);
-      return KVTC_E_MISMATCH;
-    }
-    if (info.total_bytes > in_len_host[i]) {
-      set_error("batch item %d: container length %llu > buffer %zu", i, (unsigned long long)info.total_bytes,
-                in_len_host[i]);
-      return KVTC_E_CORRUPT;
-    }
-    if (h.m && (h.payload_bytes[0] != kvtc_payload_bytes(kp, h.m) ||
-                h.payload_bytes[1] != kvtc_payload_bytes(vp, h.m))) {
-      set_error("batch item %d: payload sizes do not match the plans", i);
-      return KVTC_E_CORRUPT;
     }
     it[i].row0 = row;
     it[i].tiles = (h.m + kTileM - 1) / kTileM;
@@ -1365,7 +1503,32 @@ extern "C" kvtc_status kvtc_decompress_batch(const kvtc_basis *kb, const kvtc_pl
   float2 *cs = ws.take<float2>(rows * half);
   TileRef *d_tiles = ws.take<TileRef>(2 * ntiles);
   InflateJob *d_jobs = ws.take<InflateJob>(2 * int64_t(n));
+  int32_t *ierr = ws.take<int32_t>(n);                             // per item: checksum mismatch bits
+  uint64_t *hsum = ws.take<uint64_t>(3 * int64_t(n));              // [raw | K payload | V payload] per item
+  uint64_t *hexp = ws.take<uint64_t>(3 * int64_t(n));
+  HashJob *d_hj = ws.take<HashJob>(3 * int64_t(n));
   KVTC_CUDA_TRY(cudaMemsetAsync(err, 0, 4, st));
+  KVTC_CUDA_TRY(cudaMemsetAsync(ierr, 0, 4 * size_t(n), st));
+  KVTC_CUDA_TRY(cudaMemsetAsync(hsum, 0, 24 * size_t(n), st));
+  {
+    // checksum jobs, item-major: j = 3 i + {0 raw, 1 K payload, 2 V payload}; items
+    // without middle tokens compare their (empty) payloads against themselves
+    std::vector<HashJob> hj(3 * int64_t(n));
+    std::vector<uint64_t> ex(3 * int64_t(n));
+    for (int i = 0; i < n; ++i) {
+      const ContainerHeader &h = hdr[i];
+      const uint8_t *ib = static_cast<const uint8_t *>(in_host[i]);
+      hj[3 * i] = HashJob{ib + h.raw_off, h.raw_bytes, kSeedRaw, hsum + 3 * i};
+      ex[3 * i] = h.raw_hash;
+      for (int sv = 0; sv < 2; ++sv) {
+        hj[3 * i + 1 + sv] = HashJob{sv ? pay_v[i] : pay_k[i], h.m ? h.payload_bytes[sv] : 0, kSeedPayload,
+                                     hsum + 3 * i + 1 + sv};
+        ex[3 * i + 1 + sv] = h.m ? h.payload_hash[sv] : host_hash(nullptr, 0, kSeedPayload);
+      }
+    }
+    KVTC_CUDA_TRY(cudaMemcpyAsync(d_hj, hj.data(), hj.size() * sizeof(HashJob), cudaMemcpyHostToDevice, st));
+    KVTC_CUDA_TRY(cudaMemcpyAsync(hexp, ex.data(), ex.size() * 8, cudaMemcpyHostToDevice, st));
+  }
   for (int i = 0; i < n; ++i)
     if ((s = upload_bases(&k_out[i], kbases[i], st)) || (s = upload_bases(&v_out[i], vbases[i], st))) return s;
   // every section of every item: one inflate launch
@@ -1379,6 +1542,7 @@ extern "C" kvtc_status kvtc_decompress_batch(const kvtc_basis *kb, const kvtc_pl
         if (!h.m || h.payload_bytes[sv] == 0) continue;
         InflateJob j{};
         j.section = static_cast<const uint8_t *>(in_host[i]) + h.section_off[sv];
+        j.sec_len = h.entropy_bytes[sv];
         j.n_out = h.payload_bytes[sv];
         j.nch = uint32_t((h.payload_bytes[sv] + h.chunk_bytes - 1) / h.chunk_bytes);
         j.chunk0 = c0;
@@ -1414,6 +1578,14 @@ extern "C" kvtc_status kvtc_decompress_batch(const kvtc_basis *kb, const kvtc_pl
   }
   if (ntiles)
     KVTC_CUDA_TRY(cudaMemcpyAsync(d_tiles, tref.data(), tref.size() * sizeof(TileRef), cudaMemcpyHostToDevice, st));
+  uint64_t max_n = 0;
+  for (int i = 0; i < n; ++i)
+    max_n = std::max<uint64_t>(max_n, std::max(hdr[i].raw_bytes, std::max(hdr[i].payload_bytes[0], hdr[i].payload_bytes[1])));
+  auto run_checks = [&](cudaStream_t q, int ctas) -> kvtc_status {
+    kvtc_status r = launch_hash_batch(d_hj, 3 * n, max_n, q, ctas);
+    if (r) return r;
+    return launch_hash_check_batch(hsum, hexp, 3 * n, 3, ierr, q);
+  };
   auto dequant_all = [&](int sv, cudaStream_t q, int ctas) -> kvtc_status {
     kvtc_plan *pl = const_cast<kvtc_plan *>(sv ? vp : kp);
     for (int i = 0; i < n; ++i) {
@@ -1455,9 +1627,14 @@ extern "C" kvtc_status kvtc_decompress_batch(const kvtc_basis *kb, const kvtc_pl
         ProfScope ps(ovl ? "db.dequant_overlapped" : "db.dequant", aux);
         if ((s = dequant_all(1, aux, ovl ? corun_ctas(2) : 0))) return s;
       }
+      {
+        ProfScope ps(ovl ? "db.checksum_overlapped" : "db.checksum", aux);
+        if ((s = run_checks(aux, ovl ? corun_ctas(2) : 0))) return s;
+      }
       KVTC_CUDA_TRY(cudaEventRecord(ss->ev[3], aux));
     }
   }
+  if (!ntiles && (s = run_checks(st, 0))) return s;
   {
     ProfScope ps("db.raw_tokens", st);
     for (int i = 0; i < n; ++i) {
@@ -1481,6 +1658,20 @@ extern "C" kvtc_status kvtc_decompress_batch(const kvtc_basis *kb, const kvtc_pl
       }
     }
   }
+  // one synchronisation: the inflater's and every item's checksum status
+  std::vector<int32_t> st_host(n + 1);
+  KVTC_CUDA_TRY(cudaMemcpyAsync(st_host.data(), err, 4, cudaMemcpyDeviceToHost, st));
+  KVTC_CUDA_TRY(cudaMemcpyAsync(st_host.data() + 1, ierr, 4 * size_t(n), cudaMemcpyDeviceToHost, st));
+  KVTC_CUDA_TRY(cudaStreamSynchronize(st));
+  if (st_host[0]) {
+    set_error("corrupt container in the batch: DEFLATE stream error %d", st_host[0]);
+    return KVTC_E_CORRUPT;
+  }
+  for (int i = 0; i < n; ++i)
+    if (st_host[1 + i]) {
+      set_error("batch item %d: corrupt container (checksum mismatch bits %d)", i, st_host[1 + i]);
+      return KVTC_E_CORRUPT;
+    }
   return KVTC_OK;
 }
 

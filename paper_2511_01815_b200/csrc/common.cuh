@@ -55,6 +55,23 @@ constexpr int kMaxTileN = 256;     // UMMA N limit for cta_group::1, M = 128
 __host__ __device__ inline int bits_of(int t) { return t == KVTC_T_INT2 ? 2 : t == KVTC_T_INT4 ? 4 : t == KVTC_T_FP8 ? 8 : 0; }
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Container checksum terms (integrity.cu): SplitMix64 finaliser of a word keyed
+// by its position.
+__host__ __device__ inline uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__host__ __device__ inline uint64_t hash_term(uint64_t w, uint64_t i, uint64_t seed) {
+  return mix64(w ^ (seed + (i + 1) * 0x9E3779B97F4A7C15ull));
+}
+// Checksum of nw whole 8-byte words (header-sized inputs, one thread).
+__host__ __device__ inline uint64_t hash_words(const uint64_t *w, int nw, uint64_t seed) {
+  uint64_t h = mix64(uint64_t(nw) * 8 ^ seed);
+  for (int i = 0; i < nw; ++i) h += hash_term(w[i], uint64_t(i), seed);
+  return h;
+}
+
 // ------------------------------------------------------------ device PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -840,8 +840,8 @@ struct FastShared {
 };
 
 struct InflateJobs {
-  const uint8_t *base;
-  const uint64_t *off_dev[2];      // device section offsets from base (nullable = 0)
+  const uint8_t *sec[2];           // sections
+  uint64_t sec_len[2];             // bytes the section may occupy (bounds every read)
   uint64_t n_out[2];
   uint32_t nch[2];
   uint8_t *out[2];
@@ -921,22 +921,34 @@ __device__ int parse_header_fast(FastShared &S) {
 }
 
 // Chunk c of the section at `section` (raw size n_out, nch chunks) into out_base.
-__device__ __forceinline__ void inflate_chunk(FastShared &S, const uint8_t *section, uint64_t n_out, uint32_t nch,
-                                              uint32_t c, uint8_t *out_base, int32_t *err) {
+// Every read is bounded by sec_len (the section's extent in the container, known
+// to the host): a damaged header, chunk table, index or stream sets *err (the
+// caller reports KVTC_E_CORRUPT) and never reads outside the section.
+__device__ __forceinline__ void inflate_chunk(FastShared &S, const uint8_t *section, uint64_t sec_len, uint64_t n_out,
+                                              uint32_t nch, uint32_t c, uint8_t *out_base, int32_t *err) {
   const SectionHeader *hdr = reinterpret_cast<const SectionHeader *>(section);
   const int tid = threadIdx.x;
-  if (hdr->magic != kSectionMagic || hdr->version != kSectionVersion || hdr->raw_bytes != n_out ||
-      hdr->nchunks != nch || hdr->nseg != kNSeg || hdr->seg_bytes * kNSeg != hdr->chunk_bytes ||
-      hdr->seg_bytes % 16) {
+  const uint64_t data_off =
+      sizeof(SectionHeader) + uint64_t(nch) * sizeof(ChunkEntry) + ((uint64_t(nch) * kNSeg * 2 + 15) & ~15ull);
+  if (sec_len < data_off || hdr->magic != kSectionMagic || hdr->version != kSectionVersion ||
+      hdr->raw_bytes != n_out || hdr->nchunks != nch || hdr->nseg != kNSeg ||
+      hdr->seg_bytes * kNSeg != hdr->chunk_bytes || hdr->seg_bytes % 16 || hdr->data_offset != data_off ||
+      hdr->section_bytes > sec_len || hdr->chunk_bytes == 0 ||
+      uint64_t(nch) != (n_out + hdr->chunk_bytes - 1) / hdr->chunk_bytes) {
     if (tid == 0) atomicExch(err, -20);
     return;
   }
   const ChunkEntry e = reinterpret_cast<const ChunkEntry *>(section + sizeof(SectionHeader))[c];
-  const uint16_t *index =
-      reinterpret_cast<const uint16_t *>(section + sizeof(SectionHeader) + uint64_t(hdr->nchunks) * sizeof(ChunkEntry));
-  const uint8_t *stream = section + hdr->data_offset + e.offset;
   const uint64_t obase = uint64_t(c) * hdr->chunk_bytes;
   const uint32_t nc = uint32_t(umin64(hdr->chunk_bytes, hdr->raw_bytes - obase));
+  if (e.kind > 1 || (e.offset & 15) || e.offset + ((uint64_t(e.bytes) + 15) & ~15ull) > hdr->section_bytes - data_off ||
+      (e.kind == 1 && e.bytes < stored_bytes(nc))) {
+    if (tid == 0) atomicExch(err, -21);
+    return;
+  }
+  const uint16_t *index =
+      reinterpret_cast<const uint16_t *>(section + sizeof(SectionHeader) + uint64_t(hdr->nchunks) * sizeof(ChunkEntry));
+  const uint8_t *stream = section + data_off + e.offset;
   uint8_t *o = out_base + obase;
   if (e.kind == 1) {
     for (uint32_t i = tid; i < nc; i += kInfThreads) o[i] = stream[(i / 32768) * (32768 + 5) + 5 + (i % 32768)];
@@ -1060,6 +1072,17 @@ __device__ __forceinline__ void inflate_chunk(FastShared &S, const uint8_t *sect
     if (((i - s0) & 7) == 0) advance();
     o[i] = uint8_t(decode());
   }
+  if (s1 == nc) {                            // the chunk's last segment ends with the end-of-block code
+    advance();
+    const uint32_t w = bp >> 5;
+    const uint32_t bits = __funnelshift_r(word(w), word(w + 1), bp & 31);
+    uint32_t te = S.table[bits & ((1u << kTabBits) - 1)];
+    if (te & 0x8000) te = S.sub[((te & 0x7FFF) << kSubBits) | ((bits >> kTabBits) & ((1u << kSubBits) - 1))];
+    if ((te & 0x5000) != 0x1000) bad |= 0x4000;
+    bp += te & 15;
+  }
+  // each segment must end exactly where the side index says, inside the stream
+  if (uint64_t(bp) != pos + mylen || uint64_t(bp) > uint64_t(e.bytes) * 8) bad |= 0x4000;
   if (bad & 0x5000) atomicExch(err, -7);
   asm volatile("cp.async.wait_all;" ::: "memory");   // no copy may land in the next chunk's header
 }
@@ -1072,7 +1095,7 @@ __global__ void __launch_bounds__(kInfThreads) inflate_fast_kernel(InflateJobs J
   for (uint32_t b = blockIdx.x; b < total; b += gridDim.x) {
     const int job = b < J.nch[0] ? 0 : 1;
     const uint32_t c = job == 0 ? b : b - J.nch[0];
-    inflate_chunk(S, J.base + (J.off_dev[job] ? *J.off_dev[job] : 0), J.n_out[job], J.nch[job], c, J.out[job], err);
+    inflate_chunk(S, J.sec[job], J.sec_len[job], J.n_out[job], J.nch[job], c, J.out[job], err);
     __syncthreads();
   }
 }
@@ -1090,7 +1113,7 @@ __global__ void __launch_bounds__(kInfThreads) inflate_batch_kernel(const Inflat
       else hi = mid - 1;
     }
     const InflateJob jb = jobs[lo];
-    inflate_chunk(S, jb.section, jb.n_out, jb.nch, b - jb.chunk0, jb.out, err);
+    inflate_chunk(S, jb.section, jb.sec_len, jb.n_out, jb.nch, b - jb.chunk0, jb.out, err);
     __syncthreads();
   }
 }
@@ -1104,13 +1127,14 @@ kvtc_status launch_inflate_batch(const InflateJob *jobs_dev, int32_t njobs, uint
   return KVTC_OK;
 }
 
-kvtc_status launch_inflate_sections(const uint8_t *base, const uint64_t *off_dev0, uint64_t n0, uint32_t nch0,
-                                    uint8_t *out0, const uint64_t *off_dev1, uint64_t n1, uint32_t nch1,
-                                    uint8_t *out1, int32_t *err, cudaStream_t st, int32_t max_ctas) {
+kvtc_status launch_inflate_sections(const uint8_t *sec0, uint64_t len0, uint64_t n0, uint32_t nch0, uint8_t *out0,
+                                    const uint8_t *sec1, uint64_t len1, uint64_t n1, uint32_t nch1, uint8_t *out1,
+                                    int32_t *err, cudaStream_t st, int32_t max_ctas) {
   InflateJobs J;
-  J.base = base;
-  J.off_dev[0] = off_dev0;
-  J.off_dev[1] = off_dev1;
+  J.sec[0] = sec0;
+  J.sec[1] = sec1;
+  J.sec_len[0] = len0;
+  J.sec_len[1] = len1;
   J.n_out[0] = n0;
   J.n_out[1] = n1;
   J.nch[0] = nch0;
@@ -1125,9 +1149,9 @@ kvtc_status launch_inflate_sections(const uint8_t *base, const uint64_t *off_dev
   return KVTC_OK;
 }
 
-kvtc_status launch_inflate_section(const uint8_t *base, const uint64_t *off_dev, uint64_t n_out, uint32_t nchunks,
-                                   uint8_t *out, int32_t *err, cudaStream_t st, int32_t max_ctas) {
-  return launch_inflate_sections(base, off_dev, n_out, nchunks, out, nullptr, 0, 0, nullptr, err, st, max_ctas);
+kvtc_status launch_inflate_section(const uint8_t *sec, uint64_t len, uint64_t n_out, uint32_t nchunks, uint8_t *out,
+                                   int32_t *err, cudaStream_t st, int32_t max_ctas) {
+  return launch_inflate_sections(sec, len, n_out, nchunks, out, nullptr, 0, 0, 0, nullptr, err, st, max_ctas);
 }
 
 // Validates a section header (host copy) against the expected payload size.

@@ -295,12 +295,15 @@ kvtc_status dp_run(const float *P, int64_t n, int32_t r, int64_t B, const kvtc_d
   }
   KVTC_CHECK_ARG(int(sizes_h.size()) <= kMaxSizes, "too many group sizes");
   int maxsize = 0;
+  const uint32_t mask = (cfg && cfg->type_mask) ? (cfg->type_mask | 1u) : 0xFu;
   for (int s : sizes_h) {
     KVTC_CHECK_ARG(s >= 1 && s <= 1024, "group sizes must be in [1, 1024]");
+    for (int t = KVTC_T_INT2; t <= KVTC_T_FP8; ++t)
+      KVTC_CHECK_ARG(!((mask >> t) & 1) || group_size_supported(s, bits_of(t)),
+                     "group size unsupported by the codec kernels for an allowed type (see kvtc_plan_create)");
     maxsize = std::max(maxsize, s);
   }
   maxsize = std::min(maxsize, r);
-  const uint32_t mask = (cfg && cfg->type_mask) ? (cfg->type_mask | 1u) : 0xFu;
   const int nsz = int(sizes_h.size());
   // ---- K7
   DPParams prm = {};

@@ -277,7 +277,7 @@ __device__ __forceinline__ float4 load4(const float *p, bool vec) {
 __global__ void __launch_bounds__(128) quant_wide_kernel(const WideDesc *wide, const float *D, int64_t ldd,
                                                          int use_wcol, int64_t m, int64_t tile_bytes,
                                                          const int64_t *codes_off_last, uint8_t *payload,
-                                                         const TileRef *tiles) {
+                                                         const TileRef *tiles, int32_t *status) {
   const WideDesc wd = wide[blockIdx.x];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t m0 = int64_t(blockIdx.y) * kTileM;
@@ -310,6 +310,8 @@ __global__ void __launch_bounds__(128) quant_wide_kernel(const WideDesc *wide, c
     if (lane == 0) {
       uint8_t *pp = tile_base + 4 * (int64_t(wd.gidx) * ntok + r);
       store_u32_any(pp, uint32_t(sh) | (uint32_t(sc) << 16), (reinterpret_cast<uintptr_t>(pp) & 3) == 0);
+      int32_t *stw = tref ? tref->status : status;
+      if (stw && factor_overflow(sh, sc)) atomicOr(stw, 1);
     }
     uint8_t *dst = cb + int64_t(r) * tok_bytes;
     const bool al = (reinterpret_cast<uintptr_t>(dst) & 3) == 0;
@@ -329,11 +331,12 @@ __global__ void __launch_bounds__(128) quant_wide_kernel(const WideDesc *wide, c
 
 kvtc_status launch_quant_wide(const WideDesc *wide, int32_t nwide, const float *D, int64_t ldd, int use_wcol,
                               int64_t m, int64_t tile_bytes, const int64_t *codes_off_last, uint8_t *payload,
-                              cudaStream_t st, const TileRef *tiles) {
+                              cudaStream_t st, const TileRef *tiles, int32_t *status) {
   if (nwide == 0 || m == 0) return KVTC_OK;
   dim3 grid(unsigned(nwide), unsigned(ceil_div(m, kTileM)));
   KVTC_MAX_CARVEOUT(quant_wide_kernel);             // may run beside a GEMM (values' wide groups)
-  quant_wide_kernel<<<grid, 128, 0, st>>>(wide, D, ldd, use_wcol, m, tile_bytes, codes_off_last, payload, tiles);
+  quant_wide_kernel<<<grid, 128, 0, st>>>(wide, D, ldd, use_wcol, m, tile_bytes, codes_off_last, payload, tiles,
+                                          status);
   KVTC_LAUNCH_CHECK();
   return KVTC_OK;
 }

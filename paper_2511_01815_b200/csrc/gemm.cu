@@ -97,6 +97,7 @@ struct Params {
   int32_t nsegs;                   // QUANT: number of 256-column segments
   int32_t epi_skip;                // measurement only (KVTC_EPI_SKIP=1): release TMEM without an epilogue
   const TileRef *tiles;            // batched rows (QUANT / RECON), else null
+  int32_t *status;                 // QUANT: bit 0 set when an fp16 shift / scale overflowed (Q4)
 };
 
 __device__ __forceinline__ void cluster_sync_all() {
@@ -600,8 +601,11 @@ __global__ void __launch_bounds__(kThreads, MODE == EPI_RECON ? 1 : 2)
           }
         };
         auto store_params = [&](const GroupDesc &g, uint16_t sh, uint16_t sc) {
-          if (valid && g.part == 0)
+          if (valid && g.part == 0) {
             store_u32_any(tile_base + 4 * (int64_t(g.gidx) * ntok + row), uint32_t(sh) | (uint32_t(sc) << 16), !last);
+            int32_t *stw = tref ? tref->status : P.status;
+            if (factor_overflow(sh, sc) && stw) atomicOr(stw, 1);
+          }
         };
         for (int gi = sdq.g_begin; gi < sdq.g_end;) {
           const GroupDesc gd = P.groups[gi];
@@ -936,6 +940,7 @@ kvtc_status launch_gemm_project_quant(const GemmCompressArgs &a, cudaStream_t st
   p.D = a.D;
   p.ldd = a.ldd;
   p.tiles = a.tiles;
+  p.status = a.status;
   // KVTC_QUANT_NSUB=2: two segments per tile (Cfg<true, 2>, 25 % less L2 traffic);
   // measured slower (tensor pipe 58 % vs 88 %: the 512-column epilogue is not
   // overlapped), so one segment per tile with double-buffered TMEM is the default

@@ -58,6 +58,7 @@ struct TileRef {
   int32_t ntok;                     // valid rows (<= 128)
   int32_t layout, page_tokens;      // decompress: output view layout
   int32_t pad;
+  int32_t *status;                  // compress: the item's status word (Q4 overflow bit), nullable
 };
 
 // Operands of a (basis, plan) pair, compacted to the plan's non-None PCs.
@@ -105,6 +106,7 @@ struct GemmCompressArgs {
   int64_t a_row0;
   int64_t a_layer_rows;    // a_hd > 0 and a_layer_rows > 0: tmA is a 2-D map over [layers * tokens][h*d]
   const TileRef *tiles;    // non-null: batched rows (tile mb -> tiles[mb]); payload / m unused
+  int32_t *status;         // nullable: bit 0 set when an fp16 shift / scale overflowed (Q4)
 };
 kvtc_status launch_gemm_project_f32(const GemmCompressArgs &a, int32_t ncols, cudaStream_t st);
 kvtc_status launch_gemm_project_quant(const GemmCompressArgs &a, cudaStream_t st);
@@ -145,7 +147,7 @@ kvtc_status launch_gather_rows(const kvtc_kv_view *seqs, int32_t nseq, __nv_bflo
 // Wide groups: D [m x ldd] fp32; column of group w = use_wcol ? wcol : col.
 kvtc_status launch_quant_wide(const WideDesc *wide, int32_t nwide, const float *D, int64_t ldd, int use_wcol, int64_t m,
                               int64_t tile_bytes, const int64_t *codes_off_last, uint8_t *payload, cudaStream_t st,
-                              const TileRef *tiles = nullptr);
+                              const TileRef *tiles = nullptr, int32_t *status = nullptr);
 kvtc_status launch_quant_pack_simt(const SegDesc *segs, const GroupDesc *groups, int32_t nsegs, int32_t G,
                                    const float *D, int64_t ldd, int64_t m, int64_t tile_bytes,
                                    const int64_t *codes_off_last, uint8_t *payload, cudaStream_t st);
@@ -205,17 +207,20 @@ int corun_ctas(int per_sm);
                                             true);                                                  \
     (void)kvtc_carveout_set_;                                                                       \
   } while (0)
-kvtc_status launch_inflate_section(const uint8_t *base, const uint64_t *off_dev, uint64_t n_out, uint32_t nchunks,
-                                   uint8_t *out, int32_t *err, cudaStream_t st, int32_t max_ctas = 0);
+// Inflate one section (sec: device pointer, len: bytes the section may occupy;
+// every read stays inside [sec, sec + len)); *err != 0 afterwards = corrupt.
+kvtc_status launch_inflate_section(const uint8_t *sec, uint64_t len, uint64_t n_out, uint32_t nchunks, uint8_t *out,
+                                   int32_t *err, cudaStream_t st, int32_t max_ctas = 0);
 kvtc_status check_section_header(const void *hdr_host, size_t len, size_t n_out, uint32_t *nchunks);
-// Both streams' sections in one launch (warp per chunk); sections at base + *off_dev.
-kvtc_status launch_inflate_sections(const uint8_t *base, const uint64_t *off_dev0, uint64_t n0, uint32_t nch0,
-                                    uint8_t *out0, const uint64_t *off_dev1, uint64_t n1, uint32_t nch1,
-                                    uint8_t *out1, int32_t *err, cudaStream_t st, int32_t max_ctas = 0);
+// Both streams' sections in one launch (two warps per chunk).
+kvtc_status launch_inflate_sections(const uint8_t *sec0, uint64_t len0, uint64_t n0, uint32_t nch0, uint8_t *out0,
+                                    const uint8_t *sec1, uint64_t len1, uint64_t n1, uint32_t nch1, uint8_t *out1,
+                                    int32_t *err, cudaStream_t st, int32_t max_ctas = 0);
 constexpr size_t kSectionHeaderBytes = 64;
 // One section of a batched inflate (device table, chunk0 ascending).
 struct InflateJob {
   const uint8_t *section;
+  uint64_t sec_len;                // bytes the section may occupy
   uint64_t n_out;
   uint32_t nch, chunk0;
   uint8_t *out;
@@ -225,6 +230,27 @@ kvtc_status launch_inflate_batch(const InflateJob *jobs_dev, int32_t njobs, uint
 kvtc_status launch_inflate_raw(const uint8_t *in, const int64_t *in_off, const int64_t *in_len, int32_t n,
                                uint8_t *out, const int64_t *out_off, const int64_t *out_len, int32_t *status,
                                cudaStream_t st);
+
+// integrity.cu: 64-bit container checksums (see the file header).  launch_hash
+// ADDS the checksum of [p, p + n) (p 16-byte aligned) to *out (zero it first);
+// launch_hash_check ORs `bit` into *status when *got != expect.
+constexpr uint64_t kSeedPayload = 0x4B5654432D504159ull, kSeedRaw = 0x4B5654432D524157ull,
+                   kSeedHeader = 0x4B5654432D484452ull;
+uint64_t host_hash(const void *data, size_t n, uint64_t seed);
+kvtc_status launch_hash(const void *p, uint64_t n, uint64_t seed, uint64_t *out, cudaStream_t st,
+                        int32_t max_ctas = 0);
+kvtc_status launch_hash_check(const uint64_t *got, uint64_t expect, int32_t bit, int32_t *status, cudaStream_t st);
+// Batched: job j adds the checksum of [p, p + n) to *out (device table).
+struct HashJob {
+  const uint8_t *p;
+  uint64_t n, seed;
+  uint64_t *out;
+};
+kvtc_status launch_hash_batch(const HashJob *jobs_dev, int32_t njobs, uint64_t max_n, cudaStream_t st,
+                              int32_t max_ctas = 0);
+// status[j / per] |= bit_of(j % per) for every j with got[j] != expect[j] (device arrays).
+kvtc_status launch_hash_check_batch(const uint64_t *got, const uint64_t *expect, int32_t njobs, int32_t per,
+                                   int32_t *status, cudaStream_t st);
 
 // Stage timing (kvtc_profile_*): records an event pair around a scope when enabled.
 struct ProfScope {

@@ -28,6 +28,11 @@ __device__ __forceinline__ void group_factors(int type, float mn, float mx, uint
     sc = f16_bits_f32(__fdiv_rn(__fsub_rn(mx, mn), L));
   }
 }
+// Q4: a 16-bit factor that is not finite (exponent field all ones: inf or NaN)
+// means the coefficient range overflowed binary16 -> KVTC_E_NUMERIC.
+__device__ __forceinline__ bool factor_overflow(uint16_t sh, uint16_t sc) {
+  return (sh & 0x7C00u) == 0x7C00u || (sc & 0x7C00u) == 0x7C00u;
+}
 __device__ __forceinline__ uint32_t encode_one(int type, float x, float shift, float scale) {
   if (scale == 0.0f) return 0u;
   const float y = __fdiv_rn(__fsub_rn(x, shift), scale);

@@ -13,7 +13,7 @@ import numpy as np
 import torch
 
 from . import _lib as L
-from ._lib import check, lib
+from ._lib import KvtcError, check, lib  # noqa: F401  (KvtcError: the status-carrying exception)
 
 
 def _stream(stream=None):
@@ -277,11 +277,25 @@ def decompress(kb: Basis, kp: Plan, vb: Basis, vp: Plan, container: torch.Tensor
                layer_begin: int = 0, layer_end: int | None = None, stream=None, workspace=None):
     layer_end = k_out.shape[0] if layer_end is None else layer_end
     if workspace is None:
-        hdr = container[: L.HEADER_BYTES].cpu().numpy().tobytes()
+        hdr = container[: L.HEADER_BYTES].cpu().numpy().tobytes().ljust(L.HEADER_BYTES, b"\0")
         workspace = torch.empty(decompress_workspace_bytes(kb, kp, vb, vp, hdr), dtype=torch.uint8, device="cuda")
     check(lib().kvtc_decompress(kb.h, kp.h, vb.h, vp.h, _ptr(container), container.numel(), layer_begin, layer_end,
                                 C.byref(k_out.c), C.byref(v_out.c), _ptr(workspace), workspace.numel(),
                                 _stream(stream)))
+
+
+def decompress_async(kb: Basis, kp: Plan, vb: Basis, vp: Plan, container: torch.Tensor, header: bytes,
+                     k_out: KVView, v_out: KVView, status: torch.Tensor, layer_begin: int = 0,
+                     layer_end: int | None = None, stream=None, workspace=None):
+    """kvtc_decompress_async: no host synchronisation; the integrity verdict
+    (0 or KVTC_E_CORRUPT) lands in status (device int32 [1]) on the stream."""
+    layer_end = k_out.shape[0] if layer_end is None else layer_end
+    if workspace is None:
+        workspace = torch.empty(decompress_workspace_bytes(kb, kp, vb, vp, header), dtype=torch.uint8, device="cuda")
+    assert status.dtype == torch.int32 and status.is_cuda
+    check(lib().kvtc_decompress_async(kb.h, kp.h, vb.h, vp.h, _ptr(container), container.numel(),
+                                      C.c_char_p(header), layer_begin, layer_end, C.byref(k_out.c), C.byref(v_out.c),
+                                      _ptr(status), _ptr(workspace), workspace.numel(), _stream(stream)))
 
 
 # ------------------------------------------------- layer-streamed decompression

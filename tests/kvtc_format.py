@@ -7,7 +7,7 @@ import struct
 import numpy as np
 
 SECTION_HDR = struct.Struct("<IIQIIIIQQ16x")
-CONTAINER_HDR = struct.Struct("<II6iqqqQQ2Q2Q2Q2QQ2Q")
+CONTAINER_HDR = struct.Struct("<II6iqqqQQ2Q2Q2Q2QQ2QII2QQ56xQ")
 
 
 def parse_section(buf: bytes):
@@ -27,9 +27,9 @@ def parse_container(buf: bytes):
     f = CONTAINER_HDR.unpack_from(buf, 0)
     names = ["magic", "version", "layers", "kv_heads", "head_dim", "sinks", "window", "chunk_bytes", "tokens", "pos0",
              "m", "total_bytes", "raw_bytes", "pay_k", "pay_v", "ent_k", "ent_v", "bfp_k", "bfp_v", "pfp_k", "pfp_v",
-             "raw_off", "sec_k", "sec_v"]
+             "raw_off", "sec_k", "sec_v", "flags", "reserved", "hash_k", "hash_v", "raw_hash", "header_hash"]
     h = dict(zip(names, f))
-    assert h["magic"] == 0x4354564B
+    assert h["magic"] == 0x4354564B and h["version"] == 2 and CONTAINER_HDR.size == 256
     return h
 
 
