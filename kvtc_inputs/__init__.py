@@ -7,6 +7,8 @@ channel magnitudes, a non-zero mean, sink outliers and RoPE on keys, as
 described in DESIGN.md §5 (recipe) — and the random sample positions the
 calibration step draws, which are passed to both sides as inputs.
 """
-from .synth import SynthSpec, SHAPES, make_spec, generate, sample_positions, lengths_for
+from .synth import (DP_CASES, SHAPES, SynthSpec, dp_coefficients, generate, lengths_for, make_spec,
+                    sample_positions)
 
-__all__ = ["SynthSpec", "SHAPES", "make_spec", "generate", "sample_positions", "lengths_for"]
+__all__ = ["SynthSpec", "SHAPES", "make_spec", "generate", "sample_positions", "lengths_for", "DP_CASES",
+           "dp_coefficients"]

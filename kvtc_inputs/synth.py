@@ -172,3 +172,30 @@ def sample_positions(lengths, n: int, sinks: int = 4, seed: int = 0) -> np.ndarr
     rng = np.random.default_rng(seed)
     idx = rng.choice(len(pool), size=n, replace=False)
     return pool[idx]
+
+
+# DP-parity inputs at production shape (tests/test_gpu_calib_dp.py,
+# scripts/make_dp_golden.py): projected calibration coefficients P [n x r] whose
+# column scales mimic a PCA spectrum.  kind "decay": scale_i = 3 (1 + i)^-0.8
+# plus a per-column offset (as the small DP cases); kind "flat_tail": a head of
+# `head` PCs decaying as 3 / (1 + i) and a flat noise floor `tail` after it, so
+# the optimum spends the leftover budget on 256- / 1024-PC int groups.  fp32.
+DP_CASES = {
+    "decay_b32768": dict(kind="decay", n=128, r=2200, budget=32768, seed=7),
+    "tail_1024": dict(kind="flat_tail", n=64, r=2300, budget=8000, head=200, tail=0.02, seed=1),
+    "tail_256": dict(kind="flat_tail", n=64, r=2300, budget=6000, head=128, tail=0.01, seed=4),
+}
+
+
+def dp_coefficients(kind: str, n: int, r: int, seed: int, head: int = 0, tail: float = 0.0, **_) -> np.ndarray:
+    rng = np.random.default_rng(seed)
+    i = np.arange(r)
+    if kind == "decay":
+        scale = (1.0 + i) ** -0.8 * 3.0
+        P = rng.standard_normal((n, r)) * scale + rng.normal(0, 0.3, (1, r))
+    elif kind == "flat_tail":
+        scale = np.where(i < head, 3.0 * (1.0 + i) ** -1.0, tail)
+        P = rng.standard_normal((n, r)) * scale
+    else:
+        raise KeyError(kind)
+    return P.astype(np.float32)

@@ -71,10 +71,11 @@ def canonical_sq_sum(e) -> float:
 
 
 # ------------------------------------------------------------------- E/Z tables
-def ez_tables(P, sizes=SIZES, types=TYPES):
-    """Z[i, si] = sum x^2 and Q[i, si, ti] = sum (x - x^)^2 over P[:, i-size:i].
-
-    Rows i = 0..r (row 0 unused); NaN where size > i."""
+def ez_tables_loop(P, sizes=SIZES, types=TYPES):
+    """Z[i, si] = sum x^2 and Q[i, si, ti] = sum (x - x^)^2 over P[:, i-size:i],
+    one block at a time (the plain form; ``ez_tables`` evaluates the same
+    expressions for many blocks per NumPy call).  Rows i = 0..r (row 0 unused);
+    NaN where size > i."""
     P = np.asarray(P, dtype=np.float64)
     n, r = P.shape
     Z = np.full((r + 1, len(sizes)), np.nan)
@@ -86,6 +87,49 @@ def ez_tables(P, sizes=SIZES, types=TYPES):
             for ti, t in enumerate(types):
                 xh, _ = simulate_quantization(blk, t)
                 Q[i, si, ti] = canonical_sq_sum(blk - xh)
+    return Z, Q
+
+
+def _tree_sum_rows(v):
+    """tree_sum applied to every column of v [n, k] (rows zero-padded to a
+    power of two, adjacent pairs added level by level)."""
+    n = v.shape[0]
+    k = 1
+    while k < n:
+        k *= 2
+    w = np.zeros((k,) + v.shape[1:])
+    w[:n] = v
+    while w.shape[0] > 1:
+        w = w[0::2] + w[1::2]
+    return w[0]
+
+
+def ez_tables(P, sizes=SIZES, types=TYPES, max_elems: int = 1 << 23):
+    """Same values as ``ez_tables_loop``, bit for bit: every block's quantisation
+    is per row (Q1), so many blocks are stacked as extra rows of one
+    ``quantize_rows`` call; the sums keep the canonical order of Q9 (per row
+    sequential over the block's columns, product then add; across rows the
+    adjacent-pair tree).  Needed for the DP parity at production shape
+    (r ~ 2000+ PCs with 256- and 1024-blocks)."""
+    P = np.asarray(P, dtype=np.float64)
+    n, r = P.shape
+    Z = np.full((r + 1, len(sizes)), np.nan)
+    Q = np.full((r + 1, len(sizes), len(types)), np.nan)
+    for si, s in enumerate(sizes):
+        if s > r:
+            continue
+        ends = np.arange(s, r + 1)
+        step = max(1, max_elems // (n * s))
+        for c0 in range(0, len(ends), step):
+            e = ends[c0:c0 + step]
+            nb = len(e)
+            # blk[row, b, col] = P[row, e[b] - s + col]
+            blk = np.lib.stride_tricks.sliding_window_view(P, s, axis=1)[:, e - s, :]
+            Z[e, si] = _tree_sum_rows(row_sq_sums(blk))
+            flat = blk.reshape(n * nb, s)
+            for ti, t in enumerate(types):
+                xh, _ = simulate_quantization(flat, t)
+                Q[e, si, ti] = _tree_sum_rows(row_sq_sums((flat - xh).reshape(n, nb, s)))
     return Z, Q
 
 

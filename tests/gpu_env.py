@@ -168,3 +168,48 @@ def assert_codes_parity(payload_gpu, groups, D_ref, m, X, basis, cols, label="")
           f"beyond-typical={beyond} per-type={per}")
     assert unexplained == 0 and beyond == 0, (mism, unexplained, beyond, total)
     assert mism <= max(2, 5e-3 * total), (mism, total)
+
+
+def oracle_restore(buf: bytes, kb, okp, vb, ovp, invf):
+    """The oracle's decompression of a GPU container (stock zlib for every chunk,
+    oracle unpack / dequantise / reconstruct / RoPE, raw tokens from the
+    container): (K, V) as fp64 [l, t, h, d].  Parity of the decompress path
+    against the oracle, independent of the GPU's own decompression."""
+    import zlib
+    from oracle import codec as OC
+    from oracle import numerics as ON
+    from oracle import rope as OR
+    from tests.kvtc_format import parse_container, parse_section
+    h = parse_container(buf)
+    l, hh, d, t, s, w, m, pos0 = (h[k] for k in ("layers", "kv_heads", "head_dim", "tokens", "sinks", "window", "m",
+                                                  "pos0"))
+    nraw = s + w if m else t
+    raw = np.frombuffer(buf, dtype="<u2", count=2 * l * nraw * hh * d, offset=256).reshape(2, l, nraw, hh, d)
+    out = []
+    for sv, ob, op in ((0, kb, okp), (1, vb, ovp)):
+        X = np.zeros((l, t, hh, d))
+        rv = ON.bf16_from_bits(raw[sv])
+        if not m:
+            X[:] = rv
+            out.append(X)
+            continue
+        X[:, :s] = rv[:, :s]
+        X[:, t - w:] = rv[:, s:]
+        sec = parse_section(buf[h["sec_k" if sv == 0 else "sec_v"]:])
+        payload = b"".join(zlib.decompress(x, wbits=-15) for x in sec["streams"])
+        Xh = OC.reconstruct_stream(payload, ob, op, m).reshape(m, l, hh, d).transpose(1, 0, 2, 3)
+        pos = pos0 + s + np.arange(m)
+        X[:, s:t - w] = OR.rope_apply_r7(Xh, pos, invf, 0) if sv == 0 else ON.bf16(Xh)
+        out.append(X)
+    return out[0], out[1]
+
+
+def assert_restored_like_oracle(got_k, got_v, ref_k, ref_v, layers=None, tol=1e-3):
+    """GPU output vs oracle_restore: raw tokens are inside ref exactly (bitwise),
+    the whole tensor within tol relative L2 (the rounding points are shared)."""
+    for g, r in ((got_k, ref_k), (got_v, ref_v)):
+        g = g.float().cpu().numpy().astype(np.float64)
+        if layers is not None:
+            g, r = g[layers], r[layers]
+        rel = np.linalg.norm(g - r) / max(np.linalg.norm(r), 1e-30)
+        assert rel < tol, rel

@@ -30,6 +30,14 @@ def art(K):
     return spec, KB, VB, K.Plan.create(kb.r, g), K.Plan.create(vb.r, g)
 
 
+@pytest.fixture(scope="module")
+def oracle_art():
+    from oracle import dp as ODP
+    spec, invf, kb, vb, Ck, Cv = E.setup("mid")
+    g = E.mid_plan_groups()
+    return invf, kb, vb, ODP.Plan(r=kb.r, blocks=list(g)), ODP.Plan(r=vb.r, blocks=list(g))
+
+
 def _caches(lengths, pos0s):
     out = []
     for i, (t, p0) in enumerate(zip(lengths, pos0s)):
@@ -82,7 +90,7 @@ def test_decompress_batch_matches_single(K, art):
         assert torch.equal(gk, rk) and torch.equal(gv, rv), i
 
 
-def test_incremental_ranges(K, art):
+def test_incremental_ranges(K, art, oracle_art):
     """Turn-by-turn compression: every 16 tokens that leave the window
     are compressed as their own range (sinks = window = 0 inside the range),
     for several conversations at once; each range decompresses to exactly what
@@ -111,8 +119,23 @@ def test_incremental_ranges(K, art):
         K.decompress(KB, KP, VB, VP, conts[i], K.KVView(rk, pos0=meta[i][1]), K.KVView(rv, pos0=meta[i][1]))
         torch.cuda.synchronize()
         assert torch.equal(outs[i][0], rk) and torch.equal(outs[i][1], rv), i
-        # and the range is a faithful reconstruction of those tokens
+        # and directly against the oracle: its decompression of the range's container
+        # (s = w = 0: every token coded) and its own compression of the same 16 tokens
+        invf, kb, vb, okp, ovp = oracle_art
         ci, a, b = meta[i]
-        ref = cc[ci][1][:, a:b].float()
-        rel = (outs[i][1].float() - ref).norm() / ref.norm()
-        assert rel < 0.5, rel
+        buf = conts[i].cpu().numpy().tobytes()
+        rk_o, rv_o = E.oracle_restore(buf, kb, okp, vb, ovp, invf)
+        E.assert_restored_like_oracle(outs[i][0], outs[i][1], rk_o, rv_o)
+        from oracle import codec as OC
+        from tests.kvtc_format import parse_container, parse_section
+        import zlib
+        Kr = cc[ci][0][:, a:b].double().cpu().numpy()
+        Vr = cc[ci][1][:, a:b].double().cpu().numpy()
+        oc = OC.compress(Kr, Vr, a, kb, okp, vb, ovp, invf, s=0, w=0)
+        h = parse_container(buf)
+        for sv, so, ob, X in ((0, oc.k, kb, OC.stream_rows(Kr, 0, 0, a, True, invf, 0)),
+                              (1, oc.v, vb, OC.stream_rows(Vr, 0, 0, a, False))):
+            sec = parse_section(buf[h["sec_k" if sv == 0 else "sec_v"]:])
+            payload = b"".join(zlib.decompress(x, wbits=-15) for x in sec["streams"])
+            cols = np.concatenate([np.arange(s0, s0 + z) for (s0, z, _) in okp.groups])
+            E.assert_codes_parity(payload, okp.groups, so.D, b - a, X, ob, cols, f"range {i} stream={sv}")

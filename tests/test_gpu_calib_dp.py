@@ -124,3 +124,41 @@ def test_randomized_svd_path(K, monkeypatch):
     gaps = np.abs(np.diff(vb.sigma[: k + 1] ** 2))
     well = gaps[:k] > 1e-2 * vb.sigma[0] ** 2
     assert np.all(cos[well] > 0.99), cos[well].min()
+
+
+def _golden_dp():
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "dp_production.json")) as f:
+        return json.load(f)["cases"]
+
+
+@pytest.mark.parametrize("case", ["decay_b32768", "tail_1024", "tail_256"])
+def test_dp_bitexact_at_production_shape(K, case):
+    """the 256- and 1024-block E-table paths and the scan over 16,385
+    even budgets (B = 32768, the Llama-8B budget at CR 16) against the literal
+    loop of P:L1541-1603.  Expected values: tests/golden/dp_production.json,
+    written by scripts/make_dp_golden.py from oracle/ only (oracle DP on the same
+    seeded inputs); the GPU's even-budget best_error table must hash identically
+    and the backtracked plan and best_error[r][B] must be equal."""
+    import hashlib
+    from kvtc_inputs import dp_coefficients
+    g = _golden_dp()[case]
+    prm = g["params"]
+    B = prm["budget"]
+    P = dp_coefficients(**prm)
+    Pd = torch.from_numpy(P).cuda()
+    got = K.dp_best_table(Pd, B).cpu().numpy()
+    assert list(got.shape) == g["best_even_shape"]
+    if hashlib.sha256(np.ascontiguousarray(got).astype("<f8").tobytes()).hexdigest() != g["best_even_sha256"]:
+        r = P.shape[1]
+        step = max(1, got.shape[1] // 16)
+        for i, row in g["rows_hex"].items():
+            np.testing.assert_array_equal(got[int(i), ::step], [float.fromhex(v) for v in row], err_msg=f"row {i}")
+        raise AssertionError("best_error table differs from the oracle's (rows sampled above agree)")
+    plan = K.allocate_bits_from_coeffs(Pd, p_original=B, target_cr=16.0)
+    info = plan.info()
+    assert info.budget == B
+    assert info.groups == [tuple(x) for x in g["groups"]]
+    assert info.expected_error == float.fromhex(g["expected_error_hex"])
+    assert set(z for (_, z, _) in info.groups) >= set(g["sizes_in_plan"]) - {1}

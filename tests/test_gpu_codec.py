@@ -113,6 +113,11 @@ def test_layer_range_decompress(K):
     torch.cuda.synchronize()
     assert torch.equal(part_k[1], full_k[1]) and torch.equal(part_v[1], full_v[1])
     assert not part_k[0].any() and not part_v[0].any()
+    # and directly against the oracle's decompression of the same container (layer 1 only)
+    rk, rv = E.oracle_restore(cont.cpu().numpy().tobytes(), kb, okp, vb, ovp, invf)
+    E.assert_restored_like_oracle(part_k, part_v, rk, rv, layers=slice(1, 2))
+    np.testing.assert_array_equal(part_k[1, :4].cpu(), kd[1, :4].cpu())
+    np.testing.assert_array_equal(part_v[1, tokens - 128:].cpu(), vd[1, tokens - 128:].cpu())
 
 
 @pytest.mark.parametrize("name,tokens", [("mid", 700), ("toy", 400)])

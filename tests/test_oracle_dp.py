@@ -145,3 +145,15 @@ def test_budget_rule():
     assert DP.budget_bits(32768, 16) == 32768           # headline: 4096 B per token per stream
     assert DP.budget_bits(128, 16) == 128
     assert DP.budget_bits(40960, 20) == 32768
+
+
+def test_vectorised_ez_tables_equal_the_block_loop():
+    """ez_tables stacks many blocks per NumPy call; it must reproduce the plain
+    per-block loop bit for bit (same expressions, same Q9 summation order)."""
+    rng = np.random.default_rng(11)
+    for n, r, sizes in ((37, 40, (1, 2, 4)), (100, 130, (1, 16, 64, 256, 1024)), (7, 300, (1, 16, 64, 256))):
+        P = rng.standard_normal((n, r)) * (1 + np.arange(r)) ** -0.8
+        a = DP.ez_tables_loop(P, sizes)
+        b = DP.ez_tables(P, sizes, max_elems=5000)
+        np.testing.assert_array_equal(a[0], b[0])
+        np.testing.assert_array_equal(a[1], b[1])

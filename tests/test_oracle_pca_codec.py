@@ -131,3 +131,41 @@ def test_nothing_to_compress(toy):
     K2, V2 = C.decompress(c, kb, plan, vb, plan, invf)
     np.testing.assert_array_equal(K2, K)
     np.testing.assert_array_equal(V2, V)
+
+
+def _exact_basis():
+    """An orthonormal, NON-symmetric 4x4 basis whose entries (+-1/2) are exact in
+    bf16 and fp16, so V_c = V_d = V and every step below is exact in fp64: the
+    Hadamard matrix / 2 with its columns permuted (2, 0, 3, 1)."""
+    H = 0.5 * np.array([[1, 1, 1, 1], [1, -1, 1, -1], [1, 1, -1, -1], [1, -1, -1, 1]], dtype=np.float64)
+    V = H[:, [2, 0, 3, 1]]
+    mu = np.array([1.0, 2.0, 3.0, 4.0])
+    return PCA.Basis(mu=mu, V=V, sigma=np.ones(4), n=0), V, mu
+
+
+def test_project_worked_example():
+    """D = (X - mu) V.  Worked by hand: X - mu = [2, 0, 0, 0] gives
+    2 * (row 0 of V) = [1, 1, 1, 1]; X - mu = [0, 2, 0, 0] gives 2 * row 1 =
+    [1, 1, -1, -1]; X = mu gives 0 (a dropped mu V_c term fails this);
+    X - mu = [0, 0, 0, 4] gives 4 * row 3 = [-2, 2, 2, -2] (a transposed V
+    fails, V is not symmetric)."""
+    b, V, mu = _exact_basis()
+    X = mu[None, :] + np.array([[2.0, 0, 0, 0], [0, 2.0, 0, 0], [0, 0, 0, 0], [0, 0, 0, 4.0]])
+    D = PCA.project(b, X)
+    np.testing.assert_array_equal(D, [[1, 1, 1, 1], [1, 1, -1, -1], [0, 0, 0, 0], [-2, 2, 2, -2]])
+    # a column subset projects onto those PCs only
+    np.testing.assert_array_equal(PCA.project(b, X, cols=[3, 1]), D[:, [3, 1]])
+
+
+def test_reconstruct_inverts_projection_and_truncation_error():
+    """P:L232-234: X = D V^T + mu with all p PCs (exact here: V^T V = I);
+    keeping a subset of PCs leaves ||X - X^||^2 = the sum of the discarded
+    squared coefficients (orthonormal invariance)."""
+    b, V, mu = _exact_basis()
+    rng = np.random.default_rng(3)
+    X = mu[None, :] + rng.integers(-8, 9, (5, 4)).astype(np.float64)
+    D = PCA.project(b, X)
+    np.testing.assert_array_equal(PCA.reconstruct(b, D), X)
+    keep = [0, 2]
+    Xh = PCA.reconstruct(b, D[:, keep], cols=keep)
+    np.testing.assert_array_equal(np.sum((X - Xh) ** 2, axis=1), np.sum(D[:, [1, 3]] ** 2, axis=1))

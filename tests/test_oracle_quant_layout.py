@@ -9,10 +9,16 @@ from oracle import layout as L
 from oracle.numerics import f16_bits, e4m3_decode
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden", "quant_pack_golden.json")
+GOLD_FP8 = os.path.join(os.path.dirname(__file__), "golden", "fp8_golden.json")
+
+import pytest
 
 
-def test_golden_vector():
-    g = json.load(open(GOLD))
+@pytest.mark.parametrize("path", [GOLD, GOLD_FP8])
+def test_golden_vector(path):
+    """Hand-derived vectors (int2/int4: SURVEY §8(c); fp8: reading Q3 with the
+    midpoint shift and half-range/448 scale, subnormal and saturated codes)."""
+    g = json.load(open(path))
     rows = np.array(g["rows"])
     groups = [tuple(x) for x in g["groups"]]
     shifts, scales, codes = [], [], []
