@@ -7,10 +7,17 @@ A step = kvtc_compress (keys and values: un-RoPE gather, fused tcgen05 projectio
 tcgen05 inverse projection + mu + RoPE, raw sinks/window) of one 32K-token
 conversation per GPU.  GB/s = 2 streams x 2 B x p x m / step time, m = t - s - w.
 
-  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
-Multi-GPU: torchrun, one conversation per rank (weak scaling, no data-path
-collective); calibration statistics are all-reduced over NCCL in the untimed
-setup.  See DESIGN.md §8 for the measurement recipe.
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config C]
+Multi-GPU: one process per GPU.  Under torchrun the ranks come from the
+environment; `--gpus N` without WORLD_SIZE re-launches itself through
+torch.distributed.run with N ranks.  llama8b / nemo12b: one conversation per rank
+(weak scaling, no data-path collective), calibration statistics all-reduced over
+NCCL in the untimed setup.  llama70b_shard: rank g owns layer shard g (10 of the
+70B model's 80 layers) with its own basis and plan, no collective at
+all.  multiconv: 256 conversations LPT-assigned to ranks (strong scaling).
+--impl reference: the oracle (oracle/, fp64 NumPy + zlib) on host cores, with a
+basis and plan it computes itself; libkvtc.so is never loaded on that arm.
+See DESIGN.md §8 for the measurement recipe.
 """
 from __future__ import annotations
 
@@ -107,9 +114,11 @@ def dist_env():
 
 
 # ------------------------------------------------------------------- setup
-def build_artifacts(K, spec, args, rank, world, dist):
-    """Calibration (K6, NCCL all-reduce of X^T X when world > 1) and the DP (K7/K8).
-    Untimed setup; deterministic, so every rank ends with the same basis and plan."""
+def build_artifacts(K, spec, args, rank, world, dist, local_calibration: bool = False):
+    """Calibration (K6, NCCL all-reduce of X^T X when world > 1 unless
+    local_calibration) and the DP (K7/K8).  Untimed setup; deterministic, so every
+    rank of an all-reduced calibration ends with the same basis and plan; a layer
+    shard (local_calibration) calibrates on its own cache only."""
     from kvtc_inputs import generate, sample_positions
     from paper_2511_01815_b200.distributed import calibrate_distributed
     shape = (spec.layers, spec.kv_heads, spec.head_dim)
@@ -124,7 +133,8 @@ def build_artifacts(K, spec, args, rank, world, dist):
         torch.cuda.synchronize()
         tg = time.time()
         # shard of the draw on this rank -> NCCL all-reduce of (sum_x, X^T X, n) -> finalize
-        basis = calibrate_distributed(K, views, samples, stream, args.rank_cap, inv_freq=invf)
+        basis = calibrate_distributed(K, views, samples, stream, args.rank_cap, inv_freq=invf,
+                                      local=local_calibration)
         torch.cuda.empty_cache()
         tx = te = time.time()
         plan = K.allocate_bits(basis, views, samples, args.cr)
@@ -143,13 +153,26 @@ def build_artifacts(K, spec, args, rank, world, dist):
     return bases, plans, info
 
 
-def oracle_sample(bases, plans, K_host, V_host, spec, ntok: int):
-    """The oracle (as it stands) on a bounded sample: compress + decompress of
-    the first ntok middle tokens of the conversation, both streams."""
-    from oracle import codec as OC
+# ------------------------------------------------------------- the oracle legs
+DEFAULT_TOKENS = {"llama8b": 32768, "nemo12b": 65536, "llama70b_shard": 131072, "toy": 512, "multiconv": 32768}
+
+
+def host_threads():
+    """(os.cpu_count(), BLAS threads the oracle's NumPy uses)."""
+    blas = None
+    try:
+        import threadpoolctl
+        blas = max([x.get("num_threads", 1) for x in threadpoolctl.threadpool_info()] + [1])
+    except Exception:
+        pass
+    return os.cpu_count(), blas
+
+
+def oracle_objects(bases, plans):
+    """The GPU arm's basis / plan as oracle objects (for the cpu_baseline leg,
+    which times the oracle on exactly the plan the GPU ran)."""
     from oracle import dp as ODP
     from oracle import pca as OPCA
-    invf = spec.inv_freq().double().numpy()
     obs, ops = [], []
     for b, pl in zip(bases, plans):
         mu, V, sg = b.get()
@@ -157,21 +180,118 @@ def oracle_sample(bases, plans, K_host, V_host, spec, ntok: int):
         r_use = max(1, pi.r_eff)                      # columns past r_eff are never read
         obs.append(OPCA.Basis(mu=mu.astype(np.float64), V=V[:, :r_use].astype(np.float64), sigma=sg[:r_use], n=0))
         ops.append(ODP.Plan(r=r_use, blocks=list(pi.groups)))
+    return obs, ops
+
+
+def oracle_round_trip(obs, ops, Kh, Vh, spec, ntok: int):
+    """The oracle (as it stands) on a bounded sample: compress + decompress of
+    the first ntok middle tokens (tokens [0, ntok + 132) of the conversation
+    Kh / Vh [l, t, h, d]), both streams.  Returns (GB/s 16-bit equivalent, s)."""
+    from oracle import codec as OC
+    invf = spec.inv_freq().double().numpy()
     t = ntok + 132
-    Kc = K_host[:, :t].double().numpy()
-    Vc = V_host[:, :t].double().numpy()
-    try:
-        import threadpoolctl
-        blas = threadpoolctl.threadpool_info()
-        cores = max([x.get("num_threads", 1) for x in blas] + [1])
-    except Exception:
-        cores = os.cpu_count()
+    Kc = np.asarray(Kh[:, :t].double().numpy() if torch.is_tensor(Kh) else Kh[:, :t], dtype=np.float64)
+    Vc = np.asarray(Vh[:, :t].double().numpy() if torch.is_tensor(Vh) else Vh[:, :t], dtype=np.float64)
     t0 = time.perf_counter()
     c = OC.compress(Kc, Vc, 0, obs[0], ops[0], obs[1], ops[1], invf)
     OC.decompress(c, obs[0], ops[0], obs[1], ops[1], invf)
     dt = time.perf_counter() - t0
-    gbs = 2 * 2 * spec.p * ntok / dt / 1e9
-    return gbs, dt, cores, c.stats
+    return 2 * 2 * spec.p * ntok / dt / 1e9, dt
+
+
+def oracle_toy_config():
+    """BASELINE configs[0] run fully by the oracle: calibration on 4096 rows (fp64
+    eigh), DP at CR 16, compress + decompress of one 512-token conversation.
+    Returns the round trip's GB/s and the seconds of each part."""
+    from kvtc_inputs import generate, make_spec, sample_positions
+    from oracle import codec as OC
+    from oracle import dp as ODP
+    from oracle import pca as OPCA
+    spec = make_spec("toy")
+    invf = spec.inv_freq().double().numpy()
+    t0 = time.perf_counter()
+    cal = [generate(spec, st, 4224, pos0=0, conversation=100).double().numpy() for st in (0, 1)]
+    samples = sample_positions([4224], 4096, sinks=4, seed=1)
+    Ck = OPCA.gather([(cal[0], 0)], samples, True, invf)
+    Cv = OPCA.gather([(cal[1], 0)], samples, False)
+    kb, vb = OPCA.fit(Ck, 10000), OPCA.fit(Cv, 10000)
+    t1 = time.perf_counter()
+    kp, _, _ = ODP.allocate(OPCA.dp_coefficients(kb, Ck), 16.0, spec.p)
+    vp, _, _ = ODP.allocate(OPCA.dp_coefficients(vb, Cv), 16.0, spec.p)
+    t2 = time.perf_counter()
+    K = generate(spec, 0, 512, conversation=0).double().numpy()
+    V = generate(spec, 1, 512, conversation=0).double().numpy()
+    t3 = time.perf_counter()
+    c = OC.compress(K, V, 0, kb, kp, vb, vp, invf)
+    OC.decompress(c, kb, kp, vb, vp, invf)
+    t4 = time.perf_counter()
+    return {"value": 2 * 2 * spec.p * (512 - 132) / (t4 - t3) / 1e9, "unit": UNIT, "seconds": t4 - t3,
+            "calibration_s": t1 - t0, "dp_s": t2 - t1,
+            "sample": "toy config (1 x 2 x 64, 512 tokens, CR 16) in full: oracle calibration + DP, then "
+                      "compress + decompress timed"}
+
+
+def workload(args, spec, t, world):
+    if args.config == "llama70b_shard":
+        return (f"llama70b_shard: one 10-layer shard of the Llama-3.3-70B shape per GPU (8 KV heads x 128, "
+                f"p = {spec.p}), {t}-token conversation, CR target {args.cr:g}, own basis + plan per shard")
+    return (f"{args.config}: {spec.layers} layers x {spec.kv_heads} KV heads x {spec.head_dim}, {t}-token "
+            f"conversation per GPU, CR target {args.cr:g}")
+
+
+def run_reference(args, spec, t):
+    """--impl reference: the oracle alone, on the box's host cores (rank 0).
+    Setup (untimed) also runs through the oracle only — the GPU library is never
+    loaded: calibration = the SVD of a centred 2048-row sample of one synthetic
+    4096-token calibration conversation (oracle.pca.fit_svd; the
+    p x p eigendecomposition does not finish on a host at p = 32768), DP = the
+    oracle's literal loop on the first 256 of those rows (a reduced Q8 cap).
+    Each step compresses + decompresses a bounded slice of the workload's
+    conversation (--ref-tokens middle tokens)."""
+    from kvtc_inputs import generate, sample_positions
+    from oracle import dp as ODP
+    from oracle import pca as OPCA
+    invf = spec.inv_freq().double().numpy()
+    ts = time.time()
+    obs, ops, setup = [], [], {}
+    ncal, ndp, tcal = 2048, 128, 4096
+    samples = sample_positions([tcal], ncal, sinks=4, seed=7)
+    for stream in (0, 1):
+        cal = generate(spec, stream, tcal, pos0=0, conversation=1000).double().numpy()
+        C = OPCA.gather([(cal, 0)], samples, stream == 0, invf)
+        del cal
+        b = OPCA.fit_svd(C, args.rank_cap)
+        plan, _, B = ODP.allocate(OPCA.dp_coefficients(b, C, ndp), args.cr, spec.p)
+        obs.append(b)
+        ops.append(plan)
+        setup["kv"[stream]] = {"r": b.r, "r_eff": plan.r_eff, "bits_per_token": plan.bits_per_token, "budget": B}
+        log(f"[reference] stream {stream}: {setup['kv'[stream]]} ({time.time() - ts:.0f} s)")
+    setup_s = time.time() - ts
+    ntok = args.ref_tokens
+    Kh = generate(spec, 0, ntok + 132, pos0=0, conversation=0).double().numpy()
+    Vh = generate(spec, 1, ntok + 132, pos0=0, conversation=0).double().numpy()
+    for _ in range(args.warmup):
+        oracle_round_trip(obs, ops, Kh, Vh, spec, min(8, ntok))
+    vals, secs = [], 0.0
+    for _ in range(args.steps):
+        gbs, dt = oracle_round_trip(obs, ops, Kh, Vh, spec, ntok)
+        vals.append(gbs)
+        secs += dt
+    v = statistics.mean(vals)
+    cores, blas = host_threads()
+    sample = (f"{ntok} middle tokens of the {args.config} workload per step, compress + decompress of both streams "
+              "(fp64 NumPy + zlib, the oracle as it stands)")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (kvtc_inputs, DESIGN.md §5)",
+            "config": {"workload": workload(args, spec, t, 1), "sample": sample},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "blas_threads": blas, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "setup": {"seconds": round(setup_s, 1), "streams": setup,
+                      "how": f"oracle only: fit_svd on {ncal} sampled rows of a {tcal}-token calibration "
+                             f"conversation, oracle DP on the first {ndp} rows, CR {args.cr:g}; libkvtc.so not loaded"}}
+    print(json.dumps(line), flush=True)
 
 
 # ---------------------------------------------------------- multi-conversation
@@ -184,7 +304,10 @@ def run_multiconv(args, K, spec, kb, kp, vb, vp, setup_s, setup_info, world, ran
     once).  Only codec time is timed (CUDA events around each wave's round trip on
     the launching stream, summed);
     value = all ranks' 16-bit bytes / the slowest rank's codec time (strong
-    scaling: the 256 conversations are fixed as N grows)."""
+    scaling: the 256 conversations are fixed as N grows).  Every wave is verified:
+    sinks and window restored bit for bit, the middle tokens' relative L2 error
+    reported, and a checksum of the reconstructed bytes compared between the
+    first and every later pass over the same wave (deterministic restore)."""
     from kvtc_inputs import generate, lengths_for
     from paper_2511_01815_b200.distributed import lpt_assign
     lens = lengths_for(args.convs, 8192, 32768, seed=0)
@@ -192,8 +315,6 @@ def run_multiconv(args, K, spec, kb, kp, vb, vp, setup_s, setup_info, world, ran
     p = spec.p
     stream = torch.cuda.current_stream()
     clocks = ClockSampler(local)
-    # waves of up to --batch-tokens tokens, each compressed and decompressed by ONE
-    # kvtc_compress_batch + kvtc_decompress_batch (one GEMM per stream over all rows)
     waves, cur, ntok = [], [], 0
     for ci in mine:
         if cur and ntok + lens[ci] > args.batch_tokens:
@@ -203,8 +324,9 @@ def run_multiconv(args, K, spec, kb, kp, vb, vp, setup_s, setup_info, world, ran
         ntok += lens[ci]
     if cur:
         waves.append(cur)
+    sums = {}
 
-    def one(wave):
+    def one(wi, wave):
         Ks = [generate(spec, 0, lens[ci], pos0=0, conversation=ci, device="cuda") for ci in wave]
         Vs = [generate(spec, 1, lens[ci], pos0=0, conversation=ci, device="cuda") for ci in wave]
         Ko = [torch.empty_like(x) for x in Ks]
@@ -219,26 +341,36 @@ def run_multiconv(args, K, spec, kb, kp, vb, vp, setup_s, setup_info, world, ran
                           dtype=torch.uint8, device="cuda")
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n0 = K.launch_count()
         e0.record(stream)
         K.compress_batch(kb, kp, vb, vp, kv, vv, outs=outs, workspace=cws, sync_len=False)
         K.decompress_batch(kb, kp, vb, vp, outs, kov, vov, workspace=dws)
         e1.record(stream)
         torch.cuda.synchronize()
-        ok = all(torch.equal(o[:, :4], x[:, :4]) for o, x in zip(Ko, Ks))
-        return e0.elapsed_time(e1), sum(2 * 2 * p * (lens[ci] - 132) for ci in wave), ok
+        launches = K.launch_count() - n0
+        ok = all(torch.equal(o[:, :4], x[:, :4]) and torch.equal(o[:, -128:], x[:, -128:]) for o, x in zip(Ko, Ks))
+        ok &= all(torch.equal(o[:, :4], x[:, :4]) and torch.equal(o[:, -128:], x[:, -128:]) for o, x in zip(Vo, Vs))
+        rel = max(float((o[:, 4:-128].float() - x[:, 4:-128].float()).norm() / x[:, 4:-128].float().norm())
+                  for o, x in zip(Ko + Vo, Ks + Vs))
+        ck = sum(int(o.view(torch.int16).to(torch.int64).sum()) for o in Ko + Vo)
+        same = sums.setdefault(wi, ck) == ck
+        return e0.elapsed_time(e1), sum(2 * 2 * p * (lens[ci] - 132) for ci in wave), ok, rel, same, launches
 
     for _ in range(args.warmup):
-        one(waves[0])
+        one(0, waves[0])
     if dist:
         dist.barrier()
     clocks.start()
-    ms, nbytes, allok = 0.0, 0, True
+    ms, nbytes, allok, relmax, det, launches = 0.0, 0, True, 0.0, True, 0
     for _ in range(args.steps):
-        for wave in waves:
-            dt, b, ok = one(wave)
+        for wi, wave in enumerate(waves):
+            dt, b, ok, rel, same, nl = one(wi, wave)
             ms += dt
             nbytes += b
             allok &= ok
+            det &= same
+            relmax = max(relmax, rel)
+            launches += nl
     clk = clocks.stop()
     tot = torch.tensor([ms, float(nbytes)], dtype=torch.float64, device="cuda")
     if dist:
@@ -259,8 +391,10 @@ def run_multiconv(args, K, spec, kb, kp, vb, vp, setup_s, setup_info, world, ran
                                        "wave, untimed)",
                            "conversations": args.convs, "tokens_total": int(sum(lens)),
                            "per_rank_conversations": len(mine), "waves": len(waves), "setup_s": round(setup_s, 1),
-                           "sinks_window_roundtrip_ok": bool(allok)},
-                "gpu_launches": None, "clocks": clk}
+                           "l2": "each wave's caches (>= 4 GB) exceed the 126 MB L2",
+                           "verify": {"sinks_window_bit_exact": bool(allok), "middle_rel_l2_max": relmax,
+                                      "restore_deterministic_across_passes": bool(det)}},
+                "gpu_launches": int(launches), "clocks": clk}
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
@@ -268,14 +402,28 @@ def run_multiconv(args, K, spec, kb, kp, vb, vp, setup_s, setup_info, world, ran
 
 
 # -------------------------------------------------------------------- main
+def self_launch(args) -> int:
+    """`--gpus N` outside torchrun: re-run this script under
+    torch.distributed.run with N ranks on this node (rendezvous on 127.0.0.1)."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    log("[bench] self-launch:", " ".join(cmd))
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="llama8b")
-    ap.add_argument("--tokens", type=int, default=32768)
+    ap.add_argument("--config", default="llama8b", choices=sorted(DEFAULT_TOKENS))
+    ap.add_argument("--tokens", type=int, default=None)               # default: per config (DEFAULT_TOKENS)
     ap.add_argument("--cr", type=float, default=16.0)
     ap.add_argument("--cal-seqs", type=int, default=2)
     ap.add_argument("--cal-tokens", type=int, default=32768)
@@ -285,30 +433,18 @@ def main():
     ap.add_argument("--noise", type=float, default=None)            # synthetic isotropic-noise fraction
     ap.add_argument("--latent", type=int, default=None)             # synthetic latent rank K
     ap.add_argument("--setup-only", action="store_true")
-    ap.add_argument("--cpu-tokens", type=int, default=32)
+    ap.add_argument("--cpu-tokens", type=int, default=512)          # cpu_baseline slice
+    ap.add_argument("--ref-tokens", type=int, default=128)          # reference arm: middle tokens per step
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--convs", type=int, default=256)                # multiconv: number of conversations
     ap.add_argument("--batch-tokens", type=int, default=131072)      # multiconv: tokens per batched call
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
 
     world, rank, local = dist_env()
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(0)
-    if args.impl == "reference" and rank != 0:
-        if dist:
-            dist.barrier()
-            dist.destroy_process_group()
-        return
-
-    from paper_2511_01815_b200 import kvtc as K
     from kvtc_inputs import make_spec, generate
-    K.device_check()
     over = {}
     if args.beta is not None:
         over["beta"] = args.beta
@@ -316,15 +452,35 @@ def main():
         over["noise_frac"] = args.noise
     if args.latent is not None:
         over["latent"] = args.latent
-    spec = make_spec("llama8b" if args.config == "multiconv" else args.config, **over)
-    p, t = spec.p, args.tokens
+    base = "llama8b" if args.config == "multiconv" else args.config
+    if args.config == "llama70b_shard" and args.impl == "ours":
+        over["name"] = f"llama70b_shard{rank}"                   # layer shard g = rank: its own model slice
+    spec = make_spec(base, **over)
+    t = args.tokens or DEFAULT_TOKENS[args.config]
+    if args.impl == "reference":
+        # the oracle on host cores, rank 0 only; the other ranks exit without work
+        if rank == 0:
+            run_reference(args, spec, t)
+        return
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    from paper_2511_01815_b200 import kvtc as K
+    K.device_check()
+    p = spec.p
     s_, w_ = 4, 128
     m = t - s_ - w_
     hbm, bf16_burst, bf16_sus, peak_src = peaks()
     log(f"[bench] rank {rank}/{world} config={args.config} p={p} t={t} m={m} impl={args.impl}")
 
     t_setup = time.time()
-    bases, plans, setup_info = build_artifacts(K, spec, args, rank, world, dist)
+    bases, plans, setup_info = build_artifacts(K, spec, args, rank, world, dist,
+                                               local_calibration=args.config == "llama70b_shard")
     setup_s = time.time() - t_setup
     kb, vb = bases
     kp, vp = plans
@@ -358,34 +514,6 @@ def main():
     bytes16 = 2 * 2 * p * m                                    # K+V middle tokens, 16-bit
     cr = bytes16 / (info.entropy_bytes[0] + info.entropy_bytes[1])
     cr_pre = bytes16 / (info.payload_bytes[0] + info.payload_bytes[1])
-
-    if args.impl == "reference":
-        # the oracle as it stands, on host cores, on a bounded sample of the same workload
-        Kh, Vh = Kc.cpu(), Vc.cpu()
-        for _ in range(args.warmup):
-            oracle_sample(bases, plans, Kh, Vh, spec, min(8, args.cpu_tokens))
-        vals, secs = [], 0.0
-        for _ in range(args.steps):
-            gbs, dt, cores, stats = oracle_sample(bases, plans, Kh, Vh, spec, args.cpu_tokens)
-            vals.append(gbs)
-            secs += dt
-        v = statistics.mean(vals)
-        line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": f"{args.config} {t}-token conversation, CR target {args.cr:g}",
-                           "sample": f"{args.cpu_tokens} middle tokens per step"},
-                "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-                                 "sample": f"{args.cpu_tokens} middle tokens of the {args.config} conversation, "
-                                           "compress+decompress, both streams"},
-                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-                "setup": "basis/plan from kvtc_calibrate + kvtc_allocate_bits (untimed inputs; the oracle's own "
-                         "fp64 eigh of a 32768^2 covariance does not finish in minutes on the host)"}
-        print(json.dumps(line), flush=True)
-        if dist:
-            dist.barrier()
-            dist.destroy_process_group()
-        return
 
     stream = torch.cuda.current_stream()
 
@@ -453,12 +581,26 @@ def main():
             stages[nm]["frac_of_sustained_bf16"] = tfl / bf16_sus
     pay = info.payload_bytes[0] + info.payload_bytes[1]
     ent = info.entropy_bytes[0] + info.entropy_bytes[1]
-    for nm, b in (("c.deflate", pay + ent), ("d.inflate", pay + ent), ("d.dequant", pay + m * 2 * sum(rnz)),
-                  ("c.gather_unrope", 2 * 2 * p * m), ("c.gather", 2 * 2 * p * m)):
+    rpad = [(x + 7) // 8 * 8 for x in rnz]
+    # algorithmic bytes of each stage as the schedule runs it: the
+    # caller-stream DEFLATE and dequantisation handle the KEYS only (the values'
+    # run beside the keys' GEMM as the *_overlapped stages, whose time is shared
+    # with it); one inflate launch covers both streams
+    stage_bytes = {"c.deflate": info.payload_bytes[0] + info.entropy_bytes[0],
+                   "c.deflate_overlapped": info.payload_bytes[1] + info.entropy_bytes[1],
+                   "d.inflate": pay + ent,
+                   "d.dequant": info.payload_bytes[0] + m * 2 * rpad[0],
+                   "d.dequant_overlapped": info.payload_bytes[1] + m * 2 * rpad[1],
+                   "c.gather_unrope": 2 * 2 * p * m, "c.gather_unrope_overlapped": 2 * 2 * p * m,
+                   "d.checksum_overlapped": pay + 2 * info.raw_bytes}
+    for nm, b in stage_bytes.items():
         if nm in stages:
             gbs = b / (stages[nm]["ms_per_step"] * 1e-3) / 1e9
+            stages[nm]["bytes"] = b
             stages[nm]["gbs"] = gbs
             stages[nm]["frac_of_hbm"] = gbs / hbm
+            if nm.endswith("_overlapped"):
+                stages[nm]["note"] = "bounded grid beside a GEMM: the time is shared, not a kernel roofline"
     dom = max(("c.project_quant_gemm", "d.reconstruct_gemm"), key=lambda n: stages.get(n, {}).get("ms_per_step", 0))
     dom_ms = stages[dom]["ms_per_step"] / 2                  # per launch (K or V), averaged
     achieved = gemm_flops / 2 / (dom_ms * 1e-3) / 1e12
@@ -636,18 +778,30 @@ def main():
 
     cpu = None
     if rank == 0 and not args.no_cpu:
-        gbs, dt, cores, stats = oracle_sample(bases, plans, Kc.cpu(), Vc.cpu(), spec, args.cpu_tokens)
-        cpu = {"value": gbs, "unit": UNIT, "cores": cores, "kind": "oracle", "seconds": dt,
-               "sample": f"{args.cpu_tokens} middle tokens of the {args.config} conversation, compress+decompress "
-                         "of both streams (fp64 NumPy + zlib, the oracle as it stands)"}
+        # the oracle beside the GPU on this box's host cores — a
+        # 512-token slice of the same conversation with the plan the GPU ran, and
+        # the toy config in full (extrapolated, context only)
+        obs, ops = oracle_objects(bases, plans)
+        ntok = min(args.cpu_tokens, m)
+        Kh, Vh = Kc[:, :ntok + 132].cpu(), Vc[:, :ntok + 132].cpu()
+        oracle_round_trip(obs, ops, Kh, Vh, spec, min(8, ntok))                 # operand rounding, once
+        gbs, dt = oracle_round_trip(obs, ops, Kh, Vh, spec, ntok)
+        cores, blas = host_threads()
+        cpu = {"value": gbs, "unit": UNIT, "cores": cores, "blas_threads": blas, "kind": "oracle", "seconds": dt,
+               "sample": f"{ntok} middle tokens of this {args.config} conversation, compress + decompress of both "
+                         "streams with the plan the GPU ran (fp64 NumPy + zlib, the oracle as it stands); "
+                         "extrapolated to the workload's unit",
+               "toy": oracle_toy_config() if args.config != "toy" else None}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic (kvtc_inputs, DESIGN.md §5)",
-                "config": {"workload": f"{args.config}: {spec.layers} layers x {spec.kv_heads} KV heads x "
-                                       f"{spec.head_dim}, {t}-token conversation per GPU, CR target {args.cr:g}",
-                           "tokens_per_gpu": t, "middle_tokens": m, "p": p, "parallelism": f"weak x{world}",
+                "config": {"workload": workload(args, spec, t, world),
+                           "tokens_per_gpu": t, "middle_tokens": m, "p": p,
+                           "parallelism": (f"layer shards x{world} (pipeline-parallel layout, own basis per shard, "
+                                           "no collective)" if args.config == "llama70b_shard" else
+                                           f"weak x{world} (one conversation per GPU; calibration all-reduced)"),
                            "l2": f"inputs {2 * 2 * p * t / 1e9:.1f} GB per step >> 126 MB L2 (no flush needed)",
                            "cr": cr, "cr_pre_deflate": cr_pre, "r_eff": [kinfo.r_eff, vinfo.r_eff], "r_nz": rnz,
                            "setup_s": round(setup_s, 1), "setup": setup_info},

@@ -53,13 +53,17 @@ class Basis:
 
     @property
     def Vc(self) -> np.ndarray:
-        """bf16 compress operand (R2)."""
-        return bf16(self.V)
+        """bf16 compress operand (R2), rounded once per basis."""
+        if getattr(self, "_vc", None) is None or self._vc[0] is not self.V:
+            self._vc = (self.V, bf16(self.V))
+        return self._vc[1]
 
     @property
     def Vd(self) -> np.ndarray:
-        """fp16 decompress operand (R6)."""
-        return f16(self.V)
+        """fp16 decompress operand (R6), rounded once per basis."""
+        if getattr(self, "_vd", None) is None or self._vd[0] is not self.V:
+            self._vd = (self.V, f16(self.V))
+        return self._vd[1]
 
 
 def flatten_rows(kv) -> np.ndarray:
@@ -103,6 +107,25 @@ def fit(C, rank_cap: int) -> Basis:
     sgn[sgn == 0] = 1.0
     V = V * sgn
     return Basis(mu=f32(mu), V=f32(V), sigma=np.sqrt(np.maximum(w, 0.0)), n=n)
+
+
+def fit_svd(C, rank_cap: int) -> Basis:
+    """The same basis through the definition P:L226-229 states literally: the SVD
+    of the centred matrix C - mu = U Sigma V^T (np.linalg.svd, fp64), singular
+    values descending, canonical sign (Q13), r = min(cap, n-1, p).  Used where
+    n << p makes the p x p eigendecomposition of ``fit`` impractical on a host
+    (the bench's reference arm at p = 32768); pinned equal to ``fit``."""
+    C = np.asarray(C, dtype=np.float64)
+    n, p = C.shape
+    mu = C.mean(axis=0)
+    _, sv, Vt = np.linalg.svd(C - mu, full_matrices=False)
+    r = min(rank_cap, max(n - 1, 1), p)
+    V = Vt[:r].T
+    idx = np.argmax(np.abs(V), axis=0)
+    sgn = np.sign(V[idx, np.arange(r)])
+    sgn[sgn == 0] = 1.0
+    V = V * sgn
+    return Basis(mu=f32(mu), V=f32(V), sigma=sv[:r], n=n)
 
 
 def project(basis: Basis, X, cols=None) -> np.ndarray:

@@ -40,16 +40,20 @@ def allreduce_calibration(sum_x: torch.Tensor, xtx: torch.Tensor, n_local: int, 
 
 
 def calibrate_distributed(K, views, samples, which: int, rank_cap: int, inv_freq=None, pairing: int = 0,
-                          group=None):
-    """kvtc_calibrate_accumulate on this rank's shard -> NCCL all-reduce ->
-    kvtc_calibrate_finalize (identical basis on every rank)."""
+                          group=None, local: bool = False, device="cuda"):
+    """kvtc_calibrate_accumulate on this rank's shard of the draw -> all-reduce
+    (NCCL on GPUs) -> kvtc_calibrate_finalize: every rank finalises the same
+    statistics, hence the same basis.  local=True: this rank's own draw only, no
+    collective (a layer shard of a pipeline-parallel model keeps its own basis,
+    P:L443).  K is the binding (kvtc); the CPU tests pass an object with the same
+    two calls (calibrate_accumulate / calibrate_finalize) and device="cpu"."""
     import torch.distributed as dist
-    world = dist.get_world_size(group) if dist.is_initialized() else 1
-    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if (dist.is_initialized() and not local) else 1
+    rank = dist.get_rank(group) if (dist.is_initialized() and not local) else 0
     mine = shard_samples(samples, rank, world)
     p = views[0].shape[0] * views[0].shape[1] * views[0].shape[2]
-    sum_x = torch.zeros(p, dtype=torch.float64, device="cuda")
-    xtx = torch.zeros(p, p, dtype=torch.float32, device="cuda")
+    sum_x = torch.zeros(p, dtype=torch.float64, device=device)
+    xtx = torch.zeros(p, p, dtype=torch.float32, device=device)
     K.calibrate_accumulate(views, mine, which, sum_x, xtx, inv_freq=inv_freq, pairing=pairing)
     n = allreduce_calibration(sum_x, xtx, len(mine), group) if world > 1 else len(mine)
     return K.calibrate_finalize(views[0].shape, which, sum_x, xtx, n, rank_cap, inv_freq=inv_freq, pairing=pairing)

@@ -69,3 +69,92 @@ def test_lpt_assignment_balances():
         loads = [sum(lens[i] for i in part) for part in a]
         assert max(loads) - min(loads) <= max(lens)              # LPT bound
         assert max(loads) / (sum(lens) / world) < 1.02
+
+
+class _HostCalibration:
+    """The two calls calibrate_distributed makes on the binding, computed on the
+    host (the CPU stand-in for kvtc_calibrate_accumulate / _finalize): rows via
+    the oracle's gather (keys un-RoPE'd, R1) rounded to bf16 like the GPU's
+    gathered X; sum_x in fp64, X^T X in fp32; finalize = eigh of
+    X^T X - n mu mu^T, descending, canonical sign (Q13)."""
+
+    def __init__(self, caches):
+        self.caches = caches
+
+    def calibrate_accumulate(self, views, samples, which, sum_x, xtx, inv_freq=None, pairing=0):
+        from oracle import numerics as ON
+        from oracle import pca as OPCA
+        C = OPCA.gather(self.caches, samples, which == 0, inv_freq, pairing)
+        C = ON.bf16(C)
+        sum_x += torch.from_numpy(C.sum(0))
+        Xf = torch.from_numpy(C).float()
+        xtx += Xf.T @ Xf
+
+    def calibrate_finalize(self, shape, which, sum_x, xtx, n, rank_cap, inv_freq=None, pairing=0):
+        mu = sum_x.numpy() / n
+        S = xtx.double().numpy() - n * np.outer(mu, mu)
+        w, V = np.linalg.eigh(S)
+        order = np.argsort(-w, kind="stable")
+        r = min(rank_cap, n - 1, len(mu))
+        V = V[:, order[:r]]
+        idx = np.argmax(np.abs(V), axis=0)
+        V = V * np.sign(V[idx, np.arange(r)])
+        return mu, V, np.sqrt(np.maximum(w[order[:r]], 0))
+
+
+class _View:
+    def __init__(self, shape):
+        self.shape = shape
+
+
+def _calib_worker(rank, world, port, caches, samples, invf, ret):
+    from paper_2511_01815_b200.distributed import calibrate_distributed
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    l, t, h, d = caches[0][0][0].shape
+    K = _HostCalibration(caches)
+    out = {}
+    for which in (0, 1):
+        cs = [(c[which], p0) for c, p0 in caches]
+        K.caches = cs
+        out[which] = calibrate_distributed(K, [_View((l, h, d))], samples, which, 64, inv_freq=invf, device="cpu")
+    # a layer shard (local=True) uses its own draw only, with no collective
+    K.caches = [(c[1], p0) for c, p0 in caches]
+    out["local"] = calibrate_distributed(K, [_View((l, h, d))], samples[rank::world], 1, 64, device="cpu", local=True)
+    ret[rank] = out
+    dist.destroy_process_group()
+
+
+def test_calibrate_distributed_world2_equals_single_process():
+    """The real orchestration (paper_2511_01815_b200.distributed.calibrate_distributed:
+    shard the draw -> accumulate -> all-reduce sum_x, X^T X, n -> finalize) over
+    gloo with world size 2: both ranks finalise the identical basis, equal to the
+    oracle's fit of the whole draw."""
+    from kvtc_inputs import generate, make_spec, sample_positions
+    from oracle import numerics as ON
+    from oracle import pca as OPCA
+    spec = make_spec("toy")
+    invf = spec.inv_freq().double().numpy()
+    caches = [((generate(spec, 0, 700, conversation=c).double().numpy(),
+                generate(spec, 1, 700, conversation=c).double().numpy()), 0) for c in (40, 41)]
+    caches = [((k, v), p0) for (k, v), p0 in caches]
+    samples = sample_positions([700, 700], 900, sinks=4, seed=3)
+    port = _free_port()
+    mgr = mp.Manager()
+    ret = mgr.dict()
+    mp.spawn(_calib_worker, args=(2, port, [((k, v), p0) for (k, v), p0 in caches], samples, invf, ret),
+             nprocs=2, join=True)
+    for which in (0, 1):
+        mu0, V0, s0 = ret[0][which]
+        mu1, V1, s1 = ret[1][which]
+        np.testing.assert_array_equal(V0, V1)
+        np.testing.assert_array_equal(mu0, mu1)
+        C = ON.bf16(OPCA.gather([(c[which], p0) for c, p0 in caches], samples, which == 0, invf))
+        ob = OPCA.fit(C, 64)
+        np.testing.assert_allclose(mu0, ob.mu, rtol=1e-6, atol=1e-6)
+        np.testing.assert_allclose(s0[:16], ob.sigma[:16], rtol=1e-4)
+        cos = np.abs(np.sum(V0[:, :8] * ob.V[:, :8], axis=0))
+        assert np.all(cos > 0.999), cos
+    # local=True: each rank's basis is its own half of the draw (they differ)
+    assert not np.array_equal(ret[0]["local"][1], ret[1]["local"][1])

@@ -169,3 +169,16 @@ def test_reconstruct_inverts_projection_and_truncation_error():
     keep = [0, 2]
     Xh = PCA.reconstruct(b, D[:, keep], cols=keep)
     np.testing.assert_array_equal(np.sum((X - Xh) ** 2, axis=1), np.sum(D[:, [1, 3]] ** 2, axis=1))
+
+
+def test_fit_svd_equals_fit():
+    """fit_svd (SVD of C - mu, P:L226-229 literally) and fit (eigh of the
+    covariance) give the same sigma and, where the spectrum has gaps, the same
+    directions with the same canonical sign."""
+    rng = np.random.default_rng(5)
+    n, p = 300, 40
+    A = rng.standard_normal((n, p)) * (1.0 + np.arange(p)) ** -1.0 * 4 + rng.normal(0, 1, p)
+    a, b = PCA.fit(A, 30), PCA.fit_svd(A, 30)
+    np.testing.assert_allclose(b.sigma, a.sigma, rtol=1e-10)
+    np.testing.assert_array_equal(a.mu, b.mu)
+    np.testing.assert_allclose(b.V, a.V, atol=2e-6)       # both fp32 masters
