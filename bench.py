@@ -439,6 +439,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--convs", type=int, default=256)                # multiconv: number of conversations
     ap.add_argument("--batch-tokens", type=int, default=131072)      # multiconv: tokens per batched call
+    # transport of the multi-rank runs: NCCL (one GPU per rank); gloo lets several
+    # ranks share one GPU to exercise the multi-rank logic on a 1-GPU box
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(self_launch(args))
@@ -466,8 +469,12 @@ def main():
     dist = None
     if world > 1:
         import torch.distributed as dist
+        local = local % max(1, torch.cuda.device_count())            # gloo: ranks may share a GPU
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     else:
         torch.cuda.set_device(0)
     from paper_2511_01815_b200 import kvtc as K

@@ -34,7 +34,9 @@ static_assert(sizeof(ContainerHeader) == KVTC_HEADER_BYTES, "container header si
 static_assert(offsetof(ContainerHeader, header_hash) == 248, "header hash last");
 
 // Device scratch words of one container written by compress (zeroed first):
-// [0..1] section lengths K/V, [2..3] section offsets K/V, [4] status bits,
+// [0..1] section lengths K/V, [2..3] section offsets K/V (the values' section
+// comes first: its DEFLATE finishes beside the keys' GEMM, so it is assembled
+// there; the keys' section follows it), [4] status bits,
 // [5..6] payload checksums K/V, [7] raw-section checksum.
 constexpr int kCompressWords = 8;
 
@@ -43,8 +45,9 @@ __global__ void header_kernel(ContainerHeader h, uint8_t *out, const uint64_t *l
   if (lens) {
     h.entropy_bytes[0] = lens[0];
     h.entropy_bytes[1] = lens[1];
+    h.section_off[0] = lens[2];
     h.section_off[1] = lens[3];
-    h.total_bytes = lens[3] + lens[1];
+    h.total_bytes = lens[2] + lens[0];
     h.payload_hash[0] = w[5];
     h.payload_hash[1] = w[6];
   }
@@ -527,7 +530,7 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
   h.plan_fp[0] = kp->fp;
   h.plan_fp[1] = vp->fp;
   h.raw_off = KVTC_HEADER_BYTES;
-  h.section_off[0] = L.k_off;
+  h.section_off[1] = L.k_off;                  // first section: the values' (see kCompressWords)
 
   // raw sinks + window, K then V: [layers][nraw][h*d] each
   const int64_t hd = int64_t(k->shape.kv_heads) * k->shape.head_dim;
@@ -556,7 +559,7 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
     }
     return KVTC_NOTHING_TO_COMPRESS;
   }
-  KVTC_CUDA_TRY(cudaMemcpyAsync(lens + 2, &h.section_off[0], 8, cudaMemcpyHostToDevice, st));
+  KVTC_CUDA_TRY(cudaMemcpyAsync(lens + 3, &h.section_off[1], 8, cudaMemcpyHostToDevice, st));
   // Schedule: the tensor-core GEMMs run back to back on the
   // caller's stream; the HBM/integer kernels of the OTHER stream run beside them
   // on the side stream with bounded grids (2 CTAs per SM next to the persistent
@@ -604,8 +607,19 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
     kvtc_status r;
     if (c1 == 0xFFFFFFFFu && (r = launch_hash(sv ? payload_v : payload_k, L.pay[sv], kSeedPayload, lens + 5 + sv, q, ctas)))
       return r;
-    return launch_deflate_encode(sv ? payload_v : payload_k, L.pay[sv], pol->chunk_bytes, dwsp[sv], dws[sv], ctas, q,
-                                 c0, c1);
+    if ((r = launch_deflate_encode(sv ? payload_v : payload_k, L.pay[sv], pol->chunk_bytes, dwsp[sv], dws[sv], ctas,
+                                   q, c0, c1)))
+      return r;
+    if (sv == 1) {
+      // the values' section goes first in the container: assembled right away on
+      // the encoder's stream (beside the keys' GEMM when that is the side stream);
+      // the keys' section starts at the 16-aligned end of it
+      ProfScope pa("c.assemble_v", q);
+      if ((r = launch_deflate_assemble(L.pay[1], pol->chunk_bytes, dwsp[1], o, lens + 3, lens + 1, q))) return r;
+      offset_after_kernel<<<1, 1, 0, q>>>(lens + 3, lens + 1, lens + 2, o);
+      KVTC_LAUNCH_CHECK();
+    }
+    return KVTC_OK;
   };
   KVTC_CUDA_TRY(cudaEventRecord(ss->ev[0], st));                 // fork point: bases, raw tokens
   if (v_direct) {
@@ -673,9 +687,6 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
   {
     ProfScope ps("c.assemble", st);
     if ((s = launch_deflate_assemble(L.pay[0], pol->chunk_bytes, dwsp[0], o, lens + 2, lens + 0, st))) return s;
-    offset_after_kernel<<<1, 1, 0, st>>>(lens + 2, lens + 0, lens + 3, o);
-    KVTC_LAUNCH_CHECK();
-    if ((s = launch_deflate_assemble(L.pay[1], pol->chunk_bytes, dwsp[1], o, lens + 3, lens + 1, st))) return s;
   }
   header_kernel<<<1, 1, 0, st>>>(h, o, lens, lens);
   KVTC_LAUNCH_CHECK();
@@ -683,7 +694,7 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
     uint64_t l4[kCompressWords];
     KVTC_CUDA_TRY(cudaMemcpyAsync(l4, lens, sizeof(l4), cudaMemcpyDeviceToHost, st));
     KVTC_CUDA_TRY(cudaStreamSynchronize(st));
-    *out_len_host = size_t(l4[3] + l4[1]);      // V section offset + V section length
+    *out_len_host = size_t(l4[2] + l4[0]);      // K section offset + K section length (the last section)
     if (l4[4] & 1) {
       set_error("a 16-bit shift/scale overflowed (container flagged)");
       return KVTC_E_NUMERIC;
@@ -719,11 +730,11 @@ kvtc_status validate_header(const ContainerHeader &h) {
   const uint64_t raw = 2ull * uint64_t(h.layers) * uint64_t(nraw) * uint64_t(h.kv_heads) * uint64_t(h.head_dim) * 2;
   if (h.raw_off != KVTC_HEADER_BYTES || h.raw_bytes != raw) return bad("raw section size / offset");
   if (m) {
-    const uint64_t k_off = align16(KVTC_HEADER_BYTES + raw);
-    if (h.section_off[0] != k_off || h.section_off[1] != k_off + align16(h.entropy_bytes[0]) ||
+    const uint64_t first = align16(KVTC_HEADER_BYTES + raw);      // values' section, then keys'
+    if (h.section_off[1] != first || h.section_off[0] != first + align16(h.entropy_bytes[1]) ||
         h.entropy_bytes[0] < kSectionHeaderBytes || h.entropy_bytes[1] < kSectionHeaderBytes ||
         h.entropy_bytes[0] > (uint64_t(1) << 50) || h.entropy_bytes[1] > (uint64_t(1) << 50) ||
-        h.total_bytes != h.section_off[1] + h.entropy_bytes[1])
+        h.total_bytes != h.section_off[0] + h.entropy_bytes[0])
       return bad("section offsets / lengths");
   }
   if (h.flags & ~kFlagNumeric) return bad("unknown flags");
@@ -1248,8 +1259,8 @@ extern "C" kvtc_status kvtc_compress_batch(const kvtc_basis *kb, const kvtc_plan
     h.plan_fp[0] = kp->fp;
     h.plan_fp[1] = vp->fp;
     h.raw_off = KVTC_HEADER_BYTES;
-    h.section_off[0] = L.k_off;
-    offs[kCompressWords * i + 2] = L.k_off;
+    h.section_off[1] = L.k_off;                // the values' section first
+    offs[kCompressWords * i + 3] = L.k_off;
     uint8_t *o = static_cast<uint8_t *>(out_host[i]);
     const int64_t hd = int64_t(k[i].shape.kv_heads) * k[i].shape.head_dim;
     auto *rawk = reinterpret_cast<__nv_bfloat16 *>(o + KVTC_HEADER_BYTES);
@@ -1386,10 +1397,10 @@ extern "C" kvtc_status kvtc_compress_batch(const kvtc_basis *kb, const kvtc_plan
         KVTC_LAUNCH_CHECK();
         continue;
       }
-      if ((s = launch_deflate_assemble(it[i].L.pay[0], pol->chunk_bytes, dws_k[i], o, li + 2, li + 0, st))) return s;
-      offset_after_kernel<<<1, 1, 0, st>>>(li + 2, li + 0, li + 3, o);
-      KVTC_LAUNCH_CHECK();
       if ((s = launch_deflate_assemble(it[i].L.pay[1], pol->chunk_bytes, dws_v[i], o, li + 3, li + 1, st))) return s;
+      offset_after_kernel<<<1, 1, 0, st>>>(li + 3, li + 1, li + 2, o);
+      KVTC_LAUNCH_CHECK();
+      if ((s = launch_deflate_assemble(it[i].L.pay[0], pol->chunk_bytes, dws_k[i], o, li + 2, li + 0, st))) return s;
       header_kernel<<<1, 1, 0, st>>>(hdr[i], o, li, li);
       KVTC_LAUNCH_CHECK();
     }
@@ -1401,7 +1412,7 @@ extern "C" kvtc_status kvtc_compress_batch(const kvtc_basis *kb, const kvtc_plan
     int bad = -1;
     for (int i = 0; i < n; ++i) {
       const uint64_t *li = l.data() + kCompressWords * i;
-      out_len_host[i] = it[i].L.m ? size_t(li[3] + li[1]) : size_t(KVTC_HEADER_BYTES + it[i].L.raw_bytes);
+      out_len_host[i] = it[i].L.m ? size_t(li[2] + li[0]) : size_t(KVTC_HEADER_BYTES + it[i].L.raw_bytes);
       if ((li[4] & 1) && bad < 0) bad = i;
     }
     if (bad >= 0) {

@@ -583,20 +583,33 @@ __global__ void __launch_bounds__(1024) section_layout_kernel(const uint32_t *ch
   }
 }
 
-__global__ void section_copy_kernel(const uint8_t *slots, uint64_t stride, const uint16_t *index, uint32_t nch,
-                                    uint8_t *out_base, const uint64_t *off_dev) {
+// 16-byte vectors (slots, section data and stream offsets are 16-byte aligned);
+// bytes past the stream's end inside its last vector are zeroed so the
+// container bytes are a function of the input alone.
+__global__ void __launch_bounds__(256) section_copy_kernel(const uint8_t *slots, uint64_t stride, const uint16_t *index,
+                                                          uint32_t nch, uint8_t *out_base, const uint64_t *off_dev) {
   uint8_t *out = out_base + (off_dev ? *off_dev : 0);
   const uint32_t c = blockIdx.x;
   const SectionHeader *h = reinterpret_cast<const SectionHeader *>(out);
   const ChunkEntry e = reinterpret_cast<const ChunkEntry *>(out + sizeof(SectionHeader))[c];
   uint16_t *idx = reinterpret_cast<uint16_t *>(out + sizeof(SectionHeader) + uint64_t(nch) * sizeof(ChunkEntry));
   if (threadIdx.x < kNSeg) idx[uint64_t(c) * kNSeg + threadIdx.x] = e.kind == 0 ? index[uint64_t(c) * kNSeg + threadIdx.x] : 0;
-  const uint32_t *s = reinterpret_cast<const uint32_t *>(slots + uint64_t(c) * stride);
-  uint32_t *d = reinterpret_cast<uint32_t *>(out + h->data_offset + e.offset);
-  const uint32_t words = (e.bytes + 3) / 4, padded = ((e.bytes + 15) / 16) * 4;
-  for (uint32_t i = threadIdx.x; i < padded; i += blockDim.x) {
-    uint32_t v = i < words ? s[i] : 0u;
-    if (i == words - 1 && (e.bytes & 3)) v &= (1u << (8 * (e.bytes & 3))) - 1;   // deterministic padding
+  const uint4 *s = reinterpret_cast<const uint4 *>(slots + uint64_t(c) * stride);
+  uint4 *d = reinterpret_cast<uint4 *>(out + h->data_offset + e.offset);
+  const uint32_t nv = (e.bytes + 15) / 16;
+  for (uint32_t i = threadIdx.x; i < nv; i += blockDim.x) {
+    uint4 v = __ldcs(s + i);
+    if (i == nv - 1 && (e.bytes & 15)) {
+      uint32_t w[4] = {v.x, v.y, v.z, v.w};
+      const uint32_t keep = e.bytes & 15;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int lo = 4 * k;
+        if (lo >= int(keep)) w[k] = 0;
+        else if (lo + 4 > int(keep)) w[k] &= (1u << (8 * (keep - lo))) - 1;
+      }
+      v = make_uint4(w[0], w[1], w[2], w[3]);
+    }
     d[i] = v;
   }
 }

@@ -124,12 +124,33 @@ def fp32_dot_bound(X, Vc_cols, bias_cols, D_ref):
     return worst, typical
 
 
+def boundary_spacing(D_ref, shift, scale, t):
+    """Distance between the two decision boundaries that enclose each oracle
+    coefficient (D units): int-k: one quantisation step (= scale); fp8: the E4M3
+    grid step of the interval holding (x - shift)/scale, times scale.  inf for
+    constant groups (scale 0: every value codes to 0)."""
+    sc = scale[:, None]
+    if t in (T2, T4):
+        return np.where(sc == 0, np.inf, np.broadcast_to(sc, D_ref.shape))
+    from oracle.numerics import E4M3_VALUES
+    vals = np.sort(np.unique(E4M3_VALUES[~np.isnan(E4M3_VALUES)]))
+    y = (D_ref - shift[:, None]) / np.where(sc == 0, 1.0, sc)
+    k = np.clip(np.searchsorted(vals, y), 1, len(vals) - 1)
+    step = vals[k] - vals[k - 1]
+    return np.where(sc == 0, np.inf, step * np.where(sc == 0, 1.0, sc))
+
+
 def codes_parity(payload_gpu, groups, D_ref, m, X, basis, cols):
-    """GPU codes vs oracle codes from the fp64 D.  Every mismatch must sit within
-    the worst-case fp32 accumulation bound of a decision boundary, or be where the
-    GPU's fp16 shift/scale differ from the oracle's (fp32 vs fp64 evaluation of
-    the same formula).  Returns (total, mismatches, unexplained, beyond_typical,
-    per-type counts)."""
+    """GPU codes vs oracle codes from the fp64 D.  A mismatch is explained when
+    the oracle coefficient lies within the worst-case fp32 accumulation bound of
+    a decision boundary, or when the GPU's fp16 shift/scale differ from the
+    oracle's (fp32 vs fp64 evaluation of the same formula).  Per type also the
+    LIMIT of DESIGN.md §7: sum over codes of min(1, 2 tau / spacing), tau = the
+    typical fp32 error of that coefficient, spacing = the distance between the
+    two decision boundaries around it — the expected number of codes whose
+    boundary lies within tau of the exact value, an upper bound on the flips an
+    error of size tau can cause.  Returns (total, mismatches, unexplained,
+    beyond_typical, {type: (mismatches, codes, limit)})."""
     sh_g, sc_g, cd_g = OL.unpack(groups, payload_gpu, m)
     Vc = basis.Vc[:, cols]
     bias = basis.mu @ Vc
@@ -143,31 +164,37 @@ def codes_parity(payload_gpu, groups, D_ref, m, X, basis, cols):
         bad = cd != cd_g[g]
         dist = boundary_distance(D_ref[:, off:off + z], sh, sc, t)
         ok = (dist <= worst[:, off:off + z]) | ~same_f[:, None]
+        limit = float(np.sum(np.minimum(1.0, 2 * typical[:, off:off + z] /
+                                        boundary_spacing(D_ref[:, off:off + z], sh, sc, t))))
         total += cd.size
         mism += int(bad.sum())
         unexplained += int((bad & ~ok).sum())
         beyond += int((bad & same_f[:, None] & (dist > typical[:, off:off + z])).sum())
-        a, b = per.get(t, (0, 0))
-        per[t] = (a + int(bad.sum()), b + cd.size)
+        a, b, c = per.get(t, (0, 0, 0.0))
+        per[t] = (a + int(bad.sum()), b + cd.size, c + limit)
         off += z
     return total, mism, unexplained, beyond, per
 
 
-
 def assert_codes_parity(payload_gpu, groups, D_ref, m, X, basis, cols, label=""):
-    """The code-parity gate.  Every mismatch must lie within the
-    TYPICAL fp32 accumulation error (sqrt(K) 2^-24 sum|x v|, K = p terms) of a
-    decision boundary, or sit where the fp16 factors differ (fp32 vs fp64
-    evaluation of the same formula): no other mismatch is tolerated.  Aggregate
-    agreement >= 99.5 %: at K = 32768 the codes within that error of a boundary
-    are ~0.1-0.3 % of the fp8/int4 codes, so the north star's 99.99 % is not
-    reachable with an fp32-accumulated projection (measured: 100 % at toy size,
-    99.84 % at the Llama shape)."""
+    """The code-parity gate of DESIGN.md §7, per element type:
+      (1) every mismatch lies within the TYPICAL fp32 accumulation error
+          tau = sqrt(K) 2^-24 sum|x v| (+ the bias / output rounding) of a
+          decision boundary, or sits where the fp16 factors differ;
+      (2) mismatches of type t <= max(2, limit_t), limit_t = sum over its codes of
+          min(1, 2 tau / spacing) (see codes_parity): what an fp32-accumulated
+          projection can flip.  At K = p = 32768 that is ~0.1-0.5 % of the
+          int4 / fp8 codes, so the north star's >= 99.99 % agreement is not
+          reachable without a wider accumulator (measured per type in
+          profiles/r02_code_parity.md)."""
     total, mism, unexplained, beyond, per = codes_parity(payload_gpu, groups, D_ref, m, X, basis, cols)
+    names = {T2: "int2", T4: "int4", T8: "fp8"}
+    desc = ", ".join(f"{names[t]} {a}/{b} ({a / max(b, 1):.2e}, limit {c:.1f})" for t, (a, b, c) in sorted(per.items()))
     print(f"\n[codes] {label} total={total} mismatches={mism} ({mism / max(total, 1):.2e}) "
-          f"beyond-typical={beyond} per-type={per}")
+          f"beyond-typical={beyond} per-type: {desc}")
     assert unexplained == 0 and beyond == 0, (mism, unexplained, beyond, total)
-    assert mism <= max(2, 5e-3 * total), (mism, total)
+    for t, (a, b, c) in per.items():
+        assert a <= max(2.0, c), (names[t], a, b, c)
 
 
 def oracle_restore(buf: bytes, kb, okp, vb, ovp, invf):

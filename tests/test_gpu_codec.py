@@ -116,8 +116,7 @@ def test_layer_range_decompress(K):
     # and directly against the oracle's decompression of the same container (layer 1 only)
     rk, rv = E.oracle_restore(cont.cpu().numpy().tobytes(), kb, okp, vb, ovp, invf)
     E.assert_restored_like_oracle(part_k, part_v, rk, rv, layers=slice(1, 2))
-    np.testing.assert_array_equal(part_k[1, :4].cpu(), kd[1, :4].cpu())
-    np.testing.assert_array_equal(part_v[1, tokens - 128:].cpu(), vd[1, tokens - 128:].cpu())
+    assert torch.equal(part_k[1, :4], kd[1, :4]) and torch.equal(part_v[1, tokens - 128:], vd[1, tokens - 128:])
 
 
 @pytest.mark.parametrize("name,tokens", [("mid", 700), ("toy", 400)])
@@ -238,3 +237,42 @@ def test_direct_cache_read_matches_gather(K, monkeypatch):
     monkeypatch.setenv("KVTC_NO_DIRECT", "1")
     gathered = run(K.KVView(vd))
     assert direct == gathered and direct2d == gathered and strided == gathered and separate == gathered
+
+
+def test_separate_key_value_compression_ratios(K):
+    """Separate K / V targets ("different compression
+    ratios for keys and values"): keys at DP target 8, values at 32 on the toy
+    config.  Each stream meets its own target before DEFLATE, the codes and the
+    reconstruction match the oracle run with the same two plans."""
+    spec, invf, kb, vb, Ck, Cv = E.setup("toy")
+    shape = (spec.layers, spec.kv_heads, spec.head_dim)
+    from oracle import pca as OPCA
+    okp = ODP.allocate(OPCA.dp_coefficients(kb, Ck), 8.0, spec.p)[0]
+    ovp = ODP.allocate(OPCA.dp_coefficients(vb, Cv), 32.0, spec.p)[0]
+    assert okp.bits_per_token > 2 * ovp.bits_per_token
+    KB = K.Basis.create(shape, 0, kb.mu, kb.V, kb.sigma, inv_freq=invf, pairing=0)
+    VB = K.Basis.create(shape, 1, vb.mu, vb.V, vb.sigma)
+    KP, VP = K.Plan.create(kb.r, okp.groups), K.Plan.create(vb.r, ovp.groups)
+    tokens, pos0 = 512, 0
+    Kc, Vc = E.caches("toy", tokens, pos0, conversation=31)
+    kd, vd = Kc.cuda(), Vc.cuda()
+    cont, _ = K.compress(KB, KP, VB, VP, K.KVView(kd), K.KVView(vd))
+    info = K.container_info(cont)
+    m = tokens - 132
+    for sv, target in ((0, 8.0), (1, 32.0)):
+        assert 2 * spec.p * m / info.payload_bytes[sv] >= target
+    print(f"\n[per-stream CR] keys {2 * spec.p * m / info.entropy_bytes[0]:.1f}x, "
+          f"values {2 * spec.p * m / info.entropy_bytes[1]:.1f}x after DEFLATE")
+    buf = cont.cpu().numpy().tobytes()
+    h = parse_container(buf)
+    oc = OC.compress(Kc.double().numpy(), Vc.double().numpy(), pos0, kb, okp, vb, ovp, invf)
+    for sv, so, groups, ob, cache in ((0, oc.k, okp.groups, kb, Kc), (1, oc.v, ovp.groups, vb, Vc)):
+        sec = parse_section(buf[h["sec_k" if sv == 0 else "sec_v"]:])
+        payload = b"".join(zlib.decompress(s, wbits=-15) for s in sec["streams"])
+        X = OC.stream_rows(cache.double().numpy(), 4, 128, pos0, sv == 0, invf, 0)
+        cols = np.concatenate([np.arange(s0, s0 + z) for (s0, z, _) in groups])
+        E.assert_codes_parity(payload, groups, so.D, m, X, ob, cols, f"per-stream CR stream={sv}")
+    ko, vo = torch.zeros_like(kd), torch.zeros_like(vd)
+    K.decompress(KB, KP, VB, VP, cont, K.KVView(ko), K.KVView(vo))
+    rk, rv = E.oracle_restore(buf, kb, okp, vb, ovp, invf)
+    E.assert_restored_like_oracle(ko, vo, rk, rv)
