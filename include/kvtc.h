@@ -306,6 +306,14 @@ kvtc_status kvtc_decompress_batch(const kvtc_basis *kb, const kvtc_plan *kp, con
                                   const kvtc_plan *vp, const void *const *in_host, const size_t *in_len_host,
                                   int32_t n, const kvtc_kv_view *k_out, const kvtc_kv_view *v_out, void *workspace,
                                   size_t workspace_bytes, void *stream);
+/* As kvtc_decompress_batch without any host synchronisation: in_header_host[i]
+ * are host copies of the containers' headers; status_dev [n] (device int32)
+ * receives each item's integrity verdict (0 or KVTC_E_CORRUPT) on `stream`. */
+kvtc_status kvtc_decompress_batch_async(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb,
+                                        const kvtc_plan *vp, const void *const *in_host, const size_t *in_len_host,
+                                        const void *const *in_header_host, int32_t n, const kvtc_kv_view *k_out,
+                                        const kvtc_kv_view *v_out, int32_t *status_dev, void *workspace,
+                                        size_t workspace_bytes, void *stream);
 
 /* Parse a container header (first KVTC_HEADER_BYTES bytes, copied to host).
  * info is filled in any case; the status is the header validation (KVTC_OK,

@@ -94,6 +94,8 @@ _SIGS = {
                                   vp]),
     "kvtc_decompress_batch_workspace_bytes": (sz, [vp, vp, vp, vp, P(vp), i32]),
     "kvtc_decompress_batch": (i32, [vp, vp, vp, vp, P(vp), P(sz), i32, P(View), P(View), vp, sz, vp]),
+    "kvtc_decompress_batch_async": (i32, [vp, vp, vp, vp, P(vp), P(sz), P(vp), i32, P(View), P(View), vp, vp, sz,
+                                          vp]),
     "kvtc_container_parse": (i32, [vp, P(ContainerInfo)]),
     "kvtc_stage_gather": (i32, [P(View), i64, i64, i32, P(Rope), vp, vp]),
     "kvtc_stage_project": (i32, [vp, vp, vp, i64, vp, vp]),

@@ -1453,21 +1453,21 @@ extern "C" size_t kvtc_decompress_batch_workspace_bytes(const kvtc_basis *kb, co
   return b.used + 256;
 }
 
-extern "C" kvtc_status kvtc_decompress_batch(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb,
-                                             const kvtc_plan *vp, const void *const *in_host, const size_t *in_len_host,
-                                             int32_t n, const kvtc_kv_view *k_out, const kvtc_kv_view *v_out,
-                                             void *workspace, size_t workspace_bytes, void *stream) {
-  KVTC_CHECK_ARG(kb && kp && vb && vp && in_host && in_len_host && k_out && v_out && n > 0,
-                 "decompress_batch arguments");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
+namespace {
+__global__ void batch_status_kernel(const int32_t *ierr, int32_t n, int32_t *status_out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    status_out[i] = ierr[i] ? int32_t(KVTC_E_CORRUPT) : 0;
+}
+
+// The batched decompression of host header copies `hdr` (validated here);
+// status_dev (nullable): per-item verdicts written on the stream; otherwise the
+// caller synchronises and reads *ierr_out (the per-item error words).
+kvtc_status decompress_batch_core(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb, const kvtc_plan *vp,
+                                  const void *const *in_host, const size_t *in_len_host, int32_t n,
+                                  const kvtc_kv_view *k_out, const kvtc_kv_view *v_out,
+                                  std::vector<ContainerHeader> &hdr, int32_t *status_dev, void *workspace,
+                                  size_t workspace_bytes, cudaStream_t st, int32_t **ierr_out) {
   kvtc_status s;
-  // all headers in one device-to-host round trip
-  std::vector<ContainerHeader> hdr(n);
-  for (int i = 0; i < n; ++i) {
-    KVTC_CHECK_ARG(in_len_host[i] >= KVTC_HEADER_BYTES, "container too short");
-    KVTC_CUDA_TRY(cudaMemcpyAsync(&hdr[i], in_host[i], sizeof(ContainerHeader), cudaMemcpyDeviceToHost, st));
-  }
-  KVTC_CUDA_TRY(cudaStreamSynchronize(st));
   std::vector<BatchItem> it(n);
   std::vector<const void *> hptr(n);
   int64_t row = 0;
@@ -1514,7 +1514,8 @@ extern "C" kvtc_status kvtc_decompress_batch(const kvtc_basis *kb, const kvtc_pl
   float2 *cs = ws.take<float2>(rows * half);
   TileRef *d_tiles = ws.take<TileRef>(2 * ntiles);
   InflateJob *d_jobs = ws.take<InflateJob>(2 * int64_t(n));
-  int32_t *ierr = ws.take<int32_t>(n);                             // per item: checksum mismatch bits
+  int32_t *ierr = ws.take<int32_t>(n);                             // per item: inflate error / checksum bits
+  *ierr_out = ierr;
   uint64_t *hsum = ws.take<uint64_t>(3 * int64_t(n));              // [raw | K payload | V payload] per item
   uint64_t *hexp = ws.take<uint64_t>(3 * int64_t(n));
   HashJob *d_hj = ws.take<HashJob>(3 * int64_t(n));
@@ -1558,6 +1559,7 @@ extern "C" kvtc_status kvtc_decompress_batch(const kvtc_basis *kb, const kvtc_pl
         j.nch = uint32_t((h.payload_bytes[sv] + h.chunk_bytes - 1) / h.chunk_bytes);
         j.chunk0 = c0;
         j.out = sv ? pay_v[i] : pay_k[i];
+        j.err = ierr + i;
         c0 += j.nch;
         jobs.push_back(j);
       }
@@ -1669,21 +1671,62 @@ extern "C" kvtc_status kvtc_decompress_batch(const kvtc_basis *kb, const kvtc_pl
       }
     }
   }
-  // one synchronisation: the inflater's and every item's checksum status
-  std::vector<int32_t> st_host(n + 1);
-  KVTC_CUDA_TRY(cudaMemcpyAsync(st_host.data(), err, 4, cudaMemcpyDeviceToHost, st));
-  KVTC_CUDA_TRY(cudaMemcpyAsync(st_host.data() + 1, ierr, 4 * size_t(n), cudaMemcpyDeviceToHost, st));
-  KVTC_CUDA_TRY(cudaStreamSynchronize(st));
-  if (st_host[0]) {
-    set_error("corrupt container in the batch: DEFLATE stream error %d", st_host[0]);
-    return KVTC_E_CORRUPT;
+  (void)err;
+  if (status_dev) {
+    batch_status_kernel<<<unsigned(ceil_div(n, 256)), 256, 0, st>>>(ierr, n, status_dev);
+    KVTC_LAUNCH_CHECK();
   }
+  return KVTC_OK;
+}
+}  // namespace
+
+extern "C" kvtc_status kvtc_decompress_batch(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb,
+                                             const kvtc_plan *vp, const void *const *in_host, const size_t *in_len_host,
+                                             int32_t n, const kvtc_kv_view *k_out, const kvtc_kv_view *v_out,
+                                             void *workspace, size_t workspace_bytes, void *stream) {
+  KVTC_CHECK_ARG(kb && kp && vb && vp && in_host && in_len_host && k_out && v_out && n > 0,
+                 "decompress_batch arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // all headers in one device-to-host round trip
+  std::vector<ContainerHeader> hdr(n);
+  for (int i = 0; i < n; ++i) {
+    KVTC_CHECK_ARG(in_len_host[i] >= KVTC_HEADER_BYTES, "container too short");
+    KVTC_CUDA_TRY(cudaMemcpyAsync(&hdr[i], in_host[i], sizeof(ContainerHeader), cudaMemcpyDeviceToHost, st));
+  }
+  KVTC_CUDA_TRY(cudaStreamSynchronize(st));
+  int32_t *ierr = nullptr;
+  kvtc_status s = decompress_batch_core(kb, kp, vb, vp, in_host, in_len_host, n, k_out, v_out, hdr, nullptr, workspace,
+                                        workspace_bytes, st, &ierr);
+  if (s) return s;
+  // one synchronisation: every item's inflate / checksum status
+  std::vector<int32_t> st_host(n);
+  KVTC_CUDA_TRY(cudaMemcpyAsync(st_host.data(), ierr, 4 * size_t(n), cudaMemcpyDeviceToHost, st));
+  KVTC_CUDA_TRY(cudaStreamSynchronize(st));
   for (int i = 0; i < n; ++i)
-    if (st_host[1 + i]) {
-      set_error("batch item %d: corrupt container (checksum mismatch bits %d)", i, st_host[1 + i]);
+    if (st_host[i]) {
+      set_error("batch item %d: corrupt container (inflate / checksum status %d)", i, st_host[i]);
       return KVTC_E_CORRUPT;
     }
   return KVTC_OK;
+}
+
+extern "C" kvtc_status kvtc_decompress_batch_async(const kvtc_basis *kb, const kvtc_plan *kp, const kvtc_basis *vb,
+                                                   const kvtc_plan *vp, const void *const *in_host,
+                                                   const size_t *in_len_host, const void *const *in_header_host,
+                                                   int32_t n, const kvtc_kv_view *k_out, const kvtc_kv_view *v_out,
+                                                   int32_t *status_dev, void *workspace, size_t workspace_bytes,
+                                                   void *stream) {
+  KVTC_CHECK_ARG(kb && kp && vb && vp && in_host && in_len_host && in_header_host && k_out && v_out && n > 0 &&
+                     status_dev,
+                 "decompress_batch_async arguments");
+  std::vector<ContainerHeader> hdr(n);
+  for (int i = 0; i < n; ++i) {
+    KVTC_CHECK_ARG(in_len_host[i] >= KVTC_HEADER_BYTES && in_header_host[i], "container too short / no header");
+    memcpy(&hdr[i], in_header_host[i], sizeof(ContainerHeader));
+  }
+  int32_t *ierr = nullptr;
+  return decompress_batch_core(kb, kp, vb, vp, in_host, in_len_host, n, k_out, v_out, hdr, status_dev, workspace,
+                               workspace_bytes, static_cast<cudaStream_t>(stream), &ierr);
 }
 
 // ------------------------------------------------- calibration / allocation

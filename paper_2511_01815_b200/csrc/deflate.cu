@@ -1126,7 +1126,7 @@ __global__ void __launch_bounds__(kInfThreads) inflate_batch_kernel(const Inflat
       else hi = mid - 1;
     }
     const InflateJob jb = jobs[lo];
-    inflate_chunk(S, jb.section, jb.sec_len, jb.n_out, jb.nch, b - jb.chunk0, jb.out, err);
+    inflate_chunk(S, jb.section, jb.sec_len, jb.n_out, jb.nch, b - jb.chunk0, jb.out, jb.err ? jb.err : err);
     __syncthreads();
   }
 }

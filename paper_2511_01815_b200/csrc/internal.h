@@ -224,6 +224,7 @@ struct InflateJob {
   uint64_t n_out;
   uint32_t nch, chunk0;
   uint8_t *out;
+  int32_t *err;                    // this job's error word (nullable: the launch's)
 };
 kvtc_status launch_inflate_batch(const InflateJob *jobs_dev, int32_t njobs, uint32_t total_chunks, int32_t *err,
                                  cudaStream_t st);

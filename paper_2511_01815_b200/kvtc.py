@@ -369,6 +369,24 @@ def decompress_batch(kb: Basis, kp: Plan, vb: Basis, vp: Plan, containers: list,
                                       _ptr(workspace), workspace.numel(), _stream(stream)))
 
 
+def decompress_batch_async(kb: Basis, kp: Plan, vb: Basis, vp: Plan, containers: list, headers: list, k_outs: list,
+                           v_outs: list, status: torch.Tensor, stream=None, workspace=None):
+    """kvtc_decompress_batch_async: no host synchronisation; headers[i] = host
+    copies of the containers' first 256 bytes; status (device int32 [n]) gets each
+    item's verdict (0 or KVTC_E_CORRUPT)."""
+    n = len(containers)
+    hb = [C.create_string_buffer(h, len(h)) for h in headers]
+    hp = (C.c_void_p * n)(*[C.cast(b, C.c_void_p) for b in hb])
+    if workspace is None:
+        wsb = int(lib().kvtc_decompress_batch_workspace_bytes(kb.h, kp.h, vb.h, vp.h, hp, n))
+        workspace = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    assert status.dtype == torch.int32 and status.is_cuda and status.numel() >= n
+    ptrs = (C.c_void_p * n)(*[c.data_ptr() for c in containers])
+    lens = (C.c_size_t * n)(*[c.numel() for c in containers])
+    check(lib().kvtc_decompress_batch_async(kb.h, kp.h, vb.h, vp.h, ptrs, lens, hp, n, _views(k_outs), _views(v_outs),
+                                            _ptr(status), _ptr(workspace), workspace.numel(), _stream(stream)))
+
+
 def decompress_batch_workspace_bytes(kb, kp, vb, vp, headers: list) -> int:
     hb = [C.create_string_buffer(h, len(h)) for h in headers]
     hp = (C.c_void_p * len(headers))(*[C.cast(b, C.c_void_p) for b in hb])

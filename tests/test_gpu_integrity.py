@@ -236,3 +236,22 @@ def test_rope_is_part_of_the_basis_fingerprint(K):
             K.decompress(other, KP, VB, VP, cont, K.KVView(torch.zeros_like(Kc.cuda())),
                          K.KVView(torch.zeros_like(Vc.cuda())))
         assert ei.value.status == MISMATCH
+
+
+def test_batch_async_per_item_status(K, mid):
+    """kvtc_decompress_batch_async: no synchronisation, one verdict per item on
+    the stream — the damaged item is flagged, the intact one restores exactly."""
+    M = mid
+    buf = bytearray(M["cont"].cpu().numpy().tobytes())
+    h = parse_container(bytes(buf))
+    buf[h["sec_v"] + 9000] ^= 0x01
+    bad = torch.frombuffer(buf, dtype=torch.uint8).cuda()
+    hdr = M["cont"][:256].cpu().numpy().tobytes()
+    outs = [(torch.zeros_like(M["kd"]), torch.zeros_like(M["vd"])) for _ in range(2)]
+    status = torch.full((2,), 77, dtype=torch.int32, device="cuda")
+    K.decompress_batch_async(M["KB"], M["KP"], M["VB"], M["VP"], [M["cont"], bad], [hdr, hdr],
+                             [K.KVView(o[0], pos0=M["pos0"]) for o in outs],
+                             [K.KVView(o[1], pos0=M["pos0"]) for o in outs], status)
+    torch.cuda.synchronize()
+    assert status.tolist() == [0, CORRUPT]
+    assert torch.equal(outs[0][0], M["ref_k"]) and torch.equal(outs[0][1], M["ref_v"])
