@@ -426,6 +426,7 @@ def main():
     ap.add_argument("--config", default="llama8b", choices=sorted(DEFAULT_TOKENS))
     ap.add_argument("--tokens", type=int, default=None)               # default: per config (DEFAULT_TOKENS)
     ap.add_argument("--cr", type=float, default=16.0)
+    ap.add_argument("--chunk-bytes", type=int, default=65536)        # DEFLATE chunk (reading Q15)
     ap.add_argument("--cal-seqs", type=int, default=2)
     ap.add_argument("--cal-tokens", type=int, default=32768)
     ap.add_argument("--ncal", type=int, default=65000)
@@ -511,10 +512,10 @@ def main():
     kview, vview = K.KVView(Kc), K.KVView(Vc)
     Ko, Vo = torch.zeros_like(Kc), torch.zeros_like(Vc)
     koview, voview = K.KVView(Ko), K.KVView(Vo)
-    cap, wsb = K.compress_sizes(kb, kp, vb, vp, kview)
+    cap, wsb = K.compress_sizes(kb, kp, vb, vp, kview, chunk_bytes=args.chunk_bytes)
     cont = torch.empty(cap, dtype=torch.uint8, device="cuda")
     cws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
-    cont_valid, st = K.compress(kb, kp, vb, vp, kview, vview, out=cont, workspace=cws)
+    cont_valid, st = K.compress(kb, kp, vb, vp, kview, vview, out=cont, workspace=cws, chunk_bytes=args.chunk_bytes)
     info = K.container_info(cont_valid)
     hdr = cont[:256].cpu().numpy().tobytes()                  # the container header, read once (host copy)
     dws = torch.empty(K.decompress_workspace_bytes(kb, kp, vb, vp, hdr), dtype=torch.uint8, device="cuda")
@@ -531,7 +532,7 @@ def main():
         if mark:
             e = tuple(torch.cuda.Event(enable_timing=True) for _ in range(3))
             e[0].record(stream)
-        K.compress(kb, kp, vb, vp, kview, vview, out=cont, workspace=cws, sync_len=False)
+        K.compress(kb, kp, vb, vp, kview, vview, out=cont, workspace=cws, sync_len=False, chunk_bytes=args.chunk_bytes)
         if mark:
             e[1].record(stream)
         K.decompress_async(kb, kp, vb, vp, cont, hdr, koview, voview, dstatus, workspace=dws)
@@ -591,9 +592,10 @@ def main():
     ent = info.entropy_bytes[0] + info.entropy_bytes[1]
     rpad = [(x + 7) // 8 * 8 for x in rnz]
     # algorithmic bytes of each stage as the schedule runs it: the
-    # caller-stream DEFLATE and dequantisation handle the KEYS only (the values'
-    # run beside the keys' GEMM as the *_overlapped stages, whose time is shared
-    # with it); one inflate launch covers both streams
+    # caller-stream DEFLATE handles the KEYS only (the values' runs beside the keys'
+    # GEMM as the *_overlapped stage, whose time is shared with it); one inflate
+    # launch covers both streams; the keys' dequantisation runs on the caller's
+    # stream, the values' beside the keys' GEMM (KVTC_DQ_FUSED=1: inside the GEMM)
     stage_bytes = {"c.deflate": info.payload_bytes[0] + info.entropy_bytes[0],
                    "c.deflate_overlapped": info.payload_bytes[1] + info.entropy_bytes[1],
                    "d.inflate": pay + ent,
@@ -644,8 +646,8 @@ def main():
             alls.append(t0.elapsed_time(t2))
         streaming = {"first_layer_ms": statistics.median(firsts), "all_layers_ms": statistics.median(alls),
                      "layers": spec.layers,
-                     "what": "kvtc_decompress_begin (inflate + dequantise once) + kvtc_decompress_layers(0, 1): "
-                             "attention on layer 0 can start after first_layer_ms"}
+                     "what": "kvtc_decompress_begin (inflate + dequantise + checksums once) + "
+                             "kvtc_decompress_layers(0, 1): attention on layer 0 can start after first_layer_ms"}
 
     # ---- end to end through the public API with host buffers: every step copies
     # that step's K/V from pinned host memory to the device (H2D), compresses and
@@ -691,6 +693,7 @@ def main():
                 if i >= 2:
                     stream.wait_event(ev_out[sl])
                 K.compress(kb, kp, vb, vp, in_views[sl][0], in_views[sl][1], out=cont, workspace=cws,
+                           chunk_bytes=args.chunk_bytes,
                            sync_len=False)
                 K.decompress_async(kb, kp, vb, vp, cont, hdr, out_views[sl][0], out_views[sl][1], dstatus,
                                    workspace=dws)
@@ -746,7 +749,8 @@ def main():
                     sl = i % 2
                     if i >= 2:
                         stream.wait_event(ev_d[sl])          # container i-2 consumed from cbuf/cland
-                    K.compress(kb, kp, vb, vp, kv_in, vv_in, out=cbuf[sl], workspace=cws, sync_len=False)
+                    K.compress(kb, kp, vb, vp, kv_in, vv_in, out=cbuf[sl], workspace=cws, sync_len=False,
+                               chunk_bytes=args.chunk_bytes)
                     ev_c[sl].record(stream)
                     with torch.cuda.stream(d2h):
                         d2h.wait_event(ev_c[sl])
@@ -811,7 +815,8 @@ def main():
                                            "no collective)" if args.config == "llama70b_shard" else
                                            f"weak x{world} (one conversation per GPU; calibration all-reduced)"),
                            "l2": f"inputs {2 * 2 * p * t / 1e9:.1f} GB per step >> 126 MB L2 (no flush needed)",
-                           "cr": cr, "cr_pre_deflate": cr_pre, "r_eff": [kinfo.r_eff, vinfo.r_eff], "r_nz": rnz,
+                           "cr": cr, "cr_pre_deflate": cr_pre, "chunk_bytes": args.chunk_bytes,
+                           "r_eff": [kinfo.r_eff, vinfo.r_eff], "r_nz": rnz,
                            "setup_s": round(setup_s, 1), "setup": setup_info},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "layer_streaming": streaming,

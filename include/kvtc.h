@@ -352,6 +352,17 @@ size_t kvtc_payload_bytes(const kvtc_plan *plan, int64_t m);
 /* Quantise + pack from a given fp32 D [m x ncols(plan)] (SIMT reference kernel). */
 kvtc_status kvtc_stage_quantize_pack(const kvtc_plan *plan, const float *D, int64_t m, uint8_t *payload,
                                      void *stream);
+/* Joint cross-shard compression ("chunks could be compressed jointly";
+ * SURVEY §8(f)2): one basis over the features of all layer shards.  Shard g holds
+ * the gathered rows X [m x (feat_end - feat_begin)] bf16 of its features
+ * [feat_begin, feat_end) of the basis (multiples of 8); writes its partial
+ * projection D [m x ncols(plan)] fp32 = X V_c[feat_begin:feat_end, plan PCs], minus
+ * mu V_c when add_bias (exactly one shard).  The partials summed over the shards
+ * (a reduce-scatter over token rows) are kvtc_stage_project's D of the joint
+ * features, up to fp32 summation order.  Device pointers, caller-owned. */
+kvtc_status kvtc_stage_project_partial(const kvtc_basis *b, const kvtc_plan *plan, const void *X, int64_t m,
+                                       int32_t feat_begin, int32_t feat_end, int32_t add_bias, float *D,
+                                       void *stream);
 /* K2: fused tcgen05 projection + quantise + pack straight from TMEM. */
 kvtc_status kvtc_stage_project_quantize(const kvtc_basis *b, const kvtc_plan *plan, const void *X, int64_t m,
                                         uint8_t *payload, void *stream);
@@ -369,7 +380,8 @@ kvtc_status kvtc_stage_inflate(const uint8_t *section, size_t len, uint8_t *out,
 kvtc_status kvtc_stage_inflate_raw(const uint8_t *in, const int64_t *in_off, const int64_t *in_len,
                                    int32_t nstreams, uint8_t *out, const int64_t *out_off,
                                    const int64_t *out_len, int32_t *status_dev, void *stream);
-/* Unpack + dequantise: payload -> D^ [m x ld] fp16 (ld >= ncols(plan), even). */
+/* Unpack + dequantise: payload -> D^ [m x ld] fp16 (ld >= ncols(plan), even);
+ * D^ = fp16(code * scale + shift) rounded once (R5). */
 kvtc_status kvtc_stage_dequantize(const kvtc_plan *plan, const uint8_t *payload, int64_t m, uint16_t *Dh,
                                   int64_t ld, void *stream);
 /* K5: X^ = D^ V_d^T + mu for layers [layer_begin, layer_end), keys re-rotated
@@ -377,6 +389,14 @@ kvtc_status kvtc_stage_dequantize(const kvtc_plan *plan, const uint8_t *payload,
 kvtc_status kvtc_stage_reconstruct(const kvtc_basis *b, const kvtc_plan *plan, const uint16_t *Dh, int64_t ld,
                                    int64_t m, int64_t tok_begin, int32_t layer_begin, int32_t layer_end,
                                    const kvtc_kv_view *out, void *stream);
+/* D2 + K5 fused (the product path of kvtc_decompress): the same
+ * reconstruction with A = D^ dequantised from the payload (m tokens of 128-token
+ * tiles, as kvtc_stage_project_quantize writes it) by the GEMM's producer warps,
+ * never written to HBM.  Bitwise equal to kvtc_stage_dequantize followed by
+ * kvtc_stage_reconstruct. */
+kvtc_status kvtc_stage_reconstruct_payload(const kvtc_basis *b, const kvtc_plan *plan, const uint8_t *payload,
+                                           int64_t m, int64_t tok_begin, int32_t layer_begin, int32_t layer_end,
+                                           const kvtc_kv_view *out, void *stream);
 
 /* ------------------------------------------------------------- diagnostics
  * Per-stage device timing with CUDA events recorded on the caller's stream

@@ -109,6 +109,8 @@ _SIGS = {
     "kvtc_stage_inflate_raw": (i32, [vp, vp, vp, i32, vp, vp, vp, vp, vp]),
     "kvtc_stage_dequantize": (i32, [vp, vp, i64, vp, i64, vp]),
     "kvtc_stage_reconstruct": (i32, [vp, vp, vp, i64, i64, i64, i32, i32, P(View), vp]),
+    "kvtc_stage_reconstruct_payload": (i32, [vp, vp, vp, i64, i64, i32, i32, P(View), vp]),
+    "kvtc_stage_project_partial": (i32, [vp, vp, vp, i64, i32, i32, i32, vp, vp]),
     "kvtc_profile_enable": (None, [i32]),
     "kvtc_profile_read": (i32, [C.c_char_p, sz, P(f64), P(i32), i32]),
     "kvtc_launch_count": (i64, []),

@@ -246,6 +246,9 @@ kvtc_plan::~kvtc_plan() {
   cudaFree(d_gdesc);
   cudaFree(d_pgroups);
   cudaFree(d_codes_off_full);
+  cudaFree(d_dqcols);
+  cudaFree(d_dqchunks);
+  cudaFree(d_tail_cols);
   for (auto &kv : codes_off_last) cudaFree(kv.second);
   for (auto &kv : ops) {
     cudaFree(kv.second.VcT);
@@ -263,7 +266,15 @@ int64_t plan_tile_bytes(const kvtc_plan *pl, int64_t ntok) {
 namespace kvtc {
 kvtc_status plan_compile(kvtc_plan *pl) {
   const int G = int(pl->groups.size());
+  if (G > 65535) {
+    set_error("plan has %d non-None groups (at most 65535)", G);
+    return KVTC_E_INVALID;
+  }
   pl->G = G;
+  if (plan_tile_bytes(pl, kTileM) > (int64_t(1) << 31) - 1) {
+    set_error("plan bits per token too large for 32-bit tile offsets");
+    return KVTC_E_INVALID;
+  }
   int col = 0;
   pl->bits = 0;
   for (auto &g : pl->groups) {
@@ -283,8 +294,8 @@ kvtc_status plan_compile(kvtc_plan *pl) {
   }
   // segments: groups of <= 256 columns packed greedily into <= 256-column tiles;
   // wider groups (k * 256) become k pieces whose tiles store fp32 coefficients
-  // to a scratch, quantised afterwards by quant_wide_kernel (the row min/max
-  // spans the pieces).
+  // and row min/max to a scratch; the last piece to finish quantises the group
+  // in its epilogue (the row min/max spans the pieces).
   std::vector<SegDesc> segs;
   std::vector<GroupDesc> gd;
   std::vector<SegDesc> wide_segs;
@@ -293,7 +304,7 @@ kvtc_status plan_compile(kvtc_plan *pl) {
   SegDesc cur{-1, 0, 0, 0, -1};
   auto close = [&]() {
     if (cur.col0 >= 0 && cur.g_end > cur.g_begin) segs.push_back(cur);
-    cur = SegDesc{-1, 0, int32_t(gd.size()), int32_t(gd.size()), -1};
+    cur = SegDesc{-1, 0, int32_t(gd.size()), int32_t(gd.size()), -1, -1};
   };
   close();
   for (int g = 0; g < G; ++g) {
@@ -312,7 +323,7 @@ kvtc_status plan_compile(kvtc_plan *pl) {
         return KVTC_E_INVALID;
       }
       for (int q = 0; q < pg.size / kMaxTileN; ++q)
-        wide_segs.push_back(SegDesc{pg.col + q * kMaxTileN, kMaxTileN, 0, 0, wcol + q * kMaxTileN});
+        wide_segs.push_back(SegDesc{pg.col + q * kMaxTileN, kMaxTileN, 0, 0, wcol + q * kMaxTileN, int32_t(wide.size())});
       wide.push_back(WideDesc{g, pg.size, pg.type, pg.col, wcol, 0, off[g]});
       wcol += pg.size;
     }
@@ -338,6 +349,48 @@ kvtc_status plan_compile(kvtc_plan *pl) {
   if (G) {
     KVTC_CUDA_TRY(cudaMemcpy(pl->d_pgroups, pl->groups.data(), G * sizeof(PlanGroup), cudaMemcpyHostToDevice));
     KVTC_CUDA_TRY(cudaMemcpy(pl->d_codes_off_full, off.data(), G * sizeof(int64_t), cudaMemcpyHostToDevice));
+  }
+  // decompress A-operand columns (fused dequantising producer of K5): one entry
+  // per compacted column, padded with zero columns to whole 128-column stages
+  {
+    const int ncols = int(ceil_div(std::max(col, 1), 2 * kBlockK) * 2 * kBlockK);
+    std::vector<DqCol> dq(ncols, DqCol{0, 0, 0, 0, 0, 0, 0});
+    for (int g = 0; g < G; ++g) {
+      const PlanGroup &pg = pl->groups[g];
+      for (int j = 0; j < pg.size; ++j)
+        dq[pg.col + j] = DqCol{uint16_t(g), uint8_t(pg.type), 0, uint16_t(j), uint16_t(pg.size), int32_t(off[g]), 0};
+    }
+    std::vector<DqChunk> ch(ncols / 8, DqChunk{0, 0, 0, 0, 0, 0});
+    std::vector<int32_t> tail;
+    for (int c = 0; c < ncols; c += 8) {
+      const DqCol &d = dq[c];
+      DqChunk &k = ch[c / 8];
+      bool any = false;
+      for (int q = 0; q < 8; ++q) any |= dq[c + q].type != 0;
+      k.type = any ? uint8_t(d.type ? d.type : 0xFF) : 0;
+      if (c + 8 <= col && d.type && d.j % 8 == 0 && d.j + 8 <= d.size) {
+        dq[c].chunk = 1;
+        const int b = bits_of(d.type);
+        k.ok = 1;
+        k.code_base = d.off_full + d.j * b / 8;
+        k.par_base = 4 * d.gidx * kTileM;
+        k.stride = uint16_t(d.size * b / 8);
+      } else if (any) {
+        k.ok = 3;                       // dequantised by the pre-pass into the tail buffer
+        k.code_base = int32_t(tail.size()) * 16;
+        tail.push_back(c);
+      }
+    }
+    pl->dq_cols_n = ncols;
+    pl->n_tail = int32_t(tail.size());
+    if (!tail.empty()) {
+      KVTC_CUDA_TRY(cudaMalloc(&pl->d_tail_cols, tail.size() * sizeof(int32_t)));
+      KVTC_CUDA_TRY(cudaMemcpy(pl->d_tail_cols, tail.data(), tail.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
+    KVTC_CUDA_TRY(cudaMalloc(&pl->d_dqcols, ncols * sizeof(DqCol)));
+    KVTC_CUDA_TRY(cudaMemcpy(pl->d_dqcols, dq.data(), ncols * sizeof(DqCol), cudaMemcpyHostToDevice));
+    KVTC_CUDA_TRY(cudaMalloc(&pl->d_dqchunks, ch.size() * sizeof(DqChunk)));
+    KVTC_CUDA_TRY(cudaMemcpy(pl->d_dqchunks, ch.data(), ch.size() * sizeof(DqChunk), cudaMemcpyHostToDevice));
   }
   uint64_t h = 0xCBF29CE484222325ull;
   h = fnv1a(&pl->r, 4, h);

@@ -44,6 +44,11 @@ struct kvtc_plan {
   kvtc::GroupDesc *d_gdesc = nullptr;
   kvtc::PlanGroup *d_pgroups = nullptr;
   int64_t *d_codes_off_full = nullptr;
+  kvtc::DqCol *d_dqcols = nullptr;      // [r_nz rounded up to 128] decompress A-operand columns
+  kvtc::DqChunk *d_dqchunks = nullptr;  // [the same / 8] 8-column chunks (fused producer table)
+  int32_t dq_cols_n = 0;
+  int32_t n_tail = 0;                   // ok = 3 chunks (dequantised by the pre-pass)
+  int32_t *d_tail_cols = nullptr;
   std::map<int, int64_t *> codes_off_last;
   std::mutex mu;
   std::map<uint64_t, kvtc::Operands> ops;

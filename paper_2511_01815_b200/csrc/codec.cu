@@ -113,12 +113,13 @@ bool direct_view_map(const kvtc_kv_view &v, int64_t tok0, CUtensorMap *m, int64_
 }
 
 // X: the gathered rows [m x p], or nullptr with `direct` = the 3-D map of the
-// cache itself (rows = tokens tok0 ..).  wide: fp32 scratch [m x wide_cols] for
-// the plan's wide groups (nullptr if it has none).
+// cache itself (rows = tokens tok0 ..).  wide: scratch of wide_scratch_bytes(m,
+// wide_cols, nwide) bytes for the plan's wide groups (nullptr if it has none);
+// they are quantised inside the GEMM's epilogue.
 kvtc_status run_project_quant(const kvtc_basis *b, kvtc_plan *pl, const Operands *op, const void *X, int64_t m,
                               uint8_t *payload, float *wide, cudaStream_t st, const CUtensorMap *direct = nullptr,
                               int64_t tok0 = 0, int64_t ldx = 0, const TileRef *tiles = nullptr,
-                              int64_t layer_rows = 0, bool defer_wide = false, int32_t *status = nullptr) {
+                              int64_t layer_rows = 0, int32_t *status = nullptr) {
   if (m == 0 || pl->G == 0) return KVTC_OK;
   KVTC_CHECK_ARG(pl->nwide == 0 || wide, "wide-group scratch");
   CUtensorMap tA;
@@ -146,33 +147,55 @@ kvtc_status run_project_quant(const kvtc_basis *b, kvtc_plan *pl, const Operands
   a.ldd = pl->wide_cols;
   a.tiles = tiles;
   a.status = status;
-  if ((s = launch_gemm_project_quant(a, st))) return s;
-  // groups wider than a tile: quantised from the fp32 scratch (defer_wide: the
-  // caller launches run_quant_wide itself, e.g. on the side stream)
-  if (defer_wide) return KVTC_OK;
-  return launch_quant_wide(pl->d_wide, pl->nwide, wide, pl->wide_cols, 1, m, pl->tile_bytes, a.codes_off_last,
-                           payload, st, tiles, status);
+  a.wide = pl->d_wide;
+  a.nwide = pl->nwide;
+  return launch_gemm_project_quant(a, st);
 }
 
-kvtc_status run_quant_wide(kvtc_plan *pl, float *wide, int64_t m, uint8_t *payload, cudaStream_t st,
-                           int32_t *status) {
-  return launch_quant_wide(pl->d_wide, pl->nwide, wide, pl->wide_cols, 1, m, pl->tile_bytes,
-                           plan_codes_off_last(pl, m % kTileM), payload, st, nullptr, status);
+// The inverse path's A operand.  Default: the SIMT kernel dequantises into D^
+// (HBM, fp16) and the reconstruction GEMM reads it through TMA.  KVTC_DQ_FUSED=1:
+// the GEMM's producer warps dequantise straight into the shared-memory stages
+// (D^ never reaches HBM; bitwise equal output), for plans whose A-chunk table
+// fits in shared memory.  Measured 7-8x slower on the bench shape (48 ms vs
+// 6.3 ms per launch): the tensor core's operand reads leave the
+// producers' shared-memory stores too little bandwidth, so it stays opt-in.
+bool dq_fused_env() {
+  const char *e = getenv("KVTC_DQ_FUSED");
+  return e && e[0] == '1';
 }
+bool dq_fits(const kvtc_plan *pl) { return int64_t(pl->dq_cols_n) / 8 * int64_t(sizeof(DqChunk)) <= kDqTabMaxBytes; }
+bool dq_fused(const kvtc_plan *kp, const kvtc_plan *vp) { return dq_fused_env() && dq_fits(kp) && dq_fits(vp); }
 
-kvtc_status run_reconstruct(const kvtc_basis *b, const kvtc_plan *pl, const Operands *op, const __half *Dh,
+// The reconstruction GEMM (K5).  payload != nullptr (or tiles carrying payload
+// pointers, `fused`): A = D^ is dequantised from the payload inside the GEMM;
+// otherwise A is the fp16 D^ [m x ld] in HBM.
+kvtc_status run_reconstruct(const kvtc_basis *b, kvtc_plan *pl, const Operands *op, const __half *Dh,
                             int64_t ld, int64_t m, int64_t tok_begin, int32_t lb, int32_t le, const kvtc_kv_view *out,
                             __nv_bfloat16 *const *bases_dev, const float2 *cs, cudaStream_t st,
-                            const TileRef *tiles = nullptr) {
+                            const TileRef *tiles = nullptr, const uint8_t *payload = nullptr, bool fused = false,
+                            uint8_t *dq_tail = nullptr) {
   const int hd = b->shape.kv_heads * b->shape.head_dim;
   if (m == 0 || lb >= le) return KVTC_OK;
   GemmDecompressArgs a = {};
   CUtensorMap tA;
   // with an empty plan D^ has no columns: use a 1-column zero view (K = 0 -> only mu)
   const int64_t kcols = std::max<int64_t>(pl->r_nz, 1);
-  kvtc_status s = make_tmap_2d(&tA, Dh, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, uint64_t(kcols), uint64_t(m),
-                               uint64_t(ld) * 2, kBlockK, kTileM);
+  kvtc_status s = make_tmap_2d(&tA, fused ? static_cast<const void *>(b->d_mu) : Dh, CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                               uint64_t(kcols), uint64_t(fused ? 1 : m), fused ? uint64_t((kcols * 2 + 15) / 16 * 16)
+                                                                          : uint64_t(ld) * 2,
+                               kBlockK, kTileM);
   if (s) return s;
+  if (fused) {
+    a.payload = payload;
+    a.codes_off_full = pl->d_codes_off_full;
+    a.codes_off_last = plan_codes_off_last(pl, m % kTileM);
+    a.tile_bytes = pl->tile_bytes;
+    a.dqcols = pl->d_dqcols;
+    a.dqchunks = pl->d_dqchunks;
+    a.tail_cols = pl->d_tail_cols;
+    a.n_tail = pl->n_tail;
+    a.dq_tail = dq_tail;
+  }
   a.tmA = &tA;
   a.tmB = pl->r_nz ? &op->tm_Vd : &tA;
   a.K = pl->r_nz;
@@ -282,6 +305,47 @@ extern "C" kvtc_status kvtc_stage_project(const kvtc_basis *b, const kvtc_plan *
   return launch_gemm_project_f32(a, ncols, st);
 }
 
+// Joint cross-shard compression: the partial
+// projection of one layer shard, D_g = X_g V_c[f0:f1, plan PCs] (- mu V_c when
+// add_bias), fp32 [m x r_nz].  The shards' partials sum to kvtc_stage_project's
+// D of the joint features.
+extern "C" kvtc_status kvtc_stage_project_partial(const kvtc_basis *b, const kvtc_plan *plan, const void *X, int64_t m,
+                                                  int32_t feat_begin, int32_t feat_end, int32_t add_bias, float *D,
+                                                  void *stream) {
+  KVTC_CHECK_ARG(b && plan && X && D && m >= 0, "project_partial arguments");
+  KVTC_CHECK_ARG(0 <= feat_begin && feat_begin < feat_end && feat_end <= b->p && feat_begin % 8 == 0 &&
+                     (feat_end - feat_begin) % 8 == 0,
+                 "project_partial: feature range (multiples of 8 inside the basis)");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (m == 0) return KVTC_OK;
+  const Operands *op;
+  kvtc_status s = plan_operands(b, const_cast<kvtc_plan *>(plan), &op);
+  if (s) return s;
+  if (op->r_nz == 0) return KVTC_OK;
+  const int32_t pg = feat_end - feat_begin;
+  CUtensorMap tA, tB;
+  if ((s = tmap_X(&tA, X, m, pg))) return s;
+  if ((s = make_tmap_2d(&tB, op->VcT + feat_begin, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, uint64_t(pg), uint64_t(op->r_nz),
+                        uint64_t(b->p + kXPad) * 2, kBlockK, kMaxTileN / 2)))
+    return s;
+  float *zero = nullptr;
+  if (!add_bias) {
+    KVTC_CUDA_TRY(cudaMallocAsync(&zero, size_t(op->r_nz) * 4, st));
+    KVTC_CUDA_TRY(cudaMemsetAsync(zero, 0, size_t(op->r_nz) * 4, st));
+  }
+  GemmCompressArgs a = {};
+  a.tmA = &tA;
+  a.tmB = &tB;
+  a.K = pg;
+  a.m = m;
+  a.D = D;
+  a.ldd = op->r_nz;
+  a.bias = add_bias ? op->bias : zero;
+  s = launch_gemm_project_f32(a, op->r_nz, st);
+  if (zero) cudaFreeAsync(zero, st);
+  return s;
+}
+
 extern "C" kvtc_status kvtc_stage_quantize_pack(const kvtc_plan *plan, const float *D, int64_t m, uint8_t *payload,
                                                 void *stream) {
   KVTC_CHECK_ARG(plan && D && payload && m >= 0, "quantize_pack arguments");
@@ -303,7 +367,7 @@ extern "C" kvtc_status kvtc_stage_project_quantize(const kvtc_basis *b, const kv
   if (s) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   float *wide = nullptr;      // stream-ordered scratch for the wide groups
-  if (pl->nwide && m) KVTC_CUDA_TRY(cudaMallocAsync(&wide, size_t(m) * pl->wide_cols * sizeof(float), st));
+  if (pl->nwide && m) KVTC_CUDA_TRY(cudaMallocAsync(&wide, wide_scratch_bytes(m, pl->wide_cols, pl->nwide), st));
   s = run_project_quant(b, pl, op, X, m, payload, wide, st);
   if (wide) cudaFreeAsync(wide, st);
   return s;
@@ -379,13 +443,14 @@ extern "C" kvtc_status kvtc_stage_dequantize(const kvtc_plan *plan, const uint8_
                         static_cast<cudaStream_t>(stream));
 }
 
-extern "C" kvtc_status kvtc_stage_reconstruct(const kvtc_basis *b, const kvtc_plan *plan, const uint16_t *Dh,
-                                              int64_t ld, int64_t m, int64_t tok_begin, int32_t layer_begin,
-                                              int32_t layer_end, const kvtc_kv_view *out, void *stream) {
+namespace {
+kvtc_status stage_reconstruct(const kvtc_basis *b, const kvtc_plan *plan, const uint16_t *Dh, const uint8_t *payload,
+                              int64_t ld, int64_t m, int64_t tok_begin, int32_t layer_begin, int32_t layer_end,
+                              const kvtc_kv_view *out, void *stream) {
   kvtc_status s = check_view(out);
   if (s) return s;
-  KVTC_CHECK_ARG(b && plan && Dh && same_shape(out->shape, b->shape), "reconstruct arguments");
-  KVTC_CHECK_ARG(ld % 8 == 0 && ld >= plan->r_nz, "ld must be a multiple of 8 and >= plan columns");
+  KVTC_CHECK_ARG(b && plan && (Dh || payload) && same_shape(out->shape, b->shape), "reconstruct arguments");
+  KVTC_CHECK_ARG(payload || (ld % 8 == 0 && ld >= plan->r_nz), "ld must be a multiple of 8 and >= plan columns");
   KVTC_CHECK_ARG(0 <= layer_begin && layer_begin <= layer_end && layer_end <= b->shape.layers, "layer range");
   KVTC_CHECK_ARG(tok_begin >= 0 && tok_begin + m <= out->tokens, "token range");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -396,17 +461,34 @@ extern "C" kvtc_status kvtc_stage_reconstruct(const kvtc_basis *b, const kvtc_pl
   Bump need;
   need.take<void *>(b->shape.layers);
   need.take<float2>(m * half);
+  need.take<uint8_t>(payload ? dq_tail_bytes(m, pl->n_tail) : 0);
   void *scratch = nullptr;
   KVTC_CUDA_TRY(cudaMallocAsync(&scratch, need.used, st));
   Bump ws(scratch, need.used);
   auto *bases = ws.take<__nv_bfloat16 *>(b->shape.layers);
   float2 *cs = ws.take<float2>(m * half);
+  uint8_t *tail = ws.take<uint8_t>(payload ? dq_tail_bytes(m, pl->n_tail) : 0);
   if ((s = upload_bases(out, bases, st))) return s;
   if (b->has_rope && (s = rope_table_for(b, out->pos0 + tok_begin, m, cs, st))) return s;
   s = run_reconstruct(b, pl, op, reinterpret_cast<const __half *>(Dh), ld, m, tok_begin, layer_begin, layer_end, out,
-                      bases, cs, st);
+                      bases, cs, st, nullptr, payload, payload != nullptr, tail);
   cudaFreeAsync(scratch, st);
   return s;
+}
+}  // namespace
+
+extern "C" kvtc_status kvtc_stage_reconstruct(const kvtc_basis *b, const kvtc_plan *plan, const uint16_t *Dh,
+                                              int64_t ld, int64_t m, int64_t tok_begin, int32_t layer_begin,
+                                              int32_t layer_end, const kvtc_kv_view *out, void *stream) {
+  return stage_reconstruct(b, plan, Dh, nullptr, ld, m, tok_begin, layer_begin, layer_end, out, stream);
+}
+
+extern "C" kvtc_status kvtc_stage_reconstruct_payload(const kvtc_basis *b, const kvtc_plan *plan,
+                                                      const uint8_t *payload, int64_t m, int64_t tok_begin,
+                                                      int32_t layer_begin, int32_t layer_end, const kvtc_kv_view *out,
+                                                      void *stream) {
+  KVTC_CHECK_ARG(payload, "reconstruct_payload: null payload");
+  return stage_reconstruct(b, plan, nullptr, payload, 0, m, tok_begin, layer_begin, layer_end, out, stream);
 }
 
 // ================================================================== codec
@@ -456,8 +538,7 @@ extern "C" size_t kvtc_compress_workspace_bytes(const kvtc_basis *kb, const kvtc
   b.take<uint8_t>(L.pay[1] + 16);
   b.take<uint8_t>(deflate_workspace(L.pay[0], pol->chunk_bytes));
   b.take<uint8_t>(deflate_workspace(L.pay[1], pol->chunk_bytes));
-  b.take<float>(L.m * std::max(kp->wide_cols, vp->wide_cols));
-  b.take<float>(L.m * vp->wide_cols);                      // the values' own (quantised on the side stream)
+  b.take<uint8_t>(wide_scratch_bytes(L.m, std::max(kp->wide_cols, vp->wide_cols), std::max(kp->nwide, vp->nwide)));
   return b.used + 256;
 }
 
@@ -504,8 +585,9 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
   void *dwsp[2];
   dwsp[0] = ws.take<uint8_t>(dws[0]);
   dwsp[1] = ws.take<uint8_t>(dws[1]);
-  float *wide = ws.take<float>(L.m * std::max(kp->wide_cols, vp->wide_cols));
-  float *wide_v = ws.take<float>(L.m * vp->wide_cols);
+  // one scratch for both streams' wide groups (their GEMMs run one after the other on st)
+  float *wide = reinterpret_cast<float *>(
+      ws.take<uint8_t>(wide_scratch_bytes(L.m, std::max(kp->wide_cols, vp->wide_cols), std::max(kp->nwide, vp->nwide))));
   if ((s = upload_bases(k, kbases, st)) || (s = upload_bases(v, vbases, st))) return s;
   KVTC_CUDA_TRY(cudaMemsetAsync(lens, 0, kCompressWords * 8, st));
 
@@ -583,21 +665,17 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
     return launch_gather(*k, kbases, pol->sinks, L.m, cs, kb->pairing, X, q, ctas, ldx);
   };
   // rows [r0, r1) of a stream (r0 a multiple of the 128-token tile): payload tiles
-  // and wide-group scratch rows are addressed from r0
-  bool defer_v_wide = false;
+  // are addressed from r0; the wide-group scratch is per launch (launches on st
+  // run one after the other)
   auto gemm = [&](int sv, bool direct, int64_t r0 = 0, int64_t r1 = -1) -> kvtc_status {
     ProfScope ps("c.project_quant_gemm", st);
     if (r1 < 0) r1 = L.m;
     const kvtc_plan *pl = sv ? vpl : kpl;
     uint8_t *pay = (sv ? payload_v : payload_k) + (r0 / kTileM) * pl->tile_bytes;
-    float *wd = wide ? wide + r0 * pl->wide_cols : nullptr;      // scratch rows of stride wide_cols
-    // the values' wide groups go to their own scratch and are quantised on the side
-    // stream (before their DEFLATE) when the schedule overlaps it
-    if (sv && defer_v_wide) wd = wide_v;
-    return sv ? run_project_quant(vb, vpl, vop, X, r1 - r0, pay, wd, st, direct ? &tV : nullptr, pol->sinks + r0,
-                                  ldx, nullptr, v_layer_rows, defer_v_wide, cstatus)
-              : run_project_quant(kb, kpl, kop, X + r0 * ldx, r1 - r0, pay, wd, st, nullptr, 0, ldx, nullptr, 0,
-                                  false, cstatus);
+    return sv ? run_project_quant(vb, vpl, vop, X, r1 - r0, pay, wide, st, direct ? &tV : nullptr, pol->sinks + r0,
+                                  ldx, nullptr, v_layer_rows, cstatus)
+              : run_project_quant(kb, kpl, kop, X + r0 * ldx, r1 - r0, pay, wide, st, nullptr, 0, ldx, nullptr, 0,
+                                  cstatus);
   };
   // the payload checksum is taken on the encoder's stream right before the call
   // that encodes the last chunk range: the whole payload is complete there
@@ -628,7 +706,6 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
     // runs both encoders after the GEMMs instead of the values' beside the keys' GEMM
     const bool gather_side = ovl && env_flag("KVTC_C_GATHER_SIDE", true);
     const bool deflate_side = ovl && env_flag("KVTC_C_DEFLATE_SIDE", true);
-    defer_v_wide = deflate_side && vpl->nwide > 0;
     if (!gather_side && (s = gather_keys(st, 0, "c.gather_unrope"))) return s;
     if ((s = gemm(1, true))) return s;
     KVTC_CUDA_TRY(cudaEventRecord(ss->ev[2], st));               // V payload ready
@@ -656,10 +733,6 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
       return s;
     }
     if (deflate_side) {
-      if (defer_v_wide) {
-        ProfScope ps("c.quant_wide_overlapped", aux);
-        if ((s = run_quant_wide(vpl, wide_v, L.m, payload_v, aux, cstatus))) return s;
-      }
       if ((s = encode(1, aux, side_ctas, "c.deflate_overlapped"))) return s;
       if (split) {
         KVTC_CUDA_TRY(cudaStreamWaitEvent(aux, ss->ev[1], 0));
@@ -815,6 +888,7 @@ struct DecompWs {
   uint8_t *payloads[2];
   __half *Dh[2];
   float2 *cs;
+  uint8_t *tail;         // fused path: the pre-pass columns (shared by K and V, one GEMM at a time)
   int64_t ld;
 };
 DecompWs carve_decomp(const kvtc_plan *kp, const kvtc_plan *vp, const ContainerHeader &h, void *workspace,
@@ -828,9 +902,12 @@ DecompWs carve_decomp(const kvtc_plan *kp, const kvtc_plan *vp, const ContainerH
   w.payloads[0] = ws.take<uint8_t>(h.payload_bytes[0] + 16);
   w.payloads[1] = ws.take<uint8_t>(h.payload_bytes[1] + 16);
   w.ld = std::max(std::max(kp->r_nz_pad, vp->r_nz_pad), 8);
-  w.Dh[0] = ws.take<__half>(h.m * w.ld);
-  w.Dh[1] = ws.take<__half>(h.m * w.ld);
+  // D^ only exists in HBM on the unfused (measurement) path
+  const int64_t dh_rows = dq_fused(kp, vp) ? 0 : h.m;
+  w.Dh[0] = ws.take<__half>(dh_rows * w.ld);
+  w.Dh[1] = ws.take<__half>(dh_rows * w.ld);
   w.cs = ws.take<float2>(h.m * (h.head_dim / 2));
+  w.tail = ws.take<uint8_t>(dq_fused(kp, vp) ? dq_tail_bytes(h.m, std::max(kp->n_tail, vp->n_tail)) : 0);
   return w;
 }
 
@@ -919,7 +996,9 @@ kvtc_status decompress_enqueue(const kvtc_basis *kb, const kvtc_plan *kp, const 
   const bool ovl = !overlap_off();
   cudaStream_t aux = ovl ? ss->s : st;
   if ((s = enqueue_inflate(ib, h, w, st))) return s;
+  const bool fused = dq_fused(kp, vp);
   auto expand = [&](int sv, cudaStream_t q, int ctas) -> kvtc_status {
+    if (fused) return KVTC_OK;                    // dequantised inside the reconstruction GEMM
     kvtc_plan *pl = const_cast<kvtc_plan *>(sv ? vp : kp);
     kvtc_status r;
     ProfScope ps(sv && ovl ? "d.dequant_overlapped" : "d.dequant", q);
@@ -941,7 +1020,8 @@ kvtc_status decompress_enqueue(const kvtc_basis *kb, const kvtc_plan *kp, const 
     if (sv == 1) KVTC_CUDA_TRY(cudaStreamWaitEvent(st, ss->ev[3], 0));   // join: values expanded, checks done
     {
       ProfScope ps("d.reconstruct_gemm", st);
-      if ((s = run_reconstruct(b, pl, op, w.Dh[sv], w.ld, h.m, h.sinks, layer_begin, layer_end, vw, bs, w.cs, st)))
+      if ((s = run_reconstruct(b, pl, op, w.Dh[sv], w.ld, h.m, h.sinks, layer_begin, layer_end, vw, bs, w.cs, st,
+                               nullptr, w.payloads[sv], fused, w.tail)))
         return s;
     }
     if (sv == 0) {
@@ -979,9 +1059,11 @@ extern "C" size_t kvtc_decompress_workspace_bytes(const kvtc_basis *kb, const kv
   b.take<uint64_t>(4);
   b.take<uint8_t>(h.payload_bytes[0] + 16);
   b.take<uint8_t>(h.payload_bytes[1] + 16);
-  b.take<__half>(h.m * std::max(std::max(kp->r_nz_pad, vp->r_nz_pad), 8));
-  b.take<__half>(h.m * std::max(std::max(kp->r_nz_pad, vp->r_nz_pad), 8));
+  const int64_t dh_rows = dq_fused(kp, vp) ? 0 : h.m;
+  b.take<__half>(dh_rows * std::max(std::max(kp->r_nz_pad, vp->r_nz_pad), 8));
+  b.take<__half>(dh_rows * std::max(std::max(kp->r_nz_pad, vp->r_nz_pad), 8));
   b.take<float2>(h.m * (kb->shape.head_dim / 2));
+  b.take<uint8_t>(dq_fused(kp, vp) ? dq_tail_bytes(h.m, std::max(kp->n_tail, vp->n_tail)) : 0);
   return b.used + 256;
 }
 
@@ -1051,7 +1133,7 @@ extern "C" kvtc_status kvtc_decompress_begin(const kvtc_basis *kb, const kvtc_pl
   if (h.m) {
     if ((s = enqueue_inflate(ib, h, w, st))) return s;
     ProfScope ps("d.dequant", st);
-    for (int sv = 0; sv < 2; ++sv) {
+    for (int sv = 0; sv < 2 && !dq_fused(kp, vp); ++sv) {
       kvtc_plan *pl = const_cast<kvtc_plan *>(sv ? vp : kp);
       if ((s = launch_dequant(pl->d_pgroups, pl->d_codes_off_full, pl->G, plan_codes_off_last(pl, h.m % kTileM),
                               pl->tile_bytes, w.payloads[sv], h.m, w.Dh[sv], w.ld, st)))
@@ -1109,7 +1191,8 @@ extern "C" kvtc_status kvtc_decompress_layers(const kvtc_basis *kb, const kvtc_p
     if ((s = plan_operands(b, pl, &op))) return s;
     {
       ProfScope ps("d.reconstruct_gemm", st);
-      if ((s = run_reconstruct(b, pl, op, w.Dh[sv], w.ld, h.m, h.sinks, layer_begin, layer_end, vw, bs, w.cs, st)))
+      if ((s = run_reconstruct(b, pl, op, w.Dh[sv], w.ld, h.m, h.sinks, layer_begin, layer_end, vw, bs, w.cs, st,
+                               nullptr, w.payloads[sv], dq_fused(kp, vp), w.tail)))
         return s;
     }
     if ((s = launch_unpack_raw(raw, nraw, 0, h.sinks, *vw, bs, 0, layer_begin, layer_end, st))) return s;
@@ -1162,7 +1245,7 @@ extern "C" size_t kvtc_compress_batch_workspace_bytes(const kvtc_basis *kb, cons
   b.take<__nv_bfloat16>(rows * (kb->p + kXPad));
   b.take<__nv_bfloat16>(rows * (kb->p + kXPad));
   b.take<float2>(rows * (kb->shape.head_dim / 2));
-  b.take<float>(rows * std::max(kp->wide_cols, vp->wide_cols));
+  b.take<uint8_t>(wide_scratch_bytes(rows, std::max(kp->wide_cols, vp->wide_cols), std::max(kp->nwide, vp->nwide)));
   b.take<TileRef>(2 * (rows / kTileM));
   b.take<EncodeJob>(2 * int64_t(n));
   b.take<HashJob>(3 * int64_t(n));
@@ -1225,7 +1308,8 @@ extern "C" kvtc_status kvtc_compress_batch(const kvtc_basis *kb, const kvtc_plan
   auto *X = ws.take<__nv_bfloat16>(rows * ldx);
   auto *X2 = ws.take<__nv_bfloat16>(rows * ldx);          // the values' rows (gathered beside the keys' GEMM)
   float2 *cs = ws.take<float2>(rows * half);
-  float *wide = ws.take<float>(rows * std::max(kp->wide_cols, vp->wide_cols));
+  float *wide = reinterpret_cast<float *>(
+      ws.take<uint8_t>(wide_scratch_bytes(rows, std::max(kp->wide_cols, vp->wide_cols), std::max(kp->nwide, vp->nwide))));
   TileRef *d_tiles = ws.take<TileRef>(2 * ntiles);
   EncodeJob *d_jobs = ws.take<EncodeJob>(2 * int64_t(n));
   HashJob *d_hjobs = ws.take<HashJob>(3 * int64_t(n));            // raw sections, K payloads, V payloads
@@ -1440,10 +1524,12 @@ extern "C" size_t kvtc_decompress_batch_workspace_bytes(const kvtc_basis *kb, co
     b.take<uint8_t>(h.payload_bytes[1] + 16);
   }
   const int64_t ld = std::max(std::max(kp->r_nz_pad, vp->r_nz_pad), 8);
+  const int64_t dh_rows = dq_fused(kp, vp) ? 0 : rows;
   b.take<int32_t>(4);
-  b.take<__half>(rows * ld);
-  b.take<__half>(rows * ld);
+  b.take<__half>(dh_rows * ld);
+  b.take<__half>(dh_rows * ld);
   b.take<float2>(rows * (kb->shape.head_dim / 2));
+  b.take<uint8_t>(dq_fused(kp, vp) ? dq_tail_bytes(rows, std::max(kp->n_tail, vp->n_tail)) : 0);
   b.take<TileRef>(2 * (rows / kTileM));
   b.take<InflateJob>(2 * int64_t(n));
   b.take<int32_t>(n);
@@ -1508,10 +1594,12 @@ kvtc_status decompress_batch_core(const kvtc_basis *kb, const kvtc_plan *kp, con
     pay_k[i] = ws.take<uint8_t>(hdr[i].payload_bytes[0] + 16);
     pay_v[i] = ws.take<uint8_t>(hdr[i].payload_bytes[1] + 16);
   }
+  const bool fused = dq_fused(kp, vp);
   int32_t *err = ws.take<int32_t>(4);
-  __half *Dh = ws.take<__half>(rows * ld);
-  __half *Dh_v = ws.take<__half>(rows * ld);
+  __half *Dh = ws.take<__half>((fused ? 0 : rows) * ld);
+  __half *Dh_v = ws.take<__half>((fused ? 0 : rows) * ld);
   float2 *cs = ws.take<float2>(rows * half);
+  uint8_t *dtail = ws.take<uint8_t>(fused ? dq_tail_bytes(rows, std::max(kp->n_tail, vp->n_tail)) : 0);
   TileRef *d_tiles = ws.take<TileRef>(2 * ntiles);
   InflateJob *d_jobs = ws.take<InflateJob>(2 * int64_t(n));
   int32_t *ierr = ws.take<int32_t>(n);                             // per item: inflate error / checksum bits
@@ -1587,6 +1675,10 @@ kvtc_status decompress_batch_core(const kvtc_basis *kb, const kvtc_plan *kp, con
         r.page_tokens = vw.page_tokens;
         r.tok0 = h.sinks + j * kTileM;
         r.ntok = int(std::min<int64_t>(kTileM, h.m - j * kTileM));
+        // the fused inverse path reads this tile's payload bytes
+        kvtc_plan *pl = const_cast<kvtc_plan *>(sv ? vp : kp);
+        r.payload = (sv ? pay_v[i] : pay_k[i]) + j * pl->tile_bytes;
+        r.codes_off = r.ntok < kTileM ? plan_codes_off_last(pl, r.ntok) : pl->d_codes_off_full;
       }
   }
   if (ntiles)
@@ -1600,6 +1692,7 @@ kvtc_status decompress_batch_core(const kvtc_basis *kb, const kvtc_plan *kp, con
     return launch_hash_check_batch(hsum, hexp, 3 * n, 3, ierr, q);
   };
   auto dequant_all = [&](int sv, cudaStream_t q, int ctas) -> kvtc_status {
+    if (fused) return KVTC_OK;                    // dequantised inside the reconstruction GEMM
     kvtc_plan *pl = const_cast<kvtc_plan *>(sv ? vp : kp);
     for (int i = 0; i < n; ++i) {
       const ContainerHeader &h = hdr[i];
@@ -1631,7 +1724,7 @@ kvtc_status decompress_batch_core(const kvtc_basis *kb, const kvtc_plan *kp, con
       ProfScope ps("db.reconstruct_gemm", st);
       // the view arguments only carry the shape here: every tile's output comes from its TileRef
       if ((s = run_reconstruct(b, pl, op, sv ? Dh_v : Dh, ld, rows, 0, 0, b->shape.layers, sv ? &v_out[0] : &k_out[0],
-                               sv ? vbases[0] : kbases[0], cs, st, d_tiles + sv * ntiles)))
+                               sv ? vbases[0] : kbases[0], cs, st, d_tiles + sv * ntiles, nullptr, fused, dtail)))
         return s;
     }
     if (sv == 0) {

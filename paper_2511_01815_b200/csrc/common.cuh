@@ -130,6 +130,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   }
 }
 
+// Waits by spinning on try_wait without a suspend hint: for barriers completed
+// by arrivals from the PEER CTA of a pair (remote mbarrier.arrive, multicast
+// commits), where a suspended waiter measured to wake up microseconds late
+// (ncu: NANOSLEEP.SYNCS dominating the fused reconstruction GEMM).  Traps after
+// ~4 s like mbar_wait.
+__device__ __forceinline__ void mbar_wait_spin(uint64_t *bar, uint32_t parity) {
+  uint64_t t0 = 0;
+  for (uint32_t i = 0;; ++i) {
+    if (mbar_try_wait(bar, parity)) return;
+    if ((i & 1023) == 1023) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (!t0) t0 = t;
+      else if (t - t0 > 4000000000ull) __trap();
+    }
+  }
+}
+
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap *m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
 }

@@ -125,6 +125,56 @@ __device__ void min_redundancy_lengths(int *A, int n) {
   }
 }
 
+
+// Phase 1 of the in-place minimum-redundancy construction (Moffat-Katajainen,
+// the first loop of min_redundancy_lengths) with the two queue fronts cached in
+// registers and the next values prefetched, so each step is ALU work instead of
+// a chain of dependent shared-memory loads.  A[0..n) = weights ascending (n >= 2);
+// on return A[i] (i < n - 2) = parent of internal node i, A[n - 2] = 0 (the root).
+__device__ void mk_merge(int *A, const int n) {
+  constexpr int INF = 0x7FFFFFFF;
+  A[0] += A[1];
+  int root = 0, leaf = 2;
+  // internal-node queue [root, next): r0 = A[root], r1 = A[root + 1] (when they exist)
+  int r0 = A[0], r1 = INF;
+  // leaf queue [leaf, n): l0..l3 = A[leaf .. leaf + 3]
+  int l0 = leaf < n ? A[leaf] : INF, l1 = leaf + 1 < n ? A[leaf + 1] : INF, l2 = leaf + 2 < n ? A[leaf + 2] : INF,
+      l3 = leaf + 3 < n ? A[leaf + 3] : INF;
+  for (int next = 1; next < n - 1; ++next) {
+    int w;
+    // first child (the internal queue is never empty here)
+    if (leaf >= n || r0 < l0) {
+      w = r0;
+      A[root] = next;
+      ++root;
+      r0 = r1;
+      r1 = root + 1 < next ? A[root + 1] : INF;
+    } else {
+      w = l0;
+      ++leaf;
+      l0 = l1; l1 = l2; l2 = l3;
+      l3 = leaf + 3 < n ? A[leaf + 3] : INF;
+    }
+    // second child
+    if (leaf >= n || (root < next && r0 < l0)) {
+      w += r0;
+      A[root] = next;
+      ++root;
+      r0 = r1;
+      r1 = root + 1 < next ? A[root + 1] : INF;
+    } else {
+      w += l0;
+      ++leaf;
+      l0 = l1; l1 = l2; l2 = l3;
+      l3 = leaf + 3 < n ? A[leaf + 3] : INF;
+    }
+    A[next] = w;
+    if (root == next) r0 = w;             // the new node is the internal queue's front ...
+    else if (root + 1 == next) r1 = w;    // ... or right behind it
+  }
+  A[n - 2] = 0;
+}
+
 // Single-thread: code lengths (<= maxbits, complete prefix code) for nsym
 // symbols with frequencies freq[]; sorted[] = symbols with freq > 0 sorted by
 // (freq, symbol) ascending, count nz.  work: int[nsym].
@@ -199,18 +249,28 @@ struct BitWriter {
 
 
 constexpr int kSortItems = (kLitSyms + kEncThreads - 1) / kEncThreads;   // >= 257 sort keys
+// three 64-bit words of 12-bit counters (one per code length 1..15), block-scanned
+struct U3 {
+  uint64_t a, b, c;
+};
+struct U3Sum {
+  __device__ U3 operator()(const U3 &x, const U3 &y) const { return U3{x.a + y.a, x.b + y.b, x.c + y.c}; }
+};
+__device__ __forceinline__ uint64_t &u3_word(U3 &u, int i) { return i == 0 ? u.a : (i == 1 ? u.b : u.c); }
 using EncSort = cub::BlockRadixSort<uint32_t, kEncThreads, kSortItems>;
 
 struct EncShared {
   union {
     uint32_t whist[kEncThreads / 32][kLitSyms + 3];   // warp-private histograms
     typename EncSort::TempStorage sort;               // (freq, symbol) radix sort, after the merge
+    uint32_t skeys[kEncThreads * kSortItems];       // sorted (freq << 9 | symbol) keys, after the sort
+    struct {                                          // code construction, after nz / sorted are read
+      int work[kLitSyms + 3], dep[kLitSyms + 3], par[kLitSyms + 3], ndep[kLitSyms + 3];
+    } mk;
   } u;
-  uint32_t skeys[kEncThreads * kSortItems];         // sorted (freq << 9 | symbol) keys
   uint32_t hist[kLitSyms + 3];
   uint32_t clhist[19];
   int sorted[kLitSyms + 3];
-  int work[kLitSyms + 3];
   int num[33];
   int nz;
   uint8_t len[kLitSyms + 3];
@@ -222,6 +282,10 @@ struct EncShared {
   uint8_t rle_extra[kLitSyms + 8];
   uint32_t hdr[160];   // header bits (<= 5120)
   uint32_t hdr_bits;
+  int next_code[16];
+  uint32_t startmask[9];                             // run starts of the 258 code lengths
+  int nrle;
+  typename cub::BlockScan<U3, kEncThreads>::TempStorage scan3;
   uint32_t total_bits;
   uint32_t segst[kNSeg];
   int use_stored;
@@ -282,6 +346,273 @@ struct WordWriter {
   }
 };
 
+
+// Number of code-length-code symbols the RLE (RFC 1951 §3.2.7) emits for a run of
+// L equal lengths v (the rule of the former serial loop: zeros -> 18 (11..138)
+// while >= 11, then one 17 (3..10), then single zeros; v != 0 -> v, then 16
+// (3..6 repeats) while >= 3, then single v's).
+__device__ __forceinline__ int rle_count(int v, int L) {
+  if (v == 0) {
+    const int n18 = L / 138 + ((L % 138) >= 11 ? 1 : 0);
+    const int left = (L % 138) >= 11 ? 0 : L % 138;
+    return n18 + (left >= 3 ? 1 : left);
+  }
+  const int rep = L - 1;
+  const int n16 = rep / 6 + ((rep % 6) >= 3 ? 1 : 0);
+  const int left = (rep % 6) >= 3 ? 0 : rep % 6;
+  return 1 + n16 + left;
+}
+__device__ __forceinline__ int rle_emit(int v, int L, uint16_t *sym, uint8_t *extra) {
+  int n = 0;
+  if (v == 0) {
+    int left = L;
+    while (left >= 11) {
+      const int r = min(left, 138);
+      sym[n] = 18; extra[n++] = uint8_t(r - 11); left -= r;
+    }
+    if (left >= 3) {
+      sym[n] = 17; extra[n++] = uint8_t(left - 3); left = 0;
+    }
+    while (left-- > 0) { sym[n] = 0; extra[n++] = 0; }
+  } else {
+    sym[n] = uint16_t(v); extra[n++] = 0;
+    int left = L - 1;
+    while (left >= 3) {
+      const int r = min(left, 6);
+      sym[n] = 16; extra[n++] = uint8_t(r - 3); left -= r;
+    }
+    while (left-- > 0) { sym[n] = uint16_t(v); extra[n++] = 0; }
+  }
+  return n;
+}
+__device__ __forceinline__ void hdr_put(uint32_t *hdr, uint32_t pos, uint32_t v, int n) {
+  const uint64_t x = uint64_t(v & ((1u << n) - 1)) << (pos & 31);
+  atomicOr(&hdr[pos >> 5], uint32_t(x));
+  if ((pos & 31) + n > 32) atomicOr(&hdr[(pos >> 5) + 1], uint32_t(x >> 32));
+}
+
+// The chunk's Huffman code and dynamic block header, all 128 threads.  Only the
+// minimum-redundancy length computation (O(nz), in-place two-queue merge) and the
+// 19-symbol code-length code run on one thread; lengths -> symbols, canonical
+// codes (ranks by block scan), the run-length coding of the code lengths and the
+// header bits (scanned offsets, atomicOr) are parallel.  Bit-identical to the
+// former single-thread construction.
+__device__ __forceinline__ void build_header(EncShared &S, const int t) {
+  const int nz = S.nz;
+  for (int s = t; s < kLitSyms + 3; s += kEncThreads) S.len[s] = 0;
+  for (int j = t; j < nz; j += kEncThreads) S.u.mk.work[j] = int(S.hist[S.sorted[j]]);
+  if (t < 33) S.num[t] = 0;
+  if (t < 9) S.startmask[t] = 0;
+  for (int d = t; d < kLitSyms + 3; d += kEncThreads) S.u.mk.ndep[d] = 0;
+  __syncthreads();
+  // minimum-redundancy code lengths (Moffat-Katajainen): the merge on one thread
+  // (register-cached queue fronts), internal-node depths by pointer jumping, the
+  // leaf-length counts from the per-depth internal-node counts -- the same
+  // lengths as min_redundancy_lengths, of which only num[] is needed
+  if (t == 0 && nz > 1) mk_merge(S.u.mk.work, nz);
+  __syncthreads();
+  const int n_int = nz - 1;                       // internal nodes 0 .. nz - 2, root nz - 2
+  for (int i = t; i < n_int; i += kEncThreads) {
+    S.u.mk.dep[i] = i == n_int - 1 ? 0 : 1;
+    S.u.mk.par[i] = i == n_int - 1 ? i : S.u.mk.work[i];
+  }
+  __syncthreads();
+  for (int round = 0; round < 9; ++round) {       // depth <= 256 < 2^9
+    int nd[2], np[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int i = t + k * kEncThreads;
+      if (i < n_int) {
+        nd[k] = S.u.mk.dep[i] + S.u.mk.dep[S.u.mk.par[i]];
+        np[k] = S.u.mk.par[S.u.mk.par[i]];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int i = t + k * kEncThreads;
+      if (i < n_int) {
+        S.u.mk.dep[i] = nd[k];
+        S.u.mk.par[i] = np[k];
+      }
+    }
+    __syncthreads();
+  }
+  for (int i = t; i < n_int; i += kEncThreads) atomicAdd(&S.u.mk.ndep[S.u.mk.dep[i]], 1);
+  __syncthreads();
+  if (t == 0) {
+    int *num = S.num;
+    if (nz == 1) num[1] = 1;
+    else {
+      // depth d holds avbl(d) nodes, ndep[d] of them internal: the rest are leaves
+      int avbl = 1;
+      for (int d = 0; avbl > 0; ++d) {
+        const int used = d < kLitSyms + 3 ? S.u.mk.ndep[d] : 0;
+        num[d > 32 ? 32 : d] += avbl - used;
+        avbl = 2 * used;
+      }
+    }
+    // enforce the maximum length while keeping the Kraft sum exactly 1
+    for (int i = kMaxBits + 1; i <= 32; i++) {
+      num[kMaxBits] += num[i];
+      num[i] = 0;
+    }
+    if (nz > 1) {
+      uint32_t total = 0;
+      for (int i = kMaxBits; i > 0; i--) total += uint32_t(num[i]) << (kMaxBits - i);
+      while (total != (1u << kMaxBits)) {
+        num[kMaxBits]--;
+        for (int i = kMaxBits - 1; i > 0; i--)
+          if (num[i]) {
+            num[i]--;
+            num[i + 1] += 2;
+            break;
+          }
+        total--;
+      }
+    }
+    int code = 0;
+    S.next_code[0] = 0;
+    for (int b = 1; b <= kMaxBits; ++b) {
+      code = (code + (b > 1 ? num[b - 1] : 0)) << 1;
+      S.next_code[b] = code;
+    }
+  }
+  __syncthreads();
+  // most frequent symbols get the shortest codes: sorted position j (ascending
+  // frequency) has rank nz-1-j from the top
+  for (int j = t; j < nz; j += kEncThreads) {
+    const int r = nz - 1 - j;
+    int l = 1, c = S.num[1];
+    while (r >= c && l < kMaxBits) c += S.num[++l];
+    S.len[S.sorted[j]] = uint8_t(l);
+  }
+  __syncthreads();
+  // canonical codes: code(s) = next_code[l] + #{s' < s : len[s'] = l}; thread t owns
+  // symbols 3t .. 3t+2, cross-thread ranks from one block scan of packed counters
+  {
+    U3 mine{0, 0, 0};
+    uint8_t l3[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int s = 3 * t + k;
+      l3[k] = s < kLitSyms ? S.len[s] : 0;
+      if (l3[k]) u3_word(mine, (l3[k] - 1) / 5) += 1ull << (12 * ((l3[k] - 1) % 5));
+    }
+    U3 before;
+    cub::BlockScan<U3, kEncThreads>(S.scan3).ExclusiveScan(mine, before, U3{0, 0, 0}, U3Sum());
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int s = 3 * t + k;
+      if (s >= kLitSyms) continue;
+      const int l = l3[k];
+      if (!l) {
+        S.rev[s] = 0;
+        continue;
+      }
+      int r = int((u3_word(before, (l - 1) / 5) >> (12 * ((l - 1) % 5))) & 0xFFF);
+      for (int q = 0; q < k; ++q) r += l3[q] == l;
+      const uint32_t c = uint32_t(S.next_code[l] + r);
+      S.rev[s] = uint16_t(__brev(c) >> (32 - l));
+    }
+  }
+  // run-length coding of the 257 literal/length code lengths + 1 distance length (0)
+  constexpr int nseq = kLitSyms + 1;
+  auto val = [&](int i) -> int { return i < kLitSyms ? S.len[i] : 0; };
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int i = 3 * t + k;
+    if (i < nseq && (i == 0 || val(i) != val(i - 1))) atomicOr(&S.startmask[i >> 5], 1u << (i & 31));
+  }
+  if (t < 19) S.clhist[t] = 0;
+  __syncthreads();
+  int run_v[3], run_l[3], nrun = 0, my_syms = 0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int i = 3 * t + k;
+    if (i >= nseq || !((S.startmask[i >> 5] >> (i & 31)) & 1u)) continue;
+    // next run start after i (or the end)
+    int q = nseq;
+    int w = (i + 1) >> 5;
+    uint32_t mbits = (i + 1) < 32 * 9 ? (S.startmask[w] & (~0u << ((i + 1) & 31))) : 0u;
+    while (true) {
+      if (mbits) {
+        q = min(nseq, 32 * w + __ffs(mbits) - 1);
+        break;
+      }
+      if (++w >= 9) break;
+      mbits = S.startmask[w];
+    }
+    run_v[nrun] = val(i);
+    run_l[nrun] = q - i;
+    my_syms += rle_count(run_v[nrun], run_l[nrun]);
+    ++nrun;
+  }
+  uint32_t sym_off_u, nr;
+  cub::BlockScan<uint32_t, kEncThreads>(S.scan).ExclusiveSum(uint32_t(my_syms), sym_off_u, nr);
+  const int sym_off = int(sym_off_u);
+  {
+    int o = sym_off;
+    for (int r = 0; r < nrun; ++r) o += rle_emit(run_v[r], run_l[r], S.rle_sym + o, S.rle_extra + o);
+    for (int q = sym_off; q < o; ++q) atomicAdd(&S.clhist[S.rle_sym[q]], 1u);
+  }
+  __syncthreads();
+  if (t == 0) {
+    // code-length code (19 symbols, <= 7 bits); a complete code needs >= 2 used symbols
+    int used = 0;
+    for (int i = 0; i < 19; ++i) used += S.clhist[i] != 0;
+    for (int i = 0; i < 19 && used < 2; ++i)
+      if (!S.clhist[i]) { S.clhist[i] = 1; used++; }
+    int csorted[19];
+    int cnz = 0;
+    for (int s = 0; s < 19; ++s)
+      if (S.clhist[s]) {
+        int k = cnz++;
+        while (k > 0 && (S.clhist[csorted[k - 1]] > S.clhist[s])) { csorted[k] = csorted[k - 1]; --k; }
+        csorted[k] = s;
+      }
+    build_lengths_s(S.clhist, csorted, cnz, 7, S.cllen, 19, S.u.mk.work, S.num);
+    canonical_codes(S.cllen, 19, S.clrev);
+    const int order[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
+    int hclen = 19;
+    while (hclen > 4 && S.cllen[order[hclen - 1]] == 0) hclen--;
+    WordWriter bw{S.hdr, 0, 0, 0};
+    bw.put(1, 1);            // BFINAL
+    bw.put(2, 2);            // BTYPE = 10 (dynamic Huffman)
+    bw.put(0, 5);            // HLIT  = 257 - 257
+    bw.put(0, 5);            // HDIST = 1 - 1
+    bw.put(hclen - 4, 4);    // HCLEN
+    for (int i = 0; i < hclen; ++i) bw.put(S.cllen[order[i]], 3);
+    S.hdr_bits = bw.finish();   // prefix; the code-length symbols follow
+  }
+  __syncthreads();
+  // code-length symbols at scanned bit offsets
+  {
+    uint32_t my_bits = 0;
+    for (int q = sym_off; q < sym_off + my_syms; ++q) {
+      const int sm = S.rle_sym[q];
+      my_bits += S.cllen[sm] + (sm == 16 ? 2 : sm == 17 ? 3 : sm == 18 ? 7 : 0);
+    }
+    uint32_t boff, btot;
+    cub::BlockScan<uint32_t, kEncThreads>(S.scan).ExclusiveSum(my_bits, boff, btot);
+    uint32_t pos = S.hdr_bits + boff;
+    for (int q = sym_off; q < sym_off + my_syms; ++q) {
+      const int sm = S.rle_sym[q];
+      hdr_put(S.hdr, pos, S.clrev[sm], S.cllen[sm]);
+      pos += S.cllen[sm];
+      const int ne = sm == 16 ? 2 : sm == 17 ? 3 : sm == 18 ? 7 : 0;
+      if (ne) {
+        hdr_put(S.hdr, pos, S.rle_extra[q], ne);
+        pos += ne;
+      }
+    }
+    __syncthreads();
+    if (t == 0) S.hdr_bits += btot;
+  }
+  (void)nr;
+  __syncthreads();
+}
+
 __device__ __forceinline__ void encode_chunk(EncShared &S, const int c, const uint8_t *in, uint64_t n, int32_t chunk,
                                              uint8_t *slots, uint64_t stride, uint32_t *chunk_bytes,
                                              uint32_t *chunk_kind, uint16_t *index) {
@@ -331,82 +662,17 @@ __device__ __forceinline__ void encode_chunk(EncShared &S, const int c, const ui
       keys[i] = sym < kLitSyms ? (S.hist[sym] << 9) | uint32_t(sym) : 0x3FFFFFFu;
     }
     EncSort(S.u.sort).Sort(keys, 0, 26);
+    __syncthreads();                               // the sort's storage is reused for the keys
 #pragma unroll
-    for (int i = 0; i < kSortItems; ++i) S.skeys[t * kSortItems + i] = keys[i];
+    for (int i = 0; i < kSortItems; ++i) S.u.skeys[t * kSortItems + i] = keys[i];
   }
   __syncthreads();
   for (int i = t; i < kLitSyms; i += kEncThreads)
-    if ((S.skeys[i] >> 9) != 0 && (i == 0 || (S.skeys[i - 1] >> 9) == 0)) S.nz = kLitSyms - i;
+    if ((S.u.skeys[i] >> 9) != 0 && (i == 0 || (S.u.skeys[i - 1] >> 9) == 0)) S.nz = kLitSyms - i;
   __syncthreads();
-  for (int j = t; j < S.nz; j += kEncThreads) S.sorted[j] = int(S.skeys[kLitSyms - S.nz + j] & 511u);
+  for (int j = t; j < S.nz; j += kEncThreads) S.sorted[j] = int(S.u.skeys[kLitSyms - S.nz + j] & 511u);
   __syncthreads();
-  if (t == 0) {
-    build_lengths_s(S.hist, S.sorted, S.nz, kMaxBits, S.len, kLitSyms, S.work, S.num);
-    canonical_codes(S.len, kLitSyms, S.rev);
-    // code-length sequence: 257 literal/length lengths + 1 distance length (0)
-    const int nseq = kLitSyms + 1;
-    int nr = 0;
-    for (int i = 0; i < nseq;) {
-      const uint8_t v = i < kLitSyms ? S.len[i] : 0;
-      int run = 1;
-      while (i + run < nseq && (i + run < kLitSyms ? S.len[i + run] : 0) == v) run++;
-      if (v == 0) {
-        int left = run;
-        while (left >= 11) {
-          const int r = min(left, 138);
-          S.rle_sym[nr] = 18; S.rle_extra[nr++] = uint8_t(r - 11); left -= r;
-        }
-        if (left >= 3) {
-          S.rle_sym[nr] = 17; S.rle_extra[nr++] = uint8_t(left - 3); left = 0;
-        }
-        while (left-- > 0) { S.rle_sym[nr] = 0; S.rle_extra[nr++] = 0; }
-      } else {
-        S.rle_sym[nr] = v; S.rle_extra[nr++] = 0;
-        int left = run - 1;
-        while (left >= 3) {
-          const int r = min(left, 6);
-          S.rle_sym[nr] = 16; S.rle_extra[nr++] = uint8_t(r - 3); left -= r;
-        }
-        while (left-- > 0) { S.rle_sym[nr] = v; S.rle_extra[nr++] = 0; }
-      }
-      i += run;
-    }
-    for (int i = 0; i < nr; ++i) S.clhist[S.rle_sym[i]]++;
-    // a complete code-length code needs >= 2 used symbols
-    int used = 0;
-    for (int i = 0; i < 19; ++i) used += S.clhist[i] != 0;
-    for (int i = 0; i < 19 && used < 2; ++i)
-      if (!S.clhist[i]) { S.clhist[i] = 1; used++; }
-    int csorted[19];
-    int cnz = 0;
-    for (int s = 0; s < 19; ++s)
-      if (S.clhist[s]) {
-        int k = cnz++;
-        while (k > 0 && (S.clhist[csorted[k - 1]] > S.clhist[s])) { csorted[k] = csorted[k - 1]; --k; }
-        csorted[k] = s;
-      }
-    build_lengths_s(S.clhist, csorted, cnz, 7, S.cllen, 19, S.work, S.num);
-    canonical_codes(S.cllen, 19, S.clrev);
-    const int order[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
-    int hclen = 19;
-    while (hclen > 4 && S.cllen[order[hclen - 1]] == 0) hclen--;
-    WordWriter bw{S.hdr, 0, 0, 0};
-    bw.put(1, 1);            // BFINAL
-    bw.put(2, 2);            // BTYPE = 10 (dynamic Huffman)
-    bw.put(0, 5);            // HLIT  = 257 - 257
-    bw.put(0, 5);            // HDIST = 1 - 1
-    bw.put(hclen - 4, 4);    // HCLEN
-    for (int i = 0; i < hclen; ++i) bw.put(S.cllen[order[i]], 3);
-    for (int i = 0; i < nr; ++i) {
-      const int s = S.rle_sym[i];
-      bw.put(S.clrev[s], S.cllen[s]);
-      if (s == 16) bw.put(S.rle_extra[i], 2);
-      else if (s == 17) bw.put(S.rle_extra[i], 3);
-      else if (s == 18) bw.put(S.rle_extra[i], 7);
-    }
-    S.hdr_bits = bw.finish();
-  }
-  __syncthreads();
+  build_header(S, t);
   for (int i = t; i < 256; i += kEncThreads) S.sym[i] = uint32_t(S.rev[i]) | (uint32_t(S.len[i]) << 16);
   __syncthreads();
   // ---- bit counts per piece, exclusive scan
@@ -844,6 +1110,9 @@ struct FastShared {
   uint16_t table[1 << kTabBits];   // (sym << 4) | len; 0x8000 | k: longer code, subtable k
   uint16_t sub[kSubTabs << kSubBits];  // second level: the next kSubBits bits
   uint16_t code[260];
+  int cnt[16], next[16];
+  uint32_t wsum[2][4];
+  uint32_t premask[(1 << kTabBits) / 32], prebase[(1 << kTabBits) / 32];
   Huff h;
   uint8_t lens[320];
   uint8_t cltab[128];              // code-length code: (sym << 3) | len, 7-bit lookup
@@ -927,10 +1196,8 @@ __device__ int parse_header_fast(FastShared &S) {
   }
   if (br.pos > 32u * kHdrWords) return -7;
   if (S.lens[256] == 0) return -9;
-  if (huff_build(S.h, S.lens, 257) < 0) return -4;
-  reversed_codes(S.lens, 257, S.code);
   S.hdr_bits = br.pos;
-  return 0;
+  return 0;   // the literal/length code itself is checked and built in parallel (inflate_chunk)
 }
 
 // Chunk c of the section at `section` (raw size n_out, nch chunks) into out_base.
@@ -983,27 +1250,110 @@ __device__ __forceinline__ void inflate_chunk(FastShared &S, const uint8_t *sect
   }
   __syncthreads();
   if (S.status) return;
+  // ---- the literal/length code, all 64 threads (thread t owns symbols 5t .. 5t+4):
+  // length counts, Kraft check (over-subscribed = corrupt), canonical codes by
+  // rank within each length, first-level table, subtables for codes > 11 bits
+  // indexed by the rank of their first-level prefix
+  if (tid < 16) S.cnt[tid] = 0;
+  if (tid < (1 << kTabBits) / 32) S.premask[tid] = 0;
+  __syncthreads();
+  uint8_t l5[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const int sym = 5 * tid + k;
+    l5[k] = sym < 257 ? S.lens[sym] : 0;
+    if (l5[k]) atomicAdd(&S.cnt[l5[k]], 1);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int left = 1;                             // RFC 1951 §3.2.2 / zlib: over-subscribed codes are invalid
+    int code = 0;
+    for (int b = 1; b < 16; ++b) {
+      left = (left << 1) - S.cnt[b];
+      if (left < 0) {
+        S.status = -4;
+        atomicExch(err, -4);
+        break;
+      }
+      code = (code + (b > 1 ? S.cnt[b - 1] : 0)) << 1;
+      S.next[b] = code;
+    }
+  }
+  // ranks: per-thread length counts, exclusive prefix over the 64 threads (two
+  // warps) with 16 x 9-bit... counters packed as 4 lengths per 32-bit word x 4 words
+  {
+    uint32_t pk[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < 5; ++k)
+      if (l5[k]) pk[l5[k] >> 2] += 1u << (8 * (l5[k] & 3));
+    uint32_t ex[4];
+    const int lane = tid & 31, w = tid >> 5;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t v = pk[q];
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, v, d);
+        if (lane >= d) v += y;
+      }
+      ex[q] = v - pk[q];
+      if (lane == 31) S.wsum[w][q] = v;
+    }
+    __syncthreads();
+    if (S.status) return;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const int sym = 5 * tid + k;
+      const int l = l5[k];
+      if (sym >= 257) break;
+      if (!l) {
+        S.code[sym] = 0;
+        continue;
+      }
+      int r = int((ex[l >> 2] >> (8 * (l & 3))) & 0xFF);
+      if (w) r += int((S.wsum[0][l >> 2] >> (8 * (l & 3))) & 0xFF);
+      for (int q = 0; q < k; ++q) r += l5[q] == l;
+      S.code[sym] = uint16_t(__brev(uint32_t(S.next[l] + r)) >> (32 - l));
+    }
+  }
+  __syncthreads();
   for (int sym = tid; sym < 257; sym += kInfThreads) {
     const int l = S.lens[sym];
-    if (l == 0 || l > kTabBits) continue;
-    for (uint32_t f = S.code[sym]; f < (1u << kTabBits); f += (1u << l)) S.table[f] = uint16_t((sym << 4) | l);
+    if (l == 0) continue;
+    if (l <= kTabBits) {
+      for (uint32_t f = S.code[sym]; f < (1u << kTabBits); f += (1u << l)) S.table[f] = uint16_t((sym << 4) | l);
+    } else {
+      const uint32_t pre = S.code[sym] & ((1u << kTabBits) - 1);
+      atomicOr(&S.premask[pre >> 5], 1u << (pre & 31));
+    }
   }
-  if (tid == 0) {
-    // long codes: one subtable per distinct first-level prefix
-    int nsub = 0;
-    for (int sym = 0; sym < 257 && !S.status; ++sym) {
+  __syncthreads();
+  {
+    // subtable index of a prefix = its rank among the marked prefixes
+    if (tid < 32) {
+      const uint32_t a = __popc(S.premask[2 * tid]), b = __popc(S.premask[2 * tid + 1]);
+      uint32_t v = a + b;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, v, d);
+        if (tid >= d) v += y;
+      }
+      S.prebase[2 * tid] = v - a - b;
+      S.prebase[2 * tid + 1] = v - b;
+    }
+    __syncthreads();
+    for (int sym = tid; sym < 257; sym += kInfThreads) {
       const int l = S.lens[sym];
       if (l <= kTabBits) continue;
       const uint32_t pre = S.code[sym] & ((1u << kTabBits) - 1);
-      if (!(S.table[pre] & 0x8000)) {
-        if (nsub == kSubTabs) {
-          S.status = -8;
-          atomicExch(err, -8);
-          break;
-        }
-        S.table[pre] = uint16_t(0x8000 | nsub++);
+      const uint32_t k = S.prebase[pre >> 5] + __popc(S.premask[pre >> 5] & ((1u << (pre & 31)) - 1));
+      if (k >= uint32_t(kSubTabs)) {
+        S.status = -8;
+        atomicExch(err, -8);
+        continue;
       }
-      uint16_t *st = S.sub + ((S.table[pre] & 0x7FFF) << kSubBits);
+      S.table[pre] = uint16_t(0x8000 | k);
+      uint16_t *st = S.sub + (k << kSubBits);
       for (uint32_t f = S.code[sym] >> kTabBits; f < (1u << kSubBits); f += (1u << (l - kTabBits)))
         st[f] = uint16_t((sym << 4) | l);
     }

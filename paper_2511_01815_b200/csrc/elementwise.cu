@@ -371,6 +371,14 @@ __device__ __forceinline__ uint64_t load_le(const uint8_t *p, int n) {
   return v;
 }
 
+// R5: D^ = fp16(x^), x^ = v * scale + shift.  v (integer level or E4M3 value),
+// scale and shift are exact in fp16, so one fp16 fma rounds the exact x^ once,
+// which is the oracle's fp16(fp64 x^).
+__device__ __forceinline__ __half dq_value(bool fp8, uint32_t code, __half scale, __half shift) {
+  const __half v = fp8 ? __float2half_rn(e4m3_to_f32(uint8_t(code))) : __uint2half_rn(code);
+  return __hfma(v, scale, shift);
+}
+
 __global__ void __launch_bounds__(kDqThreads) dequant_kernel(const PlanGroup *groups, const int64_t *codes_off_full,
                                                              int32_t G, const int64_t *codes_off_last,
                                                              int64_t tile_bytes, const uint8_t *payload, int64_t m,
@@ -400,14 +408,13 @@ __global__ void __launch_bounds__(kDqThreads) dequant_kernel(const PlanGroup *gr
         const int tau = j / per_tok;
         const int c0 = (j - tau * per_tok) * 8;
         const uint32_t pr = uint32_t(load_le(params + 4 * tau, 4));
-        const float shift = f16_val(uint16_t(pr & 0xFFFF)), scale = f16_val(uint16_t(pr >> 16));
+        const __half shift = __ushort_as_half(uint16_t(pr & 0xFFFF)), scale = __ushort_as_half(uint16_t(pr >> 16));
         const uint64_t codes = load_le(cb + (int64_t(j) * 8 * b) / 8, b);     // 8 codes = b bytes
         __align__(16) __half out[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const uint32_t code = uint32_t(codes >> (k * b)) & mask;
-          const float v = fp8 ? e4m3_to_f32(uint8_t(code)) : float(code);
-          out[k] = __float2half_rn(__fadd_rn(__fmul_rn(v, scale), shift));
+          out[k] = dq_value(fp8, code, scale, shift);
         }
         __half *dst = Dh + (m0 + tau) * ld + pg.col + c0;
         if (vec) {
@@ -423,11 +430,10 @@ __global__ void __launch_bounds__(kDqThreads) dequant_kernel(const PlanGroup *gr
         const int tau = e / size;
         const int c = e - tau * size;
         const uint32_t pr = uint32_t(load_le(params + 4 * tau, 4));
-        const float shift = f16_val(uint16_t(pr & 0xFFFF)), scale = f16_val(uint16_t(pr >> 16));
+        const __half shift = __ushort_as_half(uint16_t(pr & 0xFFFF)), scale = __ushort_as_half(uint16_t(pr >> 16));
         const int64_t bit = int64_t(e) * b;
         const uint32_t code = (cb[bit >> 3] >> (bit & 7)) & mask;
-        const float v = fp8 ? e4m3_to_f32(uint8_t(code)) : float(code);
-        Dh[(m0 + tau) * ld + pg.col + c] = __float2half_rn(__fadd_rn(__fmul_rn(v, scale), shift));
+        Dh[(m0 + tau) * ld + pg.col + c] = dq_value(fp8, code, scale, shift);
       }
     }
   }

@@ -9,7 +9,12 @@
 //   EPI_F32        the same GEMM with an fp32 D output (DP coefficients, tests).
 //   EPI_RECON  K5  decompress: X^ = D^ V_d^T + mu, keys
 //                  re-rotated (RoPE, R7), bf16 RNE, scattered into a contiguous
-//                  or paged cache.
+//                  or paged cache.  With ASRC = 1 (the product path) the A operand
+//                  D^ never exists in HBM: four dequantising producer warps read
+//                  the inflated payload (codes + fp16 shift/scale) and write the
+//                  fp16 A k-blocks straight into the swizzled shared-memory stages
+//                  (unpack + dequantise fused into the GEMM, D2 of SURVEY
+//                  §8(a)); only V_d comes through TMA.
 //   EPI_XTX    K6  calibration: S += C^T C over a chunk of rows.
 //
 // Persistent kernel, one CTA pair (cta_group::2, M = 256) per 2 SMs: tiles are
@@ -56,6 +61,12 @@ struct Cfg {
 };
 constexpr int kBBoxRows = 128;                     // B tensor maps load 128 rows per box
 constexpr int kThreads = 256;
+#ifndef KVTC_DQ_GROUPS
+#define KVTC_DQ_GROUPS 2
+#endif
+constexpr int kDqGroups = KVTC_DQ_GROUPS;          // groups of 4 dequantising producer warps (ASRC = 1),
+constexpr int kDqWarps = 4 * kDqGroups;            // warps 8 .., taking the pipeline stages round robin
+__host__ __device__ constexpr int threads_for(int asrc) { return asrc ? kThreads + 32 * kDqWarps : kThreads; }
 constexpr int kTmemCols = 512;                     // two 256-column accumulators
 constexpr int kGroupM = 8;                         // raster group (M-blocks)
 
@@ -98,6 +109,22 @@ struct Params {
   int32_t epi_skip;                // measurement only (KVTC_EPI_SKIP=1): release TMEM without an epilogue
   const TileRef *tiles;            // batched rows (QUANT / RECON), else null
   int32_t *status;                 // QUANT: bit 0 set when an fp16 shift / scale overflowed (Q4)
+  // QUANT wide groups: fp32 pieces in D, per-piece row min/max, arrival counters
+  const WideDesc *wide;
+  int32_t nwide, wpieces;
+  float2 *wmm;
+  int32_t *wcnt;
+  // RECON with ASRC = 1: A = D^ dequantised from the payload
+  const uint8_t *dq_payload;
+  const int64_t *dq_off_full, *dq_off_last;
+  const DqCol *dq_cols;
+  const DqChunk *dq_chunks;        // [num_st * 16]
+  int32_t dq_debug;                // KVTC_DQ_DEBUG (measurement only): 1 no payload loads, 2 no A stores,
+                                   // 4 no proxy fence
+  int32_t spin;                    // KVTC_SPIN_WAITS bit mask: spin (no suspend) on 1 producer empty,
+                                   // 2 MMA tmem_empty, 4 epilogue tmem_full, 8 MMA full barrier
+  const uint8_t *dq_tail;          // [rows][dq_tail_ld] fp16 columns of the ok = 3 chunks (pre-pass)
+  int64_t dq_tail_ld;
 };
 
 __device__ __forceinline__ void cluster_sync_all() {
@@ -251,10 +278,274 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t *bar) {
       "h"(uint16_t(3))
       : "memory");
 }
+// Arrive on the same barrier offset in CTA `cta` of the cluster.  Default (.cta
+// scope) release semantics, as CUTLASS's ClusterBarrier::arrive(cta_id): with
+// .release.cluster ptxas emits MEMBAR.ALL.GPU + ERRBAR before every arrive (ncu:
+// the fused reconstruction's per-stage remote arrivals), and the consumers here
+// are the pair leader's tensor core / MMA thread, ordered by the tcgen05 and
+// proxy fences around the barrier.
 __device__ __forceinline__ void mbar_arrive_remote(uint64_t *local_bar, uint32_t cta) {
   uint32_t ra;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(local_bar)), "r"(cta));
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+}
+
+
+// ---------------------------------------------- fused dequantisation (ASRC = 1)
+// R5: D^ = fp16(x^) with x^ = v * scale + shift, v the integer level (int2 /
+// int4) or the E4M3 value (fp8).  v, scale and shift are exact in fp16, so
+// fma.rn.f16x2 rounds the exact x^ once: the oracle's fp16(fp64 x^).
+__device__ __forceinline__ uint32_t hfma2_u(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t hsub2_u(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t prmt_u(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+__device__ __forceinline__ uint32_t and_or(uint32_t a, uint32_t mask, uint32_t bits) {   // (a & mask) | bits
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "r"(mask), "r"(bits));
+  return d;
+}
+__device__ __forceinline__ uint32_t e4m3x2_to_f16x2(uint32_t two_bytes) {
+  uint32_t d;
+  const unsigned short in = static_cast<unsigned short>(two_bytes & 0xFFFF);
+  asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(d) : "h"(in));
+  return d;
+}
+__device__ __forceinline__ uint32_t ld_u32_any(const uint8_t *p) {
+  if ((reinterpret_cast<uintptr_t>(p) & 3) == 0) return *reinterpret_cast<const uint32_t *>(p);
+  return uint32_t(p[0]) | (uint32_t(p[1]) << 8) | (uint32_t(p[2]) << 16) | (uint32_t(p[3]) << 24);
+}
+// The codes of 8 consecutive elements of one token (8 * b bits, byte aligned).
+__device__ __forceinline__ void load_codes8(const uint8_t *p, int b, uint32_t &lo, uint32_t &hi) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  hi = 0;
+  if (b == 2) {
+    lo = (a & 1) == 0 ? uint32_t(*reinterpret_cast<const uint16_t *>(p)) : uint32_t(p[0]) | (uint32_t(p[1]) << 8);
+  } else if (b == 4) {
+    lo = ld_u32_any(p);
+  } else if ((a & 7) == 0) {
+    const uint2 v = *reinterpret_cast<const uint2 *>(p);
+    lo = v.x;
+    hi = v.y;
+  } else {
+    lo = ld_u32_any(p);
+    hi = ld_u32_any(p + 4);
+  }
+}
+// 8 elements -> 8 fp16 (one 16-byte chunk of an A row).  Integer levels become
+// fp16 through the 1024 + c bit trick (exact), pairs (c_k, c_k+4) per word,
+// reordered with prmt after the fma.
+__device__ __forceinline__ uint4 dq8(int type, uint32_t lo, uint32_t hi, uint32_t params) {
+  const uint32_t sh = params & 0xFFFFu, sc = params >> 16;
+  const uint32_t sh2 = sh | (sh << 16), sc2 = sc | (sc << 16);
+  uint4 o;
+  if (type == KVTC_T_FP8) {
+    o.x = hfma2_u(e4m3x2_to_f16x2(lo), sc2, sh2);
+    o.y = hfma2_u(e4m3x2_to_f16x2(lo >> 16), sc2, sh2);
+    o.z = hfma2_u(e4m3x2_to_f16x2(hi), sc2, sh2);
+    o.w = hfma2_u(e4m3x2_to_f16x2(hi >> 16), sc2, sh2);
+    return o;
+  }
+  // int4: nibble k at bits 4k; int2: spread the two code bytes to bytes 0 and 2
+  const bool i4 = type == KVTC_T_INT4;
+  const uint32_t x = i4 ? lo : prmt_u(lo, 0u, 0x4140u);
+  const uint32_t mask = i4 ? 0x000F000Fu : 0x00030003u;
+  const int step = i4 ? 4 : 2;
+  uint32_t y[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    y[k] = hfma2_u(hsub2_u(and_or(x >> (k * step), mask, 0x64006400u), 0x64006400u), sc2, sh2);   // (c_k, c_k+4)
+  o.x = prmt_u(y[0], y[1], 0x5410u);
+  o.y = prmt_u(y[2], y[3], 0x5410u);
+  o.z = prmt_u(y[0], y[1], 0x7632u);
+  o.w = prmt_u(y[2], y[3], 0x7632u);
+  return o;
+}
+// One element of any group (columns that are not whole aligned 8-chunks of one
+// group: size-1 groups, misaligned starts).
+__device__ __forceinline__ uint16_t dq1(const uint8_t *tile, const int64_t *coff, int ntok, int row, const DqCol &d) {
+  if (!d.type) return 0;
+  const uint32_t pr = ld_u32_any(tile + 4 * (int64_t(d.gidx) * ntok + row));
+  const int b = bits_of(d.type);
+  const int64_t bit = (int64_t(row) * d.size + d.j) * b;
+  const uint32_t code = (uint32_t(tile[coff[d.gidx] + (bit >> 3)]) >> (bit & 7)) & ((1u << b) - 1);
+  const uint32_t v = d.type == KVTC_T_FP8 ? e4m3x2_to_f16x2(code) : uint32_t(__half_as_ushort(__uint2half_rn(code)));
+  return uint16_t(hfma2_u(v, pr >> 16, pr & 0xFFFFu) & 0xFFFFu);
+}
+// Loads of one 16-byte A chunk of a FULL tile (code blocks b-aligned, params
+// 4-aligned), issued for a whole stage before any is consumed: no branches, the
+// fp8 high word through a predicated load, read-only path.
+__device__ __forceinline__ uint32_t ldg_u32(const uint8_t *p) {
+  return __ldg(reinterpret_cast<const unsigned int *>(p));
+}
+__device__ __forceinline__ uint32_t ldg_u32_if(const uint8_t *p, bool pred) {
+  uint32_t v = 0;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.nc.u32 %0, [%1];\n\t}"
+      : "+r"(v)
+      : "l"(p), "r"(uint32_t(pred)));
+  return v;
+}
+// One (row, chunk) item of the fused producer.  Full tiles: ok = 1 chunks load
+// their fp16 factors and 8 codes (2 / 4 / 8 bytes, b-aligned) straight from the
+// payload; ok = 3 chunks (size-1 groups, misaligned starts: columns the pre-pass
+// dequantised) load their 16 bytes from the tail buffer.  Branch-free address
+// selection, predicated loads, read-only path; the words are consumed one stage
+// later by dq_item_store.
+struct DqItem {
+  uint32_t w0, w1, w2, w3;
+};
+__device__ __forceinline__ void dq_item_issue(const DqChunk &d, const uint8_t *tile, const uint8_t *tail_row, int row,
+                                              DqItem &it) {
+  const bool dense = d.ok == 1, copy = d.ok == 3;
+  const uint8_t *pp = dense ? tile + d.par_base + 4 * row : (copy ? tail_row + d.code_base : tile);
+  const uint8_t *cp = dense ? tile + d.code_base + row * int32_t(d.stride) : pp;
+  const uint8_t *cq = reinterpret_cast<const uint8_t *>(reinterpret_cast<uintptr_t>(cp) & ~uintptr_t(3));
+  it.w0 = ldg_u32(pp);
+  it.w1 = ldg_u32_if(cq + (copy ? 4 : 0), dense || copy);
+  it.w2 = ldg_u32_if(cq + (copy ? 8 : 4), copy || (dense && d.type == KVTC_T_FP8));
+  it.w3 = ldg_u32_if(cq + 12, copy);
+  if (dense && d.type != KVTC_T_FP8) it.w1 >>= (reinterpret_cast<uintptr_t>(cp) & 3) * 8;   // int2: 2-aligned
+}
+// Element-by-element chunk (partial tiles only): out of line, so the unrolled
+// per-stage loops stay small (the inlined copies overflowed the instruction cache).
+__device__ __noinline__ uint4 dq_generic8(const DqCol *cols, int col0, const uint8_t *tile, const int64_t *coff,
+                                          int ntok, int row) {
+  uint16_t h[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) h[k] = dq1(tile, coff, ntok, row, cols[col0 + k]);
+  return make_uint4(uint32_t(h[0]) | (uint32_t(h[1]) << 16), uint32_t(h[2]) | (uint32_t(h[3]) << 16),
+                    uint32_t(h[4]) | (uint32_t(h[5]) << 16), uint32_t(h[6]) | (uint32_t(h[7]) << 16));
+}
+__device__ __forceinline__ uint4 dq_item_value(const DqChunk &d, const DqCol *cols, int col0, const uint8_t *tile,
+                                               const int64_t *coff, int ntok, int row, const DqItem &it) {
+  if (row >= ntok || !d.type) return make_uint4(0u, 0u, 0u, 0u);
+  if (d.ok == 3) return make_uint4(it.w0, it.w1, it.w2, it.w3);
+  if (ntok == kTileM && d.ok == 1) return dq8(d.type, it.w1, it.w2, it.w0);
+  return dq_generic8(cols, col0, tile, coff, ntok, row);   // partial tile
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// Wait with cluster-scope acquire (the full barrier also collects the peer CTA's
+// dequantising warps' release arrivals).
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
+  uint64_t t0 = 0;
+  for (uint32_t i = 0;; ++i) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if ((i & 1023) == 1023) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (!t0) t0 = t;
+      else if (t - t0 > 4000000000ull) __trap();
+    }
+  }
+}
+
+
+
+// Pre-pass of the fused inverse path: the A columns that are not whole aligned
+// 8-chunks of one group (size-1 groups -- the DP's fp16 "keep" option -- and
+// misaligned starts; 112 of the 4352 columns of the bench plan) are dequantised
+// here into a small side buffer, 16 bytes per (row, chunk), which the GEMM's
+// producer copies (R5: one fp16 rounding, like dq8).
+__global__ void __launch_bounds__(256) dq_tail_kernel(const DqCol *cols, const int32_t *tail_col, int32_t n_tail,
+                                                      const uint8_t *payload, int64_t m, int64_t tile_bytes,
+                                                      const int64_t *off_full, const int64_t *off_last,
+                                                      const TileRef *tiles, int32_t num_m, uint8_t *tail, int64_t ld) {
+  const int64_t total = int64_t(num_m) * kTileM * n_tail;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total; idx += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t rg = idx / n_tail;
+    const int k = int(idx - rg * n_tail);
+    const int mb = int(rg / kTileM), row = int(rg % kTileM);
+    const uint8_t *tile;
+    const int64_t *coff;
+    int ntok;
+    if (tiles) {
+      tile = tiles[mb].payload;
+      coff = tiles[mb].codes_off;
+      ntok = tiles[mb].ntok;
+    } else {
+      const int64_t m0 = int64_t(mb) * kTileM;
+      ntok = int(m - m0 < kTileM ? m - m0 : kTileM);
+      tile = payload + int64_t(mb) * tile_bytes;
+      coff = ntok < kTileM ? off_last : off_full;
+    }
+    uint4 o = make_uint4(0u, 0u, 0u, 0u);
+    if (row < ntok) {
+      const int c0 = tail_col[k];
+      uint16_t h[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) h[j] = dq1(tile, coff, ntok, row, cols[c0 + j]);
+      o = make_uint4(uint32_t(h[0]) | (uint32_t(h[1]) << 16), uint32_t(h[2]) | (uint32_t(h[3]) << 16),
+                     uint32_t(h[4]) | (uint32_t(h[5]) << 16), uint32_t(h[6]) | (uint32_t(h[7]) << 16));
+    }
+    *reinterpret_cast<uint4 *>(tail + rg * ld + k * 16) = o;
+  }
+}
+
+// Wide group (k 256-column pieces, P:L256 allows groups up to 1024): called by
+// all 128 epilogue threads of a CTA after they stored their piece's fp32
+// coefficients and row min/max.  The CTA whose piece arrives last for this
+// (M-block, group) quantises and packs the whole group from the scratch (L2),
+// so no separate pass over the coefficients is needed.
+__device__ __noinline__ void wide_fixup(const Params &P, int w, int mb, int row, int64_t tok, bool valid, int ntok,
+                                        bool last, uint8_t *tile_base, const int64_t *codes_off_last, int32_t *stw,
+                                        volatile int *flag) {
+  __threadfence();
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  const WideDesc wd = P.wide[w];
+  const int k = wd.size / kMaxTileN;
+  if (row == 0) *flag = atomicAdd(P.wcnt + int64_t(mb) * P.nwide + w, 1) == k - 1;
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  if (!*flag) return;
+  __threadfence();
+  if (!valid) return;
+  const float2 *mm = P.wmm + tok * P.wpieces + wd.wcol / kMaxTileN;
+  float mn = INFINITY, mx = -INFINITY;
+  for (int q = 0; q < k; ++q) {
+    const float2 v = __ldcg(mm + q);
+    mn = fminf(mn, v.x);
+    mx = fmaxf(mx, v.y);
+  }
+  uint16_t sh, sc;
+  group_factors(wd.type, mn, mx, sh, sc);
+  store_u32_any(tile_base + 4 * (int64_t(wd.gidx) * ntok + row), uint32_t(sh) | (uint32_t(sc) << 16), !last);
+  if (stw && factor_overflow(sh, sc)) atomicOr(stw, 1);
+  const float shift = f16_val(sh), scale = f16_val(sc);
+  const int b = bits_of(wd.type);
+  const int per_word = 32 / b;
+  const int words = wd.size * b / 32;
+  uint8_t *dst = tile_base + (last ? codes_off_last[wd.gidx] : wd.codes_off) + int64_t(row) * (wd.size * b / 8);
+  const float *x = P.D + tok * P.ldd + wd.wcol;
+  for (int wi = 0; wi < words; ++wi) {
+    uint32_t word = 0;
+    for (int j = 0; j < per_word; j += 4) {
+      const float4 v = __ldcg(reinterpret_cast<const float4 *>(x + wi * per_word + j));
+      word |= encode_one(wd.type, v.x, shift, scale) << (j * b);
+      word |= encode_one(wd.type, v.y, shift, scale) << ((j + 1) * b);
+      word |= encode_one(wd.type, v.z, shift, scale) << ((j + 2) * b);
+      word |= encode_one(wd.type, v.w, shift, scale) << ((j + 3) * b);
+    }
+    store_u32_any(dst + 4 * wi, word, !last);
+  }
 }
 
 // Soft tile barrier of the TMA producers: the CTAs of one wave of tiles share
@@ -299,12 +590,13 @@ __device__ __forceinline__ int tile_nsub(const Params &P, const Tile &T) {
 // Register budget: the compress GEMM runs beside the side-stream gather / encoder
 // CTAs (2-3 per SM), so it is held to 128 registers (min 2 blocks); the
 // decompress GEMM (beside the dequantiser) may use more.
-template <int MODE, bool PAIR, int NSUB, int KB>
-__global__ void __launch_bounds__(kThreads, MODE == EPI_RECON ? 1 : 2)
+template <int MODE, bool PAIR, int NSUB, int KB, int ASRC>
+__global__ void __launch_bounds__(threads_for(ASRC), MODE == EPI_RECON ? 1 : 2)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ Params P) {
   static_assert(NSUB == 1 || (MODE == EPI_QUANT && PAIR), "two-segment tiles: compress, CTA pairs");
   static_assert(KB == 1 || (PAIR && NSUB == 1), "two k-blocks per stage: CTA pairs, one segment");
+  static_assert(ASRC == 0 || (MODE == EPI_RECON && PAIR && KB == 2), "fused A producer: decompress, pairs, KB 2");
   using C = Cfg<PAIR, NSUB, KB>;
   constexpr int kStages = C::kStages;
   constexpr int kABytes = C::kABytes;
@@ -312,13 +604,18 @@ __global__ void __launch_bounds__(kThreads, MODE == EPI_RECON ? 1 : 2)
   constexpr int kBSub = C::kBSubBytes;
   constexpr int kAccBufs = C::kAccBufs;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte alignment by pointer arithmetic on the __shared__ array (an integer
+  // round trip would make every smem access generic: ST.E / LD.E instead of STS / LDS)
+  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t *tiles = smem;
   uint64_t *full_bar = reinterpret_cast<uint64_t *>(smem + kStages * kStageBytes);
   uint64_t *empty_bar = full_bar + kStages;
   uint64_t *tmem_full = empty_bar + kStages;      // [2]
   uint64_t *tmem_empty = tmem_full + 2;           // [2]
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_empty + 2);
+  volatile int *wide_flag = reinterpret_cast<volatile int *>(tmem_slot + 1);
+  // ASRC: the plan's A-chunk table (DqChunk per 8 columns) in shared memory
+  uint8_t *dq_tab = smem + kStages * kStageBytes + 256;
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -331,12 +628,18 @@ __global__ void __launch_bounds__(kThreads, MODE == EPI_RECON ? 1 : 2)
   const int64_t t_step = int64_t(PAIR ? gridDim.x / 2 : gridDim.x);
   const int num_kb = (P.K + kBlockK - 1) / kBlockK;
   const int num_st = (num_kb + KB - 1) / KB;       // pipeline stages per tile
+  if constexpr (ASRC == 1) {
+    const uint4 *src = reinterpret_cast<const uint4 *>(P.dq_chunks);
+    uint4 *dst = reinterpret_cast<uint4 *>(dq_tab);
+    for (int i = threadIdx.x; i < num_st * (KB * kBlockK / 8); i += blockDim.x) dst[i] = src[i];
+  }
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full_bar[s], 1);
+      // ASRC: + one arrival per dequantising warp of both CTAs (leader's barrier)
+      mbar_init(&full_bar[s], ASRC ? 1 + 2 * 4 : 1);
       mbar_init(&empty_bar[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -383,7 +686,10 @@ __global__ void __launch_bounds__(kThreads, MODE == EPI_RECON ? 1 : 2)
       const int nsub = tile_nsub<NSUB>(P, T);
       for (int ks = 0; ks < num_st; ++ks, ++it) {
         const int s = it % kStages;
-        if (it >= kStages) mbar_wait(&empty_bar[s], ((it / kStages) - 1) & 1);
+        if (it >= kStages) {
+          if (P.spin & 1) mbar_wait_spin(&empty_bar[s], ((it / kStages) - 1) & 1);
+          else mbar_wait(&empty_bar[s], ((it / kStages) - 1) & 1);
+        }
         uint8_t *a = tiles + s * kStageBytes;
         uint8_t *b = a + kABytes;
         const int32_t ka = ks * KB * kBlockK;
@@ -399,6 +705,12 @@ __global__ void __launch_bounds__(kThreads, MODE == EPI_RECON ? 1 : 2)
             const int nm = (sd.width + 15) & ~15;
             tma_load_2d_pair(b + sb * kBSub, &tmB, &full_bar[s], ka, sd.col0 + int(rank) * (nm / 2));
           }
+        } else if constexpr (KB == 2 && ASRC == 1) {
+          // A comes from the dequantising warps: only the B k-blocks through TMA
+          if (leader) mbar_arrive_expect_tx(&full_bar[s], 2 * C::kBBytes);
+#pragma unroll
+          for (int kk = 0; kk < KB; ++kk)
+            tma_load_2d_pair(b + kk * kBSub, &tmB, &full_bar[s], ka + kk * kBlockK, n0 + int(rank) * (n_mma / 2));
         } else if constexpr (KB == 2) {
           // two k-blocks per stage: A blocks then B blocks; both CTAs' bytes on the leader's barrier
           if (leader) mbar_arrive_expect_tx(&full_bar[s], 2 * kStageBytes);
@@ -455,7 +767,10 @@ __global__ void __launch_bounds__(kThreads, MODE == EPI_RECON ? 1 : 2)
       const int n_mma = (ncols + 15) & ~15;
       const uint32_t idesc = make_idesc_f16(P.fmt, PAIR ? 2 * kTileM : kTileM, n_mma);
       const uint32_t acc = acc_it % kAccBufs;
-      if (acc_it >= kAccBufs) mbar_wait(&tmem_empty[acc], ((acc_it / kAccBufs) - 1) & 1);
+      if (acc_it >= kAccBufs) {
+        if (P.spin & 2) mbar_wait_spin(&tmem_empty[acc], ((acc_it / kAccBufs) - 1) & 1);
+        else mbar_wait(&tmem_empty[acc], ((acc_it / kAccBufs) - 1) & 1);
+      }
       tc_fence_after();
       const uint32_t tacc = tmem_base + acc * kMaxTileN;
       const int nsub = tile_nsub<NSUB>(P, T);
@@ -468,7 +783,9 @@ __global__ void __launch_bounds__(kThreads, MODE == EPI_RECON ? 1 : 2)
       for (int ks = 0; ks < num_st; ++ks, ++it) {
         const int kb = ks;                         // KB == 1: stage == k-block
         const int s = it % kStages;
-        mbar_wait(&full_bar[s], (it / kStages) & 1);
+        if constexpr (ASRC == 1) mbar_wait_cluster(&full_bar[s], (it / kStages) & 1);
+        else if (P.spin & 8) mbar_wait_spin(&full_bar[s], (it / kStages) & 1);
+        else mbar_wait(&full_bar[s], (it / kStages) & 1);
         tc_fence_after();
         const uint64_t ad = make_sdesc_sw128(tiles + s * kStageBytes);
         const uint64_t bd = make_sdesc_sw128(tiles + s * kStageBytes + kABytes);
@@ -506,7 +823,83 @@ __global__ void __launch_bounds__(kThreads, MODE == EPI_RECON ? 1 : 2)
       else umma_commit(&tmem_full[acc]);
       ++acc_it;
     }
-  } else if (warp >= 4) {
+  } else if (ASRC == 1 && warp >= 8) {
+    // ---------------- dequantising A producer (D2 fused into K5).  Two
+    // groups of four warps take alternate pipeline stages (two stages' loads in
+    // flight); in a group, warp q covers rows 32 q .. 32 q + 31 of this CTA's A
+    // half, two rows per step with lane = (row, 16-byte chunk) so a row's codes
+    // are read as contiguous bytes.  All loads of a stage are issued before its
+    // smem slot is awaited.
+    constexpr int kCh = KB * kBlockK / 8;          // 16 chunks per stage and row
+    const int grp = (warp - 8) / 4, q = (warp - 8) % 4;
+    const int half = lane >> 4, ch = lane & 15;
+    const int kk = ch / 8, c8 = ch % 8;
+    const DqChunk *tab = reinterpret_cast<const DqChunk *>(dq_tab);
+    const int64_t my_tiles = t_first < total ? (total - t_first + t_step - 1) / t_step : 0;
+    int64_t ti = 0;
+    int ks = grp;
+    while (ks >= num_st && num_st > 0) {           // few stages per tile: the group starts on a later tile
+      ks -= num_st;
+      ++ti;
+      while (ks >= num_st && num_st > 0) {
+        ks -= num_st;
+        ++ti;
+      }
+    }
+    for (; ti < my_tiles && num_st > 0;) {
+      const Tile T = get_tile(t_first + ti * t_step);
+      const uint8_t *tile = P.dq_payload;
+      const int64_t *coff = P.dq_off_full;
+      int ntok = 0;
+      int64_t row0 = 0;                             // first tail-buffer row of this tile
+      if (P.tiles) {
+        if (T.mb < P.num_m) {
+          const TileRef &tr = P.tiles[T.mb];
+          tile = tr.payload;
+          coff = tr.codes_off;
+          ntok = tr.ntok;
+        }
+        row0 = int64_t(T.mb) * kTileM;
+      } else {
+        row0 = int64_t(T.mb) * kTileM;
+        ntok = int(P.m - row0 < kTileM ? (P.m > row0 ? P.m - row0 : 0) : kTileM);
+        tile = P.dq_payload + int64_t(T.mb) * P.tile_bytes;
+        coff = ntok < kTileM ? P.dq_off_last : P.dq_off_full;
+      }
+      for (; ks < num_st; ks += kDqGroups) {
+        const uint32_t n = uint32_t(ti * num_st + ks);          // stage index of this CTA
+        const DqChunk d = tab[ks * kCh + ch];
+        DqItem items[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int row = 32 * q + 2 * i + half;
+          const uint8_t *tail_row = P.dq_tail ? P.dq_tail + (row0 + row) * P.dq_tail_ld : tile;
+          if ((P.dq_debug & 1) == 0 && (ntok == kTileM || (ntok > 0 && d.ok == 3)))
+            dq_item_issue(d, tile, tail_row, row, items[i]);
+          else
+            items[i] = DqItem{0x3C003C00u, 0u, 0u, 0u};
+        }
+        const int s = int(n % kStages);
+        if (n >= uint32_t(kStages)) mbar_wait_spin(&empty_bar[s], ((n / kStages) - 1) & 1);
+        uint8_t *a = tiles + s * kStageBytes + kk * (kTileM * kBlockK * 2);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          if (P.dq_debug & 2) break;
+          const int row = 32 * q + 2 * i + half;
+          const uint4 o = dq_item_value(d, P.dq_cols, ks * KB * kBlockK + ch * 8, tile, coff, ntok, row, items[i]);
+          *reinterpret_cast<uint4 *>(a + row * 128 + ((c8 ^ (row & 7)) << 4)) = o;
+        }
+        if (!(P.dq_debug & 4)) fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if (leader) mbar_arrive(&full_bar[s]);
+          else mbar_arrive_remote(&full_bar[s], 0);
+        }
+      }
+      ks -= num_st;
+      ++ti;
+    }
+  } else if (warp >= 4 && warp < 8) {
     // ---------------- epilogue
     auto release_acc = [&](uint32_t a) {
       if (!PAIR || leader) mbar_arrive(&tmem_empty[a]);
@@ -528,7 +921,8 @@ __global__ void __launch_bounds__(kThreads, MODE == EPI_RECON ? 1 : 2)
           (MODE == EPI_QUANT || MODE == EPI_RECON) && P.tiles && T.mb < P.num_m ? P.tiles + T.mb : nullptr;
       const bool valid = tref ? row < tref->ntok : tok < P.m;
       const uint32_t acc = acc_it % kAccBufs;
-      mbar_wait(&tmem_full[acc], (acc_it / kAccBufs) & 1);
+      if (P.spin & 4) mbar_wait_spin(&tmem_full[acc], (acc_it / kAccBufs) & 1);
+      else mbar_wait(&tmem_full[acc], (acc_it / kAccBufs) & 1);
       tc_fence_after();
       const uint32_t trow = tmem_base + acc * kMaxTileN + (uint32_t((warp & 3) * 32) << 16);
 
@@ -558,6 +952,9 @@ __global__ void __launch_bounds__(kThreads, MODE == EPI_RECON ? 1 : 2)
         uint8_t *tile_base = tref ? tref->payload : P.payload + T.mb * P.tile_bytes;
         const int64_t *codes_off_last = tref ? tref->codes_off : P.codes_off_last;
         const int nsub = P.epi_skip ? 0 : tile_nsub<NSUB>(P, T);
+        int wide_w[NSUB];                          // wide groups whose piece this tile stored
+#pragma unroll
+        for (int sb = 0; sb < NSUB; ++sb) wide_w[sb] = -1;
         for (int sb = 0; sb < nsub; ++sb) {
         const SegDesc sdq = P.segs[T.nb * NSUB + sb];
         const uint32_t trow_s = trow + (NSUB == 2 ? uint32_t(sb * kMaxTileN) : 0u);
@@ -565,17 +962,25 @@ __global__ void __launch_bounds__(kThreads, MODE == EPI_RECON ? 1 : 2)
         const int f32_col = sdq.f32_col;
         const int ncols_s = sdq.width;
         if (f32_col >= 0) {
-          // piece of a wide group: fp32 D - mu V_c to the scratch
+          // piece of a wide group: fp32 D - mu V_c and its row min/max to the scratch
           float *dst = P.D + (valid ? tok : 0) * P.ldd + f32_col;
+          float pmn = INFINITY, pmx = -INFINITY;
           for (int c = 0; c < ncols_s; c += 16) {
             float x[16];
             load_cols(trow_s, bias, c, 16, x);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              pmn = fminf(pmn, x[j]);
+              pmx = fmaxf(pmx, x[j]);
+            }
             if (valid) {
 #pragma unroll
               for (int j = 0; j < 16; j += 4)
                 *reinterpret_cast<float4 *>(dst + c + j) = make_float4(x[j], x[j + 1], x[j + 2], x[j + 3]);
             }
           }
+          if (valid) P.wmm[tok * P.wpieces + f32_col / kMaxTileN] = make_float2(pmn, pmx);
+          wide_w[sb] = sdq.wide;
         }
         // sub-byte code block of one group (tokens of size * bits < 8 bits): OR-reduction over the warp
         auto emit_subbyte = [&](const GroupDesc &g, uint32_t bits_v) {
@@ -709,6 +1114,15 @@ __global__ void __launch_bounds__(kThreads, MODE == EPI_RECON ? 1 : 2)
         }
         tc_fence_before();
         release_acc(acc);
+        // wide groups: the last piece's CTA quantises the whole group (after the
+        // accumulator is released, so the next tile's MMAs are not held up)
+        if (ntok > 0) {
+          int32_t *stw = tref ? tref->status : P.status;
+#pragma unroll
+          for (int sb = 0; sb < NSUB; ++sb)
+            if (wide_w[sb] >= 0)
+              wide_fixup(P, wide_w[sb], T.mb, row, tok, valid, ntok, last, tile_base, codes_off_last, stw, wide_flag);
+        }
       } else if constexpr (MODE == EPI_RECON) {
         // tcgen05.ld is warp-collective: every lane loads, only valid rows store
         const int d = P.head_dim;
@@ -829,16 +1243,27 @@ static int num_sms() {
   return n;
 }
 
-template <int MODE, bool PAIR, int NSUB = 1, int KB = 1>
+template <int MODE, bool PAIR, int NSUB = 1, int KB = 1, int ASRC = 0>
 static kvtc_status launch(const CUtensorMap *tmA, const CUtensorMap *tmB, const Params &p, dim3 grid, int cluster,
                           cudaStream_t st) {
   static bool configured = false;
-  constexpr int kSmemBytes = Cfg<PAIR, NSUB, KB>::kSmemBytes;
+  using C = Cfg<PAIR, NSUB, KB>;
+  // ASRC: the A-chunk table lives after the barriers (256 B in), up to kDqTabMaxBytes
+  constexpr int kSmemMax = ASRC ? C::kStages * C::kStageBytes + 1024 + 256 + kDqTabMaxBytes : C::kSmemBytes;
+  int smem_bytes = C::kSmemBytes;
+  if (ASRC) {
+    const int num_st = int(ceil_div(ceil_div(p.K, kBlockK), KB));
+    smem_bytes = std::max(smem_bytes, C::kStages * C::kStageBytes + 1024 + 256 + num_st * KB * kBlockK / 8 * 16);
+    if (smem_bytes > kSmemMax) {
+      set_error("fused reconstruction: %d plan columns exceed the shared-memory chunk table", p.K);
+      return KVTC_E_INVALID;
+    }
+  }
   if (!configured) {
-    KVTC_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<MODE, PAIR, NSUB, KB>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    KVTC_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<MODE, PAIR, NSUB, KB, ASRC>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
     // the 228 KB configuration, shared with the side-stream kernels (internal.h)
-    KVTC_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<MODE, PAIR, NSUB, KB>,
+    KVTC_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<MODE, PAIR, NSUB, KB, ASRC>,
                                        cudaFuncAttributePreferredSharedMemoryCarveout,
                                        int(cudaSharedmemCarveoutMaxShared)));
     configured = true;
@@ -857,6 +1282,10 @@ static kvtc_status launch(const CUtensorMap *tmA, const CUtensorMap *tmB, const 
     if (hb) pp.hint_b = atoi(hb);
     // soft tile barrier (tile_barrier) for the codec GEMMs; KVTC_TILE_SYNC = bit mask
     // over modes overrides (0 = off)
+    const char *dd = getenv("KVTC_DQ_DEBUG");
+    pp.dq_debug = dd ? atoi(dd) : 0;
+    const char *sw = getenv("KVTC_SPIN_WAITS");
+    pp.spin = sw ? atoi(sw) : 0;
     const char *es = getenv("KVTC_EPI_SKIP");
     pp.epi_skip = es && es[0] == '1';
     const char *ts = getenv("KVTC_TILE_SYNC");
@@ -875,8 +1304,8 @@ static kvtc_status launch(const CUtensorMap *tmA, const CUtensorMap *tmB, const 
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.blockDim = dim3(threads_for(ASRC));
+  cfg.dynamicSmemBytes = smem_bytes;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -885,7 +1314,7 @@ static kvtc_status launch(const CUtensorMap *tmA, const CUtensorMap *tmB, const 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  KVTC_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_kernel<MODE, PAIR, NSUB, KB>, *tmA, *tmB, pp));
+  KVTC_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_kernel<MODE, PAIR, NSUB, KB, ASRC>, *tmA, *tmB, pp));
   note_launch();
   return KVTC_OK;
 }
@@ -941,6 +1370,15 @@ kvtc_status launch_gemm_project_quant(const GemmCompressArgs &a, cudaStream_t st
   p.ldd = a.ldd;
   p.tiles = a.tiles;
   p.status = a.status;
+  if (a.nwide > 0) {
+    // scratch layout (wide_scratch_bytes): fp32 pieces, row min/max, counters
+    p.wide = a.wide;
+    p.nwide = a.nwide;
+    p.wpieces = int32_t(a.ldd / kMaxTileN);
+    p.wmm = reinterpret_cast<float2 *>(a.D + a.m * a.ldd);
+    p.wcnt = reinterpret_cast<int32_t *>(p.wmm + a.m * p.wpieces);
+    KVTC_CUDA_TRY(cudaMemsetAsync(p.wcnt, 0, size_t(ceil_div(a.m, kTileM)) * a.nwide * 4, st));
+  }
   // KVTC_QUANT_NSUB=2: two segments per tile (Cfg<true, 2>, 25 % less L2 traffic);
   // measured slower (tensor pipe 58 % vs 88 %: the 512-column epilogue is not
   // overlapped), so one segment per tile with double-buffered TMEM is the default
@@ -978,6 +1416,28 @@ kvtc_status launch_gemm_reconstruct(const GemmDecompressArgs &a, cudaStream_t st
   p.tile_n = a.tile_n;
   p.num_m = int32_t(ceil_div(a.m, kTileM));
   p.num_n = int32_t(ceil_div(a.n_end - a.n_begin, a.tile_n));
+  if (a.dqcols) {
+    // fused inverse path: A dequantised from the payload by the producer warps
+    p.dq_payload = a.payload;
+    p.dq_off_full = a.codes_off_full;
+    p.dq_off_last = a.codes_off_last;
+    p.dq_cols = a.dqcols;
+    p.dq_chunks = a.dqchunks;
+    p.dq_tail = a.dq_tail;
+    p.dq_tail_ld = int64_t(a.n_tail) * 16;
+    if (a.n_tail > 0 && a.m > 0) {
+      KVTC_CHECK_ARG(a.dq_tail && a.tail_cols, "fused reconstruction: tail buffer");
+      const int64_t items = int64_t(p.num_m) * kTileM * a.n_tail;
+      KVTC_MAX_CARVEOUT(dq_tail_kernel);
+      dq_tail_kernel<<<unsigned(std::min<int64_t>(ceil_div(items, 256), 8 * num_sms())), 256, 0, st>>>(
+          a.dqcols, a.tail_cols, a.n_tail, a.payload, a.m, a.tile_bytes, a.codes_off_full, a.codes_off_last, a.tiles,
+          p.num_m, a.dq_tail, p.dq_tail_ld);
+      KVTC_LAUNCH_CHECK();
+    }
+    p.tile_bytes = a.tile_bytes;
+    return launch<EPI_RECON, true, 1, 2, 1>(a.tmB, a.tmB, p,
+                                            dim3(pair_grid(int64_t((p.num_m + 1) / 2) * p.num_n)), 2, st);
+  }
   if (kb2_for(EPI_RECON))
     return launch<EPI_RECON, true, 1, 2>(a.tmA, a.tmB, p, dim3(pair_grid(int64_t((p.num_m + 1) / 2) * p.num_n)), 2,
                                          st);

@@ -34,9 +34,13 @@ struct SegDesc {
   int32_t g_begin, g_end;  // GroupDesc range
   int32_t f32_col;    // >= 0: a 256-column piece of a wide group; the epilogue
                       // stores D - mu V_c (fp32) at this column of the wide scratch
+  int32_t wide;       // wide pieces: index of the group in the plan's WideDesc table, else -1
 };
-// A group wider than one tile (size = k * 256): quantised after the GEMM from
-// its fp32 coefficients (quant_wide_kernel).
+// A group wider than one tile (size = k * 256).  Each of its k pieces is a GEMM
+// tile whose epilogue stores fp32 coefficients + the row min/max of the piece to
+// a scratch; the epilogue of the piece that completes last (an arrival counter
+// per (M-block, group)) quantises and packs the whole group (SIMT reference:
+// quant_wide_kernel).
 struct WideDesc {
   int32_t gidx;       // index among non-None groups (params slot)
   int32_t size, type;
@@ -46,12 +50,40 @@ struct WideDesc {
   int64_t codes_off;  // code block offset in a FULL tile
 };
 
+// One column of the decompress GEMM's A operand (a compacted non-None PC) for the
+// dequantising producer of the fused inverse path (D2 inside K5):
+// the producer warps read codes + fp16 factors from the payload and write the
+// fp16 A tile straight into shared memory.
+struct DqCol {
+  uint16_t gidx;      // group among non-None groups (params slot / code block)
+  uint8_t type;       // kvtc_type; 0 = padding column past r_nz (A = 0)
+  uint8_t chunk;      // 1: columns [c, c + 8) are elements j .. j + 7 (j % 8 == 0) of this group
+  uint16_t j;         // element index inside the group
+  uint16_t size;      // group size
+  int32_t off_full;   // byte offset of the group's code block in a FULL tile
+  int32_t pad;
+};
+
+// One 16-byte A chunk (8 columns) of the fused producer, per pipeline position
+// (shared-memory table): ok = 1 when the 8 columns are elements j .. j+7
+// (j % 8 == 0) of one group (byte offsets of a FULL tile); ok = 3 for the other
+// chunks with columns (code_base = 16 * its index in the tail buffer).
+struct DqChunk {
+  int32_t code_base;  // group code block + j * bits / 8
+  int32_t par_base;   // 4 * gidx * 128 (params of token 0)
+  uint16_t stride;    // code bytes per token (size * bits / 8)
+  uint8_t type;       // kvtc_type of the chunk's group (0: padding)
+  uint8_t ok;
+  uint32_t pad;
+};
+constexpr int kDqTabMaxBytes = 32 * 1024;   // shared-memory budget of the chunk table (16384 columns)
+
 // Batched codec (kvtc_compress_batch / kvtc_decompress_batch): ONE GEMM over the
 // concatenated rows of several conversations, each padded to whole 128-token
 // tiles; tile mb of the GEMM refers to one tile of one conversation.
 struct TileRef {
-  uint8_t *payload;                 // compress: this tile's payload bytes
-  const int64_t *codes_off;         // compress: code-block offsets (full or partial tile)
+  uint8_t *payload;                 // this tile's payload bytes (compress: written; decompress: read by K5)
+  const int64_t *codes_off;         // code-block offsets (full or partial tile)
   __nv_bfloat16 *const *bases;      // decompress: the conversation's device layer-base array
   const int32_t *block_table;       // decompress: paged layout
   int64_t tok0;                     // decompress: cache token of the tile's first row
@@ -83,6 +115,15 @@ kvtc_status make_tmap_3d(CUtensorMap *m, const void *base, CUtensorMapDataType d
                          uint64_t d2, uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box0, uint32_t box1);
 
 // ------------------------------------------------------------------ launchers
+// Scratch of the wide groups of a compress GEMM over m rows: fp32 coefficients
+// [m x wide_cols], per-piece row min/max [m x wide_cols/256] float2, arrival
+// counters [ceil(m/128) x nwide] int32.
+inline size_t wide_scratch_bytes(int64_t m, int32_t wide_cols, int32_t nwide) {
+  if (!nwide || !m) return 0;
+  return size_t(m) * wide_cols * 4 + size_t(m) * (wide_cols / kMaxTileN) * 8 + size_t(ceil_div(m, kTileM)) * nwide * 4 +
+         256;
+}
+
 struct GemmCompressArgs {
   const CUtensorMap *tmA;  // X [m x p] bf16, box {64, 128}
   const CUtensorMap *tmB;  // VcT [r_nz x p] bf16, box {64, 128}
@@ -107,6 +148,10 @@ struct GemmCompressArgs {
   int64_t a_layer_rows;    // a_hd > 0 and a_layer_rows > 0: tmA is a 2-D map over [layers * tokens][h*d]
   const TileRef *tiles;    // non-null: batched rows (tile mb -> tiles[mb]); payload / m unused
   int32_t *status;         // nullable: bit 0 set when an fp16 shift / scale overflowed (Q4)
+  // wide groups (quantised in the epilogue of their last piece): D is the scratch
+  // of wide_scratch_bytes(m, ldd, nwide) bytes
+  const WideDesc *wide;
+  int32_t nwide;
 };
 kvtc_status launch_gemm_project_f32(const GemmCompressArgs &a, int32_t ncols, cudaStream_t st);
 kvtc_status launch_gemm_project_quant(const GemmCompressArgs &a, cudaStream_t st);
@@ -127,7 +172,19 @@ struct GemmDecompressArgs {
   int64_t tok_begin;                 // cache token index of row 0
   int32_t tile_n;                    // N tile (<= 256, divides heads*head_dim)
   const TileRef *tiles;              // non-null: batched rows; the output view comes from tiles[mb]
+  // fused inverse path (payload != nullptr or tiles != nullptr with dqcols): A = D^ is
+  // dequantised from the payload inside the GEMM (tmA unused)
+  const uint8_t *payload;            // m rows of 128-token payload tiles
+  const int64_t *codes_off_full, *codes_off_last;
+  int64_t tile_bytes;
+  const DqCol *dqcols;               // [ceil(K / 128) * 128]; non-null selects the fused path
+  const DqChunk *dqchunks;           // [ceil(K / 128) * 16]
+  const int32_t *tail_cols;          // [n_tail] first column of each ok = 3 chunk
+  int32_t n_tail;
+  uint8_t *dq_tail;                  // [ceil(m / 128) * 128][n_tail * 16 B] pre-pass output
 };
+// Bytes of the fused path's tail buffer for m rows.
+inline size_t dq_tail_bytes(int64_t m, int32_t n_tail) { return size_t(ceil_div(m, kTileM)) * kTileM * n_tail * 16; }
 kvtc_status launch_gemm_reconstruct(const GemmDecompressArgs &a, cudaStream_t st);
 
 // XtX accumulation: S[p x p] += C^T C for a chunk Ct [p x nk] (K-major);

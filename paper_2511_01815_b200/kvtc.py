@@ -171,6 +171,16 @@ def project(basis: Basis, plan: Plan | None, X: torch.Tensor, ncols: int, stream
     return D
 
 
+def project_partial(basis: Basis, plan: Plan, X: torch.Tensor, feat_begin: int, feat_end: int, add_bias: bool,
+                    stream=None):
+    """Joint cross-shard compression: this shard's partial projection (fp32 [m x ncols(plan)])."""
+    ncols = sum(z for (_, z, _) in plan.info().groups)
+    D = torch.zeros(X.shape[0], max(ncols, 1), dtype=torch.float32, device="cuda")
+    check(lib().kvtc_stage_project_partial(basis.h, plan.h, _ptr(X), X.shape[0], feat_begin, feat_end, int(add_bias),
+                                           _ptr(D), _stream(stream)))
+    return D[:, :ncols]
+
+
 def quantize_pack(plan: Plan, D: torch.Tensor, stream=None):
     m = D.shape[0]
     out = torch.zeros(plan.payload_bytes(m) + 16, dtype=torch.uint8, device="cuda")
@@ -233,6 +243,13 @@ def reconstruct(basis: Basis, plan: Plan, Dh: torch.Tensor, m: int, tok_begin: i
                 layer_end: int, out: KVView, stream=None):
     check(lib().kvtc_stage_reconstruct(basis.h, plan.h, _ptr(Dh), Dh.shape[1], m, tok_begin, layer_begin, layer_end,
                                        C.byref(out.c), _stream(stream)))
+
+
+def reconstruct_payload(basis: Basis, plan: Plan, payload: torch.Tensor, m: int, tok_begin: int, layer_begin: int,
+                        layer_end: int, out: KVView, stream=None):
+    """D2 + K5 fused: the reconstruction GEMM dequantising its A operand from the payload."""
+    check(lib().kvtc_stage_reconstruct_payload(basis.h, plan.h, _ptr(payload), m, tok_begin, layer_begin, layer_end,
+                                               C.byref(out.c), _stream(stream)))
 
 
 # ------------------------------------------------------------------ codec

@@ -43,6 +43,9 @@ def main():
             for kvp in var.split(","):
                 k, v = kvp.split("=")
                 os.environ[k] = v
+        # the decompression workspace depends on the variant (KVTC_DQ_FUSED=0 adds D^)
+        dws = torch.empty(K.decompress_workspace_bytes(kb, kp, vb, vp, cont[:256].cpu().numpy().tobytes()),
+                          dtype=torch.uint8, device="cuda")
         for _ in range(2):
             K.compress(kb, kp, vb, vp, kv, vv, out=cont, workspace=cws, sync_len=False)
             K.decompress(kb, kp, vb, vp, cont, K.KVView(Ko), K.KVView(Vo), workspace=dws)

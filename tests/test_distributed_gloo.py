@@ -158,3 +158,55 @@ def test_calibrate_distributed_world2_equals_single_process():
         assert np.all(cos > 0.999), cos
     # local=True: each rank's basis is its own half of the draw (they differ)
     assert not np.array_equal(ret[0]["local"][1], ret[1]["local"][1])
+
+
+# ---------------------------------------------------------------- joint cross-shard exchange
+def _joint_worker(rank, world, port, Xs, V, ret):
+    """Rank g holds the rows X_g of its layer shard and V_g (its rows of V): the
+    reduce-scatter of the partial products must give each rank its tile-aligned
+    slice of X V (block identity sum_g X_g V_g = X V), and the all-gather of the
+    slices every row (joint.py; the kernels are replaced by torch matmuls here)."""
+    from paper_2511_01815_b200.joint import all_gather_rows, reduce_scatter_rows, row_partition
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    f0 = sum(x.shape[1] for x in Xs[:rank])
+    Xg = torch.from_numpy(Xs[rank])
+    Vg = torch.from_numpy(V[f0:f0 + Xs[rank].shape[1]])
+    P = Xg @ Vg
+    mine = reduce_scatter_rows(P, world, rank)
+    m = P.shape[0]
+    full = all_gather_rows(mine, m, world, rank)
+    ret[rank] = (mine.numpy().copy(), full.numpy().copy(), row_partition(m, world)[1][rank])
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("m", [1000, 100, 257])
+def test_joint_exchange_world2(m):
+    rng = np.random.default_rng(m)
+    Xs = [rng.standard_normal((m, 48)), rng.standard_normal((m, 80))]       # two shards of 48 / 80 features
+    V = rng.standard_normal((128, 24))
+    port = _free_port()
+    mgr = mp.Manager()
+    ret = mgr.dict()
+    mp.spawn(_joint_worker, args=(2, port, Xs, V, ret), nprocs=2, join=True)
+    D = np.concatenate(Xs, axis=1) @ V                                       # the joint projection
+    rows = []
+    for r in range(2):
+        mine, full, (r0, r1) = ret[r]
+        assert (r0 % 128 == 0 or r0 == m) and mine.shape == (r1 - r0, 24)   # empty tail slices allowed
+        np.testing.assert_allclose(mine, D[r0:r1], rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(full, D, rtol=1e-12, atol=1e-12)
+        rows.append((r0, r1))
+    assert rows[0][0] == 0 and rows[0][1] == rows[1][0] and rows[1][1] == m   # the slices tile the rows
+
+
+def test_row_partition_properties():
+    from paper_2511_01815_b200.joint import row_partition
+    for m in (0, 1, 127, 128, 129, 1000, 32636):
+        for world in (1, 2, 3, 8):
+            per, parts = row_partition(m, world)
+            assert per % 128 == 0 and world * per >= m
+            assert parts[0][0] == 0 and parts[-1][1] == m
+            for (a, b), (c, d) in zip(parts, parts[1:]):
+                assert b == c and a <= b and (a % 128 == 0 or a == m)

@@ -276,3 +276,33 @@ def test_separate_key_value_compression_ratios(K):
     K.decompress(KB, KP, VB, VP, cont, K.KVView(ko), K.KVView(vo))
     rk, rv = E.oracle_restore(buf, kb, okp, vb, ovp, invf)
     E.assert_restored_like_oracle(ko, vo, rk, rv)
+
+
+@pytest.mark.parametrize("name,tokens", [("mid", 1000), ("toy", 400)])
+def test_fused_dequant_decompress_matches(K, monkeypatch, name, tokens):
+    """KVTC_DQ_FUSED=1 (the reconstruction GEMM's producer warps dequantise the
+    payload straight into shared memory, D^ never in HBM; D2 fused into K5,
+    P:L209) gives bit-identical caches to the default D^-through-TMA path, for the
+    whole decompression, a layer range and the layer-streamed calls."""
+    spec, invf, kb, vb, KB, VB, KP, VP, okp, ovp = _setup(K, name)
+    Kc, Vc = E.caches(name, tokens, 5, conversation=11)
+    kd, vd = Kc.cuda(), Vc.cuda()
+    cont, _ = K.compress(KB, KP, VB, VP, K.KVView(kd, pos0=5), K.KVView(vd, pos0=5))
+
+    def run(lb=0, le=None, streamed=False):
+        ok, ov = torch.zeros_like(kd), torch.zeros_like(vd)
+        le = spec.layers if le is None else le
+        if streamed:
+            sd = K.StreamedDecompress(KB, KP, VB, VP, cont)
+            sd.layers(K.KVView(ok, pos0=5), K.KVView(ov, pos0=5), lb, le)
+        else:
+            K.decompress(KB, KP, VB, VP, cont, K.KVView(ok, pos0=5), K.KVView(ov, pos0=5), layer_begin=lb,
+                         layer_end=le)
+        torch.cuda.synchronize()
+        return ok, ov
+
+    ref = [run(), run(spec.layers - 1), run(0, 1, True)]
+    monkeypatch.setenv("KVTC_DQ_FUSED", "1")
+    got = [run(), run(spec.layers - 1), run(0, 1, True)]
+    for (a, b), (c, d) in zip(ref, got):
+        assert torch.equal(a, c) and torch.equal(b, d)
