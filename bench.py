@@ -37,6 +37,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "KV GB/s (16-bit equiv) compress+decompress at ~20x CR"
+CODERS = {"deflate": 0, "rans": 1}
 UNIT = "GB/s"
 
 
@@ -426,7 +427,8 @@ def main():
     ap.add_argument("--config", default="llama8b", choices=sorted(DEFAULT_TOKENS))
     ap.add_argument("--tokens", type=int, default=None)               # default: per config (DEFAULT_TOKENS)
     ap.add_argument("--cr", type=float, default=16.0)
-    ap.add_argument("--chunk-bytes", type=int, default=65536)        # DEFLATE chunk (reading Q15)
+    ap.add_argument("--chunk-bytes", type=int, default=65536)        # entropy-coder chunk (reading Q15)
+    ap.add_argument("--coder", default="deflate", choices=["deflate", "rans"])   # lossless back-end (Q24)
     ap.add_argument("--cal-seqs", type=int, default=2)
     ap.add_argument("--cal-tokens", type=int, default=32768)
     ap.add_argument("--ncal", type=int, default=65000)
@@ -512,10 +514,10 @@ def main():
     kview, vview = K.KVView(Kc), K.KVView(Vc)
     Ko, Vo = torch.zeros_like(Kc), torch.zeros_like(Vc)
     koview, voview = K.KVView(Ko), K.KVView(Vo)
-    cap, wsb = K.compress_sizes(kb, kp, vb, vp, kview, chunk_bytes=args.chunk_bytes)
+    cap, wsb = K.compress_sizes(kb, kp, vb, vp, kview, chunk_bytes=args.chunk_bytes, coder=CODERS[args.coder])
     cont = torch.empty(cap, dtype=torch.uint8, device="cuda")
     cws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
-    cont_valid, st = K.compress(kb, kp, vb, vp, kview, vview, out=cont, workspace=cws, chunk_bytes=args.chunk_bytes)
+    cont_valid, st = K.compress(kb, kp, vb, vp, kview, vview, out=cont, workspace=cws, chunk_bytes=args.chunk_bytes, coder=CODERS[args.coder])
     info = K.container_info(cont_valid)
     hdr = cont[:256].cpu().numpy().tobytes()                  # the container header, read once (host copy)
     dws = torch.empty(K.decompress_workspace_bytes(kb, kp, vb, vp, hdr), dtype=torch.uint8, device="cuda")
@@ -532,7 +534,7 @@ def main():
         if mark:
             e = tuple(torch.cuda.Event(enable_timing=True) for _ in range(3))
             e[0].record(stream)
-        K.compress(kb, kp, vb, vp, kview, vview, out=cont, workspace=cws, sync_len=False, chunk_bytes=args.chunk_bytes)
+        K.compress(kb, kp, vb, vp, kview, vview, out=cont, workspace=cws, sync_len=False, chunk_bytes=args.chunk_bytes, coder=CODERS[args.coder])
         if mark:
             e[1].record(stream)
         K.decompress_async(kb, kp, vb, vp, cont, hdr, koview, voview, dstatus, workspace=dws)
@@ -596,7 +598,10 @@ def main():
     # GEMM as the *_overlapped stage, whose time is shared with it); one inflate
     # launch covers both streams; the keys' dequantisation runs on the caller's
     # stream, the values' beside the keys' GEMM (KVTC_DQ_FUSED=1: inside the GEMM)
-    stage_bytes = {"c.deflate": info.payload_bytes[0] + info.entropy_bytes[0],
+    stage_bytes = {"c.rans_keys": info.payload_bytes[0] + info.entropy_bytes[0],
+                   "c.rans_values_overlapped": info.payload_bytes[1] + info.entropy_bytes[1],
+                   "d.rans_decode": pay + ent,
+                   "c.deflate": info.payload_bytes[0] + info.entropy_bytes[0],
                    "c.deflate_overlapped": info.payload_bytes[1] + info.entropy_bytes[1],
                    "d.inflate": pay + ent,
                    "d.dequant": info.payload_bytes[0] + m * 2 * rpad[0],
@@ -693,7 +698,7 @@ def main():
                 if i >= 2:
                     stream.wait_event(ev_out[sl])
                 K.compress(kb, kp, vb, vp, in_views[sl][0], in_views[sl][1], out=cont, workspace=cws,
-                           chunk_bytes=args.chunk_bytes,
+                           chunk_bytes=args.chunk_bytes, coder=CODERS[args.coder],
                            sync_len=False)
                 K.decompress_async(kb, kp, vb, vp, cont, hdr, out_views[sl][0], out_views[sl][1], dstatus,
                                    workspace=dws)
@@ -750,7 +755,7 @@ def main():
                     if i >= 2:
                         stream.wait_event(ev_d[sl])          # container i-2 consumed from cbuf/cland
                     K.compress(kb, kp, vb, vp, kv_in, vv_in, out=cbuf[sl], workspace=cws, sync_len=False,
-                               chunk_bytes=args.chunk_bytes)
+                               chunk_bytes=args.chunk_bytes, coder=CODERS[args.coder])
                     ev_c[sl].record(stream)
                     with torch.cuda.stream(d2h):
                         d2h.wait_event(ev_c[sl])
@@ -816,6 +821,7 @@ def main():
                                            f"weak x{world} (one conversation per GPU; calibration all-reduced)"),
                            "l2": f"inputs {2 * 2 * p * t / 1e9:.1f} GB per step >> 126 MB L2 (no flush needed)",
                            "cr": cr, "cr_pre_deflate": cr_pre, "chunk_bytes": args.chunk_bytes,
+                           "coder": args.coder,
                            "r_eff": [kinfo.r_eff, vinfo.r_eff], "r_nz": rnz,
                            "setup_s": round(setup_s, 1), "setup": setup_info},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),

@@ -89,9 +89,14 @@ typedef struct {
 } kvtc_kv_view;
 
 /* Tokens kept raw: the first `sinks` (attention sinks, s = 4) and the last
- * `window` (w = 128).  chunk_bytes: DEFLATE chunk (Q15, 65536). */
+ * `window` (w = 128).  chunk_bytes: entropy-coder chunk (Q15, 65536).
+ * coder: the lossless back-end, KVTC_CODER_DEFLATE (default) or
+ * KVTC_CODER_RANS (the static-model rANS of reading Q24, SURVEY §8(f)4;
+ * single-conversation calls only). */
+typedef enum { KVTC_CODER_DEFLATE = 0, KVTC_CODER_RANS = 1 } kvtc_coder;
 typedef struct {
   int32_t sinks, window, chunk_bytes;
+  int32_t coder;
 } kvtc_policy;
 
 /* DP configuration.  Budget B = floor(feature_bits * p / target_cr)
@@ -380,6 +385,19 @@ kvtc_status kvtc_stage_inflate(const uint8_t *section, size_t len, uint8_t *out,
 kvtc_status kvtc_stage_inflate_raw(const uint8_t *in, const int64_t *in_off, const int64_t *in_len,
                                    int32_t nstreams, uint8_t *out, const int64_t *out_off,
                                    const int64_t *out_len, int32_t *status_dev, void *stream);
+/* Alternative lossless back-end (ANS is in the paper's ablation,
+ * P:L1305-1317): static-model interleaved rANS, one order-0 table per payload
+ * tile-offset class (reading Q24; oracle/rans.py).  tile_bytes: the
+ * payload's tile period (kvtc_payload_bytes of 128 tokens), 0 = none.  The
+ * section is written at out (16-byte aligned, >= kvtc_rans_bound bytes);
+ * *out_len_host receives its length (synchronising).  Decode returns
+ * KVTC_E_CORRUPT for a malformed section or stream. */
+size_t kvtc_rans_bound(size_t n, int32_t chunk_bytes, int64_t tile_bytes);
+size_t kvtc_rans_workspace_bytes(size_t n, int32_t chunk_bytes, int64_t tile_bytes);
+kvtc_status kvtc_stage_rans_encode(const uint8_t *in, size_t n, int32_t chunk_bytes, int64_t tile_bytes, uint8_t *out,
+                                   size_t out_cap, size_t *out_len_host, void *workspace, size_t workspace_bytes,
+                                   void *stream);
+kvtc_status kvtc_stage_rans_decode(const uint8_t *section, size_t len, uint8_t *out, size_t n_out, void *stream);
 /* Unpack + dequantise: payload -> D^ [m x ld] fp16 (ld >= ncols(plan), even);
  * D^ = fp16(code * scale + shift) rounded once (R5). */
 kvtc_status kvtc_stage_dequantize(const kvtc_plan *plan, const uint8_t *payload, int64_t m, uint16_t *Dh,

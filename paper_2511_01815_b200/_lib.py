@@ -19,6 +19,7 @@ KEYS, VALUES = 0, 1
 T_NONE, T_INT2, T_INT4, T_FP8 = 0, 1, 2, 3
 LAYOUT_CONTIGUOUS, LAYOUT_PAGED = 0, 1
 HEADER_BYTES = 256
+CODER_DEFLATE, CODER_RANS = 0, 1
 
 
 class KvtcError(RuntimeError):
@@ -42,7 +43,7 @@ class View(C.Structure):
 
 
 class Policy(C.Structure):
-    _fields_ = [("sinks", C.c_int32), ("window", C.c_int32), ("chunk_bytes", C.c_int32)]
+    _fields_ = [("sinks", C.c_int32), ("window", C.c_int32), ("chunk_bytes", C.c_int32), ("coder", C.c_int32)]
 
 
 class DPConfig(C.Structure):
@@ -111,6 +112,10 @@ _SIGS = {
     "kvtc_stage_reconstruct": (i32, [vp, vp, vp, i64, i64, i64, i32, i32, P(View), vp]),
     "kvtc_stage_reconstruct_payload": (i32, [vp, vp, vp, i64, i64, i32, i32, P(View), vp]),
     "kvtc_stage_project_partial": (i32, [vp, vp, vp, i64, i32, i32, i32, vp, vp]),
+    "kvtc_rans_bound": (C.c_size_t, [C.c_size_t, i32, i64]),
+    "kvtc_rans_workspace_bytes": (C.c_size_t, [C.c_size_t, i32, i64]),
+    "kvtc_stage_rans_encode": (i32, [vp, C.c_size_t, i32, i64, vp, C.c_size_t, P(C.c_size_t), vp, C.c_size_t, vp]),
+    "kvtc_stage_rans_decode": (i32, [vp, C.c_size_t, vp, C.c_size_t, vp]),
     "kvtc_profile_enable": (None, [i32]),
     "kvtc_profile_read": (i32, [C.c_char_p, sz, P(f64), P(i32), i32]),
     "kvtc_launch_count": (i64, []),

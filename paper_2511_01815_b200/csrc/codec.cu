@@ -13,6 +13,7 @@ namespace {
 constexpr uint32_t kContainerMagic = 0x4354564Bu;  // "KVTC"
 constexpr uint32_t kContainerVersion = 2;
 constexpr uint32_t kFlagNumeric = 1u;              // an fp16 shift / scale overflowed (Q4)
+constexpr uint32_t kFlagRans = 2u;                 // sections are rANS (Q24), not DEFLATE
 
 // DESIGN.md §4.  Integrity (integrity.cu): payload_hash = checksum of each
 // stream's payload before DEFLATE, raw_hash = of the raw sink / window section,
@@ -51,7 +52,7 @@ __global__ void header_kernel(ContainerHeader h, uint8_t *out, const uint64_t *l
     h.payload_hash[0] = w[5];
     h.payload_hash[1] = w[6];
   }
-  h.flags = (w[4] & 1) ? kFlagNumeric : 0u;
+  h.flags = (h.flags & kFlagRans) | ((w[4] & 1) ? kFlagNumeric : 0u);   // the coder flag comes from the host
   h.raw_hash = w[7];
   h.header_hash = hash_words(reinterpret_cast<const uint64_t *>(&h), 31, kSeedHeader);
   *reinterpret_cast<ContainerHeader *>(out) = h;
@@ -149,7 +150,14 @@ kvtc_status run_project_quant(const kvtc_basis *b, kvtc_plan *pl, const Operands
   a.status = status;
   a.wide = pl->d_wide;
   a.nwide = pl->nwide;
-  return launch_gemm_project_quant(a, st);
+  if ((s = launch_gemm_project_quant(a, st))) return s;
+  // KVTC_WIDE_DEFER=1 (A/B measurement only): the wide groups quantised by the
+  // separate SIMT pass over the fp32 scratch instead of the epilogue fixup
+  const char *wd = getenv("KVTC_WIDE_DEFER");
+  if (pl->nwide && wd && wd[0] == '1')
+    return launch_quant_wide(pl->d_wide, pl->nwide, wide, pl->wide_cols, 1, m, pl->tile_bytes, a.codes_off_last,
+                             payload, st, tiles, status);
+  return KVTC_OK;
 }
 
 // The inverse path's A operand.  Default: the SIMT kernel dequantises into D^
@@ -434,6 +442,59 @@ extern "C" kvtc_status kvtc_stage_inflate_raw(const uint8_t *in, const int64_t *
                             static_cast<cudaStream_t>(stream));
 }
 
+// rANS back-end stage entries (reading Q24).
+extern "C" size_t kvtc_rans_bound(size_t n, int32_t chunk_bytes, int64_t tile_bytes) {
+  return rans_section_bound(n, chunk_bytes, tile_bytes);
+}
+extern "C" size_t kvtc_rans_workspace_bytes(size_t n, int32_t chunk_bytes, int64_t tile_bytes) {
+  return rans_workspace(n, chunk_bytes, tile_bytes);
+}
+extern "C" kvtc_status kvtc_stage_rans_encode(const uint8_t *in, size_t n, int32_t chunk_bytes, int64_t tile_bytes,
+                                              uint8_t *out, size_t out_cap, size_t *out_len_host, void *workspace,
+                                              size_t workspace_bytes, void *stream) {
+  KVTC_CHECK_ARG(in && out && out_len_host, "rans_encode arguments");
+  KVTC_CHECK_ARG(chunk_bytes >= 1024 && chunk_bytes <= (1 << 20) && chunk_bytes % 32 == 0, "rans chunk_bytes");
+  KVTC_CHECK_ARG(out_cap >= rans_section_bound(n, chunk_bytes, tile_bytes), "rans output capacity");
+  KVTC_CHECK_ARG((reinterpret_cast<uintptr_t>(out) & 15) == 0, "rans output must be 16-byte aligned");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint64_t *len_dev = nullptr;
+  KVTC_CUDA_TRY(cudaMallocAsync(&len_dev, 8, st));
+  kvtc_status s = launch_rans_encode(in, n, chunk_bytes, tile_bytes, out, nullptr, len_dev, workspace,
+                                     workspace_bytes, st);
+  if (s) return s;
+  uint64_t len = 0;
+  KVTC_CUDA_TRY(cudaMemcpyAsync(&len, len_dev, 8, cudaMemcpyDeviceToHost, st));
+  KVTC_CUDA_TRY(cudaStreamSynchronize(st));
+  cudaFreeAsync(len_dev, st);
+  *out_len_host = size_t(len);
+  return KVTC_OK;
+}
+extern "C" kvtc_status kvtc_stage_rans_decode(const uint8_t *section, size_t len, uint8_t *out, size_t n_out,
+                                              void *stream) {
+  KVTC_CHECK_ARG(section && out && len >= kRansHeaderBytes, "rans_decode arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t hdr[kRansHeaderBytes];
+  KVTC_CUDA_TRY(cudaMemcpyAsync(hdr, section, sizeof(hdr), cudaMemcpyDeviceToHost, st));
+  KVTC_CUDA_TRY(cudaStreamSynchronize(st));
+  uint32_t nch = 0, ncls = 0;
+  kvtc_status s = check_rans_header(hdr, len, n_out, &nch, &ncls);
+  if (s) return s;
+  void *ws = nullptr;
+  KVTC_CUDA_TRY(cudaMallocAsync(&ws, rans_decode_workspace(ncls) + 16, st));
+  int32_t *err = reinterpret_cast<int32_t *>(static_cast<uint8_t *>(ws) + rans_decode_workspace(ncls));
+  KVTC_CUDA_TRY(cudaMemsetAsync(err, 0, 4, st));
+  if ((s = launch_rans_decode(section, len, n_out, nch, ncls, out, ws, err, st))) return s;
+  int32_t e = 0;
+  KVTC_CUDA_TRY(cudaMemcpyAsync(&e, err, 4, cudaMemcpyDeviceToHost, st));
+  KVTC_CUDA_TRY(cudaStreamSynchronize(st));
+  cudaFreeAsync(ws, st);
+  if (e) {
+    set_error("corrupt rANS section (%d)", e);
+    return KVTC_E_CORRUPT;
+  }
+  return KVTC_OK;
+}
+
 extern "C" kvtc_status kvtc_stage_dequantize(const kvtc_plan *plan, const uint8_t *payload, int64_t m, uint16_t *Dh,
                                              int64_t ld, void *stream) {
   KVTC_CHECK_ARG(plan && payload && Dh && ld >= plan->r_nz && m >= 0, "dequantize arguments");
@@ -511,12 +572,21 @@ CompressLayout compress_layout(const kvtc_plan *kp, const kvtc_plan *vp, const k
   L.raw_bytes = 2 * int64_t(k->shape.layers) * L.nraw * hd * 2;
   L.pay[0] = kvtc_payload_bytes(kp, L.m);
   L.pay[1] = kvtc_payload_bytes(vp, L.m);
-  for (int s = 0; s < 2; ++s) L.sec_bound[s] = deflate_section_bound(L.pay[s], pol->chunk_bytes);
+  for (int s = 0; s < 2; ++s)
+    L.sec_bound[s] = pol->coder == KVTC_CODER_RANS
+                         ? rans_section_bound(L.pay[s], pol->chunk_bytes, (s ? vp : kp)->tile_bytes)
+                         : deflate_section_bound(L.pay[s], pol->chunk_bytes);
   L.k_off = align16(KVTC_HEADER_BYTES + L.raw_bytes);
   L.bound = L.k_off + align16(L.sec_bound[0]) + align16(L.sec_bound[1]) + 64;
   return L;
 }
 }  // namespace
+
+// Entropy-coder workspace of one stream (the chosen back-end).
+size_t entropy_workspace(const kvtc_policy *pol, uint64_t n, const kvtc_plan *pl) {
+  return pol->coder == KVTC_CODER_RANS ? rans_workspace(n, pol->chunk_bytes, pl->tile_bytes)
+                                       : deflate_workspace(n, pol->chunk_bytes);
+}
 
 extern "C" size_t kvtc_compress_bound(const kvtc_plan *kp, const kvtc_plan *vp, const kvtc_kv_view *k,
                                       const kvtc_policy *pol) {
@@ -536,8 +606,8 @@ extern "C" size_t kvtc_compress_workspace_bytes(const kvtc_basis *kb, const kvtc
   b.take<float2>(L.m * (kb->shape.head_dim / 2));
   b.take<uint8_t>(L.pay[0] + 16);
   b.take<uint8_t>(L.pay[1] + 16);
-  b.take<uint8_t>(deflate_workspace(L.pay[0], pol->chunk_bytes));
-  b.take<uint8_t>(deflate_workspace(L.pay[1], pol->chunk_bytes));
+  b.take<uint8_t>(entropy_workspace(pol, L.pay[0], kp));
+  b.take<uint8_t>(entropy_workspace(pol, L.pay[1], vp));
   b.take<uint8_t>(wide_scratch_bytes(L.m, std::max(kp->wide_cols, vp->wide_cols), std::max(kp->nwide, vp->nwide)));
   return b.used + 256;
 }
@@ -555,6 +625,8 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
   KVTC_CHECK_ARG(kb->which == KVTC_KEYS && vb->which == KVTC_VALUES, "basis streams");
   KVTC_CHECK_ARG(pol->sinks >= 0 && pol->window >= 0, "policy");
   KVTC_CHECK_ARG(pol->chunk_bytes == 16384 || pol->chunk_bytes == 32768 || pol->chunk_bytes == 65536, "chunk_bytes");
+  KVTC_CHECK_ARG(pol->coder == KVTC_CODER_DEFLATE || pol->coder == KVTC_CODER_RANS, "policy coder");
+  const bool rans = pol->coder == KVTC_CODER_RANS;
   const CompressLayout L = compress_layout(kp, vp, k, pol);
   if (out_cap < L.bound) {
     set_error("output capacity %zu < bound %llu", out_cap, (unsigned long long)L.bound);
@@ -581,7 +653,7 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
   float2 *cs = ws.take<float2>(L.m * (kb->shape.head_dim / 2));
   uint8_t *payload_k = ws.take<uint8_t>(L.pay[0] + 16);
   uint8_t *payload_v = ws.take<uint8_t>(L.pay[1] + 16);
-  const size_t dws[2] = {deflate_workspace(L.pay[0], pol->chunk_bytes), deflate_workspace(L.pay[1], pol->chunk_bytes)};
+  const size_t dws[2] = {entropy_workspace(pol, L.pay[0], kp), entropy_workspace(pol, L.pay[1], vp)};
   void *dwsp[2];
   dwsp[0] = ws.take<uint8_t>(dws[0]);
   dwsp[1] = ws.take<uint8_t>(dws[1]);
@@ -601,6 +673,7 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
   h.sinks = pol->sinks;
   h.window = pol->window;
   h.chunk_bytes = pol->chunk_bytes;
+  h.flags = rans && L.m ? kFlagRans : 0u;
   h.tokens = k->tokens;
   h.pos0 = k->pos0;
   h.m = L.m;
@@ -681,10 +754,23 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
   // that encodes the last chunk range: the whole payload is complete there
   auto encode = [&](int sv, cudaStream_t q, int ctas, const char *tag, uint32_t c0 = 0,
                     uint32_t c1 = 0xFFFFFFFFu) -> kvtc_status {
-    ProfScope ps(tag, q);
+    // stage names: the rANS back-end encodes the values here (keys at the assembly point)
+    ProfScope ps(!rans ? tag : (sv == 0 ? "c.rans_hash_k" : (q == st ? "c.rans_values" : "c.rans_values_overlapped")), q);
     kvtc_status r;
     if (c1 == 0xFFFFFFFFu && (r = launch_hash(sv ? payload_v : payload_k, L.pay[sv], kSeedPayload, lens + 5 + sv, q, ctas)))
       return r;
+    if (rans) {
+      // rANS back-end (Q24): histogram, tables, encode and the section in one call.
+      // The values' section goes first (offset lens[3]); the keys' is encoded at the
+      // assembly point below, once its offset (lens[2]) is known.
+      if (sv == 0) return KVTC_OK;
+      if ((r = launch_rans_encode(payload_v, L.pay[1], pol->chunk_bytes, vpl->tile_bytes, o, lens + 3, lens + 1,
+                                  dwsp[1], dws[1], q)))
+        return r;
+      offset_after_kernel<<<1, 1, 0, q>>>(lens + 3, lens + 1, lens + 2, o);
+      KVTC_LAUNCH_CHECK();
+      return KVTC_OK;
+    }
     if ((r = launch_deflate_encode(sv ? payload_v : payload_k, L.pay[sv], pol->chunk_bytes, dwsp[sv], dws[sv], ctas,
                                    q, c0, c1)))
       return r;
@@ -723,7 +809,7 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
     const int64_t tiles = (L.m + kTileM - 1) / kTileM;
     const int64_t half = (tiles / 2) * kTileM;
     const uint32_t c_half = uint32_t(uint64_t(half / kTileM) * kpl->tile_bytes / uint64_t(pol->chunk_bytes));
-    const bool split = deflate_side && env_flag("KVTC_C_SPLIT", false) && half > 0 && c_half > 0;
+    const bool split = deflate_side && !rans && env_flag("KVTC_C_SPLIT", false) && half > 0 && c_half > 0;
     if (deflate_side) KVTC_CUDA_TRY(cudaStreamWaitEvent(aux, ss->ev[2], 0));
     if (split) {
       if ((s = gemm(0, false, 0, half))) return s;
@@ -758,8 +844,14 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
   KVTC_CUDA_TRY(cudaEventRecord(ss->ev[3], aux));
   KVTC_CUDA_TRY(cudaStreamWaitEvent(st, ss->ev[3], 0));          // join: both streams encoded
   {
-    ProfScope ps("c.assemble", st);
-    if ((s = launch_deflate_assemble(L.pay[0], pol->chunk_bytes, dwsp[0], o, lens + 2, lens + 0, st))) return s;
+    ProfScope ps(rans ? "c.rans_keys" : "c.assemble", st);
+    if (rans) {
+      if ((s = launch_rans_encode(payload_k, L.pay[0], pol->chunk_bytes, kpl->tile_bytes, o, lens + 2, lens + 0,
+                                  dwsp[0], dws[0], st)))
+        return s;
+    } else if ((s = launch_deflate_assemble(L.pay[0], pol->chunk_bytes, dwsp[0], o, lens + 2, lens + 0, st))) {
+      return s;
+    }
   }
   header_kernel<<<1, 1, 0, st>>>(h, o, lens, lens);
   KVTC_LAUNCH_CHECK();
@@ -810,7 +902,7 @@ kvtc_status validate_header(const ContainerHeader &h) {
         h.total_bytes != h.section_off[0] + h.entropy_bytes[0])
       return bad("section offsets / lengths");
   }
-  if (h.flags & ~kFlagNumeric) return bad("unknown flags");
+  if (h.flags & ~(kFlagNumeric | kFlagRans)) return bad("unknown flags");
   if (h.flags & kFlagNumeric) {
     set_error("container flagged at compression: a 16-bit shift/scale overflowed (Q4)");
     return KVTC_E_NUMERIC;
@@ -889,6 +981,7 @@ struct DecompWs {
   __half *Dh[2];
   float2 *cs;
   uint8_t *tail;         // fused path: the pre-pass columns (shared by K and V, one GEMM at a time)
+  uint8_t *rans_ws[2];   // rANS containers: the decoder tables of each stream
   int64_t ld;
 };
 DecompWs carve_decomp(const kvtc_plan *kp, const kvtc_plan *vp, const ContainerHeader &h, void *workspace,
@@ -908,6 +1001,9 @@ DecompWs carve_decomp(const kvtc_plan *kp, const kvtc_plan *vp, const ContainerH
   w.Dh[1] = ws.take<__half>(dh_rows * w.ld);
   w.cs = ws.take<float2>(h.m * (h.head_dim / 2));
   w.tail = ws.take<uint8_t>(dq_fused(kp, vp) ? dq_tail_bytes(h.m, std::max(kp->n_tail, vp->n_tail)) : 0);
+  const size_t rw = (h.flags & kFlagRans) ? rans_decode_workspace(kRansMaxClasses) : 0;
+  w.rans_ws[0] = ws.take<uint8_t>(rw);
+  w.rans_ws[1] = ws.take<uint8_t>(rw);
   return w;
 }
 
@@ -917,6 +1013,16 @@ DecompWs carve_decomp(const kvtc_plan *kp, const kvtc_plan *vp, const ContainerH
 kvtc_status enqueue_inflate(const uint8_t *ib, const ContainerHeader &h, const DecompWs &w, cudaStream_t st) {
   uint32_t nch[2];
   for (int sv = 0; sv < 2; ++sv) nch[sv] = uint32_t((h.payload_bytes[sv] + h.chunk_bytes - 1) / h.chunk_bytes);
+  if (h.flags & kFlagRans) {
+    // rANS sections (Q24): tables + decode per stream; a bad section sets w.err
+    ProfScope ps("d.rans_decode", st);
+    for (int sv = 0; sv < 2; ++sv) {
+      kvtc_status s = launch_rans_decode(ib + h.section_off[sv], h.entropy_bytes[sv], h.payload_bytes[sv], nch[sv],
+                                         kRansMaxClasses, w.payloads[sv], w.rans_ws[sv], w.err, st);
+      if (s) return s;
+    }
+    return KVTC_OK;
+  }
   ProfScope ps("d.inflate", st);
   return launch_inflate_sections(ib + h.section_off[0], h.entropy_bytes[0], h.payload_bytes[0], nch[0], w.payloads[0],
                                  ib + h.section_off[1], h.entropy_bytes[1], h.payload_bytes[1], nch[1], w.payloads[1],
@@ -1064,6 +1170,8 @@ extern "C" size_t kvtc_decompress_workspace_bytes(const kvtc_basis *kb, const kv
   b.take<__half>(dh_rows * std::max(std::max(kp->r_nz_pad, vp->r_nz_pad), 8));
   b.take<float2>(h.m * (kb->shape.head_dim / 2));
   b.take<uint8_t>(dq_fused(kp, vp) ? dq_tail_bytes(h.m, std::max(kp->n_tail, vp->n_tail)) : 0);
+  b.take<uint8_t>((h.flags & kFlagRans) ? rans_decode_workspace(kRansMaxClasses) : 0);
+  b.take<uint8_t>((h.flags & kFlagRans) ? rans_decode_workspace(kRansMaxClasses) : 0);
   return b.used + 256;
 }
 
@@ -1261,6 +1369,7 @@ extern "C" kvtc_status kvtc_compress_batch(const kvtc_basis *kb, const kvtc_plan
   KVTC_CHECK_ARG(kb->which == KVTC_KEYS && vb->which == KVTC_VALUES, "basis streams");
   KVTC_CHECK_ARG(pol->sinks >= 0 && pol->window >= 0, "policy");
   KVTC_CHECK_ARG(pol->chunk_bytes == 16384 || pol->chunk_bytes == 32768 || pol->chunk_bytes == 65536, "chunk_bytes");
+  KVTC_CHECK_ARG(pol->coder == KVTC_CODER_DEFLATE, "batched compression writes DEFLATE sections (coder 0)");
   kvtc_status s;
   std::vector<BatchItem> it(n);
   int64_t row = 0;
@@ -1563,6 +1672,10 @@ kvtc_status decompress_batch_core(const kvtc_basis *kb, const kvtc_plan *kp, con
       const std::string msg = kvtc_last_error();
       set_error("batch item %d: %s", i, msg.c_str());
       return s;
+    }
+    if (h.flags & kFlagRans) {
+      set_error("batch item %d: batched decompression reads DEFLATE containers (rANS: kvtc_decompress)", i);
+      return KVTC_E_INVALID;
     }
     KVTC_CHECK_ARG((reinterpret_cast<uintptr_t>(in_host[i]) & 15) == 0, "containers must be 16-byte aligned");
     if ((s = check_view(&k_out[i])) || (s = check_view(&v_out[i]))) return s;

@@ -114,6 +114,7 @@ struct Params {
   int32_t nwide, wpieces;
   float2 *wmm;
   int32_t *wcnt;
+  int32_t wide_defer;              // KVTC_WIDE_DEFER=1 (A/B only): no fixup, quant_wide_kernel afterwards
   // RECON with ASRC = 1: A = D^ dequantised from the payload
   const uint8_t *dq_payload;
   const int64_t *dq_off_full, *dq_off_last;
@@ -1116,7 +1117,7 @@ __global__ void __launch_bounds__(threads_for(ASRC), MODE == EPI_RECON ? 1 : 2)
         release_acc(acc);
         // wide groups: the last piece's CTA quantises the whole group (after the
         // accumulator is released, so the next tile's MMAs are not held up)
-        if (ntok > 0) {
+        if (ntok > 0 && !P.wide_defer) {
           int32_t *stw = tref ? tref->status : P.status;
 #pragma unroll
           for (int sb = 0; sb < NSUB; ++sb)
@@ -1378,6 +1379,8 @@ kvtc_status launch_gemm_project_quant(const GemmCompressArgs &a, cudaStream_t st
     p.wmm = reinterpret_cast<float2 *>(a.D + a.m * a.ldd);
     p.wcnt = reinterpret_cast<int32_t *>(p.wmm + a.m * p.wpieces);
     KVTC_CUDA_TRY(cudaMemsetAsync(p.wcnt, 0, size_t(ceil_div(a.m, kTileM)) * a.nwide * 4, st));
+    const char *wd = getenv("KVTC_WIDE_DEFER");
+    p.wide_defer = wd && wd[0] == '1';
   }
   // KVTC_QUANT_NSUB=2: two segments per tile (Cfg<true, 2>, 25 % less L2 traffic);
   // measured slower (tensor pipe 58 % vs 88 %: the 512-column epilogue is not

@@ -289,6 +289,21 @@ kvtc_status launch_inflate_raw(const uint8_t *in, const int64_t *in_off, const i
                                uint8_t *out, const int64_t *out_off, const int64_t *out_len, int32_t *status,
                                cudaStream_t st);
 
+// rans.cu: the static-model interleaved rANS back-end (reading Q24).  Encode
+// writes a section at out + (*off_dev) like launch_deflate; decode needs
+// rans_decode_workspace(nclasses) bytes of device scratch (the decoder tables).
+size_t rans_section_bound(size_t n, int32_t chunk, int64_t tile_bytes);
+size_t rans_workspace(size_t n, int32_t chunk, int64_t tile_bytes);
+kvtc_status launch_rans_encode(const uint8_t *in, size_t n, int32_t chunk, int64_t tile_bytes, uint8_t *out,
+                               const uint64_t *off_dev, uint64_t *section_len_dev, void *ws, size_t ws_bytes,
+                               cudaStream_t st);
+kvtc_status check_rans_header(const void *hdr_host, size_t len, size_t n_out, uint32_t *nchunks, uint32_t *nclasses);
+size_t rans_decode_workspace(uint32_t nclasses);
+kvtc_status launch_rans_decode(const uint8_t *sec, uint64_t len, uint64_t n_out, uint32_t nchunks, uint32_t nclasses,
+                               uint8_t *out, void *ws, int32_t *err, cudaStream_t st);
+constexpr size_t kRansHeaderBytes = 64;
+constexpr uint32_t kRansMaxClasses = 64;          // span_log2 is chosen so a tile has <= 64 classes
+
 // integrity.cu: 64-bit container checksums (see the file header).  launch_hash
 // ADDS the checksum of [p, p + n) (p 16-byte aligned) to *out (zero it first);
 // launch_hash_check ORs `bit` into *status when *got != expect.

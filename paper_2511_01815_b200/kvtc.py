@@ -207,6 +207,25 @@ def deflate(data: torch.Tensor, chunk_bytes: int = 65536, stream=None):
     return out[: ln.value]
 
 
+def rans_encode(data: torch.Tensor, tile_bytes: int = 0, chunk_bytes: int = 65536, stream=None):
+    """rANS back-end (reading Q24): payload bytes -> section (device uint8)."""
+    n = data.numel()
+    cap = int(lib().kvtc_rans_bound(n, chunk_bytes, tile_bytes))
+    out = torch.zeros(cap + 16, dtype=torch.uint8, device="cuda")
+    wsb = int(lib().kvtc_rans_workspace_bytes(n, chunk_bytes, tile_bytes))
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    ln = C.c_size_t()
+    check(lib().kvtc_stage_rans_encode(_ptr(data), n, chunk_bytes, tile_bytes, _ptr(out), cap + 16, C.byref(ln),
+                                       _ptr(ws), wsb, _stream(stream)))
+    return out[: ln.value]
+
+
+def rans_decode(section: torch.Tensor, n_out: int, stream=None):
+    out = torch.zeros(max(n_out, 1), dtype=torch.uint8, device="cuda")
+    check(lib().kvtc_stage_rans_decode(_ptr(section), section.numel(), _ptr(out), n_out, _stream(stream)))
+    return out[:n_out]
+
+
 def inflate(section: torch.Tensor, n_out: int, stream=None):
     out = torch.empty(n_out + 16, dtype=torch.uint8, device="cuda")
     sec = torch.zeros(section.numel() + 64, dtype=torch.uint8, device="cuda")
@@ -255,9 +274,9 @@ def reconstruct_payload(basis: Basis, plan: Plan, payload: torch.Tensor, m: int,
 # ------------------------------------------------------------------ codec
 def compress(kb: Basis, kp: Plan, vb: Basis, vp: Plan, k: KVView, v: KVView, sinks: int = 4, window: int = 128,
              chunk_bytes: int = 65536, stream=None, out: torch.Tensor | None = None, workspace=None,
-             sync_len: bool = True):
-    """Returns (container tensor [len], status)."""
-    pol = L.Policy(sinks, window, chunk_bytes)
+             sync_len: bool = True, coder: int = 0):
+    """Returns (container tensor [len], status).  coder: 0 DEFLATE, 1 rANS (Q24)."""
+    pol = L.Policy(sinks, window, chunk_bytes, coder)
     cap = int(lib().kvtc_compress_bound(kp.h, vp.h, C.byref(k.c), C.byref(pol)))
     wsb = int(lib().kvtc_compress_workspace_bytes(kb.h, kp.h, vb.h, vp.h, C.byref(k.c), C.byref(pol)))
     if out is None:
@@ -272,8 +291,8 @@ def compress(kb: Basis, kp: Plan, vb: Basis, vp: Plan, k: KVView, v: KVView, sin
     return (out[: ln.value] if sync_len else out), st
 
 
-def compress_sizes(kb, kp, vb, vp, k: KVView, sinks=4, window=128, chunk_bytes=65536):
-    pol = L.Policy(sinks, window, chunk_bytes)
+def compress_sizes(kb, kp, vb, vp, k: KVView, sinks=4, window=128, chunk_bytes=65536, coder: int = 0):
+    pol = L.Policy(sinks, window, chunk_bytes, coder)
     cap = int(lib().kvtc_compress_bound(kp.h, vp.h, C.byref(k.c), C.byref(pol)))
     wsb = int(lib().kvtc_compress_workspace_bytes(kb.h, kp.h, vb.h, vp.h, C.byref(k.c), C.byref(pol)))
     return cap, wsb
@@ -348,7 +367,7 @@ def compress_batch(kb: Basis, kp: Plan, vb: Basis, vp: Plan, ks: list, vs: list,
     """kvtc_compress_batch: one container per (ks[i], vs[i]); returns the list of
     containers (trimmed to their lengths when sync_len)."""
     n = len(ks)
-    pol = L.Policy(sinks, window, chunk_bytes)
+    pol = L.Policy(sinks, window, chunk_bytes, 0)
     karr, varr = _views(ks), _views(vs)
     if outs is None:
         outs = [torch.empty(int(lib().kvtc_compress_bound(kp.h, vp.h, C.byref(k.c), C.byref(pol))),
@@ -365,7 +384,7 @@ def compress_batch(kb: Basis, kp: Plan, vb: Basis, vp: Plan, ks: list, vs: list,
 
 
 def compress_batch_workspace_bytes(kb, kp, vb, vp, ks: list, sinks=4, window=128, chunk_bytes=65536) -> int:
-    pol = L.Policy(sinks, window, chunk_bytes)
+    pol = L.Policy(sinks, window, chunk_bytes, 0)
     return int(lib().kvtc_compress_batch_workspace_bytes(kb.h, kp.h, vb.h, vp.h, _views(ks), len(ks), C.byref(pol)))
 
 

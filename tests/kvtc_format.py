@@ -138,3 +138,44 @@ def _dynamic_header(stream: bytes):
         else:
             lens += [0] * (3 + get(3) if sym == 17 else 11 + get(7))
     return pos, lens
+
+
+RANS_HDR = struct.Struct("<IIQIIQIIQQ8x")
+RANS_CHUNK = np.dtype([("off", "<u8"), ("bytes", "<u4"), ("kind", "<u4")])
+
+
+def _pad16(x: int) -> int:
+    return (x + 15) & ~15
+
+
+def parse_rans_section(buf: bytes):
+    """rANS section (reading Q24): header, frequency tables, chunk table, streams."""
+    magic, ver, raw, chunk, nch, period, sl, ncls, data_off, total = RANS_HDR.unpack_from(buf, 0)
+    assert magic == 0x4154564B and ver == 1 and RANS_HDR.size == 64
+    freqs = np.frombuffer(buf, dtype="<u2", count=ncls * 256, offset=64).reshape(ncls, 256).astype(np.int64)
+    ctab_off = 64 + _pad16(ncls * 512)
+    tab = np.frombuffer(buf, dtype=RANS_CHUNK, count=nch, offset=ctab_off)
+    assert data_off == ctab_off + _pad16(16 * nch)
+    streams = [(int(e["kind"]), buf[data_off + int(e["off"]): data_off + int(e["off"]) + int(e["bytes"])]) for e in tab]
+    return dict(raw=raw, chunk=chunk, nchunks=nch, period=period, span_log2=sl, nclasses=ncls, data_off=data_off,
+                total=total, freqs=freqs, table=tab, streams=streams)
+
+
+def build_rans_section(freqs, sl: int, chunks, n: int, chunk: int, period: int) -> bytes:
+    """The inverse of parse_rans_section (byte layout only): lets the GPU decoder
+    read streams the oracle wrote."""
+    freqs = np.asarray(freqs, dtype=np.int64)
+    ncls = freqs.shape[0]
+    ctab_off = 64 + _pad16(ncls * 512)
+    data_off = ctab_off + _pad16(16 * len(chunks))
+    tab, data, off = [], b"", 0
+    for kind, st in chunks:
+        tab.append(struct.pack("<QII", off, len(st), kind))
+        data += st + b"\0" * (_pad16(len(st)) - len(st))
+        off += _pad16(len(st))
+    eff = max(1, min(period, n)) if period > 0 else max(1, n)          # the period the header records
+    hdr = RANS_HDR.pack(0x4154564B, 1, n, chunk, len(chunks), eff, sl, ncls, data_off, data_off + off)
+    body = freqs.astype("<u2").tobytes()
+    out = hdr + body + b"\0" * (ctab_off - 64 - len(body))
+    out += b"".join(tab) + b"\0" * (data_off - ctab_off - 16 * len(chunks))
+    return out + data

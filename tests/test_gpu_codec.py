@@ -306,3 +306,38 @@ def test_fused_dequant_decompress_matches(K, monkeypatch, name, tokens):
     got = [run(), run(spec.layers - 1), run(0, 1, True)]
     for (a, b), (c, d) in zip(ref, got):
         assert torch.equal(a, c) and torch.equal(b, d)
+
+
+@pytest.mark.parametrize("name,tokens", [("mid", 1000), ("toy", 400), ("mid", 132)])
+def test_rans_container_roundtrip(K, name, tokens):
+    """coder = rANS (reading Q24): the same payloads behind another
+    lossless back-end, so decompression is bit-identical to the DEFLATE
+    container's; the payload checksums still verify every decoded byte."""
+    spec, invf, kb, vb, KB, VB, KP, VP, okp, ovp = _setup(K, name)
+    Kc, Vc = E.caches(name, tokens, 3, conversation=12)
+    kd, vd = Kc.cuda(), Vc.cuda()
+    cd, _ = K.compress(KB, KP, VB, VP, K.KVView(kd, pos0=3), K.KVView(vd, pos0=3))
+    cr, _ = K.compress(KB, KP, VB, VP, K.KVView(kd, pos0=3), K.KVView(vd, pos0=3), coder=1)
+    outs = []
+    for c in (cd, cr):
+        ok, ov = torch.zeros_like(kd), torch.zeros_like(vd)
+        K.decompress(KB, KP, VB, VP, c, K.KVView(ok, pos0=3), K.KVView(ov, pos0=3))
+        torch.cuda.synchronize()
+        outs.append((ok, ov))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    ii, ir = K.container_info(cd), K.container_info(cr)
+    assert ii.payload_bytes[0] == ir.payload_bytes[0] and ii.payload_bytes[1] == ir.payload_bytes[1]
+    print(f"\n[rans] {name} t={tokens}: sections deflate={ii.entropy_bytes[0] + ii.entropy_bytes[1]} "
+          f"rans={ir.entropy_bytes[0] + ir.entropy_bytes[1]} payload={ii.payload_bytes[0] + ii.payload_bytes[1]}")
+    # a damaged rANS section is reported
+    if tokens > 132:
+        from tests.kvtc_format import parse_container
+        hc = parse_container(cr.cpu().numpy().tobytes())
+        assert hc["flags"] & 2                                    # the rANS flag
+        bad = cr.clone()
+        bad[int(hc["sec_k"]) + int(hc["ent_k"]) // 2] ^= 0x41
+        ok, ov = torch.zeros_like(kd), torch.zeros_like(vd)
+        from paper_2511_01815_b200 import _lib as L
+        with pytest.raises(L.KvtcError) as e:
+            K.decompress(KB, KP, VB, VP, bad, K.KVView(ok, pos0=3), K.KVView(ov, pos0=3))
+        assert e.value.status == -3
