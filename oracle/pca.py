@@ -135,6 +135,16 @@ def project(basis: Basis, X, cols=None) -> np.ndarray:
     return X @ Vc - (basis.mu @ Vc)[None, :]
 
 
+def project_partial(basis: Basis, Xg, f0: int, f1: int, add_bias: bool, cols=None) -> np.ndarray:
+    """Joint cross-shard compression (reading Q23): one shard's part of
+    the projection, D_g = X_g V_c[f0:f1] (- mu V_c when add_bias), fp64.  The
+    shards' parts sum to project() of the joint features (block identity; pinned in
+    tests/test_oracle_pca_codec.py)."""
+    Vc = basis.Vc if cols is None else basis.Vc[:, cols]
+    D = np.asarray(Xg, dtype=np.float64) @ Vc[f0:f1]
+    return D - (basis.mu @ Vc)[None, :] if add_bias else D
+
+
 def reconstruct(basis: Basis, Dh, cols=None) -> np.ndarray:
     """X^ = D^ V_d^T + mu in fp64 (P:L232-234, R6)."""
     Vd = basis.Vd if cols is None else basis.Vd[:, cols]

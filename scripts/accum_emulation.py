@@ -41,7 +41,7 @@ def codes_of(D, groups):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--tokens", type=int, default=48)
+    ap.add_argument("--tokens", type=int, default=128)
     args = ap.parse_args()
     import bench
     import zlib
@@ -105,11 +105,31 @@ def main():
         while len(w) > 1:
             w = [f32(w[i] + w[i + 1]) if i + 1 < len(w) else w[i] for i in range(0, len(w), 2)]
         emu["tree"] = f32(w[0] - bias[None, :])
+        # measured on the GPU: the K = p projection as 1 / 2 / 4 tcgen05 GEMMs over
+        # feature ranges (kvtc_stage_project_partial), the partials added in fp32 (RNE),
+        # quantised by the library's SIMT quantiser: does a shorter tensor-core
+        # accumulation chain reduce the boundary flips?
+        import torch
+        Xg = torch.from_numpy(X).to(torch.bfloat16).cuda()
+        p_ = X.shape[1]
+        gpu_split = {}
+        for nsp in (1, 2, 4):
+            step = p_ // nsp
+            Dg = None
+            for q in range(nsp):
+                Pq = K.project_partial(B, P, Xg[:, q * step:(q + 1) * step].contiguous(), q * step, (q + 1) * step, q == 0)
+                Dg = Pq if Dg is None else Dg + Pq
+            pay = K.quantize_pack(P, Dg.contiguous()).cpu().numpy().tobytes()
+            _, _, cdq = OL.unpack(groups, pay, len(taus))
+            gpu_split["gpu_split%d" % nsp] = [(t, np.array(cdq[g])) for g, (_, _, t) in enumerate(groups)]
         ref = codes_of(D_ref, groups)
         out = {}
-        for name, D in [("gpu", None)] + list(emu.items()):
+        for name, D in [("gpu", None)] + list(gpu_split.items()) + list(emu.items()):
             per = {}
-            cds = codes_of(D, groups) if D is not None else [(t, np.array(gpu[g])) for g, (_, _, t) in enumerate(groups)]
+            if isinstance(D, list):
+                cds = D
+            else:
+                cds = codes_of(D, groups) if D is not None else [(t, np.array(gpu[g])) for g, (_, _, t) in enumerate(groups)]
             for (t, a), (_, b) in zip(ref, cds):
                 x, y = per.get(t, (0, 0))
                 per[t] = (x + int((a != b).sum()), y + a.size)

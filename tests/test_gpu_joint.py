@@ -53,18 +53,23 @@ def test_joint_partials_vs_oracle(K, tokens, pos0):
         ncols = sum(z for (_, z, _) in groups)
         Dfull = K.project(B, Pl, Xfull, ncols)
         Psum = torch.zeros_like(Dfull)
+        cols = np.concatenate([np.arange(s0, s0 + z) for (s0, z, _) in groups])
+        Xn_full = _bf16_np(Xfull)
         for g in range(spec.layers):
             sh = JointShard(K, B, Pl, g, g + 1)
             view_g = K.KVView(cache_d[g:g + 1].contiguous(), pos0=pos0)
-            Psum += sh.partial(view_g, 4, m, unrope, invf.astype(np.float32), 0, add_bias=(g == 0))
+            Pg = sh.partial(view_g, 4, m, unrope, invf.astype(np.float32), 0, add_bias=(g == 0))
+            # each shard's partial vs the oracle's (fp64) partial of the same rows
+            ref_g = OPCA.project_partial(ob, Xn_full[:, g * hd:(g + 1) * hd], g * hd, (g + 1) * hd, g == 0, cols)
+            assert np.abs(Pg.cpu().numpy() - ref_g).max() <= 2e-5 * np.abs(ref_g).max()
+            Psum += Pg
         torch.cuda.synchronize()
         scale = float(Dfull.abs().max())
         assert float((Psum - Dfull).abs().max()) <= 2e-5 * scale          # fp32 sums in another order
         # codes of the summed partials vs the oracle's fp64 projection of the joint features
         payload = K.quantize_pack(Pl, Psum.contiguous())
         pb = payload.cpu().numpy().tobytes()
-        cols = np.concatenate([np.arange(s0, s0 + z) for (s0, z, _) in groups])
-        Xn = _bf16_np(Xfull)
+        Xn = Xn_full
         D_ref = OPCA.project(ob, Xn, cols)
         E.assert_codes_parity(pb, groups, D_ref, m, Xn, ob, cols, f"joint stream={which}")
         # decompression by shard: each shard rebuilds its own layer from the gathered D^

@@ -182,3 +182,22 @@ def test_fit_svd_equals_fit():
     np.testing.assert_allclose(b.sigma, a.sigma, rtol=1e-10)
     np.testing.assert_array_equal(a.mu, b.mu)
     np.testing.assert_allclose(b.V, a.V, atol=2e-6)       # both fp32 masters
+
+
+def test_project_partial_block_identity():
+    """Q23: the shards' partial projections sum to the projection of the joint
+    features, D = sum_g X_g V_g - mu V (the block-matrix identity), checked against
+    the joint project() for an uneven split into three layer shards."""
+    rng = np.random.default_rng(23)
+    n, p, r = 50, 96, 10
+    X = rng.standard_normal((n, p))
+    C = rng.standard_normal((200, p)) @ rng.standard_normal((p, p)) * 0.1
+    b = PCA.fit(C, r)
+    cols = np.arange(0, r, 2)
+    splits = [(0, 32), (32, 40), (40, 96)]
+    parts = [PCA.project_partial(b, X[:, f0:f1], f0, f1, k == 0, cols) for k, (f0, f1) in enumerate(splits)]
+    np.testing.assert_allclose(sum(parts), PCA.project(b, X, cols), rtol=1e-12, atol=1e-12)
+    # the mean enters once: without any bias the sum is X V, not (X - mu) V
+    no_bias = sum(PCA.project_partial(b, X[:, f0:f1], f0, f1, False, cols) for (f0, f1) in splits)
+    np.testing.assert_allclose(no_bias - PCA.project(b, X, cols), np.tile(b.mu @ b.Vc[:, cols], (n, 1)),
+                               rtol=1e-12, atol=1e-12)
