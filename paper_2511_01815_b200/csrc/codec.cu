@@ -1101,7 +1101,18 @@ kvtc_status decompress_enqueue(const kvtc_basis *kb, const kvtc_plan *kp, const 
   SideStream *ss = side_stream();
   const bool ovl = !overlap_off();
   cudaStream_t aux = ovl ? ss->s : st;
-  if ((s = enqueue_inflate(ib, h, w, st))) return s;
+  // KVTC_D_INFLATE_SIDE=1 (A/B): only the keys' section is inflated up front; the
+  // values' is inflated on the side stream (bounded grid) beside the keys' GEMM
+  const bool inflate_side = ovl && !(h.flags & kFlagRans) && env_flag("KVTC_D_INFLATE_SIDE", false);
+  if (inflate_side) {
+    ProfScope ps("d.inflate_k", st);
+    const uint32_t nk = uint32_t((h.payload_bytes[0] + h.chunk_bytes - 1) / h.chunk_bytes);
+    if ((s = launch_inflate_section(ib + h.section_off[0], h.entropy_bytes[0], h.payload_bytes[0], nk,
+                                    w.payloads[0], w.err, st)))
+      return s;
+  } else if ((s = enqueue_inflate(ib, h, w, st))) {
+    return s;
+  }
   const bool fused = dq_fused(kp, vp);
   auto expand = [&](int sv, cudaStream_t q, int ctas) -> kvtc_status {
     if (fused) return KVTC_OK;                    // dequantised inside the reconstruction GEMM
@@ -1133,6 +1144,13 @@ kvtc_status decompress_enqueue(const kvtc_basis *kb, const kvtc_plan *kp, const 
     if (sv == 0) {
       KVTC_CUDA_TRY(cudaStreamWaitEvent(aux, ss->ev[2], 0));
       const int ctas = ovl ? corun_ctas(corun_per_sm("KVTC_CORUN_DEQUANT", 2)) : 0;
+      if (inflate_side) {
+        ProfScope ps("d.inflate_v_overlapped", aux);
+        const uint32_t nv = uint32_t((h.payload_bytes[1] + h.chunk_bytes - 1) / h.chunk_bytes);
+        if ((s = launch_inflate_section(ib + h.section_off[1], h.entropy_bytes[1], h.payload_bytes[1], nv,
+                                        w.payloads[1], w.err, aux, corun_ctas(corun_per_sm("KVTC_CORUN_INFLATE", 4)))))
+          return s;
+      }
       if ((s = expand(1, aux, ctas))) return s;
       {
         ProfScope ps(ovl ? "d.checksum_overlapped" : "d.checksum", aux);
