@@ -417,14 +417,16 @@ __device__ __forceinline__ void build_header(EncShared &S, const int t) {
     S.u.mk.par[i] = i == n_int - 1 ? i : S.u.mk.work[i];
   }
   __syncthreads();
-  for (int round = 0; round < 9; ++round) {       // depth <= 256 < 2^9
+  for (int round = 0; round < 9; ++round) {       // depth <= 256 < 2^9; stops once every node points at the root
     int nd[2], np[2];
+    int open = 0;
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
       const int i = t + k * kEncThreads;
       if (i < n_int) {
         nd[k] = S.u.mk.dep[i] + S.u.mk.dep[S.u.mk.par[i]];
         np[k] = S.u.mk.par[S.u.mk.par[i]];
+        open |= np[k] != n_int - 1;
       }
     }
     __syncthreads();
@@ -436,7 +438,7 @@ __device__ __forceinline__ void build_header(EncShared &S, const int t) {
         S.u.mk.par[i] = np[k];
       }
     }
-    __syncthreads();
+    if (!__syncthreads_or(open)) break;
   }
   for (int i = t; i < n_int; i += kEncThreads) atomicAdd(&S.u.mk.ndep[S.u.mk.dep[i]], 1);
   __syncthreads();

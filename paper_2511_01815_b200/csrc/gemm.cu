@@ -502,6 +502,25 @@ __global__ void __launch_bounds__(256) dq_tail_kernel(const DqCol *cols, const i
   }
 }
 
+// Codes of 32 coefficients of one wide-group row into B 32-bit words.
+template <int B>
+__device__ __forceinline__ void wide_pack32(int type, const float4 (&v)[8], float shift, float scale, uint8_t *dst,
+                                            bool last) {
+  constexpr int PW = 32 / B;
+#pragma unroll
+  for (int w = 0; w < B; ++w) {
+    uint32_t word = 0;
+#pragma unroll
+    for (int j = 0; j < PW; ++j) {
+      const int i = w * PW + j;
+      const float4 q = v[i >> 2];
+      const float f = (i & 3) == 0 ? q.x : (i & 3) == 1 ? q.y : (i & 3) == 2 ? q.z : q.w;
+      word |= encode_one(type, f, shift, scale) << (j * B);
+    }
+    store_u32_any(dst + 4 * w, word, !last);
+  }
+}
+
 // Wide group (k 256-column pieces, P:L256 allows groups up to 1024): called by
 // all 128 epilogue threads of a CTA after they stored their piece's fp32
 // coefficients and row min/max.  The CTA whose piece arrives last for this
@@ -532,20 +551,17 @@ __device__ __noinline__ void wide_fixup(const Params &P, int w, int mb, int row,
   if (stw && factor_overflow(sh, sc)) atomicOr(stw, 1);
   const float shift = f16_val(sh), scale = f16_val(sc);
   const int b = bits_of(wd.type);
-  const int per_word = 32 / b;
-  const int words = wd.size * b / 32;
   uint8_t *dst = tile_base + (last ? codes_off_last[wd.gidx] : wd.codes_off) + int64_t(row) * (wd.size * b / 8);
   const float *x = P.D + tok * P.ldd + wd.wcol;
-  for (int wi = 0; wi < words; ++wi) {
-    uint32_t word = 0;
-    for (int j = 0; j < per_word; j += 4) {
-      const float4 v = __ldcg(reinterpret_cast<const float4 *>(x + wi * per_word + j));
-      word |= encode_one(wd.type, v.x, shift, scale) << (j * b);
-      word |= encode_one(wd.type, v.y, shift, scale) << ((j + 1) * b);
-      word |= encode_one(wd.type, v.z, shift, scale) << ((j + 2) * b);
-      word |= encode_one(wd.type, v.w, shift, scale) << ((j + 3) * b);
-    }
-    store_u32_any(dst + 4 * wi, word, !last);
+  // 32 coefficients (b words) per step, their 8 loads issued together: the
+  // pieces were stored tiles ago and come back from L2 / DRAM
+  for (int c0 = 0; c0 < wd.size; c0 += 32) {
+    float4 v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = __ldcg(reinterpret_cast<const float4 *>(x + c0) + j);
+    if (b == 8) wide_pack32<8>(wd.type, v, shift, scale, dst + c0, last);
+    else if (b == 4) wide_pack32<4>(wd.type, v, shift, scale, dst + c0 / 2, last);
+    else wide_pack32<2>(wd.type, v, shift, scale, dst + c0 / 4, last);
   }
 }
 
