@@ -398,8 +398,10 @@ kvtc_status kvtc_stage_rans_encode(const uint8_t *in, size_t n, int32_t chunk_by
                                    size_t out_cap, size_t *out_len_host, void *workspace, size_t workspace_bytes,
                                    void *stream);
 kvtc_status kvtc_stage_rans_decode(const uint8_t *section, size_t len, uint8_t *out, size_t n_out, void *stream);
-/* Unpack + dequantise: payload -> D^ [m x ld] fp16 (ld >= ncols(plan), even);
- * D^ = fp16(code * scale + shift) rounded once (R5). */
+/* Unpack + dequantise: payload -> D^ [m x ld] fp16 (ld a multiple of 8 and >=
+ * ncols(plan) rounded up to 8, Dh 16-byte aligned, else KVTC_E_INVALID);
+ * D^ = fp16(code * scale + shift) rounded once (R5).  Columns from
+ * ncols to the next multiple of 8 are written as 0. */
 kvtc_status kvtc_stage_dequantize(const kvtc_plan *plan, const uint8_t *payload, int64_t m, uint16_t *Dh,
                                   int64_t ld, void *stream);
 /* K5: X^ = D^ V_d^T + mu for layers [layer_begin, layer_end), keys re-rotated

@@ -499,7 +499,7 @@ extern "C" kvtc_status kvtc_stage_dequantize(const kvtc_plan *plan, const uint8_
                                              int64_t ld, void *stream) {
   KVTC_CHECK_ARG(plan && payload && Dh && ld >= plan->r_nz && m >= 0, "dequantize arguments");
   auto *pl = const_cast<kvtc_plan *>(plan);
-  return launch_dequant(pl->d_pgroups, pl->d_codes_off_full, pl->G, plan_codes_off_last(pl, m % kTileM),
+  return launch_dequant(pl->d_dqchunks, pl->d_dqcols, pl->r_nz, pl->d_codes_off_full, plan_codes_off_last(pl, m % kTileM),
                         pl->tile_bytes, payload, m, reinterpret_cast<__half *>(Dh), ld,
                         static_cast<cudaStream_t>(stream));
 }
@@ -1119,7 +1119,7 @@ kvtc_status decompress_enqueue(const kvtc_basis *kb, const kvtc_plan *kp, const 
     kvtc_plan *pl = const_cast<kvtc_plan *>(sv ? vp : kp);
     kvtc_status r;
     ProfScope ps(sv && ovl ? "d.dequant_overlapped" : "d.dequant", q);
-    if ((r = launch_dequant(pl->d_pgroups, pl->d_codes_off_full, pl->G, plan_codes_off_last(pl, h.m % kTileM),
+    if ((r = launch_dequant(pl->d_dqchunks, pl->d_dqcols, pl->r_nz, pl->d_codes_off_full, plan_codes_off_last(pl, h.m % kTileM),
                             pl->tile_bytes, w.payloads[sv], h.m, w.Dh[sv], w.ld, q, ctas)))
       return r;
     if (pl->r_nz == 0) KVTC_CUDA_TRY(cudaMemsetAsync(w.Dh[sv], 0, h.m * w.ld * 2, q));
@@ -1261,7 +1261,7 @@ extern "C" kvtc_status kvtc_decompress_begin(const kvtc_basis *kb, const kvtc_pl
     ProfScope ps("d.dequant", st);
     for (int sv = 0; sv < 2 && !dq_fused(kp, vp); ++sv) {
       kvtc_plan *pl = const_cast<kvtc_plan *>(sv ? vp : kp);
-      if ((s = launch_dequant(pl->d_pgroups, pl->d_codes_off_full, pl->G, plan_codes_off_last(pl, h.m % kTileM),
+      if ((s = launch_dequant(pl->d_dqchunks, pl->d_dqcols, pl->r_nz, pl->d_codes_off_full, plan_codes_off_last(pl, h.m % kTileM),
                               pl->tile_bytes, w.payloads[sv], h.m, w.Dh[sv], w.ld, st)))
         return s;
       if (pl->r_nz == 0) KVTC_CUDA_TRY(cudaMemsetAsync(w.Dh[sv], 0, h.m * w.ld * 2, st));
@@ -1829,7 +1829,7 @@ kvtc_status decompress_batch_core(const kvtc_basis *kb, const kvtc_plan *kp, con
       const ContainerHeader &h = hdr[i];
       if (!h.m) continue;
       __half *D = (sv ? Dh_v : Dh) + it[i].row0 * ld;
-      kvtc_status r = launch_dequant(pl->d_pgroups, pl->d_codes_off_full, pl->G, plan_codes_off_last(pl, h.m % kTileM),
+      kvtc_status r = launch_dequant(pl->d_dqchunks, pl->d_dqcols, pl->r_nz, pl->d_codes_off_full, plan_codes_off_last(pl, h.m % kTileM),
                                      pl->tile_bytes, sv ? pay_v[i] : pay_k[i], h.m, D, ld, q, ctas);
       if (r) return r;
       if (pl->r_nz == 0) KVTC_CUDA_TRY(cudaMemsetAsync(D, 0, h.m * ld * 2, q));

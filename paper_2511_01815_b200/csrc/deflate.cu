@@ -40,7 +40,13 @@ constexpr int kEncThreads = 128;  // two threads per index segment; ~14 chunks r
 constexpr int kNSeg = 64;
 constexpr uint32_t kSectionVersion = 3;
 constexpr int kLitSyms = 257;                    // 0..255 literals + 256 end-of-block
-constexpr int kMaxBits = 15;
+constexpr int kMaxBits = 15;                     // RFC 1951 limit
+// Code-length limit the encoder builds (runtime, <= kMaxBits).  A chunk whose
+// codes all fit the inflater's 11-bit first-level table decodes without the
+// subtable branch; KVTC_DEFLATE_MAXBITS=11 forces that for every chunk (A/B:
+// inflate -15 % cycles, CR 19.08 -> 18.99 on the bench workload, so the default
+// stays at the RFC limit).  Any limit >= 9 (257 symbols) is valid.
+constexpr int kDefaultMaxBits = 15;
 
 __host__ __device__ inline uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 __host__ __device__ inline uint32_t umin32(uint32_t a, uint32_t b) { return a < b ? a : b; }
@@ -397,7 +403,7 @@ __device__ __forceinline__ void hdr_put(uint32_t *hdr, uint32_t pos, uint32_t v,
 // codes (ranks by block scan), the run-length coding of the code lengths and the
 // header bits (scanned offsets, atomicOr) are parallel.  Bit-identical to the
 // former single-thread construction.
-__device__ __forceinline__ void build_header(EncShared &S, const int t) {
+__device__ __forceinline__ void build_header(EncShared &S, const int t, const int maxbits) {
   const int nz = S.nz;
   for (int s = t; s < kLitSyms + 3; s += kEncThreads) S.len[s] = 0;
   for (int j = t; j < nz; j += kEncThreads) S.u.mk.work[j] = int(S.hist[S.sorted[j]]);
@@ -455,16 +461,16 @@ __device__ __forceinline__ void build_header(EncShared &S, const int t) {
       }
     }
     // enforce the maximum length while keeping the Kraft sum exactly 1
-    for (int i = kMaxBits + 1; i <= 32; i++) {
-      num[kMaxBits] += num[i];
+    for (int i = maxbits + 1; i <= 32; i++) {
+      num[maxbits] += num[i];
       num[i] = 0;
     }
     if (nz > 1) {
       uint32_t total = 0;
-      for (int i = kMaxBits; i > 0; i--) total += uint32_t(num[i]) << (kMaxBits - i);
-      while (total != (1u << kMaxBits)) {
-        num[kMaxBits]--;
-        for (int i = kMaxBits - 1; i > 0; i--)
+      for (int i = maxbits; i > 0; i--) total += uint32_t(num[i]) << (maxbits - i);
+      while (total != (1u << maxbits)) {
+        num[maxbits]--;
+        for (int i = maxbits - 1; i > 0; i--)
           if (num[i]) {
             num[i]--;
             num[i + 1] += 2;
@@ -475,7 +481,7 @@ __device__ __forceinline__ void build_header(EncShared &S, const int t) {
     }
     int code = 0;
     S.next_code[0] = 0;
-    for (int b = 1; b <= kMaxBits; ++b) {
+    for (int b = 1; b <= maxbits; ++b) {
       code = (code + (b > 1 ? num[b - 1] : 0)) << 1;
       S.next_code[b] = code;
     }
@@ -486,7 +492,7 @@ __device__ __forceinline__ void build_header(EncShared &S, const int t) {
   for (int j = t; j < nz; j += kEncThreads) {
     const int r = nz - 1 - j;
     int l = 1, c = S.num[1];
-    while (r >= c && l < kMaxBits) c += S.num[++l];
+    while (r >= c && l < maxbits) c += S.num[++l];
     S.len[S.sorted[j]] = uint8_t(l);
   }
   __syncthreads();
@@ -617,7 +623,7 @@ __device__ __forceinline__ void build_header(EncShared &S, const int t) {
 
 __device__ __forceinline__ void encode_chunk(EncShared &S, const int c, const uint8_t *in, uint64_t n, int32_t chunk,
                                              uint8_t *slots, uint64_t stride, uint32_t *chunk_bytes,
-                                             uint32_t *chunk_kind, uint16_t *index) {
+                                             uint32_t *chunk_kind, uint16_t *index, const int maxbits) {
   const uint64_t base = uint64_t(c) * chunk;
   const uint32_t nc = uint32_t(umin64(chunk, n - base));
   const uint8_t *src = in + base;
@@ -674,7 +680,7 @@ __device__ __forceinline__ void encode_chunk(EncShared &S, const int c, const ui
   __syncthreads();
   for (int j = t; j < S.nz; j += kEncThreads) S.sorted[j] = int(S.u.skeys[kLitSyms - S.nz + j] & 511u);
   __syncthreads();
-  build_header(S, t);
+  build_header(S, t, maxbits);
   for (int i = t; i < 256; i += kEncThreads) S.sym[i] = uint32_t(S.rev[i]) | (uint32_t(S.len[i]) << 16);
   __syncthreads();
   // ---- bit counts per piece, exclusive scan
@@ -799,10 +805,11 @@ __device__ __forceinline__ void encode_chunk(EncShared &S, const int c, const ui
 __global__ void __launch_bounds__(kEncThreads, 14) deflate_encode_kernel(const uint8_t *in, uint64_t n, int32_t chunk,
                                                                         uint32_t c_begin, uint32_t c_end, uint8_t *slots,
                                                                         uint64_t stride, uint32_t *chunk_bytes,
-                                                                        uint32_t *chunk_kind, uint16_t *index) {
+                                                                        uint32_t *chunk_kind, uint16_t *index,
+                                                                        int maxbits) {
   __shared__ EncShared S;
   for (uint32_t c = c_begin + blockIdx.x; c < c_end; c += gridDim.x) {
-    encode_chunk(S, int(c), in, n, chunk, slots, stride, chunk_bytes, chunk_kind, index);
+    encode_chunk(S, int(c), in, n, chunk, slots, stride, chunk_bytes, chunk_kind, index, maxbits);
     __syncthreads();
   }
 }
@@ -912,6 +919,16 @@ int corun_ctas(int per_sm) {
   return sms * per_sm;
 }
 
+// Code-length limit of the encoder (kDefaultMaxBits; KVTC_DEFLATE_MAXBITS in [9, 15] for A/B runs).
+static int deflate_max_bits() {
+  static const int v = [] {
+    const char *e = getenv("KVTC_DEFLATE_MAXBITS");
+    const int b = e ? atoi(e) : kDefaultMaxBits;
+    return b < 9 ? 9 : (b > kMaxBits ? kMaxBits : b);
+  }();
+  return v;
+}
+
 kvtc_status launch_deflate_encode(const uint8_t *in, size_t n, int32_t chunk, void *ws, size_t ws_bytes,
                                   int32_t max_ctas, cudaStream_t st, uint32_t c_begin, uint32_t c_end) {
   KVTC_CHECK_ARG(chunk == 16384 || chunk == 32768 || chunk == 65536, "chunk_bytes must be 16/32/64 KiB");
@@ -923,14 +940,15 @@ kvtc_status launch_deflate_encode(const uint8_t *in, size_t n, int32_t chunk, vo
   const uint32_t grid = max_ctas > 0 ? std::min<uint32_t>(nc, uint32_t(max_ctas)) : nc;
   KVTC_MAX_CARVEOUT(deflate_encode_kernel);
   deflate_encode_kernel<<<grid, kEncThreads, 0, st>>>(in, n, chunk, c_begin, c_end, w.slots, w.stride, w.cbytes,
-                                                      w.ckind, w.index);
+                                                      w.ckind, w.index, deflate_max_bits());
   KVTC_LAUNCH_CHECK();
   return KVTC_OK;
 }
 
 // Batched codec: the chunks of many payloads in one launch (jobs[j].chunk0 ascending).
 __global__ void __launch_bounds__(kEncThreads, 14) deflate_encode_batch_kernel(const EncodeJob *jobs, int32_t njobs,
-                                                                              uint32_t total, int32_t chunk) {
+                                                                              uint32_t total, int32_t chunk,
+                                                                              int maxbits) {
   __shared__ EncShared S;
   const uint64_t stride = slot_stride(chunk);
   for (uint32_t b = blockIdx.x; b < total; b += gridDim.x) {
@@ -942,7 +960,7 @@ __global__ void __launch_bounds__(kEncThreads, 14) deflate_encode_batch_kernel(c
     }
     const EncodeJob jb = jobs[lo];
     const DeflateWs w = deflate_ws(jb.n, chunk, jb.ws);
-    encode_chunk(S, int(b - jb.chunk0), jb.in, jb.n, chunk, w.slots, stride, w.cbytes, w.ckind, w.index);
+    encode_chunk(S, int(b - jb.chunk0), jb.in, jb.n, chunk, w.slots, stride, w.cbytes, w.ckind, w.index, maxbits);
     __syncthreads();
   }
 }
@@ -953,7 +971,7 @@ kvtc_status launch_deflate_encode_batch(const EncodeJob *jobs_dev, int32_t njobs
   if (njobs == 0 || total_chunks == 0) return KVTC_OK;
   KVTC_MAX_CARVEOUT(deflate_encode_batch_kernel);
   const uint32_t grid = max_ctas > 0 ? std::min<uint32_t>(total_chunks, uint32_t(max_ctas)) : total_chunks;
-  deflate_encode_batch_kernel<<<grid, kEncThreads, 0, st>>>(jobs_dev, njobs, total_chunks, chunk);
+  deflate_encode_batch_kernel<<<grid, kEncThreads, 0, st>>>(jobs_dev, njobs, total_chunks, chunk, deflate_max_bits());
   KVTC_LAUNCH_CHECK();
   return KVTC_OK;
 }
@@ -1107,9 +1125,11 @@ constexpr int kRing = 4;           // per-lane ring of 16-byte stream blocks (cp
 struct FastShared {
   union {
     uint32_t hdr[kHdrWords + 2];   // header words (header parse), then
-    uint4 ring[kRing][kNSeg];      // per-lane read-ahead blocks (segment decode)
+    uint4 ring[kNSeg][kRing];      // per-lane read-ahead blocks (segment decode), lane-contiguous
   };
-  uint16_t table[1 << kTabBits];   // (sym << 4) | len; 0x8000 | k: longer code, subtable k
+  // entries: literal (sym << 8) | len; end-of-block kTeEob | len; no code kTeBad;
+  // longer code (k << 8) | kTeLink: subtable k (first level only)
+  uint16_t table[1 << kTabBits];
   uint16_t sub[kSubTabs << kSubBits];  // second level: the next kSubBits bits
   uint16_t code[260];
   int cnt[16], next[16];
@@ -1121,7 +1141,9 @@ struct FastShared {
   uint32_t segstart[kNSeg];
   uint32_t hdr_bits;
   int status;
+  int fast;                        // every code <= kTabBits bits: no subtables
 };
+constexpr uint32_t kTeLink = 0x10, kTeBad = 0x20, kTeEob = 0x40;
 
 struct InflateJobs {
   const uint8_t *sec[2];           // sections
@@ -1202,6 +1224,75 @@ __device__ int parse_header_fast(FastShared &S) {
   return 0;   // the literal/length code itself is checked and built in parallel (inflate_chunk)
 }
 
+// One lane's serial decoder over its segment.  Per pair of codes: one 32-bit
+// window at the bit position (two ring words, one funnel shift; two codes of
+// <= 15 bits fit), two table lookups, the output byte taken from the entry's high
+// byte by a byte permute.  With every code <= kTabBits bits (kFast, the encoder's
+// default limit) there is no subtable branch and the ring advances once per 16
+// codes (16 x 11 + 64 bits stay inside 3 blocks), else once per 8 (8 x 15 + 64).
+struct DecodeLane {
+  const uint16_t *table, *sub;
+  const uint32_t *ring;                    // this lane's 16 ring words
+  const uint4 *blk;
+  uint32_t nblk, issued, bp, bad;
+
+  __device__ __forceinline__ void advance(uint4 *ring_slots) {   // blocks of bp .. bp+2 resident
+    const uint32_t last = (bp >> 7) + kRing - 1;
+    for (; issued <= last; ++issued) {
+      if (issued < nblk)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(ring_slots + (issued & (kRing - 1)))),
+                     "l"(blk + issued)
+                     : "memory");
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+  }
+  __device__ __forceinline__ uint32_t window() const {
+    const uint32_t w = bp >> 5;
+    return __funnelshift_r(ring[w & 15], ring[(w + 1) & 15], bp);
+  }
+  template <bool kFast>
+  __device__ __forceinline__ uint32_t lookup(uint32_t bits) const {
+    uint32_t te = table[bits & ((1u << kTabBits) - 1)];
+    if (!kFast && (te & kTeLink)) te = sub[((te >> 8) << kSubBits) | ((bits >> kTabBits) & ((1u << kSubBits) - 1))];
+    return te;
+  }
+  template <bool kFast>
+  __device__ __forceinline__ uint32_t pair() {       // two codes -> bytes 0, 1
+    const uint32_t bits = window();
+    const uint32_t t0 = lookup<kFast>(bits);
+    const uint32_t t1 = lookup<kFast>(bits >> (t0 & 15));
+    bp += (t0 & 15) + (t1 & 15);
+    bad |= t0 | t1;
+    return __byte_perm(t0, t1, 0x0051);
+  }
+  template <bool kFast>
+  __device__ __forceinline__ void run(uint8_t *o, uint32_t s0, uint32_t s1, bool vec_out, uint4 *ring_slots) {
+    uint32_t i = s0;
+    // 16 codes -> one 16-byte store (segments are 16-byte aligned)
+    for (; vec_out && i + 16 <= s1; i += 16) {
+      uint32_t w[4];
+      if (kFast) advance(ring_slots);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (!kFast) advance(ring_slots);
+        const uint32_t p0 = pair<kFast>(), p1 = pair<kFast>();
+        w[2 * h] = __byte_perm(p0, p1, 0x5410);
+        const uint32_t p2 = pair<kFast>(), p3 = pair<kFast>();
+        w[2 * h + 1] = __byte_perm(p2, p3, 0x5410);
+      }
+      *reinterpret_cast<uint4 *>(o + i) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    for (; i < s1; ++i) {
+      if (((i - s0) & 7) == 0) advance(ring_slots);
+      const uint32_t te = lookup<kFast>(window());
+      bp += te & 15;
+      bad |= te;
+      o[i] = uint8_t(te >> 8);
+    }
+  }
+};
+
 // Chunk c of the section at `section` (raw size n_out, nch chunks) into out_base.
 // Every read is bounded by sec_len (the section's extent in the container, known
 // to the host): a damaged header, chunk table, index or stream sets *err (the
@@ -1240,9 +1331,8 @@ __device__ __forceinline__ void inflate_chunk(FastShared &S, const uint8_t *sect
   const uint32_t *words = reinterpret_cast<const uint32_t *>(stream);
   const uint32_t nw = umin32((e.bytes + 3) / 4, kHdrWords);
   for (uint32_t i = tid; i < kHdrWords + 2; i += kInfThreads) S.hdr[i] = i < nw ? __ldg(words + i) : 0u;
-  // 0x4000 marks "no code here" (len 0): a corrupt stream sets it in `bad`
-  for (int i = tid; i < (1 << kTabBits); i += kInfThreads) S.table[i] = 0x4000;
-  for (int i = tid; i < (kSubTabs << kSubBits); i += kInfThreads) S.sub[i] = 0x4000;
+  // kTeBad marks "no code here" (len 0): a corrupt stream sets it in `bad`
+  for (int i = tid; i < (1 << kTabBits); i += kInfThreads) S.table[i] = kTeBad;
   const uint32_t mylen = index[uint64_t(c) * kNSeg + tid];
   __syncthreads();
   if (tid == 0) {
@@ -1280,6 +1370,9 @@ __device__ __forceinline__ void inflate_chunk(FastShared &S, const uint8_t *sect
       code = (code + (b > 1 ? S.cnt[b - 1] : 0)) << 1;
       S.next[b] = code;
     }
+    int longer = 0;
+    for (int b = kTabBits + 1; b < 16; ++b) longer |= S.cnt[b];
+    S.fast = longer == 0;
   }
   // ranks: per-thread length counts, exclusive prefix over the 64 threads (two
   // warps) with 16 x 9-bit... counters packed as 4 lengths per 32-bit word x 4 words
@@ -1319,11 +1412,14 @@ __device__ __forceinline__ void inflate_chunk(FastShared &S, const uint8_t *sect
     }
   }
   __syncthreads();
+  if (!S.fast)
+    for (int i = tid; i < (kSubTabs << kSubBits); i += kInfThreads) S.sub[i] = kTeBad;
   for (int sym = tid; sym < 257; sym += kInfThreads) {
     const int l = S.lens[sym];
     if (l == 0) continue;
+    const uint16_t ent = uint16_t(sym < 256 ? (sym << 8) | l : kTeEob | l);
     if (l <= kTabBits) {
-      for (uint32_t f = S.code[sym]; f < (1u << kTabBits); f += (1u << l)) S.table[f] = uint16_t((sym << 4) | l);
+      for (uint32_t f = S.code[sym]; f < (1u << kTabBits); f += (1u << l)) S.table[f] = ent;
     } else {
       const uint32_t pre = S.code[sym] & ((1u << kTabBits) - 1);
       atomicOr(&S.premask[pre >> 5], 1u << (pre & 31));
@@ -1354,10 +1450,10 @@ __device__ __forceinline__ void inflate_chunk(FastShared &S, const uint8_t *sect
         atomicExch(err, -8);
         continue;
       }
-      S.table[pre] = uint16_t(0x8000 | k);
+      S.table[pre] = uint16_t((k << 8) | kTeLink);
       uint16_t *st = S.sub + (k << kSubBits);
-      for (uint32_t f = S.code[sym] >> kTabBits; f < (1u << kSubBits); f += (1u << (l - kTabBits)))
-        st[f] = uint16_t((sym << 4) | l);
+      const uint16_t ent = uint16_t(sym < 256 ? (sym << 8) | l : kTeEob | l);
+      for (uint32_t f = S.code[sym] >> kTabBits; f < (1u << kSubBits); f += (1u << (l - kTabBits))) st[f] = ent;
     }
   }
   // segment start = header bits + exclusive prefix of the segment lengths
@@ -1379,76 +1475,24 @@ __device__ __forceinline__ void inflate_chunk(FastShared &S, const uint8_t *sect
   uint64_t pos = S.hdr_bits + S.segstart[tid] - mylen + (tid >= 32 ? S.segstart[31] : 0);
   // Read-ahead through shared memory: each lane streams its own segment, so
   // loads cannot be coalesced; 16-byte cp.async copies fill a per-lane ring of 4
-  // blocks in the background.  (Rotating prefetched registers instead made every
-  // rotation wait for its load: ncu showed ~40 % of the samples stalled on it.)
-  // Decoding is branch-free per code: the 32 bits at the bit position come from
-  // two ring words and a funnel shift, so refills are not if-converted into every
-  // symbol (the earlier 64-bit bit buffer cost ~35 instructions per symbol); the
-  // ring advances once per 8 codes (8 x 15 bits + 32 stay inside 3 blocks).
-  // The stream is 16-byte aligned and zero-padded.
+  // blocks (16 words, lane-contiguous) in the background.
   const uint4 *blk = reinterpret_cast<const uint4 *>(stream);
   const uint32_t nblk = (e.bytes + 15) / 16;
-  uint32_t issued = uint32_t(pos >> 7);    // next block to copy into the ring
-  auto issue_upto = [&](uint32_t last) {   // copies blocks [issued, last] (slot b % 4)
-    for (; issued <= last; ++issued) {
-      if (issued < nblk)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&S.ring[issued % kRing][tid])),
-                     "l"(blk + issued)
-                     : "memory");
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    }
-  };
-  const uint32_t *ring32 = reinterpret_cast<const uint32_t *>(&S.ring[0][0]);
-  auto word = [&](uint32_t gw) -> uint32_t {    // stream word gw (its block is resident)
-    return ring32[(((gw >> 2) % kRing) * kNSeg + tid) * 4 + (gw & 3)];
-  };
-  uint32_t bp = uint32_t(pos);
-  uint32_t bad = 0;
-  auto decode = [&]() -> uint32_t {
-    const uint32_t w = bp >> 5;
-    const uint32_t bits = __funnelshift_r(word(w), word(w + 1), bp & 31);
-    uint32_t te = S.table[bits & ((1u << kTabBits) - 1)];
-    if (te & 0x8000) te = S.sub[((te & 0x7FFF) << kSubBits) | ((bits >> kTabBits) & ((1u << kSubBits) - 1))];
-    bp += te & 15;
-    bad |= te;                               // 0x4000: no code / 0x1000: end-of-block inside a segment
-    return (te >> 4) & 0xFF;
-  };
-  auto advance = [&]() {                     // blocks of bp .. bp + 8 x 15 + 32 bits resident
-    issue_upto((bp >> 7) + kRing - 1);
-    asm volatile("cp.async.wait_group 1;" ::: "memory");
-  };
-  uint32_t i = s0;
-  // 16 codes -> one 16-byte store (segments are 16-byte aligned)
+  DecodeLane L{S.table, S.sub, reinterpret_cast<const uint32_t *>(&S.ring[tid][0]), blk, nblk, uint32_t(pos >> 7),
+               uint32_t(pos), 0u};
   const bool vec_out = (reinterpret_cast<uintptr_t>(o) & 15) == 0;
-  for (; vec_out && i + 16 <= s1; i += 16) {
-    uint32_t w[4];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      advance();
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const uint32_t b0 = decode(), b1 = decode(), b2 = decode(), b3 = decode();
-        w[2 * h + q] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
-      }
-    }
-    *reinterpret_cast<uint4 *>(o + i) = make_uint4(w[0], w[1], w[2], w[3]);
-  }
-  for (; i < s1; ++i) {
-    if (((i - s0) & 7) == 0) advance();
-    o[i] = uint8_t(decode());
-  }
+  if (S.fast) L.run<true>(o, s0, s1, vec_out, &S.ring[tid][0]);
+  else L.run<false>(o, s0, s1, vec_out, &S.ring[tid][0]);
+  uint32_t bad = L.bad;
   if (s1 == nc) {                            // the chunk's last segment ends with the end-of-block code
-    advance();
-    const uint32_t w = bp >> 5;
-    const uint32_t bits = __funnelshift_r(word(w), word(w + 1), bp & 31);
-    uint32_t te = S.table[bits & ((1u << kTabBits) - 1)];
-    if (te & 0x8000) te = S.sub[((te & 0x7FFF) << kSubBits) | ((bits >> kTabBits) & ((1u << kSubBits) - 1))];
-    if ((te & 0x5000) != 0x1000) bad |= 0x4000;
-    bp += te & 15;
+    L.advance(&S.ring[tid][0]);
+    const uint32_t te = L.lookup<false>(L.window());
+    if ((te & (kTeBad | kTeEob)) != kTeEob) bad |= kTeBad;
+    L.bp += te & 15;
   }
   // each segment must end exactly where the side index says, inside the stream
-  if (uint64_t(bp) != pos + mylen || uint64_t(bp) > uint64_t(e.bytes) * 8) bad |= 0x4000;
-  if (bad & 0x5000) atomicExch(err, -7);
+  if (uint64_t(L.bp) != pos + mylen || uint64_t(L.bp) > uint64_t(e.bytes) * 8) bad |= kTeBad;
+  if (bad & (kTeBad | kTeEob)) atomicExch(err, -7);
   asm volatile("cp.async.wait_all;" ::: "memory");   // no copy may land in the next chunk's header
 }
 

@@ -9,6 +9,7 @@
 //   raw token copies for sinks / window.
 #include "internal.h"
 #include "quant.cuh"
+#include "dequant.cuh"
 
 namespace kvtc {
 
@@ -353,103 +354,70 @@ kvtc_status launch_quant_pack_simt(const SegDesc *segs, const GroupDesc *groups,
 }
 
 // ---------------------------------------------------------------- dequant
-// Block = one tile x a run of kDqGroups groups.  A thread owns 8 consecutive
-// codes of one token (every group size but 1 is a multiple of 8): one 2/4/8-byte
-// code read, the token's (shift, scale) read straight from the params section,
-// one 16-byte fp16 store when the column is 8-aligned.  x^ = code*scale + shift
-// in fp32 (fp8: e4m3(code)*scale + shift), D^ = fp16(x^) (R5).
-constexpr int kDqGroups = 8;
-constexpr int kDqThreads = 256;
+// D2 (R5): D^ [m][ld] fp16 from the payload.  Thread (chunk k, row) writes the
+// 16-byte chunk D^[row][8k, 8k+8): a warp covers 32 consecutive chunks of one row
+// (512 contiguous bytes), a block 32 chunks x 32 rows (4 rows per thread, loads
+// issued before any is consumed).  Chunks that are 8 aligned elements of one
+// group (DqChunk ok = 1) read their token's fp16 factors (4 B) and 8 codes (2 /
+// 4 / 8 B, aligned in a full tile) and convert with dq8 (the 1024 + c bit trick,
+// fma.rn.f16x2: one rounding of the exact x^); every other chunk (size-1 groups,
+// misaligned starts, the partial last tile) goes element by element (dq1).
+// Columns past r_nz in the last chunk are written as 0 (the GEMM's tensor map
+// never reads them).  Grid-stride over blocks (bounded grid beside a GEMM).
+constexpr int kDqRowsPerThread = 4;
 
-__device__ __forceinline__ uint64_t load_le(const uint8_t *p, int n) {
-  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
-  if (n == 8 && (a & 7) == 0) return *reinterpret_cast<const uint64_t *>(p);
-  if (n == 4 && (a & 3) == 0) return *reinterpret_cast<const uint32_t *>(p);
-  if (n == 2 && (a & 1) == 0) return *reinterpret_cast<const uint16_t *>(p);
-  uint64_t v = 0;
-  for (int i = 0; i < n; ++i) v |= uint64_t(p[i]) << (8 * i);
-  return v;
-}
-
-// R5: D^ = fp16(x^), x^ = v * scale + shift.  v (integer level or E4M3 value),
-// scale and shift are exact in fp16, so one fp16 fma rounds the exact x^ once,
-// which is the oracle's fp16(fp64 x^).
-__device__ __forceinline__ __half dq_value(bool fp8, uint32_t code, __half scale, __half shift) {
-  const __half v = fp8 ? __float2half_rn(e4m3_to_f32(uint8_t(code))) : __uint2half_rn(code);
-  return __hfma(v, scale, shift);
-}
-
-__global__ void __launch_bounds__(kDqThreads) dequant_kernel(const PlanGroup *groups, const int64_t *codes_off_full,
-                                                             int32_t G, const int64_t *codes_off_last,
-                                                             int64_t tile_bytes, const uint8_t *payload, int64_t m,
-                                                             __half *Dh, int64_t ld) {
-  const int64_t gx = (G + kDqGroups - 1) / kDqGroups;
-  const int64_t nblk = gx * ((m + kTileM - 1) / kTileM);
-  for (int64_t bid = blockIdx.x; bid < nblk; bid += gridDim.x) {
-  const int64_t by = bid / gx, bx = bid - by * gx;
-  const int64_t m0 = by * kTileM;
-  const int ntok = int(m - m0 < kTileM ? m - m0 : kTileM);
-  const bool last = ntok < kTileM;
-  const uint8_t *tile = payload + by * tile_bytes;
-  const int g_end = min(G, int(bx + 1) * kDqGroups);
-  for (int g = int(bx) * kDqGroups; g < g_end; ++g) {
-    const PlanGroup pg = groups[g];
-    const uint8_t *cb = tile + (last ? codes_off_last[g] : codes_off_full[g]);
-    const uint8_t *params = tile + 4 * int64_t(g) * ntok;
-    const int b = bits_of(pg.type);
-    const uint32_t mask = (1u << b) - 1;
-    const bool fp8 = pg.type == KVTC_T_FP8;
-    const int size = pg.size;
-    if (size % 8 == 0) {
-      const int per_tok = size / 8;
-      const int n = ntok * per_tok;
-      const bool vec = (pg.col % 8 == 0) && (ld % 8 == 0);
-      for (int j = threadIdx.x; j < n; j += kDqThreads) {
-        const int tau = j / per_tok;
-        const int c0 = (j - tau * per_tok) * 8;
-        const uint32_t pr = uint32_t(load_le(params + 4 * tau, 4));
-        const __half shift = __ushort_as_half(uint16_t(pr & 0xFFFF)), scale = __ushort_as_half(uint16_t(pr >> 16));
-        const uint64_t codes = load_le(cb + (int64_t(j) * 8 * b) / 8, b);     // 8 codes = b bytes
-        __align__(16) __half out[8];
+__global__ void __launch_bounds__(256) dequant_rows_kernel(const DqChunk *chunks, const DqCol *cols, int32_t nch8,
+                                                           const int64_t *codes_off_full,
+                                                           const int64_t *codes_off_last, int64_t tile_bytes,
+                                                           const uint8_t *payload, int64_t m, __half *Dh, int64_t ld) {
+  const int64_t nbx = (nch8 + 31) / 32, nby = (m + 31) / 32;
+  for (int64_t blk = blockIdx.x; blk < nbx * nby; blk += gridDim.x) {
+    const int64_t by = blk / nbx, bx = blk - by * nbx;
+    const int k = int(bx) * 32 + threadIdx.x;
+    if (k >= nch8) continue;
+    const int64_t t = (by * 32) / kTileM;                        // tile (32 | 128)
+    const int ntok = int(m - t * kTileM < kTileM ? m - t * kTileM : kTileM);
+    const int row0 = int(by * 32 - t * kTileM) + threadIdx.y;
+    const uint8_t *tile = payload + t * tile_bytes;
+    const DqChunk d = chunks[k];
+    __half *dst = Dh + (t * kTileM + row0) * ld + 8 * int64_t(k);
+    if (ntok == kTileM && d.ok == 1) {
+      const int b = bits_of(d.type);
+      uint32_t pr[kDqRowsPerThread], lo[kDqRowsPerThread], hi[kDqRowsPerThread];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint32_t code = uint32_t(codes >> (k * b)) & mask;
-          out[k] = dq_value(fp8, code, scale, shift);
-        }
-        __half *dst = Dh + (m0 + tau) * ld + pg.col + c0;
-        if (vec) {
-          *reinterpret_cast<uint4 *>(dst) = *reinterpret_cast<const uint4 *>(out);
-        } else {
-#pragma unroll
-          for (int k = 0; k < 8; ++k) dst[k] = out[k];
-        }
+      for (int r = 0; r < kDqRowsPerThread; ++r) {
+        const int row = row0 + 8 * r;
+        pr[r] = __ldg(reinterpret_cast<const unsigned int *>(tile + d.par_base + 4 * row));
+        load_codes8(tile + d.code_base + row * int32_t(d.stride), b, lo[r], hi[r]);
       }
+#pragma unroll
+      for (int r = 0; r < kDqRowsPerThread; ++r)
+        *reinterpret_cast<uint4 *>(dst + 8 * r * ld) = dq8(d.type, lo[r], hi[r], pr[r]);
     } else {
-      const int n = ntok * size;
-      for (int e = threadIdx.x; e < n; e += kDqThreads) {
-        const int tau = e / size;
-        const int c = e - tau * size;
-        const uint32_t pr = uint32_t(load_le(params + 4 * tau, 4));
-        const __half shift = __ushort_as_half(uint16_t(pr & 0xFFFF)), scale = __ushort_as_half(uint16_t(pr >> 16));
-        const int64_t bit = int64_t(e) * b;
-        const uint32_t code = (cb[bit >> 3] >> (bit & 7)) & mask;
-        Dh[(m0 + tau) * ld + pg.col + c] = dq_value(fp8, code, scale, shift);
+      const int64_t *coff = ntok == kTileM ? codes_off_full : codes_off_last;
+      for (int r = 0; r < kDqRowsPerThread; ++r) {
+        const int row = row0 + 8 * r;
+        if (row >= ntok) break;
+        *reinterpret_cast<uint4 *>(dst + 8 * r * ld) =
+            d.type ? dq_generic8(cols, 8 * k, tile, coff, ntok, row) : make_uint4(0u, 0u, 0u, 0u);
       }
     }
   }
-  }
 }
 
-kvtc_status launch_dequant(const PlanGroup *groups_dev, const int64_t *codes_off_full, int32_t G,
+kvtc_status launch_dequant(const DqChunk *chunks, const DqCol *cols, int32_t r_nz, const int64_t *codes_off_full,
                            const int64_t *codes_off_last, int64_t tile_bytes, const uint8_t *payload, int64_t m,
                            __half *Dh, int64_t ld, cudaStream_t st, int32_t max_ctas) {
-  if (G == 0 || m == 0) return KVTC_OK;
-  int64_t grid = ceil_div(G, kDqGroups) * ceil_div(m, kTileM);
+  if (r_nz == 0 || m == 0) return KVTC_OK;
+  KVTC_CHECK_ARG(ld % 8 == 0 && ld >= (r_nz + 7) / 8 * 8, "D^ leading dimension");
+  KVTC_CHECK_ARG((reinterpret_cast<uintptr_t>(Dh) & 15) == 0, "D^ must be 16-byte aligned");
+  const int32_t nch8 = (r_nz + 7) / 8;
+  int64_t grid = ceil_div(nch8, 32) * ceil_div(m, 32);
   if (max_ctas > 0) grid = std::min<int64_t>(grid, max_ctas);
   grid = std::min<int64_t>(grid, int64_t(1) << 30);
-  KVTC_MAX_CARVEOUT(dequant_kernel);
-  dequant_kernel<<<unsigned(grid), kDqThreads, 0, st>>>(groups_dev, codes_off_full, G, codes_off_last, tile_bytes, payload, m,
-                                               Dh, ld);
+  KVTC_MAX_CARVEOUT(dequant_rows_kernel);
+  dequant_rows_kernel<<<unsigned(grid), dim3(32, 8), 0, st>>>(chunks, cols, nch8, codes_off_full, codes_off_last,
+                                                              tile_bytes, payload, m, Dh, ld);
   KVTC_LAUNCH_CHECK();
   return KVTC_OK;
 }

@@ -210,7 +210,9 @@ kvtc_status launch_quant_pack_simt(const SegDesc *segs, const GroupDesc *groups,
                                    const int64_t *codes_off_last, uint8_t *payload, cudaStream_t st);
 kvtc_status launch_codes_off_last(const int32_t *gsize, const int32_t *gbits, int32_t G, int32_t ntok,
                                   int64_t *out, cudaStream_t st);
-kvtc_status launch_dequant(const PlanGroup *groups_dev, const int64_t *codes_off_full, int32_t G,
+// D2: D^ [m x ld] fp16 (ld % 8 == 0, >= r_nz rounded up to 8; 16-byte aligned)
+// from m tokens of payload, with the plan's chunk / column tables (api.cu).
+kvtc_status launch_dequant(const DqChunk *chunks, const DqCol *cols, int32_t r_nz, const int64_t *codes_off_full,
                            const int64_t *codes_off_last, int64_t tile_bytes, const uint8_t *payload, int64_t m,
                            __half *Dh, int64_t ld, cudaStream_t st, int32_t max_ctas = 0);
 kvtc_status launch_copy_tokens(const kvtc_kv_view &src, __nv_bfloat16 *const *src_bases, int64_t src_tok,

@@ -99,6 +99,11 @@ def segment_bit_lengths(stream: bytes, nbytes: int, seg_bytes: int, nseg: int):
     return lengths, bytes(out), pos
 
 
+def code_lengths(stream: bytes):
+    """Literal/length code lengths (symbols 0..256) of a dynamic chunk stream."""
+    return _dynamic_header(stream)[1][:257]
+
+
 def _dynamic_header(stream: bytes):
     bits = int.from_bytes(stream[:2048], "little")
     pos = 0

@@ -1,4 +1,7 @@
 """GPU parity of each kernel against the oracle on identical seeded inputs."""
+import os
+import subprocess
+import sys
 import zlib
 
 import numpy as np
@@ -6,7 +9,9 @@ import pytest
 import torch
 
 from tests import gpu_env as E
-from tests.kvtc_format import parse_section, segment_bit_lengths
+from tests.kvtc_format import code_lengths, parse_section, segment_bit_lengths
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 pytestmark = pytest.mark.gpu
 
@@ -126,10 +131,12 @@ def test_deflate_roundtrip_zlib(K):
         (rng.geometric(0.05, 300001) % 256).astype(np.uint8),           # skewed: long codes
         np.array([7], dtype=np.uint8),
     ]
-    for data in cases:
+    for ci, data in enumerate(cases):
         t = torch.from_numpy(data).cuda()
         sec = K.deflate(t)
         info = parse_section(sec.cpu().numpy().tobytes())
+        if ci == 3:   # skewed: codes past the inflater's 11-bit first level (its subtable path)
+            assert max(max(code_lengths(s)) for s, e in zip(info["streams"], info["table"]) if e["kind"] == 0) > 11
         assert info["raw"] == len(data)
         # every chunk is an independent raw DEFLATE stream stock zlib inflates
         got = b"".join(zlib.decompress(s, wbits=-15) for s in info["streams"])
@@ -141,6 +148,7 @@ def test_deflate_roundtrip_zlib(K):
             if info["table"][c]["kind"] != 0:
                 assert not info["index"][c].any()
                 continue
+            assert max(code_lengths(info["streams"][c])) <= 15          # RFC 1951 limit
             nb = min(info["chunk"], len(data) - c * info["chunk"])
             lens, dec, end = segment_bit_lengths(info["streams"][c], nb, info["seg"], 64)
             assert dec == data.tobytes()[c * info["chunk"]: c * info["chunk"] + nb]
@@ -149,6 +157,35 @@ def test_deflate_roundtrip_zlib(K):
         # and the GPU inflates its own section
         back = K.inflate(sec, len(data))
         assert torch.equal(back.cpu(), t.cpu())
+
+
+_RFC_LIMIT_SCRIPT = r"""
+import sys, zlib, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+sys.path.insert(0, sys.argv[1] + "/tests")
+from paper_2511_01815_b200 import kvtc as K
+from kvtc_format import parse_section, code_lengths
+rng = np.random.default_rng(3)
+data = (rng.geometric(0.05, 300001) % 256).astype(np.uint8)
+t = torch.from_numpy(data).cuda()
+sec = K.deflate(t)
+info = parse_section(sec.cpu().numpy().tobytes())
+assert b"".join(zlib.decompress(s, wbits=-15) for s in info["streams"]) == data.tobytes()
+longest = max(max(code_lengths(s)) for s, e in zip(info["streams"], info["table"]) if e["kind"] == 0)
+assert longest == 11, longest
+assert torch.equal(K.inflate(sec, len(data)).cpu(), t.cpu())
+print("ok", longest)
+"""
+
+
+def test_deflate_limit11_fast_inflate():
+    """KVTC_DEFLATE_MAXBITS=11: skewed chunks (codes up to 15 bits under the
+    default RFC limit, test above) get length-limited codes that zlib still
+    inflates, and the inflater takes its subtable-free path."""
+    env = dict(os.environ, KVTC_DEFLATE_MAXBITS="11")
+    r = subprocess.run([sys.executable, "-c", _RFC_LIMIT_SCRIPT, ROOT], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and r.stdout.startswith("ok"), r.stdout + r.stderr
 
 
 def test_gpu_inflates_zlib_streams(K):
