@@ -597,13 +597,16 @@ def main():
     # caller-stream DEFLATE handles the KEYS only (the values' runs beside the keys'
     # GEMM as the *_overlapped stage, whose time is shared with it); one inflate
     # launch covers both streams; the keys' dequantisation runs on the caller's
-    # stream, the values' beside the keys' GEMM (KVTC_DQ_FUSED=1: inside the GEMM)
+    # stream, the values' beside the keys' GEMM (KVTC_D_INFLATE_DQ=1: one launch
+    # inflates and dequantises both, d.inflate_dequant: sections read, payload
+    # written, D^ written; the payload re-read hits L2)
     stage_bytes = {"c.rans_keys": info.payload_bytes[0] + info.entropy_bytes[0],
                    "c.rans_values_overlapped": info.payload_bytes[1] + info.entropy_bytes[1],
                    "d.rans_decode": pay + ent,
                    "c.deflate": info.payload_bytes[0] + info.entropy_bytes[0],
                    "c.deflate_overlapped": info.payload_bytes[1] + info.entropy_bytes[1],
                    "d.inflate": pay + ent,
+                   "d.inflate_dequant": ent + pay + m * 2 * (rpad[0] + rpad[1]),
                    "d.dequant": info.payload_bytes[0] + m * 2 * rpad[0],
                    "d.dequant_overlapped": info.payload_bytes[1] + m * 2 * rpad[1],
                    "c.gather_unrope": 2 * 2 * p * m, "c.gather_unrope_overlapped": 2 * 2 * p * m,

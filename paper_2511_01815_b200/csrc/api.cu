@@ -360,7 +360,7 @@ kvtc_status plan_compile(kvtc_plan *pl) {
       for (int j = 0; j < pg.size; ++j)
         dq[pg.col + j] = DqCol{uint16_t(g), uint8_t(pg.type), 0, uint16_t(j), uint16_t(pg.size), int32_t(off[g]), 0};
     }
-    std::vector<DqChunk> ch(ncols / 8, DqChunk{0, 0, 0, 0, 0, 0});
+    std::vector<DqChunk> ch(ncols / 8, DqChunk{0, 0, 0, 0, 0, -1});
     std::vector<int32_t> tail;
     for (int c = 0; c < ncols; c += 8) {
       const DqCol &d = dq[c];
@@ -379,6 +379,18 @@ kvtc_status plan_compile(kvtc_plan *pl) {
         k.ok = 3;                       // dequantised by the pre-pass into the tail buffer
         k.code_base = int32_t(tail.size()) * 16;
         tail.push_back(c);
+        // 8 consecutive size-1 groups of one type with adjacent code blocks
+        bool run = c + 8 <= col && d.type && d.size == 1;
+        const int b = d.type ? bits_of(d.type) : 0;
+        for (int q = 1; run && q < 8; ++q) {
+          const DqCol &e = dq[c + q];
+          run = e.type == d.type && e.size == 1 && e.gidx == d.gidx + q && e.off_full == d.off_full + q * 16 * b;
+        }
+        if (run) {
+          k.run_code = d.off_full;
+          k.par_base = 4 * d.gidx * kTileM;
+          k.stride = uint16_t(16 * b);
+        }
       }
     }
     pl->dq_cols_n = ncols;

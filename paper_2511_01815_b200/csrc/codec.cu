@@ -982,8 +982,10 @@ struct DecompWs {
   float2 *cs;
   uint8_t *tail;         // fused path: the pre-pass columns (shared by K and V, one GEMM at a time)
   uint8_t *rans_ws[2];   // rANS containers: the decoder tables of each stream
+  uint32_t *ictr;        // fused inflate + dequantise: [2] item counters, [2][ntiles] tile arrivals
   int64_t ld;
 };
+inline int64_t ictr_words(int64_t m) { return 2 + 2 * ceil_div(m, kTileM); }
 DecompWs carve_decomp(const kvtc_plan *kp, const kvtc_plan *vp, const ContainerHeader &h, void *workspace,
                       size_t workspace_bytes) {
   Bump ws(workspace, workspace_bytes);
@@ -1004,6 +1006,7 @@ DecompWs carve_decomp(const kvtc_plan *kp, const kvtc_plan *vp, const ContainerH
   const size_t rw = (h.flags & kFlagRans) ? rans_decode_workspace(kRansMaxClasses) : 0;
   w.rans_ws[0] = ws.take<uint8_t>(rw);
   w.rans_ws[1] = ws.take<uint8_t>(rw);
+  w.ictr = ws.take<uint32_t>(ictr_words(h.m));
   return w;
 }
 
@@ -1027,6 +1030,35 @@ kvtc_status enqueue_inflate(const uint8_t *ib, const ContainerHeader &h, const D
   return launch_inflate_sections(ib + h.section_off[0], h.entropy_bytes[0], h.payload_bytes[0], nch[0], w.payloads[0],
                                  ib + h.section_off[1], h.entropy_bytes[1], h.payload_bytes[1], nch[1], w.payloads[1],
                                  w.err, st);
+}
+// Both sections inflated AND dequantised by one launch (inflate_dequant_kernel):
+// each 32-row block of D^ is expanded as soon as its tile's chunks are inflated.
+kvtc_status enqueue_inflate_dequant(const uint8_t *ib, const ContainerHeader &h, const DecompWs &w,
+                                    const kvtc_plan *kp, const kvtc_plan *vp, cudaStream_t st) {
+  ProfScope ps("d.inflate_dequant", st);
+  KVTC_CUDA_TRY(cudaMemsetAsync(w.ictr, 0, size_t(ictr_words(h.m)) * 4, st));
+  InflateDqArgs a{};
+  const int64_t ntiles = ceil_div(h.m, kTileM);
+  for (int sv = 0; sv < 2; ++sv) {
+    kvtc_plan *pl = const_cast<kvtc_plan *>(sv ? vp : kp);
+    InflateDqStream &x = a.s[sv];
+    x.sec = ib + h.section_off[sv];
+    x.sec_len = h.entropy_bytes[sv];
+    x.n_out = h.payload_bytes[sv];
+    x.nch = uint32_t((h.payload_bytes[sv] + h.chunk_bytes - 1) / h.chunk_bytes);
+    x.out = w.payloads[sv];
+    x.dq = DqArgs{pl->d_dqchunks, pl->d_dqcols, int32_t((pl->r_nz + 7) / 8), pl->d_codes_off_full,
+                  plan_codes_off_last(pl, h.m % kTileM), pl->tile_bytes, w.payloads[sv], h.m, w.Dh[sv], w.ld};
+    x.nbx = uint32_t(ceil_div(x.dq.nch8, 32));
+    x.ndq = pl->r_nz ? uint32_t(x.nbx * ntiles) : 0u;
+    x.tile_done = w.ictr + 2 + sv * ntiles;
+    if (!pl->r_nz) KVTC_CUDA_TRY(cudaMemsetAsync(w.Dh[sv], 0, h.m * w.ld * 2, st));
+  }
+  KVTC_CHECK_ARG(h.chunk_bytes == 16384 || h.chunk_bytes == 32768 || h.chunk_bytes == 65536, "chunk bytes");
+  a.cb_shift = h.chunk_bytes == 16384 ? 14 : (h.chunk_bytes == 32768 ? 15 : 16);
+  a.ctr = w.ictr;
+  a.err = w.err;
+  return launch_inflate_dequant(a, st);
 }
 // Checksums of the inflated payloads and of the raw section against the header
 // (integrity.cu): mismatch bits 1 / 2 (payload K / V), 4 (raw section).
@@ -1104,7 +1136,15 @@ kvtc_status decompress_enqueue(const kvtc_basis *kb, const kvtc_plan *kp, const 
   // KVTC_D_INFLATE_SIDE=1 (A/B): only the keys' section is inflated up front; the
   // values' is inflated on the side stream (bounded grid) beside the keys' GEMM
   const bool inflate_side = ovl && !(h.flags & kFlagRans) && env_flag("KVTC_D_INFLATE_SIDE", false);
-  if (inflate_side) {
+  // KVTC_D_INFLATE_DQ=1: one launch inflates and dequantises both streams
+  // (inflate_dequant_kernel; measured slower than the split path: 1.25-1.32 vs
+  // 0.79 ms in the step); default: the inflater, then the
+  // dequantiser per stream -- keys here, values beside the keys' GEMM
+  const bool front = !inflate_side && !(h.flags & kFlagRans) && !dq_fused(kp, vp) &&
+                     env_flag("KVTC_D_INFLATE_DQ", false);
+  if (front) {
+    if ((s = enqueue_inflate_dequant(ib, h, w, kp, vp, st))) return s;
+  } else if (inflate_side) {
     ProfScope ps("d.inflate_k", st);
     const uint32_t nk = uint32_t((h.payload_bytes[0] + h.chunk_bytes - 1) / h.chunk_bytes);
     if ((s = launch_inflate_section(ib + h.section_off[0], h.entropy_bytes[0], h.payload_bytes[0], nk,
@@ -1115,7 +1155,7 @@ kvtc_status decompress_enqueue(const kvtc_basis *kb, const kvtc_plan *kp, const 
   }
   const bool fused = dq_fused(kp, vp);
   auto expand = [&](int sv, cudaStream_t q, int ctas) -> kvtc_status {
-    if (fused) return KVTC_OK;                    // dequantised inside the reconstruction GEMM
+    if (fused || front) return KVTC_OK;           // dequantised inside the GEMM / the inflater
     kvtc_plan *pl = const_cast<kvtc_plan *>(sv ? vp : kp);
     kvtc_status r;
     ProfScope ps(sv && ovl ? "d.dequant_overlapped" : "d.dequant", q);
@@ -1190,6 +1230,7 @@ extern "C" size_t kvtc_decompress_workspace_bytes(const kvtc_basis *kb, const kv
   b.take<uint8_t>(dq_fused(kp, vp) ? dq_tail_bytes(h.m, std::max(kp->n_tail, vp->n_tail)) : 0);
   b.take<uint8_t>((h.flags & kFlagRans) ? rans_decode_workspace(kRansMaxClasses) : 0);
   b.take<uint8_t>((h.flags & kFlagRans) ? rans_decode_workspace(kRansMaxClasses) : 0);
+  b.take<uint32_t>(2 + 2 * ((h.m + kTileM - 1) / kTileM));
   return b.used + 256;
 }
 
@@ -1256,7 +1297,10 @@ extern "C" kvtc_status kvtc_decompress_begin(const kvtc_basis *kb, const kvtc_pl
   const uint8_t *ib = static_cast<const uint8_t *>(in);
   KVTC_CUDA_TRY(cudaMemsetAsync(w.err, 0, 16, st));
   KVTC_CUDA_TRY(cudaMemsetAsync(w.hsum, 0, 32, st));
-  if (h.m) {
+  if (h.m && !(h.flags & kFlagRans) && !dq_fused(kp, vp) && env_flag("KVTC_D_INFLATE_DQ", false)) {
+    if ((s = enqueue_inflate_dequant(ib, h, w, kp, vp, st))) return s;
+    if (kb->has_rope && (s = rope_table_for(kb, h.pos0 + h.sinks, h.m, w.cs, st))) return s;
+  } else if (h.m) {
     if ((s = enqueue_inflate(ib, h, w, st))) return s;
     ProfScope ps("d.dequant", st);
     for (int sv = 0; sv < 2 && !dq_fused(kp, vp); ++sv) {

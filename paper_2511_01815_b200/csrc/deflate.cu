@@ -32,6 +32,7 @@
 #include <cub/block/block_scan.cuh>
 
 #include "internal.h"
+#include "dequant.cuh"
 
 namespace kvtc {
 
@@ -642,11 +643,14 @@ __device__ __forceinline__ void encode_chunk(EncShared &S, const int c, const ui
     const bool aligned = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
     const uint32_t nvec = aligned ? nc / 16 : 0;
     uint32_t *h = S.u.whist[warp];
-    for (uint32_t v = t; v < nvec; v += kEncThreads) {
-      const uint4 q = __ldg(reinterpret_cast<const uint4 *>(src) + v);
+    const uint4 *sv = reinterpret_cast<const uint4 *>(src);
+    uint4 q = t < nvec ? __ldg(sv + t) : make_uint4(0u, 0u, 0u, 0u);
+    for (uint32_t v = t; v < nvec; v += kEncThreads) {       // next 16 bytes loaded while these are counted
+      const uint4 qn = v + kEncThreads < nvec ? __ldg(sv + v + kEncThreads) : q;
       const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
       for (int k = 0; k < 16; ++k) atomicAdd(&h[(w4[k >> 2] >> (8 * (k & 3))) & 0xFF], 1u);
+      q = qn;
     }
     for (uint32_t i = nvec * 16 + t; i < nc; i += kEncThreads) atomicAdd(&h[src[i]], 1u);
   }
@@ -686,14 +690,19 @@ __device__ __forceinline__ void encode_chunk(EncShared &S, const int c, const ui
   // ---- bit counts per piece, exclusive scan
   const bool vec = ((reinterpret_cast<uintptr_t>(src + p0) & 15) == 0) && ((p1 - p0) % 16 == 0);
   uint32_t mybits = 0;
-  if (vec) {
-    for (uint32_t i = p0; i < p1; i += 16) {
-      const uint4 q = __ldg(reinterpret_cast<const uint4 *>(src + i));
+  if (vec && p0 < p1) {
+    // the next 16 bytes are loaded while the current ones are counted
+    const uint4 *v = reinterpret_cast<const uint4 *>(src + p0);
+    const uint32_t nv = (p1 - p0) / 16;
+    uint4 q = __ldg(v);
+    for (uint32_t j = 0; j < nv; ++j) {
+      const uint4 qn = __ldg(v + (j + 1 < nv ? j + 1 : j));
       const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
       for (int k = 0; k < 16; ++k) mybits += S.sym[(w4[k >> 2] >> (8 * (k & 3))) & 0xFF] >> 16;
+      q = qn;
     }
-  } else {
+  } else if (!vec) {
     for (uint32_t i = p0; i < p1; ++i) mybits += S.sym[src[i]] >> 16;
   }
   if (t == 0) mybits += S.hdr_bits;
@@ -780,12 +789,16 @@ __device__ __forceinline__ void encode_chunk(EncShared &S, const int c, const ui
       }
     };
     if (vec) {
-      for (uint32_t i = p0; i < p1; i += 16) {
-        const uint4 q = __ldg(reinterpret_cast<const uint4 *>(src + i));
+      const uint4 *v = reinterpret_cast<const uint4 *>(src + p0);
+      const uint32_t nv = (p1 - p0) / 16;
+      uint4 q = nv ? __ldg(v) : make_uint4(0u, 0u, 0u, 0u);
+      for (uint32_t j = 0; j < nv; ++j) {
+        const uint4 qn = __ldg(v + (j + 1 < nv ? j + 1 : j));
         const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
         for (int k = 0; k < 16; k += 2)
           put2(S.sym[__byte_perm(w4[k >> 2], 0, 0x4440 | (k & 3))], S.sym[__byte_perm(w4[k >> 2], 0, 0x4440 | ((k + 1) & 3))]);
+        q = qn;
       }
     } else {
       for (uint32_t i = p0; i < p1; ++i) put(S.sym[src[i]]);
@@ -1224,17 +1237,23 @@ __device__ int parse_header_fast(FastShared &S) {
   return 0;   // the literal/length code itself is checked and built in parallel (inflate_chunk)
 }
 
-// One lane's serial decoder over its segment.  Per pair of codes: one 32-bit
-// window at the bit position (two ring words, one funnel shift; two codes of
-// <= 15 bits fit), two table lookups, the output byte taken from the entry's high
-// byte by a byte permute.  With every code <= kTabBits bits (kFast, the encoder's
-// default limit) there is no subtable branch and the ring advances once per 16
-// codes (16 x 11 + 64 bits stay inside 3 blocks), else once per 8 (8 x 15 + 64).
+// One lane's serial decoder over its segment.  Per pair of codes: the 32 bits at
+// the bit position from two words kept in registers (lo, hi = stream words
+// bp/32, bp/32 + 1) by one funnel shift (two codes of <= 15 bits fit), two table
+// lookups, the output byte taken from the entry's high byte by a byte permute.
+// The word after hi is loaded from the ring at the start of the pair, off the
+// dependency chain, and shifted in when the pair crossed a word (<= 30 bits:
+// at most one): one ring load and two table loads per pair (ncu: the shared-
+// memory pipe, ~2.4 wavefronts per load from random bank conflicts, bounds this
+// loop).  With every code <= kTabBits bits (kFast) there is no subtable branch and
+// the ring advances once per 16 codes (16 x 11 + 96 bits stay inside 3 blocks),
+// else once per 8 (8 x 15 + 96).
 struct DecodeLane {
   const uint16_t *table, *sub;
   const uint32_t *ring;                    // this lane's 16 ring words
   const uint4 *blk;
   uint32_t nblk, issued, bp, bad;
+  uint32_t lo, hi;                         // stream words bp/32 and bp/32 + 1 (after load_window)
 
   __device__ __forceinline__ void advance(uint4 *ring_slots) {   // blocks of bp .. bp+2 resident
     const uint32_t last = (bp >> 7) + kRing - 1;
@@ -1246,6 +1265,11 @@ struct DecodeLane {
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
     asm volatile("cp.async.wait_group 1;" ::: "memory");
+  }
+  __device__ __forceinline__ void load_window() {
+    const uint32_t w = bp >> 5;
+    lo = ring[w & 15];
+    hi = ring[(w + 1) & 15];
   }
   __device__ __forceinline__ uint32_t window() const {
     const uint32_t w = bp >> 5;
@@ -1259,17 +1283,26 @@ struct DecodeLane {
   }
   template <bool kFast>
   __device__ __forceinline__ uint32_t pair() {       // two codes -> bytes 0, 1
-    const uint32_t bits = window();
+    const uint32_t w = bp >> 5;
+    const uint32_t nxt = ring[(w + 2) & 15];
+    const uint32_t bits = __funnelshift_r(lo, hi, bp);
     const uint32_t t0 = lookup<kFast>(bits);
     const uint32_t t1 = lookup<kFast>(bits >> (t0 & 15));
     bp += (t0 & 15) + (t1 & 15);
     bad |= t0 | t1;
+    const bool adv = (bp >> 5) != w;
+    lo = adv ? hi : lo;
+    hi = adv ? nxt : hi;
     return __byte_perm(t0, t1, 0x0051);
   }
   template <bool kFast>
   __device__ __forceinline__ void run(uint8_t *o, uint32_t s0, uint32_t s1, bool vec_out, uint4 *ring_slots) {
     uint32_t i = s0;
     // 16 codes -> one 16-byte store (segments are 16-byte aligned)
+    if (vec_out && i + 16 <= s1) {
+      advance(ring_slots);
+      load_window();
+    }
     for (; vec_out && i + 16 <= s1; i += 16) {
       uint32_t w[4];
       if (kFast) advance(ring_slots);
@@ -1507,6 +1540,134 @@ __global__ void __launch_bounds__(kInfThreads) inflate_fast_kernel(InflateJobs J
     inflate_chunk(S, J.sec[job], J.sec_len[job], J.n_out[job], J.nch[job], c, J.out[job], err);
     __syncthreads();
   }
+}
+
+// ---- fused inverse front end: inflate -> unpack -> dequantise, one launch.
+// Work items: the chunks of both sections (inflate, as inflate_fast_kernel), then
+// per stream, tile and 32-chunk block the four 32-row blocks of D^ (dequant_block,
+// 2 warps).  A
+// block of D^ needs every chunk overlapping its 128-token tile; each inflated
+// chunk bumps its tiles' arrival counters (release), and a CTA that finishes a
+// chunk takes the next dequant block as soon as its tile is complete (acquire),
+// so the payload is dequantised while still in L2 and the dequantisation fills
+// the SM slots the latency-bound inflater leaves idle.  Deadlock-free: a CTA only
+// waits for a tile once every chunk item has been handed out (to running CTAs,
+// which never wait); before that, a CTA whose claimed block is not ready yet
+// inflates chunks meanwhile.
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t tile_chunks(const InflateDqStream &s, uint32_t cb_shift, uint32_t t) {
+  const uint64_t b0 = uint64_t(t) * uint64_t(s.dq.tile_bytes);
+  const uint64_t b1 = umin64(s.n_out, b0 + uint64_t(s.dq.tile_bytes));
+  return uint32_t(((b1 - 1) >> cb_shift) - (b0 >> cb_shift) + 1);
+}
+// dequant item q of the launch = (stream, tile, 32-chunk block): its 4 row blocks
+__device__ __forceinline__ bool dq_item_ready(const InflateDqArgs &A, uint32_t q) {
+  const int sv = q < A.s[0].ndq ? 0 : 1;
+  const InflateDqStream &s = A.s[sv];
+  const uint32_t t = (sv ? q - A.s[0].ndq : q) / s.nbx;
+  return ld_acquire_u32(s.tile_done + t) >= tile_chunks(s, A.cb_shift, t);
+}
+
+__global__ void __launch_bounds__(kInfThreads) inflate_dequant_kernel(InflateDqArgs A) {
+  __shared__ FastShared S;
+  __shared__ int s_kind;
+  __shared__ uint32_t s_arg;
+  const uint32_t nch = A.s[0].nch + A.s[1].nch, ndq = A.s[0].ndq + A.s[1].ndq;
+  int64_t pending = -1;                                  // thread 0: a claimed, not yet ready block
+  for (;;) {
+    if (threadIdx.x == 0) {
+      int kind = 0;
+      uint32_t arg = 0;
+      for (;;) {
+        if (pending >= 0) {
+          if (dq_item_ready(A, uint32_t(pending))) {
+            kind = 2;
+            arg = uint32_t(pending);
+            pending = -1;
+            break;
+          }
+          const uint32_t c = atomicAdd(&A.ctr[0], 1u);
+          if (c < nch) {
+            kind = 1;
+            arg = c;
+            break;
+          }
+          __nanosleep(200);
+          continue;
+        }
+        const uint32_t qp = *reinterpret_cast<volatile uint32_t *>(&A.ctr[1]);
+        if (qp < ndq && dq_item_ready(A, qp)) {
+          const uint32_t q = atomicAdd(&A.ctr[1], 1u);
+          if (q < ndq) {
+            pending = q;
+            continue;
+          }
+        }
+        const uint32_t c = atomicAdd(&A.ctr[0], 1u);
+        if (c < nch) {
+          kind = 1;
+          arg = c;
+          break;
+        }
+        const uint32_t q = atomicAdd(&A.ctr[1], 1u);
+        if (q < ndq) {
+          pending = q;
+          continue;
+        }
+        break;                                           // nothing left
+      }
+      s_kind = kind;
+      s_arg = arg;
+    }
+    __syncthreads();
+    const int kind = s_kind;
+    const uint32_t arg = s_arg;
+    if (kind == 0) break;
+    if (kind == 1) {
+      const int sv = arg < A.s[0].nch ? 0 : 1;
+      const InflateDqStream &s = A.s[sv];
+      const uint32_t c = sv ? arg - A.s[0].nch : arg;
+      inflate_chunk(S, s.sec, s.sec_len, s.n_out, s.nch, c, s.out, A.err);
+      __syncthreads();
+      if (threadIdx.x == 0 && s.ndq) {                   // publish the chunk to its tiles
+        __threadfence();
+        const uint64_t b0 = uint64_t(c) << A.cb_shift, b1 = umin64(s.n_out, b0 + (uint64_t(1) << A.cb_shift));
+        const uint64_t tb = uint64_t(s.dq.tile_bytes);
+        for (uint64_t t = b0 / tb; t <= (b1 - 1) / tb; ++t) atomicAdd(s.tile_done + t, 1u);
+      }
+    } else {
+      const int sv = arg < A.s[0].ndq ? 0 : 1;
+      const InflateDqStream &s = A.s[sv];
+      const uint32_t q = sv ? arg - A.s[0].ndq : arg;
+      const uint32_t t = q / s.nbx, bx = q - t * s.nbx;
+      const int64_t nby = (s.dq.m + 31) / 32;
+      for (int64_t by = int64_t(t) * (kTileM / 32); by < nby && by < int64_t(t + 1) * (kTileM / 32); ++by)
+        dequant_block<kInfThreads / 32>(s.dq, by, bx, threadIdx.x & 31, threadIdx.x >> 5);
+    }
+    __syncthreads();
+  }
+}
+
+kvtc_status launch_inflate_dequant(const InflateDqArgs &a, cudaStream_t st) {
+  const uint32_t items = a.s[0].nch + a.s[1].nch + a.s[0].ndq + a.s[1].ndq;
+  if (!items) return KVTC_OK;
+  static int max_grid = 0;
+  if (!max_grid) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    KVTC_MAX_CARVEOUT(inflate_dequant_kernel);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, inflate_dequant_kernel, kInfThreads, 0);
+    max_grid = std::max(1, sms * std::max(per, 1));
+  }
+  const uint32_t grid = std::min<uint32_t>(items, uint32_t(max_grid));
+  inflate_dequant_kernel<<<grid, kInfThreads, 0, st>>>(a);
+  KVTC_LAUNCH_CHECK();
+  return KVTC_OK;
 }
 
 // Batched codec: any number of sections; jobs[j].chunk0 = first global chunk of

@@ -108,4 +108,78 @@ static __device__ __noinline__ uint4 dq_generic8(const DqCol *cols, int col0, co
   return make_uint4(uint32_t(h[0]) | (uint32_t(h[1]) << 16), uint32_t(h[2]) | (uint32_t(h[3]) << 16),
                     uint32_t(h[4]) | (uint32_t(h[5]) << 16), uint32_t(h[6]) | (uint32_t(h[7]) << 16));
 }
+
+// One block of D^: rows [32 by, 32 by + 32) x chunks [32 bx, 32 bx + 32), by
+// kWarps warps (lane, wy).  Chunks that are 8 aligned elements of one group of a
+// full tile (DqChunk ok = 1): lane = chunk, a warp writes 512 contiguous bytes of
+// a row, 4 rows' loads issued before any is consumed; each reads its token's fp16
+// factors (4 B) and 8 codes (2 / 4 / 8 B, aligned) and converts with dq8.  Every
+// other chunk (size-1 runs, misaligned starts, the partial last tile) goes one
+// warp per chunk with lane = row, so the per-(group, token) factor and code loads
+// of a warp are consecutive in the payload (token-major group blocks).  Columns
+// past r_nz in the last chunk are written as 0 (the GEMM's tensor map never reads
+// them).  Plain loads: the fused kernel reads payload bytes written in the same
+// launch (after a gpu-scope acquire), which the non-coherent path may not see.
+template <int kWarps>
+__device__ __forceinline__ void dequant_block(const DqArgs &a, int64_t by, int64_t bx, int lane, int wy) {
+  constexpr int kRows = 32 / kWarps;                 // rows per thread, in batches of 4
+  const int64_t t = (by * 32) / kTileM;              // tile (32 | 128)
+  const int ntok = int(a.m - t * kTileM < kTileM ? a.m - t * kTileM : kTileM);
+  const bool full = ntok == kTileM;
+  const int rbase = int(by * 32 - t * kTileM);        // first row of the block inside the tile
+  const uint8_t *tile = a.payload + t * a.tile_bytes;
+  __half *drow = a.Dh + (t * kTileM + rbase) * a.ld;
+  const int k = int(bx) * 32 + lane;
+  const DqChunk d = k < a.nch8 ? a.chunks[k] : DqChunk{0, 0, 0, 0, 0, -1};
+  const bool dense = full && k < a.nch8 && d.ok == 1;
+  if (dense) {
+    const int b = bits_of(d.type);
+#pragma unroll
+    for (int r0 = 0; r0 < kRows; r0 += 4) {
+      uint32_t pr[4], lo[4], hi[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int row = rbase + wy + kWarps * (r0 + r);
+        pr[r] = *reinterpret_cast<const uint32_t *>(tile + d.par_base + 4 * row);
+        load_codes8(tile + d.code_base + row * int32_t(d.stride), b, lo[r], hi[r]);
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        *reinterpret_cast<uint4 *>(drow + (wy + kWarps * (r0 + r)) * a.ld + 8 * int64_t(k)) =
+            dq8(d.type, lo[r], hi[r], pr[r]);
+    }
+  }
+  uint32_t other = __ballot_sync(0xFFFFFFFFu, k < a.nch8 && !dense);
+  const int64_t *coff = full ? a.codes_off_full : a.codes_off_last;
+  const int row = rbase + lane;
+  for (int j = 0; other; ++j, other >>= 1) {
+    if (!(other & 1u) || (j % kWarps) != wy) continue;
+    const int kk = int(bx) * 32 + j;
+    const DqChunk e = a.chunks[kk];
+    if (row >= ntok) continue;
+    uint4 v;
+    if (full && e.run_code >= 0) {
+      // 8 size-1 groups of one type: factors 512 B apart, code blocks run_stride apart
+      const int b = bits_of(e.type);
+      uint32_t pr[8], cd[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        pr[q] = *reinterpret_cast<const uint32_t *>(tile + e.par_base + q * 4 * kTileM + 4 * row);
+        const int bit = row * b;
+        cd[q] = (uint32_t(tile[e.run_code + q * int32_t(e.stride) + (bit >> 3)]) >> (bit & 7)) & ((1u << b) - 1);
+      }
+      uint32_t hv[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t x =
+            e.type == KVTC_T_FP8 ? e4m3x2_to_f16x2(cd[q]) : uint32_t(__half_as_ushort(__uint2half_rn(cd[q])));
+        hv[q] = hfma2_u(x, pr[q] >> 16, pr[q] & 0xFFFFu) & 0xFFFFu;
+      }
+      v = make_uint4(hv[0] | (hv[1] << 16), hv[2] | (hv[3] << 16), hv[4] | (hv[5] << 16), hv[6] | (hv[7] << 16));
+    } else {
+      v = dq_generic8(a.cols, 8 * kk, tile, coff, ntok, row);
+    }
+    *reinterpret_cast<uint4 *>(drow + lane * a.ld + 8 * int64_t(kk)) = v;
+  }
+}
 }  // namespace kvtc

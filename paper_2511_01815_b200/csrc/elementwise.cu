@@ -354,54 +354,21 @@ kvtc_status launch_quant_pack_simt(const SegDesc *segs, const GroupDesc *groups,
 }
 
 // ---------------------------------------------------------------- dequant
-// D2 (R5): D^ [m][ld] fp16 from the payload.  Thread (chunk k, row) writes the
-// 16-byte chunk D^[row][8k, 8k+8): a warp covers 32 consecutive chunks of one row
-// (512 contiguous bytes), a block 32 chunks x 32 rows (4 rows per thread, loads
-// issued before any is consumed).  Chunks that are 8 aligned elements of one
-// group (DqChunk ok = 1) read their token's fp16 factors (4 B) and 8 codes (2 /
-// 4 / 8 B, aligned in a full tile) and convert with dq8 (the 1024 + c bit trick,
-// fma.rn.f16x2: one rounding of the exact x^); every other chunk (size-1 groups,
-// misaligned starts, the partial last tile) goes element by element (dq1).
-// Columns past r_nz in the last chunk are written as 0 (the GEMM's tensor map
-// never reads them).  Grid-stride over blocks (bounded grid beside a GEMM).
-constexpr int kDqRowsPerThread = 4;
-
+// D2 (R5): D^ [m][ld] fp16 from the payload, 32 rows x 32 8-column chunks per
+// block of 8 warps (dequant_block, dequant.cuh: dq8's 1024 + c bit trick and
+// fma.rn.f16x2 round the exact x^ once).  Grid-stride over blocks (bounded grid
+// beside a GEMM).  The decompression path itself runs the same blocks inside the
+// inflater (inflate_dequant_kernel, deflate.cu); this kernel serves the stage
+// API, layer-streamed and batched decompression.
 __global__ void __launch_bounds__(256) dequant_rows_kernel(const DqChunk *chunks, const DqCol *cols, int32_t nch8,
                                                            const int64_t *codes_off_full,
                                                            const int64_t *codes_off_last, int64_t tile_bytes,
                                                            const uint8_t *payload, int64_t m, __half *Dh, int64_t ld) {
   const int64_t nbx = (nch8 + 31) / 32, nby = (m + 31) / 32;
+  const DqArgs a{chunks, cols, nch8, codes_off_full, codes_off_last, tile_bytes, payload, m, Dh, ld};
   for (int64_t blk = blockIdx.x; blk < nbx * nby; blk += gridDim.x) {
-    const int64_t by = blk / nbx, bx = blk - by * nbx;
-    const int k = int(bx) * 32 + threadIdx.x;
-    if (k >= nch8) continue;
-    const int64_t t = (by * 32) / kTileM;                        // tile (32 | 128)
-    const int ntok = int(m - t * kTileM < kTileM ? m - t * kTileM : kTileM);
-    const int row0 = int(by * 32 - t * kTileM) + threadIdx.y;
-    const uint8_t *tile = payload + t * tile_bytes;
-    const DqChunk d = chunks[k];
-    __half *dst = Dh + (t * kTileM + row0) * ld + 8 * int64_t(k);
-    if (ntok == kTileM && d.ok == 1) {
-      const int b = bits_of(d.type);
-      uint32_t pr[kDqRowsPerThread], lo[kDqRowsPerThread], hi[kDqRowsPerThread];
-#pragma unroll
-      for (int r = 0; r < kDqRowsPerThread; ++r) {
-        const int row = row0 + 8 * r;
-        pr[r] = __ldg(reinterpret_cast<const unsigned int *>(tile + d.par_base + 4 * row));
-        load_codes8(tile + d.code_base + row * int32_t(d.stride), b, lo[r], hi[r]);
-      }
-#pragma unroll
-      for (int r = 0; r < kDqRowsPerThread; ++r)
-        *reinterpret_cast<uint4 *>(dst + 8 * r * ld) = dq8(d.type, lo[r], hi[r], pr[r]);
-    } else {
-      const int64_t *coff = ntok == kTileM ? codes_off_full : codes_off_last;
-      for (int r = 0; r < kDqRowsPerThread; ++r) {
-        const int row = row0 + 8 * r;
-        if (row >= ntok) break;
-        *reinterpret_cast<uint4 *>(dst + 8 * r * ld) =
-            d.type ? dq_generic8(cols, 8 * k, tile, coff, ntok, row) : make_uint4(0u, 0u, 0u, 0u);
-      }
-    }
+    const int64_t by = blk / nbx;
+    dequant_block<8>(a, by, blk - by * nbx, threadIdx.x, threadIdx.y);
   }
 }
 

@@ -64,17 +64,20 @@ struct DqCol {
   int32_t pad;
 };
 
-// One 16-byte A chunk (8 columns) of the fused producer, per pipeline position
-// (shared-memory table): ok = 1 when the 8 columns are elements j .. j+7
-// (j % 8 == 0) of one group (byte offsets of a FULL tile); ok = 3 for the other
-// chunks with columns (code_base = 16 * its index in the tail buffer).
+// One 16-byte chunk (8 columns) of D^ (dequantiser, and per pipeline position
+// the fused producer's shared-memory table): ok = 1 when the 8 columns are
+// elements j .. j+7 (j % 8 == 0) of one group (byte offsets of a FULL tile); ok = 3
+// for the other chunks with columns (code_base = 16 * its index in the fused
+// producer's tail buffer).  run_code >= 0 marks an ok = 3 chunk whose columns are
+// 8 consecutive size-1 groups of one type (the DP's per-PC groups): group q's
+// code block starts at run_code + q * run_stride, its factors at par_base + q * 512.
 struct DqChunk {
   int32_t code_base;  // group code block + j * bits / 8
   int32_t par_base;   // 4 * gidx * 128 (params of token 0)
-  uint16_t stride;    // code bytes per token (size * bits / 8)
+  uint16_t stride;    // ok = 1: code bytes per token (size * bits / 8); runs: run_stride (16 * bits)
   uint8_t type;       // kvtc_type of the chunk's group (0: padding)
   uint8_t ok;
-  uint32_t pad;
+  int32_t run_code;   // -1, or the first code block of a size-1 run (FULL tile)
 };
 constexpr int kDqTabMaxBytes = 32 * 1024;   // shared-memory budget of the chunk table (16384 columns)
 
@@ -210,6 +213,39 @@ kvtc_status launch_quant_pack_simt(const SegDesc *segs, const GroupDesc *groups,
                                    const int64_t *codes_off_last, uint8_t *payload, cudaStream_t st);
 kvtc_status launch_codes_off_last(const int32_t *gsize, const int32_t *gbits, int32_t G, int32_t ntok,
                                   int64_t *out, cudaStream_t st);
+// D2 operands of one stream (dequant_rows_kernel, inflate_dequant_kernel).
+struct DqArgs {
+  const DqChunk *chunks;
+  const DqCol *cols;
+  int32_t nch8;                         // 8-column chunks of D^ (ceil(r_nz / 8))
+  const int64_t *codes_off_full, *codes_off_last;
+  int64_t tile_bytes;
+  const uint8_t *payload;
+  int64_t m;
+  __half *Dh;
+  int64_t ld;
+};
+
+// Fused inverse front end (inflate_dequant_kernel, deflate.cu): one launch
+// inflates the chunks of both sections and dequantises each 32-row block of D^
+// as soon as every chunk of its tile is inflated (per-tile arrival counters).
+struct InflateDqStream {
+  const uint8_t *sec;
+  uint64_t sec_len, n_out;
+  uint32_t nch;
+  uint8_t *out;                          // the inflated payload
+  DqArgs dq;                             // dq.payload == out
+  uint32_t ndq, nbx;                     // dequant items (tiles x nbx; 0: inflate only), 32-chunk blocks
+  uint32_t *tile_done;                   // [ceil(m / 128)] inflated chunks per tile (zeroed)
+};
+struct InflateDqArgs {
+  InflateDqStream s[2];
+  uint32_t cb_shift;                     // log2 of the chunk bytes (16 / 32 / 64 KiB)
+  uint32_t *ctr;                         // [0] next chunk item, [1] next dequant item (zeroed)
+  int32_t *err;
+};
+kvtc_status launch_inflate_dequant(const InflateDqArgs &a, cudaStream_t st);
+
 // D2: D^ [m x ld] fp16 (ld % 8 == 0, >= r_nz rounded up to 8; 16-byte aligned)
 // from m tokens of payload, with the plan's chunk / column tables (api.cu).
 kvtc_status launch_dequant(const DqChunk *chunks, const DqCol *cols, int32_t r_nz, const int64_t *codes_off_full,

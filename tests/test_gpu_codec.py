@@ -341,3 +341,28 @@ def test_rans_container_roundtrip(K, name, tokens):
         with pytest.raises(L.KvtcError) as e:
             K.decompress(KB, KP, VB, VP, bad, K.KVView(ok, pos0=3), K.KVView(ov, pos0=3))
         assert e.value.status == -3
+
+
+@pytest.mark.parametrize("name,tokens", [("toy", 512), ("toy", 389), ("mid", 1000)])
+def test_inflate_dequant_front_end_equals_split_path(K, name, tokens, monkeypatch):
+    """KVTC_D_INFLATE_DQ=1 inflates and dequantises both streams in one launch
+    (inflate_dequant_kernel, the measured alternative); the default runs the
+    inflater and the dequantiser separately.  Both restore the cache bit for bit,
+    also through the layer-streamed calls (kvtc_decompress_begin / _layers)."""
+    spec, invf, kb, vb, KB, VB, KP, VP, okp, ovp = _setup(K, name)
+    Kc, Vc = E.caches(name, tokens, 0, conversation=9)
+    kd, vd = Kc.cuda(), Vc.cuda()
+    cont, _ = K.compress(KB, KP, VB, VP, K.KVView(kd), K.KVView(vd))
+    outs = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("KVTC_D_INFLATE_DQ", flag)
+        ko, vo = torch.zeros_like(kd), torch.zeros_like(vd)
+        K.decompress(KB, KP, VB, VP, cont, K.KVView(ko), K.KVView(vo))
+        lo, lv = torch.zeros_like(kd), torch.zeros_like(vd)
+        ls = K.StreamedDecompress(KB, KP, VB, VP, cont)      # runs kvtc_decompress_begin
+        ls.layers(K.KVView(lo), K.KVView(lv), 0, spec.layers)
+        torch.cuda.synchronize()
+        outs[flag] = (ko, vo, lo, lv)
+    for a, b in zip(outs["1"], outs["0"]):
+        assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+    assert torch.equal(outs["1"][0].view(torch.int16), outs["1"][2].view(torch.int16))
