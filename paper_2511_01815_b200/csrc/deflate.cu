@@ -737,8 +737,7 @@ __device__ __forceinline__ void encode_chunk(EncShared &S, const int c, const ui
   if (t % pieces_per_seg == 0) S.segst[t / pieces_per_seg] = myoff + (t == 0 ? S.hdr_bits : 0);
   __syncthreads();
   if (t < kNSeg) index[uint64_t(c) * kNSeg + t] = uint16_t((t + 1 < kNSeg ? S.segst[t + 1] : S.total_bits) - S.segst[t]);
-  // ---- emission: words wholly inside this thread's bit range are stored,
-  // the two edge words (shared with the neighbours) are OR-ed atomically
+  // ---- emission (the words a thread shares with its neighbours start zeroed)
   uint32_t *ow = reinterpret_cast<uint32_t *>(out);
   const uint32_t w_first = myoff >> 5, w_last = (myoff + mybits - 1) >> 5;
   if (mybits) {
@@ -746,66 +745,54 @@ __device__ __forceinline__ void encode_chunk(EncShared &S, const int c, const ui
     ow[w_last] = 0;
   }
   __syncthreads();
+  // Every completed word is stored plainly, the first one of a thread included
+  // (its low bits, the previous thread's tail, are still zero there); after a
+  // barrier each thread ORs its final partial word -- the only word a thread
+  // shares with the next one -- atomically.  No branch per flush.
+  uint64_t acc = 0;
+  uint32_t nb = myoff & 31;
+  uint32_t *wp = ow + w_first;
   if (mybits) {
-    uint64_t acc = 0;
-    uint32_t nb = myoff & 31;
-    uint32_t w = w_first;
-    bool edge = nb != 0;                                 // first word shared with the previous thread
     if (t == 0) {
       // the block header: whole words copied, the partial last word seeds the accumulator
       const uint32_t hw = S.hdr_bits >> 5;
       for (uint32_t i = 0; i < hw; ++i) ow[i] = S.hdr[i];
-      w = hw;
+      wp = ow + hw;
       nb = S.hdr_bits & 31;
       acc = nb ? (S.hdr[hw] & ((1u << nb) - 1)) : 0;
-      edge = false;
     }
+    auto flush = [&]() {
+      *wp++ = uint32_t(acc);
+      acc >>= 32;
+      nb -= 32;
+    };
     auto put = [&](uint32_t e) {
       acc |= uint64_t(e & 0xFFFF) << nb;
       nb += e >> 16;
-      if (nb >= 32) {
-        const uint32_t word = uint32_t(acc);
-        if (edge || w == w_last) atomicOr(&ow[w], word);
-        else ow[w] = word;
-        edge = false;
-        acc >>= 32;
-        nb -= 32;
-        ++w;
-      }
+      if (nb >= 32) flush();
     };
     // two codes (<= 15 bits each) per accumulator step: nb < 32 before, < 62 after
     auto put2 = [&](uint32_t e0, uint32_t e1) {
       const uint32_t l0 = e0 >> 16;
       acc |= uint64_t((e0 & 0xFFFF) | ((e1 & 0xFFFF) << l0)) << nb;
       nb += l0 + (e1 >> 16);
-      if (nb >= 32) {
-        const uint32_t word = uint32_t(acc);
-        if (edge || w == w_last) atomicOr(&ow[w], word);
-        else ow[w] = word;
-        edge = false;
-        acc >>= 32;
-        nb -= 32;
-        ++w;
-      }
+      if (nb >= 32) flush();
     };
     if (vec) {
-      const uint4 *v = reinterpret_cast<const uint4 *>(src + p0);
-      const uint32_t nv = (p1 - p0) / 16;
-      uint4 q = nv ? __ldg(v) : make_uint4(0u, 0u, 0u, 0u);
-      for (uint32_t j = 0; j < nv; ++j) {
-        const uint4 qn = __ldg(v + (j + 1 < nv ? j + 1 : j));
+      for (uint32_t i = p0; i < p1; i += 16) {
+        const uint4 q = __ldg(reinterpret_cast<const uint4 *>(src + i));
         const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
         for (int k = 0; k < 16; k += 2)
           put2(S.sym[__byte_perm(w4[k >> 2], 0, 0x4440 | (k & 3))], S.sym[__byte_perm(w4[k >> 2], 0, 0x4440 | ((k + 1) & 3))]);
-        q = qn;
       }
     } else {
       for (uint32_t i = p0; i < p1; ++i) put(S.sym[src[i]]);
     }
     if (p1 == nc) put(uint32_t(S.rev[256]) | (uint32_t(S.len[256]) << 16));
-    if (nb) atomicOr(&ow[w], uint32_t(acc));
   }
+  __syncthreads();
+  if (mybits && nb) atomicOr(wp, uint32_t(acc));
   if (t == 0) {
     chunk_bytes[c] = (S.total_bits + 7) / 8;
     chunk_kind[c] = 0;
@@ -1136,19 +1123,20 @@ static_assert(kNSeg == 64, "the segment-start scan below assumes two warps");
 
 constexpr int kRing = 4;           // per-lane ring of 16-byte stream blocks (cp.async read-ahead)
 struct FastShared {
-  union {
-    uint32_t hdr[kHdrWords + 2];   // header words (header parse), then
-    uint4 ring[kNSeg][kRing];      // per-lane read-ahead blocks (segment decode), lane-contiguous
+  union {                          // three phases of a chunk:
+    uint32_t hdr[kHdrWords + 2];   //   header words (header parse by thread 0),
+    struct {                       //   canonical codes + subtable prefixes (table build),
+      uint16_t code[260];
+      uint32_t premask[(1 << kTabBits) / 32], prebase[(1 << kTabBits) / 32];
+    } tb;
+    uint4 ring[kNSeg][kRing];      //   per-lane read-ahead blocks (segment decode), lane-contiguous
   };
   // entries: literal (sym << 8) | len; end-of-block kTeEob | len; no code kTeBad;
   // longer code (k << 8) | kTeLink: subtable k (first level only)
   uint16_t table[1 << kTabBits];
   uint16_t sub[kSubTabs << kSubBits];  // second level: the next kSubBits bits
-  uint16_t code[260];
   int cnt[16], next[16];
   uint32_t wsum[2][4];
-  uint32_t premask[(1 << kTabBits) / 32], prebase[(1 << kTabBits) / 32];
-  Huff h;
   uint8_t lens[320];
   uint8_t cltab[128];              // code-length code: (sym << 3) | len, 7-bit lookup
   uint32_t segstart[kNSeg];
@@ -1380,7 +1368,7 @@ __device__ __forceinline__ void inflate_chunk(FastShared &S, const uint8_t *sect
   // rank within each length, first-level table, subtables for codes > 11 bits
   // indexed by the rank of their first-level prefix
   if (tid < 16) S.cnt[tid] = 0;
-  if (tid < (1 << kTabBits) / 32) S.premask[tid] = 0;
+  if (tid < (1 << kTabBits) / 32) S.tb.premask[tid] = 0;
   __syncthreads();
   uint8_t l5[5];
 #pragma unroll
@@ -1435,13 +1423,13 @@ __device__ __forceinline__ void inflate_chunk(FastShared &S, const uint8_t *sect
       const int l = l5[k];
       if (sym >= 257) break;
       if (!l) {
-        S.code[sym] = 0;
+        S.tb.code[sym] = 0;
         continue;
       }
       int r = int((ex[l >> 2] >> (8 * (l & 3))) & 0xFF);
       if (w) r += int((S.wsum[0][l >> 2] >> (8 * (l & 3))) & 0xFF);
       for (int q = 0; q < k; ++q) r += l5[q] == l;
-      S.code[sym] = uint16_t(__brev(uint32_t(S.next[l] + r)) >> (32 - l));
+      S.tb.code[sym] = uint16_t(__brev(uint32_t(S.next[l] + r)) >> (32 - l));
     }
   }
   __syncthreads();
@@ -1452,32 +1440,32 @@ __device__ __forceinline__ void inflate_chunk(FastShared &S, const uint8_t *sect
     if (l == 0) continue;
     const uint16_t ent = uint16_t(sym < 256 ? (sym << 8) | l : kTeEob | l);
     if (l <= kTabBits) {
-      for (uint32_t f = S.code[sym]; f < (1u << kTabBits); f += (1u << l)) S.table[f] = ent;
+      for (uint32_t f = S.tb.code[sym]; f < (1u << kTabBits); f += (1u << l)) S.table[f] = ent;
     } else {
-      const uint32_t pre = S.code[sym] & ((1u << kTabBits) - 1);
-      atomicOr(&S.premask[pre >> 5], 1u << (pre & 31));
+      const uint32_t pre = S.tb.code[sym] & ((1u << kTabBits) - 1);
+      atomicOr(&S.tb.premask[pre >> 5], 1u << (pre & 31));
     }
   }
   __syncthreads();
   {
     // subtable index of a prefix = its rank among the marked prefixes
     if (tid < 32) {
-      const uint32_t a = __popc(S.premask[2 * tid]), b = __popc(S.premask[2 * tid + 1]);
+      const uint32_t a = __popc(S.tb.premask[2 * tid]), b = __popc(S.tb.premask[2 * tid + 1]);
       uint32_t v = a + b;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
         const uint32_t y = __shfl_up_sync(0xffffffffu, v, d);
         if (tid >= d) v += y;
       }
-      S.prebase[2 * tid] = v - a - b;
-      S.prebase[2 * tid + 1] = v - b;
+      S.tb.prebase[2 * tid] = v - a - b;
+      S.tb.prebase[2 * tid + 1] = v - b;
     }
     __syncthreads();
     for (int sym = tid; sym < 257; sym += kInfThreads) {
       const int l = S.lens[sym];
       if (l <= kTabBits) continue;
-      const uint32_t pre = S.code[sym] & ((1u << kTabBits) - 1);
-      const uint32_t k = S.prebase[pre >> 5] + __popc(S.premask[pre >> 5] & ((1u << (pre & 31)) - 1));
+      const uint32_t pre = S.tb.code[sym] & ((1u << kTabBits) - 1);
+      const uint32_t k = S.tb.prebase[pre >> 5] + __popc(S.tb.premask[pre >> 5] & ((1u << (pre & 31)) - 1));
       if (k >= uint32_t(kSubTabs)) {
         S.status = -8;
         atomicExch(err, -8);
@@ -1486,7 +1474,7 @@ __device__ __forceinline__ void inflate_chunk(FastShared &S, const uint8_t *sect
       S.table[pre] = uint16_t((k << 8) | kTeLink);
       uint16_t *st = S.sub + (k << kSubBits);
       const uint16_t ent = uint16_t(sym < 256 ? (sym << 8) | l : kTeEob | l);
-      for (uint32_t f = S.code[sym] >> kTabBits; f < (1u << kSubBits); f += (1u << (l - kTabBits))) st[f] = ent;
+      for (uint32_t f = S.tb.code[sym] >> kTabBits; f < (1u << kSubBits); f += (1u << (l - kTabBits))) st[f] = ent;
     }
   }
   // segment start = header bits + exclusive prefix of the segment lengths
@@ -1531,7 +1519,7 @@ __device__ __forceinline__ void inflate_chunk(FastShared &S, const uint8_t *sect
 
 // Grid-stride over the chunks of both jobs (full grid alone; bounded grid
 // beside a persistent GEMM, see deflate_encode_kernel).
-__global__ void __launch_bounds__(kInfThreads) inflate_fast_kernel(InflateJobs J, int32_t *err) {
+__global__ void __launch_bounds__(kInfThreads, 16) inflate_fast_kernel(InflateJobs J, int32_t *err) {
   __shared__ FastShared S;
   const uint32_t total = J.nch[0] + J.nch[1];
   for (uint32_t b = blockIdx.x; b < total; b += gridDim.x) {
@@ -1572,7 +1560,7 @@ __device__ __forceinline__ bool dq_item_ready(const InflateDqArgs &A, uint32_t q
   return ld_acquire_u32(s.tile_done + t) >= tile_chunks(s, A.cb_shift, t);
 }
 
-__global__ void __launch_bounds__(kInfThreads) inflate_dequant_kernel(InflateDqArgs A) {
+__global__ void __launch_bounds__(kInfThreads, 16) inflate_dequant_kernel(InflateDqArgs A) {
   __shared__ FastShared S;
   __shared__ int s_kind;
   __shared__ uint32_t s_arg;
@@ -1672,7 +1660,7 @@ kvtc_status launch_inflate_dequant(const InflateDqArgs &a, cudaStream_t st) {
 
 // Batched codec: any number of sections; jobs[j].chunk0 = first global chunk of
 // job j (ascending), a binary search maps a chunk to its job.
-__global__ void __launch_bounds__(kInfThreads) inflate_batch_kernel(const InflateJob *jobs, int32_t njobs,
+__global__ void __launch_bounds__(kInfThreads, 16) inflate_batch_kernel(const InflateJob *jobs, int32_t njobs,
                                                                    uint32_t total, int32_t *err) {
   __shared__ FastShared S;
   for (uint32_t b = blockIdx.x; b < total; b += gridDim.x) {
