@@ -274,6 +274,8 @@ struct EncShared {
     struct {                                          // code construction, after nz / sorted are read
       int work[kLitSyms + 3], dep[kLitSyms + 3], par[kLitSyms + 3], ndep[kLitSyms + 3];
     } mk;
+    uint32_t len4[32];   // after the header: literal code lengths, 8 nibbles per word, so the
+                         // bit-count pass's lookups hit 32 words (bank-conflict free)
   } u;
   uint32_t hist[kLitSyms + 3];
   uint32_t clhist[19];
@@ -686,6 +688,12 @@ __device__ __forceinline__ void encode_chunk(EncShared &S, const int c, const ui
   __syncthreads();
   build_header(S, t, maxbits);
   for (int i = t; i < 256; i += kEncThreads) S.sym[i] = uint32_t(S.rev[i]) | (uint32_t(S.len[i]) << 16);
+  if (t < 32) {
+    uint32_t v = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v |= uint32_t(S.len[8 * t + k]) << (4 * k);
+    S.u.len4[t] = v;
+  }
   __syncthreads();
   // ---- bit counts per piece, exclusive scan
   const bool vec = ((reinterpret_cast<uintptr_t>(src + p0) & 15) == 0) && ((p1 - p0) % 16 == 0);
@@ -699,7 +707,10 @@ __device__ __forceinline__ void encode_chunk(EncShared &S, const int c, const ui
       const uint4 qn = __ldg(v + (j + 1 < nv ? j + 1 : j));
       const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-      for (int k = 0; k < 16; ++k) mybits += S.sym[(w4[k >> 2] >> (8 * (k & 3))) & 0xFF] >> 16;
+      for (int k = 0; k < 16; ++k) {
+        const uint32_t b = (w4[k >> 2] >> (8 * (k & 3))) & 0xFF;
+        mybits += (S.u.len4[b >> 3] >> ((b & 7) * 4)) & 15u;
+      }
       q = qn;
     }
   } else if (!vec) {
