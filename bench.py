@@ -619,6 +619,10 @@ def main():
             stages[nm]["frac_of_hbm"] = gbs / hbm
             if nm.endswith("_overlapped"):
                 stages[nm]["note"] = "bounded grid beside a GEMM: the time is shared, not a kernel roofline"
+            elif nm in ("c.deflate", "d.inflate"):
+                # Huffman coding: lane-serial code emission / decode, bound by the shared-memory
+                # pipe (table lookups) and latency, not by HBM (ncu in profiles/)
+                stages[nm]["bound"] = "shared-memory pipe / latency (frac_of_hbm for context)"
     dom = max(("c.project_quant_gemm", "d.reconstruct_gemm"), key=lambda n: stages.get(n, {}).get("ms_per_step", 0))
     dom_ms = stages[dom]["ms_per_step"] / 2                  # per launch (K or V), averaged
     achieved = gemm_flops / 2 / (dom_ms * 1e-3) / 1e12

@@ -81,6 +81,33 @@ def runs_plan_groups():
     return g
 
 
+def same_type_runs_plan_groups():
+    """Explicit plan over 2048 PCs whose size-1 groups come in same-type runs (as
+    the DP's per-PC fp8 groups do in the bench plan): aligned runs of 8 that the
+    dequantiser treats as one chunk kind (fp8 x 3, int4, int2), a run that starts
+    on an unaligned column (41) and one broken by a type change, a None gap, then
+    wider groups from an aligned column (72)."""
+    g = []
+    c = 0
+    for t in (T8, T8, T8, T4, T2):                  # five aligned runs of 8
+        for _ in range(8):
+            g.append((c, 1, t)); c += 1
+    g.append((c, 1, T4)); c += 1                    # column 40: the next run starts at 41
+    for _ in range(16):
+        g.append((c, 1, T8)); c += 1
+    for i in range(8):                              # a run of 8 broken by a type change
+        g.append((c, 1, T8 if i < 5 else T4)); c += 1
+    c += 5                                          # None gap (no D^ columns)
+    for _ in range(7):                              # 72 size-1 columns: the 16-groups start aligned
+        g.append((c, 1, T2)); c += 1
+    for t in (T4, T2, T8):
+        g.append((c, 16, t)); c += 16
+    g.append((c, 256, T2)); c += 256
+    g.append((c, 1024, T4)); c += 1024
+    assert c <= 2048
+    return g
+
+
 def toy_plans(cr: float = 16):
     spec, invf, kb, vb, Ck, Cv = setup("toy")
     kp, _, _ = ODP.allocate(OPCA.dp_coefficients(kb, Ck), cr, spec.p)

@@ -75,6 +75,9 @@ def _plan_for(name):
     if name == "mid-runs":
         g = E.runs_plan_groups()
         return g, g
+    if name == "mid-typed-runs":
+        g = E.same_type_runs_plan_groups()
+        return g, g
     g = E.mid_plan_groups()
     return g, g
 
@@ -205,10 +208,10 @@ def test_gpu_inflates_zlib_streams(K):
     assert out.cpu().numpy().tobytes() == b"".join(raw * 4)
 
 
-@pytest.mark.parametrize("name,tokens", [("toy", 512), ("mid", 1000), ("mid-runs", 777)])
+@pytest.mark.parametrize("name,tokens", [("toy", 512), ("mid", 1000), ("mid-runs", 777), ("mid-typed-runs", 643)])
 def test_dequant_and_reconstruct(K, name, tokens):
     gk, gv = _plan_for(name)
-    name = "mid" if name == "mid-runs" else name
+    name = "mid" if name.startswith("mid") else name
     spec, invf, kb, vb, Ck, Cv = E.setup(name)
     Kc, Vc = E.caches(name, tokens, 50)
     m = tokens - 132
