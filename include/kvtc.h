@@ -409,7 +409,8 @@ kvtc_status kvtc_stage_dequantize(const kvtc_plan *plan, const uint8_t *payload,
 kvtc_status kvtc_stage_reconstruct(const kvtc_basis *b, const kvtc_plan *plan, const uint16_t *Dh, int64_t ld,
                                    int64_t m, int64_t tok_begin, int32_t layer_begin, int32_t layer_end,
                                    const kvtc_kv_view *out, void *stream);
-/* D2 + K5 fused (the product path of kvtc_decompress): the same
+/* D2 + K5 fused (kvtc_decompress takes this path only with
+ * KVTC_DQ_FUSED=1, it is measured 7-8x slower: DESIGN.md §11): the same
  * reconstruction with A = D^ dequantised from the payload (m tokens of 128-token
  * tiles, as kvtc_stage_project_quantize writes it) by the GEMM's producer warps,
  * never written to HBM.  Bitwise equal to kvtc_stage_dequantize followed by

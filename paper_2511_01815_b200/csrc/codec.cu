@@ -165,8 +165,9 @@ kvtc_status run_project_quant(const kvtc_basis *b, kvtc_plan *pl, const Operands
 // the GEMM's producer warps dequantise straight into the shared-memory stages
 // (D^ never reaches HBM; bitwise equal output), for plans whose A-chunk table
 // fits in shared memory.  Measured 7-8x slower on the bench shape (48 ms vs
-// 6.3 ms per launch): the tensor core's operand reads leave the
-// producers' shared-memory stores too little bandwidth, so it stays opt-in.
+// 6.3 ms per launch): A is consumed by all p / 256 column tiles,
+// so the producers dequantise every element 128 times, and their shared-memory
+// stores compete with the tensor core's operand reads; so it stays opt-in.
 bool dq_fused_env() {
   const char *e = getenv("KVTC_DQ_FUSED");
   return e && e[0] == '1';
