@@ -123,6 +123,8 @@ struct Params {
   const DqChunk *dq_chunks;        // [num_st * 16]
   int32_t dq_debug;                // KVTC_DQ_DEBUG (measurement only): 1 no payload loads, 2 no A stores,
                                    // 4 no proxy fence
+  int32_t l2_pref;                 // > 0: the producer prefetches the k-blocks this many stages ahead
+                                   // into L2 (KVTC_L2_PREF_QUANT / _RECON, A/B)
   int32_t spin;                    // KVTC_SPIN_WAITS bit mask: spin (no suspend) on 1 producer empty,
                                    // 2 MMA tmem_empty, 4 epilogue tmem_full, 8 MMA full barrier
   const uint8_t *dq_tail;          // [rows][dq_tail_ld] fp16 columns of the ok = 3 chunks (pre-pass)
@@ -645,6 +647,19 @@ __global__ void __launch_bounds__(threads_for(ASRC), MODE == EPI_RECON ? 1 : 2)
             else
               tma_load_2d_pair(ak, &tmA, &full_bar[s], kak, T.mb * kTileM);
             tma_load_2d_pair(b + kk * kBSub, &tmB, &full_bar[s], kak, n0 + int(rank) * (n_mma / 2));
+          }
+          if (P.l2_pref > 0 && ks + P.l2_pref < num_st) {
+#pragma unroll
+            for (int kk = 0; kk < KB; ++kk) {
+              const int32_t kpf = (ks + P.l2_pref) * KB * kBlockK + kk * kBlockK;
+              if (P.a_hd && P.a_layer_rows)
+                tma_prefetch_l2_2d(&tmA, kpf % P.a_hd, int((kpf / P.a_hd) * P.a_layer_rows + P.a_row0) + T.mb * kTileM);
+              else if (P.a_hd)
+                tma_prefetch_l2_3d(&tmA, kpf % P.a_hd, int(P.a_row0) + T.mb * kTileM, kpf / P.a_hd);
+              else
+                tma_prefetch_l2_2d(&tmA, kpf, T.mb * kTileM);
+              tma_prefetch_l2_2d(&tmB, kpf, n0 + int(rank) * (n_mma / 2));
+            }
           }
         } else if constexpr (PAIR) {
           // both CTAs' bytes land on the leader's barrier
@@ -1205,6 +1220,10 @@ static kvtc_status launch(const CUtensorMap *tmA, const CUtensorMap *tmB, const 
     pp.dq_debug = dd ? atoi(dd) : 0;
     const char *sw = getenv("KVTC_SPIN_WAITS");
     pp.spin = sw ? atoi(sw) : 0;
+    static const char *pref_names[4] = {"KVTC_L2_PREF_F32", "KVTC_L2_PREF_QUANT", "KVTC_L2_PREF_RECON",
+                                        "KVTC_L2_PREF_XTX"};
+    const char *pf = getenv(pref_names[MODE]);
+    pp.l2_pref = pf ? atoi(pf) : 0;
     const char *es = getenv("KVTC_EPI_SKIP");
     pp.epi_skip = es && es[0] == '1';
     const char *ts = getenv("KVTC_TILE_SYNC");
