@@ -593,9 +593,10 @@ def main():
     pay = info.payload_bytes[0] + info.payload_bytes[1]
     ent = info.entropy_bytes[0] + info.entropy_bytes[1]
     rpad = [(x + 7) // 8 * 8 for x in rnz]
-    # algorithmic bytes of each stage as the schedule runs it: the
-    # caller-stream DEFLATE handles the KEYS only (the values' runs beside the keys'
-    # GEMM as the *_overlapped stage, whose time is shared with it); one inflate
+    # algorithmic bytes of each stage as the schedule runs it: with
+    # KVTC_OVERLAP=1 the caller-stream DEFLATE handles the KEYS only (the values' runs
+    # beside the keys' GEMM as the *_overlapped stage, whose time is shared with it),
+    # by default it covers both streams (fixed up below); one inflate
     # launch covers both streams; the keys' dequantisation runs on the caller's
     # stream, the values' beside the keys' GEMM (KVTC_D_INFLATE_DQ=1: one launch
     # inflates and dequantises both, d.inflate_dequant: sections read, payload
@@ -609,8 +610,15 @@ def main():
                    "d.inflate_dequant": ent + pay + m * 2 * (rpad[0] + rpad[1]),
                    "d.dequant": info.payload_bytes[0] + m * 2 * rpad[0],
                    "d.dequant_overlapped": info.payload_bytes[1] + m * 2 * rpad[1],
+                   "d.checksum": pay + 2 * info.raw_bytes,
                    "c.gather_unrope": 2 * 2 * p * m, "c.gather_unrope_overlapped": 2 * 2 * p * m,
                    "d.checksum_overlapped": pay + 2 * info.raw_bytes}
+    # default (serial) schedule: no *_overlapped stages, so the caller-stream DEFLATE
+    # and dequantisation cover both streams
+    if "c.deflate_overlapped" not in stages:
+        stage_bytes["c.deflate"] = pay + ent
+    if "d.dequant_overlapped" not in stages:
+        stage_bytes["d.dequant"] = pay + m * 2 * (rpad[0] + rpad[1])
     for nm, b in stage_bytes.items():
         if nm in stages:
             gbs = b / (stages[nm]["ms_per_step"] * 1e-3) / 1e9

@@ -262,10 +262,17 @@ bool env_flag(const char *name, bool dflt) {
   return e ? e[0] == '1' : dflt;
 }
 
-// KVTC_NO_OVERLAP=1 runs the codec kernels on the caller's stream (measurements).
+// The integer codec kernels run on the library's side stream beside the GEMMs by
+// default; KVTC_NO_OVERLAP=1 (or KVTC_OVERLAP=0) runs every kernel on the caller's
+// stream.  Re-measured after the round-2 codec rewrites (in-process interleaved
+// sweep, profiles/r02j_sweep_overlap.log): 32.42 ms per step overlapped vs 32.55 ms
+// serial -- the co-runners cost the GEMMs ~2.1 ms, about what the codec kernels
+// take on their own, so the two schedules are within noise.
 bool overlap_off() {
   const char *e = getenv("KVTC_NO_OVERLAP");
-  return e && e[0] == '1';
+  if (e) return e[0] == '1';
+  const char *o = getenv("KVTC_OVERLAP");
+  return o && o[0] == '0';
 }
 
 // KVTC_NO_DIRECT=1 forces the gathered path (tests compare the two).

@@ -366,3 +366,24 @@ def test_inflate_dequant_front_end_equals_split_path(K, name, tokens, monkeypatc
     for a, b in zip(outs["1"], outs["0"]):
         assert torch.equal(a.view(torch.int16), b.view(torch.int16))
     assert torch.equal(outs["1"][0].view(torch.int16), outs["1"][2].view(torch.int16))
+
+
+@pytest.mark.parametrize("name,tokens", [("toy", 512), ("mid", 1000)])
+def test_overlapped_schedule_equals_serial(K, name, tokens, monkeypatch):
+    """The integer codec kernels run on the library's side stream beside the GEMMs
+    by default (KVTC_OVERLAP=1); KVTC_OVERLAP=0 runs everything on the caller's
+    stream.  Same container bytes, same restored cache, either way."""
+    spec, invf, kb, vb, KB, VB, KP, VP, okp, ovp = _setup(K, name)
+    Kc, Vc = E.caches(name, tokens, 0, conversation=11)
+    kd, vd = Kc.cuda(), Vc.cuda()
+    res = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("KVTC_OVERLAP", flag)
+        cont, _ = K.compress(KB, KP, VB, VP, K.KVView(kd), K.KVView(vd))
+        ko, vo = torch.zeros_like(kd), torch.zeros_like(vd)
+        K.decompress(KB, KP, VB, VP, cont, K.KVView(ko), K.KVView(vo))
+        torch.cuda.synchronize()
+        res[flag] = (cont.cpu(), ko, vo)
+    assert torch.equal(res["0"][0], res["1"][0])
+    assert torch.equal(res["0"][1].view(torch.int16), res["1"][1].view(torch.int16))
+    assert torch.equal(res["0"][2].view(torch.int16), res["1"][2].view(torch.int16))
