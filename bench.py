@@ -593,20 +593,24 @@ def main():
     pay = info.payload_bytes[0] + info.payload_bytes[1]
     ent = info.entropy_bytes[0] + info.entropy_bytes[1]
     rpad = [(x + 7) // 8 * 8 for x in rnz]
-    # algorithmic bytes of each stage as the schedule runs it: with
-    # KVTC_OVERLAP=1 the caller-stream DEFLATE handles the KEYS only (the values' runs
-    # beside the keys' GEMM as the *_overlapped stage, whose time is shared with it),
-    # by default it covers both streams (fixed up below); one inflate
-    # launch covers both streams; the keys' dequantisation runs on the caller's
-    # stream, the values' beside the keys' GEMM (KVTC_D_INFLATE_DQ=1: one launch
-    # inflates and dequantises both, d.inflate_dequant: sections read, payload
-    # written, D^ written; the payload re-read hits L2)
+    # algorithmic bytes of each stage as the schedule runs it.  Default
+    # (overlapped) schedule: the caller-stream DEFLATE handles the KEYS only (the
+    # values' runs beside the keys' GEMM as the *_overlapped stage, whose time is
+    # shared with it); the keys' section is inflated on the caller's stream
+    # (d.inflate_k), the values' beside the keys' GEMM; the keys' dequantisation runs
+    # on the caller's stream, the values' beside the keys' GEMM.  KVTC_OVERLAP=0:
+    # DEFLATE and dequantisation cover both streams (fixed up below);
+    # KVTC_D_INFLATE_SIDE=0: one inflate launch for both (d.inflate);
+    # KVTC_D_INFLATE_DQ=1: one launch inflates and dequantises both
+    # (d.inflate_dequant: sections read, payload written, D^ written).
     stage_bytes = {"c.rans_keys": info.payload_bytes[0] + info.entropy_bytes[0],
                    "c.rans_values_overlapped": info.payload_bytes[1] + info.entropy_bytes[1],
                    "d.rans_decode": pay + ent,
                    "c.deflate": info.payload_bytes[0] + info.entropy_bytes[0],
                    "c.deflate_overlapped": info.payload_bytes[1] + info.entropy_bytes[1],
                    "d.inflate": pay + ent,
+                   "d.inflate_k": info.payload_bytes[0] + info.entropy_bytes[0],
+                   "d.inflate_v_overlapped": info.payload_bytes[1] + info.entropy_bytes[1],
                    "d.inflate_dequant": ent + pay + m * 2 * (rpad[0] + rpad[1]),
                    "d.dequant": info.payload_bytes[0] + m * 2 * rpad[0],
                    "d.dequant_overlapped": info.payload_bytes[1] + m * 2 * rpad[1],
@@ -627,7 +631,7 @@ def main():
             stages[nm]["frac_of_hbm"] = gbs / hbm
             if nm.endswith("_overlapped"):
                 stages[nm]["note"] = "bounded grid beside a GEMM: the time is shared, not a kernel roofline"
-            elif nm in ("c.deflate", "d.inflate"):
+            elif nm in ("c.deflate", "d.inflate", "d.inflate_k"):
                 # Huffman coding: lane-serial code emission / decode, bound by the shared-memory
                 # pipe (table lookups) and latency, not by HBM (ncu in profiles/)
                 stages[nm]["bound"] = "shared-memory pipe / latency (frac_of_hbm for context)"

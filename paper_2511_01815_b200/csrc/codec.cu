@@ -1141,9 +1141,12 @@ kvtc_status decompress_enqueue(const kvtc_basis *kb, const kvtc_plan *kp, const 
   SideStream *ss = side_stream();
   const bool ovl = !overlap_off();
   cudaStream_t aux = ovl ? ss->s : st;
-  // KVTC_D_INFLATE_SIDE=1 (A/B): only the keys' section is inflated up front; the
-  // values' is inflated on the side stream (bounded grid) beside the keys' GEMM
-  const bool inflate_side = ovl && !(h.flags & kFlagRans) && env_flag("KVTC_D_INFLATE_SIDE", false);
+  // Only the keys' section is inflated up front; the values' is inflated on the side
+  // stream (bounded grid) beside the keys' GEMM.  With the round-2 inflater this is
+  // 0.2-0.4 ms per step faster than one two-stream launch up front (in-process
+  // interleaved sweeps, profiles/r02k_sweep_inflate_side.log); KVTC_D_INFLATE_SIDE=0
+  // restores the single launch.
+  const bool inflate_side = ovl && !(h.flags & kFlagRans) && env_flag("KVTC_D_INFLATE_SIDE", true);
   // KVTC_D_INFLATE_DQ=1: one launch inflates and dequantises both streams
   // (inflate_dequant_kernel; measured slower than the split path: 1.25-1.32 vs
   // 0.79 ms in the step); default: the inflater, then the
