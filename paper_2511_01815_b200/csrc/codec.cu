@@ -700,17 +700,21 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
   auto *rawk = reinterpret_cast<__nv_bfloat16 *>(o + KVTC_HEADER_BYTES);
   auto *rawv = rawk + int64_t(k->shape.layers) * L.nraw * hd;
   const int64_t t = k->tokens;
-  if (L.m) {
-    ProfScope ps_raw("c.raw_tokens", st);
+  // raw sinks + window of the middle-token case: packed (and hashed) on the side
+  // stream after the fork below, beside the values' GEMM
+  auto pack_raw = [&](cudaStream_t q) -> kvtc_status {
+    ProfScope ps_raw("c.raw_tokens", q);
+    kvtc_status r;
     for (int sv = 0; sv < 2; ++sv) {
       const kvtc_kv_view *vw = sv ? v : k;
       __nv_bfloat16 *const *bs = sv ? vbases : kbases;
       __nv_bfloat16 *dst = sv ? rawv : rawk;
-      if ((s = launch_pack_raw(*vw, bs, 0, pol->sinks, dst, L.nraw, 0, st))) return s;
-      if ((s = launch_pack_raw(*vw, bs, t - pol->window, pol->window, dst, L.nraw, pol->sinks, st))) return s;
+      if ((r = launch_pack_raw(*vw, bs, 0, pol->sinks, dst, L.nraw, 0, q))) return r;
+      if ((r = launch_pack_raw(*vw, bs, t - pol->window, pol->window, dst, L.nraw, pol->sinks, q))) return r;
     }
-    if ((s = launch_hash(rawk, L.raw_bytes, kSeedRaw, lens + 7, st))) return s;
-  } else {
+    return launch_hash(rawk, L.raw_bytes, kSeedRaw, lens + 7, q);
+  };
+  if (!L.m) {
     if ((s = launch_pack_raw(*k, kbases, 0, t, rawk, L.nraw, 0, st))) return s;
     if ((s = launch_pack_raw(*v, vbases, 0, t, rawv, L.nraw, 0, st))) return s;
     if ((s = launch_hash(rawk, L.raw_bytes, kSeedRaw, lens + 7, st))) return s;
@@ -793,7 +797,9 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
     }
     return KVTC_OK;
   };
-  KVTC_CUDA_TRY(cudaEventRecord(ss->ev[0], st));                 // fork point: bases, raw tokens
+  KVTC_CUDA_TRY(cudaEventRecord(ss->ev[0], st));                 // fork point: bases, tables uploaded
+  KVTC_CUDA_TRY(cudaStreamWaitEvent(aux, ss->ev[0], 0));
+  if ((s = pack_raw(aux))) return s;                              // joined before the assembly (ev[3])
   if (v_direct) {
     // tuning knobs (scripts/sweep_env.py): KVTC_C_GATHER_SIDE=0 runs the keys'
     // gather before the values' GEMM instead of beside it; KVTC_C_DEFLATE_SIDE=0
@@ -1207,14 +1213,20 @@ kvtc_status decompress_enqueue(const kvtc_basis *kb, const kvtc_plan *kp, const 
         ProfScope ps(ovl ? "d.checksum_overlapped" : "d.checksum", aux);
         if ((s = enqueue_checks(ib, h, w, aux, ctas))) return s;
       }
+      {
+        // raw sinks + window of both streams (token rows the GEMMs never write)
+        ProfScope ps("d.raw_tokens", aux);
+        for (int rv = 0; rv < 2; ++rv) {
+          const __nv_bfloat16 *raw = rv ? rawv : rawk;
+          const kvtc_kv_view *ow = rv ? v_out : k_out;
+          __nv_bfloat16 *const *obs = rv ? w.vbases : w.kbases;
+          if ((s = launch_unpack_raw(raw, nraw, 0, h.sinks, *ow, obs, 0, layer_begin, layer_end, aux))) return s;
+          if ((s = launch_unpack_raw(raw, nraw, h.sinks, h.window, *ow, obs, t - h.window, layer_begin, layer_end,
+                                     aux)))
+            return s;
+        }
+      }
       KVTC_CUDA_TRY(cudaEventRecord(ss->ev[3], aux));
-    }
-    const __nv_bfloat16 *raw = sv ? rawv : rawk;
-    {
-      ProfScope ps("d.raw_tokens", st);
-      if ((s = launch_unpack_raw(raw, nraw, 0, h.sinks, *vw, bs, 0, layer_begin, layer_end, st))) return s;
-      if ((s = launch_unpack_raw(raw, nraw, h.sinks, h.window, *vw, bs, t - h.window, layer_begin, layer_end, st)))
-        return s;
     }
   }
   return enqueue_status(w, status_dev, st);
