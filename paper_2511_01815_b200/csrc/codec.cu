@@ -702,8 +702,8 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
   const int64_t t = k->tokens;
   // raw sinks + window of the middle-token case: packed (and hashed) on the side
   // stream after the fork below, beside the values' GEMM
-  auto pack_raw = [&](cudaStream_t q) -> kvtc_status {
-    ProfScope ps_raw("c.raw_tokens", q);
+  auto pack_raw = [&](cudaStream_t q, bool side) -> kvtc_status {
+    ProfScope ps_raw(side ? "c.raw_tokens_overlapped" : "c.raw_tokens", q);
     kvtc_status r;
     for (int sv = 0; sv < 2; ++sv) {
       const kvtc_kv_view *vw = sv ? v : k;
@@ -799,7 +799,7 @@ extern "C" kvtc_status kvtc_compress(const kvtc_basis *kb, const kvtc_plan *kp, 
   };
   KVTC_CUDA_TRY(cudaEventRecord(ss->ev[0], st));                 // fork point: bases, tables uploaded
   KVTC_CUDA_TRY(cudaStreamWaitEvent(aux, ss->ev[0], 0));
-  if ((s = pack_raw(aux))) return s;                              // joined before the assembly (ev[3])
+  if ((s = pack_raw(aux, ovl))) return s;                         // joined before the assembly (ev[3])
   if (v_direct) {
     // tuning knobs (scripts/sweep_env.py): KVTC_C_GATHER_SIDE=0 runs the keys'
     // gather before the values' GEMM instead of beside it; KVTC_C_DEFLATE_SIDE=0
@@ -1215,7 +1215,7 @@ kvtc_status decompress_enqueue(const kvtc_basis *kb, const kvtc_plan *kp, const 
       }
       {
         // raw sinks + window of both streams (token rows the GEMMs never write)
-        ProfScope ps("d.raw_tokens", aux);
+        ProfScope ps(ovl ? "d.raw_tokens_overlapped" : "d.raw_tokens", aux);
         for (int rv = 0; rv < 2; ++rv) {
           const __nv_bfloat16 *raw = rv ? rawv : rawk;
           const kvtc_kv_view *ow = rv ? v_out : k_out;
